@@ -1,0 +1,291 @@
+// FP64 DMMA GEMM for sm_100a: C = alpha * op(A) * op(B) + beta * C, column-major.
+//
+// This is the dense-contraction workhorse of the eigensolve (potrf trailing
+// updates, trsm, sygst, sytrd syr2k, D&C merges, Householder back-transform)
+// and of the stepping setup (drive projections V^T[R_D L_D M0], C V).
+// The reference does these through numpy/OpenBLAS (pkg/src/eddymodes/modal.py:79-81,
+// transient.py:140-154) or scalar numba loops (_kernels.py:56-79).
+//
+// Tile 128x128x16, 8 warps (2x4), warp tile 64x32 = 8x4 DMMA.8x8x4 fragments,
+// 3-stage cp.async pipeline, padded shared-memory layouts chosen so every
+// 8-byte fragment load is bank-conflict free (row strides = 4 mod 16 doubles).
+#include "common.cuh"
+#include "gemm.h"
+
+namespace em {
+
+constexpr int GBM = 128, GBN = 128, GBK = 16, GSTAGES = 3, GTHREADS = 256;
+constexpr int SPAD_LONG = GBM + 4;  // 132 ≡ 4 (mod 16)
+constexpr int SPAD_K = GBK + 4;     // 20  ≡ 4 (mod 16)
+
+template <int TA>
+struct ATile {
+  static constexpr int size = TA ? GBM * SPAD_K : GBK * SPAD_LONG;
+  EM_DEVINL static int idx(int m, int k) { return TA ? m * SPAD_K + k : k * SPAD_LONG + m; }
+};
+template <int TB>
+struct BTile {
+  static constexpr int size = TB ? GBK * SPAD_LONG : GBN * SPAD_K;
+  EM_DEVINL static int idx(int k, int n) { return TB ? k * SPAD_LONG + n : n * SPAD_K + k; }
+};
+
+// Load a 128 x 16 slab of op(X) (the "long" extent is 128, the k extent 16).
+// TRANS == 0: X stored long-contiguous (X[l + k*ld]); TRANS == 1: k-contiguous (X[k + l*ld]).
+template <int TRANS, int VEC>
+EM_DEVINL void load_slab(double* s, const double* __restrict__ X, int64_t ld, int64_t l0,
+                         int64_t k0, int64_t L, int64_t K, int tid) {
+  if (!TRANS) {
+    // contiguous along l; smem [k][l] stride SPAD_LONG
+    constexpr int CH = GBM * GBK / VEC;
+#pragma unroll
+    for (int c = tid; c < CH; c += GTHREADS) {
+      int kk = c / (GBM / VEC);
+      int l = (c % (GBM / VEC)) * VEC;
+      int64_t gl = l0 + l, gk = k0 + kk;
+      double* dst = s + kk * SPAD_LONG + l;
+      if (VEC == 2) {
+        int nv = (gk < K) ? (int)imin64(imax64(L - gl, 0), 2) : 0;
+        const double* src = nv ? X + gl + gk * ld : X;
+        cp_async16(dst, src, nv * 8);
+      } else {
+        bool v = (gk < K) && (gl < L);
+        cp_async8(dst, v ? X + gl + gk * ld : X, v);
+      }
+    }
+  } else {
+    // contiguous along k; smem [l][k] stride SPAD_K
+    constexpr int CH = GBM * GBK / VEC;
+#pragma unroll
+    for (int c = tid; c < CH; c += GTHREADS) {
+      int l = c / (GBK / VEC);
+      int kk = (c % (GBK / VEC)) * VEC;
+      int64_t gl = l0 + l, gk = k0 + kk;
+      double* dst = s + l * SPAD_K + kk;
+      if (VEC == 2) {
+        int nv = (gl < L) ? (int)imin64(imax64(K - gk, 0), 2) : 0;
+        const double* src = nv ? X + gk + gl * ld : X;
+        cp_async16(dst, src, nv * 8);
+      } else {
+        bool v = (gk < K) && (gl < L);
+        cp_async8(dst, v ? X + gk + gl * ld : X, v);
+      }
+    }
+  }
+}
+
+// One CTA tile of the product. Shared by the plain and grouped kernels.
+template <int TA, int TB, int LOWER, int VEC>
+EM_DEVINL void gemm_tile(const GemmArgs& p, int64_t m0, int64_t n0, double* smem) {
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp >> 2, wn = warp & 3;  // 2 x 4 warps, 64 x 32 each
+
+  constexpr int ASZ = ATile<TA>::size, BSZ = BTile<TB>::size;
+  double* As = smem;
+  double* Bs = smem + GSTAGES * ASZ;
+
+  double acc[8][4][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int64_t nk = (p.k + GBK - 1) / GBK;
+  // prologue
+#pragma unroll
+  for (int s = 0; s < GSTAGES - 1; ++s) {
+    if (s < nk) {
+      load_slab<TA, VEC>(As + s * ASZ, p.A, p.lda, m0, s * GBK, p.m, p.k, tid);
+      load_slab<!TB, VEC>(Bs + s * BSZ, p.B, p.ldb, n0, s * GBK, p.n, p.k, tid);
+    }
+    cp_async_commit();
+  }
+
+  for (int64_t kt = 0; kt < nk; ++kt) {
+    cp_async_wait<GSTAGES - 2>();
+    __syncthreads();
+    // issue the load for kt + STAGES - 1 (its buffer was consumed at kt - 1)
+    {
+      int64_t kn = kt + GSTAGES - 1;
+      int sb = (int)(kn % GSTAGES);
+      if (kn < nk) {
+        load_slab<TA, VEC>(As + sb * ASZ, p.A, p.lda, m0, kn * GBK, p.m, p.k, tid);
+        load_slab<!TB, VEC>(Bs + sb * BSZ, p.B, p.ldb, n0, kn * GBK, p.n, p.k, tid);
+      }
+      cp_async_commit();
+    }
+    const double* as = As + (kt % GSTAGES) * ASZ;
+    const double* bs = Bs + (kt % GSTAGES) * BSZ;
+#pragma unroll
+    for (int ks = 0; ks < GBK / 4; ++ks) {
+      double af[8], bf[4];
+      const int kk = ks * 4 + t;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) af[i] = as[ATile<TA>::idx(wm * 64 + i * 8 + g, kk)];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = bs[BTile<TB>::idx(kk, wn * 32 + j * 8 + g)];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+
+  // epilogue
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t row = m0 + wm * 64 + i * 8 + g;
+    if (row >= p.m) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t col = n0 + wn * 32 + j * 8 + 2 * t + e;
+        if (col >= p.n) continue;
+        if (LOWER && row + p.diag_off < col) continue;
+        double* cp = p.C + row + col * p.ldc;
+        double v = p.alpha * acc[i][j][e];
+        if (p.beta != 0.0) v = fma(p.beta, *cp, v);
+        *cp = v;
+      }
+    }
+  }
+}
+
+template <int TA, int TB, int LOWER, int VEC>
+__global__ void __launch_bounds__(GTHREADS, 1) gemm_kernel(GemmArgs p) {
+  extern __shared__ __align__(16) double smem[];
+  // grouped-M swizzle for L2 reuse: walk 8 m-tiles per n-tile column group
+  const int64_t tiles_m = (p.m + GBM - 1) / GBM;
+  const int64_t tiles_n = (p.n + GBN - 1) / GBN;
+  const int64_t bid = blockIdx.x;
+  constexpr int GROUP = 8;
+  const int64_t per_group = GROUP * tiles_n;
+  const int64_t grp = bid / per_group;
+  const int64_t first_m = grp * GROUP;
+  const int64_t gsz = imin64(tiles_m - first_m, GROUP);
+  const int64_t tm = first_m + (bid % per_group) % gsz;
+  const int64_t tn = (bid % per_group) / gsz;
+  const int64_t m0 = tm * GBM, n0 = tn * GBN;
+  if (LOWER && m0 + GBM - 1 + p.diag_off < n0) return;  // tile strictly above the diagonal
+  gemm_tile<TA, TB, LOWER, VEC>(p, m0, n0, smem);
+}
+
+// Grouped launch: blockIdx.y selects a problem; problems carry their own sizes/pointers.
+template <int TA, int TB>
+__global__ void __launch_bounds__(GTHREADS, 1) gemm_grouped_kernel(const GemmArgs* __restrict__ ps,
+                                                                   int nprob) {
+  extern __shared__ __align__(16) double smem[];
+  GemmArgs p = ps[blockIdx.y];
+  if (p.m <= 0 || p.n <= 0) return;
+  const int64_t tiles_m = (p.m + GBM - 1) / GBM;
+  const int64_t tiles_n = (p.n + GBN - 1) / GBN;
+  for (int64_t b = blockIdx.x; b < tiles_m * tiles_n; b += gridDim.x) {
+    const int64_t tm = b % tiles_m, tn = b / tiles_m;
+    if (p.k <= 0) {
+      // C = beta*C (alpha*0): handled by the tile with zero accumulators
+    }
+    gemm_tile<TA, TB, 0, 1>(p, tm * GBM, tn * GBN, smem);
+    __syncthreads();
+  }
+}
+
+static size_t smem_bytes(int ta, int tb) {
+  size_t a = ta ? GBM * SPAD_K : GBK * SPAD_LONG;
+  size_t b = tb ? GBK * SPAD_LONG : GBN * SPAD_K;
+  return (a + b) * GSTAGES * sizeof(double);
+}
+
+template <int TA, int TB, int LOWER, int VEC>
+static cudaError_t launch_t(const GemmArgs& p, cudaStream_t st) {
+  auto k = gemm_kernel<TA, TB, LOWER, VEC>;
+  size_t sm = smem_bytes(TA, TB);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    configured = true;
+  }
+  int64_t tiles = ((p.m + GBM - 1) / GBM) * ((p.n + GBN - 1) / GBN);
+  k<<<(unsigned)tiles, GTHREADS, sm, st>>>(p);
+  return cudaGetLastError();
+}
+
+template <int TA, int TB, int LOWER>
+static cudaError_t launch_v(const GemmArgs& p, cudaStream_t st) {
+  auto al = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  bool vec = al(p.A) && al(p.B) && (p.lda % 2 == 0) && (p.ldb % 2 == 0);
+  // 16-byte chunks also need the tile starts to be even along the contiguous dim;
+  // tiles start at multiples of 128 (long dims) and 16 (k), so base alignment suffices.
+  if (vec) return launch_t<TA, TB, LOWER, 2>(p, st);
+  return launch_t<TA, TB, LOWER, 1>(p, st);
+}
+
+cudaError_t gemm(cudaStream_t st, bool ta, bool tb, int64_t m, int64_t n, int64_t k, double alpha,
+                 const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
+                 int64_t ldc, bool lower, int64_t diag_off) {
+  if (m <= 0 || n <= 0) return cudaSuccess;
+  GemmArgs p{m, n, k, A, lda, B, ldb, C, ldc, alpha, beta, diag_off};
+  if (k <= 0) {
+    // pure scaling: C = beta*C
+    return scale_matrix(st, m, n, beta, C, ldc, lower, diag_off);
+  }
+  int code = (ta ? 4 : 0) | (tb ? 2 : 0) | (lower ? 1 : 0);
+  switch (code) {
+    case 0: return launch_v<0, 0, 0>(p, st);
+    case 1: return launch_v<0, 0, 1>(p, st);
+    case 2: return launch_v<0, 1, 0>(p, st);
+    case 3: return launch_v<0, 1, 1>(p, st);
+    case 4: return launch_v<1, 0, 0>(p, st);
+    case 5: return launch_v<1, 0, 1>(p, st);
+    case 6: return launch_v<1, 1, 0>(p, st);
+    default: return launch_v<1, 1, 1>(p, st);
+  }
+}
+
+template <int TA, int TB>
+static cudaError_t grouped_t(const GemmArgs* d_probs, int nprob, int max_tiles, cudaStream_t st) {
+  auto k = gemm_grouped_kernel<TA, TB>;
+  size_t sm = smem_bytes(TA, TB);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    configured = true;
+  }
+  dim3 grid((unsigned)max(1, max_tiles), (unsigned)nprob);
+  k<<<grid, GTHREADS, sm, st>>>(d_probs, nprob);
+  return cudaGetLastError();
+}
+
+cudaError_t gemm_grouped(cudaStream_t st, bool ta, bool tb, const GemmArgs* d_probs, int nprob,
+                         int max_tiles) {
+  if (nprob <= 0) return cudaSuccess;
+  if (!ta && !tb) return grouped_t<0, 0>(d_probs, nprob, max_tiles, st);
+  if (!ta && tb) return grouped_t<0, 1>(d_probs, nprob, max_tiles, st);
+  if (ta && !tb) return grouped_t<1, 0>(d_probs, nprob, max_tiles, st);
+  return grouped_t<1, 1>(d_probs, nprob, max_tiles, st);
+}
+
+__global__ void scale_kernel(int64_t m, int64_t n, double beta, double* C, int64_t ldc, int lower,
+                             int64_t diag_off) {
+  int64_t total = m * n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i % m, c = i / m;
+    if (lower && r + diag_off < c) continue;
+    double* p = C + r + c * ldc;
+    *p = beta == 0.0 ? 0.0 : beta * *p;
+  }
+}
+
+cudaError_t scale_matrix(cudaStream_t st, int64_t m, int64_t n, double beta, double* C, int64_t ldc,
+                         bool lower, int64_t diag_off) {
+  if (m <= 0 || n <= 0 || beta == 1.0) return cudaSuccess;
+  int64_t total = m * n;
+  int blocks = (int)imin64((total + 255) / 256, 148 * 16);
+  scale_kernel<<<blocks, 256, 0, st>>>(m, n, beta, C, ldc, lower ? 1 : 0, diag_off);
+  return cudaGetLastError();
+}
+
+}  // namespace em

@@ -1,0 +1,32 @@
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace em {
+
+struct GemmArgs {
+  int64_t m, n, k;
+  const double* A;
+  int64_t lda;
+  const double* B;
+  int64_t ldb;
+  double* C;
+  int64_t ldc;
+  double alpha, beta;
+  int64_t diag_off;  // lower mode: element (r, c) is written iff r + diag_off >= c
+};
+
+// C(m x n) = alpha * op(A) * op(B) + beta * C; column-major; op = transpose when ta/tb.
+// lower: only the lower triangle (r + diag_off >= c) of C is computed/written.
+cudaError_t gemm(cudaStream_t st, bool ta, bool tb, int64_t m, int64_t n, int64_t k, double alpha,
+                 const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
+                 int64_t ldc, bool lower = false, int64_t diag_off = 0);
+
+// Many independent problems in one launch (device-resident argument array).
+cudaError_t gemm_grouped(cudaStream_t st, bool ta, bool tb, const GemmArgs* d_probs, int nprob,
+                         int max_tiles);
+
+cudaError_t scale_matrix(cudaStream_t st, int64_t m, int64_t n, double beta, double* C, int64_t ldc,
+                         bool lower, int64_t diag_off);
+
+}  // namespace em

@@ -1,0 +1,193 @@
+"""Generate the golden fixtures by running the UNMODIFIED reference package.
+
+Run in the build container (where /root/reference exists); the resulting
+.npz files are committed and are all the GPU box ever sees:
+
+    python tests/golden/make_golden.py kat plate_small plate_200 tubes   # seconds
+    python tests/golden/make_golden.py c1                                # ~30 min (Jacobi at N=2000)
+
+The reference is copied to a writable temp dir first because its numba
+kernels use cache=True and would write into the (read-only) source tree.
+Inputs for the plates come from paper_2407_11993_b200.synth (seeded) and
+are stored alongside the outputs so the fixtures pin both.
+"""
+from __future__ import annotations
+
+import hashlib
+import os
+import shutil
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+REF_SRC = os.environ.get("EDDYMODES_REF", "/root/reference/pkg/src")
+TMP = "/tmp/eddymodes_ref_copy"
+
+
+def import_reference():
+    if not os.path.isdir(os.path.join(TMP, "eddymodes")):
+        shutil.copytree(os.path.join(REF_SRC, "eddymodes"), os.path.join(TMP, "eddymodes"))
+    os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join(TMP, "_numba_cache"))
+    sys.path.insert(0, TMP)
+    import eddymodes  # noqa: F401
+    return eddymodes
+
+
+def sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()[:16]
+
+
+def save(name: str, **arrays):
+    path = os.path.join(HERE, f"{name}.npz")
+    np.savez_compressed(path, **arrays)
+    print(f"wrote {path} ({os.path.getsize(path) / 1e3:.0f} kB)")
+
+
+def case_kat(em):
+    from eddymodes.linalg import cholesky, sym_eig
+    from eddymodes.errors import NotPositiveDefinite
+    rng = np.random.default_rng(20240807)
+    out = {}
+    for n in (1, 2, 5, 17, 40):
+        b = rng.standard_normal((n, n))
+        a = b.T @ b + n * np.eye(n)
+        out[f"chol_a_{n}"] = a
+        out[f"chol_c_{n}"] = cholesky(a).c
+    try:
+        cholesky(np.array([[1.0, 2.0], [2.0, 1.0]]))
+    except NotPositiveDefinite as exc:
+        out["chol_indef_pivot"] = np.array(exc.pivot)
+    for name, a in (("diag", np.diag([3.0, 1.0, 2.0])),
+                    ("two", np.array([[2.0, 1.0], [1.0, 2.0]]))):
+        lam, u = sym_eig(a)
+        out[f"eig_a_{name}"], out[f"eig_lam_{name}"], out[f"eig_u_{name}"] = a, lam, u
+    a = rng.standard_normal((12, 12))
+    a = (a + a.T) / 2
+    lam, u = sym_eig(a)
+    out["eig_a_seeded"], out["eig_lam_seeded"], out["eig_u_seeded"] = a, lam, u
+    save("kat_linalg", **out)
+
+
+def _reduced(em, r, l, r_d, l_d, m0, port_names=(), source_names=()):
+    from eddymodes.linalg import SymMatrix
+    from eddymodes.reduction import ReducedModel
+    n = r.shape[0]
+    return ReducedModel(r_i=SymMatrix(r), l_i=SymMatrix(l), r_d=r_d, l_d=l_d, m0=m0,
+                        lift=np.zeros((n, r_d.shape[1])), k=np.eye(n),
+                        port_names=tuple(port_names), source_names=tuple(source_names))
+
+
+def _run_pair(em, rm, basis, drives, theta, dt, steps, c_obs, keep_every):
+    from eddymodes.transient import TransientConfig, run_transient
+    res = {}
+    for method in ("td2", "td1"):
+        cfg = TransientConfig(theta=theta, dt=dt, t_end=steps * dt, method=method,
+                              capture_stride=1, capture_state=True)
+        t0 = time.perf_counter()
+        sim = run_transient(rm, None, drives, cfg, modal=basis if method == "td2" else None)
+        print(f"  {method} theta={theta}: {time.perf_counter() - t0:.2f}s")
+        res[f"{method}_obs"] = sim.internal_states @ c_obs.T
+        res[f"{method}_states"] = sim.internal_states[keep_every - 1::keep_every]
+    return res
+
+
+def case_plate(em, name, grid, n_ports, n_sources, n_obs, steps, dt, thetas, keep_every):
+    from eddymodes.modal import generalized_eig
+    from eddymodes.network import DriveSignal, Tone
+    sys.path.insert(0, REPO)
+    from paper_2407_11993_b200.synth import plate_model
+    m = plate_model(*grid, n_ports=n_ports, n_sources=n_sources, n_obs=n_obs)
+    ports = tuple(f"p{i}" for i in range(n_ports))
+    sources = tuple(f"s{i}" for i in range(n_sources))
+    rm = _reduced(em, m["r_i"], m["l_i"], m["r_d"], m["l_d"], m["m0"], ports, sources)
+    t0 = time.perf_counter()
+    basis = generalized_eig(rm.l_i, rm.r_i)
+    t_eig = time.perf_counter() - t0
+    print(f"{name}: N={rm.n_internal} eig {t_eig:.2f}s")
+    drives = []
+    if n_sources:
+        drives.append(DriveSignal(tones=(Tone(1.0, 1e4, 0.0),), sources=sources))
+    if n_ports:
+        drives.append(DriveSignal(tones=(Tone(0.7, 2e4, 0.3), Tone(0.2, 5e4, 1.1)), ports=ports))
+    out = dict(r_i=rm.r_i.full, l_i=rm.l_i.full, r_d=m["r_d"], l_d=m["l_d"], m0=m["m0"],
+               c=m["c"], grid=np.array(grid), dt=np.array(dt), steps=np.array(steps),
+               thetas=np.array(thetas), keep_every=np.array(keep_every),
+               tau=basis.tau, l_n=basis.l_n, r_n=basis.r_n, v=basis.v,
+               t_eig_ref=np.array(t_eig))
+    for th in thetas:
+        res = _run_pair(em, rm, basis, tuple(drives), th, dt, steps, m["c"], keep_every)
+        for k, v in res.items():
+            out[f"{k}_theta{th}"] = v
+    save(name, **out)
+
+
+def case_tubes(em):
+    from eddymodes.assembly import (assemble_branch_matrices, build_current_basis,
+                                    electrode_incidence)
+    from eddymodes.modal import generalized_eig
+    from eddymodes.network import DriveSignal, Tone, generate_tube_grid
+    from eddymodes.reduction import project_model
+    from eddymodes.transient import TransientConfig, run_transient
+    for name, (na, nc) in (("tube_small", (4, 8)), ("tube_ref", (12, 24))):
+        net = generate_tube_grid(84e-3, 0.3, 3e-3, na, nc, 1.09e-6)
+        bm = assemble_branch_matrices(net)
+        basis_c = build_current_basis(net)
+        e = electrode_incidence(net, basis_c)
+        port_names = tuple(el.name for el in net.electrodes[:-1])
+        rm = project_model(bm, basis_c, e, port_names=port_names)
+        mb = generalized_eig(rm.l_i, rm.r_i)
+        out = dict(r_i=rm.r_i.full, l_i=rm.l_i.full, r_d=rm.r_d, l_d=rm.l_d, m0=rm.m0,
+                   tau=mb.tau, l_n=mb.l_n, r_n=mb.r_n, v=mb.v, vt_r=mb.vt_r)
+        drive = DriveSignal(tones=(Tone(1.0, 1e3, 0.0),), ports=port_names[:1])
+        dt = 1 / 30000
+        for method in ("td2", "td1"):
+            cfg = TransientConfig(theta=1.0, dt=dt, t_end=200 * dt, method=method)
+            sim = run_transient(rm, None, drive, cfg, modal=mb if method == "td2" else None)
+            out[f"{method}_states"] = sim.internal_states
+        out["dt"] = np.array(dt)
+        out["n_ports"] = np.array(rm.n_ports)
+        print(f"{name}: N={rm.n_internal} ports={rm.n_ports}")
+        save(name, **out)
+
+
+def case_c1(em):
+    from eddymodes.modal import generalized_eig
+    from eddymodes.network import DriveSignal, Tone
+    sys.path.insert(0, REPO)
+    from paper_2407_11993_b200.synth import plate_model
+    m = plate_model(40, 25, 2, n_ports=0, n_sources=1, n_obs=16)
+    rm = _reduced(em, m["r_i"], m["l_i"], m["r_d"], m["l_d"], m["m0"], (), ("s0",))
+    t0 = time.perf_counter()
+    basis = generalized_eig(rm.l_i, rm.r_i)
+    t_eig = time.perf_counter() - t0
+    print(f"C1 eig {t_eig:.1f}s")
+    drive = DriveSignal(tones=(Tone(1.0, 1e4, 0.0),), sources=("s0",))
+    res = _run_pair(em, rm, basis, (drive,), 0.5, 1e-6, 2000, m["c"], 500)
+    save("c1", tau=basis.tau, l_n=basis.l_n, r_n=basis.r_n, v_lead=basis.v[:, :4].copy(),
+         t_eig_ref=np.array(t_eig), input_sha_r=np.array(sha(rm.r_i.full)),
+         input_sha_l=np.array(sha(rm.l_i.full)), input_sha_c=np.array(sha(m["c"])),
+         input_sha_m0=np.array(sha(m["m0"])), **res)
+
+
+def main(argv):
+    em = import_reference()
+    for case in argv or ["kat", "plate_small", "plate_200", "tubes"]:
+        if case == "kat":
+            case_kat(em)
+        elif case == "plate_small":
+            case_plate(em, "plate_small", (6, 8, 2), 1, 1, 8, 300, 1e-6, (0.5, 1.0), 10)
+        elif case == "plate_200":
+            case_plate(em, "plate_200", (10, 10, 2), 1, 1, 16, 1000, 1e-6, (0.5,), 100)
+        elif case == "tubes":
+            case_tubes(em)
+        elif case == "c1":
+            case_c1(em)
+        else:
+            raise SystemExit(f"unknown case {case}")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:])

@@ -1,0 +1,106 @@
+"""Pin the CPU oracle against the reference's own outputs (tests/golden/*.npz,
+produced by tests/golden/make_golden.py running the unmodified reference).
+
+The C restatement of the numba kernels must agree BIT FOR BIT with the
+reference; the LAPACK restatement used at large N must agree to the
+north-star tolerances."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from tests.conftest import GOLDEN, golden, modal_directions_match, rel_l2
+
+
+def test_kat_cholesky_bitwise():
+    g = golden("kat_linalg")
+    for n in (1, 2, 5, 17, 40):
+        c = O.cholesky(g[f"chol_a_{n}"])
+        assert np.array_equal(c, g[f"chol_c_{n}"])
+
+
+def test_kat_indefinite_pivot():
+    g = golden("kat_linalg")
+    with pytest.raises(O.OracleNotPositiveDefinite) as exc:
+        O.cholesky(np.array([[1.0, 2.0], [2.0, 1.0]]))
+    assert exc.value.pivot == int(g["chol_indef_pivot"]) == 1
+
+
+@pytest.mark.parametrize("name", ["diag", "two", "seeded"])
+def test_kat_jacobi_bitwise(name):
+    g = golden("kat_linalg")
+    lam, u = O.sym_eig(g[f"eig_a_{name}"])
+    assert np.array_equal(lam, g[f"eig_lam_{name}"])
+    assert np.array_equal(u, g[f"eig_u_{name}"])
+
+
+def _tables(g):
+    dt = float(g["dt"])
+    steps = int(g["steps"])
+    sd = O.tone_sampler([[(0.7, 2e4, 0.3), (0.2, 5e4, 1.1)]])
+    s0 = O.tone_sampler([[(1.0, 1e4, 0.0)]])
+    return O.sample_table(sd, steps, dt), O.sample_table(s0, steps, dt)
+
+
+@pytest.mark.parametrize("name", ["plate_small", "plate_200"])
+def test_plate_eig_and_trajectories_bitwise(name):
+    g = golden(name)
+    l_i, r_i = O.sym_mirror(g["l_i"]), O.sym_mirror(g["r_i"])
+    b = O.generalized_eig(l_i, r_i)
+    for k in ("tau", "l_n", "r_n", "v"):
+        assert np.array_equal(getattr(b, k), g[k]), k
+    itab, i0tab = _tables(g)
+    n = l_i.shape[0]
+    ke = int(g["keep_every"])
+    for th in g["thetas"]:
+        th = float(th)
+        st2, _ = O.run(O.Td2(b, g["r_d"], g["l_d"], g["m0"], float(g["dt"]), th), n, itab,
+                       i0tab, b)
+        assert np.array_equal(st2[ke - 1::ke], g[f"td2_states_theta{th}"])
+        assert np.array_equal(st2 @ g["c"].T, g[f"td2_obs_theta{th}"])
+        st1, _ = O.run(O.Td1(l_i, r_i, g["r_d"], g["l_d"], g["m0"], float(g["dt"]), th), n,
+                       itab, i0tab, None)
+        assert np.array_equal(st1 @ g["c"].T, g[f"td1_obs_theta{th}"])
+        # SPEC acceptance #1: TD1 == TD2 to round-off
+        assert rel_l2(st2, st1) < 1e-12
+
+
+@pytest.mark.parametrize("name", ["tube_small", "tube_ref"])
+def test_tube_eig_bitwise_and_lapack_restatement(name):
+    g = golden(name)
+    l_i, r_i = O.sym_mirror(g["l_i"]), O.sym_mirror(g["r_i"])
+    b = O.generalized_eig(l_i, r_i)
+    assert np.array_equal(b.tau, g["tau"]) and np.array_equal(b.v, g["v"])
+    lap = O.generalized_eig_lapack(l_i, r_i)
+    assert np.max(np.abs(lap.tau - g["tau"]) / g["tau"]) < 1e-10
+    # the tube's rotational symmetry makes modes degenerate: compare subspaces
+    assert modal_directions_match(g["v"], g["tau"], lap.v, tol=1e-8)
+
+
+def test_plate_lapack_restatement_trajectories():
+    g = golden("plate_200")
+    lap = O.generalized_eig_lapack(O.sym_mirror(g["l_i"]), O.sym_mirror(g["r_i"]))
+    assert np.max(np.abs(lap.tau - g["tau"]) / g["tau"]) < 1e-10
+    itab, i0tab = _tables(g)
+    st, _ = O.run(O.Td2(lap, g["r_d"], g["l_d"], g["m0"], float(g["dt"]), 0.5), 200, itab,
+                  i0tab, lap)
+    assert rel_l2(st @ g["c"].T, g["td2_obs_theta0.5"]) < 1e-10
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(GOLDEN, "c1.npz")), reason="c1 golden absent")
+def test_c1_inputs_pinned_and_lapack_eigenvalues():
+    """C1 (N=2000): the synthetic generator reproduces the inputs the reference
+    ran on (hash), and the LAPACK restatement matches the reference Jacobi."""
+    import hashlib
+    from paper_2407_11993_b200.synth import plate_model
+    g = golden("c1")
+    m = plate_model(40, 25, 2, n_ports=0, n_sources=1, n_obs=16)
+
+    def sha(a):
+        return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()[:16]
+    assert sha(O.sym_mirror(m["r_i"])) == str(g["input_sha_r"])
+    assert sha(O.sym_mirror(m["l_i"])) == str(g["input_sha_l"])
+    assert sha(m["c"]) == str(g["input_sha_c"]) and sha(m["m0"]) == str(g["input_sha_m0"])
+    lap = O.generalized_eig_lapack(O.sym_mirror(m["l_i"]), O.sym_mirror(m["r_i"]))
+    assert np.max(np.abs(lap.tau - g["tau"]) / g["tau"]) < 1e-10
