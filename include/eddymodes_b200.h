@@ -1,0 +1,160 @@
+/*
+ * eddymodes_b200 — C ABI of the B200-native modal-transient hot path.
+ *
+ * libeddymodes_b200.so replaces the compiled numerics of the reference package
+ * `eddymodes` (pkg/src/eddymodes/_kernels.py, numba @njit) and the numpy/BLAS
+ * contractions around them (modal.py, transient.py). The Python mirror
+ * (paper_2407_11993_b200/) binds these entry points through ctypes; the
+ * binding a maintainer would add to the reference is in INTEGRATION.md.
+ *
+ * Conventions
+ *  - Matrices are FP64, column-major with an explicit leading dimension.
+ *    A C-contiguous (row-major) numpy array of a SYMMETRIC matrix is the same
+ *    bytes, so symmetric inputs pass straight through.
+ *  - Pointers are DEVICE pointers unless the name ends in _h (host).
+ *  - Every call is ordered on the context's stream; calls returning data to
+ *    the host (or a status that depends on device results) synchronise it.
+ *  - Return codes: EM_OK (0) on success, EM_ERR_* < 0 otherwise; the message
+ *    is available from em_last_error(). Numerical status that the reference
+ *    reports through return values (Cholesky pivot, Jacobi non-convergence)
+ *    comes back in out-parameters with the reference's encoding:
+ *    pivot = -1 success, >= 0 the first failing pivot (_kernels.py:18-36).
+ */
+#ifndef EDDYMODES_B200_H
+#define EDDYMODES_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EM_OK 0
+#define EM_ERR_CUDA -1
+#define EM_ERR_ARG -2
+#define EM_ERR_NOT_PD -3        /* pivot out-param says which */
+#define EM_ERR_NO_CONVERGENCE -4
+#define EM_ERR_ALLOC -5
+
+typedef struct em_ctx em_ctx;
+typedef struct em_td2_plan em_td2_plan;
+typedef struct em_td1_plan em_td1_plan;
+
+/* --- context --------------------------------------------------------------- */
+int em_init(int device, em_ctx** ctx);
+void em_finalize(em_ctx* ctx);
+/* Order all work on an external CUDA stream (e.g. torch.cuda.current_stream());
+ * NULL means the legacy default stream. em_init creates a private stream. */
+int em_set_stream(em_ctx* ctx, void* cuda_stream);
+const char* em_last_error(const em_ctx* ctx);
+/* Number of kernels this library has launched on ctx (for launch accounting). */
+int64_t em_launch_count(const em_ctx* ctx);
+int em_synchronize(em_ctx* ctx);
+
+/* --- dense building blocks --------------------------------------------------- */
+
+/* C = alpha*op(A)*op(B) + beta*C (DMMA). Replaces the numpy GEMMs of
+ * modal.py:79-81,90,98 and transient.py:140-154. trans_*: 0 = N, 1 = T. */
+int em_dgemm(em_ctx* ctx, int trans_a, int trans_b, int64_t m, int64_t n, int64_t k,
+             double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
+             double beta, double* C, int64_t ldc);
+
+/* Mirror the lower triangle into the upper one in place (linalg.py:34-41 SymMatrix). */
+int em_sym_mirror_lower(em_ctx* ctx, int64_t n, double* A, int64_t lda);
+
+/* Lower Cholesky A = C C^T in place (upper triangle zeroed).
+ * Replaces _kernels.cholesky_kernel (_kernels.py:18-36) / linalg.cholesky (linalg.py:92-104).
+ * *pivot = -1 on success, else the first failing pivot; returns EM_ERR_NOT_PD then. */
+int em_potrf(em_ctx* ctx, int64_t n, double* A, int64_t lda, int64_t* pivot);
+
+/* B <- C^-1 B (trans = 0) or C^-T B (trans = 1), C lower triangular n x n, B n x m.
+ * Replaces _kernels.tri_lower_solve_mat / tri_lower_t_solve_mat (_kernels.py:56-79). */
+int em_trsm_lower(em_ctx* ctx, int trans, int64_t n, int64_t m, const double* C, int64_t ldc,
+                  double* B, int64_t ldb);
+
+/* Symmetric eigendecomposition A = U diag(w) U^T, w DESCENDING (stable ties),
+ * U orthonormal (column-major n x n). A is destroyed.
+ * Replaces linalg.sym_eig (linalg.py:119-134) / _kernels.jacobi_sym_eig (_kernels.py:82-141);
+ * computed by Householder tridiagonalisation + divide and conquer. */
+int em_syev(em_ctx* ctx, int64_t n, double* A, int64_t lda, double* w, double* U, int64_t ldu);
+
+/* Generalized eigendecomposition L v = tau R v (modal.generalized_eig, modal.py:46-81).
+ * Inputs L, R symmetric (lower triangles used), device, n x n, not modified.
+ * Outputs (device): tau (n, descending), V (n x n column-major: V[i + j*ldv] =
+ * component i of mode j, R-orthonormal, sign-fixed so the largest-|.| entry of
+ * each column is positive), l_n, r_n (n) = diag(V^T L V), diag(V^T R V),
+ * VtR (n x n column-major) = (R V), i.e. the row-major bytes of V^T R.
+ * Any of l_n, r_n, VtR may be NULL to skip it.
+ * *pivot / *which report a failing Cholesky: which = 0 resistance, 1 inductance. */
+int em_sygv(em_ctx* ctx, int64_t n, const double* L, int64_t ldl, const double* R, int64_t ldr,
+            double* tau, double* V, int64_t ldv, double* l_n, double* r_n, double* VtR,
+            int64_t ldvtr, int64_t* pivot, int* which);
+
+/* --- modal theta-method (TD2, transient.py:258-308) ------------------------------- */
+
+/* Plan for the decoupled stepper. r_n, l_n: n; P_r, P_l: n x n_p; P_m: n x n_s
+ * (column-major, P = V^T [R_D | L_D | M0] — see em_dgemm). Holds device copies. */
+int em_td2_plan_create(em_ctx* ctx, int64_t n, int n_p, int n_s, const double* l_n,
+                       const double* r_n, const double* P_r, const double* P_l, const double* P_m,
+                       double dt, double theta, em_td2_plan** plan);
+void em_td2_plan_destroy(em_td2_plan* plan);
+
+/* Observables y^k = CV q^k (+ D i_d^k): CV n_obs x n (column-major, = C V),
+ * D n_obs x n_p or NULL. */
+int em_td2_set_observables(em_td2_plan* plan, int n_obs, const double* CV, int64_t ldcv,
+                           const double* D, int64_t ldd);
+
+/* Integrate T steps from modal state q (n, device, in/out) over the drive table
+ * drive ((T+1) x (n_p + n_s) row-major: row k = [i_d(t_k), i0(t_k)]), exactly the
+ * samples run_transient uses (transient.py:432-441).
+ * Y (T x n_obs row-major, may be NULL): observables after every step.
+ * Qcap (n x n_caps column-major, may be NULL): q after every stride-th step.
+ * Blocked linear-recurrence scan over time, fused with the forcing projection
+ * and the observable reconstruction (DMMA). */
+int em_td2_run(em_td2_plan* plan, int64_t T, const double* drive, double* q, double* Y,
+               int64_t stride, double* Qcap);
+
+/* One step, reference semantics (Td2Stepper.step): q (n) in place. i_d, di_d (n_p),
+ * di0 (n_s) are HOST arrays. */
+int em_td2_step(em_td2_plan* plan, double* q, const double* i_d_h, const double* di_d_h,
+                const double* di0_h);
+
+/* Per-mode forcing increment f (n, device) = -dt P_r i_d - P_ltr di_d - P_m di0
+ * (Td2Stepper.forcing, transient.py:289-297; modal_forcing, modal.py:101-118). */
+int em_td2_forcing(em_td2_plan* plan, const double* i_d_h, const double* di_d_h,
+                   const double* di0_h, double* f);
+/* q += ((-dt r q + f)/c)/c with a given forcing (step_td2, transient.py:327-337). */
+int em_td2_step_forcing(em_td2_plan* plan, double* q, const double* f);
+
+/* --- Cholesky theta-method (TD1, transient.py:219-255) ------------------------------ */
+
+/* Z = L + dt*theta*R factored on device (potrf); R kept for the per-step matvec.
+ * r_d, l_d: n x n_p; m0: n x n_s. *pivot reports a non-SPD stepping matrix. */
+int em_td1_plan_create(em_ctx* ctx, int64_t n, int n_p, int n_s, const double* L, int64_t ldl,
+                       const double* R, int64_t ldr, const double* r_d, const double* l_d,
+                       const double* m0, double dt, double theta, em_td1_plan** plan,
+                       int64_t* pivot);
+void em_td1_plan_destroy(em_td1_plan* plan);
+int em_td1_set_observables(em_td1_plan* plan, int n_obs, const double* C, int64_t ldc,
+                           const double* D, int64_t ldd);
+/* T steps from state I (n, device, in/out). Y (T x n_obs) / Icap (n x n_caps) as for TD2. */
+int em_td1_run(em_td1_plan* plan, int64_t T, const double* drive, double* I, double* Y,
+               int64_t stride, double* Icap);
+int em_td1_step(em_td1_plan* plan, double* I, const double* i_d_h, const double* di_d_h,
+                const double* di0_h);
+/* Copy the lower Cholesky factor of the stepping matrix (n x n, column-major) to out
+ * (device). Td1Stepper.chol (transient.py:237). */
+int em_td1_factor(em_td1_plan* plan, double* out, int64_t ldo);
+
+/* --- end-to-end host-pointer entry (the reference-facing call with HOST buffers) -- */
+
+/* generalized_eig on host arrays: copies L, R in, solves, copies tau, l_n, r_n back
+ * (V, VtR back too when non-NULL). Used to time the e2e path (H2D + D2H inside). */
+int em_sygv_h(em_ctx* ctx, int64_t n, const double* L_h, const double* R_h, double* tau_h,
+              double* V_h, double* l_n_h, double* r_n_h, double* VtR_h, int64_t* pivot,
+              int* which);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

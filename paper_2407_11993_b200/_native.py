@@ -1,0 +1,164 @@
+"""ctypes binding of libeddymodes_b200.so (include/eddymodes_b200.h) and the
+device-memory plumbing (torch tensors as FP64 device buffers, one CUDA stream
+shared with torch).
+
+There is no CPU fallback: if the library or a CUDA device is missing every
+entry point raises DeviceError.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+from .errors import DeviceError, NotPositiveDefinite
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libeddymodes_b200.so")
+
+EM_OK, EM_ERR_CUDA, EM_ERR_ARG, EM_ERR_NOT_PD = 0, -1, -2, -3
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_I = ctypes.c_int
+_D = ctypes.c_double
+
+# name -> (restype, argtypes)
+SIGNATURES = {
+    "em_init": (_I, [_I, ctypes.POINTER(_P)]),
+    "em_finalize": (None, [_P]),
+    "em_set_stream": (_I, [_P, _P]),
+    "em_last_error": (ctypes.c_char_p, [_P]),
+    "em_launch_count": (_I64, [_P]),
+    "em_synchronize": (_I, [_P]),
+    "em_dgemm": (_I, [_P, _I, _I, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D, _P, _I64]),
+    "em_sym_mirror_lower": (_I, [_P, _I64, _P, _I64]),
+    "em_potrf": (_I, [_P, _I64, _P, _I64, ctypes.POINTER(_I64)]),
+    "em_trsm_lower": (_I, [_P, _I, _I64, _I64, _P, _I64, _P, _I64]),
+    "em_syev": (_I, [_P, _I64, _P, _I64, _P, _P, _I64]),
+    "em_sygv": (_I, [_P, _I64, _P, _I64, _P, _I64, _P, _P, _I64, _P, _P, _P, _I64,
+                     ctypes.POINTER(_I64), ctypes.POINTER(_I)]),
+    "em_sygv_h": (_I, [_P, _I64, _P, _P, _P, _P, _P, _P, _P, ctypes.POINTER(_I64),
+                       ctypes.POINTER(_I)]),
+    "em_td2_plan_create": (_I, [_P, _I64, _I, _I, _P, _P, _P, _P, _P, _D, _D, ctypes.POINTER(_P)]),
+    "em_td2_plan_destroy": (None, [_P]),
+    "em_td2_set_observables": (_I, [_P, _I, _P, _I64, _P, _I64]),
+    "em_td2_run": (_I, [_P, _I64, _P, _P, _P, _I64, _P]),
+    "em_td2_step": (_I, [_P, _P, _P, _P, _P]),
+    "em_td2_forcing": (_I, [_P, _P, _P, _P, _P]),
+    "em_td2_step_forcing": (_I, [_P, _P, _P]),
+    "em_td1_plan_create": (_I, [_P, _I64, _I, _I, _P, _I64, _P, _I64, _P, _P, _P, _D, _D,
+                                ctypes.POINTER(_P), ctypes.POINTER(_I64)]),
+    "em_td1_plan_destroy": (None, [_P]),
+    "em_td1_set_observables": (_I, [_P, _I, _P, _I64, _P, _I64]),
+    "em_td1_run": (_I, [_P, _I64, _P, _P, _P, _I64, _P]),
+    "em_td1_step": (_I, [_P, _P, _P, _P, _P]),
+    "em_td1_factor": (_I, [_P, _P, _I64]),
+}
+
+_lib = None
+_ctx = None
+_lock = threading.Lock()
+
+
+def load_library() -> ctypes.CDLL:
+    """Load the shared library (no device needed) and bind every symbol."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise DeviceError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                              "(there is no CPU fallback)")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def torch():
+    import torch as _t
+    return _t
+
+
+def context():
+    """The process-wide em_ctx on the current CUDA device, bound to torch's stream."""
+    global _ctx
+    with _lock:
+        if _ctx is None:
+            t = torch()
+            if not t.cuda.is_available():
+                raise DeviceError("no CUDA device: the B200 path has no CPU fallback")
+            lib = load_library()
+            dev = t.cuda.current_device()
+            ctx = _P()
+            rc = lib.em_init(dev, ctypes.byref(ctx))
+            if rc != EM_OK:
+                raise DeviceError(f"em_init failed ({rc})")
+            stream = t.cuda.current_stream(dev).cuda_stream
+            rc = lib.em_set_stream(ctx, _P(stream))
+            if rc != EM_OK:
+                raise DeviceError("em_set_stream failed")
+            _ctx = ctx
+        return _ctx
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == EM_OK:
+        return
+    msg = load_library().em_last_error(_ctx)
+    msg = msg.decode() if msg else ""
+    raise DeviceError(f"{what}: error {rc} {msg}".strip())
+
+
+def launches() -> int:
+    return int(load_library().em_launch_count(_ctx))
+
+
+def synchronize() -> None:
+    torch().cuda.current_stream().synchronize()
+
+
+# --- device buffers ------------------------------------------------------------------
+# A column-major (m x n) device matrix is held as a torch tensor of shape (n, m),
+# contiguous: element (i, j) lives at j*m + i.
+
+def device_colmajor(a: np.ndarray):
+    """Host (m x n) matrix -> device column-major buffer (tensor shaped (n, m))."""
+    t = torch()
+    a = np.asarray(a, dtype=np.float64)
+    if a.ndim == 1:
+        a = a[:, None]
+    return t.from_numpy(np.ascontiguousarray(a.T)).to("cuda")
+
+
+def device_vector(x: np.ndarray):
+    t = torch()
+    return t.from_numpy(np.ascontiguousarray(np.asarray(x, dtype=np.float64))).to("cuda")
+
+
+def empty(*shape):
+    t = torch()
+    return t.empty(*shape, dtype=t.float64, device="cuda")
+
+
+def zeros(*shape):
+    t = torch()
+    return t.zeros(*shape, dtype=t.float64, device="cuda")
+
+
+def host_colmajor(buf, m: int, n: int) -> np.ndarray:
+    """Device column-major buffer (tensor (n, m)) -> host C-contiguous (m x n)."""
+    return np.ascontiguousarray(buf.reshape(n, m).cpu().numpy().T)
+
+
+def ptr(t) -> _P:
+    return _P(t.data_ptr()) if t is not None else _P(0)
+
+
+def raise_not_pd(rc: int, pivot: int, what: str) -> None:
+    if rc == EM_ERR_NOT_PD:
+        raise NotPositiveDefinite(int(pivot), what)

@@ -1,0 +1,329 @@
+// extern "C" boundary of libeddymodes_b200.so (see include/eddymodes_b200.h).
+// Every entry catches internal exceptions and maps them to EM_ERR_* codes with
+// a message retrievable through em_last_error().
+#include <stdio.h>
+
+#include <string>
+
+#include "common.cuh"
+#include "ctx.h"
+#include "gemm.h"
+#include "linalg.h"
+
+struct em_td2_plan;
+struct em_td1_plan;
+
+namespace em {
+int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const double* R,
+             int64_t ldr, double* tau, double* V, int64_t ldv, double* l_n, double* r_n,
+             double* VtR, int64_t ldvtr, int* which);
+}
+
+// full definitions live in td1.cu / td2.cu; re-declare the layout-independent API here
+#include "plans.h"
+
+namespace {
+
+template <typename F>
+int guarded(em_ctx* ctx, F&& f) {
+  try {
+    if (ctx) cudaSetDevice(ctx->device);
+    return f();
+  } catch (const em::CudaError& e) {
+    if (ctx) ctx->err = std::string(cudaGetErrorString(e.code)) + " in " + e.where;
+    return EM_ERR_CUDA;
+  } catch (const em::ArgError& e) {
+    if (ctx) ctx->err = e.what;
+    return EM_ERR_ARG;
+  } catch (const std::bad_alloc&) {
+    if (ctx) ctx->err = "host allocation failed";
+    return EM_ERR_ALLOC;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int em_init(int device, em_ctx** out) {
+  if (!out) return EM_ERR_ARG;
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    *out = nullptr;
+    return EM_ERR_CUDA;
+  }
+  if (device < 0 || device >= count) return EM_ERR_ARG;
+  auto* ctx = new em_ctx();
+  ctx->device = device;
+  if (cudaSetDevice(device) != cudaSuccess) {
+    delete ctx;
+    return EM_ERR_CUDA;
+  }
+  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete ctx;
+    return EM_ERR_CUDA;
+  }
+  ctx->own_stream = true;
+  ctx->sms = em::num_sms();
+  // keep freed pool memory cached between calls (stream-ordered allocator)
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  *out = ctx;
+  return EM_OK;
+}
+
+void em_finalize(em_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->own_stream && ctx->stream) {
+    cudaStreamSynchronize(ctx->stream);
+    cudaStreamDestroy(ctx->stream);
+  }
+  delete ctx;
+}
+
+int em_set_stream(em_ctx* ctx, void* s) {
+  if (!ctx) return EM_ERR_ARG;
+  return guarded(ctx, [&] {
+    if (ctx->own_stream && ctx->stream) {
+      EM_CK(cudaStreamSynchronize(ctx->stream));
+      EM_CK(cudaStreamDestroy(ctx->stream));
+    }
+    // used as given: NULL is the legacy default stream (torch's default stream)
+    ctx->stream = reinterpret_cast<cudaStream_t>(s);
+    ctx->own_stream = false;
+    return EM_OK;
+  });
+}
+
+const char* em_last_error(const em_ctx* ctx) { return ctx ? ctx->err.c_str() : "no context"; }
+
+int64_t em_launch_count(const em_ctx*) { return em::g_launches.load(); }
+
+int em_synchronize(em_ctx* ctx) {
+  return guarded(ctx, [&] {
+    EM_CK(cudaStreamSynchronize(ctx->stream));
+    return EM_OK;
+  });
+}
+
+int em_dgemm(em_ctx* ctx, int ta, int tb, int64_t m, int64_t n, int64_t k, double alpha,
+             const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
+             int64_t ldc) {
+  return guarded(ctx, [&] {
+    EM_CK(em::gemm(ctx->stream, ta != 0, tb != 0, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc));
+    return EM_OK;
+  });
+}
+
+int em_sym_mirror_lower(em_ctx* ctx, int64_t n, double* A, int64_t lda) {
+  return guarded(ctx, [&] {
+    em::mirror_lower(ctx->stream, n, A, lda);
+    return EM_OK;
+  });
+}
+
+int em_potrf(em_ctx* ctx, int64_t n, double* A, int64_t lda, int64_t* pivot) {
+  return guarded(ctx, [&] {
+    const int64_t p = em::potrf(ctx->stream, n, A, lda);
+    if (pivot) *pivot = p;
+    return p >= 0 ? EM_ERR_NOT_PD : EM_OK;
+  });
+}
+
+int em_trsm_lower(em_ctx* ctx, int trans, int64_t n, int64_t m, const double* C, int64_t ldc,
+                  double* B, int64_t ldb) {
+  return guarded(ctx, [&] {
+    em::trsm_lower(ctx->stream, trans != 0, n, m, C, ldc, B, ldb);
+    return EM_OK;
+  });
+}
+
+int em_syev(em_ctx* ctx, int64_t n, double* A, int64_t lda, double* w, double* U, int64_t ldu) {
+  return guarded(ctx, [&] {
+    cudaStream_t st = ctx->stream;
+    em::DBuf wa(n, st), Za((size_t)n * n, st);
+    em::syev_ascending(st, n, A, lda, wa.p, Za.p, n);
+    // descending order (linalg.py:132-134): reverse
+    em::reverse_columns(st, n, n, Za.p, n, wa.p, U, ldu, w);
+    EM_CK(cudaStreamSynchronize(st));
+    return EM_OK;
+  });
+}
+
+int em_sygv(em_ctx* ctx, int64_t n, const double* L, int64_t ldl, const double* R, int64_t ldr,
+            double* tau, double* V, int64_t ldv, double* l_n, double* r_n, double* VtR,
+            int64_t ldvtr, int64_t* pivot, int* which) {
+  return guarded(ctx, [&] {
+    int wh = -1;
+    const int64_t p = em::sygv(ctx->stream, n, L, ldl, R, ldr, tau, V, ldv, l_n, r_n, VtR, ldvtr,
+                               &wh);
+    if (pivot) *pivot = p;
+    if (which) *which = wh;
+    return p >= 0 ? EM_ERR_NOT_PD : EM_OK;
+  });
+}
+
+int em_sygv_h(em_ctx* ctx, int64_t n, const double* L_h, const double* R_h, double* tau_h,
+              double* V_h, double* l_n_h, double* r_n_h, double* VtR_h, int64_t* pivot,
+              int* which) {
+  return guarded(ctx, [&] {
+    cudaStream_t st = ctx->stream;
+    const size_t nn = (size_t)n * n;
+    em::DBuf L(nn, st), R(nn, st), V(nn, st), t(n, st), ln(n, st), rn(n, st), VtR;
+    if (VtR_h) VtR.alloc(nn, st);
+    EM_CK(cudaMemcpyAsync(L.p, L_h, nn * 8, cudaMemcpyHostToDevice, st));
+    EM_CK(cudaMemcpyAsync(R.p, R_h, nn * 8, cudaMemcpyHostToDevice, st));
+    int wh = -1;
+    const int64_t p = em::sygv(st, n, L.p, n, R.p, n, t.p, V.p, n, ln.p, rn.p,
+                               VtR_h ? VtR.p : nullptr, n, &wh);
+    if (pivot) *pivot = p;
+    if (which) *which = wh;
+    if (p >= 0) return EM_ERR_NOT_PD;
+    EM_CK(cudaMemcpyAsync(tau_h, t.p, n * 8, cudaMemcpyDeviceToHost, st));
+    if (l_n_h) EM_CK(cudaMemcpyAsync(l_n_h, ln.p, n * 8, cudaMemcpyDeviceToHost, st));
+    if (r_n_h) EM_CK(cudaMemcpyAsync(r_n_h, rn.p, n * 8, cudaMemcpyDeviceToHost, st));
+    if (V_h) EM_CK(cudaMemcpyAsync(V_h, V.p, nn * 8, cudaMemcpyDeviceToHost, st));
+    if (VtR_h) EM_CK(cudaMemcpyAsync(VtR_h, VtR.p, nn * 8, cudaMemcpyDeviceToHost, st));
+    EM_CK(cudaStreamSynchronize(st));
+    return EM_OK;
+  });
+}
+
+// ---- TD2 ----------------------------------------------------------------------------
+
+int em_td2_plan_create(em_ctx* ctx, int64_t n, int n_p, int n_s, const double* l_n,
+                       const double* r_n, const double* P_r, const double* P_l, const double* P_m,
+                       double dt, double theta, em_td2_plan** plan) {
+  return guarded(ctx, [&] {
+    if (!plan || n < 0 || n_p < 0 || n_s < 0) throw em::ArgError{"bad td2 plan arguments"};
+    auto* P = em::td2_new(ctx, n, n_p, n_s, dt, theta);
+    try {
+      em::td2_plan_init(P, l_n, r_n, P_r, P_l, P_m);
+      EM_CK(cudaStreamSynchronize(ctx->stream));
+    } catch (...) {
+      em::td2_delete(P);
+      throw;
+    }
+    *plan = P;
+    return EM_OK;
+  });
+}
+
+void em_td2_plan_destroy(em_td2_plan* plan) { em::td2_delete(plan); }
+
+int em_td2_set_observables(em_td2_plan* plan, int n_obs, const double* CV, int64_t ldcv,
+                           const double* D, int64_t ldd) {
+  em_ctx* ctx = em::td2_ctx(plan);
+  return guarded(ctx, [&] {
+    em::td2_set_observables(plan, n_obs, CV, ldcv, D, ldd);
+    return EM_OK;
+  });
+}
+
+int em_td2_run(em_td2_plan* plan, int64_t T, const double* drive, double* q, double* Y,
+               int64_t stride, double* Qcap) {
+  em_ctx* ctx = em::td2_ctx(plan);
+  return guarded(ctx, [&] {
+    em::td2_run(plan, T, drive, q, Y, stride, Qcap);
+    return EM_OK;
+  });
+}
+
+int em_td2_step(em_td2_plan* plan, double* q, const double* i_d_h, const double* di_d_h,
+                const double* di0_h) {
+  em_ctx* ctx = em::td2_ctx(plan);
+  return guarded(ctx, [&] {
+    em::td2_step_host(plan, q, i_d_h, di_d_h, di0_h);
+    return EM_OK;
+  });
+}
+
+int em_td2_forcing(em_td2_plan* plan, const double* i_d_h, const double* di_d_h,
+                   const double* di0_h, double* f) {
+  em_ctx* ctx = em::td2_ctx(plan);
+  return guarded(ctx, [&] {
+    em::td2_forcing_host(plan, i_d_h, di_d_h, di0_h, f);
+    return EM_OK;
+  });
+}
+
+int em_td2_step_forcing(em_td2_plan* plan, double* q, const double* f) {
+  em_ctx* ctx = em::td2_ctx(plan);
+  return guarded(ctx, [&] {
+    em::td2_step_forcing(plan, q, f);
+    EM_CK(cudaStreamSynchronize(ctx->stream));
+    return EM_OK;
+  });
+}
+
+// ---- TD1 ----------------------------------------------------------------------------
+
+int em_td1_plan_create(em_ctx* ctx, int64_t n, int n_p, int n_s, const double* L, int64_t ldl,
+                       const double* R, int64_t ldr, const double* r_d, const double* l_d,
+                       const double* m0, double dt, double theta, em_td1_plan** plan,
+                       int64_t* pivot) {
+  return guarded(ctx, [&] {
+    if (!plan || n < 0 || n_p < 0 || n_s < 0) throw em::ArgError{"bad td1 plan arguments"};
+    auto* P = em::td1_new(ctx, n, n_p, n_s, dt, theta);
+    int64_t piv = -1;
+    try {
+      piv = em::td1_plan_init(P, L, ldl, R, ldr, r_d, l_d, m0);
+      EM_CK(cudaStreamSynchronize(ctx->stream));
+    } catch (...) {
+      em::td1_delete(P);
+      throw;
+    }
+    if (pivot) *pivot = piv;
+    if (piv >= 0) {
+      em::td1_delete(P);
+      *plan = nullptr;
+      return EM_ERR_NOT_PD;
+    }
+    *plan = P;
+    return EM_OK;
+  });
+}
+
+void em_td1_plan_destroy(em_td1_plan* plan) { em::td1_delete(plan); }
+
+int em_td1_set_observables(em_td1_plan* plan, int n_obs, const double* C, int64_t ldc,
+                           const double* D, int64_t ldd) {
+  em_ctx* ctx = em::td1_ctx(plan);
+  return guarded(ctx, [&] {
+    em::td1_set_observables(plan, n_obs, C, ldc, D, ldd);
+    return EM_OK;
+  });
+}
+
+int em_td1_run(em_td1_plan* plan, int64_t T, const double* drive, double* I, double* Y,
+               int64_t stride, double* Icap) {
+  em_ctx* ctx = em::td1_ctx(plan);
+  return guarded(ctx, [&] {
+    em::td1_run(plan, T, drive, I, Y, stride, Icap);
+    return EM_OK;
+  });
+}
+
+int em_td1_step(em_td1_plan* plan, double* I, const double* i_d_h, const double* di_d_h,
+                const double* di0_h) {
+  em_ctx* ctx = em::td1_ctx(plan);
+  return guarded(ctx, [&] {
+    em::td1_step_host(plan, I, i_d_h, di_d_h, di0_h);
+    return EM_OK;
+  });
+}
+
+int em_td1_factor(em_td1_plan* plan, double* out, int64_t ldo) {
+  em_ctx* ctx = em::td1_ctx(plan);
+  return guarded(ctx, [&] {
+    em::td1_copy_factor(plan, out, ldo);
+    return EM_OK;
+  });
+}
+
+}  // extern "C"

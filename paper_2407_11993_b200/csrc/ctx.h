@@ -1,0 +1,97 @@
+// Internal runtime: context, error capture, stream-ordered device workspace,
+// launch accounting. Everything here is plumbing for the C ABI in capi.cu.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <string>
+#include <vector>
+
+#include "../../include/eddymodes_b200.h"
+
+struct em_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::string err;
+  int sms = 148;
+};
+
+namespace em {
+
+extern std::atomic<int64_t> g_launches;
+inline void count_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+// Throws on CUDA error; caught at the C ABI boundary and turned into EM_ERR_CUDA.
+struct CudaError {
+  cudaError_t code;
+  std::string where;
+};
+struct ArgError {
+  std::string what;
+};
+
+#define EM_CK(x)                                                                      \
+  do {                                                                                \
+    cudaError_t e_ = (x);                                                             \
+    if (e_ != cudaSuccess) throw ::em::CudaError{e_, std::string(#x) + " @" __FILE__}; \
+  } while (0)
+#define EM_LAUNCHED()                      \
+  do {                                     \
+    ::em::count_launch();                  \
+    EM_CK(cudaGetLastError());             \
+  } while (0)
+
+// Stream-ordered device buffer (cudaMallocAsync pool).
+struct DBuf {
+  double* p = nullptr;
+  size_t n = 0;
+  cudaStream_t st = nullptr;
+  DBuf() = default;
+  DBuf(size_t count, cudaStream_t s) { alloc(count, s); }
+  void alloc(size_t count, cudaStream_t s) {
+    release();
+    st = s;
+    n = count;
+    if (count) EM_CK(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(double), s));
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, st);
+    p = nullptr;
+    n = 0;
+  }
+  ~DBuf() { release(); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), st(o.st) { o.p = nullptr; o.n = 0; }
+};
+
+template <typename T>
+struct DArr {
+  T* p = nullptr;
+  cudaStream_t st = nullptr;
+  DArr() = default;
+  DArr(size_t count, cudaStream_t s) : st(s) {
+    if (count) EM_CK(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), s));
+  }
+  ~DArr() {
+    if (p) cudaFreeAsync(p, st);
+  }
+  DArr(const DArr&) = delete;
+  DArr& operator=(const DArr&) = delete;
+};
+
+// --- small utility kernels (util.cu) ---------------------------------------
+void mirror_lower(cudaStream_t st, int64_t n, double* A, int64_t lda);
+// B = op(A) (m x n result), op = transpose when trans
+void copy_matrix(cudaStream_t st, bool trans, int64_t m, int64_t n, const double* A, int64_t lda,
+                 double* B, int64_t ldb);
+// C = alpha*A + beta*B^T (square n) — used for symmetrisation (A + A^T)/2
+void add_transpose(cudaStream_t st, int64_t n, double alpha, const double* A, int64_t lda,
+                   double beta, double* C, int64_t ldc);
+void zero_upper(cudaStream_t st, int64_t n, double* A, int64_t lda);
+void set_identity(cudaStream_t st, int64_t n, double* A, int64_t lda);
+int num_sms();
+
+}  // namespace em

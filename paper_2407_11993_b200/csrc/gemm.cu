@@ -11,6 +11,7 @@
 // 8-byte fragment load is bank-conflict free (row strides = 4 mod 16 doubles).
 #include "common.cuh"
 #include "gemm.h"
+#include "ctx.h"
 
 namespace em {
 
@@ -209,6 +210,7 @@ static cudaError_t launch_t(const GemmArgs& p, cudaStream_t st) {
   }
   int64_t tiles = ((p.m + GBM - 1) / GBM) * ((p.n + GBN - 1) / GBN);
   k<<<(unsigned)tiles, GTHREADS, sm, st>>>(p);
+  count_launch();
   return cudaGetLastError();
 }
 
@@ -255,6 +257,7 @@ static cudaError_t grouped_t(const GemmArgs* d_probs, int nprob, int max_tiles, 
   }
   dim3 grid((unsigned)max(1, max_tiles), (unsigned)nprob);
   k<<<grid, GTHREADS, sm, st>>>(d_probs, nprob);
+  count_launch();
   return cudaGetLastError();
 }
 
@@ -285,6 +288,7 @@ cudaError_t scale_matrix(cudaStream_t st, int64_t m, int64_t n, double beta, dou
   int64_t total = m * n;
   int blocks = (int)imin64((total + 255) / 256, 148 * 16);
   scale_kernel<<<blocks, 256, 0, st>>>(m, n, beta, C, ldc, lower ? 1 : 0, diag_off);
+  count_launch();
   return cudaGetLastError();
 }
 

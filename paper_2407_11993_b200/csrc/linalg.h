@@ -1,0 +1,55 @@
+// Internal dense FP64 linear-algebra entry points (device pointers, column-major).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+struct em_td2_plan;
+struct em_td1_plan;
+
+namespace em {
+
+// potrf.cu
+int64_t potrf(cudaStream_t st, int64_t n, double* A, int64_t lda);  // -1 ok, else pivot
+void trsm_lower(cudaStream_t st, bool trans, int64_t n, int64_t m, const double* C, int64_t ldc,
+                double* B, int64_t ldb);
+void trtri_blocks(cudaStream_t st, int nb, int64_t n, const double* C, int64_t ldc, double* Dinv);
+
+// symv.cu: y = alpha*A*x + beta*y using only the lower triangle of A (n x n)
+void symv_lower(cudaStream_t st, int64_t n, double alpha, const double* A, int64_t lda,
+                const double* x, double beta, double* y, double* work);
+size_t symv_work_size(int64_t n);
+
+// sytrd.cu: Householder tridiagonalisation (lower). On exit d (n), e (n-1), tau (n-1);
+// reflectors stored below the subdiagonal of A (LAPACK dsytrd convention).
+void sytrd_lower(cudaStream_t st, int64_t n, double* A, int64_t lda, double* d, double* e,
+                 double* tau);
+// ormtr: Z <- Q Z with Q = H(0) ... H(n-2) from sytrd_lower (Z n x m)
+void ormtr_lower(cudaStream_t st, int64_t n, int64_t m, const double* A, int64_t lda,
+                 const double* tau, double* Z, int64_t ldz);
+
+// stedc.cu: tridiagonal eigensolver (divide and conquer). Eigenvalues ascending in d,
+// eigenvectors in Z (n x n, ld ldz). e is destroyed.
+void stedc(cudaStream_t st, int64_t n, double* d, double* e, double* Z, int64_t ldz);
+
+// syev.cu: symmetric eigendecomposition, eigenvalues ASCENDING; A destroyed.
+void syev_ascending(cudaStream_t st, int64_t n, double* A, int64_t lda, double* w, double* Z,
+                    int64_t ldz);
+
+// td1.cu / td2.cu
+void td2_plan_init(em_td2_plan* P, const double* l_n, const double* r_n, const double* P_r,
+                   const double* P_l, const double* P_m);
+void td2_set_observables(em_td2_plan* P, int n_obs, const double* CV, int64_t ldcv,
+                         const double* D, int64_t ldd);
+void td2_run(em_td2_plan* P, int64_t T, const double* drive, double* q, double* Y,
+             int64_t stride, double* Qcap);
+void td2_step(em_td2_plan* P, double* q, const double* u_dev);
+
+int64_t td1_plan_init(em_td1_plan* P, const double* L, int64_t ldl, const double* R, int64_t ldr,
+                      const double* r_d, const double* l_d, const double* m0);
+void td1_set_observables(em_td1_plan* P, int n_obs, const double* C, int64_t ldc,
+                         const double* D, int64_t ldd);
+void td1_run(em_td1_plan* P, int64_t T, const double* drive, double* I, double* Y,
+             int64_t stride, double* Icap);
+void td1_step(em_td1_plan* P, double* I, const double* u_dev);
+
+}  // namespace em

@@ -1,0 +1,157 @@
+// Generalized symmetric-definite eigensolve L v = tau R v — the device version of
+// modal.generalized_eig (pkg/src/eddymodes/modal.py:46-81):
+//   R = G G^T (potrf, "modal resistance matrix")
+//   B = G^-1 L G^-T as the reference forms it: G^-1 L, G^-1 (G^-1 L)^T, (B + B^T)/2
+//   potrf(L) certificate ("modal inductance matrix"), same order as the reference
+//   B = U diag(w) U^T   (sytrd + divide & conquer + ormtr; replaces Jacobi)
+//   V = G^-T U, descending order, sign fix (largest |entry| positive),
+//   l_n = diag(V^T L V), r_n = diag(V^T R V), V^T R (= (R V)^T).
+#include "common.cuh"
+#include "ctx.h"
+#include "gemm.h"
+#include "linalg.h"
+
+namespace em {
+
+void syev_ascending(cudaStream_t st, int64_t n, double* A, int64_t lda, double* w, double* Z,
+                    int64_t ldz) {
+  if (n <= 0) return;
+  DBuf d(n, st), e(imax64(n - 1, 1), st), tau(imax64(n - 1, 1), st);
+  sytrd_lower(st, n, A, lda, d.p, e.p, tau.p);
+  stedc(st, n, d.p, e.p, Z, ldz);
+  ormtr_lower(st, n, n, A, lda, tau.p, Z, ldz);
+  EM_CK(cudaMemcpyAsync(w, d.p, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+}
+
+// V[:, j] = s_j * Z[:, n-1-j], s_j = sign of the first largest-|.| entry; tau[j] = w[n-1-j]
+__global__ void finalize_modes_kernel(int64_t n, const double* __restrict__ Z, int64_t ldz,
+                                      const double* __restrict__ w, double* __restrict__ V,
+                                      int64_t ldv, double* __restrict__ tau) {
+  __shared__ double bv[32];
+  __shared__ int64_t bi[32];
+  __shared__ double sgn;
+  const int64_t j = blockIdx.x;
+  const int64_t src = n - 1 - j;
+  const double* z = Z + src * ldz;
+  double best = -1.0;
+  int64_t idx = 0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const double a = fabs(z[i]);
+    if (a > best) {
+      best = a;
+      idx = i;
+    }
+  }
+  // (max |v|, smallest index) reduction == np.argmax semantics
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int64_t oi = __shfl_xor_sync(0xffffffffu, idx, o);
+    if (ob > best || (ob == best && oi < idx)) {
+      best = ob;
+      idx = oi;
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    bv[threadIdx.x >> 5] = best;
+    bi[threadIdx.x >> 5] = idx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = bv[0];
+    int64_t k = bi[0];
+    for (int q = 1; q < (int)(blockDim.x >> 5); ++q)
+      if (bv[q] > b || (bv[q] == b && bi[q] < k)) {
+        b = bv[q];
+        k = bi[q];
+      }
+    const double v = z[k];
+    sgn = (v < 0.0) ? -1.0 : 1.0;  // np.sign, with 0 -> +1 (modal.py:76-77)
+    tau[j] = w[src];
+  }
+  __syncthreads();
+  const double s = sgn;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) V[i + j * ldv] = s * z[i];
+}
+
+// out[j] = sum_i V[i,j] * X[i,j]
+__global__ void coldot_kernel(int64_t n, const double* __restrict__ V, int64_t ldv,
+                              const double* __restrict__ X, int64_t ldx, double* __restrict__ out) {
+  __shared__ double red[32];
+  const int64_t j = blockIdx.x;
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s = fma(V[i + j * ldv], X[i + j * ldx], s);
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double t = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) out[j] = t;
+  }
+}
+
+// Returns -1 on success; else the failing pivot with *which = 0 (R) / 1 (L).
+int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const double* R,
+             int64_t ldr, double* tau, double* V, int64_t ldv, double* l_n, double* r_n,
+             double* VtR, int64_t ldvtr, int* which) {
+  *which = -1;
+  if (n <= 0) return -1;
+  const size_t nn = (size_t)n * n;
+  DBuf G(nn, st);
+  copy_matrix(st, false, n, n, R, ldr, G.p, n);
+  int64_t piv = potrf(st, n, G.p, n);
+  if (piv >= 0) {
+    *which = 0;
+    return piv;
+  }
+  DBuf B(nn, st);
+  {
+    DBuf X(nn, st);
+    copy_matrix(st, false, n, n, L, ldl, B.p, n);
+    trsm_lower(st, false, n, n, G.p, n, B.p, n);           // G^-1 L
+    copy_matrix(st, true, n, n, B.p, n, X.p, n);           // (G^-1 L)^T
+    trsm_lower(st, false, n, n, G.p, n, X.p, n);           // G^-1 (G^-1 L)^T
+    add_transpose(st, n, 0.5, X.p, n, 0.5, B.p, n);        // (X + X^T)/2
+    // certificate only (modal.py:69-70)
+    copy_matrix(st, false, n, n, L, ldl, X.p, n);
+    piv = potrf(st, n, X.p, n);
+    if (piv >= 0) {
+      *which = 1;
+      return piv;
+    }
+  }
+  DBuf w(n, st), Z(nn, st);
+  syev_ascending(st, n, B.p, n, w.p, Z.p, n);
+  B.release();
+  trsm_lower(st, true, n, n, G.p, n, Z.p, n);              // V = G^-T U
+  G.release();
+  finalize_modes_kernel<<<(unsigned)n, 256, 0, st>>>(n, Z.p, n, w.p, V, ldv, tau);
+  EM_LAUNCHED();
+  Z.release();
+  if (l_n) {
+    DBuf LV(nn, st);
+    EM_CK(gemm(st, false, false, n, n, n, 1.0, L, ldl, V, ldv, 0.0, LV.p, n));
+    coldot_kernel<<<(unsigned)n, 256, 0, st>>>(n, V, ldv, LV.p, n, l_n);
+    EM_LAUNCHED();
+  }
+  if (r_n || VtR) {
+    DBuf tmp;
+    double* RV = VtR;
+    int64_t ldrv = ldvtr;
+    if (!RV) {
+      tmp.alloc(nn, st);
+      RV = tmp.p;
+      ldrv = n;
+    }
+    EM_CK(gemm(st, false, false, n, n, n, 1.0, R, ldr, V, ldv, 0.0, RV, ldrv));
+    if (r_n) {
+      coldot_kernel<<<(unsigned)n, 256, 0, st>>>(n, V, ldv, RV, ldrv, r_n);
+      EM_LAUNCHED();
+    }
+    EM_CK(cudaStreamSynchronize(st));
+  }
+  EM_CK(cudaStreamSynchronize(st));
+  return -1;
+}
+
+}  // namespace em

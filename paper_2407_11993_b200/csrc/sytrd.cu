@@ -1,0 +1,302 @@
+// Householder tridiagonalisation (lower, blocked: latrd panels + syr2k) and the
+// blocked back-transform Z <- Q Z (ormtr). Together with stedc.cu this replaces
+// the reference's cyclic Jacobi eigensolver (_kernels.py:82-141), which is
+// O(sweeps N^3) sequential; the result (eigenvalues, invariant subspaces) is
+// the same to round-off.
+//
+// Per panel column the memory-bound part is one lower-triangle symv over the
+// trailing matrix (symv.cu); the rank-2k trailing update and the
+// back-transform run on the DMMA GEMM.
+#include "common.cuh"
+#include "ctx.h"
+#include "gemm.h"
+#include "linalg.h"
+
+namespace em {
+
+constexpr int TRD_NB = 64;   // panel width
+constexpr int RT = 256;
+
+// A[c:n, c] -= A[c:n, i0:c] W[c, 0:i]^T + W[c:n, 0:i] A[c, i0:c]^T
+__global__ void latrd_colupd_kernel(int64_t n, double* A, int64_t lda, int64_t i0, int64_t c,
+                                    const double* __restrict__ W, int64_t ldw) {
+  const int i = (int)(c - i0);
+  __shared__ double wr[TRD_NB], ar[TRD_NB];
+  for (int k = threadIdx.x; k < i; k += blockDim.x) {
+    wr[k] = W[(c - i0) + k * ldw];     // W row c (W rows are indexed from i0)
+    ar[k] = A[c + (i0 + k) * lda];     // A row c
+  }
+  __syncthreads();
+  for (int64_t r = c + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    double s = A[r + c * lda];
+    for (int k = 0; k < i; ++k) {
+      s = fma(-A[r + (i0 + k) * lda], wr[k], s);
+      s = fma(-W[(r - i0) + k * ldw], ar[k], s);
+    }
+    A[r + c * lda] = s;
+  }
+}
+
+// dlarfg on x = A[c+1:n, c]: beta, tau; v = [1, x[1:]/(alpha-beta)]; e[c] = beta; d[c] = A[c,c].
+// Single CTA (1024 threads).
+__global__ void larfg_kernel(int64_t n, double* A, int64_t lda, int64_t c, double* d, double* e,
+                             double* tau) {
+  __shared__ double red[32];
+  __shared__ double sc;
+  const int tid = threadIdx.x;
+  double ss = 0.0;
+  for (int64_t r = c + 2 + tid; r < n; r += blockDim.x) {
+    const double v = A[r + c * lda];
+    ss = fma(v, v, ss);
+  }
+  ss = warp_sum(ss);
+  if ((tid & 31) == 0) red[tid >> 5] = ss;
+  __syncthreads();
+  if (tid < 32) {
+    double v = (tid < (int)(blockDim.x >> 5)) ? red[tid] : 0.0;
+    v = warp_sum(v);
+    if (tid == 0) {
+      const double alpha = A[(c + 1) + c * lda];
+      const double xnorm = sqrt(v);
+      d[c] = A[c + c * lda];
+      if (xnorm == 0.0) {
+        tau[c] = 0.0;
+        e[c] = alpha;
+        sc = 0.0;
+      } else {
+        const double beta = -copysign(hypot(alpha, xnorm), alpha);
+        tau[c] = (beta - alpha) / beta;
+        sc = 1.0 / (alpha - beta);
+        e[c] = beta;
+      }
+      A[(c + 1) + c * lda] = 1.0;
+    }
+  }
+  __syncthreads();
+  const double s = sc;
+  if (s != 0.0)
+    for (int64_t r = c + 2 + tid; r < n; r += blockDim.x) A[r + c * lda] *= s;
+}
+
+// tmp1[k] = W[c+1:, k] . v   tmp2[k] = A[c+1:, i0+k] . v   (k < i); one CTA per (k, which)
+__global__ void latrd_dots_kernel(int64_t n, const double* A, int64_t lda, int64_t i0, int64_t c,
+                                  const double* W, int64_t ldw, double* tmp) {
+  const int i = (int)(c - i0);
+  const int k = blockIdx.x % i;
+  const int which = blockIdx.x / i;
+  __shared__ double red[32];
+  const double* v = A + c * lda;
+  double s = 0.0;
+  for (int64_t r = c + 1 + threadIdx.x; r < n; r += blockDim.x) {
+    const double col = which == 0 ? W[(r - i0) + k * ldw] : A[r + (i0 + k) * lda];
+    s = fma(col, v[r], s);
+  }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double t = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) tmp[which * TRD_NB + k] = t;
+  }
+}
+
+// w = tau*(w - A_p tmp1 - W_p tmp2); partial dots of w.v per CTA
+__global__ void latrd_wcol_kernel(int64_t n, const double* A, int64_t lda, int64_t i0, int64_t c,
+                                  double* W, int64_t ldw, const double* tmp, const double* tau,
+                                  double* part) {
+  const int i = (int)(c - i0);
+  __shared__ double t1[TRD_NB], t2[TRD_NB], red[32];
+  for (int k = threadIdx.x; k < i; k += blockDim.x) {
+    t1[k] = tmp[k];
+    t2[k] = tmp[TRD_NB + k];
+  }
+  __syncthreads();
+  const double tc = tau[c];
+  const double* v = A + c * lda;
+  double* w = W + i * ldw;
+  double s = 0.0;
+  for (int64_t r = c + 1 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    double x = w[r - i0];
+    for (int k = 0; k < i; ++k) {
+      x = fma(-A[r + (i0 + k) * lda], t1[k], x);
+      x = fma(-W[(r - i0) + k * ldw], t2[k], x);
+    }
+    x *= tc;
+    w[r - i0] = x;
+    s = fma(x, v[r], s);
+  }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double t = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) part[blockIdx.x] = t;
+  }
+}
+
+// w += alpha v,  alpha = -tau/2 * (w.v)
+__global__ void latrd_wfix_kernel(int64_t n, const double* A, int64_t lda, int64_t i0, int64_t c,
+                                  double* W, int64_t ldw, const double* tau, const double* part,
+                                  int nparts) {
+  __shared__ double alpha;
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int p = 0; p < nparts; ++p) s += part[p];
+    alpha = -0.5 * tau[c] * s;
+  }
+  __syncthreads();
+  const int i = (int)(c - i0);
+  const double* v = A + c * lda;
+  double* w = W + i * ldw;
+  for (int64_t r = c + 1 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x)
+    w[r - i0] = fma(alpha, v[r], w[r - i0]);
+}
+
+__global__ void set_diag_kernel(int64_t n, const double* A, int64_t lda, int64_t c, double* d) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) d[c] = A[c + c * lda];
+}
+
+// restore A[c+1, c] = e[c] for the panel columns
+__global__ void restore_sub_kernel(int64_t n, double* A, int64_t lda, int64_t i0, int w,
+                                   const double* e) {
+  int k = threadIdx.x;
+  if (k < w) {
+    int64_t c = i0 + k;
+    if (c + 1 < n) A[(c + 1) + c * lda] = e[c];
+  }
+}
+
+static int grid_for(int64_t m) { return (int)imax64(1, imin64((m + RT - 1) / RT, 4 * num_sms())); }
+
+void sytrd_lower(cudaStream_t st, int64_t n, double* A, int64_t lda, double* d, double* e,
+                 double* tau) {
+  if (n <= 0) return;
+  if (n == 1) {
+    set_diag_kernel<<<1, 32, 0, st>>>(n, A, lda, 0, d);
+    EM_LAUNCHED();
+    return;
+  }
+  DBuf W((size_t)n * TRD_NB, st);
+  DBuf XW((size_t)n * 2 * TRD_NB, st), YW((size_t)n * 2 * TRD_NB, st);
+  DBuf tmp(2 * TRD_NB, st);
+  const int maxparts = 4 * num_sms();
+  DBuf part(maxparts, st);
+  DBuf swork(symv_work_size(n), st);
+  for (int64_t i0 = 0; i0 < n; i0 += TRD_NB) {
+    const int w = (int)imin64(TRD_NB, n - i0);
+    for (int i = 0; i < w; ++i) {
+      const int64_t c = i0 + i;
+      if (i > 0) {
+        latrd_colupd_kernel<<<grid_for(n - c), RT, 0, st>>>(n, A, lda, i0, c, W.p, n);
+        EM_LAUNCHED();
+      }
+      if (c == n - 1) {
+        set_diag_kernel<<<1, 32, 0, st>>>(n, A, lda, c, d);
+        EM_LAUNCHED();
+        break;
+      }
+      larfg_kernel<<<1, 1024, 0, st>>>(n, A, lda, c, d, e, tau);
+      EM_LAUNCHED();
+      const int64_t m = n - c - 1;
+      // W[c+1:, i] = A22 v  (A22 = trailing lower triangle)
+      symv_lower(st, m, 1.0, A + (c + 1) + (c + 1) * lda, lda, A + (c + 1) + c * lda, 0.0,
+                 W.p + (c + 1 - i0) + (int64_t)i * n, swork.p);
+      if (i > 0) {
+        latrd_dots_kernel<<<2 * i, RT, 0, st>>>(n, A, lda, i0, c, W.p, n, tmp.p);
+        EM_LAUNCHED();
+      }
+      const int g = grid_for(m);
+      latrd_wcol_kernel<<<g, RT, 0, st>>>(n, A, lda, i0, c, W.p, n, tmp.p, tau, part.p);
+      EM_LAUNCHED();
+      latrd_wfix_kernel<<<g, RT, 0, st>>>(n, A, lda, i0, c, W.p, n, tau, part.p, g);
+      EM_LAUNCHED();
+    }
+    const int64_t t0 = i0 + w;
+    const int64_t mt = n - t0;
+    if (mt > 0) {
+      // A22 -= V W^T + W V^T as one K = 2w lower GEMM: [V | W] [W | V]^T
+      copy_matrix(st, false, mt, w, A + t0 + i0 * lda, lda, XW.p, n);
+      copy_matrix(st, false, mt, w, W.p + (t0 - i0), n, XW.p + (int64_t)w * n, n);
+      copy_matrix(st, false, mt, w, W.p + (t0 - i0), n, YW.p, n);
+      copy_matrix(st, false, mt, w, A + t0 + i0 * lda, lda, YW.p + (int64_t)w * n, n);
+      EM_CK(gemm(st, false, true, mt, mt, 2 * w, -1.0, XW.p, n, YW.p, n, 1.0,
+                 A + t0 + t0 * lda, lda, true, 0));
+    }
+    restore_sub_kernel<<<1, TRD_NB, 0, st>>>(n, A, lda, i0, w, e);
+    EM_LAUNCHED();
+  }
+}
+
+// ---- ormtr ----------------------------------------------------------------------
+
+// Explicit V block for panel i0 (w reflectors, rows i0+1 .. n-1): V[r, k] =
+// 0 (r < k), 1 (r == k), A[i0+1+r, i0+k] (r > k), r relative to row i0+1.
+__global__ void build_v_kernel(int64_t n, const double* A, int64_t lda, int64_t i0, int w,
+                               double* V, int64_t ldv) {
+  const int64_t m = n - i0 - 1;
+  const int k = blockIdx.y;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < m;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    double v;
+    if (r < k)
+      v = 0.0;
+    else if (r == k)
+      v = 1.0;
+    else
+      v = A[(i0 + 1 + r) + (i0 + k) * lda];
+    V[r + k * ldv] = v;
+  }
+}
+
+// T (w x w upper) from G = V^T V: T[k][k] = tau_k; T[0:k, k] = -tau_k T[0:k, 0:k] G[0:k, k]
+__global__ void larft_kernel(int w, const double* G, const double* tau, int64_t c0, double* T) {
+  __shared__ double Ts[TRD_NB][TRD_NB + 1];
+  __shared__ double gk[TRD_NB];
+  const int tid = threadIdx.x;
+  for (int i = tid; i < TRD_NB * TRD_NB; i += blockDim.x) Ts[i % TRD_NB][i / TRD_NB] = 0.0;
+  __syncthreads();
+  for (int k = 0; k < w; ++k) {
+    const double tk = tau[c0 + k];
+    if (tid < k) gk[tid] = G[tid + k * w];
+    __syncthreads();
+    if (tid < k) {
+      double s = 0.0;
+      for (int j = tid; j < k; ++j) s = fma(Ts[tid][j], gk[j], s);  // T upper: j >= tid
+      Ts[tid][k] = -tk * s;
+    }
+    if (tid == 0) Ts[k][k] = tk;
+    __syncthreads();
+  }
+  for (int i = tid; i < w * w; i += blockDim.x) T[(i % w) + (i / w) * w] = Ts[i % w][i / w];
+}
+
+void ormtr_lower(cudaStream_t st, int64_t n, int64_t m, const double* A, int64_t lda,
+                 const double* tau, double* Z, int64_t ldz) {
+  const int64_t nref = n - 1;  // reflectors H(0..n-2)
+  if (nref <= 0 || m <= 0) return;
+  DBuf V((size_t)n * TRD_NB, st), G((size_t)TRD_NB * TRD_NB, st), T((size_t)TRD_NB * TRD_NB, st);
+  DBuf W1((size_t)TRD_NB * m, st), W2((size_t)TRD_NB * m, st);
+  const int64_t npan = (nref + TRD_NB - 1) / TRD_NB;
+  for (int64_t p = npan - 1; p >= 0; --p) {
+    const int64_t i0 = p * TRD_NB;
+    const int w = (int)imin64(TRD_NB, nref - i0);
+    const int64_t mr = n - i0 - 1;  // rows of V
+    dim3 grid((unsigned)imax64(1, imin64((mr + 255) / 256, 64)), (unsigned)w);
+    build_v_kernel<<<grid, 256, 0, st>>>(n, A, lda, i0, w, V.p, n);
+    EM_LAUNCHED();
+    EM_CK(gemm(st, true, false, w, w, mr, 1.0, V.p, n, V.p, n, 0.0, G.p, w));
+    larft_kernel<<<1, TRD_NB, 0, st>>>(w, G.p, tau, i0, T.p);
+    EM_LAUNCHED();
+    double* Zs = Z + (i0 + 1);
+    EM_CK(gemm(st, true, false, w, m, mr, 1.0, V.p, n, Zs, ldz, 0.0, W1.p, w));
+    EM_CK(gemm(st, false, false, w, m, w, 1.0, T.p, w, W1.p, w, 0.0, W2.p, w));
+    EM_CK(gemm(st, false, false, mr, m, w, -1.0, V.p, n, W2.p, w, 1.0, Zs, ldz));
+  }
+}
+
+}  // namespace em

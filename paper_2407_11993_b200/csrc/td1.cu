@@ -1,0 +1,433 @@
+// Cholesky-factor theta-method (TD1) on B200 — the comparator of the paper.
+//
+// Reference: Td1Stepper (pkg/src/eddymodes/transient.py:219-255) factors
+// Z = L_i + dt*theta*R_i once (cholesky, "stepping matrix") and every step runs
+// td1_step_kernel (_kernels.py:198-210): b = -dt R I + drive_rhs (modal.py:121-131),
+// forward then backward substitution with the factor (tri_solve_vec,
+// _kernels.py:39-53), I += x.
+//
+// GPU form per step: b = E u^k - dt*R*I (lower-triangle symv, HBM-bound), then two
+// PERSISTENT triangular-solve kernels. Block rows of 64 are claimed in order from
+// an atomic counter; a CTA streams the off-diagonal tiles of its block row as
+// soon as the producing block's flag (release/acquire, epoch-tagged) is up,
+// reduces with warp shuffles / shared memory, and applies the pre-inverted
+// 64x64 diagonal block. Memory-bound: each solve reads the packed factor once.
+#include "common.cuh"
+#include "ctx.h"
+#include "gemm.h"
+#include "linalg.h"
+#include "plans.h"
+
+#include <vector>
+
+struct em_td1_plan {
+  em_ctx* ctx = nullptr;
+  int64_t n = 0;
+  int n_p = 0, n_s = 0, n_u = 0;
+  double dt = 0, theta = 0;
+  em::DBuf C, R, Dinv, E, work, b, y, x;
+  em::DArr<unsigned long long>* flags = nullptr;
+  em::DArr<unsigned int>* counters = nullptr;
+  unsigned long long epoch = 0;
+  int n_obs = 0;
+  em::DBuf Cobs, D;
+  ~em_td1_plan() {
+    delete flags;
+    delete counters;
+  }
+};
+
+namespace em {
+
+constexpr int TS = 64;  // triangular-solve block
+
+__global__ void td1_z_kernel(int64_t n, const double* __restrict__ L, int64_t ldl,
+                             const double* __restrict__ R, int64_t ldr, double dt_theta,
+                             double* __restrict__ Z, double* __restrict__ Rc) {
+  const int64_t c = blockIdx.y;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    // symmetric inputs: use the lower triangle (SymMatrix semantics, linalg.py:40-41)
+    const int64_t rr = r >= c ? r : c, cc = r >= c ? c : r;
+    const double l = L[rr + cc * ldl], rv = R[rr + cc * ldr];
+    Z[r + c * n] = l + dt_theta * rv;
+    Rc[r + c * n] = rv;
+  }
+}
+
+// E = [-dt R_D | -(L_D + dt theta R_D) | -M0]  (drive_rhs, modal.py:121-131)
+__global__ void td1_e_kernel(int64_t n, int n_p, int n_s, double dt, double theta,
+                             const double* __restrict__ r_d, const double* __restrict__ l_d,
+                             const double* __restrict__ m0, double* __restrict__ E) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int p = 0; p < n_p; ++p) {
+    const double rd = r_d[i + p * n], ld = l_d[i + p * n];
+    E[i + p * n] = -dt * rd;
+    E[i + (int64_t)(n_p + p) * n] = -(ld + dt * theta * rd);
+  }
+  for (int s = 0; s < n_s; ++s) E[i + (int64_t)(2 * n_p + s) * n] = -m0[i + s * n];
+}
+
+// b = E u  (u = [i_d^k, di_d^k, di0^k] built from the drive table rows k, k+1)
+__global__ void td1_rhs_kernel(int64_t n, int n_p, int n_s, const double* __restrict__ E,
+                               const double* __restrict__ drive, int64_t k,
+                               double* __restrict__ b) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int n_c = n_p + n_s;
+  const double* d0 = drive + k * n_c;
+  const double* d1 = d0 + n_c;
+  double v = 0.0;
+  for (int p = 0; p < n_p; ++p) {
+    v = fma(E[i + p * n], d0[p], v);
+    v = fma(E[i + (int64_t)(n_p + p) * n], d1[p] - d0[p], v);
+  }
+  for (int s = 0; s < n_s; ++s) v = fma(E[i + (int64_t)(2 * n_p + s) * n], d1[n_p + s] - d0[n_p + s], v);
+  b[i] = v;
+}
+
+__global__ void td1_rhs_u_kernel(int64_t n, int n_u, const double* __restrict__ E,
+                                 const double* __restrict__ u, double* __restrict__ b) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double v = 0.0;
+  for (int j = 0; j < n_u; ++j) v = fma(E[i + (int64_t)j * n], u[j], v);
+  b[i] = v;
+}
+
+EM_DEVINL unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+EM_DEVINL void st_release(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
+}
+
+// Wait until flags[j] == epoch for all j in [j0, j1]; returns once satisfied.
+EM_DEVINL void wait_flags(const unsigned long long* flags, int64_t j0, int64_t j1,
+                          unsigned long long epoch) {
+  if (threadIdx.x == 0) {
+    for (int64_t j = j0; j <= j1; ++j)
+      while (ld_acquire(flags + j) != epoch) __nanosleep(32);
+  }
+  __syncthreads();
+}
+
+// Forward solve C y = b, C lower (col-major, ld ldc). Block rows claimed in order.
+__global__ void __launch_bounds__(256) trsv_fwd_kernel(int64_t n, const double* __restrict__ C,
+                                                       int64_t ldc, const double* __restrict__ Dinv,
+                                                       const double* __restrict__ b,
+                                                       double* __restrict__ y,
+                                                       unsigned long long* flags,
+                                                       unsigned int* counter,
+                                                       unsigned long long epoch) {
+  __shared__ int64_t rblk;
+  __shared__ double red[4][TS];
+  __shared__ double part[TS];
+  const int tid = threadIdx.x, tx = tid & 63, ty = tid >> 6;
+  const int64_t nblk = (n + TS - 1) / TS;
+  while (true) {
+    __syncthreads();
+    if (tid == 0) rblk = atomicAdd(counter, 1u);
+    __syncthreads();
+    const int64_t r = rblk;
+    if (r >= nblk) break;
+    const int64_t r0 = r * TS, row = r0 + tx;
+    double acc = 0.0;
+    int64_t j = 0;
+    while (j < r) {
+      // take every already-published block in one go (at least one)
+      __shared__ int64_t jr;
+      if (tid == 0) {
+        while (ld_acquire(flags + j) != epoch) __nanosleep(20);
+        int64_t e = j;
+        while (e + 1 < r && ld_acquire(flags + e + 1) == epoch) ++e;
+        jr = e;
+      }
+      __syncthreads();
+      const int64_t je = jr;
+      for (; j <= je; ++j) {
+        const int64_t c0 = j * TS + ty * 16;
+        double a[16], yy[16];
+#pragma unroll
+        for (int cc = 0; cc < 16; ++cc) {
+          a[cc] = (row < n) ? C[row + (c0 + cc) * ldc] : 0.0;
+          yy[cc] = __ldcg(y + c0 + cc);
+        }
+#pragma unroll
+        for (int cc = 0; cc < 16; ++cc) acc = fma(a[cc], yy[cc], acc);
+      }
+      __syncthreads();
+    }
+    red[ty][tx] = acc;
+    __syncthreads();
+    if (tid < TS) {
+      const double bb = (r0 + tid < n) ? b[r0 + tid] : 0.0;
+      part[tid] = bb - (red[0][tid] + red[1][tid] + red[2][tid] + red[3][tid]);
+    }
+    __syncthreads();
+    // y_r = Dinv_r * part
+    const double* D = Dinv + r * TS * TS;
+    double s = 0.0;
+#pragma unroll
+    for (int cc = 0; cc < 16; ++cc) s = fma(D[tx + (ty * 16 + cc) * TS], part[ty * 16 + cc], s);
+    red[ty][tx] = s;
+    __syncthreads();
+    if (tid < TS && r0 + tid < n) y[r0 + tid] = red[0][tid] + red[1][tid] + red[2][tid] + red[3][tid];
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) st_release(flags + r, epoch);
+  }
+}
+
+// Backward solve C^T x = y; then I += x (and capture). Block rows claimed from the bottom.
+__global__ void __launch_bounds__(256) trsv_bwd_kernel(
+    int64_t n, const double* __restrict__ C, int64_t ldc, const double* __restrict__ Dinv,
+    const double* __restrict__ y, double* __restrict__ x, double* __restrict__ I,
+    double* __restrict__ Icap, unsigned long long* flags, unsigned int* counter,
+    unsigned long long epoch) {
+  __shared__ int64_t rblk;
+  __shared__ double red[8][TS];
+  __shared__ double part[TS];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tx = tid & 63, ty = tid >> 6;
+  const int64_t nblk = (n + TS - 1) / TS;
+  while (true) {
+    __syncthreads();
+    if (tid == 0) rblk = nblk - 1 - (int64_t)atomicAdd(counter, 1u);
+    __syncthreads();
+    const int64_t r = rblk;
+    if (r < 0) break;
+    const int64_t r0 = r * TS;
+    double acc[16];
+#pragma unroll
+    for (int cc = 0; cc < 16; ++cc) acc[cc] = 0.0;
+    int64_t j = nblk - 1;
+    while (j > r) {
+      __shared__ int64_t jr;
+      if (tid == 0) {
+        while (ld_acquire(flags + j) != epoch) __nanosleep(20);
+        int64_t e = j;
+        while (e - 1 > r && ld_acquire(flags + e - 1) == epoch) --e;
+        jr = e;
+      }
+      __syncthreads();
+      const int64_t je = jr;
+      for (; j >= je; --j) {
+        const int64_t rowj = j * TS + tx;
+        const double xv = (rowj < n) ? __ldcg(x + rowj) : 0.0;
+        const int64_t c0 = r0 + ty * 16;
+#pragma unroll
+        for (int cc = 0; cc < 16; ++cc) {
+          const double a = (rowj < n) ? C[rowj + (c0 + cc) * ldc] : 0.0;
+          acc[cc] = fma(a, xv, acc[cc]);
+        }
+      }
+      __syncthreads();
+    }
+    // reduce acc[cc] over the 64 rows (tx): warp shuffle, then the two warps per ty
+#pragma unroll
+    for (int cc = 0; cc < 16; ++cc) acc[cc] = warp_sum(acc[cc]);
+    if (lane == 0) {
+#pragma unroll
+      for (int cc = 0; cc < 16; ++cc) red[warp][cc] = acc[cc];
+    }
+    __syncthreads();
+    if (tid < TS) {
+      const int g = tid >> 4, cc = tid & 15;  // column tid = g*16 + cc belongs to ty = g (warps 2g, 2g+1)
+      const double sumc = red[2 * g][cc] + red[2 * g + 1][cc];
+      const double yy = (r0 + tid < n) ? y[r0 + tid] : 0.0;
+      part[tid] = yy - sumc;
+    }
+    __syncthreads();
+    // x_r = Dinv_r^T part:  x[c] = sum_c' Dinv[c' + c*TS] part[c']
+    const double* D = Dinv + r * TS * TS;
+    double s = 0.0;
+#pragma unroll
+    for (int cc = 0; cc < 16; ++cc) s = fma(D[(ty * 16 + cc) + tx * TS], part[ty * 16 + cc], s);
+    __syncthreads();
+    red[ty][tx] = s;
+    __syncthreads();
+    if (tid < TS && r0 + tid < n) {
+      const double xv = red[0][tid] + red[1][tid] + red[2][tid] + red[3][tid];
+      x[r0 + tid] = xv;
+      const double iv = I[r0 + tid] + xv;
+      I[r0 + tid] = iv;
+      if (Icap) Icap[r0 + tid] = iv;
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) st_release(flags + r, epoch);
+  }
+}
+
+int64_t td1_plan_init(em_td1_plan* P, const double* L, int64_t ldl, const double* R, int64_t ldr,
+                      const double* r_d, const double* l_d, const double* m0) {
+  cudaStream_t st = P->ctx->stream;
+  const int64_t n = P->n;
+  P->C.alloc((size_t)n * n, st);
+  P->R.alloc((size_t)n * n, st);
+  dim3 grid((unsigned)imin64((n + 255) / 256, 64), (unsigned)n);
+  td1_z_kernel<<<grid, 256, 0, st>>>(n, L, ldl, R, ldr, P->dt * P->theta, P->C.p, P->R.p);
+  EM_LAUNCHED();
+  const int64_t piv = potrf(st, n, P->C.p, n);
+  if (piv >= 0) return piv;
+  const int64_t nblk = (n + TS - 1) / TS;
+  P->Dinv.alloc((size_t)nblk * TS * TS, st);
+  trtri_blocks(st, TS, n, P->C.p, n, P->Dinv.p);
+  P->E.alloc((size_t)n * imax64(P->n_u, 1), st);
+  if (P->n_u > 0) {
+    td1_e_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, P->n_p, P->n_s, P->dt, P->theta,
+                                                             r_d, l_d, m0, P->E.p);
+    EM_LAUNCHED();
+  }
+  P->work.alloc(symv_work_size(n), st);
+  P->b.alloc(n, st);
+  P->y.alloc(n, st);
+  P->x.alloc(n, st);
+  P->flags = new DArr<unsigned long long>(2 * nblk, st);
+  EM_CK(cudaMemsetAsync(P->flags->p, 0, 2 * nblk * sizeof(unsigned long long), st));
+  P->counters = new DArr<unsigned int>(2, st);
+  return -1;
+}
+
+void td1_set_observables(em_td1_plan* P, int n_obs, const double* C, int64_t ldc, const double* D,
+                         int64_t ldd) {
+  cudaStream_t st = P->ctx->stream;
+  P->n_obs = n_obs;
+  P->Cobs.alloc((size_t)n_obs * P->n, st);
+  copy_matrix(st, false, n_obs, P->n, C, ldc, P->Cobs.p, n_obs);
+  if (D && P->n_p > 0) {
+    P->D.alloc((size_t)n_obs * P->n_p, st);
+    copy_matrix(st, false, n_obs, P->n_p, D, ldd, P->D.p, n_obs);
+  } else {
+    P->D.release();
+  }
+}
+
+// one step given b already holding the drive part; I in place; Icap column or null
+static void td1_solve_step(em_td1_plan* P, double* I, double* Icap_col) {
+  cudaStream_t st = P->ctx->stream;
+  const int64_t n = P->n;
+  const int64_t nblk = (n + TS - 1) / TS;
+  // b += -dt R I
+  symv_lower(st, n, -P->dt, P->R.p, n, I, 1.0, P->b.p, P->work.p);
+  ++P->epoch;
+  EM_CK(cudaMemsetAsync(P->counters->p, 0, 2 * sizeof(unsigned int), st));
+  const int grid = (int)imin64(nblk, 2 * num_sms());
+  trsv_fwd_kernel<<<grid, 256, 0, st>>>(n, P->C.p, n, P->Dinv.p, P->b.p, P->y.p, P->flags->p,
+                                        P->counters->p, P->epoch);
+  EM_LAUNCHED();
+  trsv_bwd_kernel<<<grid, 256, 0, st>>>(n, P->C.p, n, P->Dinv.p, P->y.p, P->x.p, I, Icap_col,
+                                        P->flags->p + nblk, P->counters->p + 1, P->epoch);
+  EM_LAUNCHED();
+}
+
+void td1_step(em_td1_plan* P, double* I, const double* u_dev) {
+  cudaStream_t st = P->ctx->stream;
+  const int64_t n = P->n;
+  if (P->n_u > 0) {
+    td1_rhs_u_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, P->n_u, P->E.p, u_dev, P->b.p);
+    EM_LAUNCHED();
+  } else {
+    EM_CK(cudaMemsetAsync(P->b.p, 0, n * sizeof(double), st));
+  }
+  td1_solve_step(P, I, nullptr);
+}
+
+void td1_run(em_td1_plan* P, int64_t T, const double* drive, double* I, double* Y, int64_t stride,
+             double* Icap) {
+  cudaStream_t st = P->ctx->stream;
+  const int64_t n = P->n;
+  if (stride < 1) throw ArgError{"capture stride must be >= 1"};
+  const int64_t n_caps = T / stride;
+  const bool want_y = Y && P->n_obs > 0 && n_caps > 0;
+  // observables are formed in chunks: capture states, then one DMMA GEMM per chunk
+  const int64_t chunk = Icap ? n_caps : imin64(n_caps, 512);
+  DBuf tmpcap;
+  if (!Icap && want_y) tmpcap.alloc((size_t)n * imax64(chunk, 1), st);
+  int64_t cap = 0, chunk_start = 0;
+  auto flush = [&](int64_t upto) {
+    if (!want_y || upto <= chunk_start) return;
+    const int64_t cnt = upto - chunk_start;
+    const double* src = Icap ? Icap + chunk_start * n : tmpcap.p;
+    // Y rows [chunk_start, upto): Y^T (n_obs x cnt, col-major == row-major Y) = Cobs * I
+    EM_CK(gemm(st, false, false, P->n_obs, cnt, n, 1.0, P->Cobs.p, P->n_obs, src, n, 0.0,
+               Y + chunk_start * P->n_obs, P->n_obs));
+    chunk_start = upto;
+  };
+  for (int64_t k = 0; k < T; ++k) {
+    if (P->n_u > 0) {
+      td1_rhs_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, P->n_p, P->n_s, P->E.p,
+                                                                 drive, k, P->b.p);
+      EM_LAUNCHED();
+    } else {
+      EM_CK(cudaMemsetAsync(P->b.p, 0, n * sizeof(double), st));
+    }
+    double* col = nullptr;
+    const bool is_cap = ((k + 1) % stride) == 0;
+    if (is_cap && (Icap || want_y)) {
+      col = Icap ? Icap + cap * n : tmpcap.p + (cap - chunk_start) * n;
+    }
+    td1_solve_step(P, I, col);
+    if (is_cap) {
+      ++cap;
+      if (!Icap && want_y && cap - chunk_start == chunk) flush(cap);
+    }
+  }
+  flush(cap);
+  if (want_y && P->D.n) {
+    // Y += D i_d(t_{k+1}) at each capture: small GEMM-free loop on host-less path
+    // (drive rows (c+1)*stride): gather rows then GEMM would be overkill; use gemm on a
+    // strided view: drive row stride = (n_p+n_s)*stride.
+    const int n_c = P->n_p + P->n_s;
+    EM_CK(gemm(st, false, false, P->n_obs, n_caps, P->n_p, 1.0, P->D.p, P->n_obs,
+               drive + (int64_t)stride * n_c, (int64_t)stride * n_c, 1.0, Y, P->n_obs));
+  }
+}
+
+}  // namespace em
+
+namespace em {
+
+em_td1_plan* td1_new(em_ctx* ctx, int64_t n, int n_p, int n_s, double dt, double theta) {
+  auto* P = new em_td1_plan();
+  P->ctx = ctx;
+  P->n = n;
+  P->n_p = n_p;
+  P->n_s = n_s;
+  P->n_u = 2 * n_p + n_s;
+  P->dt = dt;
+  P->theta = theta;
+  return P;
+}
+void td1_delete(em_td1_plan* p) {
+  if (!p) return;
+  cudaSetDevice(p->ctx->device);
+  cudaStreamSynchronize(p->ctx->stream);
+  delete p;
+}
+em_ctx* td1_ctx(em_td1_plan* p) { return p ? p->ctx : nullptr; }
+void td1_copy_factor(em_td1_plan* P, double* out, int64_t ldo) {
+  copy_matrix(P->ctx->stream, false, P->n, P->n, P->C.p, P->n, out, ldo);
+  EM_CK(cudaStreamSynchronize(P->ctx->stream));
+}
+
+void td1_step_host(em_td1_plan* P, double* I, const double* i_d, const double* di_d,
+                   const double* di0) {
+  cudaStream_t st = P->ctx->stream;
+  std::vector<double> u((size_t)imax64(P->n_u, 1), 0.0);
+  for (int p = 0; p < P->n_p; ++p) {
+    u[p] = i_d[p];
+    u[P->n_p + p] = di_d[p];
+  }
+  for (int s = 0; s < P->n_s; ++s) u[2 * P->n_p + s] = di0[s];
+  DBuf du(u.size(), st);
+  EM_CK(cudaMemcpyAsync(du.p, u.data(), u.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+  td1_step(P, I, du.p);
+  EM_CK(cudaStreamSynchronize(st));
+}
+
+}  // namespace em

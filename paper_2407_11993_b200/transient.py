@@ -1,0 +1,535 @@
+"""Theta-method time integration two ways — the reference's transient module
+(pkg/src/eddymodes/transient.py:1-404) on the B200 library.
+
+td1 (Td1Stepper): Z = L_i + dt*theta*R_i factored once on the device; every step
+is a lower-triangle symv with R plus two persistent triangular-solve kernels.
+td2 (Td2Stepper): the drive is projected onto the modes once (DMMA GEMM), and a
+whole run is ONE blocked linear-recurrence scan over time fused with the
+forcing and the observable reconstruction (em_td2_run).
+
+The per-step `step()` methods keep the reference's host in-place semantics
+(one device round trip per call); `run()` and run_transient are the batched
+fast path. Observables y = C I + D i_D(t_{k+1}) (the reference's
+`t_internal @ internal + t_ports @ i_d_next`, transient.py:446-447) are given
+directly as matrices; the probe geometry (assembly.field_transfer) is a front
+end outside this path.
+"""
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as nat
+from . import linalg
+from .errors import DimensionMismatch, NotPositiveDefinite, ValidationError
+from .modal import ModalBasis, drive_rhs
+from .network import DriveSignal
+from .reduction import ReducedModel
+
+
+@dataclass(frozen=True)
+class TransientConfig:
+    """theta in [0, 1], step dt, final time t_end, method td1/td2 (transient.py:27-57)."""
+
+    theta: float
+    dt: float
+    t_end: float
+    method: str = "td1"
+    probes: np.ndarray | None = None
+    capture_stride: int = 1
+    capture_state: bool = True
+
+    def __post_init__(self):
+        if not (0.0 <= self.theta <= 1.0):
+            raise ValidationError("theta must lie in [0, 1]")
+        if self.dt <= 0:
+            raise ValidationError("dt must be positive")
+        if self.t_end < self.dt:
+            raise ValidationError("t_end must be at least one step")
+        if self.method not in ("td1", "td2"):
+            raise ValidationError(f"unknown method {self.method!r}")
+        if self.capture_stride < 1:
+            raise ValidationError("capture_stride must be >= 1")
+        if self.probes is not None:
+            object.__setattr__(self, "probes",
+                               np.atleast_2d(np.asarray(self.probes, dtype=float)))
+
+    @property
+    def n_steps(self) -> int:
+        return max(int(round(self.t_end / self.dt)), 1)
+
+
+@dataclass
+class SimulationResult:
+    """Captured trajectory plus the setup/stepping wall-time split (transient.py:60-74).
+    `observables` (n_captures, n_obs) is filled when run_transient gets observables=(C, D)."""
+
+    times: np.ndarray
+    internal_states: np.ndarray | None
+    probe_fields: np.ndarray | None
+    wall_time_setup: float
+    wall_time_stepping: float
+    n_steps: int
+    method: str
+    observables: np.ndarray | None = None
+
+    @property
+    def per_step_cost(self) -> float:
+        return self.wall_time_stepping / self.n_steps
+
+
+def _check_theta_dt(dt, theta):
+    if dt <= 0:
+        raise ValidationError("dt must be positive")
+    if not (0.0 <= theta <= 1.0):
+        raise ValidationError("theta must lie in [0, 1]")
+
+
+def _drive_table(i_d_samples, i0_samples, n_p, n_s) -> np.ndarray:
+    """(T+1) x (n_p + n_s) row-major sample table [i_d(t_k) | i0(t_k)]."""
+    i_d = np.asarray(i_d_samples, dtype=float).reshape(-1, n_p) if n_p else None
+    i0 = np.asarray(i0_samples, dtype=float).reshape(-1, n_s) if n_s else None
+    rows = (i_d if i_d is not None else i0).shape[0] if (n_p or n_s) else None
+    if rows is None:
+        raise ValidationError("drive table needs the number of samples")
+    parts = [p for p in (i_d, i0) if p is not None]
+    for p in parts:
+        if p.shape[0] != rows:
+            raise DimensionMismatch("port and source sample tables differ in length")
+    return np.ascontiguousarray(np.concatenate(parts, axis=1))
+
+
+def _obs_device(observables, n: int, n_p: int):
+    """(C (n_obs x n), D (n_obs x n_p) or None) -> device column-major buffers."""
+    c, d = observables if isinstance(observables, tuple) else (observables, None)
+    c = np.atleast_2d(np.asarray(c, dtype=float))
+    if c.shape[1] != n:
+        raise DimensionMismatch(f"observables need {n} columns, got {c.shape}")
+    if c.shape[0] > 128:
+        raise ValidationError("at most 128 observables per run")
+    dd = None
+    if d is not None and n_p:
+        d = np.asarray(d, dtype=float).reshape(c.shape[0], n_p)
+        dd = nat.device_colmajor(d)
+    return c.shape[0], nat.device_colmajor(c), dd
+
+
+class Td2Stepper:
+    """Decoupled stepper (transient.py:258-308): per-mode scalar updates after
+    projecting the drive onto the modes."""
+
+    def __init__(self, rm: ReducedModel, basis: ModalBasis, dt: float, theta: float):
+        _check_theta_dt(dt, theta)
+        if basis.n_modes != rm.n_internal:
+            raise DimensionMismatch("modal basis does not match the reduced model")
+        t0 = time.perf_counter()
+        self.rm = rm
+        self.basis = basis
+        self.dt = float(dt)
+        self.theta = float(theta)
+        n, n_p, n_s = basis.n_modes, rm.n_ports, rm.n_sources
+        self._n, self._n_p, self._n_s = n, n_p, n_s
+        # host copies kept for API compatibility (transient.py:276-286)
+        den = basis.l_n + self.dt * self.theta * basis.r_n
+        self._c = np.sqrt(den)
+        self._rn = basis.r_n.copy()
+        ctx = nat.context()
+        lib = nat.load_library()
+        nd = 2 * n_p + n_s
+        if nd:
+            drv = np.concatenate([rm.r_d.reshape(n, n_p), rm.l_d.reshape(n, n_p),
+                                  rm.m0.reshape(n, n_s)], axis=1)
+            ddrv = nat.device_colmajor(drv)
+            proj = nat.empty(nd, n)      # V^T [R_D | L_D | M0], column-major n x nd
+            nat.check(lib.em_dgemm(ctx, 1, 0, n, nd, n, 1.0, nat.ptr(basis.v_dev), n,
+                                   nat.ptr(ddrv), n, 0.0, nat.ptr(proj), n), "em_dgemm")
+        else:
+            proj = nat.zeros(1, n)
+        self._proj = proj
+        p_r = proj[0:n_p] if n_p else proj[0:1]
+        p_l = proj[n_p:2 * n_p] if n_p else proj[0:1]
+        p_m = proj[2 * n_p:] if n_s else proj[0:1]
+        self._ln_dev = nat.device_vector(basis.l_n)
+        self._rn_dev = nat.device_vector(basis.r_n)
+        plan = ctypes.c_void_p()
+        nat.check(lib.em_td2_plan_create(ctx, n, n_p, n_s, nat.ptr(self._ln_dev),
+                                         nat.ptr(self._rn_dev), nat.ptr(p_r), nat.ptr(p_l),
+                                         nat.ptr(p_m), self.dt, self.theta, ctypes.byref(plan)),
+                  "em_td2_plan_create")
+        self._plan = plan
+        self.setup_time = time.perf_counter() - t0
+
+    def __del__(self):
+        plan = getattr(self, "_plan", None)
+        if plan:
+            nat.load_library().em_td2_plan_destroy(plan)
+            self._plan = None
+
+    @property
+    def _p_r(self):
+        return nat.host_colmajor(self._proj[0:self._n_p], self._n, self._n_p)
+
+    @property
+    def _p_m(self):
+        return nat.host_colmajor(self._proj[2 * self._n_p:], self._n, self._n_s)
+
+    def forcing(self, i_d, delta_i_d, delta_i0) -> np.ndarray:
+        """-dt P_r i_D - P_ltr dI_D - P_m dI_0 (transient.py:289-297), on the device."""
+        f = nat.empty(self._n)
+        u = [np.ascontiguousarray(np.asarray(x, dtype=float)) for x in (i_d, delta_i_d, delta_i0)]
+        ptrs = [x.ctypes.data_as(ctypes.c_void_p) for x in u]
+        nat.check(nat.load_library().em_td2_forcing(self._plan, *ptrs, nat.ptr(f)),
+                  "em_td2_forcing")
+        return f.cpu().numpy()
+
+    def step(self, modal_state: np.ndarray, i_d, delta_i_d, delta_i0) -> np.ndarray:
+        """Advance one step in place (transient.py:299-308)."""
+        n = self._n
+        if modal_state.shape != (n,):
+            raise DimensionMismatch(f"modal state must have {n} components")
+        if n == 0:
+            return modal_state
+        q = nat.device_vector(modal_state)
+        u = [np.ascontiguousarray(np.asarray(x, dtype=float)) for x in (i_d, delta_i_d, delta_i0)]
+        ptrs = [x.ctypes.data_as(ctypes.c_void_p) for x in u]
+        nat.check(nat.load_library().em_td2_step(self._plan, nat.ptr(q), *ptrs), "em_td2_step")
+        modal_state[:] = q.cpu().numpy()
+        return modal_state
+
+    def set_observables(self, observables):
+        n_obs, cdev, ddev = _obs_device(observables, self._n, self._n_p)
+        ctx = nat.context()
+        cv = nat.empty(self._n, n_obs)  # C V column-major n_obs x n
+        nat.check(nat.load_library().em_dgemm(ctx, 0, 0, n_obs, self._n, self._n, 1.0,
+                                               nat.ptr(cdev), n_obs, nat.ptr(self.basis.v_dev),
+                                               self._n, 0.0, nat.ptr(cv), n_obs), "em_dgemm")
+        nat.check(nat.load_library().em_td2_set_observables(
+            self._plan, n_obs, nat.ptr(cv), n_obs, nat.ptr(ddev), n_obs), "em_td2_set_observables")
+        self._n_obs = n_obs
+
+    def run_device(self, drive_dev, steps: int, q_dev, capture_stride: int = 1,
+                   capture_state: bool = False, want_obs: bool = True):
+        """Batched device run over a device drive table ((steps+1) x (n_p+n_s)).
+        Returns (Y device (n_caps, n_obs) or None, Qcap device (n_caps, N) or None)."""
+        n_caps = steps // capture_stride
+        y = nat.empty(n_caps, self._n_obs) if (want_obs and getattr(self, "_n_obs", 0)) else None
+        qcap = nat.empty(n_caps, self._n) if capture_state else None
+        nat.check(nat.load_library().em_td2_run(self._plan, steps, nat.ptr(drive_dev),
+                                                 nat.ptr(q_dev), nat.ptr(y), capture_stride,
+                                                 nat.ptr(qcap)), "em_td2_run")
+        return y, qcap
+
+    def run(self, i_d_samples, i0_samples, capture_stride: int = 1, capture_state: bool = True,
+            observables=None, modal_state0=None):
+        """Integrate over a sample table (rows t_0..t_T) from rest (or modal_state0).
+        Returns (internal_states (n_caps, N) or None, observables or None, final q)."""
+        table = _drive_table(i_d_samples, i0_samples, self._n_p, self._n_s) \
+            if (self._n_p or self._n_s) else np.zeros((np.asarray(i_d_samples).shape[0], 0))
+        steps = table.shape[0] - 1
+        if observables is not None:
+            self.set_observables(observables)
+        drive = nat.device_vector(table.reshape(-1)) if table.size else nat.zeros(1)
+        q = nat.device_vector(np.zeros(self._n) if modal_state0 is None else modal_state0)
+        y, qcap = self.run_device(drive, steps, q, capture_stride, capture_state,
+                                  observables is not None)
+        states = None
+        if qcap is not None:
+            states = _reconstruct(self.basis, qcap, qcap.shape[0])
+        return states, (y.cpu().numpy() if y is not None else None), q.cpu().numpy()
+
+
+def _reconstruct(basis: ModalBasis, qcap, n_caps: int) -> np.ndarray:
+    """internal states I = V Q for captured modal states (n_caps x N host)."""
+    n = basis.n_modes
+    if n_caps == 0:
+        return np.zeros((0, n))
+    ctx = nat.context()
+    out = nat.empty(n_caps, n)
+    nat.check(nat.load_library().em_dgemm(ctx, 0, 0, n, n_caps, n, 1.0, nat.ptr(basis.v_dev), n,
+                                           nat.ptr(qcap), n, 0.0, nat.ptr(out), n), "em_dgemm")
+    return out.cpu().numpy()
+
+
+class Td1Stepper:
+    """Coupled stepper (transient.py:219-255): Cholesky factor of L_i + dt theta R_i."""
+
+    def __init__(self, rm: ReducedModel, dt: float, theta: float):
+        _check_theta_dt(dt, theta)
+        t0 = time.perf_counter()
+        self.rm = rm
+        self.dt = float(dt)
+        self.theta = float(theta)
+        n, n_p, n_s = rm.n_internal, rm.n_ports, rm.n_sources
+        self._n, self._n_p, self._n_s = n, n_p, n_s
+        self._chol = None
+        self._plan = None
+        if n:
+            ctx = nat.context()
+            lib = nat.load_library()
+            ld = nat.device_colmajor(rm.l_i.full)
+            rd = nat.device_colmajor(rm.r_i.full)
+            dr = nat.device_colmajor(rm.r_d.reshape(n, n_p)) if n_p else nat.zeros(1)
+            dl = nat.device_colmajor(rm.l_d.reshape(n, n_p)) if n_p else nat.zeros(1)
+            dm = nat.device_colmajor(rm.m0.reshape(n, n_s)) if n_s else nat.zeros(1)
+            plan = ctypes.c_void_p()
+            piv = ctypes.c_int64(-1)
+            rc = lib.em_td1_plan_create(ctx, n, n_p, n_s, nat.ptr(ld), n, nat.ptr(rd), n,
+                                        nat.ptr(dr), nat.ptr(dl), nat.ptr(dm), self.dt,
+                                        self.theta, ctypes.byref(plan), ctypes.byref(piv))
+            if rc == nat.EM_ERR_NOT_PD:
+                raise NotPositiveDefinite(int(piv.value), "stepping matrix")
+            nat.check(rc, "em_td1_plan_create")
+            self._plan = plan
+        self.setup_time = time.perf_counter() - t0
+
+    def __del__(self):
+        plan = getattr(self, "_plan", None)
+        if plan:
+            nat.load_library().em_td1_plan_destroy(plan)
+            self._plan = None
+
+    @property
+    def chol(self) -> linalg.LowerTriangular | None:
+        """The stepping-matrix factor (transient.py:237), copied from the device."""
+        if self._plan is None:
+            return None
+        if self._chol is None:
+            out = nat.empty(self._n, self._n)
+            nat.check(nat.load_library().em_td1_factor(self._plan, nat.ptr(out), self._n),
+                      "em_td1_factor")
+            self._chol = linalg.LowerTriangular(nat.host_colmajor(out, self._n, self._n))
+        return self._chol
+
+    def step(self, state: np.ndarray, i_d, delta_i_d, delta_i0) -> np.ndarray:
+        """Advance one step in place and return the state (transient.py:244-255)."""
+        n = self._n
+        if state.shape != (n,):
+            raise DimensionMismatch(f"state must have {n} components")
+        if n == 0:
+            return state
+        s = nat.device_vector(state)
+        u = [np.ascontiguousarray(np.asarray(x, dtype=float)) for x in (i_d, delta_i_d, delta_i0)]
+        ptrs = [x.ctypes.data_as(ctypes.c_void_p) for x in u]
+        nat.check(nat.load_library().em_td1_step(self._plan, nat.ptr(s), *ptrs), "em_td1_step")
+        state[:] = s.cpu().numpy()
+        return state
+
+    def set_observables(self, observables):
+        n_obs, cdev, ddev = _obs_device(observables, self._n, self._n_p)
+        nat.check(nat.load_library().em_td1_set_observables(
+            self._plan, n_obs, nat.ptr(cdev), n_obs, nat.ptr(ddev), n_obs), "em_td1_set_observables")
+        self._n_obs = n_obs
+
+    def run_device(self, drive_dev, steps: int, i_dev, capture_stride: int = 1,
+                   capture_state: bool = False, want_obs: bool = True):
+        n_caps = steps // capture_stride
+        y = nat.empty(n_caps, self._n_obs) if (want_obs and getattr(self, "_n_obs", 0)) else None
+        icap = nat.empty(n_caps, self._n) if capture_state else None
+        nat.check(nat.load_library().em_td1_run(self._plan, steps, nat.ptr(drive_dev),
+                                                 nat.ptr(i_dev), nat.ptr(y), capture_stride,
+                                                 nat.ptr(icap)), "em_td1_run")
+        return y, icap
+
+    def run(self, i_d_samples, i0_samples, capture_stride: int = 1, capture_state: bool = True,
+            observables=None, state0=None):
+        table = _drive_table(i_d_samples, i0_samples, self._n_p, self._n_s) \
+            if (self._n_p or self._n_s) else np.zeros((np.asarray(i_d_samples).shape[0], 0))
+        steps = table.shape[0] - 1
+        if observables is not None:
+            self.set_observables(observables)
+        drive = nat.device_vector(table.reshape(-1)) if table.size else nat.zeros(1)
+        s = nat.device_vector(np.zeros(self._n) if state0 is None else state0)
+        y, icap = self.run_device(drive, steps, s, capture_stride, capture_state,
+                                  observables is not None)
+        states = icap.cpu().numpy() if icap is not None else None
+        return states, (y.cpu().numpy() if y is not None else None), s.cpu().numpy()
+
+
+def prepare_td1(rm: ReducedModel, cfg: TransientConfig) -> Td1Stepper:
+    return Td1Stepper(rm, cfg.dt, cfg.theta)
+
+
+def step_td1(stepper: Td1Stepper, state, i_d, delta_i_d, delta_i0) -> np.ndarray:
+    """Functional wrapper over Td1Stepper.step (transient.py:315-320)."""
+    return stepper.step(np.asarray(state, dtype=float), np.asarray(i_d, dtype=float),
+                        np.asarray(delta_i_d, dtype=float), np.asarray(delta_i0, dtype=float))
+
+
+def prepare_td2(rm: ReducedModel, basis: ModalBasis, cfg: TransientConfig) -> Td2Stepper:
+    return Td2Stepper(rm, basis, cfg.dt, cfg.theta)
+
+
+def step_td2(stepper: Td2Stepper, modal_state, forcing) -> np.ndarray:
+    """Advance modal coordinates one step with a precomputed forcing (transient.py:327-337)."""
+    modal_state = np.asarray(modal_state, dtype=float)
+    forcing = np.asarray(forcing, dtype=float)
+    if forcing.shape != modal_state.shape:
+        raise DimensionMismatch("forcing and state sizes differ")
+    if modal_state.shape[0]:
+        q = nat.device_vector(modal_state)
+        f = nat.device_vector(forcing)
+        nat.check(nat.load_library().em_td2_step_forcing(stepper._plan, nat.ptr(q), nat.ptr(f)),
+                  "em_td2_step_forcing")
+        modal_state[:] = q.cpu().numpy()
+    return modal_state
+
+
+def _drive_channels(net, rm: ReducedModel, drives):
+    """Port/source name order and per-channel tone lists (transient.py:340-361)."""
+    if net is not None:
+        port_names = [el.name for el in net.electrodes[:-1]] if net.n_electrodes else []
+        source_names = [c.name for c in net.sources if c.port is None]
+    else:
+        port_names = list(rm.port_names) or [str(i) for i in range(rm.n_ports)]
+        source_names = list(rm.source_names) or [str(i) for i in range(rm.n_sources)]
+    if len(port_names) != rm.n_ports or len(source_names) != rm.n_sources:
+        raise DimensionMismatch("network and reduced model disagree on ports/sources")
+    port_tones: list[list] = [[] for _ in port_names]
+    source_tones: list[list] = [[] for _ in source_names]
+    for d in drives:
+        for p in d.ports:
+            if p not in port_names:
+                raise ValidationError(f"drive references unknown port {p!r}")
+            port_tones[port_names.index(p)].extend(d.tones)
+        for s in d.sources:
+            if s not in source_names:
+                raise ValidationError(f"drive references unknown source {s!r}")
+            source_tones[source_names.index(s)].extend(d.tones)
+    return port_tones, source_tones
+
+
+def _sample_channels(tone_lists, t: np.ndarray) -> np.ndarray:
+    """Per-channel multisine samples at times t, (len(t), n_ch); per channel the
+    tones are accumulated in order from 0.0 like np.add.at in transient.py:379-383."""
+    out = np.zeros((t.shape[0], len(tone_lists)))
+    for ch, tones in enumerate(tone_lists):
+        for tone in tones:
+            out[:, ch] += tone.amplitude * np.sin((2 * np.pi * tone.frequency) * t + tone.phase)
+    return out
+
+
+def drive_samples(net, rm: ReducedModel, drives, dt: float, n_steps: int):
+    """The sample table run_transient steps through: t_0 = 0, t_{k+1} = (k+1) dt."""
+    if isinstance(drives, DriveSignal):
+        drives = (drives,)
+    port_tones, source_tones = _drive_channels(net, rm, drives)
+    t = np.concatenate([[0.0], np.arange(1, n_steps + 1, dtype=float) * dt])
+    return _sample_channels(port_tones, t), _sample_channels(source_tones, t)
+
+
+def run_transient(rm: ReducedModel, net, drives, cfg: TransientConfig,
+                  modal: ModalBasis | None = None, observables=None) -> SimulationResult:
+    """Integrate from rest, capture every capture_stride steps (transient.py:390-454).
+
+    observables: optional (C, D) with C (n_obs x N) and D (n_obs x n_ports) or None;
+    captured values are C I + D i_D(t_{k+1}) for each capture."""
+    if isinstance(drives, DriveSignal):
+        drives = (drives,)
+    if cfg.method == "td2" and modal is None:
+        raise ValidationError("td2 requires a modal basis")
+    if cfg.probes is not None:
+        raise ValidationError("probe observers need the filament-network field transfer "
+                              "(assembly.field_transfer), which is outside this path; pass "
+                              "observables=(C, D) instead")
+    n_steps = cfg.n_steps
+    i_d_tab, i0_tab = drive_samples(net, rm, drives, cfg.dt, n_steps)
+    n_caps = n_steps // cfg.capture_stride
+    times = cfg.dt * cfg.capture_stride * np.arange(1, n_caps + 1)
+
+    setup0 = time.perf_counter()
+    if cfg.method == "td1":
+        stepper = Td1Stepper(rm, cfg.dt, cfg.theta)
+    else:
+        stepper = Td2Stepper(rm, modal, cfg.dt, cfg.theta)
+    nat.synchronize()
+    setup_time = time.perf_counter() - setup0
+
+    if rm.n_internal == 0:
+        states = np.zeros((n_caps, 0)) if cfg.capture_state else None
+        return SimulationResult(times, states, None, setup_time, 0.0, n_steps, cfg.method)
+    step0 = time.perf_counter()
+    states, obs, _ = stepper.run(i_d_tab, i0_tab, cfg.capture_stride, cfg.capture_state,
+                                 observables)
+    nat.synchronize()
+    stepping_time = time.perf_counter() - step0
+    return SimulationResult(times=times, internal_states=states, probe_fields=None,
+                            wall_time_setup=setup_time, wall_time_stepping=stepping_time,
+                            n_steps=n_steps, method=cfg.method, observables=obs)
+
+
+def exact_first_order(l_n: np.ndarray, r_n: np.ndarray, y0: np.ndarray,
+                      e0: np.ndarray, slope: np.ndarray, h: float) -> np.ndarray:
+    """Closed-form step of l y' + r y = e0 + slope t (transient.py:494-502).
+    Validation reference (host arithmetic, as in the reference)."""
+    tau = l_n / r_n
+    yp0 = (e0 - slope * tau) / r_n
+    yph = (e0 + slope * h - slope * tau) / r_n
+    return yph + (y0 - yp0) * np.exp(-h / tau)
+
+
+def exact_modal_reference(basis: ModalBasis, rm: ReducedModel, i_d_samples, i0_samples,
+                          times, modal_state0=None) -> np.ndarray:
+    """Exact per-interval integration for piecewise-linear drives (transient.py:457-491);
+    a validation reference for the theta-convergence checks."""
+    times = np.asarray(times, dtype=float)
+    n_t = times.shape[0]
+    n = basis.n_modes
+    i_d_samples = np.asarray(i_d_samples, dtype=float).reshape(n_t, rm.n_ports)
+    i0_samples = np.asarray(i0_samples, dtype=float).reshape(n_t, rm.n_sources)
+    vt = basis.v.T
+    p_r = vt @ rm.r_d if rm.n_ports else np.zeros((n, 0))
+    p_l = vt @ rm.l_d if rm.n_ports else np.zeros((n, 0))
+    p_m = vt @ rm.m0 if rm.n_sources else np.zeros((n, 0))
+    out = np.zeros((n_t, n))
+    state = np.zeros(n) if modal_state0 is None else np.asarray(modal_state0, float).copy()
+    out[0] = state
+    for k in range(n_t - 1):
+        h = times[k + 1] - times[k]
+        di_d = (i_d_samples[k + 1] - i_d_samples[k]) / h
+        di_0 = (i0_samples[k + 1] - i0_samples[k]) / h
+        e0 = -(p_r @ i_d_samples[k]) - (p_l @ di_d) - (p_m @ di_0)
+        s = -(p_r @ di_d)
+        state = exact_first_order(basis.l_n, basis.r_n, state, e0, s, h)
+        out[k + 1] = state
+    return out
+
+
+# --- CSV export (transient.py:505-546) -----------------------------------------------
+
+def write_timeseries_csv(path, result: SimulationResult, header_lines: tuple[str, ...] = ()):
+    if result.probe_fields is None:
+        raise ValidationError("result holds no probe fields")
+    with open(path, "w") as fh:
+        for line in header_lines:
+            fh.write(f"# {line}\n")
+        fh.write("t,probe_id,Bx,By,Bz\n")
+        for it, t in enumerate(result.times):
+            for p in range(result.probe_fields.shape[1]):
+                bx, by, bz = (float(v) for v in result.probe_fields[it, p])
+                fh.write(f"{float(t)!r},{p},{bx!r},{by!r},{bz!r}\n")
+
+
+def write_states_csv(path, result: SimulationResult, header_lines: tuple[str, ...] = ()):
+    if result.internal_states is None:
+        raise ValidationError("result holds no internal states")
+    n = result.internal_states.shape[1]
+    with open(path, "w") as fh:
+        for line in header_lines:
+            fh.write(f"# {line}\n")
+        fh.write("t," + ",".join(f"i{j}" for j in range(n)) + "\n")
+        for it, t in enumerate(result.times):
+            row = ",".join(repr(float(v)) for v in result.internal_states[it])
+            fh.write(f"{float(t)!r},{row}\n")
+
+
+def write_timing_csv(path, results: list[SimulationResult], header_lines: tuple[str, ...] = ()):
+    with open(path, "w") as fh:
+        for line in header_lines:
+            fh.write(f"# {line}\n")
+        fh.write("method,setup_s,stepping_s,steps,per_step_s\n")
+        for r in results:
+            fh.write(f"{r.method},{r.wall_time_setup!r},{r.wall_time_stepping!r},"
+                     f"{r.n_steps},{r.per_step_cost!r}\n")

@@ -1,0 +1,185 @@
+"""Device time stepping vs the reference trajectories (golden fixtures from the
+unmodified reference run_transient) — north-star tolerance 1e-8 relative L2
+for observables and current densities — plus the SPEC acceptance properties the
+reference suite never tested (TD1 == TD2, theta convergence)."""
+import os
+
+import numpy as np
+import pytest
+
+from tests.conftest import GOLDEN, golden, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-8  # north_star: observable waveforms and current densities, relative L2
+
+
+def _plate_rm(g):
+    from paper_2407_11993_b200 import reduction
+    return reduction.from_blocks(g["r_i"], g["l_i"], g["r_d"], g["l_d"], g["m0"],
+                                 port_names=("p0",), source_names=("s0",))
+
+
+def _plate_drives():
+    from paper_2407_11993_b200.network import DriveSignal, Tone
+    return (DriveSignal(tones=(Tone(1.0, 1e4, 0.0),), sources=("s0",)),
+            DriveSignal(tones=(Tone(0.7, 2e4, 0.3), Tone(0.2, 5e4, 1.1)), ports=("p0",)))
+
+
+@pytest.mark.parametrize("name", ["plate_small", "plate_200"])
+@pytest.mark.parametrize("method", ["td2", "td1"])
+def test_run_transient_matches_reference(name, method):
+    from paper_2407_11993_b200 import modal, transient
+    g = golden(name)
+    rm = _plate_rm(g)
+    basis = modal.generalized_eig(rm.l_i, rm.r_i) if method == "td2" else None
+    steps, dt, ke = int(g["steps"]), float(g["dt"]), int(g["keep_every"])
+    for th in g["thetas"]:
+        th = float(th)
+        cfg = transient.TransientConfig(theta=th, dt=dt, t_end=steps * dt, method=method)
+        res = transient.run_transient(rm, None, _plate_drives(), cfg, modal=basis,
+                                      observables=(g["c"], None))
+        assert res.n_steps == steps and res.internal_states.shape == (steps, rm.n_internal)
+        ref_obs = g[f"{method}_obs_theta{th}"]
+        assert rel_l2(res.observables, ref_obs) < TOL
+        assert rel_l2(res.internal_states[ke - 1::ke], g[f"{method}_states_theta{th}"]) < TOL
+        np.testing.assert_allclose(res.times, dt * np.arange(1, steps + 1))
+
+
+@pytest.mark.parametrize("name", ["tube_small", "tube_ref"])
+def test_tube_trajectories_match_reference(name):
+    """Degenerate tube spectrum: V differs by rotations inside clusters, the
+    trajectory I = V q must not."""
+    from paper_2407_11993_b200 import modal, reduction, transient
+    from paper_2407_11993_b200.network import DriveSignal, Tone
+    g = golden(name)
+    rm = reduction.from_blocks(g["r_i"], g["l_i"], g["r_d"], g["l_d"], None, port_names=("p",))
+    basis = modal.generalized_eig(rm.l_i, rm.r_i)
+    dt = float(g["dt"])
+    drive = DriveSignal(tones=(Tone(1.0, 1e3, 0.0),), ports=("p",))
+    for method in ("td2", "td1"):
+        cfg = transient.TransientConfig(theta=1.0, dt=dt, t_end=200 * dt, method=method)
+        res = transient.run_transient(rm, None, drive, cfg,
+                                      modal=basis if method == "td2" else None)
+        assert rel_l2(res.internal_states, g[f"{method}_states"]) < TOL
+
+
+def test_capture_stride_and_state_flags():
+    from paper_2407_11993_b200 import modal, transient
+    g = golden("plate_small")
+    rm = _plate_rm(g)
+    basis = modal.generalized_eig(rm.l_i, rm.r_i)
+    dt = float(g["dt"])
+    full = g["td2_obs_theta0.5"]
+    for stride in (1, 7, 64, 300):
+        cfg = transient.TransientConfig(theta=0.5, dt=dt, t_end=300 * dt, method="td2",
+                                        capture_stride=stride, capture_state=False)
+        res = transient.run_transient(rm, None, _plate_drives(), cfg, modal=basis,
+                                      observables=(g["c"], None))
+        assert res.internal_states is None
+        assert res.observables.shape == (300 // stride, g["c"].shape[0])
+        assert rel_l2(res.observables, full[stride - 1::stride][:300 // stride]) < TOL
+
+
+def test_step_api_matches_oracle_per_step():
+    """Td2Stepper.step / Td1Stepper.step / step_td2 keep the reference's
+    in-place single-step semantics."""
+    from oracle import oracle as O
+    from paper_2407_11993_b200 import modal, transient
+    g = golden("plate_small")
+    rm = _plate_rm(g)
+    basis = modal.generalized_eig(rm.l_i, rm.r_i)
+    ref = O.generalized_eig(rm.l_i.full, rm.r_i.full)
+    dt, th = 1e-6, 0.5
+    s2 = transient.Td2Stepper(rm, basis, dt, th)
+    s1 = transient.Td1Stepper(rm, dt, th)
+    o1 = O.Td1(rm.l_i.full, rm.r_i.full, g["r_d"], g["l_d"], g["m0"], dt, th)
+    q = np.zeros(rm.n_internal)
+    i1 = np.zeros(rm.n_internal)
+    i1_ref = np.zeros(rm.n_internal)
+    rng = np.random.default_rng(5)
+    for _ in range(20):
+        u = rng.standard_normal(3)
+        out = s2.step(q, u[:1], u[1:2], u[2:])
+        assert out is q
+        s1.step(i1, u[:1], u[1:2], u[2:])
+        o1.step(i1_ref, u[:1], u[1:2], u[2:])
+    assert rel_l2(basis.v @ q, i1_ref) < 1e-10
+    assert rel_l2(i1, i1_ref) < 1e-10
+    from paper_2407_11993_b200.modal import drive_rhs
+    f = s2.forcing(np.ones(1), np.ones(1), np.ones(1))
+    f_ref = basis.v.T @ drive_rhs(rm, np.ones(1), np.ones(1), np.ones(1), dt, th)
+    assert rel_l2(f, f_ref) < 1e-10
+    o2 = O.Td2(ref, g["r_d"], g["l_d"], g["m0"], dt, th)
+    q2 = q.copy()
+    transient.step_td2(s2, q2, f)
+    q3 = q.copy()
+    s2.step(q3, np.ones(1), np.ones(1), np.ones(1))
+    assert rel_l2(q2, q3) < 1e-14
+    c = s1.chol.c
+    z = rm.l_i.full + dt * th * rm.r_i.full
+    assert np.linalg.norm(c @ c.T - z) <= 1e-12 * np.linalg.norm(z)
+    assert o2 is not None
+
+
+def test_td1_equals_td2_long_horizon():
+    """SPEC acceptance #1: TD1 == TD2 to < 1e-8 over 10^4 steps."""
+    from paper_2407_11993_b200 import modal, transient
+    g = golden("plate_200")
+    rm = _plate_rm(g)
+    basis = modal.generalized_eig(rm.l_i, rm.r_i)
+    i_d, i0 = transient.drive_samples(None, rm, _plate_drives(), 1e-6, 10000)
+    c = g["c"]
+    _, y2, _ = transient.Td2Stepper(rm, basis, 1e-6, 0.5).run(i_d, i0, capture_state=False,
+                                                               observables=(c, None))
+    _, y1, _ = transient.Td1Stepper(rm, 1e-6, 0.5).run(i_d, i0, capture_state=False,
+                                                        observables=(c, None))
+    assert rel_l2(y2, y1) < 1e-8
+
+
+def test_theta_convergence_orders():
+    """SPEC acceptance #3: dt halving error ratios ~2 (theta=1) and
+    ~4 (theta=0.5) against the exact modal integrator, moderate dt/tau."""
+    from paper_2407_11993_b200 import modal, reduction, transient
+    g = golden("plate_small")
+    # scale R so dt/tau is moderate (the exact oracle's cancellation floor)
+    rm = reduction.from_blocks(g["r_i"] * 2e3, g["l_i"], g["r_d"] * 2e3, g["l_d"], g["m0"],
+                               port_names=("p0",), source_names=("s0",))
+    basis = modal.generalized_eig(rm.l_i, rm.r_i)
+    t_end = 4e-4
+
+    def final_state(theta, dt):
+        n = int(round(t_end / dt))
+        i_d, i0 = transient.drive_samples(None, rm, _plate_drives(), dt, n)
+        _, _, q = transient.Td2Stepper(rm, basis, dt, theta).run(i_d, i0, capture_state=False)
+        return q
+
+    n_ref = 4000
+    i_d, i0 = transient.drive_samples(None, rm, _plate_drives(), t_end / n_ref, n_ref)
+    exact = transient.exact_modal_reference(basis, rm, i_d, i0,
+                                            t_end / n_ref * np.arange(n_ref + 1))[-1]
+    for theta, order in ((1.0, 2.0), (0.5, 4.0)):
+        errs = [np.linalg.norm(final_state(theta, t_end / k) - exact) for k in (50, 100, 200)]
+        r1, r2 = errs[0] / errs[1], errs[1] / errs[2]
+        assert abs(r1 - order) < 0.35 * order and abs(r2 - order) < 0.35 * order, (theta, errs)
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(GOLDEN, "c1.npz")), reason="c1 golden absent")
+def test_c1_full_config_matches_reference():
+    """Config C1 (N=2000, 2000 steps): observables and current densities vs the
+    reference run (Jacobi eigensolve + Td2Stepper / Td1Stepper)."""
+    from paper_2407_11993_b200 import modal, reduction, transient
+    from paper_2407_11993_b200.network import DriveSignal, Tone
+    from paper_2407_11993_b200.synth import plate_model
+    g = golden("c1")
+    m = plate_model(40, 25, 2, n_ports=0, n_sources=1, n_obs=16)
+    rm = reduction.from_blocks(m["r_i"], m["l_i"], None, None, m["m0"], source_names=("s0",))
+    basis = modal.generalized_eig(rm.l_i, rm.r_i)
+    drive = DriveSignal(tones=(Tone(1.0, 1e4, 0.0),), sources=("s0",))
+    for method in ("td2", "td1"):
+        cfg = transient.TransientConfig(theta=0.5, dt=1e-6, t_end=2000e-6, method=method)
+        res = transient.run_transient(rm, None, drive, cfg,
+                                      modal=basis if method == "td2" else None,
+                                      observables=(m["c"], None))
+        assert rel_l2(res.observables, g[f"{method}_obs"]) < TOL
+        assert rel_l2(res.internal_states[499::500], g[f"{method}_states"]) < TOL
