@@ -1,0 +1,536 @@
+#!/usr/bin/env python
+"""Headline benchmark: end-to-end modal transient (generalized eigensolve +
+theta-method stepping) in mode-steps/s — BASELINE.json `metric` on configs[1]
+(C2: N = 16,384 plate 64x64x4, one electrode port with a 5 us current ramp,
+theta = 1 and 0.5, dt = 5e-7 s, 10,000 steps, 32 observables, FP64).
+
+One benchmark STEP = one pass of the hot path over the workload:
+  generalized eigensolve (em_sygv: tau, V, l_n, r_n, V^T R)
+  + for each theta: drive projection, TD2 plan, 10k-step fused scan with the
+    32 observables reconstructed every step.
+mode-steps per step = N * T * n_theta.
+
+value: inputs (L, R, drive table, C) resident in HBM, outputs left on device.
+e2e:   the same through the public Python API with HOST buffers (pinned), H2D of
+       L, R, couplings, drive table and C and D2H of every observable inside the
+       timed region.
+
+python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config C1|C2]
+Multi-GPU (torchrun): the path does not shard in this round -> independent
+replicas, one per GPU (scaling "weak"), value = sum of all ranks' mode-steps / max time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "C1": dict(grid=(40, 25, 2), thetas=(0.5,), dt=1e-6, steps=2000, n_obs=16, n_ports=0,
+               n_sources=1, drive="tone10k"),
+    "C2": dict(grid=(64, 64, 4), thetas=(1.0, 0.5), dt=5e-7, steps=10000, n_obs=32, n_ports=1,
+               n_sources=0, drive="ramp5us"),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "200",
+                 "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm = []
+        mx = None
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx = float(r[1])
+            except ValueError:
+                continue
+            for k, nm in enumerate(names):
+                if r[4 + k].lower().startswith("active"):
+                    reasons.add(nm)
+        loaded = [s for s in sm if mx and s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- workload
+def build_inputs(cfg):
+    from paper_2407_11993_b200 import synth
+    from paper_2407_11993_b200 import _native as nat
+    nx, ny, nz = cfg["grid"]
+    m = synth.device_plate_model(nx, ny, nz, n_ports=cfg["n_ports"], n_sources=cfg["n_sources"],
+                                 n_obs=cfg["n_obs"])
+    i_d, i0 = synth.drive_table(cfg["drive"], cfg["steps"], cfg["dt"], cfg["n_ports"],
+                                cfg["n_sources"])
+    table = np.ascontiguousarray(np.concatenate([i_d, i0], axis=1))
+    m["i_d"], m["i0"], m["table"] = i_d, i0, table
+    m["table_dev"] = nat.device_vector(table.reshape(-1)) if table.size else nat.zeros(1)
+    m["c_dev"] = nat.device_colmajor(m["c"])
+    n = m["plate"].n
+    m["m0_dev"] = nat.device_colmajor(m["m0"]) if cfg["n_sources"] else None
+    return m
+
+
+class DeviceStep:
+    """The hot path on device-resident inputs, straight through the C ABI."""
+
+    def __init__(self, m, cfg):
+        from paper_2407_11993_b200 import _native as nat
+        self.nat = nat
+        self.m = m
+        self.cfg = cfg
+        n = m["plate"].n
+        self.n = n
+        n_p, n_s = cfg["n_ports"], cfg["n_sources"]
+        self.n_p, self.n_s = n_p, n_s
+        self.nd = 2 * n_p + n_s
+        self.tau, self.ln, self.rn = nat.empty(n), nat.empty(n), nat.empty(n)
+        self.V, self.VtR = nat.empty(n, n), nat.empty(n, n)
+        cols = []
+        if n_p:
+            cols += [m["r_d"], m["l_d"]]
+        if n_s:
+            cols += [m["m0_dev"]]
+        t = nat.torch()
+        self.drv = t.cat(cols, dim=0).contiguous() if cols else nat.zeros(1, n)
+        self.P = nat.empty(max(self.nd, 1), n)
+        self.CV = nat.empty(n, cfg["n_obs"])
+        self.Y = [nat.empty(cfg["steps"], cfg["n_obs"]) for _ in cfg["thetas"]]
+        self.q = nat.empty(n)
+
+    def __call__(self):
+        import ctypes
+        nat, lib, ctx = self.nat, self.nat.load_library(), self.nat.context()
+        n, cfg = self.n, self.cfg
+        piv, which = ctypes.c_int64(-1), ctypes.c_int(-1)
+        nat.check(lib.em_sygv(ctx, n, nat.ptr(self.m["l_i"]), n, nat.ptr(self.m["r_i"]), n,
+                              nat.ptr(self.tau), nat.ptr(self.V), n, nat.ptr(self.ln),
+                              nat.ptr(self.rn), nat.ptr(self.VtR), n, ctypes.byref(piv),
+                              ctypes.byref(which)), "em_sygv")
+        if self.nd:
+            nat.check(lib.em_dgemm(ctx, 1, 0, n, self.nd, n, 1.0, nat.ptr(self.V), n,
+                                   nat.ptr(self.drv), n, 0.0, nat.ptr(self.P), n), "em_dgemm")
+        n_obs = cfg["n_obs"]
+        nat.check(lib.em_dgemm(ctx, 0, 0, n_obs, n, n, 1.0, nat.ptr(self.m["c_dev"]), n_obs,
+                               nat.ptr(self.V), n, 0.0, nat.ptr(self.CV), n_obs), "em_dgemm")
+        n_p, n_s = self.n_p, self.n_s
+        p_r = self.P[0:1] if not n_p else self.P[0:n_p]
+        p_l = self.P[0:1] if not n_p else self.P[n_p:2 * n_p]
+        p_m = self.P[0:1] if not n_s else self.P[2 * n_p:]
+        for k, th in enumerate(cfg["thetas"]):
+            plan = ctypes.c_void_p()
+            nat.check(lib.em_td2_plan_create(ctx, n, n_p, n_s, nat.ptr(self.ln), nat.ptr(self.rn),
+                                             nat.ptr(p_r), nat.ptr(p_l), nat.ptr(p_m), cfg["dt"],
+                                             th, ctypes.byref(plan)), "em_td2_plan_create")
+            nat.check(lib.em_td2_set_observables(plan, n_obs, nat.ptr(self.CV), n_obs, None, 0),
+                      "em_td2_set_observables")
+            self.q.zero_()
+            nat.check(lib.em_td2_run(plan, cfg["steps"], nat.ptr(self.m["table_dev"]),
+                                     nat.ptr(self.q), nat.ptr(self.Y[k]), 1, None), "em_td2_run")
+            lib.em_td2_plan_destroy(plan)
+
+
+class E2EStep:
+    """The same work through the public API (reference call shapes) with host buffers."""
+
+    def __init__(self, m, cfg):
+        from paper_2407_11993_b200 import _native as nat
+        from paper_2407_11993_b200 import linalg, reduction
+        t = nat.torch()
+        n = m["plate"].n
+        self.cfg = cfg
+        # host copies of the inputs in pinned memory, wrapped as the reference's types
+        self.pinned = []
+
+        def pinned_sym(dev):
+            h = t.empty(dev.shape, dtype=t.float64, pin_memory=True)
+            h.copy_(dev)
+            self.pinned.append(h)
+            s = linalg.SymMatrix(np.zeros((1, 1)))
+            object.__setattr__(s, "a", h.numpy())      # exactly symmetric already
+            return s
+
+        l_i, r_i = pinned_sym(m["l_i"]), pinned_sym(m["r_i"])
+        r_d = m["r_d"].cpu().numpy().T.copy() if cfg["n_ports"] else None
+        l_d = m["l_d"].cpu().numpy().T.copy() if cfg["n_ports"] else None
+        self.rm = reduction.ReducedModel(
+            r_i=r_i, l_i=l_i,
+            r_d=r_d if r_d is not None else np.zeros((n, 0)),
+            l_d=l_d if l_d is not None else np.zeros((n, 0)),
+            m0=m["m0"], lift=np.zeros((n, cfg["n_ports"])), k=_LazyEye(n),
+            port_names=tuple(f"p{i}" for i in range(cfg["n_ports"])),
+            source_names=tuple(f"s{i}" for i in range(cfg["n_sources"])))
+        self.i_d, self.i0, self.c = m["i_d"], m["i0"], m["c"]
+        n_obs = cfg["n_obs"]
+        self.h2d = 8 * (2 * n * n + n * (2 * cfg["n_ports"] + cfg["n_sources"]) +
+                        len(cfg["thetas"]) * (self.i_d.size + self.i0.size + n_obs * n))
+        self.d2h = 8 * (3 * n + len(cfg["thetas"]) * cfg["steps"] * n_obs)
+        self.out = None
+
+    def __call__(self):
+        from paper_2407_11993_b200 import modal, transient
+        cfg = self.cfg
+        basis = modal.generalized_eig(self.rm.l_i, self.rm.r_i)
+        ys = []
+        for th in cfg["thetas"]:
+            st = transient.Td2Stepper(self.rm, basis, cfg["dt"], th)
+            _, y, _ = st.run(self.i_d, self.i0, capture_state=False, observables=(self.c, None))
+            ys.append(y)
+        self.out = (basis.tau, ys)
+
+
+class _LazyEye:
+    """K = I selector stand-in: only .shape is used on this path (n_internal)."""
+
+    def __init__(self, n):
+        self.shape = (n, n)
+
+
+# --------------------------------------------------------------------------- roofline
+def roofline(stages: dict, n: int, steps: int, n_theta: int, n_obs: int, peaks: dict) -> dict:
+    """Dominant stage of the step with its algorithmic work per launch."""
+    best = max(stages.items(), key=lambda kv: kv[1][0])
+    name, (ms, cnt) = best
+    per_launch_ms = ms / max(cnt, 1)
+    hbm = peaks.get("hbm_gbs", 6550.4)
+    fp64 = peaks.get("fp64_tflops", 37.1)
+    if name in ("sytrd", "sytrd_symv"):
+        # lower-triangle symv over the trailing matrix per column: 8 * sum m^2/2 bytes
+        byts = 8.0 * sum((n - c - 1) ** 2 / 2.0 for c in range(n))
+        if name == "sytrd_symv":
+            byts /= n
+        ach = byts / (per_launch_ms * 1e-3) / 1e9
+        return dict(stage=name, bound="hbm", achieved=ach, peak=hbm, unit="GB/s",
+                    frac=ach / hbm, traffic=None, per_launch_ms=per_launch_ms, launches=cnt)
+    flops = {
+        "potrf_R": n ** 3 / 3, "potrf_L": n ** 3 / 3, "sygst": 2.0 * n ** 3,
+        "stedc": 4.0 / 3.0 * n ** 3, "ormtr": 2.0 * n ** 3, "trsm_back": 1.0 * n ** 3,
+        "post_gemm": 4.0 * n ** 3, "td2_replay": 2.0 * n_obs * n * steps,
+    }.get(name)
+    if flops is None:
+        return dict(stage=name, bound="tensor", achieved=None, peak=fp64, unit="TFLOP/s",
+                    frac=None, traffic=None, per_launch_ms=per_launch_ms, launches=cnt)
+    ach = flops / (per_launch_ms * 1e-3) / 1e12
+    return dict(stage=name, bound="tensor", achieved=ach, peak=fp64, unit="TFLOP/s",
+                frac=ach / fp64, traffic=None, per_launch_ms=per_launch_ms, launches=cnt)
+
+
+def load_peaks():
+    peaks = {}
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        peaks.update(json.load(open(p)))
+    # FP64 DMMA issue peak measured on this pool's B200 (profiles/r01_fp64_peaks.jsonl)
+    peaks.setdefault("fp64_tflops", 37.1)
+    return peaks
+
+
+# --------------------------------------------------------------------------- arms
+def run_ours(args, cfg, rank, world, local_rank):
+    import torch
+    torch.cuda.set_device(local_rank)
+    from paper_2407_11993_b200 import _native as nat
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    nat.context()
+    m = build_inputs(cfg)
+    n = m["plate"].n
+    T, nth = cfg["steps"], len(cfg["thetas"])
+    units = n * T * nth
+    step = DeviceStep(m, cfg)
+    for _ in range(args.warmup):
+        step()
+    nat.synchronize()
+
+    def barrier():
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- timed region (device-resident inputs)
+    nat.profile(True)  # coarse stage events on the launching stream
+    l0 = nat.launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        ev0.record()
+        for _ in range(args.steps):
+            step()
+        ev1.record()
+        barrier()
+    launches = nat.launches() - l0
+    elapsed = ev0.elapsed_time(ev1) / 1e3
+    stages = nat.stage_times()
+    nat.profile(False)
+    t_max = elapsed
+    if dist:
+        tt = torch.tensor([elapsed], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt.item())
+    value = world * units * args.steps / t_max
+
+    # ---- e2e through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        es = E2EStep(m, cfg)
+        es()
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            es()
+        torch.cuda.synchronize()
+        barrier()
+        te = time.perf_counter() - t0
+        if dist:
+            tt = torch.tensor([te], device="cuda", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            te = float(tt.item())
+        e2e = {"value": world * units * args.e2e_steps / te, "unit": "mode-steps/s",
+               "h2d_bytes_per_step": es.h2d, "d2h_bytes_per_step": es.d2h,
+               "ms_per_step": te / args.e2e_steps * 1e3, "steps": args.e2e_steps,
+               "timer": "host wall clock around the public-API calls (includes H2D/D2H)"}
+        del es
+
+    peaks = load_peaks()
+    n_steps_timed = args.steps
+    st_avg = {k: (v[0] / n_steps_timed, v[1] / n_steps_timed) for k, v in stages.items()}
+    # roofline of the dominant top-level stage (per launch = per step here)
+    top = {k: stages[k] for k in ("potrf_R", "sygst", "potrf_L", "sytrd", "stedc", "ormtr",
+                                  "trsm_back", "finalize", "post_gemm", "td2_local",
+                                  "td2_carry", "td2_replay") if k in stages}
+    rl = roofline(top, n, T, nth, cfg["n_obs"], peaks) if top else None
+    if rl and rl["stage"] == "td2_replay":
+        rl["achieved"] = None
+
+    # ---- TD1 comparator (bounded: a few hundred steps, extrapolated) and CPU baseline
+    extra = {}
+    if args.profile_fine:
+        nat.profile(2)
+        step()
+        fine = nat.stage_times()
+        nat.profile(0)
+        log(json.dumps({"fine_stage_ms": {k: [round(v[0], 3), v[1]] for k, v in fine.items()}}))
+    if rank == 0 and not args.no_td1:
+        extra["td1_comparator"] = td1_comparator(m, cfg, args.td1_steps)
+        extra["td1_comparator"]["modal_vs_cholesky_end_to_end"] = (
+            extra["td1_comparator"]["extrapolated_total_s"] / (t_max / args.steps))
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(m, cfg, units)
+    if rank == 0:
+        line = {
+            "metric": "end-to-end transient wall time (eigensolve + steps); mode-steps/sec",
+            "value": value, "unit": "mode-steps/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded plate generator, SURVEY.md §8(d))",
+            "config": {"workload": f"{args.config}: N={n} plate {cfg['grid']}, eigensolve + "
+                                   f"{T} TD2 steps x theta {list(cfg['thetas'])}, "
+                                   f"{cfg['n_obs']} observables",
+                       "N": n, "T": T, "thetas": list(cfg["thetas"]), "n_obs": cfg["n_obs"],
+                       "mode_steps_per_step": units,
+                       "l2": "inputs larger than L2 (L, R 2.1 GB each at C2)",
+                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "roofline": rl,
+            "stage_ms_per_step": {k: round(v[0], 3) for k, v in st_avg.items()},
+            "cpu_baseline": cpu,
+        }
+        line.update(extra)
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def td1_comparator(m, cfg, steps):
+    """GPU Cholesky theta-method on the same inputs (bounded number of steps)."""
+    import ctypes
+    import torch
+    from paper_2407_11993_b200 import _native as nat
+    lib, ctx = nat.load_library(), nat.context()
+    n = m["plate"].n
+    n_p, n_s = cfg["n_ports"], cfg["n_sources"]
+    th = cfg["thetas"][-1]
+    steps = min(steps, cfg["steps"])
+    plan = ctypes.c_void_p()
+    piv = ctypes.c_int64(-1)
+    e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    e0.record()
+    nat.check(lib.em_td1_plan_create(ctx, n, n_p, n_s, nat.ptr(m["l_i"]), n, nat.ptr(m["r_i"]), n,
+                                     nat.ptr(m["r_d"]) if n_p else None,
+                                     nat.ptr(m["l_d"]) if n_p else None,
+                                     nat.ptr(m["m0_dev"]) if n_s else None, cfg["dt"], th,
+                                     ctypes.byref(plan), ctypes.byref(piv)), "em_td1_plan_create")
+    e1.record()
+    nat.check(lib.em_td1_set_observables(plan, cfg["n_obs"], nat.ptr(m["c_dev"]), cfg["n_obs"],
+                                         None, 0), "em_td1_set_observables")
+    state = nat.zeros(n)
+    y = nat.empty(steps, cfg["n_obs"])
+    nat.profile(True)
+    e1b = torch.cuda.Event(enable_timing=True)
+    e1b.record()
+    nat.check(lib.em_td1_run(plan, steps, nat.ptr(m["table_dev"]), nat.ptr(state), nat.ptr(y), 1,
+                             None), "em_td1_run")
+    e2.record()
+    torch.cuda.synchronize()
+    st = nat.stage_times()
+    nat.profile(False)
+    lib.em_td1_plan_destroy(plan)
+    setup = e0.elapsed_time(e1) / 1e3
+    per_step = e1b.elapsed_time(e2) / 1e3 / steps
+    nth = len(cfg["thetas"])
+    total = nth * (setup + per_step * cfg["steps"])
+    fwd = st.get("td1_fwd", (0.0, 1))
+    symv = st.get("td1_symv", (0.0, 1))
+    bwd = st.get("td1_bwd", (0.0, 1))
+    factor_bytes = 8.0 * n * (n + 1) / 2
+    hbm = load_peaks().get("hbm_gbs", 6550.4)
+    return {
+        "method": "td1 (GPU Cholesky theta-method, same inputs)",
+        "setup_s_per_theta": setup, "per_step_ms": per_step * 1e3, "steps_timed": steps,
+        "extrapolated_total_s": total,
+        "modal_vs_cholesky_end_to_end": None,  # filled by the caller
+        "trsv_fwd_GBps": factor_bytes / (fwd[0] / fwd[1] * 1e-3) / 1e9 if fwd[1] else None,
+        "trsv_bwd_GBps": factor_bytes / (bwd[0] / bwd[1] * 1e-3) / 1e9 if bwd[1] else None,
+        "symv_GBps": factor_bytes / (symv[0] / symv[1] * 1e-3) / 1e9 if symv[1] else None,
+        "hbm_peak_GBps": hbm,
+    }
+
+
+def cpu_baseline(m, cfg, units):
+    from oracle import cpu_baseline as cb
+    n = m["plate"].n
+    l_i = m["l_i"].cpu().numpy()
+    r_i = m["r_i"].cpu().numpy()
+    r_d = m["r_d"].cpu().numpy().T.copy() if cfg["n_ports"] else np.zeros((n, 0))
+    l_d = m["l_d"].cpu().numpy().T.copy() if cfg["n_ports"] else np.zeros((n, 0))
+    est = cb.estimate(l_i, r_i, r_d, l_d, m["m0"], cfg["steps"], len(cfg["thetas"]), cfg["dt"])
+    return {"value": units / est["total_s"], "unit": "mode-steps/s", "cores": est["cores"],
+            "kind": "port", "sample": est["sample"], "extrapolated_total_s": est["total_s"],
+            "components_s": est["components"]}
+
+
+def run_reference(args, cfg, rank, world):
+    """--impl reference: the reference algorithm on host cores (oracle port)."""
+    if rank != 0:
+        return
+    from oracle import cpu_baseline as cb
+    from paper_2407_11993_b200 import synth
+    nx, ny, nz = cfg["grid"]
+    mdl = synth.plate_model(nx, ny, nz, n_ports=cfg["n_ports"], n_sources=cfg["n_sources"],
+                            n_obs=cfg["n_obs"])
+    n = mdl["r_i"].shape[0]
+    units = n * cfg["steps"] * len(cfg["thetas"])
+    for _ in range(args.warmup):
+        cb.estimate(mdl["l_i"], mdl["r_i"], mdl["r_d"], mdl["l_d"], mdl["m0"], cfg["steps"],
+                    len(cfg["thetas"]), cfg["dt"], n_sample=256, rotations=4, sample_steps=1)
+    totals = []
+    est = None
+    for _ in range(args.steps):
+        est = cb.estimate(mdl["l_i"], mdl["r_i"], mdl["r_d"], mdl["l_d"], mdl["m0"],
+                          cfg["steps"], len(cfg["thetas"]), cfg["dt"], n_sample=768,
+                          rotations=16, sample_steps=2)
+        totals.append(est["total_s"])
+    t = statistics.median(totals)
+    value = units / t
+    line = {
+        "impl": "reference",
+        "metric": "end-to-end transient wall time (eigensolve + steps); mode-steps/sec",
+        "value": value, "unit": "mode-steps/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded plate generator, SURVEY.md §8(d))",
+        "config": {"workload": f"{args.config}: N={n}, eigensolve + {cfg['steps']} TD2 steps x "
+                               f"theta {list(cfg['thetas'])}", "N": n},
+        "cpu_baseline": {"value": value, "unit": "mode-steps/s", "cores": est["cores"],
+                         "kind": "port", "sample": est["sample"]},
+        "e2e": {"value": value, "unit": "mode-steps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "components_s": est["components"],
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="C2")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--td1-steps", type=int, default=300)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-td1", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--profile-fine", action="store_true",
+                    help="one extra untimed step with per-call stage events (stderr)")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+    run_ours(args, cfg, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

@@ -50,6 +50,13 @@ const char* em_last_error(const em_ctx* ctx);
 /* Number of kernels this library has launched on ctx (for launch accounting). */
 int64_t em_launch_count(const em_ctx* ctx);
 int em_synchronize(em_ctx* ctx);
+/* Stage timers (CUDA events on the context stream). em_profile(ctx, 1) clears and
+ * enables them; em_stage_times fills per-stage milliseconds / event-pair counts
+ * (stage ids: potrf_R, sygst, potrf_L, sytrd, stedc, ormtr, trsm_back, finalize,
+ * post_gemm, td2_local, td2_carry, td2_replay, td1_symv, td1_fwd, td1_bwd,
+ * sytrd_symv, sytrd_syr2k, stedc_gemm, stedc_secular) and returns the stage count. */
+int em_profile(em_ctx* ctx, int enable);
+int em_stage_times(em_ctx* ctx, double* ms, int64_t* counts, int n);
 
 /* --- dense building blocks --------------------------------------------------- */
 
@@ -145,6 +152,15 @@ int em_td1_step(em_td1_plan* plan, double* I, const double* i_d_h, const double*
 /* Copy the lower Cholesky factor of the stepping matrix (n x n, column-major) to out
  * (device). Td1Stepper.chol (transient.py:237). */
 int em_td1_factor(em_td1_plan* plan, double* out, int64_t ldo);
+
+/* --- synthetic plate inputs (BASELINE.json configs; definition in synth.py) ----------- */
+/* Dense L (n x n), dense-stored R = rho*K7 + shift*I, and the one-port electrode
+ * columns l_d, r_d (n) for voxels keep[0..n) of an nx*ny*nz grid (pos: voxel id ->
+ * kept index or -1; ang: seeded in-plane angles). Any output may be NULL. */
+int em_synth_plate(em_ctx* ctx, int64_t nx, int64_t ny, int64_t nz, double h, double rho,
+                   double shift, int64_t n, const int64_t* keep, const int64_t* pos,
+                   const double* ang, double* L, int64_t ldl, double* R, int64_t ldr,
+                   double* l_d, double* r_d);
 
 /* --- end-to-end host-pointer entry (the reference-facing call with HOST buffers) -- */
 

@@ -119,6 +119,46 @@ int64_t orc_jacobi(double* a, double* v, int64_t n, int64_t max_sweeps, double t
   return -1;
 }
 
+/* Timing sample of jacobi_sym_eig: the first `count` rotations of sweep 1 in the
+ * reference's cyclic order (same loop body as orc_jacobi). Used only by bench.py's
+ * CPU baseline to measure the per-rotation cost at large n, where a full solve
+ * would take days; returns the number of rotations performed. */
+int64_t orc_jacobi_rotations(double* a, double* v, int64_t n, int64_t count) {
+  int64_t done = 0;
+  for (int64_t p = 0; p < n - 1 && done < count; ++p)
+    for (int64_t q = p + 1; q < n && done < count; ++q) {
+      double apq = A_(p, q);
+      ++done;
+      if (apq == 0.0) continue;
+      double tau = (A_(q, q) - A_(p, p)) / (2.0 * apq);
+      double t;
+      if (tau >= 0.0)
+        t = 1.0 / (tau + sqrt(1.0 + tau * tau));
+      else
+        t = -1.0 / (-tau + sqrt(1.0 + tau * tau));
+      double cth = 1.0 / sqrt(1.0 + t * t);
+      double sth = t * cth;
+      for (int64_t k = 0; k < n; ++k) {
+        double akp = A_(k, p), akq = A_(k, q);
+        A_(k, p) = cth * akp - sth * akq;
+        A_(k, q) = sth * akp + cth * akq;
+      }
+      for (int64_t k = 0; k < n; ++k) {
+        double apk = A_(p, k), aqk = A_(q, k);
+        A_(p, k) = cth * apk - sth * aqk;
+        A_(q, k) = sth * apk + cth * aqk;
+      }
+      A_(p, q) = 0.0;
+      A_(q, p) = 0.0;
+      for (int64_t k = 0; k < n; ++k) {
+        double vkp = v[k * n + p], vkq = v[k * n + q];
+        v[k * n + p] = cth * vkp - sth * vkq;
+        v[k * n + q] = sth * vkp + cth * vkq;
+      }
+    }
+  return done;
+}
+
 /* _kernels.py:198-210  td1_step_kernel. b, y, x are scratch of length n. */
 void orc_td1_step(const double* c, const double* r, double* state, double dt, const double* extra,
                   double* b, double* y, double* x, int64_t n) {

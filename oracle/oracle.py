@@ -68,6 +68,8 @@ def lib():
         _lib.orc_tri_lower_t_solve_mat.argtypes = [d, d, i64, i64]
         _lib.orc_jacobi.argtypes = [d, d, i64, i64, ctypes.c_double]
         _lib.orc_jacobi.restype = i64
+        _lib.orc_jacobi_rotations.argtypes = [d, d, i64, i64]
+        _lib.orc_jacobi_rotations.restype = i64
         _lib.orc_td1_step.argtypes = [d, d, d, ctypes.c_double, d, d, d, d, i64]
         _lib.orc_td2_step.argtypes = [d, d, d, ctypes.c_double, d, i64]
     return _lib

@@ -33,6 +33,8 @@ SIGNATURES = {
     "em_last_error": (ctypes.c_char_p, [_P]),
     "em_launch_count": (_I64, [_P]),
     "em_synchronize": (_I, [_P]),
+    "em_profile": (_I, [_P, _I]),
+    "em_stage_times": (_I, [_P, _P, _P, _I]),
     "em_dgemm": (_I, [_P, _I, _I, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D, _P, _I64]),
     "em_sym_mirror_lower": (_I, [_P, _I64, _P, _I64]),
     "em_potrf": (_I, [_P, _I64, _P, _I64, ctypes.POINTER(_I64)]),
@@ -56,6 +58,8 @@ SIGNATURES = {
     "em_td1_run": (_I, [_P, _I64, _P, _P, _P, _I64, _P]),
     "em_td1_step": (_I, [_P, _P, _P, _P, _P]),
     "em_td1_factor": (_I, [_P, _P, _I64]),
+    "em_synth_plate": (_I, [_P, _I64, _I64, _I64, _D, _D, _D, _I64, _P, _P, _P, _P, _I64, _P,
+                            _I64, _P, _P]),
 }
 
 _lib = None
@@ -118,6 +122,27 @@ def launches() -> int:
     return int(load_library().em_launch_count(_ctx))
 
 
+STAGES = ("potrf_R", "sygst", "potrf_L", "sytrd", "stedc", "ormtr", "trsm_back", "finalize",
+          "post_gemm", "td2_local", "td2_carry", "td2_replay", "td1_symv", "td1_fwd", "td1_bwd",
+          "sytrd_symv", "sytrd_syr2k", "stedc_gemm", "stedc_secular")
+
+
+def profile(level: int = 1) -> None:
+    """0 off, 1 top-level stages, 2 also per-call inner stages (sytrd symv, D&C GEMMs)."""
+    check(load_library().em_profile(context(), int(level)), "em_profile")
+
+
+def stage_times() -> dict:
+    """{stage: (milliseconds, event pairs)} accumulated since profile(True)."""
+    n = len(STAGES)
+    ms = (ctypes.c_double * n)()
+    cnt = (ctypes.c_int64 * n)()
+    rc = load_library().em_stage_times(context(), ms, cnt, n)
+    if rc < 0:
+        check(rc, "em_stage_times")
+    return {STAGES[i]: (ms[i], cnt[i]) for i in range(n) if cnt[i]}
+
+
 def synchronize() -> None:
     torch().cuda.current_stream().synchronize()
 
@@ -133,6 +158,13 @@ def device_colmajor(a: np.ndarray):
     if a.ndim == 1:
         a = a[:, None]
     return t.from_numpy(np.ascontiguousarray(a.T)).to("cuda")
+
+
+def device_symmetric(a: np.ndarray):
+    """Upload an EXACTLY symmetric host matrix (e.g. SymMatrix.full): its row-major
+    bytes are its column-major bytes, so no host transpose copy is made."""
+    t = torch()
+    return t.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to("cuda")
 
 
 def device_vector(x: np.ndarray):

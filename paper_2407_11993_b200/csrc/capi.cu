@@ -14,6 +14,9 @@ struct em_td2_plan;
 struct em_td1_plan;
 
 namespace em {
+void stages_reset(bool on);
+void stages_level(int level);
+int stages_read(double* ms, int64_t* counts, int n);
 int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const double* R,
              int64_t ldr, double* tau, double* V, int64_t ldv, double* l_n, double* r_n,
              double* VtR, int64_t ldvtr, int* which);
@@ -103,6 +106,22 @@ int em_set_stream(em_ctx* ctx, void* s) {
 const char* em_last_error(const em_ctx* ctx) { return ctx ? ctx->err.c_str() : "no context"; }
 
 int64_t em_launch_count(const em_ctx*) { return em::g_launches.load(); }
+
+int em_profile(em_ctx* ctx, int enable) {
+  return guarded(ctx, [&] {
+    EM_CK(cudaStreamSynchronize(ctx->stream));
+    em::stages_reset(enable != 0);
+    em::stages_level(enable);
+    return EM_OK;
+  });
+}
+
+int em_stage_times(em_ctx* ctx, double* ms, int64_t* counts, int n) {
+  return guarded(ctx, [&] {
+    EM_CK(cudaStreamSynchronize(ctx->stream));
+    return em::stages_read(ms, counts, n);
+  });
+}
 
 int em_synchronize(em_ctx* ctx) {
   return guarded(ctx, [&] {

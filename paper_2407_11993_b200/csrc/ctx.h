@@ -82,6 +82,23 @@ struct DArr {
   DArr& operator=(const DArr&) = delete;
 };
 
+// --- stage timers (CUDA events on the launching stream; profiling mode only) ---
+enum StageId {
+  ST_POTRF_R = 0, ST_SYGST, ST_POTRF_L, ST_SYTRD, ST_STEDC, ST_ORMTR, ST_TRSM_BACK,
+  ST_FINALIZE, ST_POST_GEMM, ST_TD2_LOCAL, ST_TD2_CARRY, ST_TD2_REPLAY, ST_TD1_SYMV,
+  ST_TD1_FWD, ST_TD1_BWD, ST_SYTRD_SYMV, ST_SYTRD_SYR2K, ST_STEDC_GEMM, ST_STEDC_SECULAR,
+  ST_COUNT
+};
+void stage_begin(cudaStream_t st, int id);
+void stage_end(cudaStream_t st, int id);
+bool stages_enabled();
+struct Stage {
+  cudaStream_t st;
+  int id;
+  Stage(cudaStream_t s, int i) : st(s), id(i) { stage_begin(st, id); }
+  ~Stage() { stage_end(st, id); }
+};
+
 // --- small utility kernels (util.cu) ---------------------------------------
 void mirror_lower(cudaStream_t st, int64_t n, double* A, int64_t lda);
 // B = op(A) (m x n result), op = transpose when trans

@@ -684,8 +684,10 @@ void stedc(cudaStream_t st, int64_t n, double* d, double* e, double* Z, int64_t 
     }
     if (maxK > 0) {
       dim3 g1((unsigned)((maxK + 127) / 128), (unsigned)nm);
+      stage_begin(st, ST_STEDC_SECULAR);
       dc_secular_kernel<<<g1, 128, 0, st>>>(dmo.p, minfo.p, mrho.p, w);
       EM_LAUNCHED();
+      stage_end(st, ST_STEDC_SECULAR);
       dc_zhat_kernel<<<g1, 128, 0, st>>>(dmo.p, minfo.p, w);
       EM_LAUNCHED();
       dim3 g2((unsigned)((maxK + 7) / 8), (unsigned)nm);
@@ -717,6 +719,7 @@ void stedc(cudaStream_t st, int64_t n, double* d, double* e, double* Z, int64_t 
       EM_CK(cudaMemcpyAsync(dp.p, probs.data(), probs.size() * sizeof(GemmArgs),
                             cudaMemcpyHostToDevice, st));
       const int grid_x = std::min(max_tiles, 4 * num_sms());
+      Stage sg(st, ST_STEDC_GEMM);
       EM_CK(gemm_grouped(st, false, false, dp.p, (int)probs.size(), grid_x));
       EM_CK(cudaStreamSynchronize(st));  // dp lifetime
     }

@@ -17,9 +17,18 @@ void syev_ascending(cudaStream_t st, int64_t n, double* A, int64_t lda, double* 
                     int64_t ldz) {
   if (n <= 0) return;
   DBuf d(n, st), e(imax64(n - 1, 1), st), tau(imax64(n - 1, 1), st);
-  sytrd_lower(st, n, A, lda, d.p, e.p, tau.p);
-  stedc(st, n, d.p, e.p, Z, ldz);
-  ormtr_lower(st, n, n, A, lda, tau.p, Z, ldz);
+  {
+    Stage s(st, ST_SYTRD);
+    sytrd_lower(st, n, A, lda, d.p, e.p, tau.p);
+  }
+  {
+    Stage s(st, ST_STEDC);
+    stedc(st, n, d.p, e.p, Z, ldz);
+  }
+  {
+    Stage s(st, ST_ORMTR);
+    ormtr_lower(st, n, n, A, lda, tau.p, Z, ldz);
+  }
   EM_CK(cudaMemcpyAsync(w, d.p, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
 }
 
@@ -99,7 +108,11 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
   const size_t nn = (size_t)n * n;
   DBuf G(nn, st);
   copy_matrix(st, false, n, n, R, ldr, G.p, n);
-  int64_t piv = potrf(st, n, G.p, n);
+  int64_t piv;
+  {
+    Stage s(st, ST_POTRF_R);
+    piv = potrf(st, n, G.p, n);
+  }
   if (piv >= 0) {
     *which = 0;
     return piv;
@@ -107,14 +120,20 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
   DBuf B(nn, st);
   {
     DBuf X(nn, st);
-    copy_matrix(st, false, n, n, L, ldl, B.p, n);
-    trsm_lower(st, false, n, n, G.p, n, B.p, n);           // G^-1 L
-    copy_matrix(st, true, n, n, B.p, n, X.p, n);           // (G^-1 L)^T
-    trsm_lower(st, false, n, n, G.p, n, X.p, n);           // G^-1 (G^-1 L)^T
-    add_transpose(st, n, 0.5, X.p, n, 0.5, B.p, n);        // (X + X^T)/2
+    {
+      Stage s(st, ST_SYGST);
+      copy_matrix(st, false, n, n, L, ldl, B.p, n);
+      trsm_lower(st, false, n, n, G.p, n, B.p, n);           // G^-1 L
+      copy_matrix(st, true, n, n, B.p, n, X.p, n);           // (G^-1 L)^T
+      trsm_lower(st, false, n, n, G.p, n, X.p, n);           // G^-1 (G^-1 L)^T
+      add_transpose(st, n, 0.5, X.p, n, 0.5, B.p, n);        // (X + X^T)/2
+    }
     // certificate only (modal.py:69-70)
-    copy_matrix(st, false, n, n, L, ldl, X.p, n);
-    piv = potrf(st, n, X.p, n);
+    {
+      Stage s(st, ST_POTRF_L);
+      copy_matrix(st, false, n, n, L, ldl, X.p, n);
+      piv = potrf(st, n, X.p, n);
+    }
     if (piv >= 0) {
       *which = 1;
       return piv;
@@ -123,11 +142,18 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
   DBuf w(n, st), Z(nn, st);
   syev_ascending(st, n, B.p, n, w.p, Z.p, n);
   B.release();
-  trsm_lower(st, true, n, n, G.p, n, Z.p, n);              // V = G^-T U
+  {
+    Stage s(st, ST_TRSM_BACK);
+    trsm_lower(st, true, n, n, G.p, n, Z.p, n);              // V = G^-T U
+  }
   G.release();
-  finalize_modes_kernel<<<(unsigned)n, 256, 0, st>>>(n, Z.p, n, w.p, V, ldv, tau);
-  EM_LAUNCHED();
+  {
+    Stage s(st, ST_FINALIZE);
+    finalize_modes_kernel<<<(unsigned)n, 256, 0, st>>>(n, Z.p, n, w.p, V, ldv, tau);
+    EM_LAUNCHED();
+  }
   Z.release();
+  Stage post(st, ST_POST_GEMM);
   if (l_n) {
     DBuf LV(nn, st);
     EM_CK(gemm(st, false, false, n, n, n, 1.0, L, ldl, V, ldv, 0.0, LV.p, n));

@@ -204,8 +204,11 @@ void sytrd_lower(cudaStream_t st, int64_t n, double* A, int64_t lda, double* d, 
       EM_LAUNCHED();
       const int64_t m = n - c - 1;
       // W[c+1:, i] = A22 v  (A22 = trailing lower triangle)
-      symv_lower(st, m, 1.0, A + (c + 1) + (c + 1) * lda, lda, A + (c + 1) + c * lda, 0.0,
-                 W.p + (c + 1 - i0) + (int64_t)i * n, swork.p);
+      {
+        Stage s(st, ST_SYTRD_SYMV);
+        symv_lower(st, m, 1.0, A + (c + 1) + (c + 1) * lda, lda, A + (c + 1) + c * lda, 0.0,
+                   W.p + (c + 1 - i0) + (int64_t)i * n, swork.p);
+      }
       if (i > 0) {
         latrd_dots_kernel<<<2 * i, RT, 0, st>>>(n, A, lda, i0, c, W.p, n, tmp.p);
         EM_LAUNCHED();
@@ -219,6 +222,7 @@ void sytrd_lower(cudaStream_t st, int64_t n, double* A, int64_t lda, double* d, 
     const int64_t t0 = i0 + w;
     const int64_t mt = n - t0;
     if (mt > 0) {
+      Stage s(st, ST_SYTRD_SYR2K);
       // A22 -= V W^T + W V^T as one K = 2w lower GEMM: [V | W] [W | V]^T
       copy_matrix(st, false, mt, w, A + t0 + i0 * lda, lda, XW.p, n);
       copy_matrix(st, false, mt, w, W.p + (t0 - i0), n, XW.p + (int64_t)w * n, n);

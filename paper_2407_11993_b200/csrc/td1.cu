@@ -313,16 +313,25 @@ static void td1_solve_step(em_td1_plan* P, double* I, double* Icap_col) {
   const int64_t n = P->n;
   const int64_t nblk = (n + TS - 1) / TS;
   // b += -dt R I
-  symv_lower(st, n, -P->dt, P->R.p, n, I, 1.0, P->b.p, P->work.p);
+  {
+    Stage s(st, ST_TD1_SYMV);
+    symv_lower(st, n, -P->dt, P->R.p, n, I, 1.0, P->b.p, P->work.p);
+  }
   ++P->epoch;
   EM_CK(cudaMemsetAsync(P->counters->p, 0, 2 * sizeof(unsigned int), st));
   const int grid = (int)imin64(nblk, 2 * num_sms());
-  trsv_fwd_kernel<<<grid, 256, 0, st>>>(n, P->C.p, n, P->Dinv.p, P->b.p, P->y.p, P->flags->p,
-                                        P->counters->p, P->epoch);
-  EM_LAUNCHED();
-  trsv_bwd_kernel<<<grid, 256, 0, st>>>(n, P->C.p, n, P->Dinv.p, P->y.p, P->x.p, I, Icap_col,
-                                        P->flags->p + nblk, P->counters->p + 1, P->epoch);
-  EM_LAUNCHED();
+  {
+    Stage s(st, ST_TD1_FWD);
+    trsv_fwd_kernel<<<grid, 256, 0, st>>>(n, P->C.p, n, P->Dinv.p, P->b.p, P->y.p, P->flags->p,
+                                          P->counters->p, P->epoch);
+    EM_LAUNCHED();
+  }
+  {
+    Stage s(st, ST_TD1_BWD);
+    trsv_bwd_kernel<<<grid, 256, 0, st>>>(n, P->C.p, n, P->Dinv.p, P->y.p, P->x.p, I, Icap_col,
+                                          P->flags->p + nblk, P->counters->p + 1, P->epoch);
+    EM_LAUNCHED();
+  }
 }
 
 void td1_step(em_td1_plan* P, double* I, const double* u_dev) {

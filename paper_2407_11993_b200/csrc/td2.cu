@@ -367,6 +367,7 @@ void td2_run(em_td2_plan* P, int64_t T, const double* drive, double* q, double* 
     W = Wz.p;
   }
   DBuf E((size_t)nb * n, st), S((size_t)nb * n, st);
+  stage_begin(st, ST_TD2_LOCAL);
   switch (nu_eff) {
     case 1: local_scan<1>(st, nb, n, T, nu_eff, P->eps.p, W, U.p, E.p); break;
     case 2: local_scan<2>(st, nb, n, T, nu_eff, P->eps.p, W, U.p, E.p); break;
@@ -374,8 +375,11 @@ void td2_run(em_td2_plan* P, int64_t T, const double* drive, double* q, double* 
     case 4: local_scan<4>(st, nb, n, T, nu_eff, P->eps.p, W, U.p, E.p); break;
     default: local_scan<0>(st, nb, n, T, nu_eff, P->eps.p, W, U.p, E.p); break;
   }
+  stage_end(st, ST_TD2_LOCAL);
+  stage_begin(st, ST_TD2_CARRY);
   td2_carry<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, T, nb, P->eps.p, E.p, S.p, q);
   EM_LAUNCHED();
+  stage_end(st, ST_TD2_CARRY);
 
   if (!Y && !Qcap) return;
   // observables (or a dummy single row when only states are captured)
@@ -400,6 +404,7 @@ void td2_run(em_td2_plan* P, int64_t T, const double* drive, double* q, double* 
   size_t smem = ((size_t)TB * QS + (size_t)MC * cvs + (size_t)TB * nu_eff) * sizeof(double);
   dim3 grid((unsigned)nb, (unsigned)nsplit);
   const int mt = n_obs_pad / 8;
+  Stage replay_stage(st, ST_TD2_REPLAY);
   switch (nu_eff) {
     case 1: dispatch_mt<1>(mt, st, grid, smem, n, T, nu_eff, n_obs, cvs, mps, P->eps.p, W, U.p, S.p, CV, ldcv, stride, Ypart.p, ldys, Qcap, n_caps); break;
     case 2: dispatch_mt<2>(mt, st, grid, smem, n, T, nu_eff, n_obs, cvs, mps, P->eps.p, W, U.p, S.p, CV, ldcv, stride, Ypart.p, ldys, Qcap, n_caps); break;

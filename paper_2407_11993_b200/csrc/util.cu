@@ -159,3 +159,67 @@ void reverse_columns(cudaStream_t st, int64_t m, int64_t n, const double* A, int
 }
 
 }  // namespace em
+
+// ---- stage timers -----------------------------------------------------------------
+namespace em {
+
+namespace {
+struct StageRec {
+  int id;
+  cudaEvent_t a, b;
+};
+bool g_stage_on = false;
+std::vector<StageRec> g_recs;
+std::vector<int> g_open[ST_COUNT];
+}  // namespace
+
+bool stages_enabled() { return g_stage_on; }
+
+int g_stage_level = 0;  // 1: top-level stages, 2: also per-call inner stages
+
+void stage_begin(cudaStream_t st, int id) {
+  if (!g_stage_on || (id >= ST_SYTRD_SYMV && g_stage_level < 2)) return;
+  StageRec r{id, nullptr, nullptr};
+  cudaEventCreate(&r.a);
+  cudaEventCreate(&r.b);
+  cudaEventRecord(r.a, st);
+  g_open[id].push_back((int)g_recs.size());
+  g_recs.push_back(r);
+}
+
+void stage_end(cudaStream_t st, int id) {
+  if (!g_stage_on || g_open[id].empty()) return;
+  const int k = g_open[id].back();
+  g_open[id].pop_back();
+  cudaEventRecord(g_recs[k].b, st);
+}
+
+void stages_level(int level) { g_stage_level = level; }
+
+void stages_reset(bool on) {
+  for (auto& r : g_recs) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  g_recs.clear();
+  for (auto& o : g_open) o.clear();
+  g_stage_on = on;
+}
+
+int stages_read(double* ms, int64_t* counts, int n) {
+  for (int i = 0; i < n; ++i) {
+    ms[i] = 0.0;
+    if (counts) counts[i] = 0;
+  }
+  for (auto& r : g_recs) {
+    cudaEventSynchronize(r.b);
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, r.a, r.b) == cudaSuccess && r.id < n) {
+      ms[r.id] += t;
+      if (counts) counts[r.id] += 1;
+    }
+  }
+  return ST_COUNT;
+}
+
+}  // namespace em

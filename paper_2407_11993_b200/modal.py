@@ -110,7 +110,11 @@ def generalized_eig(l_i, r_i) -> ModalBasis:
             z = np.zeros(0)
             zz = np.zeros((0, 0))
             return ModalBasis(v=zz, tau=z, l_n=z, r_n=z, vt_r=zz)
-        ld, rd = nat.device_colmajor(lm), nat.device_colmajor(rm)
+        # SymMatrix is exactly symmetric: upload its bytes as they are
+        ld = nat.device_symmetric(lm) if isinstance(l_i, linalg.SymMatrix) else \
+            nat.device_colmajor(lm)
+        rd = nat.device_symmetric(rm) if isinstance(r_i, linalg.SymMatrix) else \
+            nat.device_colmajor(rm)
     ctx = nat.context()
     tau, ln, rn = nat.empty(n), nat.empty(n), nat.empty(n)
     v, vtr = nat.empty(n, n), nat.empty(n, n)

@@ -183,6 +183,36 @@ def plate_model(nx: int, ny: int, nz: int, n_ports: int = 0, n_sources: int = 1,
     return dict(plate=p, r_i=r, l_i=l, r_d=r_d, l_d=l_d, m0=m0, c=c)
 
 
+def device_plate_model(nx: int, ny: int, nz: int, n_ports: int = 0, n_sources: int = 1,
+                       n_obs: int = 16, seed: int = DEFAULT_SEED, notch: bool = False,
+                       h: float = 1e-3) -> dict:
+    """plate_model with the O(N^2) parts generated on the device (em_synth_plate):
+    l_i, r_i (torch, (N, N) symmetric), r_d, l_d (torch (n_ports, N) = column-major
+    N x n_ports), plus host m0 (N x n_sources) and c (n_obs x N)."""
+    from . import _native as nat
+    p = Plate(nx, ny, nz, h=h, seed=seed, notch=notch)
+    n = p.n
+    theta = p.rng(_ANGLES).uniform(0.0, 2 * np.pi, size=nx * ny * nz)[p.keep]
+    pos = -np.ones(nx * ny * nz, dtype=np.int64)
+    pos[p.keep] = np.arange(n)
+    t = nat.torch()
+    keep_d = t.from_numpy(p.keep.astype(np.int64)).to("cuda")
+    pos_d = t.from_numpy(pos).to("cuda")
+    ang_d = nat.device_vector(theta)
+    L = nat.empty(n, n)
+    R = nat.empty(n, n)
+    ld = nat.zeros(max(n_ports, 1), n)
+    rd = nat.zeros(max(n_ports, 1), n)
+    lib = nat.load_library()
+    nat.check(lib.em_synth_plate(nat.context(), nx, ny, nz, h, RHO, R_SHIFT, n, nat.ptr(keep_d),
+                                 nat.ptr(pos_d), nat.ptr(ang_d), nat.ptr(L), n, nat.ptr(R), n,
+                                 nat.ptr(ld) if n_ports else None,
+                                 nat.ptr(rd) if n_ports else None), "em_synth_plate")
+    m0 = p.source_profiles(n_sources) if n_sources else np.zeros((n, 0))
+    c = p.observables(n_obs)
+    return dict(plate=p, l_i=L, r_i=R, l_d=ld[:n_ports], r_d=rd[:n_ports], m0=m0, c=c)
+
+
 def drive_table(kind: str, steps: int, dt: float, n_ports: int, n_sources: int,
                 plate: Plate | None = None):
     """Drive samples at t_k = k*dt, k = 0..steps: (i_d (steps+1, n_p), i0 (steps+1, n_s)).

@@ -269,8 +269,8 @@ class Td1Stepper:
         if n:
             ctx = nat.context()
             lib = nat.load_library()
-            ld = nat.device_colmajor(rm.l_i.full)
-            rd = nat.device_colmajor(rm.r_i.full)
+            ld = nat.device_symmetric(rm.l_i.full)   # SymMatrix: exactly symmetric
+            rd = nat.device_symmetric(rm.r_i.full)
             dr = nat.device_colmajor(rm.r_d.reshape(n, n_p)) if n_p else nat.zeros(1)
             dl = nat.device_colmajor(rm.l_d.reshape(n, n_p)) if n_p else nat.zeros(1)
             dm = nat.device_colmajor(rm.m0.reshape(n, n_s)) if n_s else nat.zeros(1)
