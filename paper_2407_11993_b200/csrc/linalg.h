@@ -10,8 +10,13 @@ namespace em {
 
 // potrf.cu
 int64_t potrf(cudaStream_t st, int64_t n, double* A, int64_t lda);  // -1 ok, else pivot
+// also returns the inverses of the 128x128 diagonal blocks (ceil(n/128) * 128^2 doubles)
+int64_t potrf(cudaStream_t st, int64_t n, double* A, int64_t lda, double* Dinv_out);
 void trsm_lower(cudaStream_t st, bool trans, int64_t n, int64_t m, const double* C, int64_t ldc,
                 double* B, int64_t ldb);
+void trsm_lower(cudaStream_t st, bool trans, int64_t n, int64_t m, const double* C, int64_t ldc,
+                double* B, int64_t ldb, const double* Dinv);
+constexpr int kTrsmBlock = 128;
 void trtri_blocks(cudaStream_t st, int nb, int64_t n, const double* C, int64_t ldc, double* Dinv);
 
 // symv.cu: y = alpha*A*x + beta*y using only the lower triangle of A (n x n)

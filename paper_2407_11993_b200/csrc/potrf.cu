@@ -1,13 +1,16 @@
-// Blocked Cholesky (potrf) and triangular solves (trsm) in FP64.
+// Cholesky (potrf) and triangular solves (trsm) in FP64, recursive so that
+// almost all flops land in large-K DMMA GEMMs.
 //
 // Reference: cholesky_kernel (_kernels.py:18-36) is an unblocked Crout loop that
 // returns the first index whose pivot s = a_jj - sum_k c_jk^2 is not > 0;
 // tri_lower_solve_mat / tri_lower_t_solve_mat (_kernels.py:56-79) are column-wise
-// substitutions. Here: right-looking blocked potrf with a 128x128 diagonal block
-// factored and inverted in shared memory (one CTA), the panel solved as a GEMM
-// against the inverted block and the trailing update done by the lower-triangle
-// DMMA GEMM; trsm likewise uses inverted diagonal blocks + DMMA GEMM updates.
-// The failing pivot is reported with the reference's index semantics.
+// substitutions.
+//
+//   potrf(A) = [ potrf(A11);  A21 <- A21 L11^-T;  A22 -= A21 A21^T;  potrf(A22) ]
+//   leaves: 128x128 diagonal blocks factored AND inverted in shared memory by one
+//   CTA (the inverse feeds every trsm leaf as a GEMM); the failing pivot is
+//   reported with the reference's global index.
+//   trsm: the same split; B2 -= L21 X1 is one GEMM with K = n/2, n/4, ...
 #include "common.cuh"
 #include "ctx.h"
 #include "gemm.h"
@@ -15,7 +18,7 @@
 
 namespace em {
 
-constexpr int PNB = 128;       // potrf / trsm block
+constexpr int PNB = 128;       // leaf block
 constexpr int PLD = PNB + 1;   // smem leading dimension
 
 // In-place inversion of the lower-triangular n x n matrix in shared memory
@@ -38,12 +41,13 @@ EM_DEVINL void smem_trtri_lower(double* A, int n, int ld, double* tmp) {
   __syncthreads();
 }
 
-// Factor the diagonal block A[k0:k0+bs, k0:k0+bs] (bs <= PNB), write the factor
-// back (upper part zeroed) and its inverse to Dinv (PNB x PNB, ld PNB).
+// Factor the diagonal block A[0:bs, 0:bs] (bs <= PNB; global offset k0 for the
+// pivot index), write the factor back (upper part zeroed) and its inverse to
+// Dinv (PNB x PNB, ld PNB).
 __global__ void __launch_bounds__(256) potf2_inv_kernel(double* A, int64_t lda, int64_t k0, int bs,
                                                         double* Dinv, int64_t* info) {
   extern __shared__ double sm[];
-  double* S = sm;             // PNB x PLD
+  double* S = sm;               // PNB x PLD
   double* tmp = S + PNB * PLD;  // PNB
   __shared__ int fail;
   if (*info >= 0) return;  // an earlier block already failed
@@ -52,9 +56,9 @@ __global__ void __launch_bounds__(256) potf2_inv_kernel(double* A, int64_t lda, 
     int r = i % PNB, c = i / PNB;
     double v;
     if (r < bs && c < bs)
-      v = (r >= c) ? A[(k0 + r) + (k0 + c) * lda] : 0.0;
+      v = (r >= c) ? A[r + c * lda] : 0.0;
     else
-      v = (r == c) ? 1.0 : 0.0;  // identity padding for a partial last block
+      v = (r == c) ? 1.0 : 0.0;  // identity padding for a partial block
     S[r + c * PLD] = v;
   }
   __syncthreads();
@@ -69,7 +73,6 @@ __global__ void __launch_bounds__(256) potf2_inv_kernel(double* A, int64_t lda, 
     if (threadIdx.x == 0) S[j + j * PLD] = d;
     for (int i = j + 1 + threadIdx.x; i < bs; i += blockDim.x) S[i + j * PLD] /= d;
     __syncthreads();
-    // trailing update of the lower triangle: S[i][k] -= S[i][j] S[k][j], j < k <= i
     const int m = bs - j - 1;
     for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) {
       const int i = j + 1 + idx % m, k = j + 1 + idx / m;
@@ -84,7 +87,7 @@ __global__ void __launch_bounds__(256) potf2_inv_kernel(double* A, int64_t lda, 
   }
   for (int i = threadIdx.x; i < bs * bs; i += blockDim.x) {
     int r = i % bs, c = i / bs;
-    A[(k0 + r) + (k0 + c) * lda] = (r >= c) ? S[r + c * PLD] : 0.0;
+    A[r + c * lda] = (r >= c) ? S[r + c * PLD] : 0.0;
   }
   smem_trtri_lower(S, PNB, PLD, tmp);
   for (int i = threadIdx.x; i < PNB * PNB; i += blockDim.x) {
@@ -138,70 +141,127 @@ void trtri_blocks(cudaStream_t st, int nb, int64_t n, const double* C, int64_t l
   EM_LAUNCHED();
 }
 
+// split point: a multiple of PNB near the middle
+static int64_t split_point(int64_t n) {
+  const int64_t nbk = (n + PNB - 1) / PNB;
+  return imax64(1, nbk / 2) * PNB;
+}
+
+// ---- trsm (left): B <- C^-1 B or C^-T B; Dinv holds inverses of C's PNB diagonal
+// blocks, block index offset by blk0 (block of C[0,0]); T is PNB x m workspace.
+static void trsm_left_rec(cudaStream_t st, bool trans, int64_t n, int64_t m, const double* C,
+                          int64_t ldc, double* B, int64_t ldb, const double* Dinv, int64_t blk0,
+                          double* T) {
+  if (n <= 0 || m <= 0) return;
+  if (n <= PNB) {
+    const double* D = Dinv + blk0 * PNB * PNB;
+    EM_CK(gemm(st, trans, false, n, m, n, 1.0, D, PNB, B, ldb, 0.0, T, PNB));
+    copy_matrix(st, false, n, m, T, PNB, B, ldb);
+    return;
+  }
+  const int64_t n1 = split_point(n), n2 = n - n1;
+  const double* C21 = C + n1;                 // n2 x n1
+  const double* C22 = C + n1 + n1 * ldc;
+  if (!trans) {
+    trsm_left_rec(st, false, n1, m, C, ldc, B, ldb, Dinv, blk0, T);
+    EM_CK(gemm(st, false, false, n2, m, n1, -1.0, C21, ldc, B, ldb, 1.0, B + n1, ldb));
+    trsm_left_rec(st, false, n2, m, C22, ldc, B + n1, ldb, Dinv, blk0 + n1 / PNB, T);
+  } else {
+    // C^T = [C11^T C21^T; 0 C22^T]
+    trsm_left_rec(st, true, n2, m, C22, ldc, B + n1, ldb, Dinv, blk0 + n1 / PNB, T);
+    EM_CK(gemm(st, true, false, n1, m, n2, -1.0, C21, ldc, B + n1, ldb, 1.0, B, ldb));
+    trsm_left_rec(st, true, n1, m, C, ldc, B, ldb, Dinv, blk0, T);
+  }
+}
+
+// ---- trsm (right, transposed): B (m x n) <- B C^-T; T is m x PNB workspace.
+static void trsm_right_t_rec(cudaStream_t st, int64_t m, int64_t n, const double* C, int64_t ldc,
+                             double* B, int64_t ldb, const double* Dinv, int64_t blk0, double* T,
+                             int64_t ldt) {
+  if (n <= 0 || m <= 0) return;
+  if (n <= PNB) {
+    const double* D = Dinv + blk0 * PNB * PNB;
+    EM_CK(gemm(st, false, true, m, n, n, 1.0, B, ldb, D, PNB, 0.0, T, ldt));
+    copy_matrix(st, false, m, n, T, ldt, B, ldb);
+    return;
+  }
+  const int64_t n1 = split_point(n), n2 = n - n1;
+  const double* C21 = C + n1;
+  const double* C22 = C + n1 + n1 * ldc;
+  // X C^T = B:  X1 = B1 C11^-T;  B2 -= X1 C21^T;  X2 = B2 C22^-T
+  trsm_right_t_rec(st, m, n1, C, ldc, B, ldb, Dinv, blk0, T, ldt);
+  EM_CK(gemm(st, false, true, m, n2, n1, -1.0, B, ldb, C21, ldc, 1.0, B + n1 * ldb, ldb));
+  trsm_right_t_rec(st, m, n2, C22, ldc, B + n1 * ldb, ldb, Dinv, blk0 + n1 / PNB, T, ldt);
+}
+
+// ---- potrf --------------------------------------------------------------------------
+static void potrf_rec(cudaStream_t st, int64_t n, double* A, int64_t lda, int64_t k0,
+                      double* Dinv, int64_t* info, double* T, int64_t ldt, size_t smem) {
+  if (n <= PNB) {
+    potf2_inv_kernel<<<1, 256, smem, st>>>(A, lda, k0, (int)n, Dinv + (k0 / PNB) * PNB * PNB,
+                                           info);
+    EM_LAUNCHED();
+    return;
+  }
+  const int64_t n1 = split_point(n), n2 = n - n1;
+  double* A21 = A + n1;
+  double* A22 = A + n1 + n1 * lda;
+  potrf_rec(st, n1, A, lda, k0, Dinv, info, T, ldt, smem);
+  trsm_right_t_rec(st, n2, n1, A, lda, A21, lda, Dinv, k0 / PNB, T, ldt);
+  EM_CK(gemm(st, false, true, n2, n2, n1, -1.0, A21, lda, A21, lda, 1.0, A22, lda, true, 0));
+  potrf_rec(st, n2, A22, lda, k0 + n1, Dinv, info, T, ldt, smem);
+}
+
 // Lower Cholesky in place. Returns the failing pivot (-1 = success); syncs the stream.
-int64_t potrf(cudaStream_t st, int64_t n, double* A, int64_t lda) {
+// If Dinv_out is given (>= ceil(n/128) * 128^2 doubles) it receives the inverses of
+// the 128 x 128 diagonal blocks of the factor.
+int64_t potrf(cudaStream_t st, int64_t n, double* A, int64_t lda, double* Dinv_out) {
   if (n <= 0) return -1;
   DArr<int64_t> info(1, st);
   const int64_t minus1 = -1;
   EM_CK(cudaMemcpyAsync(info.p, &minus1, sizeof(int64_t), cudaMemcpyHostToDevice, st));
-  DBuf Dinv((size_t)PNB * PNB, st);
-  DBuf P((size_t)n * PNB, st);
+  const int64_t nblk = (n + PNB - 1) / PNB;
+  DBuf Dloc;
+  double* Dinv = Dinv_out;
+  if (!Dinv) {
+    Dloc.alloc((size_t)nblk * PNB * PNB, st);
+    Dinv = Dloc.p;
+  }
+  DBuf T((size_t)n * PNB, st);
   const size_t smem = ((size_t)PNB * PLD + PNB) * sizeof(double);
   EM_CK(cudaFuncSetAttribute(potf2_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem));
-  for (int64_t k0 = 0; k0 < n; k0 += PNB) {
-    const int bs = (int)imin64(PNB, n - k0);
-    potf2_inv_kernel<<<1, 256, smem, st>>>(A, lda, k0, bs, Dinv.p, info.p);
-    EM_LAUNCHED();
-    const int64_t m = n - k0 - bs;
-    if (m <= 0) break;
-    double* A21 = A + (k0 + bs) + k0 * lda;
-    double* A22 = A + (k0 + bs) + (k0 + bs) * lda;
-    // P = A21 * inv(L11)^T
-    EM_CK(gemm(st, false, true, m, bs, bs, 1.0, A21, lda, Dinv.p, PNB, 0.0, P.p, n));
-    // A22 -= P P^T (lower triangle)
-    EM_CK(gemm(st, false, true, m, m, bs, -1.0, P.p, n, P.p, n, 1.0, A22, lda, true, 0));
-    copy_matrix(st, false, m, bs, P.p, n, A21, lda);
-  }
-  // zero the strict upper triangle (the reference's factor is exactly lower)
-  zero_upper(st, n, A, lda);
+  potrf_rec(st, n, A, lda, 0, Dinv, info.p, T.p, n, smem);
+  zero_upper(st, n, A, lda);  // the reference's factor is exactly lower
   int64_t h = -1;
   EM_CK(cudaMemcpyAsync(&h, info.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   EM_CK(cudaStreamSynchronize(st));
   return h;
 }
 
+int64_t potrf(cudaStream_t st, int64_t n, double* A, int64_t lda) {
+  return potrf(st, n, A, lda, nullptr);
+}
+
 // B <- C^-1 B (trans = false) or C^-T B (trans = true); C lower n x n, B n x m.
 void trsm_lower(cudaStream_t st, bool trans, int64_t n, int64_t m, const double* C, int64_t ldc,
-                double* B, int64_t ldb) {
+                double* B, int64_t ldb, const double* Dinv_in) {
   if (n <= 0 || m <= 0) return;
   const int64_t nblk = (n + PNB - 1) / PNB;
-  DBuf Dinv((size_t)nblk * PNB * PNB, st);
-  trtri_blocks(st, PNB, n, C, ldc, Dinv.p);
-  DBuf T((size_t)PNB * m, st);
-  if (!trans) {
-    for (int64_t kb = 0; kb < nblk; ++kb) {
-      const int64_t k0 = kb * PNB;
-      const int bs = (int)imin64(PNB, n - k0);
-      const double* Dk = Dinv.p + kb * PNB * PNB;
-      EM_CK(gemm(st, false, false, bs, m, bs, 1.0, Dk, PNB, B + k0, ldb, 0.0, T.p, PNB));
-      const int64_t rest = n - k0 - bs;
-      if (rest > 0)
-        EM_CK(gemm(st, false, false, rest, m, bs, -1.0, C + (k0 + bs) + k0 * ldc, ldc, T.p, PNB,
-                   1.0, B + k0 + bs, ldb));
-      copy_matrix(st, false, bs, m, T.p, PNB, B + k0, ldb);
-    }
-  } else {
-    for (int64_t kb = nblk - 1; kb >= 0; --kb) {
-      const int64_t k0 = kb * PNB;
-      const int bs = (int)imin64(PNB, n - k0);
-      const double* Dk = Dinv.p + kb * PNB * PNB;
-      EM_CK(gemm(st, true, false, bs, m, bs, 1.0, Dk, PNB, B + k0, ldb, 0.0, T.p, PNB));
-      if (k0 > 0)
-        EM_CK(gemm(st, true, false, k0, m, bs, -1.0, C + k0, ldc, T.p, PNB, 1.0, B, ldb));
-      copy_matrix(st, false, bs, m, T.p, PNB, B + k0, ldb);
-    }
+  DBuf Dloc;
+  const double* Dinv = Dinv_in;
+  if (!Dinv) {
+    Dloc.alloc((size_t)nblk * PNB * PNB, st);
+    trtri_blocks(st, PNB, n, C, ldc, Dloc.p);
+    Dinv = Dloc.p;
   }
+  DBuf T((size_t)PNB * m, st);
+  trsm_left_rec(st, trans, n, m, C, ldc, B, ldb, Dinv, 0, T.p);
+}
+
+void trsm_lower(cudaStream_t st, bool trans, int64_t n, int64_t m, const double* C, int64_t ldc,
+                double* B, int64_t ldb) {
+  trsm_lower(st, trans, n, m, C, ldc, B, ldb, nullptr);
 }
 
 }  // namespace em

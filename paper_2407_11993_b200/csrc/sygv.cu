@@ -109,9 +109,10 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
   DBuf G(nn, st);
   copy_matrix(st, false, n, n, R, ldr, G.p, n);
   int64_t piv;
+  DBuf GDinv((size_t)((n + kTrsmBlock - 1) / kTrsmBlock) * kTrsmBlock * kTrsmBlock, st);
   {
     Stage s(st, ST_POTRF_R);
-    piv = potrf(st, n, G.p, n);
+    piv = potrf(st, n, G.p, n, GDinv.p);
   }
   if (piv >= 0) {
     *which = 0;
@@ -123,9 +124,9 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
     {
       Stage s(st, ST_SYGST);
       copy_matrix(st, false, n, n, L, ldl, B.p, n);
-      trsm_lower(st, false, n, n, G.p, n, B.p, n);           // G^-1 L
+      trsm_lower(st, false, n, n, G.p, n, B.p, n, GDinv.p);  // G^-1 L
       copy_matrix(st, true, n, n, B.p, n, X.p, n);           // (G^-1 L)^T
-      trsm_lower(st, false, n, n, G.p, n, X.p, n);           // G^-1 (G^-1 L)^T
+      trsm_lower(st, false, n, n, G.p, n, X.p, n, GDinv.p);  // G^-1 (G^-1 L)^T
       add_transpose(st, n, 0.5, X.p, n, 0.5, B.p, n);        // (X + X^T)/2
     }
     // certificate only (modal.py:69-70)
@@ -144,7 +145,7 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
   B.release();
   {
     Stage s(st, ST_TRSM_BACK);
-    trsm_lower(st, true, n, n, G.p, n, Z.p, n);              // V = G^-T U
+    trsm_lower(st, true, n, n, G.p, n, Z.p, n, GDinv.p);     // V = G^-T U
   }
   G.release();
   {

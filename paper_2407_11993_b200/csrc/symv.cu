@@ -4,6 +4,12 @@
 // transposed contributions go to a per-tile workspace reduced in fixed order
 // (no floating-point atomics).
 //
+// Tile mapping: warp w owns columns 8w..8w+7 of a tile, lane l rows l and l+32
+// (every load instruction reads 256 contiguous bytes). The next tile is
+// prefetched into registers while the current one is consumed; column sums
+// are reduced with a 9-shuffle butterfly, so a tile needs no shared memory and
+// no barrier.
+//
 // Used by the Householder tridiagonalisation (the memory-bound half of sytrd)
 // and by the Cholesky theta-method's per-step R * I product
 // (reference: td1_step_kernel's dense loop, _kernels.py:198-207).
@@ -23,67 +29,126 @@ size_t symv_work_size(int64_t n) {
   return (size_t)(nb * nb * SV + nb * nch * SV);
 }
 
-// grid: (chunk, block-row i). Chunk c covers tiles j in [c*SVCH, min(i, c*SVCH+SVCH-1)].
+template <bool FULL>
+EM_DEVINL void load_tile(double (&a)[2][8], const double* __restrict__ A, int64_t lda, int64_t n,
+                         int64_t r0, int64_t c0, int lane, int w) {
+#pragma unroll
+  for (int cc = 0; cc < 8; ++cc) {
+    const int64_t c = c0 + 8 * w + cc;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t r = r0 + lane + 32 * h;
+      if (FULL)
+        a[h][cc] = A[r + c * lda];
+      else
+        a[h][cc] = (r < n && c < n) ? A[r + c * lda] : 0.0;
+    }
+  }
+}
+
+// grid: (chunk, block-row i). Chunk ch covers tiles j in [ch*SVCH, min(i, ch*SVCH+SVCH-1)].
 __global__ void __launch_bounds__(SVT) symv_tiles_kernel(int64_t n, const double* __restrict__ A,
                                                          int64_t lda, const double* __restrict__ x,
                                                          double* __restrict__ wcol,
                                                          double* __restrict__ wrow, int64_t nb,
                                                          int64_t nch) {
-  __shared__ double S[SV][SV + 1];
-  __shared__ double xi[SV], xj[SV];
-  __shared__ double red[4][SV];
+  __shared__ double red[8][SV];
   const int64_t i = blockIdx.y, ch = blockIdx.x;
   const int64_t j_begin = ch * SVCH;
   if (j_begin > i) return;
   const int64_t j_end = imin64(i, j_begin + SVCH - 1);  // inclusive
-  const int tid = threadIdx.x, tx = tid & 63, ty = tid >> 6;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int64_t r0 = i * SV;
-  if (tid < SV) xi[tid] = (r0 + tid < n) ? x[r0 + tid] : 0.0;
-  double rowacc = 0.0;
+  const bool row_full = r0 + SV <= n;
+  const double xi0 = (r0 + lane < n) ? x[r0 + lane] : 0.0;
+  const double xi1 = (r0 + lane + 32 < n) ? x[r0 + lane + 32] : 0.0;
+  double row0 = 0.0, row1 = 0.0;
+  double nxt[2][8];
+  if (row_full && j_begin * SV + SV <= n)
+    load_tile<true>(nxt, A, lda, n, r0, j_begin * SV, lane, w);
+  else
+    load_tile<false>(nxt, A, lda, n, r0, j_begin * SV, lane, w);
   for (int64_t j = j_begin; j <= j_end; ++j) {
-    const int64_t c0 = j * SV;
-    __syncthreads();
-    if (tid < SV) xj[tid] = (c0 + tid < n) ? x[c0 + tid] : 0.0;
-    double a[16];
-    const int64_t r = r0 + tx;
+    double a[2][8];
 #pragma unroll
-    for (int cc = 0; cc < 16; ++cc) {
-      const int64_t c = c0 + ty * 16 + cc;
-      a[cc] = (r < n && c < n) ? A[r + c * lda] : 0.0;
+    for (int cc = 0; cc < 8; ++cc) {
+      a[0][cc] = nxt[0][cc];
+      a[1][cc] = nxt[1][cc];
     }
-    if (j == i) {
-      // diagonal tile: symmetrise from the lower triangle in shared memory
+    const int64_t c0 = j * SV;
+    if (j < j_end) {
+      const int64_t c1 = c0 + SV;
+      if (row_full && c1 + SV <= n)
+        load_tile<true>(nxt, A, lda, n, r0, c1, lane, w);
+      else
+        load_tile<false>(nxt, A, lda, n, r0, c1, lane, w);
+    }
+    double xj[8];
 #pragma unroll
-      for (int cc = 0; cc < 16; ++cc) S[tx][ty * 16 + cc] = a[cc];
-      __syncthreads();
+    for (int cc = 0; cc < 8; ++cc) {
+      const int64_t c = c0 + 8 * w + cc;
+      xj[cc] = (c < n) ? __ldg(x + c) : 0.0;
+    }
+    double col[8];
+    if (j != i) {
 #pragma unroll
-      for (int cc = 0; cc < 16; ++cc) {
-        const int c = ty * 16 + cc;
-        const double v = (tx >= c) ? S[tx][c] : S[c][tx];
-        rowacc = fma(v, xj[c], rowacc);
+      for (int cc = 0; cc < 8; ++cc) {
+        row0 = fma(a[0][cc], xj[cc], row0);
+        row1 = fma(a[1][cc], xj[cc], row1);
+        col[cc] = fma(a[0][cc], xi0, a[1][cc] * xi1);
       }
     } else {
-      __syncthreads();  // xj visible
+      // diagonal tile: lower triangle only (r >= c for rows, r > c for the transpose)
 #pragma unroll
-      for (int cc = 0; cc < 16; ++cc) {
-        rowacc = fma(a[cc], xj[ty * 16 + cc], rowacc);
-        S[tx][ty * 16 + cc] = a[cc];
+      for (int cc = 0; cc < 8; ++cc) {
+        const int c = 8 * w + cc;
+        const double l0 = (lane >= c) ? a[0][cc] : 0.0;
+        const double l1 = (lane + 32 >= c) ? a[1][cc] : 0.0;
+        row0 = fma(l0, xj[cc], row0);
+        row1 = fma(l1, xj[cc], row1);
+        const double s0 = (lane > c) ? a[0][cc] : 0.0;
+        const double s1 = (lane + 32 > c) ? a[1][cc] : 0.0;
+        col[cc] = fma(s0, xi0, s1 * xi1);
       }
-      __syncthreads();
-      // column products: thread (cx = tx, row group ty)
-      double cs = 0.0;
+    }
+    // butterfly: reduce 8 column partials over the 32 lanes
 #pragma unroll
-      for (int rr = 0; rr < 16; ++rr) cs = fma(S[ty * 16 + rr][tx], xi[ty * 16 + rr], cs);
-      red[ty][tx] = cs;
-      __syncthreads();
-      if (tid < SV)
-        wcol[(i * nb + j) * SV + tid] = red[0][tid] + red[1][tid] + red[2][tid] + red[3][tid];
+    for (int cc = 0; cc < 4; ++cc) {  // offset 16: lanes < 16 keep cols 0..3, others 4..7
+      const bool hi = lane & 16;
+      const double send = hi ? col[cc] : col[cc + 4];
+      const double keep = hi ? col[cc + 4] : col[cc];
+      col[cc] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc) {  // offset 8
+      const bool hi = lane & 8;
+      const double send = hi ? col[cc] : col[cc + 2];
+      const double keep = hi ? col[cc + 2] : col[cc];
+      col[cc] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    {  // offset 4
+      const bool hi = lane & 4;
+      const double send = hi ? col[0] : col[1];
+      const double keep = hi ? col[1] : col[0];
+      col[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    col[0] += __shfl_xor_sync(0xffffffffu, col[0], 2);
+    col[0] += __shfl_xor_sync(0xffffffffu, col[0], 1);
+    if ((lane & 3) == 0) {
+      // column index held by this lane group: bit4 -> +4, bit3 -> +2, bit2 -> +1
+      const int cc = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+      wcol[(i * nb + j) * SV + 8 * w + cc] = col[0];
     }
   }
+  red[w][lane] = row0;
+  red[w][lane + 32] = row1;
   __syncthreads();
-  red[ty][tx] = rowacc;
-  __syncthreads();
-  if (tid < SV) wrow[(i * nch + ch) * SV + tid] = red[0][tid] + red[1][tid] + red[2][tid] + red[3][tid];
+  if (tid < SV) {
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += red[k][tid];
+    wrow[(i * nch + ch) * SV + tid] = s;
+  }
 }
 
 __global__ void symv_reduce_kernel(int64_t n, double alpha, double beta, double* __restrict__ y,
@@ -96,7 +161,7 @@ __global__ void symv_reduce_kernel(int64_t n, double alpha, double beta, double*
   double s = 0.0;
   const int64_t nchj = j / SVCH + 1;  // chunks present in block row j
   for (int64_t c = 0; c < nchj; ++c) s += wrow[(j * nch + c) * SV + t];
-  for (int64_t i = j + 1; i < nb; ++i) s += wcol[(i * nb + j) * SV + t];
+  for (int64_t i = j; i < nb; ++i) s += wcol[(i * nb + j) * SV + t];
   y[idx] = (beta == 0.0) ? alpha * s : fma(alpha, s, beta * y[idx]);
 }
 

@@ -257,44 +257,49 @@ __global__ void build_v_kernel(int64_t n, const double* A, int64_t lda, int64_t 
   }
 }
 
-// T (w x w upper) from G = V^T V: T[k][k] = tau_k; T[0:k, k] = -tau_k T[0:k, 0:k] G[0:k, k]
-__global__ void larft_kernel(int w, const double* G, const double* tau, int64_t c0, double* T) {
-  __shared__ double Ts[TRD_NB][TRD_NB + 1];
-  __shared__ double gk[TRD_NB];
+// Wide-block larft: T (w x w upper, ld ldt, global memory) from G = V^T V, w <= 256.
+__global__ void larft_wide_kernel(int w, const double* __restrict__ G, int64_t ldg,
+                                  const double* __restrict__ tau, int64_t c0, double* T,
+                                  int64_t ldt) {
+  __shared__ double gk[256];
   const int tid = threadIdx.x;
-  for (int i = tid; i < TRD_NB * TRD_NB; i += blockDim.x) Ts[i % TRD_NB][i / TRD_NB] = 0.0;
+  for (int i = tid; i < w * w; i += blockDim.x) T[(i % w) + (i / w) * ldt] = 0.0;
   __syncthreads();
   for (int k = 0; k < w; ++k) {
     const double tk = tau[c0 + k];
-    if (tid < k) gk[tid] = G[tid + k * w];
+    if (tid < k) gk[tid] = G[tid + k * ldg];
     __syncthreads();
     if (tid < k) {
       double s = 0.0;
-      for (int j = tid; j < k; ++j) s = fma(Ts[tid][j], gk[j], s);  // T upper: j >= tid
-      Ts[tid][k] = -tk * s;
+      for (int j = tid; j < k; ++j) s = fma(T[tid + j * ldt], gk[j], s);
+      T[tid + k * ldt] = -tk * s;
     }
-    if (tid == 0) Ts[k][k] = tk;
+    if (tid == 0) T[k + k * ldt] = tk;
     __syncthreads();
   }
-  for (int i = tid; i < w * w; i += blockDim.x) T[(i % w) + (i / w) * w] = Ts[i % w][i / w];
 }
+
+// Z <- Q Z, Q = H(0)...H(n-2), in blocks of ORM_NB reflectors (compact WY,
+// three DMMA GEMMs per block; a wide block keeps the rank-w updates of Z
+// compute-bound instead of re-streaming Z once per 64 reflectors).
+constexpr int ORM_NB = 256;
 
 void ormtr_lower(cudaStream_t st, int64_t n, int64_t m, const double* A, int64_t lda,
                  const double* tau, double* Z, int64_t ldz) {
   const int64_t nref = n - 1;  // reflectors H(0..n-2)
   if (nref <= 0 || m <= 0) return;
-  DBuf V((size_t)n * TRD_NB, st), G((size_t)TRD_NB * TRD_NB, st), T((size_t)TRD_NB * TRD_NB, st);
-  DBuf W1((size_t)TRD_NB * m, st), W2((size_t)TRD_NB * m, st);
-  const int64_t npan = (nref + TRD_NB - 1) / TRD_NB;
+  DBuf V((size_t)n * ORM_NB, st), G((size_t)ORM_NB * ORM_NB, st), T((size_t)ORM_NB * ORM_NB, st);
+  DBuf W1((size_t)ORM_NB * m, st), W2((size_t)ORM_NB * m, st);
+  const int64_t npan = (nref + ORM_NB - 1) / ORM_NB;
   for (int64_t p = npan - 1; p >= 0; --p) {
-    const int64_t i0 = p * TRD_NB;
-    const int w = (int)imin64(TRD_NB, nref - i0);
+    const int64_t i0 = p * ORM_NB;
+    const int w = (int)imin64(ORM_NB, nref - i0);
     const int64_t mr = n - i0 - 1;  // rows of V
     dim3 grid((unsigned)imax64(1, imin64((mr + 255) / 256, 64)), (unsigned)w);
     build_v_kernel<<<grid, 256, 0, st>>>(n, A, lda, i0, w, V.p, n);
     EM_LAUNCHED();
     EM_CK(gemm(st, true, false, w, w, mr, 1.0, V.p, n, V.p, n, 0.0, G.p, w));
-    larft_kernel<<<1, TRD_NB, 0, st>>>(w, G.p, tau, i0, T.p);
+    larft_wide_kernel<<<1, 256, 0, st>>>(w, G.p, w, tau, i0, T.p, w);
     EM_LAUNCHED();
     double* Zs = Z + (i0 + 1);
     EM_CK(gemm(st, true, false, w, m, mr, 1.0, V.p, n, Zs, ldz, 0.0, W1.p, w));
