@@ -156,8 +156,21 @@ EM_DEVINL void gemm_tile(const GemmArgs& p, int64_t m0, int64_t n0, double* smem
 }
 
 template <int TA, int TB, int LOWER, int VEC>
-__global__ void __launch_bounds__(GTHREADS, 1) gemm_kernel(GemmArgs p) {
+__global__ void __launch_bounds__(GTHREADS, 1) gemm_kernel(GemmArgs p, double* ws, int64_t kc) {
   extern __shared__ __align__(16) double smem[];
+  if (ws) {
+    // split-K: slice z of the k range into its own m x n partial (alpha = 1, beta = 0)
+    const int64_t z = blockIdx.z;
+    const int64_t k0 = z * kc;
+    const int64_t kk = imin64(kc, p.k - k0);
+    p.A += TA ? k0 : k0 * p.lda;
+    p.B += TB ? k0 * p.ldb : k0;
+    p.k = kk;
+    p.C = ws + z * p.m * p.n;
+    p.ldc = p.m;
+    p.alpha = 1.0;
+    p.beta = 0.0;
+  }
   // grouped-M swizzle for L2 reuse: walk 8 m-tiles per n-tile column group
   const int64_t tiles_m = (p.m + GBM - 1) / GBM;
   const int64_t tiles_n = (p.n + GBN - 1) / GBN;
@@ -199,6 +212,22 @@ static size_t smem_bytes(int ta, int tb) {
   return (a + b) * GSTAGES * sizeof(double);
 }
 
+// C = alpha * sum_z W_z + beta * C  (split-K reduction, fixed order)
+__global__ void splitk_reduce_kernel(int64_t m, int64_t n, int splits, const double* __restrict__ ws,
+                                     double alpha, double beta, double* C, int64_t ldc, int lower,
+                                     int64_t diag_off) {
+  const int64_t total = m * n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i % m, c = i / m;
+    if (lower && r + diag_off < c) continue;
+    double s = 0.0;
+    for (int z = 0; z < splits; ++z) s += ws[z * total + i];
+    double* cp = C + r + c * ldc;
+    *cp = (beta == 0.0) ? alpha * s : fma(alpha, s, beta * *cp);
+  }
+}
+
 template <int TA, int TB, int LOWER, int VEC>
 static cudaError_t launch_t(const GemmArgs& p, cudaStream_t st) {
   auto k = gemm_kernel<TA, TB, LOWER, VEC>;
@@ -208,9 +237,35 @@ static cudaError_t launch_t(const GemmArgs& p, cudaStream_t st) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     configured = true;
   }
-  int64_t tiles = ((p.m + GBM - 1) / GBM) * ((p.n + GBN - 1) / GBN);
-  k<<<(unsigned)tiles, GTHREADS, sm, st>>>(p);
+  const int64_t tiles = ((p.m + GBM - 1) / GBM) * ((p.n + GBN - 1) / GBN);
+  const int sms = num_sms();
+  // few output tiles and a long k loop: split k so every SM has work
+  int64_t splits = 1;
+  if (tiles < sms && p.k >= 4 * 512) {
+    splits = imin64((2 * sms + tiles - 1) / tiles, p.k / 512);
+    splits = imax64(splits, 1);
+  }
+  if (splits <= 1) {
+    k<<<(unsigned)tiles, GTHREADS, sm, st>>>(p, nullptr, 0);
+    count_launch();
+    return cudaGetLastError();
+  }
+  int64_t kc = (p.k + splits - 1) / splits;
+  kc = (kc + GBK - 1) / GBK * GBK;  // whole k-tiles per split (alignment of the slices)
+  splits = (p.k + kc - 1) / kc;
+  double* ws = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&ws),
+                                  (size_t)splits * p.m * p.n * sizeof(double), st);
+  if (e != cudaSuccess) return e;
+  dim3 grid((unsigned)tiles, 1, (unsigned)splits);
+  k<<<grid, GTHREADS, sm, st>>>(p, ws, kc);
   count_launch();
+  const int64_t total = p.m * p.n;
+  const int blocks = (int)imin64((total + 255) / 256, 8 * sms);
+  splitk_reduce_kernel<<<blocks, 256, 0, st>>>(p.m, p.n, (int)splits, ws, p.alpha, p.beta, p.C,
+                                               p.ldc, LOWER, p.diag_off);
+  count_launch();
+  cudaFreeAsync(ws, st);
   return cudaGetLastError();
 }
 

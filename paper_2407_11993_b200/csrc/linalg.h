@@ -19,6 +19,10 @@ void trsm_lower(cudaStream_t st, bool trans, int64_t n, int64_t m, const double*
 constexpr int kTrsmBlock = 128;
 void trtri_blocks(cudaStream_t st, int nb, int64_t n, const double* C, int64_t ldc, double* Dinv);
 
+// sparse.cu: C = A B through a device CSR copy of the symmetric A when nnz <= max_fill n^2
+bool sym_sparse_mm(cudaStream_t st, int64_t n, const double* A, int64_t lda, int64_t m,
+                   const double* B, int64_t ldb, double* C, int64_t ldc, double max_fill);
+
 // symv.cu: y = alpha*A*x + beta*y using only the lower triangle of A (n x n)
 void symv_lower(cudaStream_t st, int64_t n, double alpha, const double* A, int64_t lda,
                 const double* x, double beta, double* y, double* work);

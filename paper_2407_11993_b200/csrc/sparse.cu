@@ -1,0 +1,95 @@
+// Sparse-aware product R V for the post-eigensolve quantities r_n = diag(V^T R V)
+// and V^T R (modal.py:80-81). The reference stores R dense (linalg.SymMatrix) and
+// multiplies densely; the synthetic plates' R is a 7-point stencil, so when R has
+// few nonzeros a CSR copy is built on the device (two passes over the dense
+// matrix) and R V becomes an HBM-bound SpMM instead of a 2 N^3 GEMM. The sum
+// over each row's nonzeros runs in increasing column order, i.e. the same terms
+// in the same order the dense product accumulates (zeros contribute exactly 0).
+#include <vector>
+
+#include "common.cuh"
+#include "ctx.h"
+#include "linalg.h"
+
+namespace em {
+
+// nnz per row (full symmetric matrix, column-major: row i of a symmetric matrix is
+// column i, read contiguously). One warp per row.
+__global__ void csr_count_kernel(int64_t n, const double* __restrict__ A, int64_t lda,
+                                 int64_t* __restrict__ cnt) {
+  const int64_t row = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  const double* col = A + row * lda;  // symmetric: column `row` == row `row`
+  int64_t c = 0;
+  for (int64_t k = lane; k < n; k += 32) c += (col[k] != 0.0);
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane == 0) cnt[row] = c;
+}
+
+// fill: one warp per row, ballot-compacted in increasing column order
+__global__ void csr_fill_kernel(int64_t n, const double* __restrict__ A, int64_t lda,
+                                const int64_t* __restrict__ rowptr, int* __restrict__ colidx,
+                                double* __restrict__ val) {
+  const int64_t row = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  const double* col = A + row * lda;
+  int64_t pos = rowptr[row];
+  for (int64_t k0 = 0; k0 < n; k0 += 32) {
+    const int64_t k = k0 + lane;
+    const double v = (k < n) ? col[k] : 0.0;
+    const unsigned mask = __ballot_sync(0xffffffffu, v != 0.0);
+    if (v != 0.0) {
+      const int off = __popc(mask & ((1u << lane) - 1u));
+      colidx[pos + off] = (int)k;
+      val[pos + off] = v;
+    }
+    pos += __popc(mask);
+  }
+}
+
+// C (n x m) = A_csr (n x n) * B (n x m); thread per (row, column)
+__global__ void csr_spmm_kernel(int64_t n, int64_t m, const int64_t* __restrict__ rowptr,
+                                const int* __restrict__ colidx, const double* __restrict__ val,
+                                const double* __restrict__ B, int64_t ldb, double* __restrict__ C,
+                                int64_t ldc) {
+  const int64_t total = n * m;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t % n, j = t / n;
+    const double* b = B + j * ldb;
+    double s = 0.0;
+    for (int64_t p = rowptr[i]; p < rowptr[i + 1]; ++p) s = fma(val[p], b[colidx[p]], s);
+    C[i + j * ldc] = s;
+  }
+}
+
+// C = A B using CSR when A (symmetric, n x n) has at most max_fill * n^2 nonzeros.
+// Returns false (and does nothing) when A is too dense.
+bool sym_sparse_mm(cudaStream_t st, int64_t n, const double* A, int64_t lda, int64_t m,
+                   const double* B, int64_t ldb, double* C, int64_t ldc, double max_fill) {
+  if (n <= 0 || m <= 0) return true;
+  DArr<int64_t> cnt(n + 1, st);
+  csr_count_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(n, A, lda, cnt.p);
+  EM_LAUNCHED();
+  std::vector<int64_t> h(n + 1, 0);
+  EM_CK(cudaMemcpyAsync(h.data() + 1, cnt.p, n * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  EM_CK(cudaStreamSynchronize(st));
+  for (int64_t i = 0; i < n; ++i) h[i + 1] += h[i];
+  const int64_t nnz = h[n];
+  if ((double)nnz > max_fill * (double)n * (double)n) return false;
+  EM_CK(cudaMemcpyAsync(cnt.p, h.data(), (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  DArr<int> colidx(imax64(nnz, 1), st);
+  DBuf val(imax64(nnz, 1), st);
+  csr_fill_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(n, A, lda, cnt.p, colidx.p, val.p);
+  EM_LAUNCHED();
+  const int64_t total = n * m;
+  const int blocks = (int)imin64((total + 255) / 256, 32 * num_sms());
+  csr_spmm_kernel<<<blocks, 256, 0, st>>>(n, m, cnt.p, colidx.p, val.p, B, ldb, C, ldc);
+  EM_LAUNCHED();
+  EM_CK(cudaStreamSynchronize(st));  // host vector h / device temporaries lifetime
+  return true;
+}
+
+}  // namespace em

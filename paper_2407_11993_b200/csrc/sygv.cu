@@ -170,7 +170,9 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
       RV = tmp.p;
       ldrv = n;
     }
-    EM_CK(gemm(st, false, false, n, n, n, 1.0, R, ldr, V, ldv, 0.0, RV, ldrv));
+    // R is typically a stencil stored dense (the reference's SymMatrix): use CSR then
+    if (!sym_sparse_mm(st, n, R, ldr, n, V, ldv, RV, ldrv, 0.02))
+      EM_CK(gemm(st, false, false, n, n, n, 1.0, R, ldr, V, ldv, 0.0, RV, ldrv));
     if (r_n) {
       coldot_kernel<<<(unsigned)n, 256, 0, st>>>(n, V, ldv, RV, ldrv, r_n);
       EM_LAUNCHED();

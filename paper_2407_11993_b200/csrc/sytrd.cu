@@ -6,7 +6,8 @@
 //
 // Per panel column the memory-bound part is one lower-triangle symv over the
 // trailing matrix (symv.cu); the rank-2k trailing update and the
-// back-transform run on the DMMA GEMM.
+// back-transform run on the DMMA GEMM. The per-column panel work (latrd) uses
+// 8 threads per row so that a 16k-row column update keeps ~130k threads busy.
 #include "common.cuh"
 #include "ctx.h"
 #include "gemm.h"
@@ -16,145 +17,191 @@ namespace em {
 
 constexpr int TRD_NB = 64;   // panel width
 constexpr int RT = 256;
+constexpr int TPR = 8;                 // threads per row in the panel kernels
+constexpr int ROWS_PER_CTA = RT / TPR;  // 32
 
-// A[c:n, c] -= A[c:n, i0:c] W[c, 0:i]^T + W[c:n, 0:i] A[c, i0:c]^T
-__global__ void latrd_colupd_kernel(int64_t n, double* A, int64_t lda, int64_t i0, int64_t c,
-                                    const double* __restrict__ W, int64_t ldw) {
-  const int i = (int)(c - i0);
-  __shared__ double wr[TRD_NB], ar[TRD_NB];
-  for (int k = threadIdx.x; k < i; k += blockDim.x) {
-    wr[k] = W[(c - i0) + k * ldw];     // W row c (W rows are indexed from i0)
-    ar[k] = A[c + (i0 + k) * lda];     // A row c
-  }
-  __syncthreads();
-  for (int64_t r = c + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
-       r += (int64_t)gridDim.x * blockDim.x) {
-    double s = A[r + c * lda];
-    for (int k = 0; k < i; ++k) {
-      s = fma(-A[r + (i0 + k) * lda], wr[k], s);
-      s = fma(-W[(r - i0) + k * ldw], ar[k], s);
-    }
-    A[r + c * lda] = s;
-  }
+EM_DEVINL double group_sum8(double v) {
+  v += __shfl_xor_sync(0xffffffffu, v, 4);
+  v += __shfl_xor_sync(0xffffffffu, v, 2);
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  return v;
 }
 
-// dlarfg on x = A[c+1:n, c]: beta, tau; v = [1, x[1:]/(alpha-beta)]; e[c] = beta; d[c] = A[c,c].
-// Single CTA (1024 threads).
-__global__ void larfg_kernel(int64_t n, double* A, int64_t lda, int64_t c, double* d, double* e,
-                             double* tau) {
-  __shared__ double red[32];
-  __shared__ double sc;
-  const int tid = threadIdx.x;
-  double ss = 0.0;
-  for (int64_t r = c + 2 + tid; r < n; r += blockDim.x) {
-    const double v = A[r + c * lda];
-    ss = fma(v, v, ss);
-  }
-  ss = warp_sum(ss);
-  if ((tid & 31) == 0) red[tid >> 5] = ss;
+EM_DEVINL double block_sum(double v, double* red) {
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
   __syncthreads();
-  if (tid < 32) {
-    double v = (tid < (int)(blockDim.x >> 5)) ? red[tid] : 0.0;
-    v = warp_sum(v);
-    if (tid == 0) {
-      const double alpha = A[(c + 1) + c * lda];
-      const double xnorm = sqrt(v);
-      d[c] = A[c + c * lda];
-      if (xnorm == 0.0) {
+  double t = 0.0;
+  if (threadIdx.x < 32) {
+    t = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
+    t = warp_sum(t);
+  }
+  return t;  // valid in thread 0
+}
+
+// A[c:n, c] -= A[c:n, i0:c] W[c, 0:i]^T + W[c:n, 0:i] A[c, i0:c]^T, then per-CTA
+// partial sums of squares of the updated A[c+2:n, c] (the dlarfg norm).
+__global__ void __launch_bounds__(RT) latrd_colupd_kernel(int64_t n, double* A, int64_t lda,
+                                                          int64_t i0, int64_t c,
+                                                          const double* __restrict__ W,
+                                                          int64_t ldw, double* part) {
+  const int i = (int)(c - i0);
+  __shared__ double wr[TRD_NB], ar[TRD_NB], red[RT / 32];
+  for (int k = threadIdx.x; k < i; k += blockDim.x) {
+    wr[k] = W[(c - i0) + k * ldw];  // W row c (W rows are indexed from i0)
+    ar[k] = A[c + (i0 + k) * lda];  // A row c
+  }
+  __syncthreads();
+  const int sub = threadIdx.x & (TPR - 1);
+  const int64_t r = c + blockIdx.x * (int64_t)ROWS_PER_CTA + threadIdx.x / TPR;
+  double ss = 0.0;
+  if (r < n) {
+    double s = 0.0;
+    for (int k = sub; k < i; k += TPR) {
+      s = fma(A[r + (i0 + k) * lda], wr[k], s);
+      s = fma(W[(r - i0) + k * ldw], ar[k], s);
+    }
+    s = group_sum8(s);
+    if (sub == 0) {
+      const double v = A[r + c * lda] - s;
+      if (i > 0) A[r + c * lda] = v;
+      if (r >= c + 2) ss = v * v;
+    }
+  } else {
+    group_sum8(0.0);
+  }
+  const double t = block_sum(ss, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = t;
+}
+
+// dlarfg on x = A[c+1:n, c] with ||x[1:]||^2 = sum(part): beta, tau; v = [1, x[1:]/(alpha-beta)];
+// e[c] = beta; d[c] = A[c,c]. Every CTA reduces the partials itself and scales its slice.
+__global__ void __launch_bounds__(RT) larfg_kernel(int64_t n, double* A, int64_t lda, int64_t c,
+                                                   const double* __restrict__ part, int nparts,
+                                                   double* d, double* e, double* tau) {
+  __shared__ double red[RT / 32];
+  __shared__ double sc;
+  double s = 0.0;
+  for (int p = threadIdx.x; p < nparts; p += blockDim.x) s += part[p];
+  const double tot = block_sum(s, red);
+  const double alpha = A[(c + 1) + c * lda];
+  if (threadIdx.x == 0) {
+    const double xnorm = sqrt(tot);
+    double scale = 0.0;
+    if (xnorm == 0.0) {
+      if (blockIdx.x == 0) {
         tau[c] = 0.0;
         e[c] = alpha;
-        sc = 0.0;
-      } else {
-        const double beta = -copysign(hypot(alpha, xnorm), alpha);
+      }
+    } else {
+      const double beta = -copysign(hypot(alpha, xnorm), alpha);
+      scale = 1.0 / (alpha - beta);
+      if (blockIdx.x == 0) {
         tau[c] = (beta - alpha) / beta;
-        sc = 1.0 / (alpha - beta);
         e[c] = beta;
       }
-      A[(c + 1) + c * lda] = 1.0;
     }
+    sc = scale;
   }
   __syncthreads();
-  const double s = sc;
-  if (s != 0.0)
-    for (int64_t r = c + 2 + tid; r < n; r += blockDim.x) A[r + c * lda] *= s;
+  const double f = sc;
+  if (f != 0.0)
+    for (int64_t r = c + 2 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x)
+      A[r + c * lda] *= f;
+  // every CTA has read alpha above; make sure all CTAs did before CTA 0 overwrites it
 }
 
-// tmp1[k] = W[c+1:, k] . v   tmp2[k] = A[c+1:, i0+k] . v   (k < i); one CTA per (k, which)
-__global__ void latrd_dots_kernel(int64_t n, const double* A, int64_t lda, int64_t i0, int64_t c,
-                                  const double* W, int64_t ldw, double* tmp) {
+__global__ void larfg_finish_kernel(double* A, int64_t lda, int64_t c, double* d) {
+  if (threadIdx.x == 0) {
+    d[c] = A[c + c * lda];
+    A[(c + 1) + c * lda] = 1.0;
+  }
+}
+
+// Partial dots: tmp[which][k] partials over row chunks of  W[c+1:, k].v (which 0)
+// and A[c+1:, i0+k].v (which 1). grid (chunks, ceil(2i/8)); warp per column.
+constexpr int DOT_ROWS = 2048;
+__global__ void __launch_bounds__(RT) latrd_dots_kernel(int64_t n, const double* A, int64_t lda,
+                                                        int64_t i0, int64_t c, const double* W,
+                                                        int64_t ldw, double* dpart, int nchunk) {
   const int i = (int)(c - i0);
-  const int k = blockIdx.x % i;
-  const int which = blockIdx.x / i;
-  __shared__ double red[32];
+  const int col = blockIdx.y * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (col >= 2 * i) return;
+  const int which = col / i, k = col % i;
+  const int64_t rb = c + 1 + blockIdx.x * (int64_t)DOT_ROWS;
+  const int64_t re = imin64(n, rb + DOT_ROWS);
   const double* v = A + c * lda;
+  const double* colp = which == 0 ? W + k * ldw - i0 : A + (i0 + k) * lda;
   double s = 0.0;
-  for (int64_t r = c + 1 + threadIdx.x; r < n; r += blockDim.x) {
-    const double col = which == 0 ? W[(r - i0) + k * ldw] : A[r + (i0 + k) * lda];
-    s = fma(col, v[r], s);
-  }
+  for (int64_t r = rb + lane; r < re; r += 32) s = fma(colp[r], v[r], s);
   s = warp_sum(s);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    double t = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
-    t = warp_sum(t);
-    if (threadIdx.x == 0) tmp[which * TRD_NB + k] = t;
-  }
+  if (lane == 0) dpart[(which * TRD_NB + k) * nchunk + blockIdx.x] = s;
 }
 
-// w = tau*(w - A_p tmp1 - W_p tmp2); partial dots of w.v per CTA
-__global__ void latrd_wcol_kernel(int64_t n, const double* A, int64_t lda, int64_t i0, int64_t c,
-                                  double* W, int64_t ldw, const double* tmp, const double* tau,
-                                  double* part) {
+// w = tau*(w - A_p t1 - W_p t2), t1/t2 summed from the chunk partials; per-CTA
+// partial dot of w and v.
+__global__ void __launch_bounds__(RT) latrd_wcol_kernel(int64_t n, const double* A, int64_t lda,
+                                                        int64_t i0, int64_t c, double* W,
+                                                        int64_t ldw, const double* dpart,
+                                                        int nchunk, const double* tau,
+                                                        double* part) {
   const int i = (int)(c - i0);
-  __shared__ double t1[TRD_NB], t2[TRD_NB], red[32];
-  for (int k = threadIdx.x; k < i; k += blockDim.x) {
-    t1[k] = tmp[k];
-    t2[k] = tmp[TRD_NB + k];
+  __shared__ double t1[TRD_NB], t2[TRD_NB], red[RT / 32];
+  for (int q = threadIdx.x; q < 2 * i; q += blockDim.x) {
+    const int which = q / i, k = q % i;
+    double s = 0.0;
+    for (int ch = 0; ch < nchunk; ++ch) s += dpart[(which * TRD_NB + k) * nchunk + ch];
+    if (which == 0)
+      t1[k] = s;
+    else
+      t2[k] = s;
   }
   __syncthreads();
   const double tc = tau[c];
   const double* v = A + c * lda;
   double* w = W + i * ldw;
-  double s = 0.0;
-  for (int64_t r = c + 1 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
-       r += (int64_t)gridDim.x * blockDim.x) {
-    double x = w[r - i0];
-    for (int k = 0; k < i; ++k) {
-      x = fma(-A[r + (i0 + k) * lda], t1[k], x);
-      x = fma(-W[(r - i0) + k * ldw], t2[k], x);
+  const int sub = threadIdx.x & (TPR - 1);
+  const int64_t r = c + 1 + blockIdx.x * (int64_t)ROWS_PER_CTA + threadIdx.x / TPR;
+  double dd = 0.0;
+  if (r < n) {
+    double s = 0.0;
+    for (int k = sub; k < i; k += TPR) {
+      s = fma(A[r + (i0 + k) * lda], t1[k], s);
+      s = fma(W[(r - i0) + k * ldw], t2[k], s);
     }
-    x *= tc;
-    w[r - i0] = x;
-    s = fma(x, v[r], s);
+    s = group_sum8(s);
+    if (sub == 0) {
+      const double x = tc * (w[r - i0] - s);
+      w[r - i0] = x;
+      dd = x * v[r];
+    }
+  } else {
+    group_sum8(0.0);
   }
-  s = warp_sum(s);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    double t = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
-    t = warp_sum(t);
-    if (threadIdx.x == 0) part[blockIdx.x] = t;
-  }
+  const double t = block_sum(dd, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = t;
 }
 
 // w += alpha v,  alpha = -tau/2 * (w.v)
 __global__ void latrd_wfix_kernel(int64_t n, const double* A, int64_t lda, int64_t i0, int64_t c,
                                   double* W, int64_t ldw, const double* tau, const double* part,
                                   int nparts) {
+  __shared__ double red[RT / 32];
+  double s = 0.0;
+  for (int p = threadIdx.x; p < nparts; p += blockDim.x) s += part[p];
   __shared__ double alpha;
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int p = 0; p < nparts; ++p) s += part[p];
-    alpha = -0.5 * tau[c] * s;
-  }
+  const double tot = block_sum(s, red);
+  if (threadIdx.x == 0) alpha = -0.5 * tau[c] * tot;
   __syncthreads();
   const int i = (int)(c - i0);
   const double* v = A + c * lda;
   double* w = W + i * ldw;
+  const double a = alpha;
   for (int64_t r = c + 1 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
        r += (int64_t)gridDim.x * blockDim.x)
-    w[r - i0] = fma(alpha, v[r], w[r - i0]);
+    w[r - i0] = fma(a, v[r], w[r - i0]);
 }
 
 __global__ void set_diag_kernel(int64_t n, const double* A, int64_t lda, int64_t c, double* d) {
@@ -171,8 +218,6 @@ __global__ void restore_sub_kernel(int64_t n, double* A, int64_t lda, int64_t i0
   }
 }
 
-static int grid_for(int64_t m) { return (int)imax64(1, imin64((m + RT - 1) / RT, 4 * num_sms())); }
-
 void sytrd_lower(cudaStream_t st, int64_t n, double* A, int64_t lda, double* d, double* e,
                  double* tau) {
   if (n <= 0) return;
@@ -183,40 +228,47 @@ void sytrd_lower(cudaStream_t st, int64_t n, double* A, int64_t lda, double* d, 
   }
   DBuf W((size_t)n * TRD_NB, st);
   DBuf XW((size_t)n * 2 * TRD_NB, st), YW((size_t)n * 2 * TRD_NB, st);
-  DBuf tmp(2 * TRD_NB, st);
-  const int maxparts = 4 * num_sms();
-  DBuf part(maxparts, st);
+  const int max_rows_ctas = (int)((n + ROWS_PER_CTA - 1) / ROWS_PER_CTA);
+  DBuf part(imax64(max_rows_ctas, 1), st);
+  const int max_chunks = (int)((n + DOT_ROWS - 1) / DOT_ROWS);
+  DBuf dpart((size_t)2 * TRD_NB * max_chunks, st);
   DBuf swork(symv_work_size(n), st);
   for (int64_t i0 = 0; i0 < n; i0 += TRD_NB) {
     const int w = (int)imin64(TRD_NB, n - i0);
     for (int i = 0; i < w; ++i) {
       const int64_t c = i0 + i;
-      if (i > 0) {
-        latrd_colupd_kernel<<<grid_for(n - c), RT, 0, st>>>(n, A, lda, i0, c, W.p, n);
-        EM_LAUNCHED();
-      }
+      const int gcol = (int)((n - c + ROWS_PER_CTA - 1) / ROWS_PER_CTA);
+      latrd_colupd_kernel<<<gcol, RT, 0, st>>>(n, A, lda, i0, c, W.p, n, part.p);
+      EM_LAUNCHED();
       if (c == n - 1) {
         set_diag_kernel<<<1, 32, 0, st>>>(n, A, lda, c, d);
         EM_LAUNCHED();
         break;
       }
-      larfg_kernel<<<1, 1024, 0, st>>>(n, A, lda, c, d, e, tau);
-      EM_LAUNCHED();
       const int64_t m = n - c - 1;
+      const int gsc = (int)imax64(1, imin64((m + RT - 1) / RT, 2 * num_sms()));
+      larfg_kernel<<<gsc, RT, 0, st>>>(n, A, lda, c, part.p, gcol, d, e, tau);
+      EM_LAUNCHED();
+      larfg_finish_kernel<<<1, 32, 0, st>>>(A, lda, c, d);
+      EM_LAUNCHED();
       // W[c+1:, i] = A22 v  (A22 = trailing lower triangle)
       {
         Stage s(st, ST_SYTRD_SYMV);
         symv_lower(st, m, 1.0, A + (c + 1) + (c + 1) * lda, lda, A + (c + 1) + c * lda, 0.0,
                    W.p + (c + 1 - i0) + (int64_t)i * n, swork.p);
       }
+      const int nchunk = (int)((m + DOT_ROWS - 1) / DOT_ROWS);
       if (i > 0) {
-        latrd_dots_kernel<<<2 * i, RT, 0, st>>>(n, A, lda, i0, c, W.p, n, tmp.p);
+        dim3 gd((unsigned)nchunk, (unsigned)((2 * i + 7) / 8));
+        latrd_dots_kernel<<<gd, RT, 0, st>>>(n, A, lda, i0, c, W.p, n, dpart.p, nchunk);
         EM_LAUNCHED();
       }
-      const int g = grid_for(m);
-      latrd_wcol_kernel<<<g, RT, 0, st>>>(n, A, lda, i0, c, W.p, n, tmp.p, tau, part.p);
+      const int gw = (int)((m + ROWS_PER_CTA - 1) / ROWS_PER_CTA);
+      latrd_wcol_kernel<<<gw, RT, 0, st>>>(n, A, lda, i0, c, W.p, n, dpart.p, nchunk, tau,
+                                           part.p);
       EM_LAUNCHED();
-      latrd_wfix_kernel<<<g, RT, 0, st>>>(n, A, lda, i0, c, W.p, n, tau, part.p, g);
+      const int gf = (int)imax64(1, imin64((m + RT - 1) / RT, 2 * num_sms()));
+      latrd_wfix_kernel<<<gf, RT, 0, st>>>(n, A, lda, i0, c, W.p, n, tau, part.p, gw);
       EM_LAUNCHED();
     }
     const int64_t t0 = i0 + w;
