@@ -286,6 +286,8 @@ def run_ours(args, cfg, rank, world, local_rank):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     nat.context()
+    if args.two_stage is not None:
+        nat.set_two_stage_min(args.two_stage)
     m = build_inputs(cfg)
     n = m["plate"].n
     T, nth = cfg["steps"], len(cfg["thetas"])
@@ -519,6 +521,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-td1", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--two-stage", type=int, default=None,
+                    help="smallest n for the two-stage tridiagonalisation (default: library)")
     ap.add_argument("--profile-fine", action="store_true",
                     help="one extra untimed step with per-call stage events (stderr)")
     args = ap.parse_args()

@@ -50,6 +50,11 @@ const char* em_last_error(const em_ctx* ctx);
 /* Number of kernels this library has launched on ctx (for launch accounting). */
 int64_t em_launch_count(const em_ctx* ctx);
 int em_synchronize(em_ctx* ctx);
+/* Tuning knobs. EM_CFG_TWO_STAGE_MIN: smallest n that uses the two-stage
+ * (dense -> band -> tridiagonal) reduction in em_syev/em_sygv (default INT64_MAX:
+ * one-stage Householder everywhere). */
+#define EM_CFG_TWO_STAGE_MIN 1
+int em_config(em_ctx* ctx, int key, int64_t value);
 /* Stage timers (CUDA events on the context stream). em_profile(ctx, 1) clears and
  * enables them; em_stage_times fills per-stage milliseconds / event-pair counts
  * (stage ids: potrf_R, sygst, potrf_L, sytrd, stedc, ormtr, trsm_back, finalize,
@@ -65,6 +70,11 @@ int em_stage_times(em_ctx* ctx, double* ms, int64_t* counts, int n);
 int em_dgemm(em_ctx* ctx, int trans_a, int trans_b, int64_t m, int64_t n, int64_t k,
              double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
              double beta, double* C, int64_t ldc);
+
+/* y = alpha A x + beta y for symmetric A reading only its lower triangle (the dense
+ * R @ state loop of td1_step_kernel, _kernels.py:203-207). HBM-bound. */
+int em_symv_lower(em_ctx* ctx, int64_t n, double alpha, const double* A, int64_t lda,
+                  const double* x, double beta, double* y);
 
 /* Mirror the lower triangle into the upper one in place (linalg.py:34-41 SymMatrix). */
 int em_sym_mirror_lower(em_ctx* ctx, int64_t n, double* A, int64_t lda);

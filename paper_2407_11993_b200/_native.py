@@ -33,10 +33,12 @@ SIGNATURES = {
     "em_last_error": (ctypes.c_char_p, [_P]),
     "em_launch_count": (_I64, [_P]),
     "em_synchronize": (_I, [_P]),
+    "em_config": (_I, [_P, _I, _I64]),
     "em_profile": (_I, [_P, _I]),
     "em_stage_times": (_I, [_P, _P, _P, _I]),
     "em_dgemm": (_I, [_P, _I, _I, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D, _P, _I64]),
     "em_sym_mirror_lower": (_I, [_P, _I64, _P, _I64]),
+    "em_symv_lower": (_I, [_P, _I64, _D, _P, _I64, _P, _D, _P]),
     "em_potrf": (_I, [_P, _I64, _P, _I64, ctypes.POINTER(_I64)]),
     "em_trsm_lower": (_I, [_P, _I, _I64, _I64, _P, _I64, _P, _I64]),
     "em_syev": (_I, [_P, _I64, _P, _I64, _P, _P, _I64]),
@@ -124,7 +126,8 @@ def launches() -> int:
 
 STAGES = ("potrf_R", "sygst", "potrf_L", "sytrd", "stedc", "ormtr", "trsm_back", "finalize",
           "post_gemm", "td2_local", "td2_carry", "td2_replay", "td1_symv", "td1_fwd", "td1_bwd",
-          "sytrd_symv", "sytrd_syr2k", "stedc_gemm", "stedc_secular")
+          "sytrd_symv", "sytrd_syr2k", "stedc_gemm", "stedc_secular", "sy2sb", "sb2st", "q2_apply",
+          "q1_apply", "sy2sb_qr")
 
 
 def profile(level: int = 1) -> None:
@@ -141,6 +144,14 @@ def stage_times() -> dict:
     if rc < 0:
         check(rc, "em_stage_times")
     return {STAGES[i]: (ms[i], cnt[i]) for i in range(n) if cnt[i]}
+
+
+EM_CFG_TWO_STAGE_MIN = 1
+
+
+def set_two_stage_min(n: int) -> None:
+    """Smallest order that uses the two-stage tridiagonalisation (default: never)."""
+    check(load_library().em_config(context(), EM_CFG_TWO_STAGE_MIN, int(n)), "em_config")
 
 
 def synchronize() -> None:

@@ -14,6 +14,7 @@ struct em_td2_plan;
 struct em_td1_plan;
 
 namespace em {
+extern int64_t g_two_stage_min;
 void stages_reset(bool on);
 void stages_level(int level);
 int stages_read(double* ms, int64_t* counts, int n);
@@ -123,6 +124,16 @@ int em_stage_times(em_ctx* ctx, double* ms, int64_t* counts, int n) {
   });
 }
 
+int em_config(em_ctx* ctx, int key, int64_t value) {
+  return guarded(ctx, [&] {
+    if (key == EM_CFG_TWO_STAGE_MIN) {
+      em::g_two_stage_min = value;
+      return EM_OK;
+    }
+    throw em::ArgError{"unknown em_config key"};
+  });
+}
+
 int em_synchronize(em_ctx* ctx) {
   return guarded(ctx, [&] {
     EM_CK(cudaStreamSynchronize(ctx->stream));
@@ -135,6 +146,15 @@ int em_dgemm(em_ctx* ctx, int ta, int tb, int64_t m, int64_t n, int64_t k, doubl
              int64_t ldc) {
   return guarded(ctx, [&] {
     EM_CK(em::gemm(ctx->stream, ta != 0, tb != 0, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc));
+    return EM_OK;
+  });
+}
+
+int em_symv_lower(em_ctx* ctx, int64_t n, double alpha, const double* A, int64_t lda,
+                  const double* x, double beta, double* y) {
+  return guarded(ctx, [&] {
+    em::DBuf work(em::symv_work_size(n), ctx->stream);
+    em::symv_lower(ctx->stream, n, alpha, A, lda, x, beta, y, work.p);
     return EM_OK;
   });
 }

@@ -87,6 +87,7 @@ enum StageId {
   ST_POTRF_R = 0, ST_SYGST, ST_POTRF_L, ST_SYTRD, ST_STEDC, ST_ORMTR, ST_TRSM_BACK,
   ST_FINALIZE, ST_POST_GEMM, ST_TD2_LOCAL, ST_TD2_CARRY, ST_TD2_REPLAY, ST_TD1_SYMV,
   ST_TD1_FWD, ST_TD1_BWD, ST_SYTRD_SYMV, ST_SYTRD_SYR2K, ST_STEDC_GEMM, ST_STEDC_SECULAR,
+  ST_SY2SB, ST_SB2ST, ST_Q2, ST_Q1, ST_SY2SB_QR,
   ST_COUNT
 };
 void stage_begin(cudaStream_t st, int id);

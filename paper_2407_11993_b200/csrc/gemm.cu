@@ -240,10 +240,21 @@ static cudaError_t launch_t(const GemmArgs& p, cudaStream_t st) {
   const int64_t tiles = ((p.m + GBM - 1) / GBM) * ((p.n + GBN - 1) / GBN);
   const int sms = num_sms();
   // few output tiles and a long k loop: split k so every SM has work
+  // pick the split count with the best wave quantisation (each slice >= 512 deep)
   int64_t splits = 1;
-  if (tiles < sms && p.k >= 4 * 512) {
-    splits = imin64((2 * sms + tiles - 1) / tiles, p.k / 512);
-    splits = imax64(splits, 1);
+  if (tiles < 4 * sms && p.k >= 2 * 512) {
+    auto eff = [&](int64_t s) {
+      const int64_t ctas = tiles * s;
+      return (double)ctas / (double)(((ctas + sms - 1) / sms) * sms);
+    };
+    double best = eff(1);
+    for (int64_t s = 2; s <= 16 && p.k / s >= 512; ++s) {
+      const double e = eff(s);
+      if (e > best + 0.03) {
+        best = e;
+        splits = s;
+      }
+    }
   }
   if (splits <= 1) {
     k<<<(unsigned)tiles, GTHREADS, sm, st>>>(p, nullptr, 0);

@@ -35,6 +35,18 @@ void sytrd_lower(cudaStream_t st, int64_t n, double* A, int64_t lda, double* d, 
 // ormtr: Z <- Q Z with Q = H(0) ... H(n-2) from sytrd_lower (Z n x m)
 void ormtr_lower(cudaStream_t st, int64_t n, int64_t m, const double* A, int64_t lda,
                  const double* tau, double* Z, int64_t ldz);
+// Z <- H(0) ... H(nref-1) Z, reflector c's vector starts at row c + off of column c of A
+void ormqr_lower_off(cudaStream_t st, int64_t n, int64_t nref, int64_t off, int64_t m,
+                     const double* A, int64_t lda, const double* tau, double* Z, int64_t ldz);
+
+// sytrd2.cu: two-stage tridiagonalisation (dense -> band b -> tridiagonal) with the
+// eigenvector back-transforms: syev_two_stage computes ascending w and Z for A (destroyed)
+void syev_two_stage(cudaStream_t st, int64_t n, double* A, int64_t lda, double* w, double* Z,
+                    int64_t ldz);
+// stage pieces (exposed for tests): A -> band AB (ldab = 2b+1, band rows 0..b filled)
+void sy2sb(cudaStream_t st, int64_t n, double* A, int64_t lda, double* tau1, double* AB,
+           int64_t ldab);
+constexpr int kBand = 64;
 
 // stedc.cu: tridiagonal eigensolver (divide and conquer). Eigenvalues ascending in d,
 // eigenvectors in Z (n x n, ld ldz). e is destroyed.

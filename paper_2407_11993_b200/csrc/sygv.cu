@@ -13,9 +13,17 @@
 
 namespace em {
 
+// em_config(EM_CFG_TWO_STAGE_MIN). Off by default until the two-stage path beats the
+// one-stage one end to end; tests force it on.
+int64_t g_two_stage_min = INT64_MAX;
+
 void syev_ascending(cudaStream_t st, int64_t n, double* A, int64_t lda, double* w, double* Z,
                     int64_t ldz) {
   if (n <= 0) return;
+  if (n >= g_two_stage_min && n > 2 * kBand) {
+    syev_two_stage(st, n, A, lda, w, Z, ldz);
+    return;
+  }
   DBuf d(n, st), e(imax64(n - 1, 1), st), tau(imax64(n - 1, 1), st);
   {
     Stage s(st, ST_SYTRD);

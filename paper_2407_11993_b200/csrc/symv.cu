@@ -151,18 +151,39 @@ __global__ void __launch_bounds__(SVT) symv_tiles_kernel(int64_t n, const double
   }
 }
 
-__global__ void symv_reduce_kernel(int64_t n, double alpha, double beta, double* __restrict__ y,
-                                   const double* __restrict__ wcol,
-                                   const double* __restrict__ wrow, int64_t nb, int64_t nch) {
-  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (idx >= n) return;
-  const int64_t j = idx / SV;
-  const int t = (int)(idx % SV);
-  double s = 0.0;
-  const int64_t nchj = j / SVCH + 1;  // chunks present in block row j
-  for (int64_t c = 0; c < nchj; ++c) s += wrow[(j * nch + c) * SV + t];
-  for (int64_t i = j; i < nb; ++i) s += wcol[(i * nb + j) * SV + t];
-  y[idx] = (beta == 0.0) ? alpha * s : fma(alpha, s, beta * y[idx]);
+// y block j: sum of the row-strip partials of block row j and of the transposed
+// tile partials of block column j (tiles (i, j), i >= j). One CTA per block; the
+// column sum is split over 4 interleaved i-slices (fixed order) for memory-level
+// parallelism, then combined in shared memory.
+__global__ void __launch_bounds__(256) symv_reduce_kernel(int64_t n, double alpha, double beta,
+                                                          double* __restrict__ y,
+                                                          const double* __restrict__ wcol,
+                                                          const double* __restrict__ wrow,
+                                                          int64_t nb, int64_t nch) {
+  __shared__ double red[4][SV];
+  const int64_t j = blockIdx.x;
+  const int t = threadIdx.x & (SV - 1), g = threadIdx.x >> 6;
+  double s0 = 0.0, s1 = 0.0;
+  int64_t i = j + g;
+  for (; i + 4 < nb; i += 8) {
+    s0 += wcol[(i * nb + j) * SV + t];
+    s1 += wcol[((i + 4) * nb + j) * SV + t];
+  }
+  if (i < nb) s0 += wcol[(i * nb + j) * SV + t];
+  double s = s0 + s1;
+  if (g == 0) {
+    const int64_t nchj = j / SVCH + 1;  // chunks present in block row j
+    for (int64_t c = 0; c < nchj; ++c) s += wrow[(j * nch + c) * SV + t];
+  }
+  red[g][t] = s;
+  __syncthreads();
+  if (threadIdx.x < SV) {
+    const int64_t idx = j * SV + t;
+    if (idx < n) {
+      const double v = (red[0][t] + red[1][t]) + (red[2][t] + red[3][t]);
+      y[idx] = (beta == 0.0) ? alpha * v : fma(alpha, v, beta * y[idx]);
+    }
+  }
 }
 
 void symv_lower(cudaStream_t st, int64_t n, double alpha, const double* A, int64_t lda,
@@ -175,8 +196,7 @@ void symv_lower(cudaStream_t st, int64_t n, double alpha, const double* A, int64
   dim3 grid((unsigned)nch, (unsigned)nb);
   symv_tiles_kernel<<<grid, SVT, 0, st>>>(n, A, lda, x, wcol, wrow, nb, nch);
   EM_LAUNCHED();
-  symv_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, alpha, beta, y, wcol, wrow,
-                                                                  nb, nch);
+  symv_reduce_kernel<<<(unsigned)nb, 256, 0, st>>>(n, alpha, beta, y, wcol, wrow, nb, nch);
   EM_LAUNCHED();
 }
 

@@ -1,0 +1,675 @@
+// Two-stage tridiagonalisation for the symmetric eigensolve (north-star (a)):
+//
+//   stage 1 (sy2sb)  dense -> band of width b = 64: per 64-column panel a
+//                    Householder QR (one cooperative kernel: the panel lives in
+//                    shared memory across all SMs, two grid barriers per column),
+//                    then the two-sided update A22 <- Q^T A22 Q as DMMA GEMMs
+//                    (X = A22 V T, W = X - V T^T V^T X / 2, A22 -= V W^T + W V^T).
+//                    No matrix-vector product over the trailing matrix: the
+//                    memory-bound symv of one-stage sytrd disappears.
+//   stage 2 (sb2st)  band -> tridiagonal by bulge chasing: one persistent kernel,
+//                    sweep s owned by CTA s mod P, task k of sweep s waits until
+//                    sweep s-1 finished task k+2 (release/acquire progress flags);
+//                    the band (2b+1 diagonals, bulge room) stays L2-resident.
+//   back-transform   Z <- Q2 Z: stage-2 reflectors of b consecutive sweeps and the
+//                    same block position form one compact-WY block (V: 2b-1 x b
+//                    parallelogram, T precomputed per block); blocks are applied per
+//                    sweep group (last group first) in ascending position order,
+//                    which respects every non-commuting pair. A persistent kernel
+//                    gives each CTA a column slab of Z and runs the whole sequence
+//                    on DMMA in shared memory. Then Z <- Q1 Z (compact WY, GEMM).
+//
+// Replaces the reference's cyclic Jacobi (_kernels.py:82-141) for large n.
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+#include "ctx.h"
+#include "gemm.h"
+#include "linalg.h"
+
+namespace em {
+
+constexpr int B2 = kBand;  // 64
+
+// ---- grid-wide barrier (all CTAs co-resident: cooperative launch) ----------------
+struct GridBar {
+  unsigned int count;
+  unsigned int gen;
+};
+
+EM_DEVINL void grid_sync(GridBar* bar, unsigned nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned int* vgen = &bar->gen;
+    const unsigned int g = *vgen;
+    __threadfence();
+    if (atomicAdd(&bar->count, 1u) == nblocks - 1) {
+      bar->count = 0;
+      __threadfence();
+      atomicAdd(&bar->gen, 1u);
+    } else {
+      while (*vgen == g) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+EM_DEVINL double block_reduce_sum(double v, double* red) {
+  v = warp_sum(v);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x < 32) {
+    t = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
+    t = warp_sum(t);
+  }
+  return t;  // valid in thread 0
+}
+
+// ---- stage 1: cooperative panel QR ----------------------------------------------
+struct QRArgs {
+  int64_t m;      // panel rows
+  int nbw;        // panel columns (<= 64)
+  int p;          // reflectors = min(m, nbw)
+  double* P;      // panel (m x nbw, ld ldp), in place: R above, V below the diagonal
+  int64_t ldp;
+  double* tau;    // p
+  double* part;   // G + G*64 + 1 scratch
+  GridBar* bar;
+  int R;          // rows per CTA
+};
+
+__global__ void __launch_bounds__(256) qr_panel_kernel(QRArgs a) {
+  extern __shared__ double S[];  // column-major [nbw][R]
+  __shared__ double red[8];
+  __shared__ double bc[4];
+  __shared__ double wsh[B2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned G = gridDim.x;
+  const int64_t r0 = blockIdx.x * (int64_t)a.R;
+  const int nr = (int)imax64(0, imin64(a.R, a.m - r0));
+  double* normpart = a.part;
+  double* dotpart = a.part + G;
+  double* alpha_slot = a.part + G + (size_t)G * B2;
+  for (int idx = tid; idx < nr * a.nbw; idx += blockDim.x) {
+    const int lr = idx % nr, c = idx / nr;
+    S[c * a.R + lr] = a.P[(r0 + lr) + c * a.ldp];
+  }
+  __syncthreads();
+  for (int j = 0; j < a.p; ++j) {
+    double* Sj = S + j * a.R;
+    // (a) partial sum of squares below the diagonal; the owner of row j publishes alpha
+    double ss = 0.0;
+    for (int lr = tid; lr < nr; lr += blockDim.x) {
+      const int64_t r = r0 + lr;
+      if (r > j) ss = fma(Sj[lr], Sj[lr], ss);
+      else if (r == j) *alpha_slot = Sj[lr];
+    }
+    ss = block_reduce_sum(ss, red);
+    if (tid == 0) normpart[blockIdx.x] = ss;
+    grid_sync(a.bar, G);
+    // (b) every CTA forms beta, tau, scale identically
+    if (tid == 0) {
+      double xs = 0.0;
+      for (unsigned b = 0; b < G; ++b) xs += normpart[b];
+      const double alpha = *(volatile double*)alpha_slot;
+      const double xnorm = sqrt(xs);
+      double beta, tau, scale;
+      if (xnorm == 0.0) {
+        tau = 0.0;
+        beta = alpha;
+        scale = 0.0;
+      } else {
+        beta = -copysign(hypot(alpha, xnorm), alpha);
+        tau = (beta - alpha) / beta;
+        scale = 1.0 / (alpha - beta);
+      }
+      bc[0] = beta;
+      bc[1] = tau;
+      bc[2] = scale;
+      if (blockIdx.x == 0) a.tau[j] = tau;
+    }
+    __syncthreads();
+    const double beta = bc[0], tau = bc[1], scale = bc[2];
+    for (int lr = tid; lr < nr; lr += blockDim.x) {
+      const int64_t r = r0 + lr;
+      if (r > j && scale != 0.0) Sj[lr] *= scale;
+      else if (r == j) Sj[lr] = beta;
+    }
+    __syncthreads();
+    // (c) partial w_c = v^T P[:, c] for c > j (v_j = 1)
+    for (int c = j + 1 + warp; c < a.nbw; c += 8) {
+      const double* Sc = S + c * a.R;
+      double s = 0.0;
+      for (int lr = lane; lr < nr; lr += 32) {
+        const int64_t r = r0 + lr;
+        if (r >= j) s = fma(r == j ? 1.0 : Sj[lr], Sc[lr], s);
+      }
+      s = warp_sum(s);
+      if (lane == 0) dotpart[(size_t)blockIdx.x * B2 + c] = s;
+    }
+    grid_sync(a.bar, G);
+    // (d) apply H_j to the remaining columns of the own rows
+    for (int c = j + 1 + tid; c < a.nbw; c += blockDim.x) {
+      double s = 0.0;
+      for (unsigned b = 0; b < G; ++b) s += dotpart[(size_t)b * B2 + c];
+      wsh[c] = s;
+    }
+    __syncthreads();
+    if (tau != 0.0) {
+      const int ncol = a.nbw - j - 1;
+      for (int idx = tid; idx < nr * ncol; idx += blockDim.x) {
+        const int lr = idx % nr, c = j + 1 + idx / nr;
+        const int64_t r = r0 + lr;
+        if (r >= j) {
+          const double v = (r == j) ? 1.0 : Sj[lr];
+          S[c * a.R + lr] = fma(-tau * wsh[c], v, S[c * a.R + lr]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  for (int idx = tid; idx < nr * a.nbw; idx += blockDim.x) {
+    const int lr = idx % nr, c = idx / nr;
+    a.P[(r0 + lr) + c * a.ldp] = S[c * a.R + lr];
+  }
+}
+
+__global__ void band_extract_kernel(int64_t n, int b, const double* __restrict__ A, int64_t lda,
+                                    double* __restrict__ AB, int64_t ldab) {
+  const int64_t c = blockIdx.x;
+  for (int d = threadIdx.x; d < ldab; d += blockDim.x) {
+    const int64_t r = c + d;
+    AB[d + c * ldab] = (d <= b && r < n) ? A[r + c * lda] : 0.0;
+  }
+}
+
+// larft (forward, columnwise) for w <= 128 reflectors from G = V^T V (sytrd.cu)
+__global__ void __launch_bounds__(128) larft_smem_kernel(int w, int w1,
+                                                         const double* __restrict__ G,
+                                                         int64_t ldg,
+                                                         const double* __restrict__ tau,
+                                                         int64_t c0, double* T, int64_t ldt);
+__global__ void build_v_kernel(int64_t n, const double* A, int64_t lda, int64_t i0, int w,
+                               int64_t off, double* V, int64_t ldv);
+
+static void coop_launch(const void* fn, unsigned grid, unsigned block, void** args, size_t smem,
+                        cudaStream_t st) {
+  EM_CK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(block), args, smem, st));
+  count_launch();
+}
+
+void sy2sb(cudaStream_t st, int64_t n, double* A, int64_t lda, double* tau1, double* AB,
+           int64_t ldab) {
+  const int b = B2;
+  const int sms = num_sms();
+  DBuf VW((size_t)n * 2 * b, st), WV((size_t)n * 2 * b, st), VT((size_t)n * b, st);
+  DBuf Gm((size_t)b * b, st), T((size_t)b * b, st), Y((size_t)b * b, st), M((size_t)b * b, st);
+  DBuf part((size_t)sms + (size_t)sms * b + 8, st);
+  DArr<GridBar> bar(1, st);
+  EM_CK(cudaMemsetAsync(bar.p, 0, sizeof(GridBar), st));
+  EM_CK(cudaFuncSetAttribute(qr_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             200 * 1024));
+  EM_CK(cudaFuncSetAttribute(larft_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(128 * 129 * sizeof(double))));
+  for (int64_t k0 = 0; k0 + b < n; k0 += b) {
+    const int64_t m = n - k0 - b;
+    const int p = (int)imin64(b, m);
+    double* P = A + (k0 + b) + k0 * lda;
+    double* A22 = A + (k0 + b) + (k0 + b) * lda;
+    // panel QR
+    {
+      const int64_t gmax = imax64(1, imin64(sms, (m + 15) / 16));
+      const int R = (int)(((m + gmax - 1) / gmax + 7) / 8 * 8);
+      const unsigned G = (unsigned)((m + R - 1) / R);
+      QRArgs qa{m, b, p, P, lda, tau1 + k0, part.p, bar.p, R};
+      void* args[] = {&qa};
+      Stage sq(st, ST_SY2SB_QR);
+      coop_launch((const void*)qr_panel_kernel, G, 256, args, (size_t)R * b * sizeof(double), st);
+    }
+    // V (m x p) into VW[:, 0:p]; T from G = V^T V
+    double* V = VW.p;
+    double* X = VW.p + (size_t)p * n;
+    dim3 gv((unsigned)imax64(1, imin64((m + 255) / 256, 64)), (unsigned)p);
+    build_v_kernel<<<gv, 256, 0, st>>>(n, A, lda, k0, p, b, V, n);
+    EM_LAUNCHED();
+    EM_CK(gemm(st, true, false, p, p, m, 1.0, V, n, V, n, 0.0, Gm.p, p));
+    larft_smem_kernel<<<1, 128, (size_t)128 * 129 * sizeof(double), st>>>(p, p, Gm.p, p, tau1,
+                                                                          k0, T.p, p);
+    EM_LAUNCHED();
+    // X = A22 (V T);  M = T^T (V^T X);  W = X - V M / 2
+    EM_CK(gemm(st, false, false, m, p, p, 1.0, V, n, T.p, p, 0.0, VT.p, n));
+    EM_CK(gemm(st, false, false, m, p, m, 1.0, A22, lda, VT.p, n, 0.0, X, n));
+    EM_CK(gemm(st, true, false, p, p, m, 1.0, V, n, X, n, 0.0, Y.p, p));
+    EM_CK(gemm(st, true, false, p, p, p, 1.0, T.p, p, Y.p, p, 0.0, M.p, p));
+    EM_CK(gemm(st, false, false, m, p, p, -0.5, V, n, M.p, p, 1.0, X, n));
+    // A22 -= [V W] [W V]^T  (both triangles: A22 stays fully symmetric for the next X)
+    copy_matrix(st, false, m, p, X, n, WV.p, n);
+    copy_matrix(st, false, m, p, V, n, WV.p + (size_t)p * n, n);
+    EM_CK(gemm(st, false, true, m, m, 2 * p, -1.0, VW.p, n, WV.p, n, 1.0, A22, lda));
+  }
+  band_extract_kernel<<<(unsigned)n, 128, 0, st>>>(n, b, A, lda, AB, ldab);
+  EM_LAUNCHED();
+}
+
+// ---- stage 2: bulge chasing ------------------------------------------------------
+struct SbArgs {
+  int64_t n;
+  double* AB;
+  int64_t ldab;       // 2b + 1
+  double* V2;         // per task: b entries
+  double* TAU2;       // per task
+  const int64_t* toff;
+  int* prog;          // tasks completed per sweep
+  int64_t nsweeps;
+};
+
+EM_DEVINL int ld_acquire_int(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+EM_DEVINL void st_release_int(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+
+__host__ __device__ __forceinline__ int64_t ntasks(int64_t n, int64_t s) {
+  return (n - 1 - s + B2 - 1) / B2;
+}
+
+constexpr int SBLD = B2 + 1;
+
+// dlarfg on x[0..L) in shared memory: returns tau, writes v (v[0] = 1) and beta via x[0]
+EM_DEVINL double smem_larfg(double* x, int L, double* v, double* red) {
+  double ss = 0.0;
+  for (int i = 1 + threadIdx.x; i < L; i += blockDim.x) ss = fma(x[i], x[i], ss);
+  ss = block_reduce_sum(ss, red);
+  __shared__ double bcs[3];
+  if (threadIdx.x == 0) {
+    const double alpha = x[0];
+    const double xnorm = sqrt(ss);
+    if (xnorm == 0.0) {
+      bcs[0] = alpha;
+      bcs[1] = 0.0;
+      bcs[2] = 0.0;
+    } else {
+      const double beta = -copysign(hypot(alpha, xnorm), alpha);
+      bcs[0] = beta;
+      bcs[1] = (beta - alpha) / beta;
+      bcs[2] = 1.0 / (alpha - beta);
+    }
+  }
+  __syncthreads();
+  const double scale = bcs[2];
+  for (int i = threadIdx.x; i < L; i += blockDim.x) v[i] = (i == 0) ? 1.0 : x[i] * scale;
+  for (int i = threadIdx.x; i < B2; i += blockDim.x)
+    if (i >= L) v[i] = 0.0;
+  __syncthreads();
+  if (threadIdx.x == 0) x[0] = bcs[0];
+  const double tau = bcs[1];
+  __syncthreads();
+  return tau;
+}
+
+__global__ void __launch_bounds__(256) sb2st_kernel(SbArgs a) {
+  extern __shared__ double sm[];
+  double* E = sm;                 // [64][SBLD]  E[i*SBLD + j]
+  double* D = E + B2 * SBLD;      // [64][SBLD]  symmetric copy
+  __shared__ double v[B2], vn[B2], w[B2], xcol[B2], red[8];
+  __shared__ double tau_prev_s;
+  const int tid = threadIdx.x;
+  const int64_t n = a.n, ldab = a.ldab;
+  double* AB = a.AB;
+  auto ab = [&](int64_t r, int64_t c) -> double& { return AB[(r - c) + c * ldab]; };
+  for (int64_t s = blockIdx.x; s < a.nsweeps; s += gridDim.x) {
+    const int64_t K = ntasks(n, s);
+    const int64_t Kp = s > 0 ? ntasks(n, s - 1) : 0;
+    for (int64_t k = 0; k < K; ++k) {
+      if (s > 0 && tid == 0) {
+        const int need = (int)imin64(k + 3, Kp);
+        while (ld_acquire_int(a.prog + (s - 1)) < need) __nanosleep(64);
+        __threadfence();  // also invalidates this SM's L1 before the band is re-read
+      }
+      __syncthreads();
+      const int64_t a0 = s + 1 + k * B2;
+      const int L = (int)imin64(B2, n - a0);
+      double tau;
+      if (k == 0) {
+        // type 1: reflector from column s, rows a0 .. a0+L-1
+        for (int i = tid; i < L; i += blockDim.x) xcol[i] = ab(a0 + i, s);
+        __syncthreads();
+        tau = smem_larfg(xcol, L, vn, red);
+        for (int i = tid; i < L; i += blockDim.x) ab(a0 + i, s) = (i == 0) ? xcol[0] : 0.0;
+      } else {
+        // type 2: E = A[a0.., ap..] (L x 64); right-apply previous H; new H from E[:,0];
+        // left-apply the new H to E[:, 1:]
+        const int64_t ap = a0 - B2;
+        const double tp = tau_prev_s;
+        for (int idx = tid; idx < L * B2; idx += blockDim.x) {
+          const int i = idx / B2, j = idx % B2;
+          E[i * SBLD + j] = ab(a0 + i, ap + j);
+        }
+        __syncthreads();
+        for (int i = tid; i < L; i += blockDim.x) {
+          double s2 = 0.0;
+          for (int j = 0; j < B2; ++j) s2 = fma(E[i * SBLD + j], v[j], s2);
+          w[i] = s2;
+        }
+        __syncthreads();
+        for (int idx = tid; idx < L * B2; idx += blockDim.x) {
+          const int i = idx / B2, j = idx % B2;
+          E[i * SBLD + j] = fma(-tp * w[i], v[j], E[i * SBLD + j]);
+        }
+        __syncthreads();
+        for (int i = tid; i < L; i += blockDim.x) xcol[i] = E[i * SBLD];
+        __syncthreads();
+        tau = smem_larfg(xcol, L, vn, red);
+        // column 0 of E becomes (beta, 0, ...)
+        for (int i = tid; i < L; i += blockDim.x) E[i * SBLD] = (i == 0) ? xcol[0] : 0.0;
+        // left-apply on columns 1..63: u_j = sum_i vn_i E_ij
+        for (int j = 1 + tid; j < B2; j += blockDim.x) {
+          double s2 = 0.0;
+          for (int i = 0; i < L; ++i) s2 = fma(vn[i], E[i * SBLD + j], s2);
+          w[j] = s2;
+        }
+        __syncthreads();
+        for (int idx = tid; idx < L * B2; idx += blockDim.x) {
+          const int i = idx / B2, j = idx % B2;
+          if (j >= 1) E[i * SBLD + j] = fma(-tau * vn[i], w[j], E[i * SBLD + j]);
+        }
+        __syncthreads();
+        for (int idx = tid; idx < L * B2; idx += blockDim.x) {
+          const int i = idx / B2, j = idx % B2;
+          ab(a0 + i, ap + j) = E[i * SBLD + j];
+        }
+      }
+      __syncthreads();
+      // type 3 (and 1): two-sided update of the diagonal block [a0, a0+L)
+      for (int idx = tid; idx < L * L; idx += blockDim.x) {
+        const int i = idx / L, j = idx % L;
+        D[i * SBLD + j] = (i >= j) ? ab(a0 + i, a0 + j) : ab(a0 + j, a0 + i);
+      }
+      __syncthreads();
+      for (int i = tid; i < L; i += blockDim.x) {
+        double s2 = 0.0;
+        for (int j = 0; j < L; ++j) s2 = fma(D[i * SBLD + j], vn[j], s2);
+        w[i] = tau * s2;
+      }
+      __syncthreads();
+      double wv = 0.0;
+      for (int i = tid; i < L; i += blockDim.x) wv = fma(w[i], vn[i], wv);
+      wv = block_reduce_sum(wv, red);
+      __shared__ double alpha_s;
+      if (tid == 0) alpha_s = -0.5 * tau * wv;
+      __syncthreads();
+      for (int i = tid; i < L; i += blockDim.x) w[i] = fma(alpha_s, vn[i], w[i]);
+      __syncthreads();
+      for (int idx = tid; idx < L * L; idx += blockDim.x) {
+        const int i = idx / L, j = idx % L;
+        if (i >= j) ab(a0 + i, a0 + j) = D[i * SBLD + j] - vn[i] * w[j] - w[i] * vn[j];
+      }
+      // record the reflector; it becomes the "previous" one for the next task
+      const int64_t t = a.toff[s] + k;
+      for (int i = tid; i < B2; i += blockDim.x) {
+        a.V2[t * B2 + i] = vn[i];
+        v[i] = vn[i];
+      }
+      if (tid == 0) {
+        a.TAU2[t] = tau;
+        tau_prev_s = tau;
+      }
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) st_release_int(a.prog + s, (int)(k + 1));
+    }
+  }
+}
+
+__global__ void tridiag_extract_kernel(int64_t n, const double* __restrict__ AB, int64_t ldab,
+                                       double* d, double* e) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  d[i] = AB[i * ldab];
+  if (i + 1 < n) e[i] = AB[1 + i * ldab];
+}
+
+// ---- Q2 back-transform -------------------------------------------------------------
+// Block (g, k): reflectors of sweeps s = g*b + t (t < b, k < ntasks(s)), rows
+// R0 + t .. R0 + t + L - 1 with R0 = g*b + 1 + k*b. V is (2b-1) x b, T is b x b.
+
+constexpr int VR = 2 * B2;  // padded parallelogram rows (128)
+
+struct Q2Block {
+  int64_t g, k;  // group and position
+};
+
+// T for every block: V from the reflector store, G = V^T V, forward larft.
+__global__ void __launch_bounds__(256) q2_tfactor_kernel(int64_t n, const Q2Block* __restrict__ blocks,
+                                                         const double* __restrict__ V2,
+                                                         const double* __restrict__ TAU2,
+                                                         const int64_t* __restrict__ toff,
+                                                         double* __restrict__ T2) {
+  extern __shared__ double sm[];
+  double* Vs = sm;              // [VR][B2]
+  double* Ts = Vs + VR * B2;    // [B2][B2+1]
+  double* Gs = Ts + B2 * (B2 + 1);  // [B2][B2+1]
+  __shared__ double taus[B2];
+  const Q2Block blk = blocks[blockIdx.x];
+  const int tid = threadIdx.x;
+  for (int i = tid; i < VR * B2; i += blockDim.x) Vs[i] = 0.0;
+  __syncthreads();
+  for (int idx = tid; idx < B2 * B2; idx += blockDim.x) {
+    const int t = idx / B2, i = idx % B2;
+    const int64_t s = blk.g * B2 + t;
+    double tv = 0.0;
+    if (s < n - 1 && blk.k < ntasks(n, s)) {
+      const int64_t task = toff[s] + blk.k;
+      Vs[(t + i) * B2 + t] = V2[task * B2 + i];
+      tv = TAU2[task];
+    }
+    if (i == 0) taus[t] = tv;
+  }
+  __syncthreads();
+  for (int idx = tid; idx < B2 * B2; idx += blockDim.x) {
+    const int i = idx / B2, j = idx % B2;
+    if (i < j) {
+      double s2 = 0.0;
+      for (int r = j; r < i + B2; ++r) s2 = fma(Vs[r * B2 + i], Vs[r * B2 + j], s2);
+      Gs[i * (B2 + 1) + j] = s2;
+    }
+  }
+  for (int i = tid; i < B2 * (B2 + 1); i += blockDim.x) Ts[i] = 0.0;
+  __syncthreads();
+  for (int k = 0; k < B2; ++k) {
+    const double tk = taus[k];
+    if (tid < k) {
+      double s2 = 0.0;
+      for (int j = tid; j < k; ++j) s2 = fma(Ts[tid * (B2 + 1) + j], Gs[j * (B2 + 1) + k], s2);
+      Ts[tid * (B2 + 1) + k] = -tk * s2;
+    }
+    if (tid == 0) Ts[k * (B2 + 1) + k] = tk;
+    __syncthreads();
+  }
+  double* Tout = T2 + blockIdx.x * (size_t)B2 * B2;
+  for (int idx = tid; idx < B2 * B2; idx += blockDim.x) {
+    const int i = idx / B2, j = idx % B2;
+    Tout[idx] = Ts[i * (B2 + 1) + j];  // row-major i, j
+  }
+}
+
+constexpr int QWC = 48;             // Z columns per CTA
+constexpr int QZ = QWC + 4;         // smem stride of the Z window / W tiles
+constexpr int QV = B2 + 4;          // smem stride of V
+
+// acc(8x8 tile) over k in [k0, k1): A(i, kk) * B(kk, j) with smem strides
+EM_DEVINL void tile_mm(double& c0, double& c1, const double* A, int sAi, int sAk, const double* B,
+                       int sBk, int sBj, int i0, int j0, int k0, int k1) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  for (int kk = k0; kk < k1; kk += 4) {
+    const double a = A[(i0 + g) * sAi + (kk + t) * sAk];
+    const double b = B[(kk + t) * sBk + (j0 + g) * sBj];
+    dmma884(c0, c1, a, b);
+  }
+}
+
+__global__ void __launch_bounds__(256) q2_apply_kernel(int64_t n, int64_t nblocks,
+                                                       const Q2Block* __restrict__ blocks,
+                                                       const double* __restrict__ V2,
+                                                       const int64_t* __restrict__ toff,
+                                                       const double* __restrict__ T2,
+                                                       double* __restrict__ Z, int64_t ldz,
+                                                       int64_t ncols) {
+  extern __shared__ double sm[];
+  double* Vs = sm;                 // [VR][QV]
+  double* Ts = Vs + VR * QV;       // [B2][QV]  (row-major T)
+  double* Zs = Ts + B2 * QV;       // [VR][QZ]
+  double* W1 = Zs + VR * QZ;       // [B2][QZ]
+  double* W2 = W1 + B2 * QZ;       // [B2][QZ]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g8 = lane >> 2, t4 = lane & 3;
+  const int64_t c0 = blockIdx.x * (int64_t)QWC;
+  const int wc = (int)imin64(QWC, ncols - c0);
+  for (int64_t bi = 0; bi < nblocks; ++bi) {
+    const Q2Block blk = blocks[bi];
+    const int64_t R0 = blk.g * B2 + 1 + blk.k * B2;
+    const int nrow = (int)imin64(VR - 1, n - R0);
+    __syncthreads();
+    // V parallelogram, T, Z window
+    for (int i = tid; i < VR * QV; i += blockDim.x) Vs[i] = 0.0;
+    __syncthreads();
+    for (int idx = tid; idx < B2 * B2; idx += blockDim.x) {
+      const int t = idx / B2, i = idx % B2;
+      const int64_t s = blk.g * B2 + t;
+      if (s < n - 1 && blk.k < ntasks(n, s) && t + i < nrow)
+        Vs[(t + i) * QV + t] = V2[(toff[s] + blk.k) * B2 + i];
+    }
+    const double* Tg = T2 + bi * (size_t)B2 * B2;
+    for (int idx = tid; idx < B2 * B2; idx += blockDim.x) Ts[(idx / B2) * QV + idx % B2] = Tg[idx];
+    for (int idx = tid; idx < VR * QWC; idx += blockDim.x) {
+      const int r = idx / QWC, c = idx % QWC;
+      Zs[r * QZ + c] = (r < nrow && c < wc) ? Z[(R0 + r) + (c0 + c) * ldz] : 0.0;
+    }
+    __syncthreads();
+    // W1 (64 x QWC) = V^T Zs : A(i, kk) = V(kk, i); V(kk, i) != 0 for kk in [i, i+64)
+    for (int tile = warp; tile < (B2 / 8) * (QWC / 8); tile += 8) {
+      const int mt = tile / (QWC / 8), nt = tile % (QWC / 8);
+      double a0 = 0.0, a1 = 0.0;
+      tile_mm(a0, a1, Vs, 1, QV, Zs, QZ, 1, mt * 8, nt * 8, mt * 8, imin64(VR, mt * 8 + 8 + B2));
+      W1[(mt * 8 + g8) * QZ + nt * 8 + 2 * t4] = a0;
+      W1[(mt * 8 + g8) * QZ + nt * 8 + 2 * t4 + 1] = a1;
+    }
+    __syncthreads();
+    // W2 = T W1 (T upper triangular)
+    for (int tile = warp; tile < (B2 / 8) * (QWC / 8); tile += 8) {
+      const int mt = tile / (QWC / 8), nt = tile % (QWC / 8);
+      double a0 = 0.0, a1 = 0.0;
+      tile_mm(a0, a1, Ts, QV, 1, W1, QZ, 1, mt * 8, nt * 8, mt * 8, B2);
+      W2[(mt * 8 + g8) * QZ + nt * 8 + 2 * t4] = a0;
+      W2[(mt * 8 + g8) * QZ + nt * 8 + 2 * t4 + 1] = a1;
+    }
+    __syncthreads();
+    // Zs -= V W2 : A(i, kk) = V(i, kk) != 0 for kk in [i-63, i]
+    for (int tile = warp; tile < (VR / 8) * (QWC / 8); tile += 8) {
+      const int mt = tile / (QWC / 8), nt = tile % (QWC / 8);
+      double a0 = 0.0, a1 = 0.0;
+      const int klo = (int)imax64(0, (mt * 8 - (B2 - 1)) / 4 * 4);
+      const int khi = (int)imin64(B2, mt * 8 + 8);
+      tile_mm(a0, a1, Vs, QV, 1, W2, QZ, 1, mt * 8, nt * 8, klo, khi);
+      const int r = mt * 8 + g8, c = nt * 8 + 2 * t4;
+      Zs[r * QZ + c] -= a0;
+      Zs[r * QZ + c + 1] -= a1;
+    }
+    __syncthreads();
+    for (int idx = tid; idx < VR * QWC; idx += blockDim.x) {
+      const int r = idx / QWC, c = idx % QWC;
+      if (r < nrow && c < wc) Z[(R0 + r) + (c0 + c) * ldz] = Zs[r * QZ + c];
+    }
+  }
+}
+
+// ---- driver -------------------------------------------------------------------------
+void syev_two_stage(cudaStream_t st, int64_t n, double* A, int64_t lda, double* w, double* Z,
+                    int64_t ldz) {
+  const int b = B2;
+  const int64_t ldab = 2 * b + 1;
+  DBuf tau1(n, st), AB((size_t)ldab * n, st);
+  {
+    Stage s(st, ST_SYTRD);
+    mirror_lower(st, n, A, lda);  // stage 1 works on the full symmetric matrix
+    Stage s1(st, ST_SY2SB);
+    sy2sb(st, n, A, lda, tau1.p, AB.p, ldab);
+  }
+  // stage 2
+  const int64_t nsw = n - 1;
+  std::vector<int64_t> toff(nsw + 1, 0);
+  for (int64_t s = 0; s < nsw; ++s) toff[s + 1] = toff[s] + ntasks(n, s);
+  const int64_t ntask = toff[nsw];
+  DArr<int64_t> dtoff(nsw + 1, st);
+  EM_CK(cudaMemcpyAsync(dtoff.p, toff.data(), (nsw + 1) * sizeof(int64_t), cudaMemcpyHostToDevice,
+                        st));
+  DBuf V2((size_t)imax64(ntask, 1) * b, st), TAU2(imax64(ntask, 1), st);
+  DArr<int> prog(imax64(nsw, 1), st);
+  EM_CK(cudaMemsetAsync(prog.p, 0, imax64(nsw, 1) * sizeof(int), st));
+  DBuf d(n, st), e(imax64(n - 1, 1), st);
+  {
+    Stage s(st, ST_SYTRD);
+    const size_t smem = (size_t)2 * B2 * SBLD * sizeof(double);
+    EM_CK(cudaFuncSetAttribute(sb2st_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem));
+    int per_sm = 1;
+    EM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sb2st_kernel, 256, smem));
+    const unsigned grid = (unsigned)imax64(1, imin64(nsw, (int64_t)num_sms() * imax64(per_sm, 1)));
+    SbArgs sa{n, AB.p, ldab, V2.p, TAU2.p, dtoff.p, prog.p, nsw};
+    void* args[] = {&sa};
+    Stage s2(st, ST_SB2ST);
+    if (nsw > 0) coop_launch((const void*)sb2st_kernel, grid, 256, args, smem, st);
+    tridiag_extract_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, AB.p, ldab, d.p, e.p);
+    EM_LAUNCHED();
+  }
+  AB.release();
+  {
+    Stage s(st, ST_STEDC);
+    stedc(st, n, d.p, e.p, Z, ldz);
+  }
+  {
+    Stage s(st, ST_ORMTR);
+    // Q2: blocks per sweep group, groups from last to first, positions ascending
+    std::vector<Q2Block> blocks;
+    const int64_t ngroups = (nsw + b - 1) / b;
+    for (int64_t g = ngroups - 1; g >= 0; --g) {
+      const int64_t K = ntasks(n, g * b);
+      for (int64_t k = 0; k < K; ++k) blocks.push_back(Q2Block{g, k});
+    }
+    const int64_t nblk = (int64_t)blocks.size();
+    if (nblk > 0) {
+      DArr<Q2Block> dblk(nblk, st);
+      EM_CK(cudaMemcpyAsync(dblk.p, blocks.data(), nblk * sizeof(Q2Block), cudaMemcpyHostToDevice,
+                            st));
+      DBuf T2((size_t)nblk * b * b, st);
+      const size_t smt = ((size_t)VR * B2 + 2 * (size_t)B2 * (B2 + 1)) * sizeof(double);
+      EM_CK(cudaFuncSetAttribute(q2_tfactor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smt));
+      q2_tfactor_kernel<<<(unsigned)nblk, 256, smt, st>>>(n, dblk.p, V2.p, TAU2.p, dtoff.p, T2.p);
+      EM_LAUNCHED();
+      const size_t sma =
+          ((size_t)VR * QV + (size_t)B2 * QV + (size_t)VR * QZ + 2 * (size_t)B2 * QZ) *
+          sizeof(double);
+      EM_CK(cudaFuncSetAttribute(q2_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sma));
+      const unsigned grid = (unsigned)((n + QWC - 1) / QWC);
+      Stage sq(st, ST_Q2);
+      q2_apply_kernel<<<grid, 256, sma, st>>>(n, nblk, dblk.p, V2.p, dtoff.p, T2.p, Z, ldz, n);
+      EM_LAUNCHED();
+      EM_CK(cudaStreamSynchronize(st));  // block list / T2 lifetime
+    }
+    // Q1 (stage-1 reflectors, vectors start b rows below their column)
+    Stage sq1(st, ST_Q1);
+    if (n > b) ormqr_lower_off(st, n, n - b, b, n, A, lda, tau1.p, Z, ldz);
+  }
+  EM_CK(cudaMemcpyAsync(w, d.p, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+}
+
+}  // namespace em

@@ -100,7 +100,9 @@ class Plate:
         rows = rows or slice(0, self.n)
         xr, ar = x[rows], a[rows]
         d = np.sqrt(((xr[:, None, :] - x[None, :, :]) ** 2).sum(-1))
-        return MU0_4PI * (ar @ a.T) / (d + self.h / 2)
+        # elementwise (not BLAS) so the result does not depend on the BLAS thread count
+        dot = ar[:, None, 0] * a[None, :, 0] + ar[:, None, 1] * a[None, :, 1]
+        return MU0_4PI * dot / (d + self.h / 2)
 
     def inductance_full(self, chunk: int = 1024) -> np.ndarray:
         n = self.n

@@ -160,3 +160,65 @@ def test_sym_eig_degenerate_spectrum(rng):
     assert np.abs(np.sort(lam) - np.sort(w)).max() < 1e-12 * np.abs(w).max() * n
     assert np.linalg.norm(a @ u - u * lam) <= 1e-11 * np.linalg.norm(a)
     assert np.abs(u.T @ u - np.eye(n)).max() < 1e-11
+
+
+@pytest.mark.parametrize("n", [1, 63, 64, 65, 1000, 1111])
+def test_symv_lower_reads_only_lower_triangle(rng, n):
+    """em_symv_lower == A_sym x with garbage in the upper triangle (td1_step_kernel's R @ state)."""
+    from paper_2407_11993_b200 import _native as nat
+    a = rng.standard_normal((n, n))
+    sym = np.tril(a) + np.tril(a, -1).T
+    garbage = sym.copy()
+    garbage[np.triu_indices(n, 1)] = 1e300  # must never be read
+    x = rng.standard_normal(n)
+    y0 = rng.standard_normal(n)
+    ad = nat.device_colmajor(garbage)
+    xd, yd = nat.device_vector(x), nat.device_vector(y0)
+    nat.check(nat.load_library().em_symv_lower(nat.context(), n, -0.5, nat.ptr(ad), n,
+                                                nat.ptr(xd), 2.0, nat.ptr(yd)))
+    ref = -0.5 * sym @ x + 2.0 * y0
+    assert np.abs(yd.cpu().numpy() - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max())
+
+
+@pytest.fixture
+def two_stage():
+    """Force the two-stage (dense -> band -> tridiagonal) reduction for every n > 128."""
+    from paper_2407_11993_b200 import _native as nat
+    nat.set_two_stage_min(0)
+    yield
+    nat.set_two_stage_min(2**62)
+
+
+@pytest.mark.parametrize("n", [129, 200, 257, 700, 1500])
+def test_two_stage_sym_eig(rng, n, two_stage):
+    from paper_2407_11993_b200.linalg import sym_eig
+    a = rng.standard_normal((n, n))
+    a = (a + a.T) / 2
+    lam, u = sym_eig(a)
+    ref = np.linalg.eigvalsh(a)[::-1]
+    assert np.abs(lam - ref).max() <= 1e-12 * np.abs(ref).max()
+    assert np.linalg.norm(a @ u - u * lam) <= 1e-11 * np.linalg.norm(a)
+    assert np.abs(u.T @ u - np.eye(n)).max() < 1e-11
+
+
+def test_two_stage_degenerate_spectrum(rng, two_stage):
+    from paper_2407_11993_b200.linalg import sym_eig
+    n = 400
+    q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    w = np.concatenate([np.full(70, 2.0), np.full(10, -1.0), rng.standard_normal(n - 80)])
+    a = (q * w) @ q.T
+    a = (a + a.T) / 2
+    lam, u = sym_eig(a)
+    assert np.abs(np.sort(lam) - np.sort(w)).max() < 1e-12 * np.abs(w).max() * n
+    assert np.linalg.norm(a @ u - u * lam) <= 1e-11 * np.linalg.norm(a)
+    assert np.abs(u.T @ u - np.eye(n)).max() < 1e-11
+
+
+@pytest.mark.parametrize("name", ["plate_200", "tube_ref"])
+def test_two_stage_generalized_eig_matches_reference(name, two_stage):
+    from tests.conftest import modal_directions_match
+    from paper_2407_11993_b200.modal import generalized_eig
+    g = golden(name)
+    mb = generalized_eig(g["l_i"], g["r_i"])
+    assert np.max(np.abs(mb.tau - g["tau"]) / g["tau"]) < 1e-10
+    assert modal_directions_match(g["v"], g["tau"], mb.v, tol=1e-7)

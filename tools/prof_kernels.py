@@ -1,0 +1,97 @@
+"""Drive each hot kernel once or a few times at C2 scale (N = 16,384) through the
+C ABI, for ncu captures and CUDA-event timings (measurement tool, not product).
+
+    python tools/prof_kernels.py [symv|gemm|td2|td1|all]
+"""
+import ctypes
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2407_11993_b200 import _native as nat  # noqa: E402
+
+
+def timed(fn, reps=3):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    fn()
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps * 1e-3
+
+
+def main(which):
+    ctx, lib = nat.context(), nat.load_library()
+    g = torch.Generator(device="cuda").manual_seed(7)
+    out = {}
+    n = 16384
+    if which in ("symv", "all"):
+        a = torch.randn(n, n, device="cuda", dtype=torch.float64, generator=g)
+        x = torch.randn(n, device="cuda", dtype=torch.float64, generator=g)
+        y = torch.empty_like(x)
+        t = timed(lambda: nat.check(lib.em_symv_lower(ctx, n, 1.0, nat.ptr(a), n, nat.ptr(x), 0.0,
+                                                      nat.ptr(y))))
+        out["symv_n16384_s"] = t
+        out["symv_GBps_algorithmic"] = 8 * n * n / 2 / t / 1e9
+        del a
+    if which in ("gemm", "all"):
+        m = 8192
+        a = torch.randn(m, m, device="cuda", dtype=torch.float64, generator=g)
+        b = torch.randn(m, m, device="cuda", dtype=torch.float64, generator=g)
+        c = torch.empty_like(a)
+        t = timed(lambda: nat.check(lib.em_dgemm(ctx, 0, 0, m, m, m, 1.0, nat.ptr(a), m,
+                                                 nat.ptr(b), m, 0.0, nat.ptr(c), m)), reps=2)
+        out["dgemm_8192_TFps"] = 2 * m ** 3 / t / 1e12
+        del a, b, c
+    if which in ("td2", "all"):
+        T, n_obs = 10000, 32
+        ln = torch.rand(n, device="cuda", dtype=torch.float64, generator=g) * 8 + 0.1
+        rn = torch.ones(n, device="cuda", dtype=torch.float64)
+        pr = torch.randn(n, device="cuda", dtype=torch.float64, generator=g) * 1e-6
+        pl = torch.randn(n, device="cuda", dtype=torch.float64, generator=g) * 1e-6
+        cv = torch.randn(n, n_obs, device="cuda", dtype=torch.float64, generator=g)
+        tt = np.minimum(5e-7 * np.arange(T + 1) / 5e-6, 1.0)
+        drive = nat.device_vector(tt)
+        plan = ctypes.c_void_p()
+        nat.check(lib.em_td2_plan_create(ctx, n, 1, 0, nat.ptr(ln), nat.ptr(rn), nat.ptr(pr),
+                                         nat.ptr(pl), nat.ptr(pr), 5e-7, 0.5, ctypes.byref(plan)))
+        nat.check(lib.em_td2_set_observables(plan, n_obs, nat.ptr(cv), n_obs, None, 0))
+        q = nat.zeros(n)
+        y = nat.empty(T, n_obs)
+        t = timed(lambda: nat.check(lib.em_td2_run(plan, T, nat.ptr(drive), nat.ptr(q), nat.ptr(y),
+                                                   1, None)))
+        out["td2_run_s"] = t
+        out["td2_mode_steps_per_s"] = n * T / t
+        out["td2_recon_TFps"] = 2 * n_obs * n * T / t / 1e12
+        lib.em_td2_plan_destroy(plan)
+    if which in ("td1", "all"):
+        m = 8192
+        b = torch.randn(m, m, device="cuda", dtype=torch.float64, generator=g) / np.sqrt(m)
+        lmat = b @ b.T + torch.eye(m, device="cuda", dtype=torch.float64)
+        rmat = torch.eye(m, device="cuda", dtype=torch.float64) * 1e-3
+        plan = ctypes.c_void_p()
+        piv = ctypes.c_int64(-1)
+        rd = torch.randn(m, device="cuda", dtype=torch.float64, generator=g)
+        nat.check(lib.em_td1_plan_create(ctx, m, 1, 0, nat.ptr(lmat), m, nat.ptr(rmat), m,
+                                         nat.ptr(rd), nat.ptr(rd), None, 1e-6, 0.5,
+                                         ctypes.byref(plan), ctypes.byref(piv)))
+        steps = 50
+        drive = nat.device_vector(np.linspace(0, 1, steps + 1))
+        s = nat.zeros(m)
+        t = timed(lambda: nat.check(lib.em_td1_run(plan, steps, nat.ptr(drive), nat.ptr(s), None, 1,
+                                                   None)), reps=1)
+        out["td1_n8192_per_step_ms"] = t / steps * 1e3
+        lib.em_td1_plan_destroy(plan)
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1] if len(sys.argv) > 1 else "all")
