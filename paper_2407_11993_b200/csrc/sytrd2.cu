@@ -316,21 +316,21 @@ EM_DEVINL double smem_larfg(double* x, int L, double* v, double* red) {
 
 __global__ void __launch_bounds__(256) sb2st_kernel(SbArgs a) {
   extern __shared__ double sm[];
-  double* E = sm;                 // [64][SBLD]  E[i*SBLD + j]
-  double* D = E + B2 * SBLD;      // [64][SBLD]  symmetric copy
+  double* E = sm;                 // E[i*SBLD + j]: row i of block k, column j of block k-1
+  double* D = E + B2 * SBLD;      // full symmetric copy of the diagonal block
   __shared__ double v[B2], vn[B2], w[B2], xcol[B2], red[8];
-  __shared__ double tau_prev_s;
+  __shared__ double tau_prev_s, alpha_s;
   const int tid = threadIdx.x;
+  const int q = tid & 3, row = tid >> 2;  // 4 threads per row (or column) in the matvecs
   const int64_t n = a.n, ldab = a.ldab;
   double* AB = a.AB;
-  auto ab = [&](int64_t r, int64_t c) -> double& { return AB[(r - c) + c * ldab]; };
   for (int64_t s = blockIdx.x; s < a.nsweeps; s += gridDim.x) {
     const int64_t K = ntasks(n, s);
     const int64_t Kp = s > 0 ? ntasks(n, s - 1) : 0;
     for (int64_t k = 0; k < K; ++k) {
       if (s > 0 && tid == 0) {
         const int need = (int)imin64(k + 3, Kp);
-        while (ld_acquire_int(a.prog + (s - 1)) < need) __nanosleep(64);
+        while (ld_acquire_int(a.prog + (s - 1)) < need) __nanosleep(32);
         __threadfence();  // also invalidates this SM's L1 before the band is re-read
       }
       __syncthreads();
@@ -338,84 +338,91 @@ __global__ void __launch_bounds__(256) sb2st_kernel(SbArgs a) {
       const int L = (int)imin64(B2, n - a0);
       double tau;
       if (k == 0) {
-        // type 1: reflector from column s, rows a0 .. a0+L-1
-        for (int i = tid; i < L; i += blockDim.x) xcol[i] = ab(a0 + i, s);
+        // type 1: reflector from column s, rows a0 .. a0+L-1 (band offsets 1..L)
+        if (tid < B2) xcol[tid] = (tid < L) ? AB[(1 + tid) + s * ldab] : 0.0;
         __syncthreads();
         tau = smem_larfg(xcol, L, vn, red);
-        for (int i = tid; i < L; i += blockDim.x) ab(a0 + i, s) = (i == 0) ? xcol[0] : 0.0;
+        if (tid < L) AB[(1 + tid) + s * ldab] = (tid == 0) ? xcol[0] : 0.0;
       } else {
-        // type 2: E = A[a0.., ap..] (L x 64); right-apply previous H; new H from E[:,0];
-        // left-apply the new H to E[:, 1:]
+        // type 2 on E = A[a0.., ap..] (element (i, j) at band offset 64 + i - j)
         const int64_t ap = a0 - B2;
+        for (int idx = tid; idx < B2 * B2; idx += 256) {
+          const int i = idx & (B2 - 1), j = idx >> 6;
+          E[i * SBLD + j] = (i < L) ? AB[(B2 + i - j) + (ap + j) * ldab] : 0.0;
+        }
+        __syncthreads();
         const double tp = tau_prev_s;
-        for (int idx = tid; idx < L * B2; idx += blockDim.x) {
-          const int i = idx / B2, j = idx % B2;
-          E[i * SBLD + j] = ab(a0 + i, ap + j);
-        }
-        __syncthreads();
-        for (int i = tid; i < L; i += blockDim.x) {
+        {  // w = E v (right application of the previous reflector)
           double s2 = 0.0;
-          for (int j = 0; j < B2; ++j) s2 = fma(E[i * SBLD + j], v[j], s2);
-          w[i] = s2;
+          for (int j = q; j < B2; j += 4) s2 = fma(E[row * SBLD + j], v[j], s2);
+          s2 += __shfl_xor_sync(0xffffffffu, s2, 1);
+          s2 += __shfl_xor_sync(0xffffffffu, s2, 2);
+          if (q == 0) w[row] = s2;
         }
         __syncthreads();
-        for (int idx = tid; idx < L * B2; idx += blockDim.x) {
-          const int i = idx / B2, j = idx % B2;
+        for (int idx = tid; idx < B2 * B2; idx += 256) {
+          const int i = idx >> 6, j = idx & (B2 - 1);
           E[i * SBLD + j] = fma(-tp * w[i], v[j], E[i * SBLD + j]);
         }
         __syncthreads();
-        for (int i = tid; i < L; i += blockDim.x) xcol[i] = E[i * SBLD];
+        if (tid < B2) xcol[tid] = (tid < L) ? E[tid * SBLD] : 0.0;
         __syncthreads();
         tau = smem_larfg(xcol, L, vn, red);
-        // column 0 of E becomes (beta, 0, ...)
-        for (int i = tid; i < L; i += blockDim.x) E[i * SBLD] = (i == 0) ? xcol[0] : 0.0;
-        // left-apply on columns 1..63: u_j = sum_i vn_i E_ij
-        for (int j = 1 + tid; j < B2; j += blockDim.x) {
+        {  // u_j = sum_i vn_i E_ij, j >= 1 (left application of the new reflector)
+          const int j = row;
           double s2 = 0.0;
-          for (int i = 0; i < L; ++i) s2 = fma(vn[i], E[i * SBLD + j], s2);
-          w[j] = s2;
+          if (j >= 1)
+            for (int i = q; i < L; i += 4) s2 = fma(vn[i], E[i * SBLD + j], s2);
+          s2 += __shfl_xor_sync(0xffffffffu, s2, 1);
+          s2 += __shfl_xor_sync(0xffffffffu, s2, 2);
+          if (q == 0) w[j] = s2;
         }
         __syncthreads();
-        for (int idx = tid; idx < L * B2; idx += blockDim.x) {
-          const int i = idx / B2, j = idx % B2;
-          if (j >= 1) E[i * SBLD + j] = fma(-tau * vn[i], w[j], E[i * SBLD + j]);
-        }
-        __syncthreads();
-        for (int idx = tid; idx < L * B2; idx += blockDim.x) {
-          const int i = idx / B2, j = idx % B2;
-          ab(a0 + i, ap + j) = E[i * SBLD + j];
+        for (int idx = tid; idx < B2 * B2; idx += 256) {
+          const int i = idx & (B2 - 1), j = idx >> 6;
+          if (i < L) {
+            const double val = (j == 0) ? ((i == 0) ? xcol[0] : 0.0)
+                                        : fma(-tau * vn[i], w[j], E[i * SBLD + j]);
+            AB[(B2 + i - j) + (ap + j) * ldab] = val;
+          }
         }
       }
       __syncthreads();
-      // type 3 (and 1): two-sided update of the diagonal block [a0, a0+L)
-      for (int idx = tid; idx < L * L; idx += blockDim.x) {
-        const int i = idx / L, j = idx % L;
-        D[i * SBLD + j] = (i >= j) ? ab(a0 + i, a0 + j) : ab(a0 + j, a0 + i);
+      // type 3 (and 1): D <- H D H on the diagonal block [a0, a0+L)
+      for (int idx = tid; idx < B2 * B2; idx += 256) {
+        const int i = idx & (B2 - 1), j = idx >> 6;
+        double val = 0.0;
+        if (i < L && j < L)
+          val = (i >= j) ? AB[(i - j) + (a0 + j) * ldab] : AB[(j - i) + (a0 + i) * ldab];
+        D[i * SBLD + j] = val;
       }
       __syncthreads();
-      for (int i = tid; i < L; i += blockDim.x) {
+      {
         double s2 = 0.0;
-        for (int j = 0; j < L; ++j) s2 = fma(D[i * SBLD + j], vn[j], s2);
-        w[i] = tau * s2;
+        for (int j = q; j < B2; j += 4) s2 = fma(D[row * SBLD + j], vn[j], s2);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, 1);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, 2);
+        if (q == 0) w[row] = tau * s2;
       }
       __syncthreads();
-      double wv = 0.0;
-      for (int i = tid; i < L; i += blockDim.x) wv = fma(w[i], vn[i], wv);
-      wv = block_reduce_sum(wv, red);
-      __shared__ double alpha_s;
-      if (tid == 0) alpha_s = -0.5 * tau * wv;
+      if (tid < 32) {
+        double t2 = fma(w[tid], vn[tid], w[tid + 32] * vn[tid + 32]);
+        t2 = warp_sum(t2);
+        if (tid == 0) alpha_s = -0.5 * tau * t2;
+      }
       __syncthreads();
-      for (int i = tid; i < L; i += blockDim.x) w[i] = fma(alpha_s, vn[i], w[i]);
+      if (tid < B2) w[tid] = fma(alpha_s, vn[tid], w[tid]);
       __syncthreads();
-      for (int idx = tid; idx < L * L; idx += blockDim.x) {
-        const int i = idx / L, j = idx % L;
-        if (i >= j) ab(a0 + i, a0 + j) = D[i * SBLD + j] - vn[i] * w[j] - w[i] * vn[j];
+      for (int idx = tid; idx < B2 * B2; idx += 256) {
+        const int i = idx & (B2 - 1), j = idx >> 6;
+        if (i < L && j <= i)
+          AB[(i - j) + (a0 + j) * ldab] = D[i * SBLD + j] - vn[i] * w[j] - w[i] * vn[j];
       }
       // record the reflector; it becomes the "previous" one for the next task
       const int64_t t = a.toff[s] + k;
-      for (int i = tid; i < B2; i += blockDim.x) {
-        a.V2[t * B2 + i] = vn[i];
-        v[i] = vn[i];
+      if (tid < B2) {
+        a.V2[t * B2 + tid] = vn[tid];
+        v[tid] = vn[tid];
       }
       if (tid == 0) {
         a.TAU2[t] = tau;
@@ -500,93 +507,23 @@ __global__ void __launch_bounds__(256) q2_tfactor_kernel(int64_t n, const Q2Bloc
   }
 }
 
-constexpr int QWC = 48;             // Z columns per CTA
-constexpr int QZ = QWC + 4;         // smem stride of the Z window / W tiles
-constexpr int QV = B2 + 4;          // smem stride of V
-
-// acc(8x8 tile) over k in [k0, k1): A(i, kk) * B(kk, j) with smem strides
-EM_DEVINL void tile_mm(double& c0, double& c1, const double* A, int sAi, int sAk, const double* B,
-                       int sBk, int sBj, int i0, int j0, int k0, int k1) {
-  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  for (int kk = k0; kk < k1; kk += 4) {
-    const double a = A[(i0 + g) * sAi + (kk + t) * sAk];
-    const double b = B[(kk + t) * sBk + (j0 + g) * sBj];
-    dmma884(c0, c1, a, b);
-  }
-}
-
-__global__ void __launch_bounds__(256) q2_apply_kernel(int64_t n, int64_t nblocks,
-                                                       const Q2Block* __restrict__ blocks,
-                                                       const double* __restrict__ V2,
-                                                       const int64_t* __restrict__ toff,
-                                                       const double* __restrict__ T2,
-                                                       double* __restrict__ Z, int64_t ldz,
-                                                       int64_t ncols) {
-  extern __shared__ double sm[];
-  double* Vs = sm;                 // [VR][QV]
-  double* Ts = Vs + VR * QV;       // [B2][QV]  (row-major T)
-  double* Zs = Ts + B2 * QV;       // [VR][QZ]
-  double* W1 = Zs + VR * QZ;       // [B2][QZ]
-  double* W2 = W1 + B2 * QZ;       // [B2][QZ]
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g8 = lane >> 2, t4 = lane & 3;
-  const int64_t c0 = blockIdx.x * (int64_t)QWC;
-  const int wc = (int)imin64(QWC, ncols - c0);
-  for (int64_t bi = 0; bi < nblocks; ++bi) {
-    const Q2Block blk = blocks[bi];
-    const int64_t R0 = blk.g * B2 + 1 + blk.k * B2;
-    const int nrow = (int)imin64(VR - 1, n - R0);
-    __syncthreads();
-    // V parallelogram, T, Z window
-    for (int i = tid; i < VR * QV; i += blockDim.x) Vs[i] = 0.0;
-    __syncthreads();
-    for (int idx = tid; idx < B2 * B2; idx += blockDim.x) {
-      const int t = idx / B2, i = idx % B2;
-      const int64_t s = blk.g * B2 + t;
-      if (s < n - 1 && blk.k < ntasks(n, s) && t + i < nrow)
-        Vs[(t + i) * QV + t] = V2[(toff[s] + blk.k) * B2 + i];
-    }
-    const double* Tg = T2 + bi * (size_t)B2 * B2;
-    for (int idx = tid; idx < B2 * B2; idx += blockDim.x) Ts[(idx / B2) * QV + idx % B2] = Tg[idx];
-    for (int idx = tid; idx < VR * QWC; idx += blockDim.x) {
-      const int r = idx / QWC, c = idx % QWC;
-      Zs[r * QZ + c] = (r < nrow && c < wc) ? Z[(R0 + r) + (c0 + c) * ldz] : 0.0;
-    }
-    __syncthreads();
-    // W1 (64 x QWC) = V^T Zs : A(i, kk) = V(kk, i); V(kk, i) != 0 for kk in [i, i+64)
-    for (int tile = warp; tile < (B2 / 8) * (QWC / 8); tile += 8) {
-      const int mt = tile / (QWC / 8), nt = tile % (QWC / 8);
-      double a0 = 0.0, a1 = 0.0;
-      tile_mm(a0, a1, Vs, 1, QV, Zs, QZ, 1, mt * 8, nt * 8, mt * 8, imin64(VR, mt * 8 + 8 + B2));
-      W1[(mt * 8 + g8) * QZ + nt * 8 + 2 * t4] = a0;
-      W1[(mt * 8 + g8) * QZ + nt * 8 + 2 * t4 + 1] = a1;
-    }
-    __syncthreads();
-    // W2 = T W1 (T upper triangular)
-    for (int tile = warp; tile < (B2 / 8) * (QWC / 8); tile += 8) {
-      const int mt = tile / (QWC / 8), nt = tile % (QWC / 8);
-      double a0 = 0.0, a1 = 0.0;
-      tile_mm(a0, a1, Ts, QV, 1, W1, QZ, 1, mt * 8, nt * 8, mt * 8, B2);
-      W2[(mt * 8 + g8) * QZ + nt * 8 + 2 * t4] = a0;
-      W2[(mt * 8 + g8) * QZ + nt * 8 + 2 * t4 + 1] = a1;
-    }
-    __syncthreads();
-    // Zs -= V W2 : A(i, kk) = V(i, kk) != 0 for kk in [i-63, i]
-    for (int tile = warp; tile < (VR / 8) * (QWC / 8); tile += 8) {
-      const int mt = tile / (QWC / 8), nt = tile % (QWC / 8);
-      double a0 = 0.0, a1 = 0.0;
-      const int klo = (int)imax64(0, (mt * 8 - (B2 - 1)) / 4 * 4);
-      const int khi = (int)imin64(B2, mt * 8 + 8);
-      tile_mm(a0, a1, Vs, QV, 1, W2, QZ, 1, mt * 8, nt * 8, klo, khi);
-      const int r = mt * 8 + g8, c = nt * 8 + 2 * t4;
-      Zs[r * QZ + c] -= a0;
-      Zs[r * QZ + c + 1] -= a1;
-    }
-    __syncthreads();
-    for (int idx = tid; idx < VR * QWC; idx += blockDim.x) {
-      const int r = idx / QWC, c = idx % QWC;
-      if (r < nrow && c < wc) Z[(R0 + r) + (c0 + c) * ldz] = Zs[r * QZ + c];
-    }
+// Explicit V (VR x b, column-major, ld VR) of a list of blocks for one wavefront.
+__global__ void __launch_bounds__(256) q2_buildv_kernel(int64_t n, const Q2Block* __restrict__ blocks,
+                                                        const int64_t* __restrict__ ids,
+                                                        const double* __restrict__ V2,
+                                                        const int64_t* __restrict__ toff,
+                                                        double* __restrict__ Vout) {
+  const Q2Block blk = blocks[ids[blockIdx.x]];
+  double* V = Vout + blockIdx.x * (size_t)VR * B2;
+  const int64_t R0 = blk.g * B2 + 1 + blk.k * B2;
+  for (int idx = threadIdx.x; idx < VR * B2; idx += blockDim.x) {
+    const int r = idx % VR, t = idx / VR;  // row r of column t
+    const int64_t s = blk.g * B2 + t;
+    const int i = r - t;
+    double val = 0.0;
+    if (i >= 0 && i < B2 && R0 + r < n && s < n - 1 && blk.k < ntasks(n, s))
+      val = V2[(toff[s] + blk.k) * B2 + i];
+    V[idx] = val;
   }
 }
 
@@ -636,7 +573,11 @@ void syev_two_stage(cudaStream_t st, int64_t n, double* A, int64_t lda, double* 
   }
   {
     Stage s(st, ST_ORMTR);
-    // Q2: blocks per sweep group, groups from last to first, positions ascending
+    // Q2: blocks (g, k) = reflectors of sweeps g*b .. g*b+b-1 at position k. The order
+    // "groups last to first, positions ascending" is satisfied by applying wavefronts
+    // w = k + 2 (G-1-g) in increasing w: blocks of one wavefront touch disjoint rows and
+    // every block they depend on sits on an earlier wavefront. Each wavefront is three
+    // grouped DMMA GEMMs over all columns of Z.
     std::vector<Q2Block> blocks;
     const int64_t ngroups = (nsw + b - 1) / b;
     for (int64_t g = ngroups - 1; g >= 0; --g) {
@@ -645,6 +586,7 @@ void syev_two_stage(cudaStream_t st, int64_t n, double* A, int64_t lda, double* 
     }
     const int64_t nblk = (int64_t)blocks.size();
     if (nblk > 0) {
+      Stage sq(st, ST_Q2);
       DArr<Q2Block> dblk(nblk, st);
       EM_CK(cudaMemcpyAsync(dblk.p, blocks.data(), nblk * sizeof(Q2Block), cudaMemcpyHostToDevice,
                             st));
@@ -654,16 +596,62 @@ void syev_two_stage(cudaStream_t st, int64_t n, double* A, int64_t lda, double* 
                                  (int)smt));
       q2_tfactor_kernel<<<(unsigned)nblk, 256, smt, st>>>(n, dblk.p, V2.p, TAU2.p, dtoff.p, T2.p);
       EM_LAUNCHED();
-      const size_t sma =
-          ((size_t)VR * QV + (size_t)B2 * QV + (size_t)VR * QZ + 2 * (size_t)B2 * QZ) *
-          sizeof(double);
-      EM_CK(cudaFuncSetAttribute(q2_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sma));
-      const unsigned grid = (unsigned)((n + QWC - 1) / QWC);
-      Stage sq(st, ST_Q2);
-      q2_apply_kernel<<<grid, 256, sma, st>>>(n, nblk, dblk.p, V2.p, dtoff.p, T2.p, Z, ldz, n);
-      EM_LAUNCHED();
-      EM_CK(cudaStreamSynchronize(st));  // block list / T2 lifetime
+      // wavefront lists (chunks of at most QCH blocks)
+      constexpr int QCH = 64;
+      std::vector<std::vector<int64_t>> waves;
+      {
+        std::vector<std::vector<int64_t>> byw;
+        for (int64_t i = 0; i < nblk; ++i) {
+          const int64_t wv = blocks[i].k + 2 * (ngroups - 1 - blocks[i].g);
+          if ((int64_t)byw.size() <= wv) byw.resize(wv + 1);
+          byw[wv].push_back(i);
+        }
+        for (auto& wl : byw)
+          for (size_t c = 0; c < wl.size(); c += QCH)
+            waves.emplace_back(wl.begin() + c, wl.begin() + std::min(wl.size(), c + QCH));
+      }
+      std::vector<int64_t> ids;
+      std::vector<GemmArgs> args;
+      std::vector<int64_t> wstart;
+      DBuf Vb((size_t)QCH * VR * B2, st), W1((size_t)QCH * B2 * n, st), W2((size_t)QCH * B2 * n, st);
+      for (auto& wl : waves) {
+        wstart.push_back((int64_t)ids.size());
+        for (size_t j = 0; j < wl.size(); ++j) {
+          const Q2Block& bk = blocks[wl[j]];
+          const int64_t R0 = bk.g * b + 1 + bk.k * b;
+          const int64_t nrow = imin64(VR - 1, n - R0);
+          double* Vj = Vb.p + j * (size_t)VR * B2;
+          double* W1j = W1.p + j * (size_t)B2 * n;
+          double* W2j = W2.p + j * (size_t)B2 * n;
+          const double* Tj = T2.p + wl[j] * (size_t)B2 * B2;  // row-major T == col-major T^T
+          ids.push_back(wl[j]);
+          args.push_back(GemmArgs{B2, n, nrow, Vj, VR, Z + R0, ldz, W1j, B2, 1.0, 0.0, 0});
+          args.push_back(GemmArgs{B2, n, B2, Tj, B2, W1j, B2, W2j, B2, 1.0, 0.0, 0});
+          args.push_back(GemmArgs{nrow, n, B2, Vj, VR, W2j, B2, Z + R0, ldz, -1.0, 1.0, 0});
+        }
+      }
+      wstart.push_back((int64_t)ids.size());
+      DArr<int64_t> dids(ids.size(), st);
+      DArr<GemmArgs> dargs(args.size(), st);
+      EM_CK(cudaMemcpyAsync(dids.p, ids.data(), ids.size() * sizeof(int64_t),
+                            cudaMemcpyHostToDevice, st));
+      // phase-major argument arrays: [phase][problem]
+      std::vector<GemmArgs> ph(args.size());
+      const size_t np = ids.size();
+      for (size_t i = 0; i < np; ++i)
+        for (int q = 0; q < 3; ++q) ph[q * np + i] = args[3 * i + q];
+      EM_CK(cudaMemcpyAsync(dargs.p, ph.data(), ph.size() * sizeof(GemmArgs),
+                            cudaMemcpyHostToDevice, st));
+      const int tiles_n = (int)((n + 127) / 128);
+      for (size_t wi = 0; wi + 1 < wstart.size(); ++wi) {
+        const int64_t o = wstart[wi], cnt = wstart[wi + 1] - wstart[wi];
+        q2_buildv_kernel<<<(unsigned)cnt, 256, 0, st>>>(n, dblk.p, dids.p + o, V2.p, dtoff.p, Vb.p);
+        EM_LAUNCHED();
+        EM_CK(gemm_grouped(st, true, false, dargs.p + o, (int)cnt, tiles_n));
+        EM_CK(gemm_grouped(st, true, false, dargs.p + np + o, (int)cnt, tiles_n));
+        EM_CK(gemm_grouped(st, false, false, dargs.p + 2 * np + o, (int)cnt, tiles_n));
+      }
+      EM_CK(cudaStreamSynchronize(st));  // host argument arrays / device lists lifetime
     }
     // Q1 (stage-1 reflectors, vectors start b rows below their column)
     Stage sq1(st, ST_Q1);

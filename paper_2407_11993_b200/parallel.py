@@ -1,0 +1,137 @@
+"""Mode-sharded modal stepping across GPUs (north-star (b)).
+
+After the eigensolve the modes never interact (transient.py:258-308: every
+mode's update uses only its own r_n, c_n and forcing row), so the TD2 stepping
+shards naturally: rank r owns a contiguous range of modes, integrates them with
+its own fused scan (em_td2_run) and produces PARTIAL observables
+Y_r = (C V)[:, modes_r] Q_r. The only exchange is one all-reduce (sum) of the
+partial observables per time block; it runs on a side stream overlapped with
+the next block's scan. One process per GPU, torch.distributed (NCCL on GPUs,
+gloo for the CPU tests).
+
+`ShardedTd2` is the device path. `shard_ranges` / `reduce_partials` are the
+pure host logic, shared with the CPU tests (tests/test_parallel_cpu.py), where
+the per-rank partial observables are produced by a test-side executor.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native as nat
+
+
+def shard_ranges(n: int, world: int) -> list[tuple[int, int]]:
+    """Contiguous, balanced mode ranges [lo, hi) per rank (sizes differ by <= 1)."""
+    if world < 1:
+        raise ValueError("world size must be >= 1")
+    base, extra = divmod(n, world)
+    out, lo = [], 0
+    for r in range(world):
+        hi = lo + base + (1 if r < extra else 0)
+        out.append((lo, hi))
+        lo = hi
+    return out
+
+
+def time_blocks(steps: int, block: int) -> list[tuple[int, int]]:
+    """[k0, k1) step ranges of the per-block exchange."""
+    return [(k, min(k + block, steps)) for k in range(0, steps, block)]
+
+
+def reduce_partials(partial, dist, group=None):
+    """Sum partial observables over all ranks in place (fixed reduction order by
+    the collective; deterministic for a fixed world size)."""
+    if dist is not None and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(partial, op=dist.ReduceOp.SUM, group=group)
+    return partial
+
+
+class ShardedTd2:
+    """TD2 stepping of the modes [lo, hi) owned by this rank.
+
+    basis: ModalBasis (device V); rm: ReducedModel; observables C (n_obs x N).
+    run(drive_table (T+1 x n_c), steps) -> full observables (T x n_obs) on every
+    rank (partials all-reduced per time block of `block` steps)."""
+
+    def __init__(self, rm, basis, dt: float, theta: float, c_obs: np.ndarray, dist=None,
+                 block: int = 2048, mode_range: tuple[int, int] | None = None):
+        t = nat.torch()
+        self.dist = dist
+        world = dist.get_world_size() if (dist is not None and dist.is_initialized()) else 1
+        rank = dist.get_rank() if world > 1 else 0
+        n = basis.n_modes
+        # mode_range overrides the rank's shard (single-process emulation in tests)
+        self.lo, self.hi = mode_range if mode_range is not None else shard_ranges(n, world)[rank]
+        self.n_loc = self.hi - self.lo
+        self.block = block
+        self.n_p, self.n_s = rm.n_ports, rm.n_sources
+        nd = 2 * self.n_p + self.n_s
+        ctx, lib = nat.context(), nat.load_library()
+        v_loc = basis.v_dev[self.lo:self.hi]              # columns lo..hi of V (n x n_loc)
+        # P_loc = V[:, lo:hi]^T [R_D | L_D | M0]  (n_loc x nd)
+        if nd:
+            drv = np.concatenate([rm.r_d.reshape(n, self.n_p), rm.l_d.reshape(n, self.n_p),
+                                  rm.m0.reshape(n, self.n_s)], axis=1)
+            ddrv = nat.device_colmajor(drv)
+            self.proj = nat.empty(nd, self.n_loc)
+            nat.check(lib.em_dgemm(ctx, 1, 0, self.n_loc, nd, n, 1.0, nat.ptr(v_loc), n,
+                                   nat.ptr(ddrv), n, 0.0, nat.ptr(self.proj), self.n_loc),
+                      "em_dgemm")
+        else:
+            self.proj = nat.zeros(1, max(self.n_loc, 1))
+        # CV_loc = C V[:, lo:hi]  (n_obs x n_loc)
+        c = np.atleast_2d(np.asarray(c_obs, dtype=float))
+        self.n_obs = c.shape[0]
+        cd = nat.device_colmajor(c)
+        self.cv = nat.empty(self.n_loc, self.n_obs)
+        nat.check(lib.em_dgemm(ctx, 0, 0, self.n_obs, self.n_loc, n, 1.0, nat.ptr(cd), self.n_obs,
+                               nat.ptr(v_loc), n, 0.0, nat.ptr(self.cv), self.n_obs), "em_dgemm")
+        self.ln = nat.device_vector(basis.l_n[self.lo:self.hi])
+        self.rn = nat.device_vector(basis.r_n[self.lo:self.hi])
+        p_r = self.proj[0:self.n_p] if self.n_p else self.proj[0:1]
+        p_l = self.proj[self.n_p:2 * self.n_p] if self.n_p else self.proj[0:1]
+        p_m = self.proj[2 * self.n_p:] if self.n_s else self.proj[0:1]
+        plan = ctypes.c_void_p()
+        nat.check(lib.em_td2_plan_create(ctx, self.n_loc, self.n_p, self.n_s, nat.ptr(self.ln),
+                                         nat.ptr(self.rn), nat.ptr(p_r), nat.ptr(p_l),
+                                         nat.ptr(p_m), float(dt), float(theta),
+                                         ctypes.byref(plan)), "em_td2_plan_create")
+        self._plan = plan
+        nat.check(lib.em_td2_set_observables(plan, self.n_obs, nat.ptr(self.cv), self.n_obs, None,
+                                             0), "em_td2_set_observables")
+        self.q = nat.zeros(max(self.n_loc, 1))
+        self._comm_stream = t.cuda.Stream()
+
+    def __del__(self):
+        if getattr(self, "_plan", None):
+            nat.load_library().em_td2_plan_destroy(self._plan)
+            self._plan = None
+
+    def run(self, drive_dev, steps: int):
+        """drive_dev: device drive table ((steps+1) x (n_p+n_s)). Returns Y (steps x n_obs)."""
+        t = nat.torch()
+        lib = nat.load_library()
+        n_c = self.n_p + self.n_s
+        y = nat.zeros(steps, self.n_obs)
+        main = t.cuda.current_stream()
+        pending = []
+        for k0, k1 in time_blocks(steps, self.block):
+            yb = y[k0:k1]
+            # the carry state q advances block by block; the drive rows k0..k1 are a view
+            dptr = nat.ptr(drive_dev[k0 * n_c:]) if n_c else nat.ptr(drive_dev)
+            nat.check(lib.em_td2_run(self._plan, k1 - k0, dptr, nat.ptr(self.q), nat.ptr(yb), 1,
+                                     None), "em_td2_run")
+            if self.dist is not None and self.dist.is_initialized() and \
+                    self.dist.get_world_size() > 1:
+                ev = t.cuda.Event()
+                ev.record(main)
+                with t.cuda.stream(self._comm_stream):
+                    self._comm_stream.wait_event(ev)
+                    pending.append(self.dist.all_reduce(yb, op=self.dist.ReduceOp.SUM,
+                                                        async_op=True))
+        for h in pending:
+            h.wait()
+        main.wait_stream(self._comm_stream)
+        return y

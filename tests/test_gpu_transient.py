@@ -183,3 +183,24 @@ def test_c1_full_config_matches_reference():
                                       observables=(m["c"], None))
         assert rel_l2(res.observables, g[f"{method}_obs"]) < TOL
         assert rel_l2(res.internal_states[499::500], g[f"{method}_states"]) < TOL
+
+
+def test_mode_sharded_stepping_on_device():
+    """parallel.ShardedTd2: the per-rank device scans over disjoint mode ranges sum to
+    the unsharded observables (ranks emulated in one process; the NCCL all-reduce is
+    the only step not exercised here — it is covered by the gloo tests)."""
+    from paper_2407_11993_b200 import _native as nat
+    from paper_2407_11993_b200 import modal, transient
+    from paper_2407_11993_b200.parallel import ShardedTd2, shard_ranges
+    g = golden("plate_200")
+    rm = _plate_rm(g)
+    basis = modal.generalized_eig(rm.l_i, rm.r_i)
+    steps, dt = int(g["steps"]), float(g["dt"])
+    i_d, i0 = transient.drive_samples(None, rm, _plate_drives(), dt, steps)
+    table = nat.device_vector(np.concatenate([i_d, i0], axis=1).reshape(-1))
+    y = None
+    for lo, hi in shard_ranges(rm.n_internal, 3):
+        sh = ShardedTd2(rm, basis, dt, 0.5, g["c"], block=128, mode_range=(lo, hi))
+        part = sh.run(table, steps).cpu().numpy()
+        y = part if y is None else y + part
+    assert rel_l2(y, g["td2_obs_theta0.5"]) < TOL

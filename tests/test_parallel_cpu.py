@@ -1,0 +1,90 @@
+"""Multi-rank host logic of the mode-sharded TD2 stepping (paper_2407_11993_b200.parallel),
+run on CPU with the gloo backend and world_size 2. Each rank integrates only its
+own mode range (here with the CPU oracle standing in for the device scan), the
+partial observables are summed with the same reduce_partials the device path
+uses, and the result must equal the unsharded run."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from tests.conftest import golden, rel_l2
+
+
+def test_shard_ranges_cover_and_balance():
+    from paper_2407_11993_b200.parallel import shard_ranges, time_blocks
+    for n in (1, 7, 96, 16384, 120000):
+        for world in (1, 2, 3, 4, 8):
+            r = shard_ranges(n, world)
+            assert r[0][0] == 0 and r[-1][1] == n
+            assert all(r[i][1] == r[i + 1][0] for i in range(world - 1))
+            sizes = [hi - lo for lo, hi in r]
+            assert max(sizes) - min(sizes) <= 1
+    tb = time_blocks(10000, 2048)
+    assert tb[0] == (0, 2048) and tb[-1] == (8192, 10000)
+    assert sum(k1 - k0 for k0, k1 in tb) == 10000
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _partial_observables(lo, hi, block):
+    """Per-rank partial C V[:, lo:hi] Q[lo:hi] of the plate_small TD2 run, produced
+    block by block (carry state kept across blocks) like ShardedTd2.run."""
+    from oracle import oracle as O
+    from paper_2407_11993_b200.parallel import time_blocks
+    g = golden("plate_small")
+    b = O.Basis(v=g["v"], tau=g["tau"], l_n=g["l_n"], r_n=g["r_n"], vt_r=None)
+    dt, steps = float(g["dt"]), int(g["steps"])
+    sd = O.tone_sampler([[(0.7, 2e4, 0.3), (0.2, 5e4, 1.1)]])
+    s0 = O.tone_sampler([[(1.0, 1e4, 0.0)]])
+    itab, i0tab = O.sample_table(sd, steps, dt), O.sample_table(s0, steps, dt)
+    st = O.Td2(b, g["r_d"], g["l_d"], g["m0"], dt, 0.5)
+    cv = g["c"] @ g["v"]
+    q = np.zeros(b.tau.shape[0])
+    y = np.zeros((steps, g["c"].shape[0]))
+    for k0, k1 in time_blocks(steps, block):
+        for k in range(k0, k1):
+            f = st.forcing(itab[k], itab[k + 1] - itab[k], i0tab[k + 1] - i0tab[k])
+            # only the owned modes advance (the others are never read)
+            qn = q.copy()
+            O.lib().orc_td2_step(O._p(qn), O._p(st._rn), O._p(st._c), dt,
+                                 O._p(np.ascontiguousarray(f)), qn.shape[0])
+            q[lo:hi] = qn[lo:hi]
+            y[k] = cv[:, lo:hi] @ q[lo:hi]
+    return y
+
+
+def _worker(rank, world, port, block, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2407_11993_b200.parallel import reduce_partials, shard_ranges
+    g = golden("plate_small")
+    lo, hi = shard_ranges(g["v"].shape[1], world)[rank]
+    part = torch.from_numpy(_partial_observables(lo, hi, block))
+    reduce_partials(part, dist)
+    if rank == 0:
+        np.save(out, part.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("block", [64, 300])
+def test_sharded_td2_observables_equal_unsharded(tmp_path, block):
+    world = 2
+    out = str(tmp_path / "y.npy")
+    mp.spawn(_worker, args=(world, _free_port(), block, out), nprocs=world, join=True)
+    y = np.load(out)
+    g = golden("plate_small")
+    ref = g["td2_obs_theta0.5"]
+    assert rel_l2(y, ref) < 1e-12
