@@ -15,6 +15,7 @@ struct em_td1_plan;
 
 namespace em {
 extern int64_t g_two_stage_min;
+extern int g_latrd_dotr;
 void stages_reset(bool on);
 void stages_level(int level);
 int stages_read(double* ms, int64_t* counts, int n);
@@ -128,6 +129,14 @@ int em_config(em_ctx* ctx, int key, int64_t value) {
   return guarded(ctx, [&] {
     if (key == EM_CFG_TWO_STAGE_MIN) {
       em::g_two_stage_min = value;
+      return EM_OK;
+    }
+    if (key == 99) {  // debug: rows per panel-dot chunk of the fused latrd
+      em::g_latrd_dotr = (int)value;
+      return EM_OK;
+    }
+    if (key == EM_CFG_SYTRD_FUSED) {
+      em::g_sytrd_fused = value != 0;
       return EM_OK;
     }
     throw em::ArgError{"unknown em_config key"};

@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(256) qr_panel_kernel(QRArgs a) {
     // (b) every CTA forms beta, tau, scale identically
     if (tid == 0) {
       double xs = 0.0;
-      for (unsigned b = 0; b < G; ++b) xs += normpart[b];
+      for (unsigned b = 0; b < G; ++b) xs += __ldcg(normpart + b);
       const double alpha = *(volatile double*)alpha_slot;
       const double xnorm = sqrt(xs);
       double beta, tau, scale;
@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(256) qr_panel_kernel(QRArgs a) {
     // (d) apply H_j to the remaining columns of the own rows
     for (int c = j + 1 + tid; c < a.nbw; c += blockDim.x) {
       double s = 0.0;
-      for (unsigned b = 0; b < G; ++b) s += dotpart[(size_t)b * B2 + c];
+      for (unsigned b = 0; b < G; ++b) s += __ldcg(dotpart + (size_t)b * B2 + c);
       wsh[c] = s;
     }
     __syncthreads();
@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(256) sb2st_kernel(SbArgs a) {
       double tau;
       if (k == 0) {
         // type 1: reflector from column s, rows a0 .. a0+L-1 (band offsets 1..L)
-        if (tid < B2) xcol[tid] = (tid < L) ? AB[(1 + tid) + s * ldab] : 0.0;
+        if (tid < B2) xcol[tid] = (tid < L) ? __ldcg(AB + (1 + tid) + s * ldab) : 0.0;
         __syncthreads();
         tau = smem_larfg(xcol, L, vn, red);
         if (tid < L) AB[(1 + tid) + s * ldab] = (tid == 0) ? xcol[0] : 0.0;
@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(256) sb2st_kernel(SbArgs a) {
         const int64_t ap = a0 - B2;
         for (int idx = tid; idx < B2 * B2; idx += 256) {
           const int i = idx & (B2 - 1), j = idx >> 6;
-          E[i * SBLD + j] = (i < L) ? AB[(B2 + i - j) + (ap + j) * ldab] : 0.0;
+          E[i * SBLD + j] = (i < L) ? __ldcg(AB + (B2 + i - j) + (ap + j) * ldab) : 0.0;
         }
         __syncthreads();
         const double tp = tau_prev_s;
@@ -393,7 +393,7 @@ __global__ void __launch_bounds__(256) sb2st_kernel(SbArgs a) {
         const int i = idx & (B2 - 1), j = idx >> 6;
         double val = 0.0;
         if (i < L && j < L)
-          val = (i >= j) ? AB[(i - j) + (a0 + j) * ldab] : AB[(j - i) + (a0 + i) * ldab];
+          val = (i >= j) ? __ldcg(AB + (i - j) + (a0 + j) * ldab) : __ldcg(AB + (j - i) + (a0 + i) * ldab);
         D[i * SBLD + j] = val;
       }
       __syncthreads();
