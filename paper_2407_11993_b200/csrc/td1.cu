@@ -25,7 +25,7 @@ struct em_td1_plan {
   int64_t n = 0;
   int n_p = 0, n_s = 0, n_u = 0;
   double dt = 0, theta = 0;
-  em::DBuf C, R, Dinv, E, work, b, y, x;
+  em::DBuf C, R, Dinv, DinvT, E, work, b, y, x;
   em::DArr<unsigned long long>* flags = nullptr;
   em::DArr<unsigned int>* counters = nullptr;
   unsigned long long epoch = 0;
@@ -44,15 +44,25 @@ constexpr int TS = 64;  // triangular-solve block
 __global__ void td1_z_kernel(int64_t n, const double* __restrict__ L, int64_t ldl,
                              const double* __restrict__ R, int64_t ldr, double dt_theta,
                              double* __restrict__ Z, double* __restrict__ Rc) {
-  const int64_t c = blockIdx.y;
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
-       r += (int64_t)gridDim.x * blockDim.x) {
-    // symmetric inputs: use the lower triangle (SymMatrix semantics, linalg.py:40-41)
-    const int64_t rr = r >= c ? r : c, cc = r >= c ? c : r;
-    const double l = L[rr + cc * ldl], rv = R[rr + cc * ldr];
-    Z[r + c * n] = l + dt_theta * rv;
-    Rc[r + c * n] = rv;
-  }
+  for (int64_t c = blockIdx.y; c < n; c += gridDim.y)
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x) {
+      // symmetric inputs: use the lower triangle (SymMatrix semantics, linalg.py:40-41)
+      const int64_t rr = r >= c ? r : c, cc = r >= c ? c : r;
+      const double l = L[rr + cc * ldl], rv = R[rr + cc * ldr];
+      Z[r + c * n] = l + dt_theta * rv;
+      Rc[r + c * n] = rv;
+    }
+}
+
+// DinvT_b = Dinv_b^T for every TS x TS diagonal inverse (backward solve reads it coalesced)
+__global__ void transpose_blocks_kernel(const double* __restrict__ Din, double* __restrict__ Dout) {
+  __shared__ double t[TS][TS + 1];
+  const double* src = Din + (int64_t)blockIdx.x * TS * TS;
+  double* dst = Dout + (int64_t)blockIdx.x * TS * TS;
+  for (int e = threadIdx.x; e < TS * TS; e += blockDim.x) t[e % TS][e / TS] = src[e];
+  __syncthreads();
+  for (int e = threadIdx.x; e < TS * TS; e += blockDim.x) dst[e] = t[e / TS][e % TS];
 }
 
 // E = [-dt R_D | -(L_D + dt theta R_D) | -M0]  (drive_rhs, modal.py:121-131)
@@ -136,47 +146,57 @@ __global__ void __launch_bounds__(256) trsv_fwd_kernel(int64_t n, const double* 
     if (r >= nblk) break;
     const int64_t r0 = r * TS, row = r0 + tx;
     double acc = 0.0;
-    int64_t j = 0;
-    while (j < r) {
-      // take every already-published block in one go (at least one)
-      __shared__ int64_t jr;
-      if (tid == 0) {
-        while (ld_acquire(flags + j) != epoch) __nanosleep(20);
-        int64_t e = j;
-        while (e + 1 < r && ld_acquire(flags + e + 1) == epoch) ++e;
-        jr = e;
-      }
-      __syncthreads();
-      const int64_t je = jr;
-      for (; j <= je; ++j) {
-        const int64_t c0 = j * TS + ty * 16;
-        double a[16], yy[16];
+    // Off the dependency chain: the diagonal inverse and b_r are loaded up front,
+    // and tile j+1 is loaded before waiting for block j, so only the short y_j
+    // read sits on the chain.
+    const double* D = Dinv + r * TS * TS;
+    double dv[16];
 #pragma unroll
-        for (int cc = 0; cc < 16; ++cc) {
-          a[cc] = (row < n) ? C[row + (c0 + cc) * ldc] : 0.0;
-          yy[cc] = __ldcg(y + c0 + cc);
+    for (int cc = 0; cc < 16; ++cc) dv[cc] = D[tx + (ty * 16 + cc) * TS];
+    const double bb = (tid < TS && r0 + tid < n) ? b[r0 + tid] : 0.0;
+    double a[16];
+    if (r > 0) {
+#pragma unroll
+      for (int cc = 0; cc < 16; ++cc) a[cc] = (row < n) ? C[row + (ty * 16 + cc) * ldc] : 0.0;
+    }
+    int64_t ready = -1;  // highest block index known to be published
+    for (int64_t j = 0; j < r; ++j) {
+      double an[16];
+      if (j + 1 < r) {
+        const int64_t c1 = (j + 1) * TS + ty * 16;
+#pragma unroll
+        for (int cc = 0; cc < 16; ++cc) an[cc] = (row < n) ? C[row + (c1 + cc) * ldc] : 0.0;
+      }
+      if (j > ready) {
+        __shared__ int64_t jr;
+        if (tid == 0) {
+          while (ld_acquire(flags + j) != epoch) __nanosleep(20);
+          int64_t e = j;
+          while (e + 1 < r && ld_acquire(flags + e + 1) == epoch) ++e;
+          jr = e;
         }
-#pragma unroll
-        for (int cc = 0; cc < 16; ++cc) acc = fma(a[cc], yy[cc], acc);
+        __syncthreads();
+        ready = jr;
+        __syncthreads();
       }
-      __syncthreads();
+      const int64_t c0 = j * TS + ty * 16;
+#pragma unroll
+      for (int cc = 0; cc < 16; ++cc) acc = fma(a[cc], __ldcg(y + c0 + cc), acc);
+#pragma unroll
+      for (int cc = 0; cc < 16; ++cc) a[cc] = an[cc];
     }
     red[ty][tx] = acc;
     __syncthreads();
-    if (tid < TS) {
-      const double bb = (r0 + tid < n) ? b[r0 + tid] : 0.0;
-      part[tid] = bb - (red[0][tid] + red[1][tid] + red[2][tid] + red[3][tid]);
-    }
+    if (tid < TS) part[tid] = bb - (red[0][tid] + red[1][tid] + red[2][tid] + red[3][tid]);
     __syncthreads();
     // y_r = Dinv_r * part
-    const double* D = Dinv + r * TS * TS;
     double s = 0.0;
 #pragma unroll
-    for (int cc = 0; cc < 16; ++cc) s = fma(D[tx + (ty * 16 + cc) * TS], part[ty * 16 + cc], s);
+    for (int cc = 0; cc < 16; ++cc) s = fma(dv[cc], part[ty * 16 + cc], s);
     red[ty][tx] = s;
     __syncthreads();
     if (tid < TS && r0 + tid < n) y[r0 + tid] = red[0][tid] + red[1][tid] + red[2][tid] + red[3][tid];
-    __threadfence();
+    // bar.sync orders the block's stores before thread 0's gpu-scope release (cumulative)
     __syncthreads();
     if (tid == 0) st_release(flags + r, epoch);
   }
@@ -204,28 +224,46 @@ __global__ void __launch_bounds__(256) trsv_bwd_kernel(
     double acc[16];
 #pragma unroll
     for (int cc = 0; cc < 16; ++cc) acc[cc] = 0.0;
-    int64_t j = nblk - 1;
-    while (j > r) {
-      __shared__ int64_t jr;
-      if (tid == 0) {
-        while (ld_acquire(flags + j) != epoch) __nanosleep(20);
-        int64_t e = j;
-        while (e - 1 > r && ld_acquire(flags + e - 1) == epoch) --e;
-        jr = e;
-      }
-      __syncthreads();
-      const int64_t je = jr;
-      for (; j >= je; --j) {
-        const int64_t rowj = j * TS + tx;
-        const double xv = (rowj < n) ? __ldcg(x + rowj) : 0.0;
-        const int64_t c0 = r0 + ty * 16;
+    // tiles (j, r), j = nblk-1 .. r+1; tile j-1 is prefetched before waiting for block j;
+    // the transposed diagonal inverse and y_r are loaded up front (off the chain)
+    const int64_t c0 = r0 + ty * 16;
+    const double* D = Dinv + r * TS * TS;
+    double dv[16];
 #pragma unroll
-        for (int cc = 0; cc < 16; ++cc) {
-          const double a = (rowj < n) ? C[rowj + (c0 + cc) * ldc] : 0.0;
-          acc[cc] = fma(a, xv, acc[cc]);
-        }
+    for (int cc = 0; cc < 16; ++cc) dv[cc] = D[tx + (ty * 16 + cc) * TS];
+    const double yr = (tid < TS && r0 + tid < n) ? y[r0 + tid] : 0.0;
+    double a[16];
+    if (nblk - 1 > r) {
+      const int64_t rowj = (nblk - 1) * TS + tx;
+#pragma unroll
+      for (int cc = 0; cc < 16; ++cc) a[cc] = (rowj < n) ? C[rowj + (c0 + cc) * ldc] : 0.0;
+    }
+    int64_t ready = nblk;  // lowest block index known to be published
+    for (int64_t j = nblk - 1; j > r; --j) {
+      double an[16];
+      if (j - 1 > r) {
+        const int64_t rown = (j - 1) * TS + tx;
+#pragma unroll
+        for (int cc = 0; cc < 16; ++cc) an[cc] = (rown < n) ? C[rown + (c0 + cc) * ldc] : 0.0;
       }
-      __syncthreads();
+      if (j < ready) {
+        __shared__ int64_t jr;
+        if (tid == 0) {
+          while (ld_acquire(flags + j) != epoch) __nanosleep(20);
+          int64_t e = j;
+          while (e - 1 > r && ld_acquire(flags + e - 1) == epoch) --e;
+          jr = e;
+        }
+        __syncthreads();
+        ready = jr;
+        __syncthreads();
+      }
+      const int64_t rowj = j * TS + tx;
+      const double xv = (rowj < n) ? __ldcg(x + rowj) : 0.0;
+#pragma unroll
+      for (int cc = 0; cc < 16; ++cc) acc[cc] = fma(a[cc], xv, acc[cc]);
+#pragma unroll
+      for (int cc = 0; cc < 16; ++cc) a[cc] = an[cc];
     }
     // reduce acc[cc] over the 64 rows (tx): warp shuffle, then the two warps per ty
 #pragma unroll
@@ -238,16 +276,14 @@ __global__ void __launch_bounds__(256) trsv_bwd_kernel(
     if (tid < TS) {
       const int g = tid >> 4, cc = tid & 15;  // column tid = g*16 + cc belongs to ty = g (warps 2g, 2g+1)
       const double sumc = red[2 * g][cc] + red[2 * g + 1][cc];
-      const double yy = (r0 + tid < n) ? y[r0 + tid] : 0.0;
-      part[tid] = yy - sumc;
+      part[tid] = yr - sumc;
     }
     __syncthreads();
-    // x_r = Dinv_r^T part:  x[c] = sum_c' Dinv[c' + c*TS] part[c']
-    const double* D = Dinv + r * TS * TS;
+    // x_r = Dinv_r^T part with the pre-transposed block (coalesced):
+    // x[c] = sum_c' DinvT[c + c'*TS] part[c']
     double s = 0.0;
 #pragma unroll
-    for (int cc = 0; cc < 16; ++cc) s = fma(D[(ty * 16 + cc) + tx * TS], part[ty * 16 + cc], s);
-    __syncthreads();
+    for (int cc = 0; cc < 16; ++cc) s = fma(dv[cc], part[ty * 16 + cc], s);
     red[ty][tx] = s;
     __syncthreads();
     if (tid < TS && r0 + tid < n) {
@@ -257,7 +293,7 @@ __global__ void __launch_bounds__(256) trsv_bwd_kernel(
       I[r0 + tid] = iv;
       if (Icap) Icap[r0 + tid] = iv;
     }
-    __threadfence();
+    // bar.sync orders the block's stores before thread 0's gpu-scope release (cumulative)
     __syncthreads();
     if (tid == 0) st_release(flags + r, epoch);
   }
@@ -269,7 +305,7 @@ int64_t td1_plan_init(em_td1_plan* P, const double* L, int64_t ldl, const double
   const int64_t n = P->n;
   P->C.alloc((size_t)n * n, st);
   P->R.alloc((size_t)n * n, st);
-  dim3 grid((unsigned)imin64((n + 255) / 256, 64), (unsigned)n);
+  dim3 grid((unsigned)imin64((n + 255) / 256, 64), (unsigned)imin64(n, 65535));
   td1_z_kernel<<<grid, 256, 0, st>>>(n, L, ldl, R, ldr, P->dt * P->theta, P->C.p, P->R.p);
   EM_LAUNCHED();
   const int64_t piv = potrf(st, n, P->C.p, n);
@@ -277,6 +313,9 @@ int64_t td1_plan_init(em_td1_plan* P, const double* L, int64_t ldl, const double
   const int64_t nblk = (n + TS - 1) / TS;
   P->Dinv.alloc((size_t)nblk * TS * TS, st);
   trtri_blocks(st, TS, n, P->C.p, n, P->Dinv.p);
+  P->DinvT.alloc((size_t)nblk * TS * TS, st);
+  transpose_blocks_kernel<<<(unsigned)nblk, 256, 0, st>>>(P->Dinv.p, P->DinvT.p);
+  EM_LAUNCHED();
   P->E.alloc((size_t)n * imax64(P->n_u, 1), st);
   if (P->n_u > 0) {
     td1_e_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, P->n_p, P->n_s, P->dt, P->theta,
@@ -328,7 +367,7 @@ static void td1_solve_step(em_td1_plan* P, double* I, double* Icap_col) {
   }
   {
     Stage s(st, ST_TD1_BWD);
-    trsv_bwd_kernel<<<grid, 256, 0, st>>>(n, P->C.p, n, P->Dinv.p, P->y.p, P->x.p, I, Icap_col,
+    trsv_bwd_kernel<<<grid, 256, 0, st>>>(n, P->C.p, n, P->DinvT.p, P->y.p, P->x.p, I, Icap_col,
                                           P->flags->p + nblk, P->counters->p + 1, P->epoch);
     EM_LAUNCHED();
   }
