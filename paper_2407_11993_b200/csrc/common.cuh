@@ -45,6 +45,14 @@ EM_DEVINL void cp_async_wait() {
 __host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
 __host__ __device__ __forceinline__ int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }
 
+// Programmatic dependent launch (kernels launched with launch_pdl): code before
+// pdl_wait() may only read data written before the PREVIOUS kernel started (the
+// predecessor of the predecessor has completed once this grid is running, because
+// every kernel in such a chain calls pdl_wait() before pdl_trigger()). No-ops for a
+// normal launch.
+EM_DEVINL void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+EM_DEVINL void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
 EM_DEVINL double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

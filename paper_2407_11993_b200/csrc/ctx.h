@@ -6,6 +6,7 @@
 
 #include <atomic>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/eddymodes_b200.h"
@@ -42,6 +43,26 @@ struct ArgError {
     ::em::count_launch();                  \
     EM_CK(cudaGetLastError());             \
   } while (0)
+
+// Launch with programmatic stream serialization: the kernel may start while its
+// predecessor drains; it must call pdl_wait() (common.cuh) before touching the
+// predecessor's outputs.
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  EM_CK(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+  count_launch();
+}
 
 // Stream-ordered device buffer (cudaMallocAsync pool).
 struct DBuf {

@@ -27,6 +27,31 @@ bool sym_sparse_mm(cudaStream_t st, int64_t n, const double* A, int64_t lda, int
 void symv_lower(cudaStream_t st, int64_t n, double alpha, const double* A, int64_t lda,
                 const double* x, double beta, double* y, double* work);
 size_t symv_work_size(int64_t n);
+// Tridiagonalisation column (sytrd.cu): x is the raw column; the symv CTAs run dlarfg
+// themselves from the sum-of-squares partials and use v = [1, scale * x[1:]].
+struct SymvLarfg {
+  const double* part = nullptr;  // partials of ||x[1:]||^2
+  int64_t nparts = 0;
+  const double* alpha = nullptr;  // x[0]
+  double* tau = nullptr;          // outputs, written by CTA 0
+  double* e = nullptr;
+  double* scale = nullptr;
+};
+// latrd panel products t = [W_p^T v | A_p^T v] (2 x 64) from per-CTA partials over rows
+// >= c+2 of the raw column (times scale) plus row c+1 (v = 1 there).
+struct LatrdT {
+  int i = 0;  // panel columns so far (0: nothing to do)
+  int64_t G = 0;
+  const double* dpart = nullptr;  // [G][128]
+  const double* wr1 = nullptr;    // W row c+1 (stride ldw)
+  int64_t ldw = 0;
+  const double* ar1 = nullptr;    // A row c+1 from column i0 (stride lda)
+  int64_t lda = 0;
+  const double* scale = nullptr;
+  double* t = nullptr;  // [128]
+};
+void symv_lower_latrd(cudaStream_t st, int64_t n, const double* A, int64_t lda, const double* x,
+                      double* y, double* work, const SymvLarfg& lf, const LatrdT& lt);
 
 // sytrd.cu: Householder tridiagonalisation (lower). On exit d (n), e (n-1), tau (n-1);
 // reflectors stored below the subdiagonal of A (LAPACK dsytrd convention).

@@ -43,6 +43,73 @@ EM_DEVINL void symv_load_tile(double (&a)[2][8], const double* A, int64_t lda,
   }
 }
 
+// x as the tiles see it: xs * x[r], except x[0] = 1 when unit0 (a Householder vector
+// whose first entry is implicit, dlarfg convention).
+EM_DEVINL double symv_xval(const double* x, int64_t r, int64_t n, double xs, bool unit0) {
+  if (r >= n) return 0.0;
+  if (unit0 && r == 0) return 1.0;
+  return xs * __ldcg(x + r);
+}
+
+// One 64x64 tile already in registers: row partials += A_ij x_j, column sums
+// A_ij^T x_i written to wdst[0..64). diag: tile on the diagonal (lower part only).
+EM_DEVINL void symv_tile_body(const double (&a)[2][8], int64_t n, const double* x, int64_t c0,
+                              bool diag, double xi0, double xi1, double& row0, double& row1,
+                              double* wdst, int lane, int w, double xs = 1.0,
+                              bool unit0 = false) {
+  double xj[8];
+#pragma unroll
+  for (int cc = 0; cc < 8; ++cc) xj[cc] = symv_xval(x, c0 + 8 * w + cc, n, xs, unit0);
+  double col[8];
+  if (!diag) {
+#pragma unroll
+    for (int cc = 0; cc < 8; ++cc) {
+      row0 = fma(a[0][cc], xj[cc], row0);
+      row1 = fma(a[1][cc], xj[cc], row1);
+      col[cc] = fma(a[0][cc], xi0, a[1][cc] * xi1);
+    }
+  } else {
+    // diagonal tile: lower triangle only (r >= c for rows, r > c for the transpose)
+#pragma unroll
+    for (int cc = 0; cc < 8; ++cc) {
+      const int c = 8 * w + cc;
+      const double l0 = (lane >= c) ? a[0][cc] : 0.0;
+      const double l1 = (lane + 32 >= c) ? a[1][cc] : 0.0;
+      row0 = fma(l0, xj[cc], row0);
+      row1 = fma(l1, xj[cc], row1);
+      const double s0 = (lane > c) ? a[0][cc] : 0.0;
+      const double s1 = (lane + 32 > c) ? a[1][cc] : 0.0;
+      col[cc] = fma(s0, xi0, s1 * xi1);
+    }
+  }
+#pragma unroll
+  for (int cc = 0; cc < 4; ++cc) {  // offset 16: lanes < 16 keep cols 0..3, others 4..7
+    const bool hi = lane & 16;
+    const double send = hi ? col[cc] : col[cc + 4];
+    const double keep = hi ? col[cc + 4] : col[cc];
+    col[cc] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int cc = 0; cc < 2; ++cc) {  // offset 8
+    const bool hi = lane & 8;
+    const double send = hi ? col[cc] : col[cc + 2];
+    const double keep = hi ? col[cc + 2] : col[cc];
+    col[cc] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  {  // offset 4
+    const bool hi = lane & 4;
+    const double send = hi ? col[0] : col[1];
+    const double keep = hi ? col[1] : col[0];
+    col[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  col[0] += __shfl_xor_sync(0xffffffffu, col[0], 2);
+  col[0] += __shfl_xor_sync(0xffffffffu, col[0], 1);
+  if ((lane & 3) == 0) {
+    const int cc = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+    wdst[8 * w + cc] = col[0];
+  }
+}
+
 // Strip chunk `ch` of block row i (tiles j in [ch*SVCH, min(i, ch*SVCH+SVCH-1)]);
 // 256 threads. red: shared [8][SV].
 EM_DEVINL void symv_strip(int64_t n, const double* A, int64_t lda,
@@ -77,60 +144,7 @@ EM_DEVINL void symv_strip(int64_t n, const double* A, int64_t lda,
       else
         symv_load_tile<false>(nxt, A, lda, n, r0, c1, lane, w);
     }
-    double xj[8];
-#pragma unroll
-    for (int cc = 0; cc < 8; ++cc) {
-      const int64_t c = c0 + 8 * w + cc;
-      xj[cc] = (c < n) ? __ldcg(x + c) : 0.0;
-    }
-    double col[8];
-    if (j != i) {
-#pragma unroll
-      for (int cc = 0; cc < 8; ++cc) {
-        row0 = fma(a[0][cc], xj[cc], row0);
-        row1 = fma(a[1][cc], xj[cc], row1);
-        col[cc] = fma(a[0][cc], xi0, a[1][cc] * xi1);
-      }
-    } else {
-      // diagonal tile: lower triangle only (r >= c for rows, r > c for the transpose)
-#pragma unroll
-      for (int cc = 0; cc < 8; ++cc) {
-        const int c = 8 * w + cc;
-        const double l0 = (lane >= c) ? a[0][cc] : 0.0;
-        const double l1 = (lane + 32 >= c) ? a[1][cc] : 0.0;
-        row0 = fma(l0, xj[cc], row0);
-        row1 = fma(l1, xj[cc], row1);
-        const double s0 = (lane > c) ? a[0][cc] : 0.0;
-        const double s1 = (lane + 32 > c) ? a[1][cc] : 0.0;
-        col[cc] = fma(s0, xi0, s1 * xi1);
-      }
-    }
-#pragma unroll
-    for (int cc = 0; cc < 4; ++cc) {  // offset 16: lanes < 16 keep cols 0..3, others 4..7
-      const bool hi = lane & 16;
-      const double send = hi ? col[cc] : col[cc + 4];
-      const double keep = hi ? col[cc + 4] : col[cc];
-      col[cc] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-    }
-#pragma unroll
-    for (int cc = 0; cc < 2; ++cc) {  // offset 8
-      const bool hi = lane & 8;
-      const double send = hi ? col[cc] : col[cc + 2];
-      const double keep = hi ? col[cc + 2] : col[cc];
-      col[cc] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-    }
-    {  // offset 4
-      const bool hi = lane & 4;
-      const double send = hi ? col[0] : col[1];
-      const double keep = hi ? col[1] : col[0];
-      col[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-    }
-    col[0] += __shfl_xor_sync(0xffffffffu, col[0], 2);
-    col[0] += __shfl_xor_sync(0xffffffffu, col[0], 1);
-    if ((lane & 3) == 0) {
-      const int cc = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-      wcol[(i * nb + j) * SV + 8 * w + cc] = col[0];
-    }
+    symv_tile_body(a, n, x, c0, j == i, xi0, xi1, row0, row1, wcol + (i * nb + j) * SV, lane, w);
   }
   __syncthreads();  // red may still be read by a previous strip's reduction
   red[w][lane] = row0;

@@ -6,8 +6,10 @@
 //
 // Per panel column the memory-bound part is one lower-triangle symv over the
 // trailing matrix (symv.cu); the rank-2k trailing update and the
-// back-transform run on the DMMA GEMM. The per-column panel work (latrd) uses
-// 8 threads per row so that a 16k-row column update keeps ~130k threads busy.
+// back-transform run on the DMMA GEMM. A panel column is four launches:
+// latrd_col_kernel (finish the previous W column, update this column, partials of
+// its norm and of the panel products), the symv with dlarfg folded into its
+// prologue, the symv reduction (+ panel products t), latrd_w_kernel.
 #include "common.cuh"
 #include "ctx.h"
 #include "gemm.h"
@@ -17,15 +19,6 @@ namespace em {
 
 constexpr int TRD_NB = 64;   // panel width
 constexpr int RT = 256;
-constexpr int TPR = 8;                 // threads per row in the panel kernels
-constexpr int ROWS_PER_CTA = RT / TPR;  // 32
-
-EM_DEVINL double group_sum8(double v) {
-  v += __shfl_xor_sync(0xffffffffu, v, 4);
-  v += __shfl_xor_sync(0xffffffffu, v, 2);
-  v += __shfl_xor_sync(0xffffffffu, v, 1);
-  return v;
-}
 
 EM_DEVINL double block_sum(double v, double* red) {
   v = warp_sum(v);
@@ -39,176 +32,177 @@ EM_DEVINL double block_sum(double v, double* red) {
   return t;  // valid in thread 0
 }
 
-// A[c:n, c] -= A[c:n, i0:c] W[c, 0:i]^T + W[c:n, 0:i] A[c, i0:c]^T, then per-CTA
-// partial sums of squares of the updated A[c+2:n, c] (the dlarfg norm).
-__global__ void __launch_bounds__(RT) latrd_colupd_kernel(int64_t n, double* A, int64_t lda,
-                                                          int64_t i0, int64_t c,
-                                                          const double* __restrict__ W,
-                                                          int64_t ldw, double* part,
-                                                          double* alpha_buf) {
-  const int i = (int)(c - i0);
+constexpr int CRW = 64;                 // rows per CTA in the column kernels
+constexpr int CTPR = RT / CRW;          // 4 threads per row
+constexpr int CKQ = TRD_NB / CTPR;      // panel columns per thread (16)
+
+// Column kernel for panel column c (i = c - i0 earlier panel columns), LAPACK dlatrd:
+//  (1) finish W[:, i-1]: w += alpha v, alpha = -tau/2 (w.v), from wtmp (tau (y - ...))
+//      and the w.v partials of the previous latrd_w_kernel (every CTA reduces them);
+//  (2) A[c:n, c] -= A[c:n, i0:c] W[c, 0:i]^T + W[c:n, 0:i] A[c, i0:c]^T;
+//  (3) per-CTA partials over rows >= c+2 of ||x||^2 (dlarfg) and of W_p^T x, A_p^T x
+//      (the dlatrd panel products, completed in symv_reduce2_kernel), x = the updated
+//      column; alpha_buf = A[c+1, c], d[c] = A[c, c].
+// upd = 0: only (1), after the last column of a panel.
+__global__ void __launch_bounds__(RT) latrd_col_kernel(
+    int64_t n, double* A, int64_t lda, int64_t i0, int64_t c, int i, int upd, double* W,
+    int64_t ldw, const double* wtmp, const double* part_wv, int64_t n_wv, const double* tau,
+    double* part_norm, double* dpart, double* alpha_buf, double* d) {
   __shared__ double wr[TRD_NB], ar[TRD_NB], red[RT / 32];
-  for (int k = threadIdx.x; k < i; k += blockDim.x) {
-    wr[k] = W[(c - i0) + k * ldw];  // W row c (W rows are indexed from i0)
-    ar[k] = A[c + (i0 + k) * lda];  // A row c
+  __shared__ double pred[RT / 32][2 * TRD_NB];
+  __shared__ double s_alpha;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int sub = tid & (CTPR - 1);
+  const int64_t r = c + blockIdx.x * (int64_t)CRW + tid / CTPR;
+  const bool valid = r < n;
+  // before the dependency wait: panel columns k < i-1 (finished two launches ago or
+  // earlier) and the raw column c (only this kernel writes it)
+  double av[CKQ], wv[CKQ];
+  double acol = 0.0;
+  if (upd) {
+    for (int k = tid; k < i - 1; k += RT) {
+      wr[k] = W[(c - i0) + k * ldw];
+      ar[k] = A[c + (i0 + k) * lda];
+    }
+#pragma unroll
+    for (int q = 0; q < CKQ; ++q) {
+      const int k = sub + CTPR * q;
+      const bool ok = valid && k < i - 1;
+      av[q] = ok ? A[r + (i0 + k) * lda] : 0.0;
+      wv[q] = ok ? W[(r - i0) + k * ldw] : 0.0;
+    }
+    if (valid) acol = A[r + c * lda];
   }
-  __syncthreads();
-  const int sub = threadIdx.x & (TPR - 1);
-  const int64_t r = c + blockIdx.x * (int64_t)ROWS_PER_CTA + threadIdx.x / TPR;
-  double ss = 0.0;
-  if (r < n) {
+  pdl_wait();
+  pdl_trigger();
+  double alpha_p = 0.0;
+  if (i > 0) {
     double s = 0.0;
-    for (int k = sub; k < i; k += TPR) {
-      s = fma(A[r + (i0 + k) * lda], wr[k], s);
-      s = fma(W[(r - i0) + k * ldw], ar[k], s);
-    }
-    s = group_sum8(s);
-    if (sub == 0) {
-      const double v = A[r + c * lda] - s;
-      if (i > 0) A[r + c * lda] = v;
-      if (r >= c + 2) ss = v * v;
-      if (r == c + 1) *alpha_buf = v;  // dlarfg's alpha, read by larfg_kernel
-    }
-  } else {
-    group_sum8(0.0);
+    for (int64_t q = tid; q < n_wv; q += RT) s += __ldcg(part_wv + q);
+    const double t = block_sum(s, red);
+    if (tid == 0) s_alpha = -0.5 * __ldcg(tau + c - 1) * t;
+    __syncthreads();
+    alpha_p = s_alpha;
   }
-  const double t = block_sum(ss, red);
-  if (threadIdx.x == 0) part[blockIdx.x] = t;
-}
-
-// dlarfg on x = A[c+1:n, c] with ||x[1:]||^2 = sum(part): beta, tau; v = [1, x[1:]/(alpha-beta)];
-// e[c] = beta; d[c] = A[c,c]. Every CTA reduces the partials itself and scales its slice.
-__global__ void __launch_bounds__(RT) larfg_kernel(int64_t n, double* A, int64_t lda, int64_t c,
-                                                   const double* __restrict__ part, int nparts,
-                                                   const double* __restrict__ alpha_buf,
-                                                   double* d, double* e, double* tau) {
-  __shared__ double red[RT / 32];
-  __shared__ double sc;
-  double s = 0.0;
-  for (int p = threadIdx.x; p < nparts; p += blockDim.x) s += part[p];
-  const double tot = block_sum(s, red);
-  const double alpha = *alpha_buf;
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    d[c] = A[c + c * lda];
-    A[(c + 1) + c * lda] = 1.0;  // v[0]; alpha itself is read from alpha_buf
+  // column i-1 of W: w + alpha v (v_{c-1} = A[:, c-1], written by the previous launch)
+  double wlast = 0.0, vlast = 0.0;
+  if (i > 0 && valid) {
+    vlast = __ldcg(A + r + (c - 1) * lda);
+    wlast = fma(alpha_p, vlast, __ldcg(wtmp + r));
   }
-  if (threadIdx.x == 0) {
-    const double xnorm = sqrt(tot);
-    double scale = 0.0;
-    if (xnorm == 0.0) {
-      if (blockIdx.x == 0) {
-        tau[c] = 0.0;
-        e[c] = alpha;
-      }
-    } else {
-      const double beta = -copysign(hypot(alpha, xnorm), alpha);
-      scale = 1.0 / (alpha - beta);
-      if (blockIdx.x == 0) {
-        tau[c] = (beta - alpha) / beta;
-        e[c] = beta;
-      }
-    }
-    sc = scale;
+  if (!upd) {
+    if (valid && sub == 0) W[(r - i0) + (int64_t)(i - 1) * ldw] = wlast;
+    return;
+  }
+  if (i > 0 && tid == 0) {
+    const double vc = __ldcg(A + c + (c - 1) * lda);
+    wr[i - 1] = fma(alpha_p, vc, __ldcg(wtmp + c));
+    ar[i - 1] = vc;
   }
   __syncthreads();
-  const double f = sc;
-  if (f != 0.0)
-    for (int64_t r = c + 2 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
-         r += (int64_t)gridDim.x * blockDim.x)
-      A[r + c * lda] *= f;
-  // every CTA has read alpha above; make sure all CTAs did before CTA 0 overwrites it
-}
-
-__global__ void larfg_finish_kernel(double* A, int64_t lda, int64_t c, double* d) {
-  if (threadIdx.x == 0) {
-    d[c] = A[c + c * lda];
-    A[(c + 1) + c * lda] = 1.0;
+  if (i > 0 && valid && sub == ((i - 1) & (CTPR - 1))) {
+    W[(r - i0) + (int64_t)(i - 1) * ldw] = wlast;
   }
-}
-
-// Partial dots: tmp[which][k] partials over row chunks of  W[c+1:, k].v (which 0)
-// and A[c+1:, i0+k].v (which 1). grid (chunks, ceil(2i/8)); warp per column.
-constexpr int DOT_ROWS = 2048;
-__global__ void __launch_bounds__(RT) latrd_dots_kernel(int64_t n, const double* A, int64_t lda,
-                                                        int64_t i0, int64_t c, const double* W,
-                                                        int64_t ldw, double* dpart, int nchunk) {
-  const int i = (int)(c - i0);
-  const int col = blockIdx.y * 8 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (col >= 2 * i) return;
-  const int which = col / i, k = col % i;
-  const int64_t rb = c + 1 + blockIdx.x * (int64_t)DOT_ROWS;
-  const int64_t re = imin64(n, rb + DOT_ROWS);
-  const double* v = A + c * lda;
-  const double* colp = which == 0 ? W + k * ldw - i0 : A + (i0 + k) * lda;
   double s = 0.0;
-  for (int64_t r = rb + lane; r < re; r += 32) s = fma(colp[r], v[r], s);
-  s = warp_sum(s);
-  if (lane == 0) dpart[(which * TRD_NB + k) * nchunk + blockIdx.x] = s;
+#pragma unroll
+  for (int q = 0; q < CKQ; ++q) {
+    const int k = sub + CTPR * q;
+    if (k == i - 1) {
+      av[q] = vlast;
+      wv[q] = wlast;
+    }
+    if (k < i) s = fma(av[q], wr[k], fma(wv[q], ar[k], s));
+  }
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+  s += __shfl_xor_sync(0xffffffffu, s, 2);
+  double x = 0.0;
+  if (valid) {
+    x = acol - s;
+    if (sub == 0) {
+      if (i > 0) A[r + c * lda] = x;
+      if (r == c) d[c] = x;
+      if (r == c + 1) *alpha_buf = x;
+    }
+  }
+  const bool tail = valid && r >= c + 2;
+  const double ss = (tail && sub == 0) ? x * x : 0.0;
+  if (i > 0) {
+    const double xt = tail ? x : 0.0;
+#pragma unroll
+    for (int q = 0; q < CKQ; ++q) {
+      double pw = wv[q] * xt, pa = av[q] * xt;
+#pragma unroll
+      for (int off = 4; off < 32; off <<= 1) {
+        pw += __shfl_xor_sync(0xffffffffu, pw, off);
+        pa += __shfl_xor_sync(0xffffffffu, pa, off);
+      }
+      if (lane < CTPR) {
+        pred[warp][lane + CTPR * q] = pw;
+        pred[warp][TRD_NB + lane + CTPR * q] = pa;
+      }
+    }
+    __syncthreads();
+    if (tid < 2 * TRD_NB) {
+      double v = 0.0;
+      if ((tid & (TRD_NB - 1)) < i)
+#pragma unroll
+        for (int w8 = 0; w8 < RT / 32; ++w8) v += pred[w8][tid];
+      dpart[blockIdx.x * (int64_t)(2 * TRD_NB) + tid] = v;
+    }
+  }
+  const double tn = block_sum(ss, red);
+  if (tid == 0) part_norm[blockIdx.x] = tn;
 }
 
-// w = tau*(w - A_p t1 - W_p t2), t1/t2 summed from the chunk partials; per-CTA
-// partial dot of w and v.
-__global__ void __launch_bounds__(RT) latrd_wcol_kernel(int64_t n, const double* A, int64_t lda,
-                                                        int64_t i0, int64_t c, double* W,
-                                                        int64_t ldw, const double* dpart,
-                                                        int nchunk, const double* tau,
-                                                        double* part) {
-  const int i = (int)(c - i0);
+// w = tau (y - A_p t1 - W_p t2) on rows >= c+1 (y in wtmp, overwritten with w);
+// v = [1, scale x[1:]] written back into A[c+1:, c]; per-CTA partials of w.v.
+__global__ void __launch_bounds__(RT) latrd_w_kernel(int64_t n, double* A, int64_t lda,
+                                                     int64_t i0, int64_t c, int i,
+                                                     const double* W, int64_t ldw, double* wtmp,
+                                                     const double* tvec, const double* tau,
+                                                     const double* scale, double* part_wv) {
   __shared__ double t1[TRD_NB], t2[TRD_NB], red[RT / 32];
-  for (int q = threadIdx.x; q < 2 * i; q += blockDim.x) {
-    const int which = q / i, k = q % i;
-    double s = 0.0;
-    for (int ch = 0; ch < nchunk; ++ch) s += dpart[(which * TRD_NB + k) * nchunk + ch];
-    if (which == 0)
-      t1[k] = s;
-    else
-      t2[k] = s;
+  const int tid = threadIdx.x;
+  const int sub = tid & (CTPR - 1);
+  const int64_t r = c + 1 + blockIdx.x * (int64_t)CRW + tid / CTPR;
+  const bool valid = r < n;
+  // before the dependency wait: the panel (complete), tau/scale (from the symv, two
+  // launches back) and the raw column
+  double av[CKQ], wv[CKQ];
+#pragma unroll
+  for (int q = 0; q < CKQ; ++q) {
+    const int k = sub + CTPR * q;
+    const bool ok = valid && k < i;
+    av[q] = ok ? A[r + (i0 + k) * lda] : 0.0;
+    wv[q] = ok ? W[(r - i0) + k * ldw] : 0.0;
+  }
+  const double tc = tau[c], sc = *scale;
+  const double xr = valid ? A[r + c * lda] : 0.0;
+  pdl_wait();
+  pdl_trigger();
+  for (int k = tid; k < i; k += RT) {
+    t1[k] = __ldcg(tvec + k);
+    t2[k] = __ldcg(tvec + TRD_NB + k);
   }
   __syncthreads();
-  const double tc = tau[c];
-  const double* v = A + c * lda;
-  double* w = W + i * ldw;
-  const int sub = threadIdx.x & (TPR - 1);
-  const int64_t r = c + 1 + blockIdx.x * (int64_t)ROWS_PER_CTA + threadIdx.x / TPR;
+  double s = 0.0;
+#pragma unroll
+  for (int q = 0; q < CKQ; ++q) {
+    const int k = sub + CTPR * q;
+    if (k < i) s = fma(av[q], t1[k], fma(wv[q], t2[k], s));
+  }
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+  s += __shfl_xor_sync(0xffffffffu, s, 2);
   double dd = 0.0;
-  if (r < n) {
-    double s = 0.0;
-    for (int k = sub; k < i; k += TPR) {
-      s = fma(A[r + (i0 + k) * lda], t1[k], s);
-      s = fma(W[(r - i0) + k * ldw], t2[k], s);
-    }
-    s = group_sum8(s);
-    if (sub == 0) {
-      const double x = tc * (w[r - i0] - s);
-      w[r - i0] = x;
-      dd = x * v[r];
-    }
-  } else {
-    group_sum8(0.0);
+  if (valid && sub == 0) {
+    const double v = (r == c + 1) ? 1.0 : sc * xr;
+    A[r + c * lda] = v;
+    const double x = tc * (__ldcg(wtmp + r) - s);
+    wtmp[r] = x;
+    dd = x * v;
   }
   const double t = block_sum(dd, red);
-  if (threadIdx.x == 0) part[blockIdx.x] = t;
-}
-
-// w += alpha v,  alpha = -tau/2 * (w.v)
-__global__ void latrd_wfix_kernel(int64_t n, const double* A, int64_t lda, int64_t i0, int64_t c,
-                                  double* W, int64_t ldw, const double* tau, const double* part,
-                                  int nparts) {
-  __shared__ double red[RT / 32];
-  double s = 0.0;
-  for (int p = threadIdx.x; p < nparts; p += blockDim.x) s += part[p];
-  __shared__ double alpha;
-  const double tot = block_sum(s, red);
-  if (threadIdx.x == 0) alpha = -0.5 * tau[c] * tot;
-  __syncthreads();
-  const int i = (int)(c - i0);
-  const double* v = A + c * lda;
-  double* w = W + i * ldw;
-  const double a = alpha;
-  for (int64_t r = c + 1 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
-       r += (int64_t)gridDim.x * blockDim.x)
-    w[r - i0] = fma(a, v[r], w[r - i0]);
+  if (tid == 0) part_wv[blockIdx.x] = t;
 }
 
 __global__ void set_diag_kernel(int64_t n, const double* A, int64_t lda, int64_t c, double* d) {
@@ -243,15 +237,14 @@ void sytrd_lower(cudaStream_t st, int64_t n, double* A, int64_t lda, double* d, 
   }
   DBuf W((size_t)n * TRD_NB, st);
   DBuf XW((size_t)n * 2 * TRD_NB, st), YW((size_t)n * 2 * TRD_NB, st);
-  const int max_rows_ctas = (int)((n + ROWS_PER_CTA - 1) / ROWS_PER_CTA);
-  DBuf part(imax64(max_rows_ctas, 1), st);
-  const int max_chunks = (int)((n + DOT_ROWS - 1) / DOT_ROWS);
-  DBuf dpart((size_t)2 * TRD_NB * max_chunks, st);
+  const int64_t gmax = (n + CRW - 1) / CRW;
+  DBuf part_norm(gmax, st), part_wv(gmax, st), dpart((size_t)gmax * 2 * TRD_NB, st);
+  DBuf wtmp(n, st), tvec(2 * TRD_NB, st), slots(2, st);  // slots: alpha, scale
   DBuf swork(symv_work_size(n), st);
-  DBuf abuf(1, st);
-  // Each panel's ~450 dependent small launches are captured once into a CUDA graph
-  // and replayed (cudaGraphExecUpdate reuses the executable across panels), which
-  // removes most of the per-launch gap that dominates the short columns.
+  double* alpha_buf = slots.p;
+  double* scale_buf = slots.p + 1;
+  // Each panel's ~260 dependent launches (4 per column) are captured once into a CUDA
+  // graph and replayed (cudaGraphExecUpdate reuses the executable across panels).
   const bool use_graph = true;
   cudaGraphExec_t exec = nullptr;
   // capture on a private stream (the context stream may be the legacy default stream,
@@ -261,36 +254,51 @@ void sytrd_lower(cudaStream_t st, int64_t n, double* A, int64_t lda, double* d, 
   for (int64_t i0 = 0; i0 < n; i0 += TRD_NB) {
     const int w = (int)imin64(TRD_NB, n - i0);
     if (use_graph) EM_CK(cudaStreamBeginCapture(sc, cudaStreamCaptureModeThreadLocal));
+    int64_t gw_prev = 0;
+    bool last = false;
     for (int i = 0; i < w; ++i) {
       const int64_t c = i0 + i;
-      const int gcol = (int)((n - c + ROWS_PER_CTA - 1) / ROWS_PER_CTA);
-      latrd_colupd_kernel<<<gcol, RT, 0, sc>>>(n, A, lda, i0, c, W.p, n, part.p, abuf.p);
-      EM_LAUNCHED();
+      const int64_t G = (n - c + CRW - 1) / CRW;
+      launch_pdl(latrd_col_kernel, dim3((unsigned)G), dim3(RT), 0, sc, n, A, lda, i0, c, i, 1,
+                 W.p, (int64_t)n, (const double*)wtmp.p, (const double*)part_wv.p, gw_prev,
+                 (const double*)tau, part_norm.p, dpart.p, alpha_buf, d);
       if (c == n - 1) {
-        set_diag_kernel<<<1, 32, 0, sc>>>(n, A, lda, c, d);
-        EM_LAUNCHED();
+        last = true;
         break;
       }
       const int64_t m = n - c - 1;
-      const int gsc = (int)imax64(1, imin64((m + RT - 1) / RT, 2 * num_sms()));
-      larfg_kernel<<<gsc, RT, 0, sc>>>(n, A, lda, c, part.p, gcol, abuf.p, d, e, tau);
-      EM_LAUNCHED();
-      // W[c+1:, i] = A22 v  (A22 = trailing lower triangle)
-      symv_lower(sc, m, 1.0, A + (c + 1) + (c + 1) * lda, lda, A + (c + 1) + c * lda, 0.0,
-                 W.p + (c + 1 - i0) + (int64_t)i * n, swork.p);
-      const int nchunk = (int)((m + DOT_ROWS - 1) / DOT_ROWS);
-      if (i > 0) {
-        dim3 gd((unsigned)nchunk, (unsigned)((2 * i + 7) / 8));
-        latrd_dots_kernel<<<gd, RT, 0, sc>>>(n, A, lda, i0, c, W.p, n, dpart.p, nchunk);
-        EM_LAUNCHED();
-      }
-      const int gw = (int)((m + ROWS_PER_CTA - 1) / ROWS_PER_CTA);
-      latrd_wcol_kernel<<<gw, RT, 0, sc>>>(n, A, lda, i0, c, W.p, n, dpart.p, nchunk, tau,
-                                           part.p);
-      EM_LAUNCHED();
-      const int gf = (int)imax64(1, imin64((m + RT - 1) / RT, 2 * num_sms()));
-      latrd_wfix_kernel<<<gf, RT, 0, sc>>>(n, A, lda, i0, c, W.p, n, tau, part.p, gw);
-      EM_LAUNCHED();
+      SymvLarfg lf;
+      lf.part = part_norm.p;
+      lf.nparts = G;
+      lf.alpha = alpha_buf;
+      lf.tau = tau + c;
+      lf.e = e + c;
+      lf.scale = scale_buf;
+      LatrdT lt;
+      lt.i = i;
+      lt.G = G;
+      lt.dpart = dpart.p;
+      lt.wr1 = W.p + (c + 1 - i0);
+      lt.ldw = n;
+      lt.ar1 = A + (c + 1) + i0 * lda;
+      lt.lda = lda;
+      lt.scale = scale_buf;
+      lt.t = tvec.p;
+      // wtmp[c+1:] = A22 v with dlarfg folded into the symv and the panel products t
+      symv_lower_latrd(sc, m, A + (c + 1) + (c + 1) * lda, lda, A + (c + 1) + c * lda,
+                       wtmp.p + (c + 1), swork.p, lf, lt);
+      const int64_t gw = (m + CRW - 1) / CRW;
+      launch_pdl(latrd_w_kernel, dim3((unsigned)gw), dim3(RT), 0, sc, n, A, lda, i0, c, i,
+                 (const double*)W.p, (int64_t)n, wtmp.p, (const double*)tvec.p,
+                 (const double*)tau, (const double*)scale_buf, part_wv.p);
+      gw_prev = gw;
+    }
+    if (!last) {  // finish W[:, w-1] for the trailing update
+      const int64_t c = i0 + w;
+      const int64_t G = (n - c + CRW - 1) / CRW;
+      launch_pdl(latrd_col_kernel, dim3((unsigned)G), dim3(RT), 0, sc, n, A, lda, i0, c, w, 0,
+                 W.p, (int64_t)n, (const double*)wtmp.p, (const double*)part_wv.p, gw_prev,
+                 (const double*)tau, part_norm.p, dpart.p, alpha_buf, d);
     }
     if (use_graph) {
       cudaGraph_t g = nullptr;

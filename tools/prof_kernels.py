@@ -90,6 +90,30 @@ def main(which):
                                                    None)), reps=1)
         out["td1_n8192_per_step_ms"] = t / steps * 1e3
         lib.em_td1_plan_destroy(plan)
+    if which == "symvsweep":
+        big = torch.randn(n, n, device="cuda", dtype=torch.float64, generator=g)
+        x = torch.randn(n, device="cuda", dtype=torch.float64, generator=g)
+        y = torch.empty_like(x)
+        for m in (256, 512, 1024, 2048, 3072, 4096, 6144, 8192, 12288, 16384):
+            t = timed(lambda: nat.check(lib.em_symv_lower(ctx, m, 1.0, nat.ptr(big), n, nat.ptr(x),
+                                                          0.0, nat.ptr(y))), reps=20)
+            out[f"symv_{m}"] = {"us": t * 1e6, "GBps": 8 * m * m / 2 / t / 1e9}
+        del big
+    if which == "syev":
+        m = int(os.environ.get("SYEV_N", n))
+        b = torch.randn(m, m, device="cuda", dtype=torch.float64, generator=g)
+        a = (b + b.T).contiguous()
+        del b
+        w = torch.empty(m, device="cuda", dtype=torch.float64)
+        u = torch.empty(m, m, device="cuda", dtype=torch.float64)
+        for lvl in (1, 2):
+            w2 = a.clone()
+            nat.profile(lvl)
+            nat.check(lib.em_syev(ctx, m, nat.ptr(w2), m, nat.ptr(w), nat.ptr(u), m))
+            torch.cuda.synchronize()
+            out[f"syev_{m}_level{lvl}"] = nat.stage_times()
+            del w2
+        nat.profile(0)
     print(json.dumps(out))
 
 
