@@ -52,6 +52,17 @@ struct LatrdT {
 };
 void symv_lower_latrd(cudaStream_t st, int64_t n, const double* A, int64_t lda, const double* x,
                       double* y, double* work, const SymvLarfg& lf, const LatrdT& lt);
+// symv_tma.cu: TMA-fed variant. A tensor map spans a whole (rows x cols, ld) matrix; the
+// symv runs on the n x n block at coordinates (off, off). symv_map_make returns false
+// when TMA cannot address the matrix (base not 16-byte aligned or ld odd).
+struct alignas(64) SymvMap {
+  unsigned char opaque[2][128];  // CUtensorMaps: box 128 rows (even offsets), 130 rows (odd)
+};
+bool symv_map_make(SymvMap* m, const double* base, int64_t rows, int64_t cols, int64_t ld);
+size_t symv_tma_work_size(int64_t n);
+void symv_tma(cudaStream_t st, const SymvMap& m, int64_t off, int64_t n, double alpha,
+              const double* x, double beta, double* y, double* work, const SymvLarfg* lf,
+              const LatrdT* lt, bool pdl);
 
 // sytrd.cu: Householder tridiagonalisation (lower). On exit d (n), e (n-1), tau (n-1);
 // reflectors stored below the subdiagonal of A (LAPACK dsytrd convention).

@@ -7,6 +7,8 @@
 // (reference: td1_step_kernel's dense loop, _kernels.py:198-207) and exposed as
 // em_symv_lower; the tridiagonalisation runs the same tiles inside its fused
 // persistent kernel (sytrd_fused.cu).
+#include <algorithm>
+
 #include "common.cuh"
 #include "ctx.h"
 #include "linalg.h"
@@ -35,8 +37,9 @@ static SymvSched symv_sched(int64_t n) {
 
 size_t symv_work_size(int64_t n) {
   const int64_t nb = (n + SV - 1) / SV;
-  // wcol: nb*nb tiles; wrow: nb strips x (nb + 2) piece slots. Covers symv_work_doubles too.
-  return (size_t)(nb * nb * SV + nb * (nb + 2) * SV);
+  // wcol: nb*nb tiles; wrow: nb strips x (nb + 2) piece slots. Covers symv_work_doubles
+  // and the TMA variant's layout too.
+  return std::max((size_t)(nb * nb * SV + nb * (nb + 2) * SV), symv_tma_work_size(n));
 }
 
 __device__ __forceinline__ int64_t strip_of(int64_t t) {
@@ -196,6 +199,11 @@ __global__ void __launch_bounds__(512) symv_reduce2_kernel(int64_t n, double alp
 void symv_lower(cudaStream_t st, int64_t n, double alpha, const double* A, int64_t lda,
                 const double* x, double beta, double* y, double* work) {
   if (n <= 0) return;
+  SymvMap m;
+  if (symv_map_make(&m, A, n, n, lda)) {
+    symv_tma(st, m, 0, n, alpha, x, beta, y, work, nullptr, nullptr, false);
+    return;
+  }
   const SymvSched s = symv_sched(n);
   double* wcol = work;
   double* wrow = work + s.nb * s.nb * SV;

@@ -222,6 +222,7 @@ __global__ void restore_sub_kernel(int64_t n, double* A, int64_t lda, int64_t i0
 // em_config(EM_CFG_SYTRD_FUSED). The fused cooperative panel kernel (sytrd_fused.cu) is
 // experimental: slower than the graph path at N = 16k and not yet race-free; off.
 bool g_sytrd_fused = false;
+int g_sytrd_dbg = 0;
 
 void sytrd_lower(cudaStream_t st, int64_t n, double* A, int64_t lda, double* d, double* e,
                  double* tau) {
@@ -241,11 +242,13 @@ void sytrd_lower(cudaStream_t st, int64_t n, double* A, int64_t lda, double* d, 
   DBuf part_norm(gmax, st), part_wv(gmax, st), dpart((size_t)gmax * 2 * TRD_NB, st);
   DBuf wtmp(n, st), tvec(2 * TRD_NB, st), slots(2, st);  // slots: alpha, scale
   DBuf swork(symv_work_size(n), st);
+  SymvMap tmap;  // the whole matrix; each column's trailing block by coordinates
+  const bool tma_ok = !(g_sytrd_dbg & 1) && symv_map_make(&tmap, A, n, n, lda);
   double* alpha_buf = slots.p;
   double* scale_buf = slots.p + 1;
   // Each panel's ~260 dependent launches (4 per column) are captured once into a CUDA
   // graph and replayed (cudaGraphExecUpdate reuses the executable across panels).
-  const bool use_graph = true;
+  const bool use_graph = !(g_sytrd_dbg & 4);
   cudaGraphExec_t exec = nullptr;
   // capture on a private stream (the context stream may be the legacy default stream,
   // which cannot be captured); the graph itself is launched on st
@@ -285,8 +288,12 @@ void sytrd_lower(cudaStream_t st, int64_t n, double* A, int64_t lda, double* d, 
       lt.scale = scale_buf;
       lt.t = tvec.p;
       // wtmp[c+1:] = A22 v with dlarfg folded into the symv and the panel products t
-      symv_lower_latrd(sc, m, A + (c + 1) + (c + 1) * lda, lda, A + (c + 1) + c * lda,
-                       wtmp.p + (c + 1), swork.p, lf, lt);
+      if (tma_ok)
+        symv_tma(sc, tmap, c + 1, m, 1.0, A + (c + 1) + c * lda, 0.0, wtmp.p + (c + 1), swork.p,
+                 &lf, &lt, !(g_sytrd_dbg & 2));
+      else
+        symv_lower_latrd(sc, m, A + (c + 1) + (c + 1) * lda, lda, A + (c + 1) + c * lda,
+                         wtmp.p + (c + 1), swork.p, lf, lt);
       const int64_t gw = (m + CRW - 1) / CRW;
       launch_pdl(latrd_w_kernel, dim3((unsigned)gw), dim3(RT), 0, sc, n, A, lda, i0, c, i,
                  (const double*)W.p, (int64_t)n, wtmp.p, (const double*)tvec.p,
