@@ -134,23 +134,39 @@ EM_DEVINL void gemm_tile(const GemmArgs& p, int64_t m0, int64_t n0, double* smem
   }
   cp_async_wait<0>();
 
-  // epilogue
+  // epilogue: C = alpha acc + beta C. The C loads of two 8-row fragment groups are
+  // issued together before any of their stores (16 loads in flight per thread), so a
+  // beta != 0 update (trsm, syr2k, potrf, ormtr) is not a chain of dependent round trips.
+  double* __restrict__ Cr = p.C;
+  const bool has_beta = p.beta != 0.0;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int64_t row = m0 + wm * 64 + i * 8 + g;
-    if (row >= p.m) continue;
+  for (int i2 = 0; i2 < 8; i2 += 2) {
+    double cv[2][4][2];
+    bool ok[2][4][2];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int ii = 0; ii < 2; ++ii) {
+      const int64_t row = m0 + wm * 64 + (i2 + ii) * 8 + g;
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int64_t col = n0 + wn * 32 + j * 8 + 2 * t + e;
-        if (col >= p.n) continue;
-        if (LOWER && row + p.diag_off < col) continue;
-        double* cp = p.C + row + col * p.ldc;
-        double v = p.alpha * acc[i][j][e];
-        if (p.beta != 0.0) v = fma(p.beta, *cp, v);
-        *cp = v;
-      }
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t col = n0 + wn * 32 + j * 8 + 2 * t + e;
+          ok[ii][j][e] = row < p.m && col < p.n && !(LOWER && row + p.diag_off < col);
+          cv[ii][j][e] = (has_beta && ok[ii][j][e]) ? Cr[row + col * p.ldc] : 0.0;
+        }
+    }
+#pragma unroll
+    for (int ii = 0; ii < 2; ++ii) {
+      const int64_t row = m0 + wm * 64 + (i2 + ii) * 8 + g;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          if (!ok[ii][j][e]) continue;
+          const int64_t col = n0 + wn * 32 + j * 8 + 2 * t + e;
+          const double v = p.alpha * acc[i2 + ii][j][e];
+          Cr[row + col * p.ldc] = has_beta ? fma(p.beta, cv[ii][j][e], v) : v;
+        }
     }
   }
 }
