@@ -6,7 +6,7 @@
 // The reference does these through numpy/OpenBLAS (pkg/src/eddymodes/modal.py:79-81,
 // transient.py:140-154) or scalar numba loops (_kernels.py:56-79).
 //
-// Tile 128x128x16, 8 warps (2x4), warp tile 64x32 = 8x4 DMMA.8x8x4 fragments,
+// Tile 128x64x16, 8 warps (4x2), warp tile 32x32 = 4x4 DMMA.8x8x4 fragments, 2 CTAs/SM,
 // 3-stage cp.async pipeline, padded shared-memory layouts chosen so every
 // 8-byte fragment load is bank-conflict free (row strides = 4 mod 16 doubles).
 #include "common.cuh"
@@ -15,35 +15,47 @@
 
 namespace em {
 
-constexpr int GBM = 128, GBN = 128, GBK = 16, GSTAGES = 3, GTHREADS = 256;
-constexpr int SPAD_LONG = GBM + 4;  // 132 ≡ 4 (mod 16)
-constexpr int SPAD_K = GBK + 4;     // 20  ≡ 4 (mod 16)
+constexpr int GBM = 128, GBN = 64, GBK = 16, GTHREADS = 256, GMINB = 2;
+constexpr int WGM = GBM / 32;  // warp grid (each warp owns a 32 x 32 tile)
+constexpr int WTM = 4;         // warp tile: WTM x WTN DMMA 8x8 fragments
+constexpr int WTN = 4;
+static_assert(WGM * (GBN / 32) * 32 == GTHREADS, "warp grid must cover the CTA tile");
+constexpr int SPAD_M = GBM + 4;  // 132 ≡ 4 (mod 16)
+constexpr int SPAD_N = GBN + 4;  // 68  ≡ 4 (mod 16)
+constexpr int SPAD_K = GBK + 4;  // 20  ≡ 4 (mod 16)
 
 template <int TA>
 struct ATile {
-  static constexpr int size = TA ? GBM * SPAD_K : GBK * SPAD_LONG;
-  EM_DEVINL static int idx(int m, int k) { return TA ? m * SPAD_K + k : k * SPAD_LONG + m; }
+  static constexpr int size = TA ? GBM * SPAD_K : GBK * SPAD_M;
+  EM_DEVINL static int idx(int m, int k) { return TA ? m * SPAD_K + k : k * SPAD_M + m; }
 };
 template <int TB>
 struct BTile {
-  static constexpr int size = TB ? GBK * SPAD_LONG : GBN * SPAD_K;
-  EM_DEVINL static int idx(int k, int n) { return TB ? k * SPAD_LONG + n : n * SPAD_K + k; }
+  static constexpr int size = TB ? GBK * SPAD_N : GBN * SPAD_K;
+  EM_DEVINL static int idx(int k, int n) { return TB ? k * SPAD_N + n : n * SPAD_K + k; }
 };
 
-// Load a 128 x 16 slab of op(X) (the "long" extent is 128, the k extent 16).
+// Pipeline depth: 4 stages when two CTAs still fit in shared memory, else 3.
+template <int TA, int TB>
+constexpr int gstages() {
+  return (ATile<TA>::size + BTile<TB>::size) * 8 * 4 <= 113 * 1024 ? 4 : 3;
+}
+
+// Load a LONG x GBK slab of op(X) (the "long" extent is LONG, the k extent GBK).
 // TRANS == 0: X stored long-contiguous (X[l + k*ld]); TRANS == 1: k-contiguous (X[k + l*ld]).
-template <int TRANS, int VEC>
+template <int TRANS, int VEC, int LONG>
 EM_DEVINL void load_slab(double* s, const double* __restrict__ X, int64_t ld, int64_t l0,
                          int64_t k0, int64_t L, int64_t K, int tid) {
+  constexpr int SPL = LONG + 4;
   if (!TRANS) {
-    // contiguous along l; smem [k][l] stride SPAD_LONG
-    constexpr int CH = GBM * GBK / VEC;
+    // contiguous along l; smem [k][l] stride SPL
+    constexpr int CH = LONG * GBK / VEC;
 #pragma unroll
     for (int c = tid; c < CH; c += GTHREADS) {
-      int kk = c / (GBM / VEC);
-      int l = (c % (GBM / VEC)) * VEC;
+      int kk = c / (LONG / VEC);
+      int l = (c % (LONG / VEC)) * VEC;
       int64_t gl = l0 + l, gk = k0 + kk;
-      double* dst = s + kk * SPAD_LONG + l;
+      double* dst = s + kk * SPL + l;
       if (VEC == 2) {
         int nv = (gk < K) ? (int)imin64(imax64(L - gl, 0), 2) : 0;
         const double* src = nv ? X + gl + gk * ld : X;
@@ -55,7 +67,7 @@ EM_DEVINL void load_slab(double* s, const double* __restrict__ X, int64_t ld, in
     }
   } else {
     // contiguous along k; smem [l][k] stride SPAD_K
-    constexpr int CH = GBM * GBK / VEC;
+    constexpr int CH = LONG * GBK / VEC;
 #pragma unroll
     for (int c = tid; c < CH; c += GTHREADS) {
       int l = c / (GBK / VEC);
@@ -80,25 +92,26 @@ EM_DEVINL void gemm_tile(const GemmArgs& p, int64_t m0, int64_t n0, double* smem
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int wm = warp >> 2, wn = warp & 3;  // 2 x 4 warps, 64 x 32 each
+  const int wm = warp % WGM, wn = warp / WGM;  // warp grid WGM x (GBN/32), 32 x 32 each
 
   constexpr int ASZ = ATile<TA>::size, BSZ = BTile<TB>::size;
+  constexpr int GSTAGES = gstages<TA, TB>();
   double* As = smem;
   double* Bs = smem + GSTAGES * ASZ;
 
-  double acc[8][4][2];
+  double acc[WTM][WTN][2];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < WTM; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < WTN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   const int64_t nk = (p.k + GBK - 1) / GBK;
   // prologue
 #pragma unroll
   for (int s = 0; s < GSTAGES - 1; ++s) {
     if (s < nk) {
-      load_slab<TA, VEC>(As + s * ASZ, p.A, p.lda, m0, s * GBK, p.m, p.k, tid);
-      load_slab<!TB, VEC>(Bs + s * BSZ, p.B, p.ldb, n0, s * GBK, p.n, p.k, tid);
+      load_slab<TA, VEC, GBM>(As + s * ASZ, p.A, p.lda, m0, s * GBK, p.m, p.k, tid);
+      load_slab<!TB, VEC, GBN>(Bs + s * BSZ, p.B, p.ldb, n0, s * GBK, p.n, p.k, tid);
     }
     cp_async_commit();
   }
@@ -111,25 +124,34 @@ EM_DEVINL void gemm_tile(const GemmArgs& p, int64_t m0, int64_t n0, double* smem
       int64_t kn = kt + GSTAGES - 1;
       int sb = (int)(kn % GSTAGES);
       if (kn < nk) {
-        load_slab<TA, VEC>(As + sb * ASZ, p.A, p.lda, m0, kn * GBK, p.m, p.k, tid);
-        load_slab<!TB, VEC>(Bs + sb * BSZ, p.B, p.ldb, n0, kn * GBK, p.n, p.k, tid);
+        load_slab<TA, VEC, GBM>(As + sb * ASZ, p.A, p.lda, m0, kn * GBK, p.m, p.k, tid);
+        load_slab<!TB, VEC, GBN>(Bs + sb * BSZ, p.B, p.ldb, n0, kn * GBK, p.n, p.k, tid);
       }
       cp_async_commit();
     }
     const double* as = As + (kt % GSTAGES) * ASZ;
     const double* bs = Bs + (kt % GSTAGES) * BSZ;
+    // fragments double-buffered in registers: the loads for k-step ks+1 are issued
+    // before the 32 DMMAs of k-step ks
+    double af[2][WTM], bf[2][WTN];
+#pragma unroll
+    for (int i = 0; i < WTM; ++i) af[0][i] = as[ATile<TA>::idx(wm * 8 * WTM + i * 8 + g, t)];
+#pragma unroll
+    for (int j = 0; j < WTN; ++j) bf[0][j] = bs[BTile<TB>::idx(t, wn * 8 * WTN + j * 8 + g)];
 #pragma unroll
     for (int ks = 0; ks < GBK / 4; ++ks) {
-      double af[8], bf[4];
-      const int kk = ks * 4 + t;
+      const int cur = ks & 1, nx = cur ^ 1;
+      if (ks + 1 < GBK / 4) {
+        const int kk = (ks + 1) * 4 + t;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) af[i] = as[ATile<TA>::idx(wm * 64 + i * 8 + g, kk)];
+        for (int i = 0; i < WTM; ++i) af[nx][i] = as[ATile<TA>::idx(wm * 8 * WTM + i * 8 + g, kk)];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bf[j] = bs[BTile<TB>::idx(kk, wn * 32 + j * 8 + g)];
+        for (int j = 0; j < WTN; ++j) bf[nx][j] = bs[BTile<TB>::idx(kk, wn * 8 * WTN + j * 8 + g)];
+      }
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < WTM; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        for (int j = 0; j < WTN; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[cur][i], bf[cur][j]);
     }
   }
   cp_async_wait<0>();
@@ -140,30 +162,30 @@ EM_DEVINL void gemm_tile(const GemmArgs& p, int64_t m0, int64_t n0, double* smem
   double* __restrict__ Cr = p.C;
   const bool has_beta = p.beta != 0.0;
 #pragma unroll
-  for (int i2 = 0; i2 < 8; i2 += 2) {
-    double cv[2][4][2];
-    bool ok[2][4][2];
+  for (int i2 = 0; i2 < WTM; i2 += 2) {
+    double cv[2][WTN][2];
+    bool ok[2][WTN][2];
 #pragma unroll
     for (int ii = 0; ii < 2; ++ii) {
-      const int64_t row = m0 + wm * 64 + (i2 + ii) * 8 + g;
+      const int64_t row = m0 + wm * 8 * WTM + (i2 + ii) * 8 + g;
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < WTN; ++j)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int64_t col = n0 + wn * 32 + j * 8 + 2 * t + e;
+          const int64_t col = n0 + wn * 8 * WTN + j * 8 + 2 * t + e;
           ok[ii][j][e] = row < p.m && col < p.n && !(LOWER && row + p.diag_off < col);
           cv[ii][j][e] = (has_beta && ok[ii][j][e]) ? Cr[row + col * p.ldc] : 0.0;
         }
     }
 #pragma unroll
     for (int ii = 0; ii < 2; ++ii) {
-      const int64_t row = m0 + wm * 64 + (i2 + ii) * 8 + g;
+      const int64_t row = m0 + wm * 8 * WTM + (i2 + ii) * 8 + g;
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < WTN; ++j)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           if (!ok[ii][j][e]) continue;
-          const int64_t col = n0 + wn * 32 + j * 8 + 2 * t + e;
+          const int64_t col = n0 + wn * 8 * WTN + j * 8 + 2 * t + e;
           const double v = p.alpha * acc[i2 + ii][j][e];
           Cr[row + col * p.ldc] = has_beta ? fma(p.beta, cv[ii][j][e], v) : v;
         }
@@ -172,7 +194,7 @@ EM_DEVINL void gemm_tile(const GemmArgs& p, int64_t m0, int64_t n0, double* smem
 }
 
 template <int TA, int TB, int LOWER, int VEC>
-__global__ void __launch_bounds__(GTHREADS, 1) gemm_kernel(GemmArgs p, double* ws, int64_t kc) {
+__global__ void __launch_bounds__(GTHREADS, GMINB) gemm_kernel(GemmArgs p, double* ws, int64_t kc) {
   extern __shared__ __align__(16) double smem[];
   if (ws) {
     // split-K: slice z of the k range into its own m x n partial (alpha = 1, beta = 0)
@@ -205,7 +227,7 @@ __global__ void __launch_bounds__(GTHREADS, 1) gemm_kernel(GemmArgs p, double* w
 
 // Grouped launch: blockIdx.y selects a problem; problems carry their own sizes/pointers.
 template <int TA, int TB>
-__global__ void __launch_bounds__(GTHREADS, 1) gemm_grouped_kernel(const GemmArgs* __restrict__ ps,
+__global__ void __launch_bounds__(GTHREADS, GMINB) gemm_grouped_kernel(const GemmArgs* __restrict__ ps,
                                                                    int nprob) {
   extern __shared__ __align__(16) double smem[];
   GemmArgs p = ps[blockIdx.y];
@@ -223,9 +245,10 @@ __global__ void __launch_bounds__(GTHREADS, 1) gemm_grouped_kernel(const GemmArg
 }
 
 static size_t smem_bytes(int ta, int tb) {
-  size_t a = ta ? GBM * SPAD_K : GBK * SPAD_LONG;
-  size_t b = tb ? GBK * SPAD_LONG : GBN * SPAD_K;
-  return (a + b) * GSTAGES * sizeof(double);
+  size_t a = ta ? GBM * SPAD_K : GBK * SPAD_M;
+  size_t b = tb ? GBK * SPAD_N : GBN * SPAD_K;
+  const int stages = ta ? (tb ? gstages<1, 1>() : gstages<1, 0>()) : (tb ? gstages<0, 1>() : gstages<0, 0>());
+  return (a + b) * stages * sizeof(double);
 }
 
 // C = alpha * sum_z W_z + beta * C  (split-K reduction, fixed order)

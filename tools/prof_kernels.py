@@ -99,6 +99,24 @@ def main(which):
                                                           0.0, nat.ptr(y))), reps=20)
             out[f"symv_{m}"] = {"us": t * 1e6, "GBps": 8 * m * m / 2 / t / 1e9}
         del big
+    if which == "potrf":
+        m = int(os.environ.get("POTRF_N", n))
+        b = torch.randn(m, m, device="cuda", dtype=torch.float64, generator=g) / np.sqrt(m)
+        a = (b @ b.T + torch.eye(m, device="cuda", dtype=torch.float64)).contiguous()
+        del b
+        piv = ctypes.c_int64(-1)
+        for rep in range(2):
+            w2 = a.clone()
+            torch.cuda.synchronize()
+            t = timed(lambda: nat.check(lib.em_potrf(ctx, m, nat.ptr(w2), m, ctypes.byref(piv))),
+                      reps=1)
+            out[f"potrf_{m}_rep{rep}_ms"] = t * 1e3
+            out[f"potrf_{m}_TFps"] = m ** 3 / 3 / t / 1e12
+        bm = a.clone()
+        t = timed(lambda: nat.check(lib.em_trsm_lower(ctx, 0, m, m, nat.ptr(w2), m, nat.ptr(bm), m)),
+                  reps=1)
+        out[f"trsm_{m}_ms"] = t * 1e3
+        out[f"trsm_{m}_TFps"] = m ** 3 / t / 1e12
     if which == "syev":
         m = int(os.environ.get("SYEV_N", n))
         b = torch.randn(m, m, device="cuda", dtype=torch.float64, generator=g)
