@@ -44,16 +44,34 @@ EM_DEVINL void smem_trtri_lower(double* A, int n, int ld, double* tmp) {
 // Factor the diagonal block A[0:bs, 0:bs] (bs <= PNB; global offset k0 for the
 // pivot index), write the factor back (upper part zeroed) and its inverse to
 // Dinv (PNB x PNB, ld PNB).
+//
+// Blocked in shared memory with 32 x 32 blocks so that only the 32-wide diagonal
+// factorisations are sequential (one warp each, no block barriers):
+//   for each block column kb: warp 0 factors and inverts L_kk; the panel below is
+//   L_ik = A_ik L_kk^-T (a product with the inverse); the trailing lower part gets
+//   A -= P P^T.  Then the off-diagonal blocks of the inverse follow block-diagonal by
+//   block-diagonal: Linv_ij = -Linv_ii sum_{k=j}^{i-1} L_ik Linv_kj.
+// Storage: L in the lower triangle of S (with its diagonal), Linv's strictly lower
+// entries transposed into the upper triangle (Linv[r][c] at S[c + r*PLD]), Linv's
+// diagonal in dinv[]. A failing pivot (s <= 0 or NaN, the reference's test) aborts
+// with the global index of the first failing column.
+constexpr int PB = 32;  // inner block
+
+EM_DEVINL double linv_at(const double* S, const double* dinv, int r, int c) {
+  return r == c ? dinv[r] : (r > c ? S[c + r * PLD] : 0.0);
+}
+
 __global__ void __launch_bounds__(256) potf2_inv_kernel(double* A, int64_t lda, int64_t k0, int bs,
                                                         double* Dinv, int64_t* info) {
   extern __shared__ double sm[];
-  double* S = sm;               // PNB x PLD
-  double* tmp = S + PNB * PLD;  // PNB
+  double* S = sm;                // PNB x PLD
+  double* dinv = S + PNB * PLD;  // PNB
   __shared__ int fail;
   if (*info >= 0) return;  // an earlier block already failed
-  if (threadIdx.x == 0) fail = -1;
-  for (int i = threadIdx.x; i < PNB * PNB; i += blockDim.x) {
-    int r = i % PNB, c = i / PNB;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) fail = -1;
+  for (int i = tid; i < PNB * PNB; i += blockDim.x) {
+    const int r = i % PNB, c = i / PNB;
     double v;
     if (r < bs && c < bs)
       v = (r >= c) ? A[r + c * lda] : 0.0;
@@ -62,37 +80,210 @@ __global__ void __launch_bounds__(256) potf2_inv_kernel(double* A, int64_t lda, 
     S[r + c * PLD] = v;
   }
   __syncthreads();
-  for (int j = 0; j < bs; ++j) {
-    const double s = S[j + j * PLD];
-    if (!(s > 0.0)) {  // same test as the reference (NaN fails too)
-      if (threadIdx.x == 0) fail = j;
-      break;  // uniform: every thread read the same s
+  for (int kb = 0; kb < PNB / PB; ++kb) {
+    const int o = kb * PB;
+    if (warp == 0) {
+      // unblocked Cholesky of the 32 x 32 diagonal block; lane l owns row o + l and gets
+      // the column-j entries of the other rows by shuffle
+      int f = -1;
+      for (int j = 0; j < PB; ++j) {
+        const double sj = S[(o + j) + (o + j) * PLD];
+        if (!(sj > 0.0)) {
+          f = o + j;
+          break;
+        }
+        const double d = sqrt(sj);
+        const double lj = S[(o + lane) + (o + j) * PLD] * (1.0 / d);
+        __syncwarp();
+        if (lane == j) S[(o + j) + (o + j) * PLD] = d;
+        if (lane > j) S[(o + lane) + (o + j) * PLD] = lj;
+#pragma unroll
+        for (int k = 0; k < PB; ++k) {
+          const double lk = __shfl_sync(0xffffffffu, lj, k);
+          if (k > j && k <= lane)
+            S[(o + lane) + (o + k) * PLD] = fma(-lj, lk, S[(o + lane) + (o + k) * PLD]);
+        }
+        __syncwarp();
+      }
+      if (f >= 0) {
+        if (lane == 0) fail = f;
+      } else {
+        // inverse of the block, column c = lane kept in registers:
+        // X[r][c] = -(sum_{k=c}^{r-1} L_rk X[k][c]) / L_rr
+        const int c = lane;
+        const double dc = 1.0 / S[(o + c) + (o + c) * PLD];
+        dinv[o + c] = dc;
+        __syncwarp();
+        double x[PB];
+#pragma unroll
+        for (int r = 0; r < PB; ++r) x[r] = (r == c) ? dc : 0.0;
+#pragma unroll
+        for (int r = 1; r < PB; ++r) {
+          double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+          for (int k = 0; k < r; ++k) {
+            const double l = S[(o + r) + (o + k) * PLD];
+            if (k & 1)
+              a1 = fma(l, x[k], a1);
+            else
+              a0 = fma(l, x[k], a0);
+          }
+          if (r > c) x[r] = -(a0 + a1) * dinv[o + r];
+        }
+#pragma unroll
+        for (int r = 0; r < PB; ++r)
+          if (r > c) S[(o + c) + (o + r) * PLD] = x[r];
+      }
     }
-    const double d = sqrt(s);
     __syncthreads();
-    if (threadIdx.x == 0) S[j + j * PLD] = d;
-    for (int i = j + 1 + threadIdx.x; i < bs; i += blockDim.x) S[i + j * PLD] /= d;
-    __syncthreads();
-    const int m = bs - j - 1;
-    for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) {
-      const int i = j + 1 + idx % m, k = j + 1 + idx / m;
-      if (k <= i) S[i + k * PLD] = fma(-S[i + j * PLD], S[k + j * PLD], S[i + k * PLD]);
+    if (fail >= 0) break;
+    const int mp = PNB - o - PB;  // rows below the diagonal block
+    if (mp <= 0) break;
+    // panel: L[o+PB+i][o+c] = sum_{k<=c} A[o+PB+i][o+k] Linv_kk[c][k], 4 x 4 per thread
+    {
+      const int nbr = mp / 4, nbt = nbr * (PB / 4);
+      double acc[4][4];
+      const bool act = tid < nbt;
+      const int bi = tid % (nbr > 0 ? nbr : 1), bc = tid / (nbr > 0 ? nbr : 1);
+      const int r0 = o + PB + 4 * bi, c0 = 4 * bc;
+      if (act) {
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) acc[x][y] = 0.0;
+        for (int k = 0; k < c0 + 4; ++k) {
+          double a[4], b[4];
+#pragma unroll
+          for (int x = 0; x < 4; ++x) a[x] = S[(r0 + x) + (o + k) * PLD];
+#pragma unroll
+          for (int y = 0; y < 4; ++y) b[y] = linv_at(S, dinv, o + c0 + y, o + k);
+#pragma unroll
+          for (int x = 0; x < 4; ++x)
+#pragma unroll
+            for (int y = 0; y < 4; ++y) acc[x][y] = fma(a[x], b[y], acc[x][y]);
+        }
+      }
+      __syncthreads();
+      if (act) {
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) S[(r0 + x) + (o + c0 + y) * PLD] = acc[x][y];
+      }
+      __syncthreads();
     }
-    __syncthreads();
+    // trailing: A[r][q] -= sum_k P[r][k] P[q][k], r >= q >= o + PB, in 4 x 4 blocks
+    {
+      const int nb4 = mp / 4;
+      const int nblk = nb4 * (nb4 + 1) / 2;
+      for (int b = tid; b < nblk; b += 256) {
+        // block (bi, bj), bi >= bj, from the linear index
+        int bi = (int)((sqrtf(8.0f * b + 1.0f) - 1.0f) * 0.5f);
+        while (bi * (bi + 1) / 2 > b) --bi;
+        while ((bi + 1) * (bi + 2) / 2 <= b) ++bi;
+        const int bj = b - bi * (bi + 1) / 2;
+        const int r0 = o + PB + 4 * bi, q0 = o + PB + 4 * bj;
+        double acc[4][4];
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) acc[x][y] = 0.0;
+        for (int k = 0; k < PB; ++k) {
+          double pr[4], pq[4];
+#pragma unroll
+          for (int x = 0; x < 4; ++x) {
+            pr[x] = S[(r0 + x) + (o + k) * PLD];
+            pq[x] = S[(q0 + x) + (o + k) * PLD];
+          }
+#pragma unroll
+          for (int x = 0; x < 4; ++x)
+#pragma unroll
+            for (int y = 0; y < 4; ++y) acc[x][y] = fma(pr[x], pq[y], acc[x][y]);
+        }
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y)
+            if (r0 + x >= q0 + y) S[(r0 + x) + (q0 + y) * PLD] -= acc[x][y];
+      }
+      __syncthreads();
+    }
   }
   __syncthreads();
   if (fail >= 0) {
-    if (threadIdx.x == 0) *info = k0 + fail;
+    if (tid == 0) *info = k0 + fail;
     return;
   }
-  for (int i = threadIdx.x; i < bs * bs; i += blockDim.x) {
-    int r = i % bs, c = i / bs;
+  // off-diagonal blocks of the inverse, by block distance d = i - j; each thread owns a
+  // 4 x 4 piece of one block (rows a0.. of block i, columns b0.. of block j)
+  for (int d = 1; d < PNB / PB; ++d) {
+    const int nblk = PNB / PB - d;
+    const int per = (PB / 4) * (PB / 4);  // 64 pieces per block
+    const bool act = tid < nblk * per;
+    const int blk = tid / per, pc = tid % per;
+    const int j = blk, i = j + d;
+    const int r0 = i * PB + 4 * (pc % (PB / 4)), c0 = j * PB + 4 * (pc / (PB / 4));
+    double acc[4][4];
+    // W = sum_{k=j}^{i-1} L_ik Linv_kj  (Linv[kk][c] = 0 for kk < c)
+    if (act) {
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) acc[x][y] = 0.0;
+      for (int kk = c0; kk < i * PB; ++kk) {
+        double a[4], b[4];
+#pragma unroll
+        for (int x = 0; x < 4; ++x) a[x] = S[(r0 + x) + kk * PLD];
+#pragma unroll
+        for (int y = 0; y < 4; ++y) b[y] = linv_at(S, dinv, kk, c0 + y);
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) acc[x][y] = fma(a[x], b[y], acc[x][y]);
+      }
+    }
+    __syncthreads();
+    if (act) {  // W[r][c] into the (still empty) packed slot of Linv_ij
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) S[(c0 + y) + (r0 + x) * PLD] = acc[x][y];
+    }
+    __syncthreads();
+    // Linv_ij = -Linv_ii W
+    if (act) {
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) acc[x][y] = 0.0;
+      for (int kk = i * PB; kk < r0 + 4; ++kk) {
+        double a[4], b[4];
+#pragma unroll
+        for (int x = 0; x < 4; ++x) a[x] = linv_at(S, dinv, r0 + x, kk);
+#pragma unroll
+        for (int y = 0; y < 4; ++y) b[y] = S[(c0 + y) + kk * PLD];  // W[kk][c]
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) acc[x][y] = fma(a[x], b[y], acc[x][y]);
+      }
+    }
+    __syncthreads();
+    if (act) {
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) S[(c0 + y) + (r0 + x) * PLD] = -acc[x][y];
+    }
+    __syncthreads();
+  }
+  for (int i = tid; i < bs * bs; i += blockDim.x) {
+    const int r = i % bs, c = i / bs;
     A[r + c * lda] = (r >= c) ? S[r + c * PLD] : 0.0;
   }
-  smem_trtri_lower(S, PNB, PLD, tmp);
-  for (int i = threadIdx.x; i < PNB * PNB; i += blockDim.x) {
-    int r = i % PNB, c = i / PNB;
-    Dinv[r + c * PNB] = S[r + c * PLD];
+  for (int i = tid; i < PNB * PNB; i += blockDim.x) {
+    const int r = i % PNB, c = i / PNB;
+    Dinv[r + c * PNB] = linv_at(S, dinv, r, c);
   }
 }
 
