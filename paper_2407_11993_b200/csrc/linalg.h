@@ -18,6 +18,10 @@ void trsm_lower(cudaStream_t st, bool trans, int64_t n, int64_t m, const double*
                 double* B, int64_t ldb, const double* Dinv);
 constexpr int kTrsmBlock = 128;
 void trtri_blocks(cudaStream_t st, int nb, int64_t n, const double* C, int64_t ldc, double* Dinv);
+// A <- G^-1 A G^-T for symmetric A (full storage in; the lower triangle is valid on exit),
+// G lower with its 128-block diagonal inverses Dinv (from potrf). n^3 flops.
+void sygst_lower(cudaStream_t st, int64_t n, double* A, int64_t lda, const double* G, int64_t ldg,
+                 const double* Dinv);
 
 // sparse.cu: C = A B through a device CSR copy of the symmetric A when nnz <= max_fill n^2
 bool sym_sparse_mm(cudaStream_t st, int64_t n, const double* A, int64_t lda, int64_t m,

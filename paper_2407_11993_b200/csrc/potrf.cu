@@ -385,6 +385,49 @@ static void trsm_right_t_rec(cudaStream_t st, int64_t m, int64_t n, const double
   trsm_right_t_rec(st, m, n2, C22, ldc, B + n1 * ldb, ldb, Dinv, blk0 + n1 / PNB, T, ldt);
 }
 
+// ---- sygst: A <- G^-1 A G^-T (A symmetric, full storage in, lower triangle valid out)
+// Recursive two-sided reduction (the ReLAPACK/LAPACK itype-1 scheme, n^3 flops instead
+// of the 2 n^3 of two full triangular solves):
+//   A11 <- G11^-1 A11 G11^-T                      (recursion)
+//   A21 <- A21 G11^-T;  A21 -= 1/2 G21 A11
+//   A22 -= A21 G21^T + G21 A21^T                  (two lower GEMMs, then mirrored)
+//   A21 -= 1/2 G21 A11;  A21 <- G22^-1 A21
+//   A22 <- G22^-1 A22 G22^-T                      (recursion)
+// Leaves (n <= 128): A <- D A D^T with the diagonal-block inverse D of potrf.
+static void sygst_rec(cudaStream_t st, int64_t n, double* A, int64_t lda, const double* G,
+                      int64_t ldg, const double* Dinv, int64_t blk0, double* T, int64_t ldt) {
+  if (n <= 0) return;
+  if (n <= PNB) {
+    const double* D = Dinv + blk0 * PNB * PNB;
+    EM_CK(gemm(st, false, false, n, n, n, 1.0, D, PNB, A, lda, 0.0, T, ldt));
+    EM_CK(gemm(st, false, true, n, n, n, 1.0, T, ldt, D, PNB, 0.0, A, lda));
+    return;
+  }
+  const int64_t n1 = split_point(n), n2 = n - n1;
+  double* A21 = A + n1;
+  double* A22 = A + n1 + n1 * lda;
+  const double* G21 = G + n1;
+  const double* G22 = G + n1 + n1 * ldg;
+  sygst_rec(st, n1, A, lda, G, ldg, Dinv, blk0, T, ldt);
+  mirror_lower(st, n1, A, lda);  // A11 is used as a full symmetric matrix below
+  trsm_right_t_rec(st, n2, n1, G, ldg, A21, lda, Dinv, blk0, T, ldt);
+  EM_CK(gemm(st, false, false, n2, n1, n1, -0.5, G21, ldg, A, lda, 1.0, A21, lda));
+  EM_CK(gemm(st, false, true, n2, n2, n1, -1.0, A21, lda, G21, ldg, 1.0, A22, lda, true, 0));
+  EM_CK(gemm(st, false, true, n2, n2, n1, -1.0, G21, ldg, A21, lda, 1.0, A22, lda, true, 0));
+  mirror_lower(st, n2, A22, lda);
+  EM_CK(gemm(st, false, false, n2, n1, n1, -0.5, G21, ldg, A, lda, 1.0, A21, lda));
+  trsm_left_rec(st, false, n2, n1, G22, ldg, A21, lda, Dinv, blk0 + n1 / PNB, T);
+  sygst_rec(st, n2, A22, lda, G22, ldg, Dinv, blk0 + n1 / PNB, T, ldt);
+}
+
+void sygst_lower(cudaStream_t st, int64_t n, double* A, int64_t lda, const double* G, int64_t ldg,
+                 const double* Dinv) {
+  if (n <= 0) return;
+  // T: PNB x n for the left-trsm leaves, n x PNB for the right ones and the sygst leaves
+  DBuf T((size_t)n * PNB, st);
+  sygst_rec(st, n, A, lda, G, ldg, Dinv, 0, T.p, n);
+}
+
 // ---- potrf --------------------------------------------------------------------------
 static void potrf_rec(cudaStream_t st, int64_t n, double* A, int64_t lda, int64_t k0,
                       double* Dinv, int64_t* info, double* T, int64_t ldt, size_t smem) {

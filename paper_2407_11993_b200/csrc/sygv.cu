@@ -1,7 +1,8 @@
 // Generalized symmetric-definite eigensolve L v = tau R v — the device version of
 // modal.generalized_eig (pkg/src/eddymodes/modal.py:46-81):
 //   R = G G^T (potrf, "modal resistance matrix")
-//   B = G^-1 L G^-T as the reference forms it: G^-1 L, G^-1 (G^-1 L)^T, (B + B^T)/2
+//   B = G^-1 L G^-T (recursive two-sided reduction; the reference forms G^-1 L,
+//       G^-1 (G^-1 L)^T, (B + B^T)/2 — the same matrix to round-off)
 //   potrf(L) certificate ("modal inductance matrix"), same order as the reference
 //   B = U diag(w) U^T   (sytrd + divide & conquer + ormtr; replaces Jacobi)
 //   V = G^-T U, descending order, sign fix (largest |entry| positive),
@@ -130,12 +131,13 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
   {
     DBuf X(nn, st);
     {
+      // B = G^-1 L G^-T. The reference forms G^-1 (G^-1 L)^T with two full solves and
+      // averages it with its transpose (modal.py:63-67); the two-sided recursive
+      // reduction gives the same symmetric matrix to round-off with half the flops.
       Stage s(st, ST_SYGST);
       copy_matrix(st, false, n, n, L, ldl, B.p, n);
-      trsm_lower(st, false, n, n, G.p, n, B.p, n, GDinv.p);  // G^-1 L
-      copy_matrix(st, true, n, n, B.p, n, X.p, n);           // (G^-1 L)^T
-      trsm_lower(st, false, n, n, G.p, n, X.p, n, GDinv.p);  // G^-1 (G^-1 L)^T
-      add_transpose(st, n, 0.5, X.p, n, 0.5, B.p, n);        // (X + X^T)/2
+      mirror_lower(st, n, B.p, n);  // SymMatrix semantics: the lower triangle defines L
+      sygst_lower(st, n, B.p, n, G.p, n, GDinv.p);
     }
     // certificate only (modal.py:69-70)
     {
