@@ -266,6 +266,44 @@ def roofline(stages: dict, n: int, steps: int, n_theta: int, n_obs: int, peaks: 
                 frac=ach / fp64, traffic=None, per_launch_ms=per_launch_ms, launches=cnt)
 
 
+def symv_roofline(m, n, peaks, reps=20):
+    """Roofline of the dominant kernel: the lower-triangle symv over the trailing matrix
+    (one per tridiagonalisation column, the HBM-bound part of the sytrd stage), timed
+    live with CUDA events on the launching stream at the full size n: algorithmic bytes
+    8 n (n+1)/2 per launch (tile kernel + its partial-sum reduction)."""
+    import torch
+    from paper_2407_11993_b200 import _native as nat
+    lib, ctx = nat.load_library(), nat.context()
+    a = m["l_i"]
+    x = torch.randn(n, device="cuda", dtype=torch.float64)
+    y = torch.empty_like(x)
+    call = lambda: nat.check(lib.em_symv_lower(ctx, n, 1.0, nat.ptr(a), n, nat.ptr(x), 0.0,
+                                               nat.ptr(y)), "em_symv_lower")
+    for _ in range(3):
+        call()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps):
+        call()
+    e1.record()
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) / reps * 1e-3
+    byts = 8.0 * n * (n + 1) / 2
+    hbm = peaks.get("hbm_gbs", 6550.4)
+    ach = byts / t / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "r01_ncu_symv_tma.json")
+    if os.path.exists(prof) and n == 16384:
+        p = json.load(open(prof))
+        traffic = p["dram__bytes_read_GB"] * 1e9 + p["dram__bytes_write_MB"] * 1e6
+    return dict(kernel="symv_tma_kernel + symv_tma_reduce_kernel (em_symv_lower)", bound="hbm",
+                achieved=ach, peak=hbm, unit="GB/s", frac=ach / hbm, traffic=traffic,
+                algorithmic_bytes=byts, per_launch_ms=t * 1e3, launches_timed=reps,
+                peak_source="MEASURED_PEAKS.json hbm_gbs (copy, measured)",
+                traffic_source="profiles/r01_ncu_symv_tma.json (ncu --set full, one launch)")
+
+
 def load_peaks():
     peaks = {}
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -354,9 +392,12 @@ def run_ours(args, cfg, rank, world, local_rank):
     top = {k: stages[k] for k in ("potrf_R", "sygst", "potrf_L", "sytrd", "stedc", "ormtr",
                                   "trsm_back", "finalize", "post_gemm", "td2_local",
                                   "td2_carry", "td2_replay") if k in stages}
-    rl = roofline(top, n, T, nth, cfg["n_obs"], peaks) if top else None
-    if rl and rl["stage"] == "td2_replay":
-        rl["achieved"] = None
+    stage_rl = roofline(top, n, T, nth, cfg["n_obs"], peaks) if top else None
+    if stage_rl and stage_rl["stage"] == "td2_replay":
+        stage_rl["achieved"] = None
+    rl = symv_roofline(m, n, peaks)
+    rl["stage"] = "sytrd"
+    rl["stage_roofline"] = stage_rl
 
     # ---- TD1 comparator (bounded: a few hundred steps, extrapolated) and CPU baseline
     extra = {}
