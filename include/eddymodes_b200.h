@@ -119,6 +119,14 @@ int em_td2_plan_create(em_ctx* ctx, int64_t n, int n_p, int n_s, const double* l
                        double dt, double theta, em_td2_plan** plan);
 void em_td2_plan_destroy(em_td2_plan* plan);
 
+/* Exact per-interval integrator for piecewise-linear drives on a uniform grid of step h
+ * (exact_modal_reference / exact_first_order, transient.py:457-502): the same plan type
+ * and em_td2_run as the theta-method, with q^{k+1} = a q^k + c1 e0 + c2 s per mode
+ * (a = exp(-h r/l)). em_td2_step / _forcing / _step_forcing reject such a plan. */
+int em_td2_plan_create_exact(em_ctx* ctx, int64_t n, int n_p, int n_s, const double* l_n,
+                             const double* r_n, const double* P_r, const double* P_l,
+                             const double* P_m, double h, em_td2_plan** plan);
+
 /* Observables y^k = CV q^k (+ D i_d^k): CV n_obs x n (column-major, = C V),
  * D n_obs x n_p or NULL. */
 int em_td2_set_observables(em_td2_plan* plan, int n_obs, const double* CV, int64_t ldcv,

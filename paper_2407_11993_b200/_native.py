@@ -47,6 +47,8 @@ SIGNATURES = {
     "em_sygv_h": (_I, [_P, _I64, _P, _P, _P, _P, _P, _P, _P, ctypes.POINTER(_I64),
                        ctypes.POINTER(_I)]),
     "em_td2_plan_create": (_I, [_P, _I64, _I, _I, _P, _P, _P, _P, _P, _D, _D, ctypes.POINTER(_P)]),
+    "em_td2_plan_create_exact": (_I, [_P, _I64, _I, _I, _P, _P, _P, _P, _P, _D,
+                                      ctypes.POINTER(_P)]),
     "em_td2_plan_destroy": (None, [_P]),
     "em_td2_set_observables": (_I, [_P, _I, _P, _I64, _P, _I64]),
     "em_td2_run": (_I, [_P, _I64, _P, _P, _P, _I64, _P]),

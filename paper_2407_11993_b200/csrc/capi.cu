@@ -267,6 +267,25 @@ int em_td2_plan_create(em_ctx* ctx, int64_t n, int n_p, int n_s, const double* l
   });
 }
 
+int em_td2_plan_create_exact(em_ctx* ctx, int64_t n, int n_p, int n_s, const double* l_n,
+                             const double* r_n, const double* P_r, const double* P_l,
+                             const double* P_m, double h, em_td2_plan** plan) {
+  return guarded(ctx, [&] {
+    if (!plan || n < 0 || n_p < 0 || n_s < 0 || !(h > 0.0))
+      throw em::ArgError{"bad exact-integrator plan arguments"};
+    auto* P = em::td2_new(ctx, n, n_p, n_s, h, 1.0);
+    try {
+      em::td2_plan_init_exact(P, l_n, r_n, P_r, P_l, P_m);
+      EM_CK(cudaStreamSynchronize(ctx->stream));
+    } catch (...) {
+      em::td2_delete(P);
+      throw;
+    }
+    *plan = P;
+    return EM_OK;
+  });
+}
+
 void em_td2_plan_destroy(em_td2_plan* plan) { em::td2_delete(plan); }
 
 int em_td2_set_observables(em_td2_plan* plan, int n_obs, const double* CV, int64_t ldcv,
@@ -291,6 +310,7 @@ int em_td2_step(em_td2_plan* plan, double* q, const double* i_d_h, const double*
                 const double* di0_h) {
   em_ctx* ctx = em::td2_ctx(plan);
   return guarded(ctx, [&] {
+    if (em::td2_is_exact(plan)) throw em::ArgError{"per-step calls need a theta-method plan"};
     em::td2_step_host(plan, q, i_d_h, di_d_h, di0_h);
     return EM_OK;
   });
@@ -300,6 +320,7 @@ int em_td2_forcing(em_td2_plan* plan, const double* i_d_h, const double* di_d_h,
                    const double* di0_h, double* f) {
   em_ctx* ctx = em::td2_ctx(plan);
   return guarded(ctx, [&] {
+    if (em::td2_is_exact(plan)) throw em::ArgError{"per-step calls need a theta-method plan"};
     em::td2_forcing_host(plan, i_d_h, di_d_h, di0_h, f);
     return EM_OK;
   });
@@ -308,6 +329,7 @@ int em_td2_forcing(em_td2_plan* plan, const double* i_d_h, const double* di_d_h,
 int em_td2_step_forcing(em_td2_plan* plan, double* q, const double* f) {
   em_ctx* ctx = em::td2_ctx(plan);
   return guarded(ctx, [&] {
+    if (em::td2_is_exact(plan)) throw em::ArgError{"per-step calls need a theta-method plan"};
     em::td2_step_forcing(plan, q, f);
     EM_CK(cudaStreamSynchronize(ctx->stream));
     return EM_OK;

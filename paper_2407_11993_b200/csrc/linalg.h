@@ -103,6 +103,9 @@ void syev_ascending(cudaStream_t st, int64_t n, double* A, int64_t lda, double* 
 // td1.cu / td2.cu
 void td2_plan_init(em_td2_plan* P, const double* l_n, const double* r_n, const double* P_r,
                    const double* P_l, const double* P_m);
+void td2_plan_init_exact(em_td2_plan* P, const double* l_n, const double* r_n, const double* P_r,
+                         const double* P_l, const double* P_m);
+bool td2_is_exact(const em_td2_plan* P);
 void td2_set_observables(em_td2_plan* P, int n_obs, const double* CV, int64_t ldcv,
                          const double* D, int64_t ldd);
 void td2_run(em_td2_plan* P, int64_t T, const double* drive, double* q, double* Y,

@@ -34,6 +34,7 @@ struct em_td2_plan {
   em::DBuf rn, cn, Pr, Pltr, Pm;  // reference single-step form
   int n_obs = 0, n_obs_pad = 0;
   em::DBuf CV, D;
+  bool exact = false;  // exponential-integrator recurrence (no single-step form)
 };
 
 namespace em {
@@ -70,6 +71,32 @@ __global__ void td2_coeffs_kernel(int64_t n, int n_p, int n_s, double dt, double
     Pm[i + s * n] = pm;
     W[i + (int64_t)(2 * n_p + s) * n] = -pm * b;
   }
+}
+
+// Exact per-interval integrator for piecewise-linear drives (exact_modal_reference /
+// exact_first_order, E/transient.py:457-502) as the same recurrence
+// q^{k+1} = (1 - eps) q^k + W u^k:  with tau = l/r, a = exp(-h/tau),
+//   eps = -expm1(-h/tau),  q^{k+1} = a q^k + c1 e0 + c2 s,
+//   c1 = (1 - a)/r,  c2 = (h - (1 - a) tau)/r,
+//   e0 = -P_r i_d^k - P_l di_d/h - P_m di0/h,  s = -P_r di_d/h  (u = [i_d^k, di_d, di0]).
+__global__ void td2_exact_coeffs_kernel(int64_t n, int n_p, int n_s, double h,
+                                        const double* __restrict__ l_n,
+                                        const double* __restrict__ r_n,
+                                        const double* __restrict__ P_r,
+                                        const double* __restrict__ P_l,
+                                        const double* __restrict__ P_m, double* eps, double* W) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double r = r_n[i], tau = l_n[i] / r;
+  const double oma = -expm1(-h / tau);  // 1 - a
+  eps[i] = oma;
+  const double c1 = oma / r, c2 = (h - oma * tau) / r;
+  for (int p = 0; p < n_p; ++p) {
+    const double pr = P_r[i + p * n], pl = P_l[i + p * n];
+    W[i + (int64_t)p * n] = -c1 * pr;
+    W[i + (int64_t)(n_p + p) * n] = -(c1 * pl + c2 * pr) / h;
+  }
+  for (int s = 0; s < n_s; ++s) W[i + (int64_t)(2 * n_p + s) * n] = -c1 * P_m[i + s * n] / h;
 }
 
 // u^k rows from the drive table (row k = [i_d(t_k) | i0(t_k)]).
@@ -438,6 +465,20 @@ void td2_plan_init(em_td2_plan* P, const double* l_n, const double* r_n, const d
       P->rn.p, P->cn.p, P->Pr.p, P->Pltr.p, P->Pm.p);
   EM_LAUNCHED();
 }
+
+void td2_plan_init_exact(em_td2_plan* P, const double* l_n, const double* r_n, const double* P_r,
+                         const double* P_l, const double* P_m) {
+  cudaStream_t st = P->ctx->stream;
+  const int64_t n = P->n;
+  P->exact = true;
+  P->eps.alloc(n, st);
+  P->W.alloc((size_t)n * imax64(P->n_u, 1), st);
+  td2_exact_coeffs_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+      n, P->n_p, P->n_s, P->dt, l_n, r_n, P_r, P_l, P_m, P->eps.p, P->W.p);
+  EM_LAUNCHED();
+}
+
+bool td2_is_exact(const em_td2_plan* P) { return P->exact; }
 
 void td2_set_observables(em_td2_plan* P, int n_obs, const double* CV, int64_t ldcv,
                          const double* D, int64_t ldd) {

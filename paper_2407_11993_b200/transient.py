@@ -117,6 +117,23 @@ def _obs_device(observables, n: int, n_p: int):
     return c.shape[0], nat.device_colmajor(c), dd
 
 
+def _drive_projection(rm: ReducedModel, basis: ModalBasis):
+    """V^T [R_D | L_D | M0] on the device (transient.py:276-286), column-major n x n_d
+    (torch (n_d, n)); a (1, n) zero block when there are no drive channels."""
+    n, n_p, n_s = basis.n_modes, rm.n_ports, rm.n_sources
+    nd = 2 * n_p + n_s
+    if not nd:
+        return nat.zeros(1, n)
+    ctx, lib = nat.context(), nat.load_library()
+    drv = np.concatenate([rm.r_d.reshape(n, n_p), rm.l_d.reshape(n, n_p),
+                          rm.m0.reshape(n, n_s)], axis=1)
+    ddrv = nat.device_colmajor(drv)
+    proj = nat.empty(nd, n)
+    nat.check(lib.em_dgemm(ctx, 1, 0, n, nd, n, 1.0, nat.ptr(basis.v_dev), n,
+                           nat.ptr(ddrv), n, 0.0, nat.ptr(proj), n), "em_dgemm")
+    return proj
+
+
 class Td2Stepper:
     """Decoupled stepper (transient.py:258-308): per-mode scalar updates after
     projecting the drive onto the modes."""
@@ -138,16 +155,7 @@ class Td2Stepper:
         self._rn = basis.r_n.copy()
         ctx = nat.context()
         lib = nat.load_library()
-        nd = 2 * n_p + n_s
-        if nd:
-            drv = np.concatenate([rm.r_d.reshape(n, n_p), rm.l_d.reshape(n, n_p),
-                                  rm.m0.reshape(n, n_s)], axis=1)
-            ddrv = nat.device_colmajor(drv)
-            proj = nat.empty(nd, n)      # V^T [R_D | L_D | M0], column-major n x nd
-            nat.check(lib.em_dgemm(ctx, 1, 0, n, nd, n, 1.0, nat.ptr(basis.v_dev), n,
-                                   nat.ptr(ddrv), n, 0.0, nat.ptr(proj), n), "em_dgemm")
-        else:
-            proj = nat.zeros(1, n)
+        proj = _drive_projection(rm, basis)
         self._proj = proj
         p_r = proj[0:n_p] if n_p else proj[0:1]
         p_l = proj[n_p:2 * n_p] if n_p else proj[0:1]
@@ -462,8 +470,8 @@ def run_transient(rm: ReducedModel, net, drives, cfg: TransientConfig,
 
 def exact_first_order(l_n: np.ndarray, r_n: np.ndarray, y0: np.ndarray,
                       e0: np.ndarray, slope: np.ndarray, h: float) -> np.ndarray:
-    """Closed-form step of l y' + r y = e0 + slope t (transient.py:494-502).
-    Validation reference (host arithmetic, as in the reference)."""
+    """Closed-form step of l y' + r y = e0 + slope t (transient.py:494-502), per
+    component (a small host formula, as in the reference)."""
     tau = l_n / r_n
     yp0 = (e0 - slope * tau) / r_n
     yph = (e0 + slope * h - slope * tau) / r_n
@@ -472,28 +480,52 @@ def exact_first_order(l_n: np.ndarray, r_n: np.ndarray, y0: np.ndarray,
 
 def exact_modal_reference(basis: ModalBasis, rm: ReducedModel, i_d_samples, i0_samples,
                           times, modal_state0=None) -> np.ndarray:
-    """Exact per-interval integration for piecewise-linear drives (transient.py:457-491);
-    a validation reference for the theta-convergence checks."""
+    """Exact per-interval integration of every mode for piecewise-linear drives
+    (transient.py:457-491), on the device: per mode q^{k+1} = a q^k + c1 e0 + c2 s with
+    a = exp(-h r/l) is the same linear recurrence as the theta-method, so it runs as one
+    blocked scan (em_td2_plan_create_exact + em_td2_run). The scan needs one factor a
+    per mode, i.e. uniformly spaced sample times (ValidationError otherwise).
+    Returns modal coordinates at every sample time, shape (len(times), n_modes)."""
     times = np.asarray(times, dtype=float)
     n_t = times.shape[0]
-    n = basis.n_modes
-    i_d_samples = np.asarray(i_d_samples, dtype=float).reshape(n_t, rm.n_ports)
-    i0_samples = np.asarray(i0_samples, dtype=float).reshape(n_t, rm.n_sources)
-    vt = basis.v.T
-    p_r = vt @ rm.r_d if rm.n_ports else np.zeros((n, 0))
-    p_l = vt @ rm.l_d if rm.n_ports else np.zeros((n, 0))
-    p_m = vt @ rm.m0 if rm.n_sources else np.zeros((n, 0))
+    n, n_p, n_s = basis.n_modes, rm.n_ports, rm.n_sources
+    i_d_samples = np.asarray(i_d_samples, dtype=float).reshape(n_t, n_p)
+    i0_samples = np.asarray(i0_samples, dtype=float).reshape(n_t, n_s)
+    q0 = np.zeros(n) if modal_state0 is None else np.asarray(modal_state0, float).copy()
+    if q0.shape != (n,):
+        raise DimensionMismatch(f"modal state must have {n} components")
     out = np.zeros((n_t, n))
-    state = np.zeros(n) if modal_state0 is None else np.asarray(modal_state0, float).copy()
-    out[0] = state
-    for k in range(n_t - 1):
-        h = times[k + 1] - times[k]
-        di_d = (i_d_samples[k + 1] - i_d_samples[k]) / h
-        di_0 = (i0_samples[k + 1] - i0_samples[k]) / h
-        e0 = -(p_r @ i_d_samples[k]) - (p_l @ di_d) - (p_m @ di_0)
-        s = -(p_r @ di_d)
-        state = exact_first_order(basis.l_n, basis.r_n, state, e0, s, h)
-        out[k + 1] = state
+    if n_t == 0:
+        return out
+    out[0] = q0
+    if n_t == 1 or n == 0:
+        return out
+    steps = n_t - 1
+    h = (times[-1] - times[0]) / steps
+    if not h > 0 or np.max(np.abs(np.diff(times) - h)) > 1e-9 * h:
+        raise ValidationError("exact_modal_reference on the device needs uniformly spaced, "
+                              "increasing sample times")
+    ctx, lib = nat.context(), nat.load_library()
+    proj = _drive_projection(rm, basis)
+    p_r = proj[0:n_p] if n_p else proj[0:1]
+    p_l = proj[n_p:2 * n_p] if n_p else proj[0:1]
+    p_m = proj[2 * n_p:] if n_s else proj[0:1]
+    ln, rn = nat.device_vector(basis.l_n), nat.device_vector(basis.r_n)
+    plan = ctypes.c_void_p()
+    nat.check(lib.em_td2_plan_create_exact(ctx, n, n_p, n_s, nat.ptr(ln), nat.ptr(rn),
+                                           nat.ptr(p_r), nat.ptr(p_l), nat.ptr(p_m), h,
+                                           ctypes.byref(plan)), "em_td2_plan_create_exact")
+    try:
+        table = _drive_table(i_d_samples, i0_samples, n_p, n_s) if (n_p or n_s) \
+            else np.zeros((n_t, 0))
+        drive = nat.device_vector(table.reshape(-1)) if table.size else nat.zeros(1)
+        q = nat.device_vector(q0)
+        qcap = nat.empty(steps, n)
+        nat.check(lib.em_td2_run(plan, steps, nat.ptr(drive), nat.ptr(q), None, 1,
+                                 nat.ptr(qcap)), "em_td2_run")
+        out[1:] = qcap.cpu().numpy()
+    finally:
+        lib.em_td2_plan_destroy(plan)
     return out
 
 

@@ -7,6 +7,7 @@ import os
 import numpy as np
 import pytest
 
+from oracle import oracle
 from tests.conftest import GOLDEN, golden, rel_l2
 
 pytestmark = pytest.mark.gpu
@@ -156,8 +157,9 @@ def test_theta_convergence_orders():
 
     n_ref = 4000
     i_d, i0 = transient.drive_samples(None, rm, _plate_drives(), t_end / n_ref, n_ref)
-    exact = transient.exact_modal_reference(basis, rm, i_d, i0,
-                                            t_end / n_ref * np.arange(n_ref + 1))[-1]
+    # the independent host restatement of exact_modal_reference (oracle/oracle.py)
+    exact = oracle.exact_modal_reference(basis, rm.r_d, rm.l_d, rm.m0, i_d, i0,
+                                         t_end / n_ref * np.arange(n_ref + 1))[-1]
     for theta, order in ((1.0, 2.0), (0.5, 4.0)):
         errs = [np.linalg.norm(final_state(theta, t_end / k) - exact) for k in (50, 100, 200)]
         r1, r2 = errs[0] / errs[1], errs[1] / errs[2]
@@ -204,3 +206,32 @@ def test_mode_sharded_stepping_on_device():
         part = sh.run(table, steps).cpu().numpy()
         y = part if y is None else y + part
     assert rel_l2(y, g["td2_obs_theta0.5"]) < TOL
+
+
+def test_exact_modal_integrator_on_device_matches_oracle():
+    """exact_modal_reference (transient.py:457-502) on the device (the
+    exponential integrator as the blocked scan) against the host restatement, over a
+    ramp + tone drive, moderate dt/tau; with an initial state; non-uniform times rejected."""
+    from paper_2407_11993_b200 import modal, reduction, transient
+    from paper_2407_11993_b200.errors import ValidationError
+    g = golden("plate_small")
+    rm = reduction.from_blocks(g["r_i"] * 2e3, g["l_i"], g["r_d"] * 2e3, g["l_d"], g["m0"],
+                               port_names=("p0",), source_names=("s0",))
+    basis = modal.generalized_eig(rm.l_i, rm.r_i)
+    n_t, dt = 1501, 2e-7
+    times = dt * np.arange(n_t)
+    i_d = np.minimum(times / 5e-5, 1.0)[:, None]
+    i0 = np.sin(2 * np.pi * 2e4 * times)[:, None]
+    got = transient.exact_modal_reference(basis, rm, i_d, i0, times)
+    ref = oracle.exact_modal_reference(basis, rm.r_d, rm.l_d, rm.m0, i_d, i0, times)
+    assert got.shape == ref.shape == (n_t, basis.n_modes)
+    assert rel_l2(got, ref) < 1e-9
+    q0 = np.linspace(-1.0, 1.0, basis.n_modes) * 1e-3
+    got0 = transient.exact_modal_reference(basis, rm, i_d, i0, times, modal_state0=q0)
+    # linearity: the initial state decays independently of the drive
+    decay = transient.exact_modal_reference(basis, rm, 0 * i_d, 0 * i0, times, modal_state0=q0)
+    assert rel_l2(got0, got + decay) < 1e-12
+    tau = basis.l_n / basis.r_n
+    assert np.allclose(decay[-1], q0 * np.exp(-times[-1] / tau), rtol=1e-10, atol=1e-300)
+    with pytest.raises(ValidationError):
+        transient.exact_modal_reference(basis, rm, i_d[:3], i0[:3], np.array([0.0, 1e-7, 3e-7]))
