@@ -39,6 +39,7 @@ extern "C" {
 typedef struct em_ctx em_ctx;
 typedef struct em_td2_plan em_td2_plan;
 typedef struct em_td1_plan em_td1_plan;
+typedef struct em_fd_plan em_fd_plan;
 
 /* --- context --------------------------------------------------------------- */
 int em_init(int device, em_ctx** ctx);
@@ -173,6 +174,26 @@ int em_td1_step(em_td1_plan* plan, double* I, const double* i_d_h, const double*
 /* Copy the lower Cholesky factor of the stepping matrix (n x n, column-major) to out
  * (device). Td1Stepper.chol (transient.py:237). */
 int em_td1_factor(em_td1_plan* plan, double* out, int64_t ldo);
+
+/* --- frequency domain (frequency.py) --------------------------------- */
+
+/* Per-tone solve (R + j w L) I = E (frequency.solve_tone, frequency.py:56-94; the
+ * reference LU-factors the real 2n embedding [[R, wL], [wL, -R]]). The plan factors R
+ * (lower triangles of L, R used) and forms K = L R^-1 L once; each solve is one
+ * Cholesky of the SPD Schur complement R + w^2 K. *pivot reports a non-SPD R (plan)
+ * or a numerically singular tone (solve) with EM_ERR_NOT_PD. */
+int em_fd_plan_create(em_ctx* ctx, int64_t n, const double* L, int64_t ldl, const double* R,
+                      int64_t ldr, em_fd_plan** plan, int64_t* pivot);
+void em_fd_plan_destroy(em_fd_plan* plan);
+/* E = c + j d (HOST vectors, n); I = a - j b (HOST outputs), i.e. (a, b) solves the
+ * embedding [[R, wL], [wL, -R]] [a; b] = [c; d] exactly as the reference's x. */
+int em_fd_solve(em_fd_plan* plan, double omega, const double* c_h, const double* d_h, double* a_h,
+                double* b_h, int64_t* pivot);
+/* Tone table for DFT phasors (dft_phasor / extract_phasors, frequency.py:114-166):
+ * out[m + 2f*ldo] = sin(2 pi f_f t_m), out[m + (2f+1)*ldo] = cos(2 pi f_f t_m),
+ * t_m = t0 + m dt (device out, n_t x 2 n_f column-major; freqs_h host). */
+int em_tone_table(em_ctx* ctx, int64_t n_t, double dt, double t0, int n_f, const double* freqs_h,
+                  double* out, int64_t ldo);
 
 /* --- synthetic plate inputs (BASELINE.json configs; definition in synth.py) ----------- */
 /* Dense L (n x n), dense-stored R = rho*K7 + shift*I, and the one-port electrode

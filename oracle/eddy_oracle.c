@@ -180,3 +180,53 @@ void orc_td2_step(double* state, const double* r_n, const double* c_n, double dt
     state[i] += (num / c_n[i]) / c_n[i];
   }
 }
+
+/* _kernels.py:144-170  lu_factor_kernel: in-place LU with partial pivoting (row swaps
+ * recorded in piv); -1 on success, else the column with an exactly zero pivot. */
+int64_t orc_lu_factor(double* a, int64_t* piv, int64_t n) {
+  for (int64_t k = 0; k < n; ++k) {
+    double pmax = fabs(A_(k, k));
+    int64_t prow = k;
+    for (int64_t i = k + 1; i < n; ++i) {
+      const double v = fabs(A_(i, k));
+      if (v > pmax) {
+        pmax = v;
+        prow = i;
+      }
+    }
+    if (pmax == 0.0) return k;
+    piv[k] = prow;
+    if (prow != k)
+      for (int64_t j = 0; j < n; ++j) {
+        const double tmp = A_(k, j);
+        A_(k, j) = A_(prow, j);
+        A_(prow, j) = tmp;
+      }
+    const double akk = A_(k, k);
+    for (int64_t i = k + 1; i < n; ++i) {
+      const double lik = A_(i, k) / akk;
+      A_(i, k) = lik;
+      for (int64_t j = k + 1; j < n; ++j) A_(i, j) -= lik * A_(k, j);
+    }
+  }
+  return -1;
+}
+
+/* _kernels.py:173-193  lu_solve_kernel: all row swaps first, then the two sweeps. */
+void orc_lu_solve(const double* a, const int64_t* piv, double* b, int64_t n) {
+  for (int64_t k = 0; k < n; ++k) {
+    const int64_t p = piv[k];
+    if (p != k) {
+      const double tmp = b[k];
+      b[k] = b[p];
+      b[p] = tmp;
+    }
+  }
+  for (int64_t k = 0; k < n; ++k)
+    for (int64_t i = k + 1; i < n; ++i) b[i] -= A_(i, k) * b[k];
+  for (int64_t i = n - 1; i >= 0; --i) {
+    double s = b[i];
+    for (int64_t k = i + 1; k < n; ++k) s -= A_(i, k) * b[k];
+    b[i] = s / A_(i, i);
+  }
+}

@@ -72,6 +72,9 @@ def lib():
         _lib.orc_jacobi_rotations.restype = i64
         _lib.orc_td1_step.argtypes = [d, d, d, ctypes.c_double, d, d, d, d, i64]
         _lib.orc_td2_step.argtypes = [d, d, d, ctypes.c_double, d, i64]
+        _lib.orc_lu_factor.argtypes = [d, ctypes.c_void_p, i64]
+        _lib.orc_lu_factor.restype = i64
+        _lib.orc_lu_solve.argtypes = [d, ctypes.c_void_p, d, i64]
     return _lib
 
 
@@ -321,3 +324,51 @@ def exact_modal_reference(basis: Basis, r_d, l_d, m0, i_d_samples, i0_samples, t
         state = exact_first_order(basis.l_n, basis.r_n, state, e0, s, h)
         out[k + 1] = state
     return out
+
+
+# --- frequency domain (E/frequency.py) -------------------------------------------------
+
+def lu_factor(a: np.ndarray):
+    """linalg.py:137-147 + _kernels.py:144-170 (pivoted LU); SingularSystem on a zero pivot."""
+    a = np.ascontiguousarray(a, dtype=float).copy()
+    piv = np.zeros(a.shape[0], dtype=np.int64)
+    col = lib().orc_lu_factor(_p(a), piv.ctypes.data_as(ctypes.c_void_p), a.shape[0])
+    if col >= 0:
+        raise RuntimeError(f"zero pivot in column {col}")
+    return a, piv
+
+
+def lu_solve(lu_piv, b: np.ndarray) -> np.ndarray:
+    """linalg.py:150-156 + _kernels.py:173-193."""
+    lu, piv = lu_piv
+    x = np.ascontiguousarray(b, dtype=float).copy()
+    lib().orc_lu_solve(_p(lu), piv.ctypes.data_as(ctypes.c_void_p), _p(x), lu.shape[0])
+    return x
+
+
+def solve_tone(r_i, l_i, r_d, l_d, m0, omega, i_d_phasor, i0_phasor) -> np.ndarray:
+    """frequency.py:56-94: (R + j w L) I = -(R_D + j w L_D) i_D - j w M0 i0 through the
+    real 2n embedding [[R, wL], [wL, -R]] and the pivoted LU."""
+    r, l = sym_mirror(r_i), sym_mirror(l_i)
+    n = r.shape[0]
+    e = np.zeros(n, dtype=complex)
+    if r_d.shape[1]:
+        e -= (r_d + 1j * omega * l_d) @ np.asarray(i_d_phasor, dtype=complex)
+    if m0.shape[1]:
+        e -= 1j * omega * (m0 @ np.asarray(i0_phasor, dtype=complex))
+    big = np.zeros((2 * n, 2 * n))
+    big[:n, :n] = r
+    big[:n, n:] = omega * l
+    big[n:, :n] = omega * l
+    big[n:, n:] = -r
+    x = lu_solve(lu_factor(big), np.concatenate([e.real, e.imag]))
+    return x[:n] - 1j * x[n:]
+
+
+def dft_phasor(samples, dt, f, t0=0.0) -> complex:
+    """frequency.py:114-138 (Im convention: sin(w t) -> 1 + 0j)."""
+    samples = np.asarray(samples, dtype=float)
+    n = samples.shape[0]
+    t = t0 + dt * np.arange(n)
+    w = 2 * np.pi * f
+    return 1j * ((2.0 / n) * np.sum(samples * np.exp(-1j * w * t)))

@@ -62,6 +62,11 @@ SIGNATURES = {
     "em_td1_run": (_I, [_P, _I64, _P, _P, _P, _I64, _P]),
     "em_td1_step": (_I, [_P, _P, _P, _P, _P]),
     "em_td1_factor": (_I, [_P, _P, _I64]),
+    "em_fd_plan_create": (_I, [_P, _I64, _P, _I64, _P, _I64, ctypes.POINTER(_P),
+                               ctypes.POINTER(_I64)]),
+    "em_fd_plan_destroy": (None, [_P]),
+    "em_fd_solve": (_I, [_P, _D, _P, _P, _P, _P, ctypes.POINTER(_I64)]),
+    "em_tone_table": (_I, [_P, _I64, _D, _D, _I, _P, _P, _I64]),
     "em_synth_plate": (_I, [_P, _I64, _I64, _I64, _D, _D, _D, _I64, _P, _P, _P, _P, _I64, _P,
                             _I64, _P, _P]),
 }

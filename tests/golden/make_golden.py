@@ -3,7 +3,7 @@
 Run in the build container (where /root/reference exists); the resulting
 .npz files are committed and are all the GPU box ever sees:
 
-    python tests/golden/make_golden.py kat plate_small plate_200 tubes   # seconds
+    python tests/golden/make_golden.py kat plate_small plate_200 tubes fd   # seconds
     python tests/golden/make_golden.py c1                                # ~30 min (Jacobi at N=2000)
 
 The reference is copied to a writable temp dir first because its numba
@@ -172,6 +172,49 @@ def case_c1(em):
          input_sha_m0=np.array(sha(m["m0"])), **res)
 
 
+def case_fd(em):
+    """Frequency domain: the reference solve_tone on the plate_small
+    and tube_small models at several tones, dft_phasor / extract_phasors KATs."""
+    from eddymodes.frequency import dft_phasor, extract_phasors, solve_tone
+    from eddymodes.errors import NonintegerPeriods, NyquistViolation
+    out = {}
+    for name in ("plate_small", "tube_small"):
+        g = np.load(os.path.join(HERE, f"{name}.npz"))
+        n_p = g["r_d"].shape[1]
+        n_s = g["m0"].shape[1]
+        rm = _reduced(em, g["r_i"], g["l_i"], g["r_d"], g["l_d"], g["m0"],
+                      tuple(f"p{i}" for i in range(n_p)), tuple(f"s{i}" for i in range(n_s)))
+        i_d = (np.arange(n_p) + 1.0) * (1.0 + 0.5j)
+        i0 = (np.arange(n_s) + 1.0) * (0.3 - 0.2j)
+        omegas = np.array([0.0, 2e3, 2 * np.pi * 5e4, 3e6])
+        out[f"{name}_omegas"] = omegas
+        out[f"{name}_i_d"] = i_d
+        out[f"{name}_i0"] = i0
+        for k, w in enumerate(omegas):
+            out[f"{name}_I_{k}"] = solve_tone(rm, float(w), i_d, i0)
+    dt, n = 1e-6, 2000
+    t = dt * np.arange(n)
+    x = (0.7 * np.sin(2 * np.pi * 1e4 * t + 0.3) + 0.2 * np.cos(2 * np.pi * 2.5e4 * t)
+         + 0.05 * np.sin(2 * np.pi * 1e5 * t - 1.0))
+    out["dft_x"] = x
+    out["dft_dt"] = np.array(dt)
+    out["dft_freqs"] = np.array([1e4, 2.5e4, 1e5, 5e4])
+    out["dft_phasors"] = np.array([dft_phasor(x, dt, f) for f in out["dft_freqs"]])
+    out["dft_phasor_t0"] = np.array(dft_phasor(x[500:1500], dt, 1e4, t0=500 * dt))
+    rec = np.stack([x, 2 * x[::-1], np.cos(2 * np.pi * 1e4 * t)], axis=1)
+    ps = extract_phasors(t, rec, [1e4, 5e4], [0.0, 1.0, 2.0], window=(2e-4, 1.2e-3))
+    out["ext_rec"] = rec
+    out["ext_keys"] = np.array([[p, f] for (p, f) in sorted(ps.entries)])
+    out["ext_vals"] = np.array([ps.entries[k] for k in sorted(ps.entries)])
+    for bad, exc in (((x, dt, 6e5), NyquistViolation), ((x[:1999], dt, 1e4), NonintegerPeriods)):
+        try:
+            dft_phasor(*bad)
+            raise SystemExit("expected an error")
+        except exc:
+            pass
+    save("fd", **out)
+
+
 def main(argv):
     em = import_reference()
     for case in argv or ["kat", "plate_small", "plate_200", "tubes"]:
@@ -185,6 +228,8 @@ def main(argv):
             case_tubes(em)
         elif case == "c1":
             case_c1(em)
+        elif case == "fd":
+            case_fd(em)
         else:
             raise SystemExit(f"unknown case {case}")
 

@@ -105,3 +105,19 @@ def test_c1_inputs_pinned_and_lapack_eigenvalues():
     assert sha(m["c"]) == str(g["input_sha_c"]) and sha(m["m0"]) == str(g["input_sha_m0"])
     lap = O.generalized_eig_lapack(O.sym_mirror(m["l_i"]), O.sym_mirror(m["r_i"]))
     assert np.max(np.abs(lap.tau - g["tau"]) / g["tau"]) < 1e-10
+
+
+def test_fd_solve_tone_and_dft_bitwise():
+    """Frequency domain: the C restatement of lu_factor/lu_solve
+    (_kernels.py:144-193) through solve_tone's embedding (frequency.py:56-94), and
+    dft_phasor (frequency.py:114-138), bit for bit against the reference."""
+    g = golden("fd")
+    for name in ("plate_small", "tube_small"):
+        m = golden(name)
+        for k, w in enumerate(g[f"{name}_omegas"]):
+            i = O.solve_tone(m["r_i"], m["l_i"], m["r_d"], m["l_d"], m["m0"], float(w),
+                             g[f"{name}_i_d"], g[f"{name}_i0"])
+            assert np.array_equal(i, g[f"{name}_I_{k}"])
+    x, dt = g["dft_x"], float(g["dft_dt"])
+    for f, p in zip(g["dft_freqs"], g["dft_phasors"]):
+        assert O.dft_phasor(x, dt, float(f)) == p
