@@ -215,6 +215,25 @@ def case_fd(em):
     save("fd", **out)
 
 
+def case_cache(em):
+    """The reference's text cache (E/matrixio.py) for the tube_small model, with an
+    integer E and a current basis (the reference's own tube network)."""
+    from eddymodes.assembly import (assemble_branch_matrices, build_current_basis,
+                                    electrode_incidence)
+    from eddymodes.matrixio import write_cache
+    from eddymodes.network import generate_tube_grid
+    from eddymodes.reduction import project_model
+    net = generate_tube_grid(84e-3, 0.3, 3e-3, 3, 5, 1.09e-6)
+    bm = assemble_branch_matrices(net)
+    basis_c = build_current_basis(net)
+    e = electrode_incidence(net, basis_c)
+    port_names = tuple(el.name for el in net.electrodes[:-1])
+    rm = project_model(bm, basis_c, e, port_names=port_names)
+    path = os.path.join(HERE, "cache_tube.txt")
+    write_cache(path, rm, None, e=e.e, header_lines=("golden: reference write_cache",))
+    print(f"wrote {path} ({os.path.getsize(path) / 1e3:.0f} kB) N={rm.n_internal}")
+
+
 def main(argv):
     em = import_reference()
     for case in argv or ["kat", "plate_small", "plate_200", "tubes"]:
@@ -230,6 +249,8 @@ def main(argv):
             case_c1(em)
         elif case == "fd":
             case_fd(em)
+        elif case == "cache":
+            case_cache(em)
         else:
             raise SystemExit(f"unknown case {case}")
 
