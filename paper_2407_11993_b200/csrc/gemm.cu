@@ -43,9 +43,12 @@ constexpr int gstages() {
 
 // Load a LONG x GBK slab of op(X) (the "long" extent is LONG, the k extent GBK).
 // TRANS == 0: X stored long-contiguous (X[l + k*ld]); TRANS == 1: k-contiguous (X[k + l*ld]).
-template <int TRANS, int VEC, int LONG>
+// AL: X is lower triangular (element (l, k) used only when k <= l; the stored upper
+// part is ignored) — VEC == 1 only.
+template <int TRANS, int VEC, int LONG, int AL = 0>
 EM_DEVINL void load_slab(double* s, const double* __restrict__ X, int64_t ld, int64_t l0,
                          int64_t k0, int64_t L, int64_t K, int tid) {
+  static_assert(!AL || (VEC == 1 && TRANS == 0), "lower-A loads are 8-byte, long-contiguous");
   constexpr int SPL = LONG + 4;
   if (!TRANS) {
     // contiguous along l; smem [k][l] stride SPL
@@ -61,7 +64,7 @@ EM_DEVINL void load_slab(double* s, const double* __restrict__ X, int64_t ld, in
         const double* src = nv ? X + gl + gk * ld : X;
         cp_async16(dst, src, nv * 8);
       } else {
-        bool v = (gk < K) && (gl < L);
+        bool v = (gk < K) && (gl < L) && (!AL || gk <= gl);
         cp_async8(dst, v ? X + gl + gk * ld : X, v);
       }
     }
@@ -87,7 +90,8 @@ EM_DEVINL void load_slab(double* s, const double* __restrict__ X, int64_t ld, in
 }
 
 // One CTA tile of the product. Shared by the plain and grouped kernels.
-template <int TA, int TB, int LOWER, int VEC>
+// AL: A (TA == 0) is lower triangular: k-tiles past the tile's last row are skipped.
+template <int TA, int TB, int LOWER, int VEC, int AL = 0>
 EM_DEVINL void gemm_tile(const GemmArgs& p, int64_t m0, int64_t n0, double* smem) {
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -105,12 +109,13 @@ EM_DEVINL void gemm_tile(const GemmArgs& p, int64_t m0, int64_t n0, double* smem
 #pragma unroll
     for (int j = 0; j < WTN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  const int64_t nk = (p.k + GBK - 1) / GBK;
+  const int64_t nk = AL ? imin64((p.k + GBK - 1) / GBK, (m0 + GBM + GBK - 1) / GBK)
+                        : (p.k + GBK - 1) / GBK;
   // prologue
 #pragma unroll
   for (int s = 0; s < GSTAGES - 1; ++s) {
     if (s < nk) {
-      load_slab<TA, VEC, GBM>(As + s * ASZ, p.A, p.lda, m0, s * GBK, p.m, p.k, tid);
+      load_slab<TA, VEC, GBM, AL>(As + s * ASZ, p.A, p.lda, m0, s * GBK, p.m, p.k, tid);
       load_slab<!TB, VEC, GBN>(Bs + s * BSZ, p.B, p.ldb, n0, s * GBK, p.n, p.k, tid);
     }
     cp_async_commit();
@@ -124,7 +129,7 @@ EM_DEVINL void gemm_tile(const GemmArgs& p, int64_t m0, int64_t n0, double* smem
       int64_t kn = kt + GSTAGES - 1;
       int sb = (int)(kn % GSTAGES);
       if (kn < nk) {
-        load_slab<TA, VEC, GBM>(As + sb * ASZ, p.A, p.lda, m0, kn * GBK, p.m, p.k, tid);
+        load_slab<TA, VEC, GBM, AL>(As + sb * ASZ, p.A, p.lda, m0, kn * GBK, p.m, p.k, tid);
         load_slab<!TB, VEC, GBN>(Bs + sb * BSZ, p.B, p.ldb, n0, kn * GBK, p.n, p.k, tid);
       }
       cp_async_commit();
@@ -193,7 +198,7 @@ EM_DEVINL void gemm_tile(const GemmArgs& p, int64_t m0, int64_t n0, double* smem
   }
 }
 
-template <int TA, int TB, int LOWER, int VEC>
+template <int TA, int TB, int LOWER, int VEC, int AL = 0>
 __global__ void __launch_bounds__(GTHREADS, GMINB) gemm_kernel(GemmArgs p, double* ws, int64_t kc) {
   extern __shared__ __align__(16) double smem[];
   if (ws) {
@@ -222,7 +227,7 @@ __global__ void __launch_bounds__(GTHREADS, GMINB) gemm_kernel(GemmArgs p, doubl
   const int64_t tn = (bid % per_group) / gsz;
   const int64_t m0 = tm * GBM, n0 = tn * GBN;
   if (LOWER && m0 + GBM - 1 + p.diag_off < n0) return;  // tile strictly above the diagonal
-  gemm_tile<TA, TB, LOWER, VEC>(p, m0, n0, smem);
+  gemm_tile<TA, TB, LOWER, VEC, AL>(p, m0, n0, smem);
 }
 
 // Grouped launch: blockIdx.y selects a problem; problems carry their own sizes/pointers.
@@ -349,6 +354,25 @@ cudaError_t gemm(cudaStream_t st, bool ta, bool tb, int64_t m, int64_t n, int64_
     case 6: return launch_v<1, 1, 0>(p, st);
     default: return launch_v<1, 1, 1>(p, st);
   }
+}
+
+cudaError_t gemm_lower_a(cudaStream_t st, int64_t m, int64_t n, int64_t k, double alpha,
+                         const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
+                         double* C, int64_t ldc) {
+  if (m <= 0 || n <= 0) return cudaSuccess;
+  if (k <= 0) return scale_matrix(st, m, n, beta, C, ldc, false, 0);
+  GemmArgs p{m, n, k, A, lda, B, ldb, C, ldc, alpha, beta, 0};
+  auto kern = gemm_kernel<0, 0, 0, 1, 1>;
+  const size_t sm = smem_bytes(0, 0);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    configured = true;
+  }
+  const int64_t tiles = ((m + GBM - 1) / GBM) * ((n + GBN - 1) / GBN);
+  kern<<<(unsigned)tiles, GTHREADS, sm, st>>>(p, nullptr, 0);
+  count_launch();
+  return cudaGetLastError();
 }
 
 template <int TA, int TB>

@@ -22,6 +22,13 @@ cudaError_t gemm(cudaStream_t st, bool ta, bool tb, int64_t m, int64_t n, int64_
                  const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
                  int64_t ldc, bool lower = false, int64_t diag_off = 0);
 
+// C = alpha * A * B + beta * C with A (m x k) LOWER triangular: only A(r, c) with c <= r
+// is read (the stored upper part is ignored) and k-tiles past each row tile are skipped,
+// i.e. half the flops of a square product (TRMM-like).
+cudaError_t gemm_lower_a(cudaStream_t st, int64_t m, int64_t n, int64_t k, double alpha,
+                         const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
+                         double* C, int64_t ldc);
+
 // Many independent problems in one launch (device-resident argument array).
 cudaError_t gemm_grouped(cudaStream_t st, bool ta, bool tb, const GemmArgs* d_probs, int nprob,
                          int max_tiles);

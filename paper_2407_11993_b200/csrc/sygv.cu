@@ -108,6 +108,29 @@ __global__ void coldot_kernel(int64_t n, const double* __restrict__ V, int64_t l
   }
 }
 
+// out[j] = v_j^T L v_j for symmetric L from X = L_low V (L_low: lower triangle of L with
+// its diagonal): v^T L v = 2 v^T L_low v - sum_i L_ii v_i^2 (exact identity).
+__global__ void quadform_lower_kernel(int64_t n, const double* __restrict__ V, int64_t ldv,
+                                      const double* __restrict__ X, int64_t ldx,
+                                      const double* __restrict__ L, int64_t ldl,
+                                      double* __restrict__ out) {
+  __shared__ double red[32];
+  const int64_t j = blockIdx.x;
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const double v = V[i + j * ldv];
+    s = fma(v, fma(2.0, X[i + j * ldx], -L[i + i * ldl] * v), s);
+  }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double t = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) out[j] = t;
+  }
+}
+
 // Returns -1 on success; else the failing pivot with *which = 0 (R) / 1 (L).
 int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const double* R,
              int64_t ldr, double* tau, double* V, int64_t ldv, double* l_n, double* r_n,
@@ -166,9 +189,11 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
   Z.release();
   Stage post(st, ST_POST_GEMM);
   if (l_n) {
+    // l_n = diag(V^T L V) (modal.py:79) through the lower triangle of L only (the
+    // SymMatrix definition of L): a triangular-A product, half the flops of L V
     DBuf LV(nn, st);
-    EM_CK(gemm(st, false, false, n, n, n, 1.0, L, ldl, V, ldv, 0.0, LV.p, n));
-    coldot_kernel<<<(unsigned)n, 256, 0, st>>>(n, V, ldv, LV.p, n, l_n);
+    EM_CK(gemm_lower_a(st, n, n, n, 1.0, L, ldl, V, ldv, 0.0, LV.p, n));
+    quadform_lower_kernel<<<(unsigned)n, 256, 0, st>>>(n, V, ldv, LV.p, n, L, ldl, l_n);
     EM_LAUNCHED();
   }
   if (r_n || VtR) {

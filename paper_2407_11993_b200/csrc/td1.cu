@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(256) trsv_fwd_kernel(int64_t n, const double* 
       if (j > ready) {
         __shared__ int64_t jr;
         if (tid == 0) {
-          while (ld_acquire(flags + j) != epoch) __nanosleep(20);
+          while (ld_acquire(flags + j) != epoch) {}
           int64_t e = j;
           while (e + 1 < r && ld_acquire(flags + e + 1) == epoch) ++e;
           jr = e;
@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(256) trsv_bwd_kernel(
       if (j < ready) {
         __shared__ int64_t jr;
         if (tid == 0) {
-          while (ld_acquire(flags + j) != epoch) __nanosleep(20);
+          while (ld_acquire(flags + j) != epoch) {}
           int64_t e = j;
           while (e - 1 > r && ld_acquire(flags + e - 1) == epoch) --e;
           jr = e;
