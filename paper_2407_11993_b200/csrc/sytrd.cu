@@ -10,6 +10,8 @@
 // latrd_col_kernel (finish the previous W column, update this column, partials of
 // its norm and of the panel products), the symv with dlarfg folded into its
 // prologue, the symv reduction (+ panel products t), latrd_w_kernel.
+#include <vector>
+
 #include "common.cuh"
 #include "ctx.h"
 #include "gemm.h"
@@ -390,19 +392,15 @@ __global__ void larft_wide_kernel(int w, const double* __restrict__ G, int64_t l
   }
 }
 
-// larft for the diagonal 128-blocks of T (w x w, ld ldt): CTA b builds the block of
-// reflectors [b*w1, ...) from the matching diagonal block of G = V^T V in shared
+// larft for the diagonal 128-blocks of T (w x w, ld ldt): CTA half b builds the block
+// of reflectors [b*w1, ...) from the matching diagonal block of G = V^T V in shared
 // memory; also zeroes the strictly-lower blocks of T.
-__global__ void __launch_bounds__(128) larft_smem_kernel(int w, int w1,
-                                                         const double* __restrict__ G,
-                                                         int64_t ldg,
-                                                         const double* __restrict__ tau,
-                                                         int64_t c0, double* T, int64_t ldt) {
-  extern __shared__ double Ts[];  // 128 x 129
-  __shared__ double gk[128];
+EM_DEVINL void larft_smem_body(int half, int w, int w1, const double* __restrict__ G,
+                               int64_t ldg, const double* __restrict__ tau, int64_t c0,
+                               double* T, int64_t ldt, double* Ts, double* gk) {
   constexpr int LD = 129;
-  const int off = blockIdx.x * w1;
-  const int bw = blockIdx.x == 0 ? w1 : w - w1;
+  const int off = half * w1;
+  const int bw = half == 0 ? w1 : w - w1;
   const int tid = threadIdx.x;
   for (int i = tid; i < 128 * LD; i += blockDim.x) Ts[i] = 0.0;
   __syncthreads();
@@ -422,8 +420,35 @@ __global__ void __launch_bounds__(128) larft_smem_kernel(int w, int w1,
     const int r = i % bw, c = i / bw;
     T[(off + r) + (off + c) * ldt] = Ts[r + c * LD];
   }
-  if (blockIdx.x == 1)  // strictly-lower off-diagonal block
+  if (half == 1)  // strictly-lower off-diagonal block
     for (int i = tid; i < bw * w1; i += blockDim.x) T[(w1 + i % bw) + (i / bw) * ldt] = 0.0;
+}
+
+__global__ void __launch_bounds__(128) larft_smem_kernel(int w, int w1,
+                                                         const double* __restrict__ G,
+                                                         int64_t ldg,
+                                                         const double* __restrict__ tau,
+                                                         int64_t c0, double* T, int64_t ldt) {
+  extern __shared__ double Ts[];  // 128 x 129
+  __shared__ double gk[128];
+  larft_smem_body(blockIdx.x, w, w1, G, ldg, tau, c0, T, ldt, Ts, gk);
+}
+
+// every ORM_NB-reflector block of ormqr at once: block p = blockIdx.y (G, T with
+// stride nb^2, ld = its width), half = blockIdx.x
+__global__ void __launch_bounds__(128) larft_batched_kernel(int64_t nref, int nb,
+                                                            const double* __restrict__ G,
+                                                            const double* __restrict__ tau,
+                                                            double* T) {
+  extern __shared__ double Ts[];
+  __shared__ double gk[128];
+  const int64_t p = blockIdx.y;
+  const int64_t c0 = p * nb;
+  const int w = (int)imin64(nb, nref - c0);
+  const int w1 = w < 128 ? w : 128;
+  if (blockIdx.x == 1 && w <= w1) return;
+  const size_t str = (size_t)nb * nb;
+  larft_smem_body(blockIdx.x, w, w1, G + p * str, w, tau, c0, T + p * str, w, Ts, gk);
 }
 
 // Z <- Q Z, Q = H(0)...H(n-2), in blocks of ORM_NB reflectors (compact WY,
@@ -437,38 +462,72 @@ void ormtr_lower(cudaStream_t st, int64_t n, int64_t m, const double* A, int64_t
 }
 
 // Z <- H(0) ... H(nref-1) Z for reflectors stored below the `off`-th subdiagonal of A.
+// The V blocks and their T factors do not depend on Z: all of them are built first
+// (one launch each for V, the grouped G = V^T V, the larft halves of every block in
+// one grid, the grouped T12 joins), so only the three Z GEMMs per block are sequential.
 void ormqr_lower_off(cudaStream_t st, int64_t n, int64_t nref, int64_t off, int64_t m,
                      const double* A, int64_t lda, const double* tau, double* Z, int64_t ldz) {
   if (nref <= 0 || m <= 0) return;
-  DBuf V((size_t)n * ORM_NB, st), G((size_t)ORM_NB * ORM_NB, st), T((size_t)ORM_NB * ORM_NB, st);
-  DBuf W1((size_t)ORM_NB * m, st), W2((size_t)ORM_NB * m, st);
   const int64_t npan = (nref + ORM_NB - 1) / ORM_NB;
+  const size_t vstride = (size_t)n * ORM_NB, tstride = (size_t)ORM_NB * ORM_NB;
+  DBuf V(vstride * npan, st), G(tstride * npan, st), T(tstride * npan, st),
+      T1G(tstride * npan, st);
+  DBuf W1((size_t)ORM_NB * m, st), W2((size_t)ORM_NB * m, st);
   EM_CK(cudaFuncSetAttribute(larft_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(128 * 129 * sizeof(double))));
+  std::vector<GemmArgs> gg, t1, t2;
+  int max_g = 1, max_t = 1;
+  for (int64_t p = 0; p < npan; ++p) {
+    const int64_t i0 = p * ORM_NB;
+    const int w = (int)imin64(ORM_NB, nref - i0);
+    const int64_t mr = n - i0 - off;
+    double* Vp = V.p + p * vstride;
+    dim3 grid((unsigned)imax64(1, imin64((mr + 255) / 256, 64)), (unsigned)w);
+    build_v_kernel<<<grid, 256, 0, st>>>(n, A, lda, i0, w, off, Vp, n);
+    EM_LAUNCHED();
+    double* Gp = G.p + p * tstride;
+    gg.push_back(GemmArgs{w, w, mr, Vp, n, Vp, n, Gp, w, 1.0, 0.0, 0});
+    max_g = (int)imax64(max_g, ((w + 127) / 128) * ((w + 63) / 64));
+    const int w1 = (int)imin64(w, 128), w2 = w - w1;
+    double* Tp = T.p + p * tstride;
+    if (w2 > 0) {  // T12 = -T1 G12 T2 (larft joins of the two halves)
+      double* Xp = T1G.p + p * tstride;
+      t1.push_back(GemmArgs{w1, w2, w1, Tp, w, Gp + (int64_t)w1 * w, w, Xp, w1, 1.0, 0.0, 0});
+      t2.push_back(GemmArgs{w1, w2, w2, Xp, w1, Tp + w1 + (int64_t)w1 * w, w,
+                            Tp + (int64_t)w1 * w, w, -1.0, 0.0, 0});
+      max_t = (int)imax64(max_t, 4);
+    }
+  }
+  DArr<GemmArgs> dgg(gg.size(), st), dt1(imax64((int64_t)t1.size(), 1), st),
+      dt2(imax64((int64_t)t2.size(), 1), st);
+  EM_CK(cudaMemcpyAsync(dgg.p, gg.data(), gg.size() * sizeof(GemmArgs), cudaMemcpyHostToDevice,
+                        st));
+  EM_CK(gemm_grouped(st, true, false, dgg.p, (int)gg.size(), max_g));
+  EM_CK(cudaFuncSetAttribute(larft_batched_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(128 * 129 * sizeof(double))));
+  larft_batched_kernel<<<dim3(2, (unsigned)npan), 128, (size_t)128 * 129 * sizeof(double), st>>>(
+      nref, ORM_NB, G.p, tau, T.p);
+  EM_LAUNCHED();
+  if (!t1.empty()) {
+    EM_CK(cudaMemcpyAsync(dt1.p, t1.data(), t1.size() * sizeof(GemmArgs),
+                          cudaMemcpyHostToDevice, st));
+    EM_CK(cudaMemcpyAsync(dt2.p, t2.data(), t2.size() * sizeof(GemmArgs),
+                          cudaMemcpyHostToDevice, st));
+    EM_CK(gemm_grouped(st, false, false, dt1.p, (int)t1.size(), max_t));
+    EM_CK(gemm_grouped(st, false, false, dt2.p, (int)t2.size(), max_t));
+  }
   for (int64_t p = npan - 1; p >= 0; --p) {
     const int64_t i0 = p * ORM_NB;
     const int w = (int)imin64(ORM_NB, nref - i0);
-    const int64_t mr = n - i0 - off;  // rows of V
-    dim3 grid((unsigned)imax64(1, imin64((mr + 255) / 256, 64)), (unsigned)w);
-    build_v_kernel<<<grid, 256, 0, st>>>(n, A, lda, i0, w, off, V.p, n);
-    EM_LAUNCHED();
-    EM_CK(gemm(st, true, false, w, w, mr, 1.0, V.p, n, V.p, n, 0.0, G.p, w));
-    // T from two 128-halves built in shared memory, joined by T12 = -T1 G12 T2
-    const int w1 = imin64(w, 128), w2 = w - w1;
-    larft_smem_kernel<<<w2 > 0 ? 2 : 1, 128, (size_t)128 * 129 * sizeof(double), st>>>(
-        w, w1, G.p, w, tau, i0, T.p, w);
-    EM_LAUNCHED();
-    if (w2 > 0) {
-      EM_CK(gemm(st, false, false, w1, w2, w1, 1.0, T.p, w, G.p + (int64_t)w1 * w, w, 0.0,
-                 W1.p, w1));
-      EM_CK(gemm(st, false, false, w1, w2, w2, -1.0, W1.p, w1, T.p + w1 + (int64_t)w1 * w, w,
-                 0.0, T.p + (int64_t)w1 * w, w));
-    }
+    const int64_t mr = n - i0 - off;
+    const double* Vp = V.p + p * vstride;
+    const double* Tp = T.p + p * tstride;
     double* Zs = Z + (i0 + off);
-    EM_CK(gemm(st, true, false, w, m, mr, 1.0, V.p, n, Zs, ldz, 0.0, W1.p, w));
-    EM_CK(gemm(st, false, false, w, m, w, 1.0, T.p, w, W1.p, w, 0.0, W2.p, w));
-    EM_CK(gemm(st, false, false, mr, m, w, -1.0, V.p, n, W2.p, w, 1.0, Zs, ldz));
+    EM_CK(gemm(st, true, false, w, m, mr, 1.0, Vp, n, Zs, ldz, 0.0, W1.p, w));
+    EM_CK(gemm(st, false, false, w, m, w, 1.0, Tp, w, W1.p, w, 0.0, W2.p, w));
+    EM_CK(gemm(st, false, false, mr, m, w, -1.0, Vp, n, W2.p, w, 1.0, Zs, ldz));
   }
+  EM_CK(cudaStreamSynchronize(st));  // host argument arrays
 }
 
 }  // namespace em
