@@ -151,12 +151,19 @@ __global__ void __launch_bounds__(256) potf2_inv_kernel(double* A, int64_t lda, 
         for (int x = 0; x < 4; ++x)
 #pragma unroll
           for (int y = 0; y < 4; ++y) acc[x][y] = 0.0;
+        // k < c0: Linv_kk[c][k] is a strictly-lower entry (packed upper storage); the
+        // last four k (the 4 x 4 diagonal piece) go through linv_at
         for (int k = 0; k < c0 + 4; ++k) {
           double a[4], b[4];
 #pragma unroll
           for (int x = 0; x < 4; ++x) a[x] = S[(r0 + x) + (o + k) * PLD];
+          if (k < c0) {
 #pragma unroll
-          for (int y = 0; y < 4; ++y) b[y] = linv_at(S, dinv, o + c0 + y, o + k);
+            for (int y = 0; y < 4; ++y) b[y] = S[(o + k) + (o + c0 + y) * PLD];
+          } else {
+#pragma unroll
+            for (int y = 0; y < 4; ++y) b[y] = linv_at(S, dinv, o + c0 + y, o + k);
+          }
 #pragma unroll
           for (int x = 0; x < 4; ++x)
 #pragma unroll
@@ -234,8 +241,13 @@ __global__ void __launch_bounds__(256) potf2_inv_kernel(double* A, int64_t lda, 
         double a[4], b[4];
 #pragma unroll
         for (int x = 0; x < 4; ++x) a[x] = S[(r0 + x) + kk * PLD];
+        if (kk >= c0 + 4) {  // strictly below the 4 x 4 diagonal piece: packed storage
 #pragma unroll
-        for (int y = 0; y < 4; ++y) b[y] = linv_at(S, dinv, kk, c0 + y);
+          for (int y = 0; y < 4; ++y) b[y] = S[(c0 + y) + kk * PLD];
+        } else {
+#pragma unroll
+          for (int y = 0; y < 4; ++y) b[y] = linv_at(S, dinv, kk, c0 + y);
+        }
 #pragma unroll
         for (int x = 0; x < 4; ++x)
 #pragma unroll
@@ -258,8 +270,13 @@ __global__ void __launch_bounds__(256) potf2_inv_kernel(double* A, int64_t lda, 
         for (int y = 0; y < 4; ++y) acc[x][y] = 0.0;
       for (int kk = i * PB; kk < r0 + 4; ++kk) {
         double a[4], b[4];
+        if (kk < r0) {  // strictly lower entries of Linv_ii: packed storage
 #pragma unroll
-        for (int x = 0; x < 4; ++x) a[x] = linv_at(S, dinv, r0 + x, kk);
+          for (int x = 0; x < 4; ++x) a[x] = S[kk + (r0 + x) * PLD];
+        } else {
+#pragma unroll
+          for (int x = 0; x < 4; ++x) a[x] = linv_at(S, dinv, r0 + x, kk);
+        }
 #pragma unroll
         for (int y = 0; y < 4; ++y) b[y] = S[(c0 + y) + kk * PLD];  // W[kk][c]
 #pragma unroll
