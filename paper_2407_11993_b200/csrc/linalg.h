@@ -40,6 +40,7 @@ struct SymvLarfg {
   double* tau = nullptr;          // outputs, written by CTA 0
   double* e = nullptr;
   double* scale = nullptr;
+  double* vav = nullptr;  // optional: per-CTA partials of v^T A v (symv_tma only)
 };
 // latrd panel products t = [W_p^T v | A_p^T v] (2 x 64) from per-CTA partials over rows
 // >= c+2 of the raw column (times scale) plus row c+1 (v = 1 there).
@@ -67,6 +68,8 @@ size_t symv_tma_work_size(int64_t n);
 void symv_tma(cudaStream_t st, const SymvMap& m, int64_t off, int64_t n, double alpha,
               const double* x, double beta, double* y, double* work, const SymvLarfg* lf,
               const LatrdT* lt, bool pdl);
+// number of CTAs (= quadratic-form partials written to SymvLarfg::vav) for order n
+int64_t symv_tma_ctas(int64_t n);
 
 // sytrd.cu: Householder tridiagonalisation (lower). On exit d (n), e (n-1), tau (n-1);
 // reflectors stored below the subdiagonal of A (LAPACK dsytrd convention).

@@ -95,6 +95,8 @@ static TmaSched tma_sched(int64_t n) {
   return s;
 }
 
+int64_t symv_tma_ctas(int64_t n) { return tma_sched(n).P; }
+
 size_t symv_tma_work_size(int64_t n) {
   const TmaSched s = tma_sched(n);
   return (size_t)(s.nbs * s.ncj * WC + s.nbs * s.slots * HR);
@@ -161,7 +163,10 @@ __global__ void __launch_bounds__(TT, 1) symv_tma_kernel(const __grid_constant__
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int64_t p = blockIdx.x;
   const int64_t t0 = p * len, t1 = imin64(T, t0 + len);
-  if (t0 >= t1) return;
+  if (t0 >= t1) {  // not launched by symv_tma (P is trimmed to the last non-empty range)
+    if (LARFG && lf.vav != nullptr && tid == 0) lf.vav[p] = 0.0;
+    return;
+  }
   if (tid == 0) {
 #pragma unroll
     for (int s = 0; s < NST; ++s) {
@@ -213,6 +218,9 @@ __global__ void __launch_bounds__(TT, 1) symv_tma_kernel(const __grid_constant__
     }
     xs = scale;
   }
+  // v^T A v partial of this CTA (x = v): sum x_c colsum_c over tiles + x_r rowsum_r
+  double vav = 0.0;
+  const bool want_vav = LARFG && lf.vav != nullptr;
   // thread rows 64h + 2*lane + q (h, q in {0,1}); columns 4w + cc
   double xi[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
   double row[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
@@ -305,8 +313,11 @@ __global__ void __launch_bounds__(TT, 1) symv_tma_kernel(const __grid_constant__
       v += __shfl_xor_sync(0xffffffffu, v, 4);
       v += __shfl_xor_sync(0xffffffffu, v, 2);
       v += __shfl_xor_sync(0xffffffffu, v, 1);
-      if ((lane & 7) == 0)
-        wcol[(i * ncj + j) * WC + 4 * w + (h16 ? 2 : 0) + (h8 ? 1 : 0)] = v;
+      if ((lane & 7) == 0) {
+        const int cc = (h16 ? 2 : 0) + (h8 ? 1 : 0);
+        wcol[(i * ncj + j) * WC + 4 * w + cc] = v;
+        if (want_vav) vav = fma(v, xj[cc], vav);
+      }
     }
     if (j + 1 == tiles_in(i) || t + 1 == t1) {  // end of this CTA's piece of strip i
       __syncthreads();
@@ -322,10 +333,22 @@ __global__ void __launch_bounds__(TT, 1) symv_tma_kernel(const __grid_constant__
         for (int k2 = 0; k2 < TT / 32; ++k2) sum += red[k2][tid];
         const int64_t slot = p - (i * (i + 1)) / len;
         wrow[(i * slots + slot) * HR + tid] = sum;
+        if (want_vav) vav = fma(sum, symv_xval(x, r0 + tid, n, xs, LARFG), vav);
       }
       fresh = true;
     }
     if (j + 1 < tiles_in(i)) ++j; else { ++i; j = 0; }
+  }
+  if (want_vav) {
+    __syncthreads();
+    double sv = warp_sum(vav);
+    if (lane == 0) red[0][w] = sv;
+    __syncthreads();
+    if (tid == 0) {
+      double tot = 0.0;
+      for (int k2 = 0; k2 < TT / 32; ++k2) tot += red[0][k2];
+      lf.vav[p] = tot;
+    }
   }
 }
 

@@ -46,22 +46,37 @@ constexpr int CKQ = TRD_NB / CTPR;      // panel columns per thread (16)
 //      (the dlatrd panel products, completed in symv_reduce2_kernel), x = the updated
 //      column; alpha_buf = A[c+1, c], d[c] = A[c, c].
 // upd = 0: only (1), after the last column of a panel.
+// FUSEW (TMA path): the previous column's w is formed here instead of in a separate
+// kernel: wtmp holds y = A22 v (the symv reduction), tvec the panel products t, and
+// w^T v = tau (v^T A22 v - 2 t1^T t2) comes from the symv's quadratic-form partials
+// (vav, nvav), so alpha needs no reduction over w:
+//   v = [1, scale x_raw] (written back into A[c:, c-1]),  w = tau (y - A_p t1 - W_p t2),
+//   W[:, i-1] = w + alpha v,  alpha = -tau^2/2 (v^T A22 v - 2 t1^T t2).
+struct ColW {
+  const double* tvec = nullptr;   // t of column c-1 (2 x 64)
+  const double* vav = nullptr;    // symv quadratic-form partials of column c-1
+  int64_t nvav = 0;
+  const double* scale = nullptr;  // dlarfg scale of column c-1
+};
+
+template <bool FUSEW>
 __global__ void __launch_bounds__(RT) latrd_col_kernel(
     int64_t n, double* A, int64_t lda, int64_t i0, int64_t c, int i, int upd, double* W,
     int64_t ldw, const double* wtmp, const double* part_wv, int64_t n_wv, const double* tau,
-    double* part_norm, double* dpart, double* alpha_buf, double* d) {
+    double* part_norm, double* dpart, double* alpha_buf, double* d, ColW cw) {
   __shared__ double wr[TRD_NB], ar[TRD_NB], red[RT / 32];
   __shared__ double pred[RT / 32][2 * TRD_NB];
-  __shared__ double s_alpha;
+  __shared__ double t1s[TRD_NB], t2s[TRD_NB];
+  __shared__ double s_alpha, s_wc;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int sub = tid & (CTPR - 1);
   const int64_t r = c + blockIdx.x * (int64_t)CRW + tid / CTPR;
   const bool valid = r < n;
   // before the dependency wait: panel columns k < i-1 (finished two launches ago or
-  // earlier) and the raw column c (only this kernel writes it)
+  // earlier) and the raw columns c-1 (FUSEW) and c (only this kernel writes them)
   double av[CKQ], wv[CKQ];
-  double acol = 0.0;
-  if (upd) {
+  double acol = 0.0, xprev = 0.0;
+  if (upd || FUSEW) {
     for (int k = tid; k < i - 1; k += RT) {
       wr[k] = W[(c - i0) + k * ldw];
       ar[k] = A[c + (i0 + k) * lda];
@@ -73,33 +88,82 @@ __global__ void __launch_bounds__(RT) latrd_col_kernel(
       av[q] = ok ? A[r + (i0 + k) * lda] : 0.0;
       wv[q] = ok ? W[(r - i0) + k * ldw] : 0.0;
     }
-    if (valid) acol = A[r + c * lda];
+    if (valid && upd) acol = A[r + c * lda];
+    if (FUSEW && i > 0 && valid) xprev = A[r + (c - 1) * lda];
+  }
+  double tprev = 0.0, scprev = 0.0, vavsum = 0.0;
+  if (FUSEW && i > 0) {  // from the symv two launches back
+    tprev = tau[c - 1];
+    scprev = *cw.scale;
+    double sv = 0.0;
+    for (int64_t q = tid; q < cw.nvav; q += RT) sv += cw.vav[q];
+    vavsum = block_sum(sv, red);  // thread 0
   }
   pdl_wait();
   pdl_trigger();
-  double alpha_p = 0.0;
-  if (i > 0) {
-    double s = 0.0;
-    for (int64_t q = tid; q < n_wv; q += RT) s += __ldcg(part_wv + q);
-    const double t = block_sum(s, red);
-    if (tid == 0) s_alpha = -0.5 * __ldcg(tau + c - 1) * t;
+  double alpha_p = 0.0, wlast = 0.0, vlast = 0.0;
+  if (!FUSEW) {
+    if (i > 0) {
+      double s = 0.0;
+      for (int64_t q = tid; q < n_wv; q += RT) s += __ldcg(part_wv + q);
+      const double t = block_sum(s, red);
+      if (tid == 0) s_alpha = -0.5 * __ldcg(tau + c - 1) * t;
+      __syncthreads();
+      alpha_p = s_alpha;
+    }
+    // column i-1 of W: w + alpha v (v_{c-1} = A[:, c-1], written by the previous launch)
+    if (i > 0 && valid) {
+      vlast = __ldcg(A + r + (c - 1) * lda);
+      wlast = fma(alpha_p, vlast, __ldcg(wtmp + r));
+    }
+  } else if (i > 0) {
+    for (int k = tid; k < i - 1; k += RT) {
+      t1s[k] = __ldcg(cw.tvec + k);
+      t2s[k] = __ldcg(cw.tvec + TRD_NB + k);
+    }
+    __syncthreads();
+    if (warp == 0) {  // alpha and w[c] (row c: v = 1), computed by every CTA
+      double tt = 0.0, dc = 0.0;
+      for (int k = lane; k < i - 1; k += 32) {
+        tt = fma(t1s[k], t2s[k], tt);
+        dc = fma(ar[k], t1s[k], fma(wr[k], t2s[k], dc));
+      }
+      tt = warp_sum(tt);
+      dc = warp_sum(dc);
+      if (lane == 0) {
+        s_alpha = -0.5 * tprev * tprev * (vavsum - 2.0 * tt);
+        s_wc = tprev * (__ldcg(wtmp + c) - dc);
+      }
+    }
+    double sdot = 0.0;
+#pragma unroll
+    for (int q = 0; q < CKQ; ++q) {
+      const int k = sub + CTPR * q;
+      if (k < i - 1) sdot = fma(av[q], t1s[k], fma(wv[q], t2s[k], sdot));
+    }
+    sdot += __shfl_xor_sync(0xffffffffu, sdot, 1);
+    sdot += __shfl_xor_sync(0xffffffffu, sdot, 2);
     __syncthreads();
     alpha_p = s_alpha;
-  }
-  // column i-1 of W: w + alpha v (v_{c-1} = A[:, c-1], written by the previous launch)
-  double wlast = 0.0, vlast = 0.0;
-  if (i > 0 && valid) {
-    vlast = __ldcg(A + r + (c - 1) * lda);
-    wlast = fma(alpha_p, vlast, __ldcg(wtmp + r));
+    if (valid) {
+      vlast = (r == c) ? 1.0 : scprev * xprev;
+      wlast = fma(alpha_p, vlast, tprev * (__ldcg(wtmp + r) - sdot));
+      if (sub == 0) A[r + (c - 1) * lda] = vlast;
+    }
   }
   if (!upd) {
     if (valid && sub == 0) W[(r - i0) + (int64_t)(i - 1) * ldw] = wlast;
     return;
   }
   if (i > 0 && tid == 0) {
-    const double vc = __ldcg(A + c + (c - 1) * lda);
-    wr[i - 1] = fma(alpha_p, vc, __ldcg(wtmp + c));
-    ar[i - 1] = vc;
+    if (FUSEW) {
+      wr[i - 1] = fma(alpha_p, 1.0, s_wc);
+      ar[i - 1] = 1.0;
+    } else {
+      const double vc = __ldcg(A + c + (c - 1) * lda);
+      wr[i - 1] = fma(alpha_p, vc, __ldcg(wtmp + c));
+      ar[i - 1] = vc;
+    }
   }
   __syncthreads();
   if (i > 0 && valid && sub == ((i - 1) & (CTPR - 1))) {
@@ -246,6 +310,9 @@ void sytrd_lower(cudaStream_t st, int64_t n, double* A, int64_t lda, double* d, 
   DBuf swork(symv_work_size(n), st);
   SymvMap tmap;  // the whole matrix; each column's trailing block by coordinates
   const bool tma_ok = !(g_sytrd_dbg & 1) && symv_map_make(&tmap, A, n, n, lda);
+  // TMA path: 3 launches per column (the w kernel folded into the next column kernel)
+  const bool fusew = tma_ok && !(g_sytrd_dbg & 8);
+  DBuf vav(imax64(symv_tma_ctas(n), 1), st);
   double* alpha_buf = slots.p;
   double* scale_buf = slots.p + 1;
   // Each panel's ~260 dependent launches (4 per column) are captured once into a CUDA
@@ -259,14 +326,29 @@ void sytrd_lower(cudaStream_t st, int64_t n, double* A, int64_t lda, double* d, 
   for (int64_t i0 = 0; i0 < n; i0 += TRD_NB) {
     const int w = (int)imin64(TRD_NB, n - i0);
     if (use_graph) EM_CK(cudaStreamBeginCapture(sc, cudaStreamCaptureModeThreadLocal));
-    int64_t gw_prev = 0;
+    int64_t gw_prev = 0, nvav_prev = 0;
     bool last = false;
+    auto col_launch = [&](int64_t c, int i, int upd) {
+      const int64_t G = (n - c + CRW - 1) / CRW;
+      ColW cw;
+      if (fusew) {
+        cw.tvec = tvec.p;
+        cw.vav = vav.p;
+        cw.nvav = nvav_prev;
+        cw.scale = scale_buf;
+        launch_pdl(latrd_col_kernel<true>, dim3((unsigned)G), dim3(RT), 0, sc, n, A, lda, i0, c,
+                   i, upd, W.p, (int64_t)n, (const double*)wtmp.p, (const double*)part_wv.p,
+                   gw_prev, (const double*)tau, part_norm.p, dpart.p, alpha_buf, d, cw);
+      } else {
+        launch_pdl(latrd_col_kernel<false>, dim3((unsigned)G), dim3(RT), 0, sc, n, A, lda, i0,
+                   c, i, upd, W.p, (int64_t)n, (const double*)wtmp.p, (const double*)part_wv.p,
+                   gw_prev, (const double*)tau, part_norm.p, dpart.p, alpha_buf, d, cw);
+      }
+    };
     for (int i = 0; i < w; ++i) {
       const int64_t c = i0 + i;
       const int64_t G = (n - c + CRW - 1) / CRW;
-      launch_pdl(latrd_col_kernel, dim3((unsigned)G), dim3(RT), 0, sc, n, A, lda, i0, c, i, 1,
-                 W.p, (int64_t)n, (const double*)wtmp.p, (const double*)part_wv.p, gw_prev,
-                 (const double*)tau, part_norm.p, dpart.p, alpha_buf, d);
+      col_launch(c, i, 1);
       if (c == n - 1) {
         last = true;
         break;
@@ -279,6 +361,7 @@ void sytrd_lower(cudaStream_t st, int64_t n, double* A, int64_t lda, double* d, 
       lf.tau = tau + c;
       lf.e = e + c;
       lf.scale = scale_buf;
+      if (fusew) lf.vav = vav.p;
       LatrdT lt;
       lt.i = i;
       lt.G = G;
@@ -297,18 +380,14 @@ void sytrd_lower(cudaStream_t st, int64_t n, double* A, int64_t lda, double* d, 
         symv_lower_latrd(sc, m, A + (c + 1) + (c + 1) * lda, lda, A + (c + 1) + c * lda,
                          wtmp.p + (c + 1), swork.p, lf, lt);
       const int64_t gw = (m + CRW - 1) / CRW;
-      launch_pdl(latrd_w_kernel, dim3((unsigned)gw), dim3(RT), 0, sc, n, A, lda, i0, c, i,
-                 (const double*)W.p, (int64_t)n, wtmp.p, (const double*)tvec.p,
-                 (const double*)tau, (const double*)scale_buf, part_wv.p);
+      if (!fusew)
+        launch_pdl(latrd_w_kernel, dim3((unsigned)gw), dim3(RT), 0, sc, n, A, lda, i0, c, i,
+                   (const double*)W.p, (int64_t)n, wtmp.p, (const double*)tvec.p,
+                   (const double*)tau, (const double*)scale_buf, part_wv.p);
       gw_prev = gw;
+      nvav_prev = fusew ? symv_tma_ctas(m) : 0;
     }
-    if (!last) {  // finish W[:, w-1] for the trailing update
-      const int64_t c = i0 + w;
-      const int64_t G = (n - c + CRW - 1) / CRW;
-      launch_pdl(latrd_col_kernel, dim3((unsigned)G), dim3(RT), 0, sc, n, A, lda, i0, c, w, 0,
-                 W.p, (int64_t)n, (const double*)wtmp.p, (const double*)part_wv.p, gw_prev,
-                 (const double*)tau, part_norm.p, dpart.p, alpha_buf, d);
-    }
+    if (!last) col_launch(i0 + w, w, 0);  // finish W[:, w-1] for the trailing update
     if (use_graph) {
       cudaGraph_t g = nullptr;
       EM_CK(cudaStreamEndCapture(sc, &g));

@@ -119,6 +119,8 @@ def main(which):
         out[f"trsm_{m}_TFps"] = m ** 3 / t / 1e12
     if which == "syev":
         m = int(os.environ.get("SYEV_N", n))
+        if "SYTRD_DBG" in os.environ:  # em_config debug key 98 (sytrd switches)
+            nat.check(lib.em_config(ctx, 98, int(os.environ["SYTRD_DBG"])))
         b = torch.randn(m, m, device="cuda", dtype=torch.float64, generator=g)
         a = (b + b.T).contiguous()
         del b
