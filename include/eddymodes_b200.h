@@ -55,9 +55,6 @@ int em_synchronize(em_ctx* ctx);
  * (dense -> band -> tridiagonal) reduction in em_syev/em_sygv (default INT64_MAX:
  * one-stage Householder everywhere). */
 #define EM_CFG_TWO_STAGE_MIN 1
-/* EM_CFG_SYTRD_FUSED: 1 = one persistent cooperative kernel per tridiagonalisation
- * panel (experimental), 0 (default) = per-column launches captured in a CUDA graph. */
-#define EM_CFG_SYTRD_FUSED 2
 int em_config(em_ctx* ctx, int key, int64_t value);
 /* Stage timers (CUDA events on the context stream). em_profile(ctx, 1) clears and
  * enables them; em_stage_times fills per-stage milliseconds / event-pair counts

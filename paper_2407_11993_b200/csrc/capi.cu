@@ -15,7 +15,6 @@ struct em_td1_plan;
 
 namespace em {
 extern int64_t g_two_stage_min;
-extern int g_latrd_dotr;
 extern int g_sytrd_dbg;
 void stages_reset(bool on);
 void stages_level(int level);
@@ -132,16 +131,9 @@ int em_config(em_ctx* ctx, int key, int64_t value) {
       em::g_two_stage_min = value;
       return EM_OK;
     }
-    if (key == 98) {  // debug: sytrd switches (bit0 no TMA symv, bit1 no PDL, bit2 no graph)
+    if (key == 98) {  // debug: sytrd switches (bit0 no TMA symv, bit1 no PDL, bit2 no graph,
+                      // bit3 the 4-launch column chain)
       em::g_sytrd_dbg = (int)value;
-      return EM_OK;
-    }
-    if (key == 99) {  // debug: rows per panel-dot chunk of the fused latrd
-      em::g_latrd_dotr = (int)value;
-      return EM_OK;
-    }
-    if (key == EM_CFG_SYTRD_FUSED) {
-      em::g_sytrd_fused = value != 0;
       return EM_OK;
     }
     throw em::ArgError{"unknown em_config key"};

@@ -75,10 +75,6 @@ int64_t symv_tma_ctas(int64_t n);
 // reflectors stored below the subdiagonal of A (LAPACK dsytrd convention).
 void sytrd_lower(cudaStream_t st, int64_t n, double* A, int64_t lda, double* d, double* e,
                  double* tau);
-// same result, one persistent cooperative kernel per panel (sytrd_fused.cu)
-void sytrd_lower_fused(cudaStream_t st, int64_t n, double* A, int64_t lda, double* d, double* e,
-                       double* tau);
-extern bool g_sytrd_fused;
 // ormtr: Z <- Q Z with Q = H(0) ... H(n-2) from sytrd_lower (Z n x m)
 void ormtr_lower(cudaStream_t st, int64_t n, int64_t m, const double* A, int64_t lda,
                  const double* tau, double* Z, int64_t ldz);

@@ -5,8 +5,8 @@
 //
 // Used by the Cholesky theta-method's per-step R * I product
 // (reference: td1_step_kernel's dense loop, _kernels.py:198-207) and exposed as
-// em_symv_lower; the tridiagonalisation runs the same tiles inside its fused
-// persistent kernel (sytrd_fused.cu).
+// em_symv_lower. This register-prefetch kernel is the fallback when TMA cannot address
+// the matrix (symv_tma.cu).
 #include <algorithm>
 
 #include "common.cuh"

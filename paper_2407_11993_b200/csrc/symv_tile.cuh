@@ -1,9 +1,6 @@
-// (No __restrict__ here: inside the fused kernel A, x and the partials are written by
-// other CTAs between grid barriers, so they must not go through the non-coherent
-// read-only path.)
 // Tile bodies of the lower-triangle symv (y = A x, A symmetric, only the lower
-// triangle read), shared by the standalone kernels (symv.cu) and the fused
-// persistent tridiagonalisation kernel (sytrd_fused.cu).
+// triangle read): the register-prefetch kernels of symv.cu and the tile body of the
+// TMA kernel (symv_tma.cu).
 //
 // Tile mapping: warp w owns columns 8w..8w+7 of a 64x64 tile, lane l rows l and
 // l+32 (every load instruction reads 256 contiguous bytes). The next tile is

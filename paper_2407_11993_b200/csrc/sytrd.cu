@@ -285,18 +285,13 @@ __global__ void restore_sub_kernel(int64_t n, double* A, int64_t lda, int64_t i0
   }
 }
 
-// em_config(EM_CFG_SYTRD_FUSED). The fused cooperative panel kernel (sytrd_fused.cu) is
-// experimental: slower than the graph path at N = 16k and not yet race-free; off.
-bool g_sytrd_fused = false;
+// em_config debug key 98 (tests): bit0 no TMA symv, bit1 no PDL, bit2 no graph,
+// bit3 the 4-launch column chain.
 int g_sytrd_dbg = 0;
 
 void sytrd_lower(cudaStream_t st, int64_t n, double* A, int64_t lda, double* d, double* e,
                  double* tau) {
   if (n <= 0) return;
-  if (g_sytrd_fused && n > 1) {
-    sytrd_lower_fused(st, n, A, lda, d, e, tau);
-    return;
-  }
   if (n == 1) {
     set_diag_kernel<<<1, 32, 0, st>>>(n, A, lda, 0, d);
     EM_LAUNCHED();
