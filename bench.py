@@ -326,6 +326,8 @@ def run_ours(args, cfg, rank, world, local_rank):
     nat.context()
     if args.two_stage is not None:
         nat.set_two_stage_min(args.two_stage)
+    if os.environ.get("EM_SYTRD_DBG"):  # A/B switch for the tridiagonalisation code paths
+        nat.check(nat.load_library().em_config(nat.context(), 98, int(os.environ["EM_SYTRD_DBG"])))
     m = build_inputs(cfg)
     n = m["plate"].n
     T, nth = cfg["steps"], len(cfg["thetas"])

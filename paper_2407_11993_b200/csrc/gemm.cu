@@ -239,12 +239,16 @@ __global__ void __launch_bounds__(GTHREADS, GMINB) gemm_grouped_kernel(const Gem
   if (p.m <= 0 || p.n <= 0) return;
   const int64_t tiles_m = (p.m + GBM - 1) / GBM;
   const int64_t tiles_n = (p.n + GBN - 1) / GBN;
+  // 16-byte copies when this problem's operands allow them (problem-uniform branch)
+  const bool vec = ((reinterpret_cast<uintptr_t>(p.A) | reinterpret_cast<uintptr_t>(p.B)) & 15) == 0 &&
+                   ((p.lda | p.ldb) & 1) == 0;
   for (int64_t b = blockIdx.x; b < tiles_m * tiles_n; b += gridDim.x) {
     const int64_t tm = b % tiles_m, tn = b / tiles_m;
-    if (p.k <= 0) {
-      // C = beta*C (alpha*0): handled by the tile with zero accumulators
-    }
-    gemm_tile<TA, TB, 0, 1>(p, tm * GBM, tn * GBN, smem);
+    // (k <= 0: C = beta C through the tile with zero accumulators)
+    if (vec)
+      gemm_tile<TA, TB, 0, 2>(p, tm * GBM, tn * GBN, smem);
+    else
+      gemm_tile<TA, TB, 0, 1>(p, tm * GBM, tn * GBN, smem);
     __syncthreads();
   }
 }

@@ -14,6 +14,9 @@
 #include <algorithm>
 #include <vector>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "ctx.h"
 #include "gemm.h"
@@ -713,6 +716,14 @@ void stedc(cudaStream_t st, int64_t n, double* d, double* e, double* Z, int64_t 
       probs.push_back(bot);
       max_tiles = std::max<int>(max_tiles, (int)(((n1 + 127) / 128) * ((K + 127) / 128)));
       max_tiles = std::max<int>(max_tiles, (int)(((n2 + 127) / 128) * ((K + 127) / 128)));
+    }
+    if (getenv("EM_DEBUG_STEDC")) {
+      double fl = 0.0;
+      for (auto& q : probs) fl += 2.0 * q.m * q.n * q.k;
+      int maxK = 0;
+      for (int k = 0; k < nm; ++k) maxK = std::max(maxK, hi[k].K);
+      fprintf(stderr, "stedc level %d: merges %d maxn %d maxK %d gemm_gflop %.1f\n", L, nm, maxn,
+              maxK, fl * 1e-9);
     }
     if (!probs.empty()) {
       DArr<GemmArgs> dp(probs.size(), st);
