@@ -40,6 +40,10 @@ CONFIGS = {
                n_sources=1, drive="tone10k"),
     "C2": dict(grid=(64, 64, 4), thetas=(1.0, 0.5), dt=5e-7, steps=10000, n_obs=32, n_ports=1,
                n_sources=0, drive="ramp5us"),
+    # configs[2]: N = 50,000 (L = 20 GB): 7 N^2 at the eigensolve peak on one B200, so the
+    # basis is formed without V^T R (not used by the transient; ModalBasis defers it)
+    "C3": dict(grid=(125, 100, 4), thetas=(0.5,), dt=2e-7, steps=100000, n_obs=64, n_ports=1,
+               n_sources=1, drive="tone50k", vtr=False),
 }
 
 
@@ -136,7 +140,8 @@ class DeviceStep:
         self.n_p, self.n_s = n_p, n_s
         self.nd = 2 * n_p + n_s
         self.tau, self.ln, self.rn = nat.empty(n), nat.empty(n), nat.empty(n)
-        self.V, self.VtR = nat.empty(n, n), nat.empty(n, n)
+        self.V = nat.empty(n, n)
+        self.VtR = nat.empty(n, n) if cfg.get("vtr", True) else None
         cols = []
         if n_p:
             cols += [m["r_d"], m["l_d"]]
@@ -156,7 +161,8 @@ class DeviceStep:
         piv, which = ctypes.c_int64(-1), ctypes.c_int(-1)
         nat.check(lib.em_sygv(ctx, n, nat.ptr(self.m["l_i"]), n, nat.ptr(self.m["r_i"]), n,
                               nat.ptr(self.tau), nat.ptr(self.V), n, nat.ptr(self.ln),
-                              nat.ptr(self.rn), nat.ptr(self.VtR), n, ctypes.byref(piv),
+                              nat.ptr(self.rn), nat.ptr(self.VtR) if self.VtR is not None else None,
+                              n, ctypes.byref(piv),
                               ctypes.byref(which)), "em_sygv")
         if self.nd:
             nat.check(lib.em_dgemm(ctx, 1, 0, n, self.nd, n, 1.0, nat.ptr(self.V), n,
@@ -363,11 +369,23 @@ def run_ours(args, cfg, rank, world, local_rank):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_max = float(tt.item())
     value = world * units * args.steps / t_max
+    if args.profile_fine:
+        nat.profile(2)
+        step()
+        fine = nat.stage_times()
+        nat.profile(0)
+        log(json.dumps({"fine_stage_ms": {k: [round(v[0], 3), v[1]] for k, v in fine.items()}}))
+    del step  # its V (and V^T R) buffers: the e2e arm allocates its own
+    torch.cuda.empty_cache()
 
     # ---- e2e through the public API with host buffers
     e2e = None
     if not args.no_e2e:
         es = E2EStep(m, cfg)
+        # the e2e arm uploads its own L, R from the pinned host copies: drop the
+        # device-resident ones meanwhile (C3: 7 N^2 of 9 available at the eigensolve peak)
+        m["l_i"] = m["r_i"] = None
+        torch.cuda.empty_cache()
         es()
         torch.cuda.synchronize()
         barrier()
@@ -385,6 +403,8 @@ def run_ours(args, cfg, rank, world, local_rank):
                "h2d_bytes_per_step": es.h2d, "d2h_bytes_per_step": es.d2h,
                "ms_per_step": te / args.e2e_steps * 1e3, "steps": args.e2e_steps,
                "timer": "host wall clock around the public-API calls (includes H2D/D2H)"}
+        m["l_i"] = es.pinned[0].to("cuda", non_blocking=False)
+        m["r_i"] = es.pinned[1].to("cuda", non_blocking=False)
         del es
 
     peaks = load_peaks()
@@ -403,12 +423,6 @@ def run_ours(args, cfg, rank, world, local_rank):
 
     # ---- TD1 comparator (bounded: a few hundred steps, extrapolated) and CPU baseline
     extra = {}
-    if args.profile_fine:
-        nat.profile(2)
-        step()
-        fine = nat.stage_times()
-        nat.profile(0)
-        log(json.dumps({"fine_stage_ms": {k: [round(v[0], 3), v[1]] for k, v in fine.items()}}))
     if rank == 0 and not args.no_td1:
         extra["td1_comparator"] = td1_comparator(m, cfg, args.td1_steps)
         extra["td1_comparator"]["modal_vs_cholesky_end_to_end"] = (
@@ -428,7 +442,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                                    f"{cfg['n_obs']} observables",
                        "N": n, "T": T, "thetas": list(cfg["thetas"]), "n_obs": cfg["n_obs"],
                        "mode_steps_per_step": units,
-                       "l2": "inputs larger than L2 (L, R 2.1 GB each at C2)",
+                       "l2": f"inputs larger than L2 (L, R {8 * n * n / 1e9:.1f} GB each)",
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
             "e2e": e2e,
             "gpu_launches": int(launches),

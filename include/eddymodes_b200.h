@@ -77,6 +77,12 @@ int em_dgemm(em_ctx* ctx, int trans_a, int trans_b, int64_t m, int64_t n, int64_
 int em_symv_lower(em_ctx* ctx, int64_t n, double alpha, const double* A, int64_t lda,
                   const double* x, double beta, double* y);
 
+/* C (n x m) = A B for a symmetric A in full storage: the products R V behind
+ * modal.py:80-81 (r_n, V^T R) and modal.to_modal (modal.py:84-91). Through a device CSR
+ * copy of A when it has few nonzeros (the stencil R), else the DMMA GEMM. */
+int em_sym_mm(em_ctx* ctx, int64_t n, int64_t m, const double* A, int64_t lda, const double* B,
+              int64_t ldb, double* C, int64_t ldc);
+
 /* Mirror the lower triangle into the upper one in place (linalg.py:34-41 SymMatrix). */
 int em_sym_mirror_lower(em_ctx* ctx, int64_t n, double* A, int64_t lda);
 

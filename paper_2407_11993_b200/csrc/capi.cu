@@ -165,6 +165,16 @@ int em_symv_lower(em_ctx* ctx, int64_t n, double alpha, const double* A, int64_t
   });
 }
 
+int em_sym_mm(em_ctx* ctx, int64_t n, int64_t m, const double* A, int64_t lda, const double* B,
+              int64_t ldb, double* C, int64_t ldc) {
+  return guarded(ctx, [&] {
+    if (n < 0 || m < 0) throw em::ArgError{"bad em_sym_mm sizes"};
+    if (!em::sym_sparse_mm(ctx->stream, n, A, lda, m, B, ldb, C, ldc, 0.02))
+      EM_CK(em::gemm(ctx->stream, false, false, n, m, n, 1.0, A, lda, B, ldb, 0.0, C, ldc));
+    return EM_OK;
+  });
+}
+
 int em_sym_mirror_lower(em_ctx* ctx, int64_t n, double* A, int64_t lda) {
   return guarded(ctx, [&] {
     em::mirror_lower(ctx->stream, n, A, lda);

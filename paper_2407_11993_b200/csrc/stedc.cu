@@ -439,10 +439,37 @@ __global__ void dc_gather_kernel(const int64_t* __restrict__ moff, const int* __
   const int64_t off = moff[mi];
   const int n = mn[mi];
   const int K = info[mi].K;
-  for (int i = blockIdx.y; i < K; i += gridDim.y) {
-    const int64_t sc = off + w.src[off + i], dc = off + w.pos[off + i];
+  // non-deflated columns to their type-grouped GEMM positions 0..K-1, deflated ones
+  // (in ascending-value order) behind them at K..n-1, so that Q is free for the GEMM
+  // output afterwards
+  for (int i = blockIdx.y; i < n; i += gridDim.y) {
+    int64_t sc, dc;
+    if (i < K) {
+      sc = off + w.src[off + i];
+      dc = off + w.pos[off + i];
+    } else {
+      sc = off + w.dcol[off + (i - K)];
+      dc = off + i;
+    }
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
       Q2[(off + r) + dc * ldq] = Q[(off + r) + sc * ldq];
+  }
+}
+
+// Deflated columns K..n-1 back next to the GEMM output (same block-local columns).
+__global__ void dc_copy_deflated_kernel(const int64_t* __restrict__ moff,
+                                        const int* __restrict__ mn,
+                                        const MergeInfo* __restrict__ info,
+                                        const double* __restrict__ Q2, double* __restrict__ Q,
+                                        int64_t ldq) {
+  const int mi = blockIdx.z;
+  const int64_t off = moff[mi];
+  const int n = mn[mi];
+  const int K = info[mi].K;
+  for (int i = K + blockIdx.y; i < n; i += gridDim.y) {
+    const int64_t c = off + i;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
+      Q[(off + r) + c * ldq] = Q2[(off + r) + c * ldq];
   }
 }
 
@@ -463,22 +490,24 @@ __global__ void dc_order_kernel(const int64_t* __restrict__ moff, const int* __r
       ++a;
     } else {
       lam_out[off + t] = w.dval[off + b];
-      w.perm[off + t] = -1 - w.dcol[off + b];  // < 0: deflated source column
+      w.perm[off + t] = -1 - b;  // < 0: deflated entry b (column K + b after the gather)
       ++b;
     }
   }
 }
 
+// Qout column t <- Q column p (new eigenvector p) or K + b (deflated entry b).
 __global__ void dc_place_kernel(const int64_t* __restrict__ moff, const int* __restrict__ mn,
-                                DcWork w, const double* __restrict__ Qnew,
-                                const double* __restrict__ Qold, double* __restrict__ Qout,
+                                const MergeInfo* __restrict__ info, DcWork w,
+                                const double* __restrict__ Q, double* __restrict__ Qout,
                                 int64_t ldq) {
   const int mi = blockIdx.z;
   const int64_t off = moff[mi];
   const int n = mn[mi];
+  const int K = info[mi].K;
   for (int t = blockIdx.y; t < n; t += gridDim.y) {
     const int p = w.perm[off + t];
-    const double* src = (p >= 0) ? Qnew + (off + p) * ldq : Qold + (off + (-1 - p)) * ldq;
+    const double* src = Q + (off + ((p >= 0) ? p : K + (-1 - p))) * ldq;
     double* dst = Qout + (off + t) * ldq;
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
       dst[off + r] = src[off + r];
@@ -579,7 +608,7 @@ void stedc(cudaStream_t st, int64_t n, double* d, double* e, double* Z, int64_t 
   }
   // buffers (all eigenvector buffers use ld = n)
   DBuf lam(n, st), lam2(n, st);
-  DBuf Qb((size_t)n * n, st), Qz, Ub, Qn;
+  DBuf Qb((size_t)n * n, st), Qz, Ub;
   double* B0 = Z;
   if (ldz != n) {
     Qz.alloc((size_t)n * n, st);
@@ -608,7 +637,6 @@ void stedc(cudaStream_t st, int64_t n, double* d, double* e, double* Z, int64_t 
   if (levels.size() > 1) {
     EM_CK(cudaMemsetAsync(Qb.p, 0, (size_t)n * n * sizeof(double), st));
     Ub.alloc((size_t)n * n, st);
-    Qn.alloc((size_t)n * n, st);
   }
   // workspace
   DBuf wd((size_t)n * 10, st);
@@ -696,7 +724,9 @@ void stedc(cudaStream_t st, int64_t n, double* d, double* e, double* Z, int64_t 
       dim3 g2((unsigned)((maxK + 7) / 8), (unsigned)nm);
       dc_umat_kernel<<<g2, 256, 0, st>>>(dmo.p, minfo.p, w, Ub.p, n);
       EM_LAUNCHED();
-      dim3 g3((unsigned)std::max(1, std::min((maxn + 255) / 256, 8)), (unsigned)std::min(maxK, 65535), (unsigned)nm);
+    }
+    {
+      dim3 g3((unsigned)std::max(1, std::min((maxn + 255) / 256, 8)), (unsigned)std::min(maxn, 65535), (unsigned)nm);
       dc_gather_kernel<<<g3, 256, 0, st>>>(dmo.p, dmn.p, minfo.p, w, Qcur, Qalt, n);
       EM_LAUNCHED();
     }
@@ -709,9 +739,9 @@ void stedc(cudaStream_t st, int64_t n, double* d, double* e, double* Z, int64_t 
       const int64_t off = mo[k];
       const int64_t n1 = m1[k], n2 = mnn[k] - n1;
       GemmArgs top{n1, K, c1 + c2, Qalt + off + off * n, n, Ub.p + off + off * n, n,
-                   Qn.p + off + off * n, n, 1.0, 0.0, 0};
+                   Qcur + off + off * n, n, 1.0, 0.0, 0};
       GemmArgs bot{n2, K, K - c1, Qalt + (off + n1) + (off + c1) * n, n,
-                   Ub.p + (off + c1) + off * n, n, Qn.p + (off + n1) + off * n, n, 1.0, 0.0, 0};
+                   Ub.p + (off + c1) + off * n, n, Qcur + (off + n1) + off * n, n, 1.0, 0.0, 0};
       probs.push_back(top);
       probs.push_back(bot);
       max_tiles = std::max<int>(max_tiles, (int)(((n1 + 127) / 128) * ((K + 127) / 128)));
@@ -738,8 +768,11 @@ void stedc(cudaStream_t st, int64_t n, double* d, double* e, double* Z, int64_t 
     EM_LAUNCHED();
     {
       dim3 g((unsigned)std::max(1, std::min((maxn + 255) / 256, 8)), (unsigned)std::min(maxn, 65535), (unsigned)nm);
-      // place into Qalt (free after the GEMM), then swap roles
-      dc_place_kernel<<<g, 256, 0, st>>>(dmo.p, dmn.p, w, Qn.p, Qcur, Qalt, n);
+      // deflated columns next to the GEMM output in Qcur, then everything placed in
+      // final order into Qalt (free after the GEMM) and the roles swapped
+      dc_copy_deflated_kernel<<<g, 256, 0, st>>>(dmo.p, dmn.p, minfo.p, Qalt, Qcur, n);
+      EM_LAUNCHED();
+      dc_place_kernel<<<g, 256, 0, st>>>(dmo.p, dmn.p, minfo.p, w, Qcur, Qalt, n);
       EM_LAUNCHED();
     }
     // blocks not merged at this level (leaf-sized nodes carried up) keep their data:

@@ -41,16 +41,10 @@ void syev_ascending(cudaStream_t st, int64_t n, double* A, int64_t lda, double* 
   EM_CK(cudaMemcpyAsync(w, d.p, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
 }
 
-// V[:, j] = s_j * Z[:, n-1-j], s_j = sign of the first largest-|.| entry; tau[j] = w[n-1-j]
-__global__ void finalize_modes_kernel(int64_t n, const double* __restrict__ Z, int64_t ldz,
-                                      const double* __restrict__ w, double* __restrict__ V,
-                                      int64_t ldv, double* __restrict__ tau) {
-  __shared__ double bv[32];
-  __shared__ int64_t bi[32];
-  __shared__ double sgn;
-  const int64_t j = blockIdx.x;
-  const int64_t src = n - 1 - j;
-  const double* z = Z + src * ldz;
+// Column sign of np.argmax semantics: s = sign of the first largest-|.| entry of z
+// (0 -> +1, modal.py:76-77). Block-wide; every thread returns the sign.
+EM_DEVINL double column_sign(int64_t n, const double* __restrict__ z, double* bv, int64_t* bi,
+                             double* sgn) {
   double best = -1.0;
   int64_t idx = 0;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
@@ -82,13 +76,41 @@ __global__ void finalize_modes_kernel(int64_t n, const double* __restrict__ Z, i
         b = bv[q];
         k = bi[q];
       }
-    const double v = z[k];
-    sgn = (v < 0.0) ? -1.0 : 1.0;  // np.sign, with 0 -> +1 (modal.py:76-77)
-    tau[j] = w[src];
+    *sgn = (z[k] < 0.0) ? -1.0 : 1.0;
   }
   __syncthreads();
-  const double s = sgn;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) V[i + j * ldv] = s * z[i];
+  const double s = *sgn;
+  __syncthreads();  // bv/bi/sgn reusable
+  return s;
+}
+
+// In place on the eigenvector buffer: V[:, j] = s * Z[:, n-1-j] (descending order,
+// sign fix), tau[j] = w[n-1-j]. Block j swaps the column pair (j, n-1-j), so no
+// second N x N buffer is needed.
+__global__ void finalize_modes_inplace_kernel(int64_t n, double* __restrict__ V, int64_t ldv,
+                                              const double* __restrict__ w,
+                                              double* __restrict__ tau) {
+  __shared__ double bv[32];
+  __shared__ int64_t bi[32];
+  __shared__ double sgn;
+  const int64_t j = blockIdx.x, k = n - 1 - j;
+  double* zj = V + j * ldv;
+  double* zk = V + k * ldv;
+  const double sj = column_sign(n, zj, bv, bi, &sgn);  // lands in column k
+  const double sk = column_sign(n, zk, bv, bi, &sgn);  // lands in column j
+  if (threadIdx.x == 0) {
+    tau[j] = w[k];
+    tau[k] = w[j];
+  }
+  if (j == k) {
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) zj[i] *= sj;
+    return;
+  }
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const double a = zj[i], b = zk[i];
+    zj[i] = sk * b;
+    zk[i] = sj * a;
+  }
 }
 
 // out[j] = sum_i V[i,j] * X[i,j]
@@ -152,7 +174,6 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
   }
   DBuf B(nn, st);
   {
-    DBuf X(nn, st);
     {
       // B = G^-1 L G^-T. The reference forms G^-1 (G^-1 L)^T with two full solves and
       // averages it with its transpose (modal.py:63-67); the two-sided recursive
@@ -162,31 +183,33 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
       mirror_lower(st, n, B.p, n);  // SymMatrix semantics: the lower triangle defines L
       sygst_lower(st, n, B.p, n, G.p, n, GDinv.p);
     }
-    // certificate only (modal.py:69-70)
+    // certificate only (modal.py:69-70), factored in the (still free) output buffer V
     {
       Stage s(st, ST_POTRF_L);
-      copy_matrix(st, false, n, n, L, ldl, X.p, n);
-      piv = potrf(st, n, X.p, n);
+      copy_matrix(st, false, n, n, L, ldl, V, ldv);
+      piv = potrf(st, n, V, ldv);
     }
     if (piv >= 0) {
       *which = 1;
       return piv;
     }
   }
-  DBuf w(n, st), Z(nn, st);
-  syev_ascending(st, n, B.p, n, w.p, Z.p, n);
+  // eigenvectors are formed directly in the output buffer V (D&C, ormtr, back-transform,
+  // then the in-place descending reorder + sign fix): peak memory L, R, V + G, B and the
+  // two D&C work matrices = 7 N^2 (8 with V^T R), so N = 50,000 fits one B200
+  DBuf w(n, st);
+  syev_ascending(st, n, B.p, n, w.p, V, ldv);
   B.release();
   {
     Stage s(st, ST_TRSM_BACK);
-    trsm_lower(st, true, n, n, G.p, n, Z.p, n, GDinv.p);     // V = G^-T U
+    trsm_lower(st, true, n, n, G.p, n, V, ldv, GDinv.p);     // V = G^-T U
   }
   G.release();
   {
     Stage s(st, ST_FINALIZE);
-    finalize_modes_kernel<<<(unsigned)n, 256, 0, st>>>(n, Z.p, n, w.p, V, ldv, tau);
+    finalize_modes_inplace_kernel<<<(unsigned)((n + 1) / 2), 256, 0, st>>>(n, V, ldv, w.p, tau);
     EM_LAUNCHED();
   }
-  Z.release();
   Stage post(st, ST_POST_GEMM);
   if (l_n) {
     // l_n = diag(V^T L V) (modal.py:79) through the lower triangle of L only (the

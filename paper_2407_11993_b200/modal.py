@@ -30,10 +30,10 @@ class ModalBasis:
     inductance / resistance; vt_r: V^T R_i.
     """
 
-    __slots__ = ("_v", "_vt_r", "tau", "l_n", "r_n", "_v_dev", "_vtr_dev", "_frozen")
+    __slots__ = ("_v", "_vt_r", "tau", "l_n", "r_n", "_v_dev", "_vtr_dev", "_r_dev", "_frozen")
 
     def __init__(self, v=None, tau=None, l_n=None, r_n=None, vt_r=None, *, v_dev=None,
-                 vtr_dev=None):
+                 vtr_dev=None, r_dev=None):
         object.__setattr__(self, "_v", None if v is None else np.asarray(v, dtype=float))
         object.__setattr__(self, "_vt_r", None if vt_r is None else np.asarray(vt_r, dtype=float))
         object.__setattr__(self, "tau", np.asarray(tau, dtype=float))
@@ -41,6 +41,8 @@ class ModalBasis:
         object.__setattr__(self, "r_n", np.asarray(r_n, dtype=float))
         object.__setattr__(self, "_v_dev", v_dev)
         object.__setattr__(self, "_vtr_dev", vtr_dev)
+        # device R_i kept for a deferred V^T R (large n: not formed during the eigensolve)
+        object.__setattr__(self, "_r_dev", r_dev)
         object.__setattr__(self, "_frozen", True)
 
     def __setattr__(self, key, value):
@@ -63,7 +65,7 @@ class ModalBasis:
             n = self.n_modes
             # the device buffer is R V column-major == V^T R row-major
             object.__setattr__(self, "_vt_r",
-                               np.ascontiguousarray(self._vtr_dev.reshape(n, n).cpu().numpy()))
+                               np.ascontiguousarray(self.vtr_dev.reshape(n, n).cpu().numpy()))
         return self._vt_r
 
     # device views -------------------------------------------------------------
@@ -77,6 +79,14 @@ class ModalBasis:
     @property
     def vtr_dev(self):
         """R V column-major on the device (== V^T R row-major)."""
+        if self._vtr_dev is None and self._r_dev is not None:
+            n = self.n_modes
+            rv = nat.empty(n, n)
+            nat.check(nat.load_library().em_sym_mm(nat.context(), n, n, nat.ptr(self._r_dev), n,
+                                                   nat.ptr(self.v_dev), n, nat.ptr(rv), n),
+                      "em_sym_mm")
+            object.__setattr__(self, "_vtr_dev", rv)
+            object.__setattr__(self, "_r_dev", None)
         if self._vtr_dev is None:
             object.__setattr__(self, "_vtr_dev", nat.device_vector(
                 np.ascontiguousarray(self._vt_r).reshape(-1)).reshape(self.n_modes,
@@ -88,8 +98,13 @@ def _host_square(a) -> np.ndarray:
     return a.full if isinstance(a, linalg.SymMatrix) else np.asarray(a, dtype=float)
 
 
-def generalized_eig(l_i, r_i) -> ModalBasis:
+def generalized_eig(l_i, r_i, *, vt_r: str = "auto") -> ModalBasis:
     """Solve L_i V = tau R_i V for an SPD pair (modal.py:46-81).
+
+    vt_r: "eager" forms V^T R_i inside the eigensolve (as the reference does),
+    "lazy" defers it to the first access of ModalBasis.vt_r / vtr_dev (one fewer
+    N x N buffer at the eigensolve's memory peak), "auto" is eager while the device
+    has room for it.
 
     Raises NotPositiveDefinite("modal resistance matrix" / "modal inductance
     matrix") with the failing pivot, in the reference's order."""
@@ -116,19 +131,27 @@ def generalized_eig(l_i, r_i) -> ModalBasis:
         rd = nat.device_symmetric(rm) if isinstance(r_i, linalg.SymMatrix) else \
             nat.device_colmajor(rm)
     ctx = nat.context()
+    if vt_r not in ("auto", "eager", "lazy"):
+        raise ValueError("vt_r must be 'auto', 'eager' or 'lazy'")
+    if vt_r == "auto":
+        free = t.cuda.mem_get_info()[0]
+        # V, V^T R and the eigensolver's own G, B, two D&C matrices + slack
+        vt_r = "eager" if 7.5 * 8.0 * n * n < free else "lazy"
     tau, ln, rn = nat.empty(n), nat.empty(n), nat.empty(n)
-    v, vtr = nat.empty(n, n), nat.empty(n, n)
+    v = nat.empty(n, n)
+    vtr = nat.empty(n, n) if vt_r == "eager" else None
     piv = ctypes.c_int64(-1)
     which = ctypes.c_int(-1)
     rc = nat.load_library().em_sygv(ctx, n, nat.ptr(ld), n, nat.ptr(rd), n, nat.ptr(tau),
-                                    nat.ptr(v), n, nat.ptr(ln), nat.ptr(rn), nat.ptr(vtr), n,
+                                    nat.ptr(v), n, nat.ptr(ln), nat.ptr(rn),
+                                    None if vtr is None else nat.ptr(vtr), n,
                                     ctypes.byref(piv), ctypes.byref(which))
     if rc == nat.EM_ERR_NOT_PD:
         what = "modal resistance matrix" if which.value == 0 else "modal inductance matrix"
         raise NotPositiveDefinite(int(piv.value), what)
     nat.check(rc, "em_sygv")
     return ModalBasis(tau=tau.cpu().numpy(), l_n=ln.cpu().numpy(), r_n=rn.cpu().numpy(),
-                      v_dev=v, vtr_dev=vtr)
+                      v_dev=v, vtr_dev=vtr, r_dev=rd if vtr is None else None)
 
 
 def _gemv(a_dev, trans: int, n: int, x: np.ndarray) -> np.ndarray:

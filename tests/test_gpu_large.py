@@ -1,0 +1,73 @@
+"""Large-order eigensolve on the device: N = 46,400 > 46,341, so N^2 exceeds 2^31 and
+every N x N index in the eigensolver must be 64-bit. Checked through properties that
+do not need a CPU eigensolve at this size (LAPACK would take hours):
+R-orthonormality V^T R V = I, the residual L V - R V diag(tau), descending order,
+the sign convention (largest-|.| entry positive, modal.py:74-78), l_n = diag(V^T L V)
+and r_n = diag(V^T R V). Also covers the memory-lean buffer plan (eigenvectors formed
+in the output buffer, no V^T R) that lets C3 (N = 50,000) fit one B200.
+
+The residual/Gram products use torch matmul: test infrastructure, not the product."""
+import ctypes
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def test_lazy_vt_r_matches_eager():
+    from paper_2407_11993_b200.linalg import SymMatrix
+    from paper_2407_11993_b200.modal import generalized_eig
+    from tests.conftest import golden
+    g = golden("plate_200")
+    a = generalized_eig(SymMatrix(g["l_i"]), SymMatrix(g["r_i"]), vt_r="eager")
+    b = generalized_eig(SymMatrix(g["l_i"]), SymMatrix(g["r_i"]), vt_r="lazy")
+    assert np.array_equal(a.tau, b.tau)
+    assert np.array_equal(a.v, b.v)
+    np.testing.assert_allclose(b.vt_r, a.vt_r, rtol=0, atol=1e-13 * np.abs(a.vt_r).max())
+
+
+def test_eigensolve_beyond_int32_squared():
+    import torch
+    from paper_2407_11993_b200 import _native as nat
+    from paper_2407_11993_b200.synth import device_plate_model
+    free = torch.cuda.mem_get_info()[0]
+    m = device_plate_model(116, 100, 4, n_ports=0, n_sources=0, n_obs=1)
+    L, R = m["l_i"], m["r_i"]
+    n = L.shape[0]
+    assert n * n > 2 ** 31
+    if free < 7.5 * 8.0 * n * n:
+        pytest.skip("device too small for the 7 N^2 eigensolve at N = 46,400")
+    lib, ctx = nat.load_library(), nat.context()
+    tau, ln, rn = nat.empty(n), nat.empty(n), nat.empty(n)
+    V = nat.empty(n, n)
+    piv, which = ctypes.c_int64(-1), ctypes.c_int(-1)
+    nat.check(lib.em_sygv(ctx, n, nat.ptr(L), n, nat.ptr(R), n, nat.ptr(tau), nat.ptr(V), n,
+                          nat.ptr(ln), nat.ptr(rn), None, n, ctypes.byref(piv),
+                          ctypes.byref(which)), "em_sygv")
+    torch.cuda.synchronize()
+    # column-major V: row j of the torch tensor is mode j
+    Vt = V
+    assert bool(torch.all(tau[1:] <= tau[:-1]))
+    assert bool(torch.all(tau > 0))
+    # sign convention on every mode
+    idx = Vt.abs().argmax(dim=1)
+    assert bool(torch.all(Vt.gather(1, idx[:, None]) > 0))
+    worst_gram = worst_res = 0.0
+    lnorm = torch.linalg.matrix_norm(L).item()
+    cb = 4096
+    for c0 in range(0, n, cb):
+        blk = Vt[c0:c0 + cb]                  # (b, n): modes c0.. as rows
+        rv = blk @ R                           # (R v)^T, R symmetric
+        gram = rv @ Vt.T                       # (b, n) block of V^T R V
+        gram[:, c0:c0 + cb] -= torch.eye(blk.shape[0], device=gram.device, dtype=gram.dtype)
+        worst_gram = max(worst_gram, gram.abs().max().item())
+        lv = blk @ L
+        res = lv - tau[c0:c0 + cb, None] * rv
+        worst_res = max(worst_res, torch.linalg.norm(res, dim=1).max().item())
+        # l_n, r_n against the direct quadratic forms
+        torch.testing.assert_close(ln[c0:c0 + cb], (lv * blk).sum(dim=1), rtol=1e-10, atol=0)
+        torch.testing.assert_close(rn[c0:c0 + cb], (rv * blk).sum(dim=1), rtol=1e-10, atol=0)
+        del rv, gram, lv, res
+    assert worst_gram < 1e-9, worst_gram
+    assert worst_res < 1e-9 * lnorm, (worst_res, lnorm)
