@@ -44,6 +44,11 @@ CONFIGS = {
     # basis is formed without V^T R (not used by the transient; ModalBasis defers it)
     "C3": dict(grid=(125, 100, 4), thetas=(0.5,), dt=2e-7, steps=100000, n_obs=64, n_ports=1,
                n_sources=1, drive="tone50k", vtr=False),
+    # configs[4]: N = 60,000, 64 independent source waveforms as 64 right-hand sides
+    # (the excitation sweep, em_td2_run_sweep); eigensolve at 6 N^2 (R as its own factor
+    # workspace, no V^T R) on one B200
+    "C5": dict(grid=(150, 100, 4), thetas=(0.5,), dt=2e-7, steps=100000, n_obs=64, n_ports=0,
+               n_sources=64, drive="batched", vtr=False, sweep=True),
 }
 
 
@@ -116,7 +121,7 @@ def build_inputs(cfg):
     m = synth.device_plate_model(nx, ny, nz, n_ports=cfg["n_ports"], n_sources=cfg["n_sources"],
                                  n_obs=cfg["n_obs"])
     i_d, i0 = synth.drive_table(cfg["drive"], cfg["steps"], cfg["dt"], cfg["n_ports"],
-                                cfg["n_sources"])
+                                cfg["n_sources"], plate=m["plate"])
     table = np.ascontiguousarray(np.concatenate([i_d, i0], axis=1))
     m["i_d"], m["i0"], m["table"] = i_d, i0, table
     m["table_dev"] = nat.device_vector(table.reshape(-1)) if table.size else nat.zeros(1)
@@ -151,19 +156,21 @@ class DeviceStep:
         self.drv = t.cat(cols, dim=0).contiguous() if cols else nat.zeros(1, n)
         self.P = nat.empty(max(self.nd, 1), n)
         self.CV = nat.empty(n, cfg["n_obs"])
-        self.Y = [nat.empty(cfg["steps"], cfg["n_obs"]) for _ in cfg["thetas"]]
-        self.q = nat.empty(n)
+        self.n_rhs = (n_p + n_s) if cfg.get("sweep") else 1
+        self.Y = [nat.empty(self.n_rhs, cfg["steps"], cfg["n_obs"]) for _ in cfg["thetas"]]
+        self.q = nat.empty(self.n_rhs, n)
 
     def __call__(self):
         import ctypes
         nat, lib, ctx = self.nat, self.nat.load_library(), self.nat.context()
         n, cfg = self.n, self.cfg
         piv, which = ctypes.c_int64(-1), ctypes.c_int(-1)
-        nat.check(lib.em_sygv(ctx, n, nat.ptr(self.m["l_i"]), n, nat.ptr(self.m["r_i"]), n,
-                              nat.ptr(self.tau), nat.ptr(self.V), n, nat.ptr(self.ln),
-                              nat.ptr(self.rn), nat.ptr(self.VtR) if self.VtR is not None else None,
-                              n, ctypes.byref(piv),
-                              ctypes.byref(which)), "em_sygv")
+        # R (stencil) doubles as the factor workspace and is restored from its CSR copy
+        nat.check(lib.em_sygv_ex(ctx, n, nat.ptr(self.m["l_i"]), n, nat.ptr(self.m["r_i"]), n,
+                                 nat.ptr(self.tau), nat.ptr(self.V), n, nat.ptr(self.ln),
+                                 nat.ptr(self.rn),
+                                 nat.ptr(self.VtR) if self.VtR is not None else None, n, 1,
+                                 ctypes.byref(piv), ctypes.byref(which)), "em_sygv_ex")
         if self.nd:
             nat.check(lib.em_dgemm(ctx, 1, 0, n, self.nd, n, 1.0, nat.ptr(self.V), n,
                                    nat.ptr(self.drv), n, 0.0, nat.ptr(self.P), n), "em_dgemm")
@@ -182,8 +189,14 @@ class DeviceStep:
             nat.check(lib.em_td2_set_observables(plan, n_obs, nat.ptr(self.CV), n_obs, None, 0),
                       "em_td2_set_observables")
             self.q.zero_()
-            nat.check(lib.em_td2_run(plan, cfg["steps"], nat.ptr(self.m["table_dev"]),
-                                     nat.ptr(self.q), nat.ptr(self.Y[k]), 1, None), "em_td2_run")
+            if cfg.get("sweep"):
+                nat.check(lib.em_td2_run_sweep(plan, cfg["steps"], nat.ptr(self.m["table_dev"]),
+                                               nat.ptr(self.q), nat.ptr(self.Y[k]), 1),
+                          "em_td2_run_sweep")
+            else:
+                nat.check(lib.em_td2_run(plan, cfg["steps"], nat.ptr(self.m["table_dev"]),
+                                         nat.ptr(self.q), nat.ptr(self.Y[k]), 1, None),
+                          "em_td2_run")
             lib.em_td2_plan_destroy(plan)
 
 
@@ -221,7 +234,8 @@ class E2EStep:
         n_obs = cfg["n_obs"]
         self.h2d = 8 * (2 * n * n + n * (2 * cfg["n_ports"] + cfg["n_sources"]) +
                         len(cfg["thetas"]) * (self.i_d.size + self.i0.size + n_obs * n))
-        self.d2h = 8 * (3 * n + len(cfg["thetas"]) * cfg["steps"] * n_obs)
+        n_rhs = (cfg["n_ports"] + cfg["n_sources"]) if cfg.get("sweep") else 1
+        self.d2h = 8 * (3 * n + len(cfg["thetas"]) * cfg["steps"] * n_obs * n_rhs)
         self.out = None
 
     def __call__(self):
@@ -231,8 +245,13 @@ class E2EStep:
         ys = []
         for th in cfg["thetas"]:
             st = transient.Td2Stepper(self.rm, basis, cfg["dt"], th)
-            _, y, _ = st.run(self.i_d, self.i0, capture_state=False, observables=(self.c, None))
+            if cfg.get("sweep"):
+                y, _ = st.run_sweep(self.i_d, self.i0, observables=(self.c, None))
+            else:
+                _, y, _ = st.run(self.i_d, self.i0, capture_state=False,
+                                 observables=(self.c, None))
             ys.append(y)
+            del st
         self.out = (basis.tau, ys)
 
 
@@ -337,7 +356,8 @@ def run_ours(args, cfg, rank, world, local_rank):
     m = build_inputs(cfg)
     n = m["plate"].n
     T, nth = cfg["steps"], len(cfg["thetas"])
-    units = n * T * nth
+    n_rhs = (cfg["n_ports"] + cfg["n_sources"]) if cfg.get("sweep") else 1
+    units = n * T * nth * n_rhs
     step = DeviceStep(m, cfg)
     for _ in range(args.warmup):
         step()
@@ -424,7 +444,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     # ---- TD1 comparator (bounded: a few hundred steps, extrapolated) and CPU baseline
     extra = {}
     if rank == 0 and not args.no_td1:
-        extra["td1_comparator"] = td1_comparator(m, cfg, args.td1_steps)
+        extra["td1_comparator"] = td1_comparator(m, cfg, args.td1_steps, n_rhs)
         extra["td1_comparator"]["modal_vs_cholesky_end_to_end"] = (
             extra["td1_comparator"]["extrapolated_total_s"] / (t_max / args.steps))
     cpu = None
@@ -438,8 +458,11 @@ def run_ours(args, cfg, rank, world, local_rank):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded plate generator, SURVEY.md §8(d))",
             "config": {"workload": f"{args.config}: N={n} plate {cfg['grid']}, eigensolve + "
-                                   f"{T} TD2 steps x theta {list(cfg['thetas'])}, "
-                                   f"{cfg['n_obs']} observables",
+                                   f"{T} TD2 steps x theta {list(cfg['thetas'])}"
+                                   + (f" x {n_rhs} right-hand sides (excitation sweep)"
+                                      if n_rhs > 1 else "")
+                                   + f", {cfg['n_obs']} observables",
+                       "n_rhs": n_rhs,
                        "N": n, "T": T, "thetas": list(cfg["thetas"]), "n_obs": cfg["n_obs"],
                        "mode_steps_per_step": units,
                        "l2": f"inputs larger than L2 (L, R {8 * n * n / 1e9:.1f} GB each)",
@@ -457,7 +480,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         dist.destroy_process_group()
 
 
-def td1_comparator(m, cfg, steps):
+def td1_comparator(m, cfg, steps, n_rhs=1):
     """GPU Cholesky theta-method on the same inputs (bounded number of steps)."""
     import ctypes
     import torch
@@ -494,7 +517,8 @@ def td1_comparator(m, cfg, steps):
     setup = e0.elapsed_time(e1) / 1e3
     per_step = e1b.elapsed_time(e2) / 1e3 / steps
     nth = len(cfg["thetas"])
-    total = nth * (setup + per_step * cfg["steps"])
+    # a sweep needs one Cholesky run per right-hand side (same factor)
+    total = nth * (setup + per_step * cfg["steps"] * n_rhs)
     fwd = st.get("td1_fwd", (0.0, 1))
     symv = st.get("td1_symv", (0.0, 1))
     bwd = st.get("td1_bwd", (0.0, 1))
@@ -519,7 +543,9 @@ def cpu_baseline(m, cfg, units):
     r_i = m["r_i"].cpu().numpy()
     r_d = m["r_d"].cpu().numpy().T.copy() if cfg["n_ports"] else np.zeros((n, 0))
     l_d = m["l_d"].cpu().numpy().T.copy() if cfg["n_ports"] else np.zeros((n, 0))
-    est = cb.estimate(l_i, r_i, r_d, l_d, m["m0"], cfg["steps"], len(cfg["thetas"]), cfg["dt"])
+    n_rhs = (cfg["n_ports"] + cfg["n_sources"]) if cfg.get("sweep") else 1
+    est = cb.estimate(l_i, r_i, r_d, l_d, m["m0"], cfg["steps"] * n_rhs, len(cfg["thetas"]),
+                      cfg["dt"])
     return {"value": units / est["total_s"], "unit": "mode-steps/s", "cores": est["cores"],
             "kind": "port", "sample": est["sample"], "extrapolated_total_s": est["total_s"],
             "components_s": est["components"]}

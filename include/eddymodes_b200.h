@@ -114,6 +114,16 @@ int em_sygv(em_ctx* ctx, int64_t n, const double* L, int64_t ldl, const double* 
             double* tau, double* V, int64_t ldv, double* l_n, double* r_n, double* VtR,
             int64_t ldvtr, int64_t* pivot, int* which);
 
+/* em_sygv with flags. EM_SYGV_R_WORKSPACE: when R is sparse (nnz <= 2% of n^2, e.g.
+ * the stencil resistance matrix), R's own storage holds its Cholesky factor during the
+ * solve and is restored from a device CSR copy before return (its contents are
+ * transient garbage meanwhile; -0.0 entries come back as +0.0). Saves one n x n buffer:
+ * 6 n^2 doubles at the memory peak with VtR = NULL, so n = 60,000 fits one B200. */
+#define EM_SYGV_R_WORKSPACE 1
+int em_sygv_ex(em_ctx* ctx, int64_t n, const double* L, int64_t ldl, double* R, int64_t ldr,
+               double* tau, double* V, int64_t ldv, double* l_n, double* r_n, double* VtR,
+               int64_t ldvtr, int flags, int64_t* pivot, int* which);
+
 /* --- modal theta-method (TD2, transient.py:258-308) ------------------------------- */
 
 /* Plan for the decoupled stepper. r_n, l_n: n; P_r, P_l: n x n_p; P_m: n x n_s
@@ -145,6 +155,15 @@ int em_td2_set_observables(em_td2_plan* plan, int n_obs, const double* CV, int64
  * and the observable reconstruction (DMMA). */
 int em_td2_run(em_td2_plan* plan, int64_t T, const double* drive, double* q, double* Y,
                int64_t stride, double* Qcap);
+
+/* Excitation sweep (BASELINE configs[4], C5): every drive channel integrated ALONE,
+ * i.e. the n_c = n_p + n_s columns of the drive table as independent right-hand sides
+ * (the reference superposes them into one trajectory, transient.py:289-297; by
+ * linearity the sweep's responses sum to that trajectory). Q (n x n_c column-major,
+ * device, in/out): per-channel modal states. Y (n_c x n_caps x n_obs, may be NULL):
+ * Y[c] = observables of channel c alone (the D term only for port channels). */
+int em_td2_run_sweep(em_td2_plan* plan, int64_t T, const double* drive, double* Q, double* Y,
+                     int64_t stride);
 
 /* One step, reference semantics (Td2Stepper.step): q (n) in place. i_d, di_d (n_p),
  * di0 (n_s) are HOST arrays. */

@@ -45,6 +45,8 @@ SIGNATURES = {
     "em_syev": (_I, [_P, _I64, _P, _I64, _P, _P, _I64]),
     "em_sygv": (_I, [_P, _I64, _P, _I64, _P, _I64, _P, _P, _I64, _P, _P, _P, _I64,
                      ctypes.POINTER(_I64), ctypes.POINTER(_I)]),
+    "em_sygv_ex": (_I, [_P, _I64, _P, _I64, _P, _I64, _P, _P, _I64, _P, _P, _P, _I64, _I,
+                        ctypes.POINTER(_I64), ctypes.POINTER(_I)]),
     "em_sygv_h": (_I, [_P, _I64, _P, _P, _P, _P, _P, _P, _P, ctypes.POINTER(_I64),
                        ctypes.POINTER(_I)]),
     "em_td2_plan_create": (_I, [_P, _I64, _I, _I, _P, _P, _P, _P, _P, _D, _D, ctypes.POINTER(_P)]),
@@ -53,6 +55,7 @@ SIGNATURES = {
     "em_td2_plan_destroy": (None, [_P]),
     "em_td2_set_observables": (_I, [_P, _I, _P, _I64, _P, _I64]),
     "em_td2_run": (_I, [_P, _I64, _P, _P, _P, _I64, _P]),
+    "em_td2_run_sweep": (_I, [_P, _I64, _P, _P, _P, _I64]),
     "em_td2_step": (_I, [_P, _P, _P, _P, _P]),
     "em_td2_forcing": (_I, [_P, _P, _P, _P, _P]),
     "em_td2_step_forcing": (_I, [_P, _P, _P]),

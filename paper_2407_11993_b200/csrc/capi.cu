@@ -21,7 +21,7 @@ void stages_level(int level);
 int stages_read(double* ms, int64_t* counts, int n);
 int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const double* R,
              int64_t ldr, double* tau, double* V, int64_t ldv, double* l_n, double* r_n,
-             double* VtR, int64_t ldvtr, int* which);
+             double* VtR, int64_t ldvtr, int* which, int flags);
 }
 
 // full definitions live in td1.cu / td2.cu; re-declare the layout-independent API here
@@ -210,17 +210,25 @@ int em_syev(em_ctx* ctx, int64_t n, double* A, int64_t lda, double* w, double* U
   });
 }
 
-int em_sygv(em_ctx* ctx, int64_t n, const double* L, int64_t ldl, const double* R, int64_t ldr,
-            double* tau, double* V, int64_t ldv, double* l_n, double* r_n, double* VtR,
-            int64_t ldvtr, int64_t* pivot, int* which) {
+int em_sygv_ex(em_ctx* ctx, int64_t n, const double* L, int64_t ldl, double* R, int64_t ldr,
+               double* tau, double* V, int64_t ldv, double* l_n, double* r_n, double* VtR,
+               int64_t ldvtr, int flags, int64_t* pivot, int* which) {
   return guarded(ctx, [&] {
+    if (flags & ~EM_SYGV_R_WORKSPACE) throw em::ArgError{"unknown em_sygv_ex flags"};
     int wh = -1;
     const int64_t p = em::sygv(ctx->stream, n, L, ldl, R, ldr, tau, V, ldv, l_n, r_n, VtR, ldvtr,
-                               &wh);
+                               &wh, flags);
     if (pivot) *pivot = p;
     if (which) *which = wh;
     return p >= 0 ? EM_ERR_NOT_PD : EM_OK;
   });
+}
+
+int em_sygv(em_ctx* ctx, int64_t n, const double* L, int64_t ldl, const double* R, int64_t ldr,
+            double* tau, double* V, int64_t ldv, double* l_n, double* r_n, double* VtR,
+            int64_t ldvtr, int64_t* pivot, int* which) {
+  return em_sygv_ex(ctx, n, L, ldl, const_cast<double*>(R), ldr, tau, V, ldv, l_n, r_n, VtR,
+                    ldvtr, 0, pivot, which);
 }
 
 int em_sygv_h(em_ctx* ctx, int64_t n, const double* L_h, const double* R_h, double* tau_h,
@@ -234,8 +242,9 @@ int em_sygv_h(em_ctx* ctx, int64_t n, const double* L_h, const double* R_h, doub
     EM_CK(cudaMemcpyAsync(L.p, L_h, nn * 8, cudaMemcpyHostToDevice, st));
     EM_CK(cudaMemcpyAsync(R.p, R_h, nn * 8, cudaMemcpyHostToDevice, st));
     int wh = -1;
+    // R is this call's own upload: use it as the factor workspace when it is sparse
     const int64_t p = em::sygv(st, n, L.p, n, R.p, n, t.p, V.p, n, ln.p, rn.p,
-                               VtR_h ? VtR.p : nullptr, n, &wh);
+                               VtR_h ? VtR.p : nullptr, n, &wh, EM_SYGV_R_WORKSPACE);
     if (pivot) *pivot = p;
     if (which) *which = wh;
     if (p >= 0) return EM_ERR_NOT_PD;
@@ -304,6 +313,15 @@ int em_td2_run(em_td2_plan* plan, int64_t T, const double* drive, double* q, dou
   em_ctx* ctx = em::td2_ctx(plan);
   return guarded(ctx, [&] {
     em::td2_run(plan, T, drive, q, Y, stride, Qcap);
+    return EM_OK;
+  });
+}
+
+int em_td2_run_sweep(em_td2_plan* plan, int64_t T, const double* drive, double* Q, double* Y,
+                     int64_t stride) {
+  em_ctx* ctx = em::td2_ctx(plan);
+  return guarded(ctx, [&] {
+    em::td2_run_sweep(plan, T, drive, Q, Y, stride);
     return EM_OK;
   });
 }

@@ -93,14 +93,29 @@ struct DArr {
   T* p = nullptr;
   cudaStream_t st = nullptr;
   DArr() = default;
-  DArr(size_t count, cudaStream_t s) : st(s) {
+  DArr(size_t count, cudaStream_t s) { alloc(count, s); }
+  void alloc(size_t count, cudaStream_t s) {
+    release();
+    st = s;
     if (count) EM_CK(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), s));
   }
-  ~DArr() {
+  void release() {
     if (p) cudaFreeAsync(p, st);
+    p = nullptr;
   }
+  ~DArr() { release(); }
   DArr(const DArr&) = delete;
   DArr& operator=(const DArr&) = delete;
+  DArr(DArr&& o) noexcept : p(o.p), st(o.st) { o.p = nullptr; }
+  DArr& operator=(DArr&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      st = o.st;
+      o.p = nullptr;
+    }
+    return *this;
+  }
 };
 
 // --- stage timers (CUDA events on the launching stream; profiling mode only) ---

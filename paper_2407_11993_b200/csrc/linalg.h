@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "ctx.h"
+
 struct em_td2_plan;
 struct em_td1_plan;
 
@@ -23,7 +25,19 @@ void trtri_blocks(cudaStream_t st, int nb, int64_t n, const double* C, int64_t l
 void sygst_lower(cudaStream_t st, int64_t n, double* A, int64_t lda, const double* G, int64_t ldg,
                  const double* Dinv);
 
-// sparse.cu: C = A B through a device CSR copy of the symmetric A when nnz <= max_fill n^2
+// sparse.cu: device CSR of a symmetric matrix stored dense
+struct Csr {
+  int64_t n = 0, nnz = 0;
+  DArr<int64_t> rowptr;
+  DArr<int> colidx;
+  DBuf val;
+};
+bool csr_from_dense(cudaStream_t st, int64_t n, const double* A, int64_t lda, double max_fill,
+                    Csr& out);
+void csr_mm(cudaStream_t st, const Csr& a, int64_t m, const double* B, int64_t ldb, double* C,
+            int64_t ldc);
+void csr_to_dense(cudaStream_t st, const Csr& a, double* A, int64_t lda);
+// C = A B through a device CSR copy of the symmetric A when nnz <= max_fill n^2
 bool sym_sparse_mm(cudaStream_t st, int64_t n, const double* A, int64_t lda, int64_t m,
                    const double* B, int64_t ldb, double* C, int64_t ldc, double max_fill);
 
@@ -110,6 +124,8 @@ void td2_set_observables(em_td2_plan* P, int n_obs, const double* CV, int64_t ld
 void td2_run(em_td2_plan* P, int64_t T, const double* drive, double* q, double* Y,
              int64_t stride, double* Qcap);
 void td2_step(em_td2_plan* P, double* q, const double* u_dev);
+void td2_run_sweep(em_td2_plan* P, int64_t T, const double* drive, double* Q, double* Y,
+                   int64_t stride);
 
 int64_t td1_plan_init(em_td1_plan* P, const double* L, int64_t ldl, const double* R, int64_t ldr,
                       const double* r_d, const double* l_d, const double* m0);

@@ -65,11 +65,21 @@ __global__ void csr_spmm_kernel(int64_t n, int64_t m, const int64_t* __restrict_
   }
 }
 
-// C = A B using CSR when A (symmetric, n x n) has at most max_fill * n^2 nonzeros.
-// Returns false (and does nothing) when A is too dense.
-bool sym_sparse_mm(cudaStream_t st, int64_t n, const double* A, int64_t lda, int64_t m,
-                   const double* B, int64_t ldb, double* C, int64_t ldc, double max_fill) {
-  if (n <= 0 || m <= 0) return true;
+__global__ void csr_scatter_kernel(int64_t n, const int64_t* __restrict__ rowptr,
+                                   const int* __restrict__ colidx, const double* __restrict__ val,
+                                   double* __restrict__ A, int64_t lda) {
+  const int64_t row = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  double* col = A + row * lda;  // symmetric: column `row` == row `row`
+  for (int64_t p = rowptr[row] + lane; p < rowptr[row + 1]; p += 32) col[colidx[p]] = val[p];
+}
+
+// Device CSR copy of a symmetric A (full storage) when it has at most max_fill * n^2
+// nonzeros; returns false (and builds nothing) when A is too dense.
+bool csr_from_dense(cudaStream_t st, int64_t n, const double* A, int64_t lda, double max_fill,
+                    Csr& out) {
+  if (n <= 0) return false;
   DArr<int64_t> cnt(n + 1, st);
   csr_count_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(n, A, lda, cnt.p);
   EM_LAUNCHED();
@@ -80,15 +90,50 @@ bool sym_sparse_mm(cudaStream_t st, int64_t n, const double* A, int64_t lda, int
   const int64_t nnz = h[n];
   if ((double)nnz > max_fill * (double)n * (double)n) return false;
   EM_CK(cudaMemcpyAsync(cnt.p, h.data(), (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-  DArr<int> colidx(imax64(nnz, 1), st);
-  DBuf val(imax64(nnz, 1), st);
-  csr_fill_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(n, A, lda, cnt.p, colidx.p, val.p);
+  out.n = n;
+  out.nnz = nnz;
+  out.rowptr = std::move(cnt);
+  out.colidx.alloc(imax64(nnz, 1), st);
+  out.val.alloc(imax64(nnz, 1), st);
+  csr_fill_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(n, A, lda, out.rowptr.p,
+                                                          out.colidx.p, out.val.p);
   EM_LAUNCHED();
-  const int64_t total = n * m;
+  EM_CK(cudaStreamSynchronize(st));  // host vector h lifetime
+  return true;
+}
+
+// C (n x m) = A_csr B
+void csr_mm(cudaStream_t st, const Csr& a, int64_t m, const double* B, int64_t ldb, double* C,
+            int64_t ldc) {
+  const int64_t total = a.n * m;
+  if (total <= 0) return;
   const int blocks = (int)imin64((total + 255) / 256, 32 * num_sms());
-  csr_spmm_kernel<<<blocks, 256, 0, st>>>(n, m, cnt.p, colidx.p, val.p, B, ldb, C, ldc);
+  csr_spmm_kernel<<<blocks, 256, 0, st>>>(a.n, m, a.rowptr.p, a.colidx.p, a.val.p, B, ldb, C,
+                                          ldc);
   EM_LAUNCHED();
-  EM_CK(cudaStreamSynchronize(st));  // host vector h / device temporaries lifetime
+}
+
+// A (n x n, full storage) <- the matrix held in CSR (every other entry zero).
+void csr_to_dense(cudaStream_t st, const Csr& a, double* A, int64_t lda) {
+  if (lda == a.n) {
+    EM_CK(cudaMemsetAsync(A, 0, (size_t)a.n * a.n * sizeof(double), st));
+  } else {
+    EM_CK(cudaMemset2DAsync(A, lda * sizeof(double), 0, a.n * sizeof(double), a.n, st));
+  }
+  csr_scatter_kernel<<<(unsigned)((a.n + 7) / 8), 256, 0, st>>>(a.n, a.rowptr.p, a.colidx.p,
+                                                                a.val.p, A, lda);
+  EM_LAUNCHED();
+}
+
+// C = A B using CSR when A (symmetric, n x n) has at most max_fill * n^2 nonzeros.
+// Returns false (and does nothing) when A is too dense.
+bool sym_sparse_mm(cudaStream_t st, int64_t n, const double* A, int64_t lda, int64_t m,
+                   const double* B, int64_t ldb, double* C, int64_t ldc, double max_fill) {
+  if (n <= 0 || m <= 0) return true;
+  Csr a;
+  if (!csr_from_dense(st, n, A, lda, max_fill, a)) return false;
+  csr_mm(st, a, m, B, ldb, C, ldc);
+  EM_CK(cudaStreamSynchronize(st));  // device temporaries lifetime
   return true;
 }
 

@@ -156,20 +156,37 @@ __global__ void quadform_lower_kernel(int64_t n, const double* __restrict__ V, i
 // Returns -1 on success; else the failing pivot with *which = 0 (R) / 1 (L).
 int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const double* R,
              int64_t ldr, double* tau, double* V, int64_t ldv, double* l_n, double* r_n,
-             double* VtR, int64_t ldvtr, int* which) {
+             double* VtR, int64_t ldvtr, int* which, int flags) {
   *which = -1;
   if (n <= 0) return -1;
   const size_t nn = (size_t)n * n;
-  DBuf G(nn, st);
-  copy_matrix(st, false, n, n, R, ldr, G.p, n);
+  // EM_SYGV_R_WORKSPACE: when R is sparse (the stencil R of the plates), keep a CSR copy,
+  // factor R in its own storage and restore it from the copy before returning: one N x N
+  // buffer less (6 N^2 at the peak), so the C5 order N = 60,000 fits one B200
+  Csr rcsr;
+  const bool r_ws = (flags & EM_SYGV_R_WORKSPACE) && csr_from_dense(st, n, R, ldr, 0.02, rcsr);
+  DBuf Gbuf;
+  double* G = const_cast<double*>(R);
+  int64_t ldg = ldr;
+  if (!r_ws) {
+    Gbuf.alloc(nn, st);
+    copy_matrix(st, false, n, n, R, ldr, Gbuf.p, n);
+    G = Gbuf.p;
+    ldg = n;
+  }
+  auto restore_r = [&] {
+    if (r_ws) csr_to_dense(st, rcsr, G, ldg);
+  };
   int64_t piv;
   DBuf GDinv((size_t)((n + kTrsmBlock - 1) / kTrsmBlock) * kTrsmBlock * kTrsmBlock, st);
   {
     Stage s(st, ST_POTRF_R);
-    piv = potrf(st, n, G.p, n, GDinv.p);
+    piv = potrf(st, n, G, ldg, GDinv.p);
   }
   if (piv >= 0) {
     *which = 0;
+    restore_r();
+    EM_CK(cudaStreamSynchronize(st));
     return piv;
   }
   DBuf B(nn, st);
@@ -181,7 +198,7 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
       Stage s(st, ST_SYGST);
       copy_matrix(st, false, n, n, L, ldl, B.p, n);
       mirror_lower(st, n, B.p, n);  // SymMatrix semantics: the lower triangle defines L
-      sygst_lower(st, n, B.p, n, G.p, n, GDinv.p);
+      sygst_lower(st, n, B.p, n, G, ldg, GDinv.p);
     }
     // certificate only (modal.py:69-70), factored in the (still free) output buffer V
     {
@@ -191,6 +208,8 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
     }
     if (piv >= 0) {
       *which = 1;
+      restore_r();
+      EM_CK(cudaStreamSynchronize(st));
       return piv;
     }
   }
@@ -202,9 +221,10 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
   B.release();
   {
     Stage s(st, ST_TRSM_BACK);
-    trsm_lower(st, true, n, n, G.p, n, V, ldv, GDinv.p);     // V = G^-T U
+    trsm_lower(st, true, n, n, G, ldg, V, ldv, GDinv.p);     // V = G^-T U
   }
-  G.release();
+  Gbuf.release();
+  restore_r();
   {
     Stage s(st, ST_FINALIZE);
     finalize_modes_inplace_kernel<<<(unsigned)((n + 1) / 2), 256, 0, st>>>(n, V, ldv, w.p, tau);
@@ -229,7 +249,9 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
       ldrv = n;
     }
     // R is typically a stencil stored dense (the reference's SymMatrix): use CSR then
-    if (!sym_sparse_mm(st, n, R, ldr, n, V, ldv, RV, ldrv, 0.02))
+    if (r_ws)
+      csr_mm(st, rcsr, n, V, ldv, RV, ldrv);
+    else if (!sym_sparse_mm(st, n, R, ldr, n, V, ldv, RV, ldrv, 0.02))
       EM_CK(gemm(st, false, false, n, n, n, 1.0, R, ldr, V, ldv, 0.0, RV, ldrv));
     if (r_n) {
       coldot_kernel<<<(unsigned)n, 256, 0, st>>>(n, V, ldv, RV, ldrv, r_n);

@@ -368,25 +368,24 @@ static void local_scan(cudaStream_t st, int64_t nb, int64_t n, int64_t T, int n_
   EM_LAUNCHED();
 }
 
-void td2_run(em_td2_plan* P, int64_t T, const double* drive, double* q, double* Y,
-             int64_t stride, double* Qcap) {
+// One blocked-scan run over prepared inputs: U (T x n_u, row k = u^k), W (n x n_u),
+// q (n, in/out); observables Y (n_caps x n_obs) with the direct term
+// sum_p D[o, p] * dtab[k1 * dld + p] for p < n_pd (D n_obs x n_pd, ld = n_obs).
+static void td2_core(em_td2_plan* P, int64_t T, int n_u, const double* Wp, const double* Up,
+                     double* q, double* Y, int64_t stride, double* Qcap, const double* Dp,
+                     int n_pd, const double* dtab, int dld) {
   cudaStream_t st = P->ctx->stream;
   const int64_t n = P->n;
-  const int n_u = P->n_u, n_c = P->n_p + P->n_s;
-  if (T <= 0 || n <= 0) return;
-  if (stride < 1) throw ArgError{"capture stride must be >= 1"};
   const int64_t nb = (T + TB - 1) / TB;
   const int64_t n_caps = T / stride;
-
-  DBuf U((size_t)T * imax64(n_u, 1), st);
-  if (n_u > 0) {
-    td2_inputs_kernel<<<(unsigned)((T + 255) / 256), 256, 0, st>>>(T, P->n_p, P->n_s, drive, U.p);
-    EM_LAUNCHED();
-  } else {
-    EM_CK(cudaMemsetAsync(U.p, 0, (size_t)T * sizeof(double), st));
+  DBuf U0;
+  if (n_u == 0) {
+    U0.alloc((size_t)T, st);
+    EM_CK(cudaMemsetAsync(U0.p, 0, (size_t)T * sizeof(double), st));
+    Up = U0.p;
   }
   const int nu_eff = imax64(n_u, 1);
-  const double* W = n_u > 0 ? P->W.p : nullptr;
+  const double* W = n_u > 0 ? Wp : nullptr;
   DBuf Wz;
   if (n_u == 0) {  // no drive: a zero input column keeps the kernels uniform
     Wz.alloc(n, st);
@@ -396,11 +395,11 @@ void td2_run(em_td2_plan* P, int64_t T, const double* drive, double* q, double* 
   DBuf E((size_t)nb * n, st), S((size_t)nb * n, st);
   stage_begin(st, ST_TD2_LOCAL);
   switch (nu_eff) {
-    case 1: local_scan<1>(st, nb, n, T, nu_eff, P->eps.p, W, U.p, E.p); break;
-    case 2: local_scan<2>(st, nb, n, T, nu_eff, P->eps.p, W, U.p, E.p); break;
-    case 3: local_scan<3>(st, nb, n, T, nu_eff, P->eps.p, W, U.p, E.p); break;
-    case 4: local_scan<4>(st, nb, n, T, nu_eff, P->eps.p, W, U.p, E.p); break;
-    default: local_scan<0>(st, nb, n, T, nu_eff, P->eps.p, W, U.p, E.p); break;
+    case 1: local_scan<1>(st, nb, n, T, nu_eff, P->eps.p, W, Up, E.p); break;
+    case 2: local_scan<2>(st, nb, n, T, nu_eff, P->eps.p, W, Up, E.p); break;
+    case 3: local_scan<3>(st, nb, n, T, nu_eff, P->eps.p, W, Up, E.p); break;
+    case 4: local_scan<4>(st, nb, n, T, nu_eff, P->eps.p, W, Up, E.p); break;
+    default: local_scan<0>(st, nb, n, T, nu_eff, P->eps.p, W, Up, E.p); break;
   }
   stage_end(st, ST_TD2_LOCAL);
   stage_begin(st, ST_TD2_CARRY);
@@ -433,18 +432,77 @@ void td2_run(em_td2_plan* P, int64_t T, const double* drive, double* q, double* 
   const int mt = n_obs_pad / 8;
   Stage replay_stage(st, ST_TD2_REPLAY);
   switch (nu_eff) {
-    case 1: dispatch_mt<1>(mt, st, grid, smem, n, T, nu_eff, n_obs, cvs, mps, P->eps.p, W, U.p, S.p, CV, ldcv, stride, Ypart.p, ldys, Qcap, n_caps); break;
-    case 2: dispatch_mt<2>(mt, st, grid, smem, n, T, nu_eff, n_obs, cvs, mps, P->eps.p, W, U.p, S.p, CV, ldcv, stride, Ypart.p, ldys, Qcap, n_caps); break;
-    case 3: dispatch_mt<3>(mt, st, grid, smem, n, T, nu_eff, n_obs, cvs, mps, P->eps.p, W, U.p, S.p, CV, ldcv, stride, Ypart.p, ldys, Qcap, n_caps); break;
-    case 4: dispatch_mt<4>(mt, st, grid, smem, n, T, nu_eff, n_obs, cvs, mps, P->eps.p, W, U.p, S.p, CV, ldcv, stride, Ypart.p, ldys, Qcap, n_caps); break;
-    default: dispatch_mt<0>(mt, st, grid, smem, n, T, nu_eff, n_obs, cvs, mps, P->eps.p, W, U.p, S.p, CV, ldcv, stride, Ypart.p, ldys, Qcap, n_caps); break;
+    case 1: dispatch_mt<1>(mt, st, grid, smem, n, T, nu_eff, n_obs, cvs, mps, P->eps.p, W, Up, S.p, CV, ldcv, stride, Ypart.p, ldys, Qcap, n_caps); break;
+    case 2: dispatch_mt<2>(mt, st, grid, smem, n, T, nu_eff, n_obs, cvs, mps, P->eps.p, W, Up, S.p, CV, ldcv, stride, Ypart.p, ldys, Qcap, n_caps); break;
+    case 3: dispatch_mt<3>(mt, st, grid, smem, n, T, nu_eff, n_obs, cvs, mps, P->eps.p, W, Up, S.p, CV, ldcv, stride, Ypart.p, ldys, Qcap, n_caps); break;
+    case 4: dispatch_mt<4>(mt, st, grid, smem, n, T, nu_eff, n_obs, cvs, mps, P->eps.p, W, Up, S.p, CV, ldcv, stride, Ypart.p, ldys, Qcap, n_caps); break;
+    default: dispatch_mt<0>(mt, st, grid, smem, n, T, nu_eff, n_obs, cvs, mps, P->eps.p, W, Up, S.p, CV, ldcv, stride, Ypart.p, ldys, Qcap, n_caps); break;
   }
   if (Y && P->n_obs > 0 && n_caps > 0) {
     int64_t tot = n_caps * n_obs;
     td2_reduce_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
-        n_caps, n_obs, nsplit, ldys, Ypart.p, P->n_p, n_c, P->D.n ? P->D.p : nullptr, P->n_obs,
-        drive, stride, Y);
+        n_caps, n_obs, nsplit, ldys, Ypart.p, n_pd, dld, Dp, P->n_obs, dtab, stride, Y);
     EM_LAUNCHED();
+  }
+}
+
+
+void td2_run(em_td2_plan* P, int64_t T, const double* drive, double* q, double* Y,
+             int64_t stride, double* Qcap) {
+  cudaStream_t st = P->ctx->stream;
+  const int n_u = P->n_u, n_c = P->n_p + P->n_s;
+  if (T <= 0 || P->n <= 0) return;
+  if (stride < 1) throw ArgError{"capture stride must be >= 1"};
+  DBuf U((size_t)T * imax64(n_u, 1), st);
+  if (n_u > 0) {
+    td2_inputs_kernel<<<(unsigned)((T + 255) / 256), 256, 0, st>>>(T, P->n_p, P->n_s, drive, U.p);
+    EM_LAUNCHED();
+  }
+  td2_core(P, T, n_u, P->W.p, n_u > 0 ? U.p : nullptr, q, Y, stride, Qcap,
+           P->D.n ? P->D.p : nullptr, P->n_p, drive, n_c);
+}
+
+// Inputs of one drive channel alone: a port p gives u^k = [i_d,p(t_k), di_d,p], a source
+// s gives [di_0,s, 0] (the second weight column is zero).
+__global__ void td2_channel_inputs_kernel(int64_t T, int n_c, int col, bool port,
+                                          const double* __restrict__ drive,
+                                          double* __restrict__ U) {
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= T) return;
+  const double d0 = drive[k * n_c + col], d1 = drive[(k + 1) * n_c + col];
+  U[2 * k] = port ? d0 : d1 - d0;
+  U[2 * k + 1] = port ? d1 - d0 : 0.0;
+}
+
+void td2_run_sweep(em_td2_plan* P, int64_t T, const double* drive, double* Q, double* Y,
+                   int64_t stride) {
+  cudaStream_t st = P->ctx->stream;
+  const int64_t n = P->n;
+  const int n_p = P->n_p, n_c = P->n_p + P->n_s;
+  if (T <= 0 || n <= 0 || n_c == 0) return;
+  if (stride < 1) throw ArgError{"capture stride must be >= 1"};
+  const int64_t n_caps = T / stride;
+  const int n_obs = (Y && P->n_obs > 0) ? P->n_obs : 0;
+  DBuf U((size_t)T * 2, st), Wc((size_t)n * 2, st);
+  for (int c = 0; c < n_c; ++c) {
+    const bool port = c < n_p;
+    // weight columns of this channel (W = [P_r-part | P_ltr-part | P_m-part] / den)
+    if (port) {
+      EM_CK(cudaMemcpyAsync(Wc.p, P->W.p + (size_t)c * n, n * sizeof(double),
+                            cudaMemcpyDeviceToDevice, st));
+      EM_CK(cudaMemcpyAsync(Wc.p + n, P->W.p + (size_t)(n_p + c) * n, n * sizeof(double),
+                            cudaMemcpyDeviceToDevice, st));
+    } else {
+      EM_CK(cudaMemcpyAsync(Wc.p, P->W.p + (size_t)(2 * n_p + (c - n_p)) * n,
+                            n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      EM_CK(cudaMemsetAsync(Wc.p + n, 0, n * sizeof(double), st));
+    }
+    td2_channel_inputs_kernel<<<(unsigned)((T + 255) / 256), 256, 0, st>>>(T, n_c, c, port,
+                                                                         drive, U.p);
+    EM_LAUNCHED();
+    const double* Dc = (port && P->D.n) ? P->D.p + (size_t)c * P->n_obs : nullptr;
+    td2_core(P, T, 2, Wc.p, U.p, Q + (size_t)c * n, n_obs ? Y + (size_t)c * n_caps * n_obs : nullptr,
+             stride, nullptr, Dc, Dc ? 1 : 0, drive + c, n_c);
   }
 }
 

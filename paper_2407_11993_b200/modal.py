@@ -109,6 +109,7 @@ def generalized_eig(l_i, r_i, *, vt_r: str = "auto") -> ModalBasis:
     Raises NotPositiveDefinite("modal resistance matrix" / "modal inductance
     matrix") with the failing pivot, in the reference's order."""
     t = nat.torch()
+    own = False  # R uploaded here: usable as the factor workspace (EM_SYGV_R_WORKSPACE)
     if isinstance(l_i, t.Tensor) and isinstance(r_i, t.Tensor):
         # device-resident symmetric inputs (row-major bytes == column-major)
         ld = l_i.to(dtype=t.float64).contiguous()
@@ -130,6 +131,7 @@ def generalized_eig(l_i, r_i, *, vt_r: str = "auto") -> ModalBasis:
             nat.device_colmajor(lm)
         rd = nat.device_symmetric(rm) if isinstance(r_i, linalg.SymMatrix) else \
             nat.device_colmajor(rm)
+        own = True
     ctx = nat.context()
     if vt_r not in ("auto", "eager", "lazy"):
         raise ValueError("vt_r must be 'auto', 'eager' or 'lazy'")
@@ -142,10 +144,10 @@ def generalized_eig(l_i, r_i, *, vt_r: str = "auto") -> ModalBasis:
     vtr = nat.empty(n, n) if vt_r == "eager" else None
     piv = ctypes.c_int64(-1)
     which = ctypes.c_int(-1)
-    rc = nat.load_library().em_sygv(ctx, n, nat.ptr(ld), n, nat.ptr(rd), n, nat.ptr(tau),
-                                    nat.ptr(v), n, nat.ptr(ln), nat.ptr(rn),
-                                    None if vtr is None else nat.ptr(vtr), n,
-                                    ctypes.byref(piv), ctypes.byref(which))
+    rc = nat.load_library().em_sygv_ex(ctx, n, nat.ptr(ld), n, nat.ptr(rd), n, nat.ptr(tau),
+                                       nat.ptr(v), n, nat.ptr(ln), nat.ptr(rn),
+                                       None if vtr is None else nat.ptr(vtr), n,
+                                       1 if own else 0, ctypes.byref(piv), ctypes.byref(which))
     if rc == nat.EM_ERR_NOT_PD:
         what = "modal resistance matrix" if which.value == 0 else "modal inductance matrix"
         raise NotPositiveDefinite(int(piv.value), what)

@@ -248,6 +248,42 @@ class Td2Stepper:
             states = _reconstruct(self.basis, qcap, qcap.shape[0])
         return states, (y.cpu().numpy() if y is not None else None), q.cpu().numpy()
 
+    def run_sweep_device(self, drive_dev, steps: int, q_dev, capture_stride: int = 1,
+                         want_obs: bool = True):
+        """Device sweep: every drive channel integrated alone (em_td2_run_sweep).
+        q_dev: (n_c, N) torch (column-major N x n_c), in/out. Returns Y device
+        (n_c, n_caps, n_obs) or None."""
+        n_c = self._n_p + self._n_s
+        n_caps = steps // capture_stride
+        y = nat.empty(n_c, n_caps, self._n_obs) \
+            if (want_obs and getattr(self, "_n_obs", 0)) else None
+        nat.check(nat.load_library().em_td2_run_sweep(self._plan, steps, nat.ptr(drive_dev),
+                                                       nat.ptr(q_dev), nat.ptr(y),
+                                                       capture_stride), "em_td2_run_sweep")
+        return y
+
+    def run_sweep(self, i_d_samples, i0_samples, capture_stride: int = 1, observables=None,
+                  modal_states0=None):
+        """Batched-excitation sweep (BASELINE configs[4]): the response to each drive
+        channel (ports, then sources) ALONE, all channels integrated in one call — the
+        reference would run one trajectory per channel (run_transient superposes them,
+        transient.py:289-297). Returns (observables (n_c, n_caps, n_obs) or None,
+        final modal states (N, n_c))."""
+        n_c = self._n_p + self._n_s
+        if n_c == 0:
+            raise ValidationError("a sweep needs at least one drive channel")
+        table = _drive_table(i_d_samples, i0_samples, self._n_p, self._n_s)
+        steps = table.shape[0] - 1
+        if observables is not None:
+            self.set_observables(observables)
+        drive = nat.device_vector(table.reshape(-1))
+        q0 = np.zeros((self._n, n_c)) if modal_states0 is None else \
+            np.asarray(modal_states0, dtype=float).reshape(self._n, n_c)
+        q = nat.device_colmajor(q0)
+        y = self.run_sweep_device(drive, steps, q, capture_stride, observables is not None)
+        return (y.cpu().numpy() if y is not None else None), \
+            nat.host_colmajor(q, self._n, n_c)
+
 
 def _reconstruct(basis: ModalBasis, qcap, n_caps: int) -> np.ndarray:
     """internal states I = V Q for captured modal states (n_caps x N host)."""

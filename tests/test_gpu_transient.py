@@ -235,3 +235,49 @@ def test_exact_modal_integrator_on_device_matches_oracle():
     assert np.allclose(decay[-1], q0 * np.exp(-times[-1] / tau), rtol=1e-10, atol=1e-300)
     with pytest.raises(ValidationError):
         transient.exact_modal_reference(basis, rm, i_d[:3], i0[:3], np.array([0.0, 1e-7, 3e-7]))
+
+
+@pytest.mark.parametrize("theta", [0.5, 1.0])
+def test_excitation_sweep_matches_oracle_per_channel(theta):
+    """Batched-excitation sweep (BASELINE configs[4], em_td2_run_sweep): each drive
+    channel integrated alone as its own right-hand side. Every channel's observables
+    (with the port's direct term D) against the oracle run with only that channel
+    driven; the channels sum to the superposed trajectory of the UNMODIFIED reference
+    (golden td2_obs, transient.py:289-297 superposes them); final per-channel states."""
+    from paper_2407_11993_b200 import modal, reduction, transient
+    g = golden("plate_small")
+    rng = np.random.default_rng(7)
+    n = g["r_i"].shape[0]
+    m0 = np.concatenate([g["m0"], rng.standard_normal((n, 3)) / np.sqrt(n)], axis=1)
+    rm = reduction.from_blocks(g["r_i"], g["l_i"], g["r_d"], g["l_d"], m0,
+                               port_names=("p0",), source_names=("s0", "s1", "s2", "s3"))
+    basis = modal.generalized_eig(rm.l_i, rm.r_i)
+    ref = oracle.generalized_eig(g["l_i"], g["r_i"])
+    steps, dt = int(g["steps"]), float(g["dt"])
+    t = dt * np.arange(steps + 1)
+    i_d = np.minimum(t / 5e-6, 1.0)[:, None]
+    f = np.array([1e4, 3e4, 7e4, 1.3e5])
+    i0 = np.sin(2 * np.pi * f[None, :] * t[:, None] + np.arange(4)[None, :])
+    c = g["c"]
+    d = rng.standard_normal((c.shape[0], 1))
+    st = transient.Td2Stepper(rm, basis, dt, theta)
+    y, q = st.run_sweep(i_d, i0, observables=(c, d))
+    assert y.shape == (5, steps, c.shape[0]) and q.shape == (n, 5)
+    o = oracle.Td2(ref, rm.r_d, rm.l_d, rm.m0, dt, theta)
+    for ch in range(5):
+        i_d_c, i0_c = np.zeros_like(i_d), np.zeros_like(i0)
+        if ch == 0:
+            i_d_c[:] = i_d
+        else:
+            i0_c[:, ch - 1] = i0[:, ch - 1]
+        states, _ = oracle.run(o, n, i_d_c, i0_c, ref)
+        y_ref = states @ c.T + (i_d_c[1:] @ d.T if ch == 0 else 0.0)
+        assert rel_l2(y[ch], y_ref) < TOL, ch
+        # final state of the channel as currents I = V q (the oracle captures V q)
+        assert rel_l2(basis.v @ q[:, ch], states[-1]) < TOL, ch
+    # superposition of the first two channels = the reference's own superposed run
+    rm1 = _plate_rm(g)
+    st1 = transient.Td2Stepper(rm1, modal.generalized_eig(rm1.l_i, rm1.r_i), dt, theta)
+    i_d1, i01 = transient.drive_samples(None, rm1, _plate_drives(), dt, steps)
+    y1, _ = st1.run_sweep(i_d1, i01, observables=(c, None))
+    assert rel_l2(y1.sum(axis=0), g[f"td2_obs_theta{theta}"]) < TOL
