@@ -55,6 +55,9 @@ int em_synchronize(em_ctx* ctx);
  * (dense -> band -> tridiagonal) reduction in em_syev/em_sygv (default INT64_MAX:
  * one-stage Householder everywhere). */
 #define EM_CFG_TWO_STAGE_MIN 1
+/* EM_CFG_BAND_OFF: 1 = always factor R densely (default 0: a banded R, lower bandwidth
+ * b with 4 (b + 128) <= n, takes the banded Cholesky and banded solves). */
+#define EM_CFG_BAND_OFF 2
 int em_config(em_ctx* ctx, int key, int64_t value);
 /* Stage timers (CUDA events on the context stream). em_profile(ctx, 1) clears and
  * enables them; em_stage_times fills per-stage milliseconds / event-pair counts

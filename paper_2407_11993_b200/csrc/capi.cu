@@ -16,6 +16,7 @@ struct em_td1_plan;
 namespace em {
 extern int64_t g_two_stage_min;
 extern int g_sytrd_dbg;
+extern int g_band_off;
 void stages_reset(bool on);
 void stages_level(int level);
 int stages_read(double* ms, int64_t* counts, int n);
@@ -129,6 +130,10 @@ int em_config(em_ctx* ctx, int key, int64_t value) {
   return guarded(ctx, [&] {
     if (key == EM_CFG_TWO_STAGE_MIN) {
       em::g_two_stage_min = value;
+      return EM_OK;
+    }
+    if (key == EM_CFG_BAND_OFF) {
+      em::g_band_off = value ? 1 : 0;
       return EM_OK;
     }
     if (key == 98) {  // debug: sytrd switches (bit0 no TMA symv, bit1 no PDL, bit2 no graph,

@@ -37,6 +37,23 @@ bool csr_from_dense(cudaStream_t st, int64_t n, const double* A, int64_t lda, do
 void csr_mm(cudaStream_t st, const Csr& a, int64_t m, const double* B, int64_t ldb, double* C,
             int64_t ldc);
 void csr_to_dense(cudaStream_t st, const Csr& a, double* A, int64_t lda);
+// band.cu: banded Cholesky (128-wide block columns, kb blocks below the diagonal)
+struct BandChol {
+  int64_t n = 0, ldp = 0, nblk = 0;
+  int kb = 0;
+  DBuf P, Dinv;
+  double* panel(int64_t j) const { return P.p + j * ldp * 128; }
+  int64_t rows_below(int64_t j) const {
+    const int64_t r0 = (j + 1) * 128;
+    return r0 >= n ? 0 : (n - r0 < (int64_t)kb * 128 ? n - r0 : (int64_t)kb * 128);
+  }
+};
+int64_t band_lower_width(cudaStream_t st, int64_t n, const double* A, int64_t lda);
+int64_t band_potrf(cudaStream_t st, int64_t n, const double* A, int64_t lda, int64_t bw,
+                   BandChol& f);
+void band_solve(cudaStream_t st, const BandChol& f, bool trans, int64_t m, double* C,
+                int64_t ldc);
+void band_sygst(cudaStream_t st, const BandChol& f, double* B, int64_t ldb);
 // C = A B through a device CSR copy of the symmetric A when nnz <= max_fill n^2
 bool sym_sparse_mm(cudaStream_t st, int64_t n, const double* A, int64_t lda, int64_t m,
                    const double* B, int64_t ldb, double* C, int64_t ldc, double max_fill);

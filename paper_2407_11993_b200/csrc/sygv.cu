@@ -17,6 +17,8 @@ namespace em {
 // em_config(EM_CFG_TWO_STAGE_MIN). Off by default until the two-stage path beats the
 // one-stage one end to end; tests force it on.
 int64_t g_two_stage_min = INT64_MAX;
+// em_config(EM_CFG_BAND_OFF): 1 forces the dense R path (tests compare both)
+int g_band_off = 0;
 
 void syev_ascending(cudaStream_t st, int64_t n, double* A, int64_t lda, double* w, double* Z,
                     int64_t ldz) {
@@ -160,15 +162,22 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
   *which = -1;
   if (n <= 0) return -1;
   const size_t nn = (size_t)n * n;
-  // EM_SYGV_R_WORKSPACE: when R is sparse (the stencil R of the plates), keep a CSR copy,
-  // factor R in its own storage and restore it from the copy before returning: one N x N
-  // buffer less (6 N^2 at the peak), so the C5 order N = 60,000 fits one B200
+  // A banded R (the 7-point stencil R of the plates: lower bandwidth ny*nz) is factored
+  // in banded storage and every solve with its factor is banded (band.cu): the R stages
+  // cost N b^2 + 6 N^2 b instead of 7/3 N^3, and no N x N factor buffer is needed.
+  const int64_t bw = g_band_off ? n : band_lower_width(st, n, R, ldr);
+  const bool banded = n > 2 * kTrsmBlock && (bw + kTrsmBlock) * 4 <= n;
+  BandChol bc;
+  // EM_SYGV_R_WORKSPACE (dense-band R only): when R is sparse, keep a CSR copy, factor R
+  // in its own storage and restore it from the copy before returning: one N x N buffer
+  // less at the peak
   Csr rcsr;
-  const bool r_ws = (flags & EM_SYGV_R_WORKSPACE) && csr_from_dense(st, n, R, ldr, 0.02, rcsr);
+  const bool r_ws = !banded && (flags & EM_SYGV_R_WORKSPACE) &&
+                    csr_from_dense(st, n, R, ldr, 0.02, rcsr);
   DBuf Gbuf;
   double* G = const_cast<double*>(R);
   int64_t ldg = ldr;
-  if (!r_ws) {
+  if (!banded && !r_ws) {
     Gbuf.alloc(nn, st);
     copy_matrix(st, false, n, n, R, ldr, Gbuf.p, n);
     G = Gbuf.p;
@@ -178,10 +187,15 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
     if (r_ws) csr_to_dense(st, rcsr, G, ldg);
   };
   int64_t piv;
-  DBuf GDinv((size_t)((n + kTrsmBlock - 1) / kTrsmBlock) * kTrsmBlock * kTrsmBlock, st);
+  DBuf GDinv;
   {
     Stage s(st, ST_POTRF_R);
-    piv = potrf(st, n, G, ldg, GDinv.p);
+    if (banded) {
+      piv = band_potrf(st, n, R, ldr, bw, bc);
+    } else {
+      GDinv.alloc((size_t)((n + kTrsmBlock - 1) / kTrsmBlock) * kTrsmBlock * kTrsmBlock, st);
+      piv = potrf(st, n, G, ldg, GDinv.p);
+    }
   }
   if (piv >= 0) {
     *which = 0;
@@ -198,7 +212,10 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
       Stage s(st, ST_SYGST);
       copy_matrix(st, false, n, n, L, ldl, B.p, n);
       mirror_lower(st, n, B.p, n);  // SymMatrix semantics: the lower triangle defines L
-      sygst_lower(st, n, B.p, n, G, ldg, GDinv.p);
+      if (banded)
+        band_sygst(st, bc, B.p, n);  // the reference's X = G^-1 L, G^-1 X^T, (B + B^T)/2
+      else
+        sygst_lower(st, n, B.p, n, G, ldg, GDinv.p);
     }
     // certificate only (modal.py:69-70), factored in the (still free) output buffer V
     {
@@ -221,7 +238,10 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
   B.release();
   {
     Stage s(st, ST_TRSM_BACK);
-    trsm_lower(st, true, n, n, G, ldg, V, ldv, GDinv.p);     // V = G^-T U
+    if (banded)
+      band_solve(st, bc, true, n, V, ldv);                   // V = G^-T U
+    else
+      trsm_lower(st, true, n, n, G, ldg, V, ldv, GDinv.p);
   }
   Gbuf.release();
   restore_r();

@@ -101,3 +101,62 @@ def test_r_workspace_mode_identical_and_restores_r(sparse_r):
         outs.append([x.cpu().numpy() for x in (tau, ln, rn, V, VtR)])
     for a, b in zip(*outs):
         assert np.array_equal(a, b)
+
+
+def _sygv_dev(L, R, n, flags=0):
+    from paper_2407_11993_b200 import _native as nat
+    lib, ctx = nat.load_library(), nat.context()
+    tau, ln, rn, V = nat.empty(n), nat.empty(n), nat.empty(n), nat.empty(n, n)
+    piv, which = ctypes.c_int64(-1), ctypes.c_int(-1)
+    rc = lib.em_sygv_ex(ctx, n, nat.ptr(L), n, nat.ptr(R), n, nat.ptr(tau), nat.ptr(V), n,
+                        nat.ptr(ln), nat.ptr(rn), None, n, flags, ctypes.byref(piv),
+                        ctypes.byref(which))
+    return rc, piv.value, which.value, [x.cpu().numpy() for x in (tau, ln, rn, V)]
+
+
+@pytest.mark.parametrize("grid", [(32, 16, 4), (21, 13, 5)])
+def test_banded_r_path_matches_dense_path(grid):
+    """Banded Cholesky of the stencil R + banded two-sided reduction (the reference's
+    G^-1 (G^-1 L)^T, (B + B^T)/2 sequence) + banded back-transform against the dense
+    path (EM_CFG_BAND_OFF) on the same plate; a ragged last block (N = 1365)."""
+    from paper_2407_11993_b200 import _native as nat
+    from paper_2407_11993_b200.synth import device_plate_model
+    m = device_plate_model(*grid, n_ports=0, n_sources=0, n_obs=1)
+    L, R = m["l_i"], m["r_i"]
+    n = L.shape[0]
+    lib, ctx = nat.load_library(), nat.context()
+    outs = []
+    for off in (1, 0):
+        nat.check(lib.em_config(ctx, 2, off))
+        rc, _, _, o = _sygv_dev(L, R, n)
+        nat.check(rc)
+        outs.append(o)
+    nat.check(lib.em_config(ctx, 2, 0))
+    (t0, l0, r0, v0), (t1, l1, r1, v1) = outs
+    assert np.max(np.abs(t1 - t0) / t0) < 1e-12
+    np.testing.assert_allclose(l1, l0, rtol=1e-11)
+    np.testing.assert_allclose(r1, r0, rtol=1e-11)
+    # modes of well-separated eigenvalues agree column by column (sign-fixed)
+    gap = np.minimum(np.abs(np.diff(t0, prepend=np.inf)), np.abs(np.diff(t0, append=-np.inf)))
+    sep = gap > 1e-6 * t0
+    err = np.abs(v1 - v0).max(axis=1)  # host (n, n) rows = modes
+    assert np.all(err[sep] < 1e-7 * np.abs(v0).max())
+
+
+def test_banded_r_not_pd_reports_the_dense_pivot():
+    """A banded R that is not positive definite: same failing pivot (the reference's
+    first failing Crout column, cholesky_kernel _kernels.py:18-36) on both paths."""
+    from paper_2407_11993_b200 import _native as nat
+    from paper_2407_11993_b200.synth import device_plate_model
+    m = device_plate_model(32, 16, 4, n_ports=0, n_sources=0, n_obs=1)
+    L, R = m["l_i"], m["r_i"].clone()
+    n = L.shape[0]
+    R[700, 700] = -1.0  # column 700 of the lower triangle (row-major == column-major)
+    lib, ctx = nat.load_library(), nat.context()
+    res = []
+    for off in (1, 0):
+        nat.check(lib.em_config(ctx, 2, off))
+        rc, piv, which, _ = _sygv_dev(L, R, n)
+        res.append((rc, piv, which))
+    nat.check(lib.em_config(ctx, 2, 0))
+    assert res[0] == res[1] == (nat.EM_ERR_NOT_PD, 700, 0)
