@@ -40,7 +40,9 @@ struct em_td2_plan {
 namespace em {
 
 constexpr int TB = 64;        // time steps per block
-constexpr int MC = 128;       // modes per chunk in the replay kernel
+constexpr int MC = 64;        // modes per chunk in the replay kernel (70 KB of shared
+                              // memory per CTA: three CTAs per SM overlap one CTA's
+                              // recurrence and loads with the others' DMMA)
 constexpr int RT = 256;       // threads per CTA
 constexpr int QS = MC + 4;    // Qs row stride (≡ 4 mod 16 doubles: conflict-free B fragments)
 
@@ -422,7 +424,9 @@ static void td2_core(em_td2_plan* P, int64_t T, int n_u, const double* Wp, const
     ldcv = 1;
   }
   const int64_t nchunks = (n + MC - 1) / MC;
-  int nsplit = (int)imax64(1, imin64((2 * num_sms() + nb - 1) / nb, nchunks));
+  // mode splits: about 8 waves of 3 CTAs per SM (wave quantisation below ~12%); each
+  // split adds one n_caps x n_obs partial to the final reduction
+  int nsplit = (int)imax64(1, imin64((24 * num_sms() + nb - 1) / nb, nchunks));
   const int64_t mps = ((nchunks + nsplit - 1) / nsplit) * MC;
   nsplit = (int)((n + mps - 1) / mps);
   const int64_t ldys = imax64(n_caps, 1) * n_obs;

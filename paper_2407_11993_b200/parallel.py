@@ -102,6 +102,7 @@ class ShardedTd2:
         nat.check(lib.em_td2_set_observables(plan, self.n_obs, nat.ptr(self.cv), self.n_obs, None,
                                              0), "em_td2_set_observables")
         self.q = nat.zeros(max(self.n_loc, 1))
+        self.q_sweep = None
         self._comm_stream = t.cuda.Stream()
 
     def __del__(self):
@@ -134,4 +135,39 @@ class ShardedTd2:
         for h in pending:
             h.wait()
         main.wait_stream(self._comm_stream)
+        return y
+
+    def run_sweep(self, drive_dev, steps: int):
+        """Excitation sweep over this rank's modes (BASELINE configs[4]: 64 right-hand
+        sides, modes sharded across GPUs): every drive channel integrated alone
+        (em_td2_run_sweep); the partial observables (n_c x block x n_obs) are summed over
+        ranks once per time block. Returns Y (n_c, steps, n_obs) on every rank."""
+        t = nat.torch()
+        lib = nat.load_library()
+        n_c = self.n_p + self.n_s
+        if self.q_sweep is None:
+            self.q_sweep = nat.zeros(n_c, max(self.n_loc, 1))
+        y = nat.zeros(n_c, steps, self.n_obs)
+        main = t.cuda.current_stream()
+        pending = []
+        for k0, k1 in time_blocks(steps, self.block):
+            yb = nat.empty(n_c, k1 - k0, self.n_obs)
+            nat.check(lib.em_td2_run_sweep(self._plan, k1 - k0, nat.ptr(drive_dev[k0 * n_c:]),
+                                           nat.ptr(self.q_sweep), nat.ptr(yb), 1),
+                      "em_td2_run_sweep")
+            if self.dist is not None and self.dist.is_initialized() and \
+                    self.dist.get_world_size() > 1:
+                ev = t.cuda.Event()
+                ev.record(main)
+                with t.cuda.stream(self._comm_stream):
+                    self._comm_stream.wait_event(ev)
+                    pending.append((self.dist.all_reduce(yb, op=self.dist.ReduceOp.SUM,
+                                                         async_op=True), yb, k0, k1))
+            else:
+                y[:, k0:k1] = yb
+        for h, yb, k0, k1 in pending:
+            h.wait()
+        main.wait_stream(self._comm_stream)
+        for _, yb, k0, k1 in pending:
+            y[:, k0:k1] = yb
         return y

@@ -88,3 +88,59 @@ def test_sharded_td2_observables_equal_unsharded(tmp_path, block):
     g = golden("plate_small")
     ref = g["td2_obs_theta0.5"]
     assert rel_l2(y, ref) < 1e-12
+
+
+def _partial_sweep(lo, hi, block):
+    """Per-rank partial sweep (each drive channel alone) of the plate_small TD2 run over
+    modes [lo, hi), block by block with the per-channel carry states (ShardedTd2.run_sweep)."""
+    from oracle import oracle as O
+    from paper_2407_11993_b200.parallel import time_blocks
+    g = golden("plate_small")
+    b = O.Basis(v=g["v"], tau=g["tau"], l_n=g["l_n"], r_n=g["r_n"], vt_r=None)
+    dt, steps = float(g["dt"]), int(g["steps"])
+    sd = O.tone_sampler([[(0.7, 2e4, 0.3), (0.2, 5e4, 1.1)]])
+    s0 = O.tone_sampler([[(1.0, 1e4, 0.0)]])
+    itab, i0tab = O.sample_table(sd, steps, dt), O.sample_table(s0, steps, dt)
+    st = O.Td2(b, g["r_d"], g["l_d"], g["m0"], dt, 0.5)
+    cv = g["c"] @ g["v"]
+    y = np.zeros((2, steps, g["c"].shape[0]))
+    for ch in range(2):
+        it = itab if ch == 0 else 0 * itab
+        i0 = i0tab if ch == 1 else 0 * i0tab
+        q = np.zeros(b.tau.shape[0])
+        for k0, k1 in time_blocks(steps, block):
+            for k in range(k0, k1):
+                f = st.forcing(it[k], it[k + 1] - it[k], i0[k + 1] - i0[k])
+                qn = q.copy()
+                O.lib().orc_td2_step(O._p(qn), O._p(st._rn), O._p(st._c), dt,
+                                     O._p(np.ascontiguousarray(f)), qn.shape[0])
+                q[lo:hi] = qn[lo:hi]
+                y[ch, k] = cv[:, lo:hi] @ q[lo:hi]
+    return y
+
+
+def _sweep_worker(rank, world, port, block, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2407_11993_b200.parallel import reduce_partials, shard_ranges
+    g = golden("plate_small")
+    lo, hi = shard_ranges(g["v"].shape[1], world)[rank]
+    part = torch.from_numpy(_partial_sweep(lo, hi, block))
+    reduce_partials(part, dist)
+    if rank == 0:
+        np.save(out, part.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_sweep_sums_to_the_reference_run(tmp_path):
+    """The C5 layout: sweep channels x sharded modes, one all-reduce of the partial
+    per-channel observables; the channels then superpose to the reference trajectory."""
+    world = 2
+    out = str(tmp_path / "ys.npy")
+    mp.spawn(_sweep_worker, args=(world, _free_port(), 128, out), nprocs=world, join=True)
+    y = np.load(out)
+    g = golden("plate_small")
+    assert y.shape[0] == 2
+    assert rel_l2(y.sum(axis=0), g["td2_obs_theta0.5"]) < 1e-12

@@ -52,7 +52,8 @@ def main(which):
         out["dgemm_8192_TFps"] = 2 * m ** 3 / t / 1e12
         del a, b, c
     if which in ("td2", "all"):
-        T, n_obs = 10000, 32
+        n = int(os.environ.get("TD2_N", n))
+        T, n_obs = int(os.environ.get("TD2_T", 10000)), int(os.environ.get("TD2_OBS", 32))
         ln = torch.rand(n, device="cuda", dtype=torch.float64, generator=g) * 8 + 0.1
         rn = torch.ones(n, device="cuda", dtype=torch.float64)
         pr = torch.randn(n, device="cuda", dtype=torch.float64, generator=g) * 1e-6
