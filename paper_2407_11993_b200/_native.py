@@ -16,7 +16,8 @@ import numpy as np
 from .errors import DeviceError, NotPositiveDefinite
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libeddymodes_b200.so")
+# EM_LIB_PATH: load another build of the same library (A/B measurements)
+LIB_PATH = os.environ.get("EM_LIB_PATH") or os.path.join(_HERE, "libeddymodes_b200.so")
 
 EM_OK, EM_ERR_CUDA, EM_ERR_ARG, EM_ERR_NOT_PD = 0, -1, -2, -3
 

@@ -17,6 +17,7 @@ namespace em {
 extern int64_t g_two_stage_min;
 extern int g_sytrd_dbg;
 extern int g_band_off;
+extern int g_symv_align_off;
 void stages_reset(bool on);
 void stages_level(int level);
 int stages_read(double* ms, int64_t* counts, int n);
@@ -139,6 +140,7 @@ int em_config(em_ctx* ctx, int key, int64_t value) {
     if (key == 98) {  // debug: sytrd switches (bit0 no TMA symv, bit1 no PDL, bit2 no graph,
                       // bit3 the 4-launch column chain)
       em::g_sytrd_dbg = (int)value;
+      em::g_symv_align_off = (value & 16) ? 1 : 0;
       return EM_OK;
     }
     throw em::ArgError{"unknown em_config key"};

@@ -101,6 +101,8 @@ void symv_tma(cudaStream_t st, const SymvMap& m, int64_t off, int64_t n, double 
               const LatrdT* lt, bool pdl);
 // number of CTAs (= quadratic-form partials written to SymvLarfg::vav) for order n
 int64_t symv_tma_ctas(int64_t n);
+// ... for the block at (off, off) (symv_tma aligns its tiles to 32-row boundaries)
+int64_t symv_tma_ctas(int64_t n, int64_t off);
 
 // sytrd.cu: Householder tridiagonalisation (lower). On exit d (n), e (n-1), tau (n-1);
 // reflectors stored below the subdiagonal of A (LAPACK dsytrd convention).

@@ -26,6 +26,7 @@
 namespace em {
 
 static_assert(sizeof(SymvMap) == 2 * sizeof(CUtensorMap), "SymvMap holds two CUtensorMaps");
+extern int g_symv_align_off;
 
 constexpr int HR = 128;                 // tile rows (strip height)
 constexpr int WC = 64;                  // tile columns
@@ -96,6 +97,10 @@ static TmaSched tma_sched(int64_t n) {
 }
 
 int64_t symv_tma_ctas(int64_t n) { return tma_sched(n).P; }
+int64_t symv_tma_ctas(int64_t n, int64_t off) {
+  return tma_sched(n + (g_symv_align_off ? 0 : off % 32)).P;
+}
+int g_symv_align_off = 0;  // em_config debug key 98 bit 4: no 32-row alignment shift
 
 size_t symv_tma_work_size(int64_t n) {
   const TmaSched s = tma_sched(n);
@@ -140,6 +145,19 @@ EM_DEVINL void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, ui
       : "memory");
 }
 
+// x of the block extended by d leading rows/columns (see symv_tma): xd = x - d, na = n + d;
+// zero for r < d (only reachable in the first strip / first column block: callers take
+// this path there and xfast elsewhere), v = [1, xs x] starts at r = d.
+EM_DEVINL double xshift(const double* xd, int64_t r, int64_t d, int64_t na, double xs,
+                        bool unit0) {
+  if (r < d || r >= na) return 0.0;
+  if (unit0 && r == d) return 1.0;
+  return xs * __ldcg(xd + r);
+}
+EM_DEVINL double xfast(const double* xd, int64_t r, int64_t na, double xs) {
+  return r < na ? xs * __ldcg(xd + r) : 0.0;
+}
+
 // ---- kernel ----------------------------------------------------------------------------
 // SH = off & 1. Thread rows within the tile (h, q in {0, 1}): SH = 0: 64h + 2 lane + q
 // (128-bit shared loads); SH = 1: 64h + 32q + lane (the tile sits one row into the
@@ -151,7 +169,7 @@ EM_DEVINL int trow(int h, int q, int lane) {
 
 template <bool LARFG, int SH>
 __global__ void __launch_bounds__(TT, 1) symv_tma_kernel(const __grid_constant__ CUtensorMap map,
-                                                         int64_t off, int64_t n,
+                                                         int64_t off, int64_t n, int64_t d,
                                                          const double* __restrict__ x,
                                                          double* __restrict__ wcol,
                                                          double* __restrict__ wrow, int64_t nbs,
@@ -163,6 +181,8 @@ __global__ void __launch_bounds__(TT, 1) symv_tma_kernel(const __grid_constant__
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int64_t p = blockIdx.x;
   const int64_t t0 = p * len, t1 = imin64(T, t0 + len);
+  const double* xd = x - d;
+  const int64_t na = n + d;
   if (t0 >= t1) {  // not launched by symv_tma (P is trimmed to the last non-empty range)
     if (LARFG && lf.vav != nullptr && tid == 0) lf.vav[p] = 0.0;
     return;
@@ -243,14 +263,20 @@ __global__ void __launch_bounds__(TT, 1) symv_tma_kernel(const __grid_constant__
       for (int h = 0; h < 2; ++h)
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
-          xi[h][q] = symv_xval(x, r0 + trow<SH>(h, q, lane), n, xs, LARFG);
+          xi[h][q] = (i == 0) ? xshift(xd, r0 + trow<SH>(h, q, lane), d, na, xs, LARFG)
+                              : xfast(xd, r0 + trow<SH>(h, q, lane), na, xs);
           row[h][q] = 0.0;
         }
       fresh = false;
     }
     double xj[4];
+    if (j == 0) {
 #pragma unroll
-    for (int cc = 0; cc < 4; ++cc) xj[cc] = symv_xval(x, c0 + 4 * w + cc, n, xs, LARFG);
+      for (int cc = 0; cc < 4; ++cc) xj[cc] = xshift(xd, c0 + 4 * w + cc, d, na, xs, LARFG);
+    } else {
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) xj[cc] = xfast(xd, c0 + 4 * w + cc, na, xs);
+    }
     mbar_wait(&full[s], (unsigned)((k / NST) & 1));
     const double* S = ring + (size_t)s * BR * WC + SH;
     double col[4];
@@ -333,7 +359,7 @@ __global__ void __launch_bounds__(TT, 1) symv_tma_kernel(const __grid_constant__
         for (int k2 = 0; k2 < TT / 32; ++k2) sum += red[k2][tid];
         const int64_t slot = p - (i * (i + 1)) / len;
         wrow[(i * slots + slot) * HR + tid] = sum;
-        if (want_vav) vav = fma(sum, symv_xval(x, r0 + tid, n, xs, LARFG), vav);
+        if (want_vav) vav = fma(sum, xshift(xd, r0 + tid, d, na, xs, LARFG), vav);
       }
       fresh = true;
     }
@@ -359,7 +385,7 @@ __global__ void __launch_bounds__(512) symv_tma_reduce_kernel(int64_t n, double 
                                                               const double* __restrict__ wcol,
                                                               const double* __restrict__ wrow,
                                                               int64_t nbs, int64_t ncj, int64_t len,
-                                                              int64_t slots, LatrdT lt) {
+                                                              int64_t slots, int64_t d, LatrdT lt) {
   __shared__ double red8[32][WC + 1];
   const int64_t b = blockIdx.x;
   pdl_wait();
@@ -399,15 +425,15 @@ __global__ void __launch_bounds__(512) symv_tma_reduce_kernel(int64_t n, double 
   if (threadIdx.x < WC) {
     const double v = ((red8[0][t] + red8[1][t]) + (red8[2][t] + red8[3][t])) +
                      ((red8[4][t] + red8[5][t]) + (red8[6][t] + red8[7][t]));
-    const int64_t idx = b * WC + t;
-    if (idx < n) y[idx] = (beta == 0.0) ? alpha * v : fma(alpha, v, beta * y[idx]);
+    const int64_t idx = b * WC + t - d;
+    if (idx >= 0 && idx < n) y[idx] = (beta == 0.0) ? alpha * v : fma(alpha, v, beta * y[idx]);
   }
 }
 
 template <bool LARFG, int SH>
 static void symv_tma_launch(cudaStream_t st, bool pdl, const TmaSched& s, const CUtensorMap& map,
-                            int64_t off, int64_t n, const double* x, double* wcol, double* wrow,
-                            const SymvLarfg& lf) {
+                            int64_t off, int64_t n, int64_t d, const double* x, double* wcol,
+                            double* wrow, const SymvLarfg& lf) {
   static bool attr = false;
   if (!attr) {
     EM_CK(cudaFuncSetAttribute(symv_tma_kernel<LARFG, SH>,
@@ -416,10 +442,10 @@ static void symv_tma_launch(cudaStream_t st, bool pdl, const TmaSched& s, const 
   }
   if (pdl) {
     launch_pdl(symv_tma_kernel<LARFG, SH>, dim3((unsigned)s.P), dim3(TT), RING_BYTES, st, map, off,
-               n, x, wcol, wrow, s.nbs, s.ncj, s.T, s.len, s.slots, lf);
+               n, d, x, wcol, wrow, s.nbs, s.ncj, s.T, s.len, s.slots, lf);
   } else {
     symv_tma_kernel<LARFG, SH><<<(unsigned)s.P, TT, RING_BYTES, st>>>(
-        map, off, n, x, wcol, wrow, s.nbs, s.ncj, s.T, s.len, s.slots, lf);
+        map, off, n, d, x, wcol, wrow, s.nbs, s.ncj, s.T, s.len, s.slots, lf);
     EM_LAUNCHED();
   }
 }
@@ -428,32 +454,39 @@ void symv_tma(cudaStream_t st, const SymvMap& m, int64_t off, int64_t n, double 
               const double* x, double beta, double* y, double* work, const SymvLarfg* lf,
               const LatrdT* lt, bool pdl) {
   if (n <= 0) return;
-  const TmaSched s = tma_sched(n);
+  // The tiles start on a 32-row boundary: the block at (off, off) is extended by d = off
+  // mod 32 leading rows and columns whose x entries are zero (their products vanish and
+  // their y rows are dropped). With a 256-byte aligned base and ld every TMA box then
+  // starts 256-byte aligned: 5.9 TB/s instead of 5.0 for 16..64-byte aligned boxes
+  // (tools/prof_kernels.py symvoff), and no odd-row box is needed.
+  const int64_t d = g_symv_align_off ? 0 : off % 32;
+  const int64_t offa = off - d, na = n + d;
+  const TmaSched s = tma_sched(na);
   double* wcol = work;
   double* wrow = work + s.nbs * s.ncj * WC;
   const SymvLarfg lfv = lf ? *lf : SymvLarfg{};
   const LatrdT ltv = lt ? *lt : LatrdT{};
   const CUtensorMap& map0 = reinterpret_cast<const CUtensorMap&>(m.opaque[0]);
   const CUtensorMap& map1 = reinterpret_cast<const CUtensorMap&>(m.opaque[1]);
-  if (lf) {
-    if (off & 1)
-      symv_tma_launch<true, 1>(st, pdl, s, map1, off, n, x, wcol, wrow, lfv);
+  if (offa & 1) {  // only without the alignment shift: a 130-row box from the row before
+    if (lf)
+      symv_tma_launch<true, 1>(st, pdl, s, map1, offa, n, d, x, wcol, wrow, lfv);
     else
-      symv_tma_launch<true, 0>(st, pdl, s, map0, off, n, x, wcol, wrow, lfv);
+      symv_tma_launch<false, 1>(st, pdl, s, map1, offa, n, d, x, wcol, wrow, lfv);
   } else {
-    if (off & 1)
-      symv_tma_launch<false, 1>(st, pdl, s, map1, off, n, x, wcol, wrow, lfv);
+    if (lf)
+      symv_tma_launch<true, 0>(st, pdl, s, map0, offa, n, d, x, wcol, wrow, lfv);
     else
-      symv_tma_launch<false, 0>(st, pdl, s, map0, off, n, x, wcol, wrow, lfv);
+      symv_tma_launch<false, 0>(st, pdl, s, map0, offa, n, d, x, wcol, wrow, lfv);
   }
   const unsigned extra = ltv.i > 0 ? 8u : 0u;
   if (pdl) {
     launch_pdl(symv_tma_reduce_kernel, dim3((unsigned)s.ncj + extra), dim3(512), 0, st, n, alpha,
                beta, y, (const double*)wcol, (const double*)wrow, s.nbs, s.ncj, s.len, s.slots,
-               ltv);
+               d, ltv);
   } else {
     symv_tma_reduce_kernel<<<(unsigned)s.ncj + extra, 512, 0, st>>>(
-        n, alpha, beta, y, wcol, wrow, s.nbs, s.ncj, s.len, s.slots, ltv);
+        n, alpha, beta, y, wcol, wrow, s.nbs, s.ncj, s.len, s.slots, d, ltv);
     EM_LAUNCHED();
   }
 }

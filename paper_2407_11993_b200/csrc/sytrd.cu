@@ -380,7 +380,7 @@ void sytrd_lower(cudaStream_t st, int64_t n, double* A, int64_t lda, double* d, 
                    (const double*)W.p, (int64_t)n, wtmp.p, (const double*)tvec.p,
                    (const double*)tau, (const double*)scale_buf, part_wv.p);
       gw_prev = gw;
-      nvav_prev = fusew ? symv_tma_ctas(m) : 0;
+      nvav_prev = fusew ? symv_tma_ctas(m, c + 1) : 0;
     }
     if (!last) col_launch(i0 + w, w, 0);  // finish W[:, w-1] for the trailing update
     if (use_graph) {

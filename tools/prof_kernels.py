@@ -100,6 +100,19 @@ def main(which):
                                                           0.0, nat.ptr(y))), reps=20)
             out[f"symv_{m}"] = {"us": t * 1e6, "GBps": 8 * m * m / 2 / t / 1e9}
         del big
+    if which == "symvoff":
+        # trailing-block symv at row/column offsets (alignment of the TMA boxes)
+        big = torch.randn(n, n, device="cuda", dtype=torch.float64, generator=g)
+        x = torch.randn(n, device="cuda", dtype=torch.float64, generator=g)
+        y = torch.empty_like(x)
+        m = n - 64
+        base = big.data_ptr()
+        for off in (0, 2, 4, 8, 16, 32, 1):
+            ptr = ctypes.c_void_p(base + 8 * off * (n + 1))
+            t = timed(lambda: nat.check(lib.em_symv_lower(ctx, m, 1.0, ptr, n, nat.ptr(x), 0.0,
+                                                          nat.ptr(y))), reps=20)
+            out[f"symv_off{off}"] = {"us": t * 1e6, "GBps": 8 * m * m / 2 / t / 1e9}
+        del big
     if which == "potrf":
         m = int(os.environ.get("POTRF_N", n))
         b = torch.randn(m, m, device="cuda", dtype=torch.float64, generator=g) / np.sqrt(m)
