@@ -203,19 +203,22 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
     EM_CK(cudaStreamSynchronize(st));
     return piv;
   }
-  DBuf B(nn, st);
+  // leading dimension padded to 32 doubles: every column of B starts 256-byte aligned,
+  // so all TMA boxes of the tridiagonalisation's symv are (symv_tma.cu)
+  const int64_t ldb = (n + 31) / 32 * 32;
+  DBuf B((size_t)ldb * n, st);
   {
     {
       // B = G^-1 L G^-T. The reference forms G^-1 (G^-1 L)^T with two full solves and
       // averages it with its transpose (modal.py:63-67); the two-sided recursive
       // reduction gives the same symmetric matrix to round-off with half the flops.
       Stage s(st, ST_SYGST);
-      copy_matrix(st, false, n, n, L, ldl, B.p, n);
-      mirror_lower(st, n, B.p, n);  // SymMatrix semantics: the lower triangle defines L
+      copy_matrix(st, false, n, n, L, ldl, B.p, ldb);
+      mirror_lower(st, n, B.p, ldb);  // SymMatrix semantics: the lower triangle defines L
       if (banded)
-        band_sygst(st, bc, B.p, n);  // the reference's X = G^-1 L, G^-1 X^T, (B + B^T)/2
+        band_sygst(st, bc, B.p, ldb);  // the reference's X = G^-1 L, G^-1 X^T, (B + B^T)/2
       else
-        sygst_lower(st, n, B.p, n, G, ldg, GDinv.p);
+        sygst_lower(st, n, B.p, ldb, G, ldg, GDinv.p);
     }
     // certificate only (modal.py:69-70), factored in the (still free) output buffer V
     {
@@ -234,7 +237,7 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
   // then the in-place descending reorder + sign fix): peak memory L, R, V + G, B and the
   // two D&C work matrices = 7 N^2 (8 with V^T R), so N = 50,000 fits one B200
   DBuf w(n, st);
-  syev_ascending(st, n, B.p, n, w.p, V, ldv);
+  syev_ascending(st, n, B.p, ldb, w.p, V, ldv);
   B.release();
   {
     Stage s(st, ST_TRSM_BACK);
