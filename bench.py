@@ -531,7 +531,8 @@ def td1_comparator(m, cfg, steps, n_rhs=1):
         "modal_vs_cholesky_end_to_end": None,  # filled by the caller
         "trsv_fwd_GBps": factor_bytes / (fwd[0] / fwd[1] * 1e-3) / 1e9 if fwd[1] else None,
         "trsv_bwd_GBps": factor_bytes / (bwd[0] / bwd[1] * 1e-3) / 1e9 if bwd[1] else None,
-        "symv_GBps": factor_bytes / (symv[0] / symv[1] * 1e-3) / 1e9 if symv[1] else None,
+        "r_product_ms_per_step": symv[0] / symv[1] if symv[1] else None,
+        "r_product": "CSR SpMV of the stencil R (dense symv when R is not sparse)",
         "hbm_peak_GBps": hbm,
     }
 

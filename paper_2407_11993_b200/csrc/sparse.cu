@@ -113,6 +113,27 @@ void csr_mm(cudaStream_t st, const Csr& a, int64_t m, const double* B, int64_t l
   EM_LAUNCHED();
 }
 
+// y = alpha A x + beta y, one thread per row; each row's nonzeros summed in increasing
+// column order (the reference's dense loop order with its exact-zero terms skipped)
+__global__ void csr_spmv_kernel(int64_t n, const int64_t* __restrict__ rowptr,
+                                const int* __restrict__ colidx, const double* __restrict__ val,
+                                double alpha, const double* __restrict__ x, double beta,
+                                double* __restrict__ y) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = 0.0;
+  for (int64_t p = rowptr[i]; p < rowptr[i + 1]; ++p) s += val[p] * x[colidx[p]];
+  y[i] = (beta == 0.0) ? alpha * s : fma(alpha, s, beta * y[i]);
+}
+
+void csr_spmv(cudaStream_t st, const Csr& a, double alpha, const double* x, double beta,
+              double* y) {
+  if (a.n <= 0) return;
+  csr_spmv_kernel<<<(unsigned)((a.n + 255) / 256), 256, 0, st>>>(a.n, a.rowptr.p, a.colidx.p,
+                                                                  a.val.p, alpha, x, beta, y);
+  EM_LAUNCHED();
+}
+
 // A (n x n, full storage) <- the matrix held in CSR (every other entry zero).
 void csr_to_dense(cudaStream_t st, const Csr& a, double* A, int64_t lda) {
   if (lda == a.n) {

@@ -26,6 +26,8 @@ struct em_td1_plan {
   int n_p = 0, n_s = 0, n_u = 0;
   double dt = 0, theta = 0;
   em::DBuf C, R, Dinv, DinvT, E, work, b, y, x;
+  em::Csr Rs;          // R as CSR when it is sparse (the stencil): R I is an SpMV
+  bool r_sparse = false;
   em::DArr<unsigned long long>* flags = nullptr;
   em::DArr<unsigned int>* counters = nullptr;
   unsigned long long epoch = 0;
@@ -310,6 +312,9 @@ int64_t td1_plan_init(em_td1_plan* P, const double* L, int64_t ldl, const double
   EM_LAUNCHED();
   const int64_t piv = potrf(st, n, P->C.p, n);
   if (piv >= 0) return piv;
+  // the stencil R: keep only its CSR (7 nonzeros per row) for the per-step R I
+  P->r_sparse = csr_from_dense(st, n, P->R.p, n, 0.02, P->Rs);
+  if (P->r_sparse) P->R.release();
   const int64_t nblk = (n + TS - 1) / TS;
   P->Dinv.alloc((size_t)nblk * TS * TS, st);
   trtri_blocks(st, TS, n, P->C.p, n, P->Dinv.p);
@@ -354,7 +359,10 @@ static void td1_solve_step(em_td1_plan* P, double* I, double* Icap_col) {
   // b += -dt R I
   {
     Stage s(st, ST_TD1_SYMV);
-    symv_lower(st, n, -P->dt, P->R.p, n, I, 1.0, P->b.p, P->work.p);
+    if (P->r_sparse)
+      csr_spmv(st, P->Rs, -P->dt, I, 1.0, P->b.p);
+    else
+      symv_lower(st, n, -P->dt, P->R.p, n, I, 1.0, P->b.p, P->work.p);
   }
   ++P->epoch;
   EM_CK(cudaMemsetAsync(P->counters->p, 0, 2 * sizeof(unsigned int), st));
