@@ -225,31 +225,42 @@ __global__ void __launch_bounds__(RT) td2_replay(
 #pragma unroll
   for (int i = 0; i < MT; ++i) acc[i][0] = acc[i][1] = 0.0;
 
+  // recurrence state of the thread's mode in the current chunk (threads tid < MC),
+  // loaded one chunk ahead so the global-load latency leaves the recurrence's chain
+  double s_nx = 0.0, e_nx = 0.0;
+  double w_nx[NU > 0 ? NU : 1];
+  auto load_state = [&](int64_t c) {
+    const int64_t m = c + tid;
+    const bool live = m < m_end;
+    s_nx = live ? S[b * n + m] : 0.0;
+    e_nx = live ? eps[m] : 0.0;
+    if (NU > 0) {
+#pragma unroll
+      for (int j = 0; j < (NU > 0 ? NU : 1); ++j) w_nx[j] = live ? W[m + j * n] : 0.0;
+    }
+  };
+  if (tid < MC) load_state(m_begin);
   for (int64_t c0 = m_begin; c0 < m_end; c0 += MC) {
     __syncthreads();  // previous chunk's fragments consumed (and Us staged on entry)
-    // CV chunk -> Cs[mode][o]
-    for (int i = tid; i < MC * cvs; i += RT) {
-      const int mm = i / cvs, o = i % cvs;
-      const int64_t m = c0 + mm;
-      Cs[i] = (o < n_obs && m < m_end) ? CV[o + m * (int64_t)ldcv] : 0.0;
-    }
-    // recurrence: thread tid < MC owns mode c0 + tid
-    if (tid < MC) {
-      const int64_t m = c0 + tid;
-      double s = 0.0, e = 0.0;
-      double w[NU > 0 ? NU : 1];
-      const bool live = m < m_end;
-      if (live) {
-        s = S[b * n + m];
-        e = eps[m];
-        if (NU > 0) {
-#pragma unroll
-          for (int j = 0; j < (NU > 0 ? NU : 1); ++j) w[j] = W[m + j * n];
-        }
-      } else if (NU > 0) {
-#pragma unroll
-        for (int j = 0; j < (NU > 0 ? NU : 1); ++j) w[j] = 0.0;
+    if (tid >= MC) {
+      // CV chunk -> Cs[mode][o] by the warps that do not run the recurrence (their
+      // load latency overlaps it): warp-rows of modes, lanes along the observables
+      const int lw = (tid - MC) >> 5, nlw = (RT - MC) >> 5;
+      for (int mm = lw; mm < MC; mm += nlw) {
+        const int64_t m = c0 + mm;
+        const bool live = m < m_end;
+        for (int o = lane; o < cvs; o += 32)
+          Cs[mm * cvs + o] = (o < n_obs && live) ? CV[o + m * (int64_t)ldcv] : 0.0;
       }
+    } else {
+      // recurrence: thread tid < MC owns mode c0 + tid
+      const int64_t m = c0 + tid;
+      const bool live = m < m_end;
+      double s = s_nx, e = e_nx;
+      double w[NU > 0 ? NU : 1];
+#pragma unroll
+      for (int j = 0; j < (NU > 0 ? NU : 1); ++j) w[j] = w_nx[j];
+      if (c0 + MC < m_end) load_state(c0 + MC);
       for (int k = 0; k < TB; ++k) {
         double gk;
         if (NU > 0) {
