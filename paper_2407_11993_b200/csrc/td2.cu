@@ -221,9 +221,18 @@ __global__ void __launch_bounds__(RT) td2_replay(
   stage_inputs(Us, U, T, n_u, b);
   const int len = (int)imin64(TB, T - b * TB);
 
-  double acc[MT][2];
+  // warp tile: WM x 4 warps over (observables x time); each warp MTW m-tiles x NTW
+  // n-tiles of 8 x 8 (MT >= 2: half the observables x 16 steps, fewer shared-memory
+  // fragment loads per DMMA than all observables x 8 steps)
+  constexpr int WM = MT >= 2 ? 2 : 1;
+  constexpr int MTW = MT / WM;
+  constexpr int NTW = (TB / 8) / (8 / WM);
+  const int wm = warp / (8 / WM), wn = warp % (8 / WM);
+  double acc[MTW][NTW][2];
 #pragma unroll
-  for (int i = 0; i < MT; ++i) acc[i][0] = acc[i][1] = 0.0;
+  for (int i = 0; i < MTW; ++i)
+#pragma unroll
+    for (int jn = 0; jn < NTW; ++jn) acc[i][jn][0] = acc[i][jn][1] = 0.0;
 
   // recurrence state of the thread's mode in the current chunk (threads tid < MC),
   // loaded one chunk ahead so the global-load latency leaves the recurrence's chain
@@ -279,29 +288,35 @@ __global__ void __launch_bounds__(RT) td2_replay(
       }
     }
     __syncthreads();
-    // DMMA: warp w owns time columns [8w, 8w+8)
+    // DMMA: warp (wm, wn) owns m-tiles [wm MTW, (wm+1) MTW) and time columns
+    // [8 NTW wn, 8 NTW (wn+1))
 #pragma unroll 4
     for (int kb = 0; kb < MC; kb += 4) {
-      const double bf = Qs[(warp * 8 + g) * QS + kb + t];
+      double bf[NTW];
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
-        const double af = Cs[(kb + t) * cvs + mt * 8 + g];
-        dmma884(acc[mt][0], acc[mt][1], af, bf);
+      for (int jn = 0; jn < NTW; ++jn) bf[jn] = Qs[((wn * NTW + jn) * 8 + g) * QS + kb + t];
+#pragma unroll
+      for (int mt = 0; mt < MTW; ++mt) {
+        const double af = Cs[(kb + t) * cvs + (wm * MTW + mt) * 8 + g];
+#pragma unroll
+        for (int jn = 0; jn < NTW; ++jn) dmma884(acc[mt][jn][0], acc[mt][jn][1], af, bf[jn]);
       }
     }
   }
-  // epilogue: rows o = mt*8+g, time k = b*TB + 8*warp + 2t + e
+  // epilogue: rows o = (wm MTW + mt) 8 + g, time k = b TB + (wn NTW + jn) 8 + 2t + e
 #pragma unroll
-  for (int mt = 0; mt < MT; ++mt) {
-    const int o = mt * 8 + g;
+  for (int mt = 0; mt < MTW; ++mt) {
+    const int o = (wm * MTW + mt) * 8 + g;
     if (o >= n_obs) continue;
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int64_t kg = b * TB + warp * 8 + 2 * t + e;
-      if (kg >= T || ((kg + 1) % stride) != 0) continue;
-      const int64_t cap = (kg + 1) / stride - 1;
-      Yout[blockIdx.y * ldy_split + cap * n_obs + o] = acc[mt][e];
-    }
+    for (int jn = 0; jn < NTW; ++jn)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t kg = b * TB + (wn * NTW + jn) * 8 + 2 * t + e;
+        if (kg >= T || ((kg + 1) % stride) != 0) continue;
+        const int64_t cap = (kg + 1) / stride - 1;
+        Yout[blockIdx.y * ldy_split + cap * n_obs + o] = acc[mt][jn][e];
+      }
   }
 }
 

@@ -160,3 +160,31 @@ def test_banded_r_not_pd_reports_the_dense_pivot():
         res.append((rc, piv, which))
     nat.check(lib.em_config(ctx, 2, 0))
     assert res[0] == res[1] == (nat.EM_ERR_NOT_PD, 700, 0)
+
+
+def test_banded_path_l_certificate_errors_and_order():
+    """With a banded R (banded factor, dense L certificate): a non-SPD L
+    still reports the dense path's pivot with which = 1, and a non-SPD R still wins
+    (the reference checks R first, modal.py:61-70)."""
+    from paper_2407_11993_b200 import _native as nat
+    from paper_2407_11993_b200.synth import device_plate_model
+    m = device_plate_model(32, 16, 4, n_ports=0, n_sources=0, n_obs=1)
+    n = m["l_i"].shape[0]
+    L = m["l_i"].clone()
+    L[900, 900] = -1.0
+    lib, ctx = nat.load_library(), nat.context()
+    res = []
+    for off in (1, 0):
+        nat.check(lib.em_config(ctx, 2, off))
+        rc, piv, which, _ = _sygv_dev(L, m["r_i"], n)
+        res.append((rc, piv, which))
+    assert res[0] == res[1] and res[1][0] == nat.EM_ERR_NOT_PD and res[1][2] == 1
+    R = m["r_i"].clone()
+    R[300, 300] = -1.0
+    rc, piv, which, _ = _sygv_dev(L, R, n)
+    nat.check(lib.em_config(ctx, 2, 0))
+    assert (rc, piv, which) == (nat.EM_ERR_NOT_PD, 300, 0)
+    # and a clean solve right after the failed calls
+    rc, _, _, (tau, _, _, _) = _sygv_dev(m["l_i"], m["r_i"], n)
+    nat.check(rc)
+    assert np.all(tau > 0)
