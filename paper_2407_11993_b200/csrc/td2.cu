@@ -234,59 +234,75 @@ __global__ void __launch_bounds__(RT) td2_replay(
 #pragma unroll
     for (int jn = 0; jn < NTW; ++jn) acc[i][jn][0] = acc[i][jn][1] = 0.0;
 
-  // recurrence state of the thread's mode in the current chunk (threads tid < MC),
-  // loaded one chunk ahead so the global-load latency leaves the recurrence's chain
-  double s_nx = 0.0, e_nx = 0.0;
-  double w_nx[NU > 0 ? NU : 1];
-  auto load_state = [&](int64_t c) {
-    const int64_t m = c + tid;
-    const bool live = m < m_end;
-    s_nx = live ? S[b * n + m] : 0.0;
-    e_nx = live ? eps[m] : 0.0;
-    if (NU > 0) {
-#pragma unroll
-      for (int j = 0; j < (NU > 0 ? NU : 1); ++j) w_nx[j] = live ? W[m + j * n] : 0.0;
-    }
-  };
-  if (tid < MC) load_state(m_begin);
+  // Recurrence split over the whole CTA: thread (mode mm = tid % MC, quarter qq = tid / MC)
+  // scans its NQ = TB / 4 steps from zero (local values l_k, end value L_qq), the quarter
+  // start states follow from S_{q+1} = a^NQ S_q + L_q (a = 1 - eps), and every value is
+  // fixed up as s_k = l_k + a^(k - k_q + 1) S_q: a sequential chain of NQ + 3 + NQ steps
+  // on all eight warps instead of TB steps on two.
+  static_assert(RT == 4 * MC, "four threads per mode");
+  constexpr int NQ = TB / 4;
+  __shared__ double Lend[4][MC];
+  const int mm = tid % MC, qq = tid / MC;
   for (int64_t c0 = m_begin; c0 < m_end; c0 += MC) {
     __syncthreads();  // previous chunk's fragments consumed (and Us staged on entry)
-    if (tid >= MC) {
-      // CV chunk -> Cs[mode][o] by the warps that do not run the recurrence (their
-      // load latency overlaps it): warp-rows of modes, lanes along the observables
-      const int lw = (tid - MC) >> 5, nlw = (RT - MC) >> 5;
-      for (int mm = lw; mm < MC; mm += nlw) {
-        const int64_t m = c0 + mm;
+    // CV chunk -> Cs[mode][o]: asynchronous copies (no registers, overlap the scan)
+    {
+      const int nw = RT >> 5;
+      for (int r = warp; r < MC; r += nw) {
+        const int64_t m = c0 + r;
         const bool live = m < m_end;
-        for (int o = lane; o < cvs; o += 32)
-          Cs[mm * cvs + o] = (o < n_obs && live) ? CV[o + m * (int64_t)ldcv] : 0.0;
-      }
-    } else {
-      // recurrence: thread tid < MC owns mode c0 + tid
-      const int64_t m = c0 + tid;
-      const bool live = m < m_end;
-      double s = s_nx, e = e_nx;
-      double w[NU > 0 ? NU : 1];
-#pragma unroll
-      for (int j = 0; j < (NU > 0 ? NU : 1); ++j) w[j] = w_nx[j];
-      if (c0 + MC < m_end) load_state(c0 + MC);
-      for (int k = 0; k < TB; ++k) {
-        double gk;
-        if (NU > 0) {
-          gk = forcing<NU>(w, Us + k * n_u, n_u);
-        } else {
-          gk = 0.0;
-          if (live)
-            for (int j = 0; j < n_u; ++j) gk = fma(W[m + j * n], Us[k * n_u + j], gk);
+        for (int o = lane; o < cvs; o += 32) {
+          double* dst = Cs + r * cvs + o;
+          const bool ok = o < n_obs && live;
+          cp_async8(dst, ok ? CV + o + m * (int64_t)ldcv : CV, ok);  // zero fill otherwise
         }
-        s = fma(-e, s, s) + gk;
-        if (k >= len) s = 0.0;
-        Qs[k * QS + tid] = s;
-        const int64_t kg = b * TB + k;
-        if (Qcap && live && k < len && ((kg + 1) % stride) == 0)
-          Qcap[m + ((kg + 1) / stride - 1) * n] = s;
       }
+      cp_async_commit();
     }
+    const int64_t m = c0 + mm;
+    const bool live = m < m_end;
+    const double e = live ? eps[m] : 0.0;
+    const double s0 = live ? S[b * n + m] : 0.0;
+    double w[NU > 0 ? NU : 1];
+    if (NU > 0) {
+#pragma unroll
+      for (int j = 0; j < (NU > 0 ? NU : 1); ++j) w[j] = live ? W[m + j * n] : 0.0;
+    }
+    const int k0 = qq * NQ;
+    double l = 0.0;
+#pragma unroll 4
+    for (int kk = 0; kk < NQ; ++kk) {
+      const int k = k0 + kk;
+      double gk;
+      if (NU > 0) {
+        gk = forcing<NU>(w, Us + k * n_u, n_u);
+      } else {
+        gk = 0.0;
+        if (live)
+          for (int j = 0; j < n_u; ++j) gk = fma(W[m + j * n], Us[k * n_u + j], gk);
+      }
+      l = fma(-e, l, l) + gk;
+      Qs[k * QS + mm] = l;
+    }
+    Lend[qq][mm] = l;
+    __syncthreads();
+    const double a = 1.0 - e;
+    const double aq = decay_pow(e, NQ);
+    double sq = s0;
+    for (int q = 0; q < qq; ++q) sq = fma(aq, sq, Lend[q][mm]);
+    double pw = a;
+#pragma unroll 4
+    for (int kk = 0; kk < NQ; ++kk) {
+      const int k = k0 + kk;
+      double v = fma(pw, sq, Qs[k * QS + mm]);
+      pw *= a;
+      if (k >= len) v = 0.0;
+      Qs[k * QS + mm] = v;
+      const int64_t kg = b * TB + k;
+      if (Qcap && live && k < len && ((kg + 1) % stride) == 0)
+        Qcap[m + ((kg + 1) / stride - 1) * n] = v;
+    }
+    cp_async_wait<0>();
     __syncthreads();
     // DMMA: warp (wm, wn) owns m-tiles [wm MTW, (wm+1) MTW) and time columns
     // [8 NTW wn, 8 NTW (wn+1))
