@@ -440,6 +440,23 @@ def run_ours(args, cfg, rank, world, local_rank):
     rl = symv_roofline(m, n, peaks)
     rl["stage"] = "sytrd"
     rl["stage_roofline"] = stage_rl
+    # the modal stepping (north-star (b)): the fused replay is DMMA-bound on the observable
+    # reconstruction, 2 n_obs flop per mode-step (nothing N x T reaches HBM)
+    if "td2_replay" in stages:
+        ms_rep = stages["td2_replay"][0] / n_steps_timed
+        fl = 2.0 * cfg["n_obs"] * units
+        rl["stepping_roofline"] = {
+            "kernel": "td2_replay (fused forcing + recurrence + DMMA reconstruction)",
+            "bound": "tensor", "unit": "TFLOP/s",
+            "achieved": fl / (ms_rep * 1e-3) / 1e12 if ms_rep > 0 else None,
+            "peak": peaks.get("fp64_tflops", 37.1),
+            "frac": (fl / (ms_rep * 1e-3) / 1e12) / peaks.get("fp64_tflops", 37.1)
+            if ms_rep > 0 else None,
+            "algorithmic_flop_per_step": fl, "ms_per_step": ms_rep,
+            "peak_source": "DMMA issue peak measured on this pool (profiles/r01_fp64_peaks.jsonl)",
+            "mode_steps_per_s": units / ((stages["td2_replay"][0] + stages.get("td2_local", (0, 0))[0]
+                                          + stages.get("td2_carry", (0, 0))[0]) / n_steps_timed
+                                         * 1e-3)}
 
     # ---- TD1 comparator (bounded: a few hundred steps, extrapolated) and CPU baseline
     extra = {}
