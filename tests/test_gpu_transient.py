@@ -305,3 +305,60 @@ def test_mode_sharded_sweep_on_device():
     assert y.shape == ref.shape
     assert rel_l2(y, ref) < 1e-12
     assert rel_l2(y.sum(axis=0), g["td2_obs_theta0.5"]) < TOL
+
+
+@pytest.mark.parametrize("theta", [1.0, 0.5])
+def test_c2_full_size_td1_equals_td2(theta):
+    """BASELINE configs[1] at its full size (N = 16,384 plate, electrode ramp, dt = 5e-7,
+    32 observables), where no CPU oracle finishes: the two independent device paths —
+    banded-R eigensolve + modal scan vs the Cholesky theta-method (dense factor of
+    L + dt theta R, triangular solves) — must agree to the north-star 1e-8 relative L2
+    over the first 500 steps, and every current density (captured states) too."""
+    import ctypes
+    import torch
+    from paper_2407_11993_b200 import _native as nat
+    from paper_2407_11993_b200.synth import device_plate_model, drive_table
+    m = device_plate_model(64, 64, 4, n_ports=1, n_sources=0, n_obs=32)
+    n = m["l_i"].shape[0]
+    steps, dt = 500, 5e-7
+    i_d, _ = drive_table("ramp5us", steps, dt, 1, 0)
+    lib, ctx = nat.load_library(), nat.context()
+    tau, ln, rn, V = nat.empty(n), nat.empty(n), nat.empty(n), nat.empty(n, n)
+    piv, which = ctypes.c_int64(-1), ctypes.c_int(-1)
+    nat.check(lib.em_sygv_ex(ctx, n, nat.ptr(m["l_i"]), n, nat.ptr(m["r_i"]), n, nat.ptr(tau),
+                             nat.ptr(V), n, nat.ptr(ln), nat.ptr(rn), None, n, 1,
+                             ctypes.byref(piv), ctypes.byref(which)), "em_sygv_ex")
+    drv = torch.cat([m["r_d"], m["l_d"]], dim=0).contiguous()      # (2, n): [R_D | L_D]
+    P = nat.empty(2, n)
+    nat.check(lib.em_dgemm(ctx, 1, 0, n, 2, n, 1.0, nat.ptr(V), n, nat.ptr(drv), n, 0.0,
+                           nat.ptr(P), n))
+    c_dev = nat.device_colmajor(m["c"])
+    CV = nat.empty(n, 32)
+    nat.check(lib.em_dgemm(ctx, 0, 0, 32, n, n, 1.0, nat.ptr(c_dev), 32, nat.ptr(V), n, 0.0,
+                           nat.ptr(CV), 32))
+    table = nat.device_vector(np.ascontiguousarray(i_d).reshape(-1))
+    plan = ctypes.c_void_p()
+    nat.check(lib.em_td2_plan_create(ctx, n, 1, 0, nat.ptr(ln), nat.ptr(rn), nat.ptr(P[0:1]),
+                                     nat.ptr(P[1:2]), nat.ptr(P[0:1]), dt, theta,
+                                     ctypes.byref(plan)))
+    nat.check(lib.em_td2_set_observables(plan, 32, nat.ptr(CV), 32, None, 0))
+    q = nat.zeros(n)
+    y2 = nat.empty(steps, 32)
+    qcap = nat.empty(steps, n)
+    nat.check(lib.em_td2_run(plan, steps, nat.ptr(table), nat.ptr(q), nat.ptr(y2), 1,
+                             nat.ptr(qcap)))
+    lib.em_td2_plan_destroy(plan)
+    icap2 = (qcap @ V).cpu().numpy()   # currents I = V q per step (V column-major)
+    plan1 = ctypes.c_void_p()
+    nat.check(lib.em_td1_plan_create(ctx, n, 1, 0, nat.ptr(m["l_i"]), n, nat.ptr(m["r_i"]), n,
+                                     nat.ptr(m["r_d"]), nat.ptr(m["l_d"]), None, dt, theta,
+                                     ctypes.byref(plan1), ctypes.byref(piv)))
+    nat.check(lib.em_td1_set_observables(plan1, 32, nat.ptr(c_dev), 32, None, 0))
+    cur = nat.zeros(n)
+    y1 = nat.empty(steps, 32)
+    icap1 = nat.empty(steps, n)
+    nat.check(lib.em_td1_run(plan1, steps, nat.ptr(table), nat.ptr(cur), nat.ptr(y1), 1,
+                             nat.ptr(icap1)))
+    lib.em_td1_plan_destroy(plan1)
+    assert rel_l2(y2.cpu().numpy(), y1.cpu().numpy()) < 1e-8
+    assert rel_l2(icap2, icap1.cpu().numpy()) < 1e-8
