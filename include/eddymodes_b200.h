@@ -58,6 +58,11 @@ int em_synchronize(em_ctx* ctx);
 /* EM_CFG_BAND_OFF: 1 = always factor R densely (default 0: a banded R, lower bandwidth
  * b with 4 (b + 128) <= n, takes the banded Cholesky and banded solves). */
 #define EM_CFG_BAND_OFF 2
+/* EM_CFG_SYMV_L2_KEEP_MB: megabytes of the bottom-right block of a tridiagonalised
+ * matrix that the per-column symv loads with the L2 evict_last policy (re-read from the
+ * 126 MB L2 by every later column instead of HBM); every other tile is loaded
+ * evict_first. Default 32; 0 = evict_first everywhere; < 0 = no cache hint. */
+#define EM_CFG_SYMV_L2_KEEP_MB 3
 int em_config(em_ctx* ctx, int key, int64_t value);
 /* Stage timers (CUDA events on the context stream). em_profile(ctx, 1) clears and
  * enables them; em_stage_times fills per-stage milliseconds / event-pair counts

@@ -18,6 +18,7 @@ extern int64_t g_two_stage_min;
 extern int g_sytrd_dbg;
 extern int g_band_off;
 extern int g_symv_align_off;
+extern int64_t g_symv_keep_mb;
 void stages_reset(bool on);
 void stages_level(int level);
 int stages_read(double* ms, int64_t* counts, int n);
@@ -135,6 +136,10 @@ int em_config(em_ctx* ctx, int key, int64_t value) {
     }
     if (key == EM_CFG_BAND_OFF) {
       em::g_band_off = value ? 1 : 0;
+      return EM_OK;
+    }
+    if (key == EM_CFG_SYMV_L2_KEEP_MB) {
+      em::g_symv_keep_mb = value;
       return EM_OK;
     }
     if (key == 98) {  // debug: sytrd switches (bit0 no TMA symv, bit1 no PDL, bit2 no graph,

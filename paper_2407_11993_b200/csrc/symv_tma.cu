@@ -101,6 +101,7 @@ int64_t symv_tma_ctas(int64_t n, int64_t off) {
   return tma_sched(n + (g_symv_align_off ? 0 : off % 32)).P;
 }
 int g_symv_align_off = 0;  // em_config debug key 98 bit 4: no 32-row alignment shift
+int64_t g_symv_keep_mb = 32;  // EM_CFG_SYMV_L2_KEEP_MB (A/B at N = 16k: 0 -> 32 MB saves ~10 ms)
 
 size_t symv_tma_work_size(int64_t n) {
   const TmaSched s = tma_sched(n);
@@ -137,12 +138,31 @@ EM_DEVINL void mbar_wait(uint64_t* bar, unsigned parity) {
       "r"(parity)
       : "memory");
 }
-EM_DEVINL void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+EM_DEVINL void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
+                           uint64_t pol) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_u32(dst)),
-      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      ".L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
+}
+// L2 policies: the bottom-right block of the matrix (read by every column's symv of a
+// tridiagonalisation) is loaded evict_last, everything else evict_first, so the part of
+// the trailing matrix that fits in the 126 MB L2 is re-read from L2, not HBM.
+EM_DEVINL uint64_t pol_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+EM_DEVINL uint64_t pol_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+EM_DEVINL uint64_t pol_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
 }
 
 // x of the block extended by d leading rows/columns (see symv_tma): xd = x - d, na = n + d;
@@ -174,7 +194,8 @@ __global__ void __launch_bounds__(TT, 1) symv_tma_kernel(const __grid_constant__
                                                          double* __restrict__ wcol,
                                                          double* __restrict__ wrow, int64_t nbs,
                                                          int64_t ncj, int64_t T, int64_t len,
-                                                         int64_t slots, SymvLarfg lf) {
+                                                         int64_t slots, int64_t keep_c0,
+                                                         SymvLarfg lf) {
   extern __shared__ __align__(128) double ring[];
   __shared__ uint64_t full[NST], empty[NST];
   __shared__ double red[TT / 32][HR];
@@ -199,13 +220,18 @@ __global__ void __launch_bounds__(TT, 1) symv_tma_kernel(const __grid_constant__
   auto tiles_in = [&](int64_t ii) { return imin64(2 * ii + 2, ncj); };
   int64_t i = tstrip_of(t0, nbs), j = t0 - i * (i + 1);
   int64_t pi = i, pj = j;  // producer cursor (thread 0)
+  const uint64_t pkeep = pol_evict_last();
+  const uint64_t pstream = keep_c0 == INT64_MIN ? pol_evict_normal() : pol_evict_first();
+  auto pol_of = [&](int64_t cj) {
+    return keep_c0 != INT64_MIN && off + WC * cj >= keep_c0 ? pkeep : pstream;
+  };
   // prologue: the first NST-1 tiles (A is not written by the launch this one may overlap)
   if (tid == 0) {
     for (int s = 0; s < NST - 1; ++s) {
       if (t0 + s < t1) {
         mbar_expect_tx(&full[s], tile_bytes<SH>());
         tma_load_2d(ring + (size_t)s * BR * WC, &map, (int)(off + HR * pi - SH),
-                    (int)(off + WC * pj), &full[s]);
+                    (int)(off + WC * pj), &full[s], pol_of(pj));
       }
       if (pj + 1 < tiles_in(pi)) ++pj; else { ++pi; pj = 0; }
     }
@@ -254,7 +280,7 @@ __global__ void __launch_bounds__(TT, 1) symv_tma_kernel(const __grid_constant__
       if (kp >= NST) mbar_wait(&empty[ps], (unsigned)((kp / NST - 1) & 1));
       mbar_expect_tx(&full[ps], tile_bytes<SH>());
       tma_load_2d(ring + (size_t)ps * BR * WC, &map, (int)(off + HR * pi - SH),
-                  (int)(off + WC * pj), &full[ps]);
+                  (int)(off + WC * pj), &full[ps], pol_of(pj));
       if (pj + 1 < tiles_in(pi)) ++pj; else { ++pi; pj = 0; }
     }
     const int64_t r0 = i * HR, c0 = j * WC;
@@ -342,7 +368,8 @@ __global__ void __launch_bounds__(TT, 1) symv_tma_kernel(const __grid_constant__
       if ((lane & 7) == 0) {
         const int cc = (h16 ? 2 : 0) + (h8 ? 1 : 0);
         wcol[(i * ncj + j) * WC + 4 * w + cc] = v;
-        if (want_vav) vav = fma(v, xj[cc], vav);
+        // (selects, not xj[cc]: a runtime index would put xj in local memory)
+        if (want_vav) vav = fma(v, h16 ? (h8 ? xj[3] : xj[2]) : (h8 ? xj[1] : xj[0]), vav);
       }
     }
     if (j + 1 == tiles_in(i) || t + 1 == t1) {  // end of this CTA's piece of strip i
@@ -433,7 +460,7 @@ __global__ void __launch_bounds__(512) symv_tma_reduce_kernel(int64_t n, double 
 template <bool LARFG, int SH>
 static void symv_tma_launch(cudaStream_t st, bool pdl, const TmaSched& s, const CUtensorMap& map,
                             int64_t off, int64_t n, int64_t d, const double* x, double* wcol,
-                            double* wrow, const SymvLarfg& lf) {
+                            double* wrow, int64_t keep_c0, const SymvLarfg& lf) {
   static bool attr = false;
   if (!attr) {
     EM_CK(cudaFuncSetAttribute(symv_tma_kernel<LARFG, SH>,
@@ -442,10 +469,10 @@ static void symv_tma_launch(cudaStream_t st, bool pdl, const TmaSched& s, const 
   }
   if (pdl) {
     launch_pdl(symv_tma_kernel<LARFG, SH>, dim3((unsigned)s.P), dim3(TT), RING_BYTES, st, map, off,
-               n, d, x, wcol, wrow, s.nbs, s.ncj, s.T, s.len, s.slots, lf);
+               n, d, x, wcol, wrow, s.nbs, s.ncj, s.T, s.len, s.slots, keep_c0, lf);
   } else {
     symv_tma_kernel<LARFG, SH><<<(unsigned)s.P, TT, RING_BYTES, st>>>(
-        map, off, n, d, x, wcol, wrow, s.nbs, s.ncj, s.T, s.len, s.slots, lf);
+        map, off, n, d, x, wcol, wrow, s.nbs, s.ncj, s.T, s.len, s.slots, keep_c0, lf);
     EM_LAUNCHED();
   }
 }
@@ -468,16 +495,22 @@ void symv_tma(cudaStream_t st, const SymvMap& m, int64_t off, int64_t n, double 
   const LatrdT ltv = lt ? *lt : LatrdT{};
   const CUtensorMap& map0 = reinterpret_cast<const CUtensorMap&>(m.opaque[0]);
   const CUtensorMap& map1 = reinterpret_cast<const CUtensorMap&>(m.opaque[1]);
+  // L2 retention: the last `keep` columns of the block (their lower part is ~4 keep^2
+  // bytes) stay in L2 between launches; 0 = stream everything
+  const int64_t keep = (int64_t)sqrt((double)g_symv_keep_mb * 1e6 / 4.0);
+  const int64_t keep_c0 = g_symv_keep_mb > 0    ? off + n - keep
+                          : g_symv_keep_mb == 0 ? INT64_MAX   // evict_first everywhere
+                                                : INT64_MIN;  // < 0: no hint (evict_normal)
   if (offa & 1) {  // only without the alignment shift: a 130-row box from the row before
     if (lf)
-      symv_tma_launch<true, 1>(st, pdl, s, map1, offa, n, d, x, wcol, wrow, lfv);
+      symv_tma_launch<true, 1>(st, pdl, s, map1, offa, n, d, x, wcol, wrow, keep_c0, lfv);
     else
-      symv_tma_launch<false, 1>(st, pdl, s, map1, offa, n, d, x, wcol, wrow, lfv);
+      symv_tma_launch<false, 1>(st, pdl, s, map1, offa, n, d, x, wcol, wrow, keep_c0, lfv);
   } else {
     if (lf)
-      symv_tma_launch<true, 0>(st, pdl, s, map0, offa, n, d, x, wcol, wrow, lfv);
+      symv_tma_launch<true, 0>(st, pdl, s, map0, offa, n, d, x, wcol, wrow, keep_c0, lfv);
     else
-      symv_tma_launch<false, 0>(st, pdl, s, map0, offa, n, d, x, wcol, wrow, lfv);
+      symv_tma_launch<false, 0>(st, pdl, s, map0, offa, n, d, x, wcol, wrow, keep_c0, lfv);
   }
   const unsigned extra = ltv.i > 0 ? 8u : 0u;
   if (pdl) {

@@ -10,6 +10,8 @@
 // latrd_col_kernel (finish the previous W column, update this column, partials of
 // its norm and of the panel products), the symv with dlarfg folded into its
 // prologue, the symv reduction (+ panel products t), latrd_w_kernel.
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -318,6 +320,9 @@ void sytrd_lower(cudaStream_t st, int64_t n, double* A, int64_t lda, double* d, 
   // which cannot be captured); the graph itself is launched on st
   cudaStream_t sc = st;
   if (use_graph) EM_CK(cudaStreamCreateWithFlags(&sc, cudaStreamNonBlocking));
+  // debug (EM_SYTRD_PANEL_TIMES set): per-panel chain times printed to stderr
+  const bool ptimes = getenv("EM_SYTRD_PANEL_TIMES") != nullptr;
+  std::vector<cudaEvent_t> pev;
   for (int64_t i0 = 0; i0 < n; i0 += TRD_NB) {
     const int w = (int)imin64(TRD_NB, n - i0);
     if (use_graph) EM_CK(cudaStreamBeginCapture(sc, cudaStreamCaptureModeThreadLocal));
@@ -397,7 +402,14 @@ void sytrd_lower(cudaStream_t st, int64_t n, double* A, int64_t lda, double* d, 
         }
       }
       if (!ok) EM_CK(cudaGraphInstantiate(&exec, g, 0));
+      if (ptimes) {
+        pev.resize(pev.size() + 2);
+        cudaEventCreate(&pev[pev.size() - 2]);
+        cudaEventCreate(&pev.back());
+        cudaEventRecord(pev[pev.size() - 2], st);
+      }
       EM_CK(cudaGraphLaunch(exec, st));
+      if (ptimes) cudaEventRecord(pev.back(), st);
       cudaGraphDestroy(g);
     }
     const int64_t t0 = i0 + w;
@@ -418,6 +430,14 @@ void sytrd_lower(cudaStream_t st, int64_t n, double* A, int64_t lda, double* d, 
   if (exec) {
     EM_CK(cudaStreamSynchronize(st));
     cudaGraphExecDestroy(exec);
+  }
+  for (size_t k = 0; k + 1 < pev.size(); k += 2) {
+    float t = 0.f;
+    cudaEventElapsedTime(&t, pev[k], pev[k + 1]);
+    fprintf(stderr, "sytrd_panel %zu m %lld ms %.4f\n", k / 2,
+            (long long)(n - (int64_t)(k / 2) * TRD_NB), t);
+    cudaEventDestroy(pev[k]);
+    cudaEventDestroy(pev[k + 1]);
   }
   if (use_graph) cudaStreamDestroy(sc);
 }

@@ -105,9 +105,10 @@ def main(which):
         big = torch.randn(n, n, device="cuda", dtype=torch.float64, generator=g)
         x = torch.randn(n, device="cuda", dtype=torch.float64, generator=g)
         y = torch.empty_like(x)
-        m = n - 64
+        m = n - 256
         base = big.data_ptr()
-        for off in (0, 2, 4, 8, 16, 32, 1):
+        offs = [int(v) for v in os.environ.get("SYMV_OFFS", "0,2,4,8,16,32,1").split(",")]
+        for off in offs:
             ptr = ctypes.c_void_p(base + 8 * off * (n + 1))
             t = timed(lambda: nat.check(lib.em_symv_lower(ctx, m, 1.0, ptr, n, nat.ptr(x), 0.0,
                                                           nat.ptr(y))), reps=20)
@@ -135,6 +136,8 @@ def main(which):
         m = int(os.environ.get("SYEV_N", n))
         if "SYTRD_DBG" in os.environ:  # em_config debug key 98 (sytrd switches)
             nat.check(lib.em_config(ctx, 98, int(os.environ["SYTRD_DBG"])))
+        if "SYMV_KEEP_MB" in os.environ:  # EM_CFG_SYMV_L2_KEEP_MB
+            nat.check(lib.em_config(ctx, 3, int(os.environ["SYMV_KEEP_MB"])))
         b = torch.randn(m, m, device="cuda", dtype=torch.float64, generator=g)
         a = (b + b.T).contiguous()
         del b
