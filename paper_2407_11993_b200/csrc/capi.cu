@@ -19,6 +19,7 @@ extern int g_sytrd_dbg;
 extern int g_band_off;
 extern int g_symv_align_off;
 extern int64_t g_symv_keep_mb;
+extern int64_t g_gemm_cfg;
 void stages_reset(bool on);
 void stages_level(int level);
 int stages_read(double* ms, int64_t* counts, int n);
@@ -140,6 +141,10 @@ int em_config(em_ctx* ctx, int key, int64_t value) {
     }
     if (key == EM_CFG_SYMV_L2_KEEP_MB) {
       em::g_symv_keep_mb = value;
+      return EM_OK;
+    }
+    if (key == 96) {  // debug: GEMM tile configuration (0 auto, 2 64x64, 3 128x64)
+      em::g_gemm_cfg = value;
       return EM_OK;
     }
     if (key == 98) {  // debug: sytrd switches (bit0 no TMA symv, bit1 no PDL, bit2 no graph,

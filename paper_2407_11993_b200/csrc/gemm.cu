@@ -15,37 +15,57 @@
 
 namespace em {
 
-constexpr int GBM = 128, GBN = 64, GBK = 16, GTHREADS = 256, GMINB = 2;
-constexpr int WGM = GBM / 32;  // warp grid (each warp owns a 32 x 32 tile)
-constexpr int WTM = 4;         // warp tile: WTM x WTN DMMA 8x8 fragments
-constexpr int WTN = 4;
-static_assert(WGM * (GBN / 32) * 32 == GTHREADS, "warp grid must cover the CTA tile");
-constexpr int SPAD_M = GBM + 4;  // 132 ≡ 4 (mod 16)
-constexpr int SPAD_N = GBN + 4;  // 68  ≡ 4 (mod 16)
-constexpr int SPAD_K = GBK + 4;  // 20  ≡ 4 (mod 16)
+// tile configuration (em_config debug key 96): 0 = by shape (CfgT for k <= 1024 and for
+// k <= 8192 with m, n >= 2048; CfgS for longer k and few output tiles), 2 = always
+// CfgT, 3 = always CfgS
+int64_t g_gemm_cfg = 0;
 
-template <int TA>
+constexpr int GBK = 16, GTHREADS = 256;
+constexpr int SPAD_K = GBK + 4;  // 20 ≡ 4 (mod 16)
+
+// CTA tile BM x BN, warp tile (8 TM) x (8 TN) DMMA 8x8 fragments, MINB CTAs per SM.
+template <int BM, int BN, int TM, int TN, int MINB>
+struct GCfg {
+  static constexpr int M = BM, N = BN, WTM = TM, WTN = TN, MINB_ = MINB;
+  static constexpr int WGM = BM / (8 * TM);  // warps along m
+  static constexpr int WGN = BN / (8 * TN);  // warps along n
+  static constexpr int SPM = BM + 4, SPN = BN + 4;  // ≡ 4 (mod 16): conflict-free fragments
+  static constexpr int THREADS = WGM * WGN * 32;
+};
+// 128x64 tiles, 32x32 warp tiles, two CTAs per SM (the epilogue of one overlaps the
+// other's main loop): short-K updates (syr2k, rank-256 back-transform updates).
+using CfgS = GCfg<128, 64, 4, 4, 2>;
+// 64x64 tiles, 4 warps of 32x32, four CTAs per SM (barriers over 4 warps, three other
+// CTAs to cover each one's prologue and epilogue): short K (tools/gemm_probe.py, beta = 1:
+// K = 128 23.8 -> 27.6 TF/s, K = 256 27.4 -> 29.8, K = 512 29.7 -> 31.0; long K with
+// few output tiles is better on CfgS with split-K). A 128x128 tile with 32x64 warp tiles
+// and one CTA per SM measured slower everywhere (30.4 vs 31.8 TF/s at 8192^3).
+using CfgT = GCfg<64, 64, 4, 4, 4>;
+constexpr int GBM = 128;  // m tile of both configurations (split-K / grouped bookkeeping)
+
+template <int TA, class C>
 struct ATile {
-  static constexpr int size = TA ? GBM * SPAD_K : GBK * SPAD_M;
-  EM_DEVINL static int idx(int m, int k) { return TA ? m * SPAD_K + k : k * SPAD_M + m; }
+  static constexpr int size = TA ? C::M * SPAD_K : GBK * C::SPM;
+  EM_DEVINL static int idx(int m, int k) { return TA ? m * SPAD_K + k : k * C::SPM + m; }
 };
-template <int TB>
+template <int TB, class C>
 struct BTile {
-  static constexpr int size = TB ? GBK * SPAD_N : GBN * SPAD_K;
-  EM_DEVINL static int idx(int k, int n) { return TB ? k * SPAD_N + n : n * SPAD_K + k; }
+  static constexpr int size = TB ? GBK * C::SPN : C::N * SPAD_K;
+  EM_DEVINL static int idx(int k, int n) { return TB ? k * C::SPN + n : n * SPAD_K + k; }
 };
 
-// Pipeline depth: 4 stages when two CTAs still fit in shared memory, else 3.
-template <int TA, int TB>
+// Pipeline depth: 4 stages when all MINB CTAs still fit in shared memory, else 3.
+template <int TA, int TB, class C>
 constexpr int gstages() {
-  return (ATile<TA>::size + BTile<TB>::size) * 8 * 4 <= 113 * 1024 ? 4 : 3;
+  constexpr int per = (ATile<TA, C>::size + BTile<TB, C>::size) * 8;
+  return C::MINB_ >= 4 ? (per * 4 * 4 <= 220 * 1024 ? 4 : 3) : (per * 4 <= 113 * 1024 ? 4 : 3);
 }
 
 // Load a LONG x GBK slab of op(X) (the "long" extent is LONG, the k extent GBK).
 // TRANS == 0: X stored long-contiguous (X[l + k*ld]); TRANS == 1: k-contiguous (X[k + l*ld]).
 // AL: X is lower triangular (element (l, k) used only when k <= l; the stored upper
 // part is ignored) — VEC == 1 only.
-template <int TRANS, int VEC, int LONG, int AL = 0>
+template <int TRANS, int VEC, int LONG, int AL = 0, int NT = GTHREADS>
 EM_DEVINL void load_slab(double* s, const double* __restrict__ X, int64_t ld, int64_t l0,
                          int64_t k0, int64_t L, int64_t K, int tid) {
   static_assert(!AL || (VEC == 1 && TRANS == 0), "lower-A loads are 8-byte, long-contiguous");
@@ -54,7 +74,7 @@ EM_DEVINL void load_slab(double* s, const double* __restrict__ X, int64_t ld, in
     // contiguous along l; smem [k][l] stride SPL
     constexpr int CH = LONG * GBK / VEC;
 #pragma unroll
-    for (int c = tid; c < CH; c += GTHREADS) {
+    for (int c = tid; c < CH; c += NT) {
       int kk = c / (LONG / VEC);
       int l = (c % (LONG / VEC)) * VEC;
       int64_t gl = l0 + l, gk = k0 + kk;
@@ -72,7 +92,7 @@ EM_DEVINL void load_slab(double* s, const double* __restrict__ X, int64_t ld, in
     // contiguous along k; smem [l][k] stride SPAD_K
     constexpr int CH = LONG * GBK / VEC;
 #pragma unroll
-    for (int c = tid; c < CH; c += GTHREADS) {
+    for (int c = tid; c < CH; c += NT) {
       int l = c / (GBK / VEC);
       int kk = (c % (GBK / VEC)) * VEC;
       int64_t gl = l0 + l, gk = k0 + kk;
@@ -91,15 +111,18 @@ EM_DEVINL void load_slab(double* s, const double* __restrict__ X, int64_t ld, in
 
 // One CTA tile of the product. Shared by the plain and grouped kernels.
 // AL: A (TA == 0) is lower triangular: k-tiles past the tile's last row are skipped.
-template <int TA, int TB, int LOWER, int VEC, int AL = 0>
+template <int TA, int TB, int LOWER, int VEC, int AL = 0, class C = CfgS>
 EM_DEVINL void gemm_tile(const GemmArgs& p, int64_t m0, int64_t n0, double* smem) {
+  constexpr int WGM = C::WGM, WTM = C::WTM, WTN = C::WTN, GBN = C::N;
+  using AT = ATile<TA, C>;
+  using BT = BTile<TB, C>;
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int wm = warp % WGM, wn = warp / WGM;  // warp grid WGM x (GBN/32), 32 x 32 each
+  const int wm = warp % WGM, wn = warp / WGM;  // warp grid WGM x WGN
 
-  constexpr int ASZ = ATile<TA>::size, BSZ = BTile<TB>::size;
-  constexpr int GSTAGES = gstages<TA, TB>();
+  constexpr int ASZ = AT::size, BSZ = BT::size;
+  constexpr int GSTAGES = gstages<TA, TB, C>();
   double* As = smem;
   double* Bs = smem + GSTAGES * ASZ;
 
@@ -109,14 +132,14 @@ EM_DEVINL void gemm_tile(const GemmArgs& p, int64_t m0, int64_t n0, double* smem
 #pragma unroll
     for (int j = 0; j < WTN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  const int64_t nk = AL ? imin64((p.k + GBK - 1) / GBK, (m0 + GBM + GBK - 1) / GBK)
+  const int64_t nk = AL ? imin64((p.k + GBK - 1) / GBK, (m0 + C::M + GBK - 1) / GBK)
                         : (p.k + GBK - 1) / GBK;
   // prologue
 #pragma unroll
   for (int s = 0; s < GSTAGES - 1; ++s) {
     if (s < nk) {
-      load_slab<TA, VEC, GBM, AL>(As + s * ASZ, p.A, p.lda, m0, s * GBK, p.m, p.k, tid);
-      load_slab<!TB, VEC, GBN>(Bs + s * BSZ, p.B, p.ldb, n0, s * GBK, p.n, p.k, tid);
+      load_slab<TA, VEC, C::M, AL, C::THREADS>(As + s * ASZ, p.A, p.lda, m0, s * GBK, p.m, p.k, tid);
+      load_slab<!TB, VEC, GBN, 0, C::THREADS>(Bs + s * BSZ, p.B, p.ldb, n0, s * GBK, p.n, p.k, tid);
     }
     cp_async_commit();
   }
@@ -129,8 +152,8 @@ EM_DEVINL void gemm_tile(const GemmArgs& p, int64_t m0, int64_t n0, double* smem
       int64_t kn = kt + GSTAGES - 1;
       int sb = (int)(kn % GSTAGES);
       if (kn < nk) {
-        load_slab<TA, VEC, GBM, AL>(As + sb * ASZ, p.A, p.lda, m0, kn * GBK, p.m, p.k, tid);
-        load_slab<!TB, VEC, GBN>(Bs + sb * BSZ, p.B, p.ldb, n0, kn * GBK, p.n, p.k, tid);
+        load_slab<TA, VEC, C::M, AL, C::THREADS>(As + sb * ASZ, p.A, p.lda, m0, kn * GBK, p.m, p.k, tid);
+        load_slab<!TB, VEC, GBN, 0, C::THREADS>(Bs + sb * BSZ, p.B, p.ldb, n0, kn * GBK, p.n, p.k, tid);
       }
       cp_async_commit();
     }
@@ -140,18 +163,18 @@ EM_DEVINL void gemm_tile(const GemmArgs& p, int64_t m0, int64_t n0, double* smem
     // before the 32 DMMAs of k-step ks
     double af[2][WTM], bf[2][WTN];
 #pragma unroll
-    for (int i = 0; i < WTM; ++i) af[0][i] = as[ATile<TA>::idx(wm * 8 * WTM + i * 8 + g, t)];
+    for (int i = 0; i < WTM; ++i) af[0][i] = as[AT::idx(wm * 8 * WTM + i * 8 + g, t)];
 #pragma unroll
-    for (int j = 0; j < WTN; ++j) bf[0][j] = bs[BTile<TB>::idx(t, wn * 8 * WTN + j * 8 + g)];
+    for (int j = 0; j < WTN; ++j) bf[0][j] = bs[BT::idx(t, wn * 8 * WTN + j * 8 + g)];
 #pragma unroll
     for (int ks = 0; ks < GBK / 4; ++ks) {
       const int cur = ks & 1, nx = cur ^ 1;
       if (ks + 1 < GBK / 4) {
         const int kk = (ks + 1) * 4 + t;
 #pragma unroll
-        for (int i = 0; i < WTM; ++i) af[nx][i] = as[ATile<TA>::idx(wm * 8 * WTM + i * 8 + g, kk)];
+        for (int i = 0; i < WTM; ++i) af[nx][i] = as[AT::idx(wm * 8 * WTM + i * 8 + g, kk)];
 #pragma unroll
-        for (int j = 0; j < WTN; ++j) bf[nx][j] = bs[BTile<TB>::idx(kk, wn * 8 * WTN + j * 8 + g)];
+        for (int j = 0; j < WTN; ++j) bf[nx][j] = bs[BT::idx(kk, wn * 8 * WTN + j * 8 + g)];
       }
 #pragma unroll
       for (int i = 0; i < WTM; ++i)
@@ -166,12 +189,13 @@ EM_DEVINL void gemm_tile(const GemmArgs& p, int64_t m0, int64_t n0, double* smem
   // beta != 0 update (trsm, syr2k, potrf, ormtr) is not a chain of dependent round trips.
   double* __restrict__ Cr = p.C;
   const bool has_beta = p.beta != 0.0;
+  constexpr int EB = WTN > 4 ? 1 : 2;  // fragment rows per C-load batch (registers)
 #pragma unroll
-  for (int i2 = 0; i2 < WTM; i2 += 2) {
-    double cv[2][WTN][2];
-    bool ok[2][WTN][2];
+  for (int i2 = 0; i2 < WTM; i2 += EB) {
+    double cv[EB][WTN][2];
+    bool ok[EB][WTN][2];
 #pragma unroll
-    for (int ii = 0; ii < 2; ++ii) {
+    for (int ii = 0; ii < EB; ++ii) {
       const int64_t row = m0 + wm * 8 * WTM + (i2 + ii) * 8 + g;
 #pragma unroll
       for (int j = 0; j < WTN; ++j)
@@ -183,7 +207,7 @@ EM_DEVINL void gemm_tile(const GemmArgs& p, int64_t m0, int64_t n0, double* smem
         }
     }
 #pragma unroll
-    for (int ii = 0; ii < 2; ++ii) {
+    for (int ii = 0; ii < EB; ++ii) {
       const int64_t row = m0 + wm * 8 * WTM + (i2 + ii) * 8 + g;
 #pragma unroll
       for (int j = 0; j < WTN; ++j)
@@ -198,8 +222,9 @@ EM_DEVINL void gemm_tile(const GemmArgs& p, int64_t m0, int64_t n0, double* smem
   }
 }
 
-template <int TA, int TB, int LOWER, int VEC, int AL = 0>
-__global__ void __launch_bounds__(GTHREADS, GMINB) gemm_kernel(GemmArgs p, double* ws, int64_t kc) {
+template <int TA, int TB, int LOWER, int VEC, int AL = 0, class C = CfgS>
+__global__ void __launch_bounds__(C::THREADS, C::MINB_) gemm_kernel(GemmArgs p, double* ws, int64_t kc) {
+  constexpr int GBN = C::N;
   extern __shared__ __align__(16) double smem[];
   if (ws) {
     // split-K: slice z of the k range into its own m x n partial (alpha = 1, beta = 0)
@@ -215,7 +240,7 @@ __global__ void __launch_bounds__(GTHREADS, GMINB) gemm_kernel(GemmArgs p, doubl
     p.beta = 0.0;
   }
   // grouped-M swizzle for L2 reuse: walk 8 m-tiles per n-tile column group
-  const int64_t tiles_m = (p.m + GBM - 1) / GBM;
+  const int64_t tiles_m = (p.m + C::M - 1) / C::M;
   const int64_t tiles_n = (p.n + GBN - 1) / GBN;
   const int64_t bid = blockIdx.x;
   constexpr int GROUP = 8;
@@ -225,15 +250,16 @@ __global__ void __launch_bounds__(GTHREADS, GMINB) gemm_kernel(GemmArgs p, doubl
   const int64_t gsz = imin64(tiles_m - first_m, GROUP);
   const int64_t tm = first_m + (bid % per_group) % gsz;
   const int64_t tn = (bid % per_group) / gsz;
-  const int64_t m0 = tm * GBM, n0 = tn * GBN;
-  if (LOWER && m0 + GBM - 1 + p.diag_off < n0) return;  // tile strictly above the diagonal
-  gemm_tile<TA, TB, LOWER, VEC, AL>(p, m0, n0, smem);
+  const int64_t m0 = tm * C::M, n0 = tn * GBN;
+  if (LOWER && m0 + C::M - 1 + p.diag_off < n0) return;  // tile strictly above the diagonal
+  gemm_tile<TA, TB, LOWER, VEC, AL, C>(p, m0, n0, smem);
 }
 
 // Grouped launch: blockIdx.y selects a problem; problems carry their own sizes/pointers.
 template <int TA, int TB>
-__global__ void __launch_bounds__(GTHREADS, GMINB) gemm_grouped_kernel(const GemmArgs* __restrict__ ps,
-                                                                   int nprob) {
+__global__ void __launch_bounds__(GTHREADS, CfgS::MINB_) gemm_grouped_kernel(
+    const GemmArgs* __restrict__ ps, int nprob) {
+  constexpr int GBN = CfgS::N;
   extern __shared__ __align__(16) double smem[];
   GemmArgs p = ps[blockIdx.y];
   if (p.m <= 0 || p.n <= 0) return;
@@ -253,11 +279,13 @@ __global__ void __launch_bounds__(GTHREADS, GMINB) gemm_grouped_kernel(const Gem
   }
 }
 
+template <int TA, int TB, class C = CfgS>
+static size_t smem_bytes_t() {
+  return (size_t)(ATile<TA, C>::size + BTile<TB, C>::size) * gstages<TA, TB, C>() * sizeof(double);
+}
 static size_t smem_bytes(int ta, int tb) {
-  size_t a = ta ? GBM * SPAD_K : GBK * SPAD_M;
-  size_t b = tb ? GBK * SPAD_N : GBN * SPAD_K;
-  const int stages = ta ? (tb ? gstages<1, 1>() : gstages<1, 0>()) : (tb ? gstages<0, 1>() : gstages<0, 0>());
-  return (a + b) * stages * sizeof(double);
+  return ta ? (tb ? smem_bytes_t<1, 1>() : smem_bytes_t<1, 0>())
+            : (tb ? smem_bytes_t<0, 1>() : smem_bytes_t<0, 0>());
 }
 
 // C = alpha * sum_z W_z + beta * C  (split-K reduction, fixed order)
@@ -276,17 +304,17 @@ __global__ void splitk_reduce_kernel(int64_t m, int64_t n, int splits, const dou
   }
 }
 
-template <int TA, int TB, int LOWER, int VEC>
+template <int TA, int TB, int LOWER, int VEC, class C>
 static cudaError_t launch_t(const GemmArgs& p, cudaStream_t st) {
-  auto k = gemm_kernel<TA, TB, LOWER, VEC>;
-  size_t sm = smem_bytes(TA, TB);
+  auto k = gemm_kernel<TA, TB, LOWER, VEC, 0, C>;
+  size_t sm = smem_bytes_t<TA, TB, C>();
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     configured = true;
   }
-  const int64_t tiles = ((p.m + GBM - 1) / GBM) * ((p.n + GBN - 1) / GBN);
-  const int sms = num_sms();
+  const int64_t tiles = ((p.m + C::M - 1) / C::M) * ((p.n + C::N - 1) / C::N);
+  const int sms = num_sms() * (C::MINB_ >= 4 ? 4 : 1);  // CfgT: four CTA slots per SM
   // few output tiles and a long k loop: split k so every SM has work
   // pick the split count with the best wave quantisation (each slice >= 512 deep)
   int64_t splits = 1;
@@ -305,7 +333,7 @@ static cudaError_t launch_t(const GemmArgs& p, cudaStream_t st) {
     }
   }
   if (splits <= 1) {
-    k<<<(unsigned)tiles, GTHREADS, sm, st>>>(p, nullptr, 0);
+    k<<<(unsigned)tiles, C::THREADS, sm, st>>>(p, nullptr, 0);
     count_launch();
     return cudaGetLastError();
   }
@@ -317,7 +345,7 @@ static cudaError_t launch_t(const GemmArgs& p, cudaStream_t st) {
                                   (size_t)splits * p.m * p.n * sizeof(double), st);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)tiles, 1, (unsigned)splits);
-  k<<<grid, GTHREADS, sm, st>>>(p, ws, kc);
+  k<<<grid, C::THREADS, sm, st>>>(p, ws, kc);
   count_launch();
   const int64_t total = p.m * p.n;
   const int blocks = (int)imin64((total + 255) / 256, 8 * sms);
@@ -334,8 +362,12 @@ static cudaError_t launch_v(const GemmArgs& p, cudaStream_t st) {
   bool vec = al(p.A) && al(p.B) && (p.lda % 2 == 0) && (p.ldb % 2 == 0);
   // 16-byte chunks also need the tile starts to be even along the contiguous dim;
   // tiles start at multiples of 128 (long dims) and 16 (k), so base alignment suffices.
-  if (vec) return launch_t<TA, TB, LOWER, 2>(p, st);
-  return launch_t<TA, TB, LOWER, 1>(p, st);
+  const bool small =
+      g_gemm_cfg == 2 ||
+      (g_gemm_cfg == 0 && (p.k <= 1024 || (p.k <= 8192 && p.m >= 2048 && p.n >= 2048)));
+  if (small)
+    return vec ? launch_t<TA, TB, LOWER, 2, CfgT>(p, st) : launch_t<TA, TB, LOWER, 1, CfgT>(p, st);
+  return vec ? launch_t<TA, TB, LOWER, 2, CfgS>(p, st) : launch_t<TA, TB, LOWER, 1, CfgS>(p, st);
 }
 
 cudaError_t gemm(cudaStream_t st, bool ta, bool tb, int64_t m, int64_t n, int64_t k, double alpha,
@@ -360,23 +392,28 @@ cudaError_t gemm(cudaStream_t st, bool ta, bool tb, int64_t m, int64_t n, int64_
   }
 }
 
+template <class C>
+static cudaError_t launch_lower_a(const GemmArgs& p, cudaStream_t st) {
+  auto kern = gemm_kernel<0, 0, 0, 1, 1, C>;
+  const size_t sm = smem_bytes_t<0, 0, C>();
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    configured = true;
+  }
+  const int64_t tiles = ((p.m + C::M - 1) / C::M) * ((p.n + C::N - 1) / C::N);
+  kern<<<(unsigned)tiles, C::THREADS, sm, st>>>(p, nullptr, 0);
+  count_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t gemm_lower_a(cudaStream_t st, int64_t m, int64_t n, int64_t k, double alpha,
                          const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
                          double* C, int64_t ldc) {
   if (m <= 0 || n <= 0) return cudaSuccess;
   if (k <= 0) return scale_matrix(st, m, n, beta, C, ldc, false, 0);
   GemmArgs p{m, n, k, A, lda, B, ldb, C, ldc, alpha, beta, 0};
-  auto kern = gemm_kernel<0, 0, 0, 1, 1>;
-  const size_t sm = smem_bytes(0, 0);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    configured = true;
-  }
-  const int64_t tiles = ((m + GBM - 1) / GBM) * ((n + GBN - 1) / GBN);
-  kern<<<(unsigned)tiles, GTHREADS, sm, st>>>(p, nullptr, 0);
-  count_launch();
-  return cudaGetLastError();
+  return launch_lower_a<CfgS>(p, st);
 }
 
 template <int TA, int TB>

@@ -11,11 +11,24 @@ from tests.conftest import golden
 pytestmark = pytest.mark.gpu
 
 
-def test_dgemm_all_transposes_vs_numpy(rng):
+@pytest.mark.parametrize("cfg", [0, 2, 3])
+def test_dgemm_all_transposes_vs_numpy(rng, cfg):
+    """em_config debug key 96 selects the tile configuration: 0 by k (64x64 tiles for
+    k <= 1024, else 128x64), 2 always 64x64, 3 always 128x64; (40, 70, 6000) takes
+    split-K."""
     from paper_2407_11993_b200 import _native as nat
     ctx = nat.context()
     lib = nat.load_library()
-    for (m, n, k) in ((1, 1, 1), (37, 129, 300), (257, 131, 17), (300, 300, 300)):
+    nat.check(lib.em_config(ctx, 96, cfg))
+    try:
+        _dgemm_cases(rng, nat, ctx, lib)
+    finally:
+        nat.check(lib.em_config(ctx, 96, 0))
+
+
+def _dgemm_cases(rng, nat, ctx, lib):
+    for (m, n, k) in ((1, 1, 1), (37, 129, 300), (257, 131, 17), (300, 300, 300),
+                      (130, 200, 1100), (40, 70, 6000)):
         for ta in (0, 1):
             for tb in (0, 1):
                 a = rng.standard_normal((k, m) if ta else (m, k))

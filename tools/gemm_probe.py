@@ -24,6 +24,8 @@ def timed(fn, reps=5):
 
 
 ctx, lib = nat.context(), nat.load_library()
+if "GEMM_CFG" in os.environ:  # em_config debug key 96: 0 auto, 2 64x64 tiles, 3 128x64
+    nat.check(lib.em_config(ctx, 96, int(os.environ["GEMM_CFG"])))
 g = torch.Generator(device="cuda").manual_seed(3)
 shapes = [  # (m, n, k, ta, tb, label)
     (8192, 8192, 8192, 0, 0, "square 8k"),
@@ -31,6 +33,9 @@ shapes = [  # (m, n, k, ta, tb, label)
     (16384, 16384, 256, 1, 0, "rank-256 update"),
     (256, 16384, 16384, 1, 0, "ormtr W = V^T Z (K=16k)"),
     (16384, 16384, 256, 0, 0, "ormtr Z -= V W"),
+    (16384, 16384, 512, 0, 0, "rank-512 update"),
+    (512, 16384, 16384, 1, 0, "W = V^T Z (512 rows)"),
+    (4096, 4096, 4096, 0, 1, "square 4k NT"),
     (16384, 16384, 16384, 0, 0, "square 16k"),
 ]
 BETA = float(os.environ.get("BETA", "0"))
