@@ -38,8 +38,10 @@ using CfgS = GCfg<128, 64, 4, 4, 2>;
 // 64x64 tiles, 4 warps of 32x32, four CTAs per SM (barriers over 4 warps, three other
 // CTAs to cover each one's prologue and epilogue): short K (tools/gemm_probe.py, beta = 1:
 // K = 128 23.8 -> 27.6 TF/s, K = 256 27.4 -> 29.8, K = 512 29.7 -> 31.0; long K with
-// few output tiles is better on CfgS with split-K). A 128x128 tile with 32x64 warp tiles
-// and one CTA per SM measured slower everywhere (30.4 vs 31.8 TF/s at 8192^3).
+// few output tiles is better on CfgS with split-K). Measured and dropped: 128x128 tiles
+// with 32x64 warp tiles, one CTA per SM (30.4 vs 31.8 TF/s at 8192^3), and 64x128 tiles
+// with 4 warps of 32x64, two CTAs per SM (no better anywhere): every configuration
+// plateaus at ~32 TF/s on large squares (cuBLAS: 36).
 using CfgT = GCfg<64, 64, 4, 4, 4>;
 constexpr int GBM = 128;  // m tile of both configurations (split-K / grouped bookkeeping)
 
@@ -58,7 +60,8 @@ struct BTile {
 template <int TA, int TB, class C>
 constexpr int gstages() {
   constexpr int per = (ATile<TA, C>::size + BTile<TB, C>::size) * 8;
-  return C::MINB_ >= 4 ? (per * 4 * 4 <= 220 * 1024 ? 4 : 3) : (per * 4 <= 113 * 1024 ? 4 : 3);
+  return C::MINB_ >= 4 ? (per * 4 * 4 <= 220 * 1024 ? 4 : 3)
+                       : (per * 4 * C::MINB_ <= 226 * 1024 ? 4 : 3);
 }
 
 // Load a LONG x GBK slab of op(X) (the "long" extent is LONG, the k extent GBK).
