@@ -259,15 +259,14 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB_) gemm_kernel(GemmArgs p, 
 }
 
 // Grouped launch: blockIdx.y selects a problem; problems carry their own sizes/pointers.
-template <int TA, int TB>
-__global__ void __launch_bounds__(GTHREADS, CfgS::MINB_) gemm_grouped_kernel(
+template <int TA, int TB, class C>
+__global__ void __launch_bounds__(C::THREADS, C::MINB_) gemm_grouped_kernel(
     const GemmArgs* __restrict__ ps, int nprob) {
-  constexpr int GBN = CfgS::N;
   extern __shared__ __align__(16) double smem[];
   GemmArgs p = ps[blockIdx.y];
   if (p.m <= 0 || p.n <= 0) return;
-  const int64_t tiles_m = (p.m + GBM - 1) / GBM;
-  const int64_t tiles_n = (p.n + GBN - 1) / GBN;
+  const int64_t tiles_m = (p.m + C::M - 1) / C::M;
+  const int64_t tiles_n = (p.n + C::N - 1) / C::N;
   // 16-byte copies when this problem's operands allow them (problem-uniform branch)
   const bool vec = ((reinterpret_cast<uintptr_t>(p.A) | reinterpret_cast<uintptr_t>(p.B)) & 15) == 0 &&
                    ((p.lda | p.ldb) & 1) == 0;
@@ -275,9 +274,9 @@ __global__ void __launch_bounds__(GTHREADS, CfgS::MINB_) gemm_grouped_kernel(
     const int64_t tm = b % tiles_m, tn = b / tiles_m;
     // (k <= 0: C = beta C through the tile with zero accumulators)
     if (vec)
-      gemm_tile<TA, TB, 0, 2>(p, tm * GBM, tn * GBN, smem);
+      gemm_tile<TA, TB, 0, 2, 0, C>(p, tm * C::M, tn * C::N, smem);
     else
-      gemm_tile<TA, TB, 0, 1>(p, tm * GBM, tn * GBN, smem);
+      gemm_tile<TA, TB, 0, 1, 0, C>(p, tm * C::M, tn * C::N, smem);
     __syncthreads();
   }
 }
@@ -419,19 +418,27 @@ cudaError_t gemm_lower_a(cudaStream_t st, int64_t m, int64_t n, int64_t k, doubl
   return launch_lower_a<CfgS>(p, st);
 }
 
-template <int TA, int TB>
-static cudaError_t grouped_t(const GemmArgs* d_probs, int nprob, int max_tiles, cudaStream_t st) {
-  auto k = gemm_grouped_kernel<TA, TB>;
-  size_t sm = smem_bytes(TA, TB);
+// max_tiles counts 128x64 tiles (the callers' bookkeeping); the 64x64 configuration
+// (default, debug key 96 != 3) launches four CTAs per counted tile
+template <int TA, int TB, class C>
+static cudaError_t grouped_c(const GemmArgs* d_probs, int nprob, int max_tiles, cudaStream_t st) {
+  auto k = gemm_grouped_kernel<TA, TB, C>;
+  size_t sm = smem_bytes_t<TA, TB, C>();
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     configured = true;
   }
-  dim3 grid((unsigned)max(1, max_tiles), (unsigned)nprob);
-  k<<<grid, GTHREADS, sm, st>>>(d_probs, nprob);
+  const int per = (GBM / C::M) * (CfgS::N / C::N);
+  dim3 grid((unsigned)max(1, max_tiles * per), (unsigned)nprob);
+  k<<<grid, C::THREADS, sm, st>>>(d_probs, nprob);
   count_launch();
   return cudaGetLastError();
+}
+template <int TA, int TB>
+static cudaError_t grouped_t(const GemmArgs* d_probs, int nprob, int max_tiles, cudaStream_t st) {
+  if (g_gemm_cfg == 3) return grouped_c<TA, TB, CfgS>(d_probs, nprob, max_tiles, st);
+  return grouped_c<TA, TB, CfgT>(d_probs, nprob, max_tiles, st);
 }
 
 cudaError_t gemm_grouped(cudaStream_t st, bool ta, bool tb, const GemmArgs* d_probs, int nprob,
