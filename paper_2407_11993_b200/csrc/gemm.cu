@@ -285,10 +285,6 @@ template <int TA, int TB, class C = CfgS>
 static size_t smem_bytes_t() {
   return (size_t)(ATile<TA, C>::size + BTile<TB, C>::size) * gstages<TA, TB, C>() * sizeof(double);
 }
-static size_t smem_bytes(int ta, int tb) {
-  return ta ? (tb ? smem_bytes_t<1, 1>() : smem_bytes_t<1, 0>())
-            : (tb ? smem_bytes_t<0, 1>() : smem_bytes_t<0, 0>());
-}
 
 // C = alpha * sum_z W_z + beta * C  (split-K reduction, fixed order)
 __global__ void splitk_reduce_kernel(int64_t m, int64_t n, int splits, const double* __restrict__ ws,

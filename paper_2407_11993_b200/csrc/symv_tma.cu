@@ -22,24 +22,12 @@
 #include "ctx.h"
 #include "linalg.h"
 #include "symv_tile.cuh"
+#include "symv_tma.cuh"
 
 namespace em {
 
 static_assert(sizeof(SymvMap) == 2 * sizeof(CUtensorMap), "SymvMap holds two CUtensorMaps");
 extern int g_symv_align_off;
-
-constexpr int HR = 128;                 // tile rows (strip height)
-constexpr int WC = 64;                  // tile columns
-constexpr int BR = HR + 2;              // box rows for an odd offset: TMA needs a 16-byte
-                                        // aligned row start, so it loads from one row earlier
-constexpr int NST = 3;                  // ring stages
-constexpr int TT = 512;                 // threads per CTA (16 warps x 4 columns)
-// box rows / shared column stride / bytes per tile for row offset parity SH
-template <int SH>
-constexpr int box_rows() { return SH ? BR : HR; }
-template <int SH>
-constexpr unsigned tile_bytes() { return box_rows<SH>() * WC * sizeof(double); }
-constexpr size_t RING_BYTES = (size_t)NST * BR * WC * sizeof(double);
 
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -108,85 +96,7 @@ size_t symv_tma_work_size(int64_t n) {
   return (size_t)(s.nbs * s.ncj * WC + s.nbs * s.slots * HR);
 }
 
-__device__ __forceinline__ int64_t tstrip_of(int64_t t, int64_t nbs) {
-  int64_t i = (int64_t)((sqrt(4.0 * (double)t + 1.0) - 1.0) * 0.5);
-  while (i > 0 && i * (i + 1) > t) --i;
-  while ((i + 1) * (i + 2) <= t) ++i;
-  return imin64(i, nbs - 1);
-}
-
-// ---- mbarrier / TMA ------------------------------------------------------------------
-EM_DEVINL void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
-}
-EM_DEVINL void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-EM_DEVINL void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
-EM_DEVINL void mbar_wait(uint64_t* bar, unsigned parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-EM_DEVINL void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
-                           uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      ".L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(smem_u32(dst)),
-      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(pol)
-      : "memory");
-}
-// L2 policies: the bottom-right block of the matrix (read by every column's symv of a
-// tridiagonalisation) is loaded evict_last, everything else evict_first, so the part of
-// the trailing matrix that fits in the 126 MB L2 is re-read from L2, not HBM.
-EM_DEVINL uint64_t pol_evict_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
-  return p;
-}
-EM_DEVINL uint64_t pol_evict_normal() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;\n" : "=l"(p));
-  return p;
-}
-EM_DEVINL uint64_t pol_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
-  return p;
-}
-
-// x of the block extended by d leading rows/columns (see symv_tma): xd = x - d, na = n + d;
-// zero for r < d (only reachable in the first strip / first column block: callers take
-// this path there and xfast elsewhere), v = [1, xs x] starts at r = d.
-EM_DEVINL double xshift(const double* xd, int64_t r, int64_t d, int64_t na, double xs,
-                        bool unit0) {
-  if (r < d || r >= na) return 0.0;
-  if (unit0 && r == d) return 1.0;
-  return xs * __ldcg(xd + r);
-}
-EM_DEVINL double xfast(const double* xd, int64_t r, int64_t na, double xs) {
-  return r < na ? xs * __ldcg(xd + r) : 0.0;
-}
-
 // ---- kernel ----------------------------------------------------------------------------
-// SH = off & 1. Thread rows within the tile (h, q in {0, 1}): SH = 0: 64h + 2 lane + q
-// (128-bit shared loads); SH = 1: 64h + 32q + lane (the tile sits one row into the
-// box, so 64-bit loads with consecutive lanes on consecutive rows).
-template <int SH>
-EM_DEVINL int trow(int h, int q, int lane) {
-  return SH ? 64 * h + 32 * q + lane : 64 * h + 2 * lane + q;
-}
-
 template <bool LARFG, int SH>
 __global__ void __launch_bounds__(TT, 1) symv_tma_kernel(const __grid_constant__ CUtensorMap map,
                                                          int64_t off, int64_t n, int64_t d,
@@ -202,8 +112,6 @@ __global__ void __launch_bounds__(TT, 1) symv_tma_kernel(const __grid_constant__
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int64_t p = blockIdx.x;
   const int64_t t0 = p * len, t1 = imin64(T, t0 + len);
-  const double* xd = x - d;
-  const int64_t na = n + d;
   if (t0 >= t1) {  // not launched by symv_tma (P is trimmed to the last non-empty range)
     if (LARFG && lf.vav != nullptr && tid == 0) lf.vav[p] = 0.0;
     return;
@@ -217,25 +125,17 @@ __global__ void __launch_bounds__(TT, 1) symv_tma_kernel(const __grid_constant__
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  auto tiles_in = [&](int64_t ii) { return imin64(2 * ii + 2, ncj); };
-  int64_t i = tstrip_of(t0, nbs), j = t0 - i * (i + 1);
-  int64_t pi = i, pj = j;  // producer cursor (thread 0)
-  const uint64_t pkeep = pol_evict_last();
-  const uint64_t pstream = keep_c0 == INT64_MIN ? pol_evict_normal() : pol_evict_first();
-  auto pol_of = [&](int64_t cj) {
-    return keep_c0 != INT64_MIN && off + WC * cj >= keep_c0 ? pkeep : pstream;
-  };
+  const TmaRing R{ring, full, empty};
+  TmaPolicy pol;
+  pol.keep = pol_evict_last();
+  pol.stream = keep_c0 == INT64_MIN ? pol_evict_normal() : pol_evict_first();
+  if (keep_c0 == INT64_MIN) pol.keep = pol.stream;  // no hints at all
+  pol.keep_c0 = keep_c0;
+  int64_t pi = tstrip_of(t0, nbs), pj = t0 - pi * (pi + 1);  // producer cursor (thread 0)
   // prologue: the first NST-1 tiles (A is not written by the launch this one may overlap)
-  if (tid == 0) {
-    for (int s = 0; s < NST - 1; ++s) {
-      if (t0 + s < t1) {
-        mbar_expect_tx(&full[s], tile_bytes<SH>());
-        tma_load_2d(ring + (size_t)s * BR * WC, &map, (int)(off + HR * pi - SH),
-                    (int)(off + WC * pj), &full[s], pol_of(pj));
-      }
-      if (pj + 1 < tiles_in(pi)) ++pj; else { ++pi; pj = 0; }
-    }
-  }
+  if (tid == 0)
+    for (int s = 0; s < NST - 1 && t0 + s < t1; ++s)
+      symv_tma_issue<SH>(&map, R, (uint32_t)s, off, pi, pj, ncj, pol);
   pdl_wait();
   pdl_trigger();
   // dlarfg of the raw column x (while the first tiles are in flight); CTA 0 publishes
@@ -263,135 +163,11 @@ __global__ void __launch_bounds__(TT, 1) symv_tma_kernel(const __grid_constant__
       *lf.scale = scale;
     }
     xs = scale;
+    __syncthreads();  // red is reused by the tile loop
   }
-  // v^T A v partial of this CTA (x = v): sum x_c colsum_c over tiles + x_r rowsum_r
-  double vav = 0.0;
   const bool want_vav = LARFG && lf.vav != nullptr;
-  // thread rows 64h + 2*lane + q (h, q in {0,1}); columns 4w + cc
-  double xi[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-  double row[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-  bool fresh = true;
-  for (int64_t t = t0; t < t1; ++t) {
-    const int k = (int)(t - t0);
-    const int s = k % NST;
-    // producer: tile k+NST-1 into the stage released by tile k-1
-    if (tid == 0 && t + NST - 1 < t1) {
-      const int kp = k + NST - 1, ps = kp % NST;
-      if (kp >= NST) mbar_wait(&empty[ps], (unsigned)((kp / NST - 1) & 1));
-      mbar_expect_tx(&full[ps], tile_bytes<SH>());
-      tma_load_2d(ring + (size_t)ps * BR * WC, &map, (int)(off + HR * pi - SH),
-                  (int)(off + WC * pj), &full[ps], pol_of(pj));
-      if (pj + 1 < tiles_in(pi)) ++pj; else { ++pi; pj = 0; }
-    }
-    const int64_t r0 = i * HR, c0 = j * WC;
-    if (fresh) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          xi[h][q] = (i == 0) ? xshift(xd, r0 + trow<SH>(h, q, lane), d, na, xs, LARFG)
-                              : xfast(xd, r0 + trow<SH>(h, q, lane), na, xs);
-          row[h][q] = 0.0;
-        }
-      fresh = false;
-    }
-    double xj[4];
-    if (j == 0) {
-#pragma unroll
-      for (int cc = 0; cc < 4; ++cc) xj[cc] = xshift(xd, c0 + 4 * w + cc, d, na, xs, LARFG);
-    } else {
-#pragma unroll
-      for (int cc = 0; cc < 4; ++cc) xj[cc] = xfast(xd, c0 + 4 * w + cc, na, xs);
-    }
-    mbar_wait(&full[s], (unsigned)((k / NST) & 1));
-    const double* S = ring + (size_t)s * BR * WC + SH;
-    double col[4];
-    // v[h][q]: element (trow(h, q), 4w + cc) of the tile
-    auto ld2 = [&](int cc, int h, double& v0, double& v1) {
-      const double* Sc = S + (4 * w + cc) * box_rows<SH>();
-      if (SH == 0) {
-        const double2 v = *reinterpret_cast<const double2*>(Sc + 64 * h + 2 * lane);
-        v0 = v.x;
-        v1 = v.y;
-      } else {
-        v0 = Sc[64 * h + lane];
-        v1 = Sc[64 * h + 32 + lane];
-      }
-    };
-    if (j < 2 * i) {
-#pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {
-        double cs = 0.0;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          double v0, v1;
-          ld2(cc, h, v0, v1);
-          row[h][0] = fma(v0, xj[cc], row[h][0]);
-          row[h][1] = fma(v1, xj[cc], row[h][1]);
-          cs = fma(v0, xi[h][0], fma(v1, xi[h][1], cs));
-        }
-        col[cc] = cs;
-      }
-    } else {
-      // diagonal tiles j = 2i, 2i+1: element (r, c) is lower when r >= c + 64 (j - 2i)
-      const int dsh = 64 * (int)(j - 2 * i);
-#pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {
-        const int c = 4 * w + cc + dsh;
-        double cs = 0.0;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          double v0, v1;
-          ld2(cc, h, v0, v1);
-          const int ra = trow<SH>(h, 0, lane), rb = trow<SH>(h, 1, lane);
-          const double l0 = (ra >= c) ? v0 : 0.0, l1 = (rb >= c) ? v1 : 0.0;
-          const double s0 = (ra > c) ? v0 : 0.0, s1 = (rb > c) ? v1 : 0.0;
-          row[h][0] = fma(l0, xj[cc], row[h][0]);
-          row[h][1] = fma(l1, xj[cc], row[h][1]);
-          cs = fma(s0, xi[h][0], fma(s1, xi[h][1], cs));
-        }
-        col[cc] = cs;
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with the stage
-    {  // column sums over the 32 lanes: 4 values, 6 shuffles
-      const bool h16 = lane & 16, h8 = lane & 8;
-      const double a0 = h16 ? col[2] : col[0], a1 = h16 ? col[3] : col[1];
-      const double b0 = h16 ? col[0] : col[2], b1 = h16 ? col[1] : col[3];
-      const double c0v = a0 + __shfl_xor_sync(0xffffffffu, b0, 16);
-      const double c1v = a1 + __shfl_xor_sync(0xffffffffu, b1, 16);
-      double v = (h8 ? c1v : c0v) + __shfl_xor_sync(0xffffffffu, h8 ? c0v : c1v, 8);
-      v += __shfl_xor_sync(0xffffffffu, v, 4);
-      v += __shfl_xor_sync(0xffffffffu, v, 2);
-      v += __shfl_xor_sync(0xffffffffu, v, 1);
-      if ((lane & 7) == 0) {
-        const int cc = (h16 ? 2 : 0) + (h8 ? 1 : 0);
-        wcol[(i * ncj + j) * WC + 4 * w + cc] = v;
-        // (selects, not xj[cc]: a runtime index would put xj in local memory)
-        if (want_vav) vav = fma(v, h16 ? (h8 ? xj[3] : xj[2]) : (h8 ? xj[1] : xj[0]), vav);
-      }
-    }
-    if (j + 1 == tiles_in(i) || t + 1 == t1) {  // end of this CTA's piece of strip i
-      __syncthreads();
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        red[w][trow<SH>(h, 0, lane)] = row[h][0];
-        red[w][trow<SH>(h, 1, lane)] = row[h][1];
-      }
-      __syncthreads();
-      if (tid < HR) {
-        double sum = 0.0;
-#pragma unroll
-        for (int k2 = 0; k2 < TT / 32; ++k2) sum += red[k2][tid];
-        const int64_t slot = p - (i * (i + 1)) / len;
-        wrow[(i * slots + slot) * HR + tid] = sum;
-        if (want_vav) vav = fma(sum, xshift(xd, r0 + tid, d, na, xs, LARFG), vav);
-      }
-      fresh = true;
-    }
-    if (j + 1 < tiles_in(i)) ++j; else { ++i; j = 0; }
-  }
+  double vav = symv_tma_loop<LARFG, SH>(&map, R, 0u, off, n, d, x, xs, wcol, wrow, nbs, ncj, len,
+                                        slots, p, t0, t1, pi, pj, pol, want_vav, red);
   if (want_vav) {
     __syncthreads();
     double sv = warp_sum(vav);

@@ -24,7 +24,7 @@ def _syev(a, lda=None):
 
 
 @pytest.mark.parametrize("flags", [0, 1, 2, 4, 8, 15])
-@pytest.mark.parametrize("n", [1, 2, 3, 65, 130, 333])
+@pytest.mark.parametrize("n", [1, 2, 3, 65, 130, 333, 1100])
 def test_sytrd_paths_match_lapack(flags, n):
     from paper_2407_11993_b200 import _native as nat
     lib, ctx = nat.load_library(), nat.context()
@@ -53,3 +53,24 @@ def test_sytrd_odd_leading_dimension():
     w, u = _syev(a, lda=n + 1)
     ref = np.sort(np.linalg.eigvalsh(a))[::-1]
     assert np.max(np.abs(w - ref)) < 1e-12 * np.abs(ref).max() * n
+
+
+@pytest.mark.parametrize("n", [2500, 4097])
+def test_sytrd_larger_orders(n):
+    """Several panels with trailing orders past one tile wave (every CTA of the symv busy)
+    and the L2 policy switch (EM_CFG_SYMV_L2_KEEP_MB: no hints vs evict_first + keep)."""
+    from paper_2407_11993_b200 import _native as nat
+    lib, ctx = nat.load_library(), nat.context()
+    rng = np.random.default_rng(n)
+    b = rng.standard_normal((n, n))
+    a = b + b.T
+    w, u = _syev(a)
+    nat.check(lib.em_config(ctx, 3, -1))
+    try:
+        w2, _ = _syev(a)
+    finally:
+        nat.check(lib.em_config(ctx, 3, 32))
+    ref = np.sort(np.linalg.eigvalsh(a))[::-1]
+    assert np.max(np.abs(w - ref)) < 1e-12 * np.abs(ref).max() * n
+    assert np.array_equal(w, w2)  # cache hints do not change the arithmetic
+    assert np.max(np.abs(a @ u - u * w)) < 1e-11 * np.abs(ref).max() * n
