@@ -353,6 +353,9 @@ def run_ours(args, cfg, rank, world, local_rank):
         nat.set_two_stage_min(args.two_stage)
     if os.environ.get("EM_SYTRD_DBG"):  # A/B switch for the tridiagonalisation code paths
         nat.check(nat.load_library().em_config(nat.context(), 98, int(os.environ["EM_SYTRD_DBG"])))
+    for kv in filter(None, os.environ.get("EM_CONFIG", "").split(",")):  # A/B: "key=value,..."
+        key, val = kv.split("=")
+        nat.check(nat.load_library().em_config(nat.context(), int(key), int(val)))
     m = build_inputs(cfg)
     n = m["plate"].n
     T, nth = cfg["steps"], len(cfg["thetas"])

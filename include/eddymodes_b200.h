@@ -131,6 +131,14 @@ int em_sygv(em_ctx* ctx, int64_t n, const double* L, int64_t ldl, const double* 
 int em_sygv_ex(em_ctx* ctx, int64_t n, const double* L, int64_t ldl, double* R, int64_t ldr,
                double* tau, double* V, int64_t ldv, double* l_n, double* r_n, double* VtR,
                int64_t ldvtr, int flags, int64_t* pivot, int* which);
+/* em_sygv_ex with L still on the host: the library uploads L_host (n x n, leading
+ * dimension n; pinned memory makes the copy asynchronous) into the device buffer L (ld
+ * ldl) on a copy engine, after the work already queued on the context stream (e.g. R's
+ * upload) and overlapped with R's band detection and Cholesky; L is first read by the
+ * two-sided reduction. On return L holds the upload. */
+int em_sygv_lh(em_ctx* ctx, int64_t n, const double* L_host, double* L, int64_t ldl, double* R,
+               int64_t ldr, double* tau, double* V, int64_t ldv, double* l_n, double* r_n,
+               double* VtR, int64_t ldvtr, int flags, int64_t* pivot, int* which);
 
 /* --- modal theta-method (TD2, transient.py:258-308) ------------------------------- */
 

@@ -25,7 +25,8 @@ void stages_level(int level);
 int stages_read(double* ms, int64_t* counts, int n);
 int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const double* R,
              int64_t ldr, double* tau, double* V, int64_t ldv, double* l_n, double* r_n,
-             double* VtR, int64_t ldvtr, int* which, int flags);
+             double* VtR, int64_t ldvtr, int* which, int flags,
+             cudaEvent_t l_ready = nullptr);
 }
 
 // full definitions live in td1.cu / td2.cu; re-declare the layout-independent API here
@@ -241,6 +242,44 @@ int em_sygv_ex(em_ctx* ctx, int64_t n, const double* L, int64_t ldl, double* R, 
   });
 }
 
+int em_sygv_lh(em_ctx* ctx, int64_t n, const double* L_host, double* L, int64_t ldl, double* R,
+               int64_t ldr, double* tau, double* V, int64_t ldv, double* l_n, double* r_n,
+               double* VtR, int64_t ldvtr, int flags, int64_t* pivot, int* which) {
+  return guarded(ctx, [&] {
+    if (flags & ~EM_SYGV_R_WORKSPACE) throw em::ArgError{"unknown em_sygv_lh flags"};
+    if (!L_host || !L) throw em::ArgError{"em_sygv_lh: L_host and L are required"};
+    cudaStream_t st = ctx->stream;
+    // the copy engine takes L after everything already queued on the stream (R's upload)
+    cudaStream_t cs = nullptr;
+    cudaEvent_t queued = nullptr, l_ready = nullptr;
+    EM_CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    EM_CK(cudaEventCreateWithFlags(&queued, cudaEventDisableTiming));
+    EM_CK(cudaEventCreateWithFlags(&l_ready, cudaEventDisableTiming));
+    struct Cleanup {
+      cudaStream_t cs;
+      cudaEvent_t a, b;
+      ~Cleanup() {
+        cudaStreamSynchronize(cs);
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        cudaStreamDestroy(cs);
+      }
+    } cleanup{cs, queued, l_ready};
+    EM_CK(cudaEventRecord(queued, st));
+    EM_CK(cudaStreamWaitEvent(cs, queued, 0));
+    EM_CK(cudaMemcpy2DAsync(L, (size_t)ldl * 8, L_host, (size_t)n * 8, (size_t)n * 8, (size_t)n,
+                            cudaMemcpyHostToDevice, cs));
+    EM_CK(cudaEventRecord(l_ready, cs));
+    int wh = -1;
+    const int64_t p = em::sygv(st, n, L, ldl, R, ldr, tau, V, ldv, l_n, r_n, VtR, ldvtr, &wh,
+                               flags, l_ready);
+    EM_CK(cudaStreamWaitEvent(st, l_ready, 0));  // (an early R failure returns before L is used)
+    if (pivot) *pivot = p;
+    if (which) *which = wh;
+    return p >= 0 ? EM_ERR_NOT_PD : EM_OK;
+  });
+}
+
 int em_sygv(em_ctx* ctx, int64_t n, const double* L, int64_t ldl, const double* R, int64_t ldr,
             double* tau, double* V, int64_t ldv, double* l_n, double* r_n, double* VtR,
             int64_t ldvtr, int64_t* pivot, int* which) {
@@ -256,12 +295,14 @@ int em_sygv_h(em_ctx* ctx, int64_t n, const double* L_h, const double* R_h, doub
     const size_t nn = (size_t)n * n;
     em::DBuf L(nn, st), R(nn, st), V(nn, st), t(n, st), ln(n, st), rn(n, st), VtR;
     if (VtR_h) VtR.alloc(nn, st);
-    EM_CK(cudaMemcpyAsync(L.p, L_h, nn * 8, cudaMemcpyHostToDevice, st));
     EM_CK(cudaMemcpyAsync(R.p, R_h, nn * 8, cudaMemcpyHostToDevice, st));
     int wh = -1;
-    // R is this call's own upload: use it as the factor workspace when it is sparse
-    const int64_t p = em::sygv(st, n, L.p, n, R.p, n, t.p, V.p, n, ln.p, rn.p,
-                               VtR_h ? VtR.p : nullptr, n, &wh, EM_SYGV_R_WORKSPACE);
+    // L is uploaded by em_sygv_lh on a copy engine while R is factored; R is this call's
+    // own upload: use it as the factor workspace when it is sparse
+    int64_t p = -1;
+    const int rc = em_sygv_lh(ctx, n, L_h, L.p, n, R.p, n, t.p, V.p, n, ln.p, rn.p,
+                              VtR_h ? VtR.p : nullptr, n, EM_SYGV_R_WORKSPACE, &p, &wh);
+    if (rc != EM_OK && rc != EM_ERR_NOT_PD) return rc;  // (ctx->err already set)
     if (pivot) *pivot = p;
     if (which) *which = wh;
     if (p >= 0) return EM_ERR_NOT_PD;

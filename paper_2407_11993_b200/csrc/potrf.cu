@@ -61,7 +61,7 @@ EM_DEVINL double linv_at(const double* S, const double* dinv, int r, int c) {
   return r == c ? dinv[r] : (r > c ? S[c + r * PLD] : 0.0);
 }
 
-__global__ void __launch_bounds__(256) potf2_inv_kernel(double* A, int64_t lda, int64_t k0, int bs,
+__global__ void __launch_bounds__(256, 1) potf2_inv_kernel(double* A, int64_t lda, int64_t k0, int bs,
                                                         double* Dinv, int64_t* info) {
   extern __shared__ double sm[];
   double* S = sm;                // PNB x PLD
@@ -83,28 +83,32 @@ __global__ void __launch_bounds__(256) potf2_inv_kernel(double* A, int64_t lda, 
   for (int kb = 0; kb < PNB / PB; ++kb) {
     const int o = kb * PB;
     if (warp == 0) {
-      // unblocked Cholesky of the 32 x 32 diagonal block; lane l owns row o + l and gets
-      // the column-j entries of the other rows by shuffle
-      int f = -1;
-      for (int j = 0; j < PB; ++j) {
-        const double sj = S[(o + j) + (o + j) * PLD];
-        if (!(sj > 0.0)) {
-          f = o + j;
-          break;
-        }
-        const double d = sqrt(sj);
-        const double lj = S[(o + lane) + (o + j) * PLD] * (1.0 / d);
-        __syncwarp();
-        if (lane == j) S[(o + j) + (o + j) * PLD] = d;
-        if (lane > j) S[(o + lane) + (o + j) * PLD] = lj;
+      // unblocked Cholesky of the 32 x 32 diagonal block in registers: lane l holds row
+      // o + l (a[k], k <= l) and gets the column-j entries of the other rows by shuffle
+      double a[PB];
 #pragma unroll
-        for (int k = 0; k < PB; ++k) {
-          const double lk = __shfl_sync(0xffffffffu, lj, k);
-          if (k > j && k <= lane)
-            S[(o + lane) + (o + k) * PLD] = fma(-lj, lk, S[(o + lane) + (o + k) * PLD]);
+      for (int k = 0; k < PB; ++k) a[k] = (k <= lane) ? S[(o + lane) + (o + k) * PLD] : 0.0;
+      int f = -1;
+#pragma unroll
+      for (int j = 0; j < PB; ++j) {
+        const double sj = __shfl_sync(0xffffffffu, a[j], j);  // the pivot, in every lane
+        if (!(sj > 0.0) && f < 0) f = o + j;  // (the rest of the block is then unused)
+        const double d = sqrt(sj);
+        const double lj = a[j] * (1.0 / d);
+        if (lane == j) a[j] = d;
+        if (lane > j) a[j] = lj;
+#pragma unroll
+        for (int k = 0; k < PB; ++k) {  // (constant trip count: a[] stays in registers)
+          if (k > j) {
+            const double lk = __shfl_sync(0xffffffffu, lj, k);
+            if (lane >= k) a[k] = fma(-lj, lk, a[k]);
+          }
         }
-        __syncwarp();
       }
+#pragma unroll
+      for (int k = 0; k < PB; ++k)
+        if (k <= lane) S[(o + lane) + (o + k) * PLD] = a[k];
+      __syncwarp();
       if (f >= 0) {
         if (lane == 0) fail = f;
       } else {

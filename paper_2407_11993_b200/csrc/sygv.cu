@@ -156,9 +156,11 @@ __global__ void quadform_lower_kernel(int64_t n, const double* __restrict__ V, i
 }
 
 // Returns -1 on success; else the failing pivot with *which = 0 (R) / 1 (L).
+// l_ready (optional): L is still being uploaded; the stream waits for it only before the
+// first use of L (after R's band detection and factorisation).
 int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const double* R,
              int64_t ldr, double* tau, double* V, int64_t ldv, double* l_n, double* r_n,
-             double* VtR, int64_t ldvtr, int* which, int flags) {
+             double* VtR, int64_t ldvtr, int* which, int flags, cudaEvent_t l_ready) {
   *which = -1;
   if (n <= 0) return -1;
   const size_t nn = (size_t)n * n;
@@ -197,6 +199,7 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
       piv = potrf(st, n, G, ldg, GDinv.p);
     }
   }
+  if (l_ready) EM_CK(cudaStreamWaitEvent(st, l_ready, 0));
   if (piv >= 0) {
     *which = 0;
     restore_r();

@@ -110,6 +110,7 @@ def generalized_eig(l_i, r_i, *, vt_r: str = "auto") -> ModalBasis:
     matrix") with the failing pivot, in the reference's order."""
     t = nat.torch()
     own = False  # R uploaded here: usable as the factor workspace (EM_SYGV_R_WORKSPACE)
+    l_host = None  # L left on the host for em_sygv_lh
     if isinstance(l_i, t.Tensor) and isinstance(r_i, t.Tensor):
         # device-resident symmetric inputs (row-major bytes == column-major)
         ld = l_i.to(dtype=t.float64).contiguous()
@@ -126,11 +127,16 @@ def generalized_eig(l_i, r_i, *, vt_r: str = "auto") -> ModalBasis:
             z = np.zeros(0)
             zz = np.zeros((0, 0))
             return ModalBasis(v=zz, tau=z, l_n=z, r_n=z, vt_r=zz)
-        # SymMatrix is exactly symmetric: upload its bytes as they are
-        ld = nat.device_symmetric(lm) if isinstance(l_i, linalg.SymMatrix) else \
-            nat.device_colmajor(lm)
+        # SymMatrix is exactly symmetric: upload its bytes as they are. R goes first; an
+        # exactly symmetric L is uploaded by the library on a copy engine while R is
+        # factored (em_sygv_lh)
         rd = nat.device_symmetric(rm) if isinstance(r_i, linalg.SymMatrix) else \
             nat.device_colmajor(rm)
+        if isinstance(l_i, linalg.SymMatrix):
+            l_host = np.ascontiguousarray(lm, dtype=np.float64)
+            ld = nat.empty(n, n)
+        else:
+            ld = nat.device_colmajor(lm)
         own = True
     ctx = nat.context()
     if vt_r not in ("auto", "eager", "lazy"):
@@ -144,10 +150,14 @@ def generalized_eig(l_i, r_i, *, vt_r: str = "auto") -> ModalBasis:
     vtr = nat.empty(n, n) if vt_r == "eager" else None
     piv = ctypes.c_int64(-1)
     which = ctypes.c_int(-1)
-    rc = nat.load_library().em_sygv_ex(ctx, n, nat.ptr(ld), n, nat.ptr(rd), n, nat.ptr(tau),
-                                       nat.ptr(v), n, nat.ptr(ln), nat.ptr(rn),
-                                       None if vtr is None else nat.ptr(vtr), n,
-                                       1 if own else 0, ctypes.byref(piv), ctypes.byref(which))
+    lib = nat.load_library()
+    common = (nat.ptr(rd), n, nat.ptr(tau), nat.ptr(v), n, nat.ptr(ln), nat.ptr(rn),
+              None if vtr is None else nat.ptr(vtr), n, 1 if own else 0, ctypes.byref(piv),
+              ctypes.byref(which))
+    if l_host is not None:
+        rc = lib.em_sygv_lh(ctx, n, l_host.ctypes.data, nat.ptr(ld), n, *common)
+    else:
+        rc = lib.em_sygv_ex(ctx, n, nat.ptr(ld), n, *common)
     if rc == nat.EM_ERR_NOT_PD:
         what = "modal resistance matrix" if which.value == 0 else "modal inductance matrix"
         raise NotPositiveDefinite(int(piv.value), what)
