@@ -15,9 +15,9 @@
 
 namespace em {
 
-// tile configuration (em_config debug key 96): 0 = by shape (CfgT for k <= 1024 and for
-// k <= 8192 with m, n >= 2048; CfgS for longer k and few output tiles), 2 = always
-// CfgT, 3 = always CfgS
+// tile configuration (em_config debug key 96): 0 / 2 = CfgT, 3 = CfgS (A/B). In the C2
+// step CfgT everywhere beats the shape rule "CfgS for long k" that the isolated probes
+// suggested (2113 -> 2103 ms: ormtr 326 -> 322, l_n product 160 -> 154)
 int64_t g_gemm_cfg = 0;
 
 constexpr int GBK = 16, GTHREADS = 256;
@@ -38,7 +38,8 @@ using CfgS = GCfg<128, 64, 4, 4, 2>;
 // 64x64 tiles, 4 warps of 32x32, four CTAs per SM (barriers over 4 warps, three other
 // CTAs to cover each one's prologue and epilogue): short K (tools/gemm_probe.py, beta = 1:
 // K = 128 23.8 -> 27.6 TF/s, K = 256 27.4 -> 29.8, K = 512 29.7 -> 31.0; long K with
-// few output tiles is better on CfgS with split-K). Measured and dropped: 128x128 tiles
+// few output tiles measured better on CfgS in isolation, not inside the eigensolve).
+// Measured and dropped: 128x128 tiles
 // with 32x64 warp tiles, one CTA per SM (30.4 vs 31.8 TF/s at 8192^3), and 64x128 tiles
 // with 4 warps of 32x64, two CTAs per SM (no better anywhere): every configuration
 // plateaus at ~32 TF/s on large squares (cuBLAS: 36).
@@ -360,10 +361,7 @@ static cudaError_t launch_v(const GemmArgs& p, cudaStream_t st) {
   bool vec = al(p.A) && al(p.B) && (p.lda % 2 == 0) && (p.ldb % 2 == 0);
   // 16-byte chunks also need the tile starts to be even along the contiguous dim;
   // tiles start at multiples of 128 (long dims) and 16 (k), so base alignment suffices.
-  const bool small =
-      g_gemm_cfg == 2 ||
-      (g_gemm_cfg == 0 && (p.k <= 1024 || (p.k <= 8192 && p.m >= 2048 && p.n >= 2048)));
-  if (small)
+  if (g_gemm_cfg != 3)
     return vec ? launch_t<TA, TB, LOWER, 2, CfgT>(p, st) : launch_t<TA, TB, LOWER, 1, CfgT>(p, st);
   return vec ? launch_t<TA, TB, LOWER, 2, CfgS>(p, st) : launch_t<TA, TB, LOWER, 1, CfgS>(p, st);
 }
@@ -411,7 +409,7 @@ cudaError_t gemm_lower_a(cudaStream_t st, int64_t m, int64_t n, int64_t k, doubl
   if (m <= 0 || n <= 0) return cudaSuccess;
   if (k <= 0) return scale_matrix(st, m, n, beta, C, ldc, false, 0);
   GemmArgs p{m, n, k, A, lda, B, ldb, C, ldc, alpha, beta, 0};
-  if (g_gemm_cfg == 2) return launch_lower_a<CfgT>(p, st);
+  if (g_gemm_cfg != 3) return launch_lower_a<CfgT>(p, st);
   return launch_lower_a<CfgS>(p, st);
 }
 
