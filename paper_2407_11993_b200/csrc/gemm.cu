@@ -6,9 +6,10 @@
 // The reference does these through numpy/OpenBLAS (pkg/src/eddymodes/modal.py:79-81,
 // transient.py:140-154) or scalar numba loops (_kernels.py:56-79).
 //
-// Tile 128x64x16, 8 warps (4x2), warp tile 32x32 = 4x4 DMMA.8x8x4 fragments, 2 CTAs/SM,
-// 3-stage cp.async pipeline, padded shared-memory layouts chosen so every
-// 8-byte fragment load is bank-conflict free (row strides = 4 mod 16 doubles).
+// Warp tile 32x32 = 4x4 DMMA.8x8x4 fragments, k tile 16, 3-4-stage cp.async pipeline,
+// padded shared-memory layouts chosen so every 8-byte fragment load is bank-conflict
+// free (row strides = 4 mod 16 doubles). Two CTA configurations (GCfg below): 64x64
+// tiles with 4 warps and 4 CTAs per SM (the default), 128x64 with 8 warps and 2 CTAs.
 #include "common.cuh"
 #include "gemm.h"
 #include "ctx.h"
@@ -33,16 +34,16 @@ struct GCfg {
   static constexpr int THREADS = WGM * WGN * 32;
 };
 // 128x64 tiles, 32x32 warp tiles, two CTAs per SM (the epilogue of one overlaps the
-// other's main loop): short-K updates (syr2k, rank-256 back-transform updates).
+// other's main loop): the previous default, kept for A/B (debug key 96 = 3).
 using CfgS = GCfg<128, 64, 4, 4, 2>;
 // 64x64 tiles, 4 warps of 32x32, four CTAs per SM (barriers over 4 warps, three other
 // CTAs to cover each one's prologue and epilogue): short K (tools/gemm_probe.py, beta = 1:
 // K = 128 23.8 -> 27.6 TF/s, K = 256 27.4 -> 29.8, K = 512 29.7 -> 31.0; long K with
 // few output tiles measured better on CfgS in isolation, not inside the eigensolve).
-// Measured and dropped: 128x128 tiles
-// with 32x64 warp tiles, one CTA per SM (30.4 vs 31.8 TF/s at 8192^3), and 64x128 tiles
-// with 4 warps of 32x64, two CTAs per SM (no better anywhere): every configuration
-// plateaus at ~32 TF/s on large squares (cuBLAS: 36).
+// Measured and dropped: 128x128 tiles with 32x64 warp tiles, one CTA per SM (30.4 vs
+// 31.8 TF/s at 8192^3), and 64x128 tiles with 4 warps of 32x64, two CTAs per SM (no
+// better anywhere): every configuration plateaus at ~32 TF/s on large squares
+// (cuBLAS: 36).
 using CfgT = GCfg<64, 64, 4, 4, 4>;
 constexpr int GBM = 128;  // m tile of both configurations (split-K / grouped bookkeeping)
 
