@@ -119,6 +119,10 @@ __global__ void __launch_bounds__(RT) latrd_col_kernel(
       wlast = fma(alpha_p, vlast, __ldcg(wtmp + r));
     }
   } else if (i > 0) {
+    // everything from the previous launch in one round of loads: t, y at this row and
+    // (warp 0) y at row c
+    const double yr = valid ? __ldcg(wtmp + r) : 0.0;
+    const double yc = (warp == 0) ? __ldcg(wtmp + c) : 0.0;
     for (int k = tid; k < i - 1; k += RT) {
       t1s[k] = __ldcg(cw.tvec + k);
       t2s[k] = __ldcg(cw.tvec + TRD_NB + k);
@@ -134,7 +138,7 @@ __global__ void __launch_bounds__(RT) latrd_col_kernel(
       dc = warp_sum(dc);
       if (lane == 0) {
         s_alpha = -0.5 * tprev * tprev * (vavsum - 2.0 * tt);
-        s_wc = tprev * (__ldcg(wtmp + c) - dc);
+        s_wc = tprev * (yc - dc);
       }
     }
     double sdot = 0.0;
@@ -149,7 +153,7 @@ __global__ void __launch_bounds__(RT) latrd_col_kernel(
     alpha_p = s_alpha;
     if (valid) {
       vlast = (r == c) ? 1.0 : scprev * xprev;
-      wlast = fma(alpha_p, vlast, tprev * (__ldcg(wtmp + r) - sdot));
+      wlast = fma(alpha_p, vlast, tprev * (yr - sdot));
       if (sub == 0) A[r + (c - 1) * lda] = vlast;
     }
   }
