@@ -92,6 +92,8 @@ def load_library() -> ctypes.CDLL:
                               "(there is no CPU fallback)")
         lib = ctypes.CDLL(LIB_PATH)
         for name, (res, args) in SIGNATURES.items():
+            if os.environ.get("EM_LIB_PATH") and not hasattr(lib, name):
+                continue  # an older build under A/B: bind what it has
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args

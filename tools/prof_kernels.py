@@ -33,6 +33,8 @@ def main(which):
     g = torch.Generator(device="cuda").manual_seed(7)
     out = {}
     n = 16384
+    if "SYMV_KEEP_MB" in os.environ:  # EM_CFG_SYMV_L2_KEEP_MB (every branch)
+        nat.check(lib.em_config(ctx, 3, int(os.environ["SYMV_KEEP_MB"])))
     if which in ("symv", "all"):
         a = torch.randn(n, n, device="cuda", dtype=torch.float64, generator=g)
         x = torch.randn(n, device="cuda", dtype=torch.float64, generator=g)
