@@ -6,12 +6,14 @@
 // forward then backward substitution with the factor (tri_solve_vec,
 // _kernels.py:39-53), I += x.
 //
-// GPU form per step: b = E u^k - dt*R*I (lower-triangle symv, HBM-bound), then two
-// PERSISTENT triangular-solve kernels. Block rows of 64 are claimed in order from
-// an atomic counter; a CTA streams the off-diagonal tiles of its block row as
-// soon as the producing block's flag (release/acquire, epoch-tagged) is up,
-// reduces with warp shuffles / shared memory, and applies the pre-inverted
-// 64x64 diagonal block. Memory-bound: each solve reads the packed factor once.
+// GPU form per step: b = E u^k - dt*R*I (CSR SpMV of the stencil R, or the lower-triangle
+// symv), then two PERSISTENT triangular-solve kernels. Block rows of 64 are claimed in
+// order from an atomic counter; a CTA streams the off-diagonal tiles of its block row as
+// soon as the producing block's flag (release/acquire, epoch-tagged) is up, reduces with
+// warp shuffles / shared memory and applies the pre-inverted 64x64 diagonal block. The
+// product with the neighbouring block's solution is folded into one precomputed 64x64
+// matrix (E_r = D_r C_{r,r-1}, F_r = D_r^T C_{r+1,r}^T), so a block's chain step is one
+// product. Each solve reads the factor once.
 #include "common.cuh"
 #include "ctx.h"
 #include "gemm.h"
@@ -25,7 +27,7 @@ struct em_td1_plan {
   int64_t n = 0;
   int n_p = 0, n_s = 0, n_u = 0;
   double dt = 0, theta = 0;
-  em::DBuf C, R, Dinv, DinvT, E, work, b, y, x;
+  em::DBuf C, R, Dinv, DinvT, Ef, Fb, E, work, b, y, x;
   em::Csr Rs;          // R as CSR when it is sparse (the stencil): R I is an SpMV
   bool r_sparse = false;
   em::DArr<unsigned long long>* flags = nullptr;
@@ -128,8 +130,12 @@ EM_DEVINL void wait_flags(const unsigned long long* flags, int64_t j0, int64_t j
 }
 
 // Forward solve C y = b, C lower (col-major, ld ldc). Block rows claimed in order.
+// y_r = D_r (b_r - sum_{j < r-1} C_rj y_j) - E_r y_{r-1} with E_r = D_r C_{r,r-1}
+// precomputed: everything but one 64 x 64 product waits only on blocks up to r-2, so the
+// dependency chain per block is: see y_{r-1}, one product, publish y_r.
 __global__ void __launch_bounds__(256) trsv_fwd_kernel(int64_t n, const double* __restrict__ C,
                                                        int64_t ldc, const double* __restrict__ Dinv,
+                                                       const double* __restrict__ Ef,
                                                        const double* __restrict__ b,
                                                        double* __restrict__ y,
                                                        unsigned long long* flags,
@@ -148,38 +154,30 @@ __global__ void __launch_bounds__(256) trsv_fwd_kernel(int64_t n, const double* 
     if (r >= nblk) break;
     const int64_t r0 = r * TS, row = r0 + tx;
     double acc = 0.0;
-    // Off the dependency chain: the diagonal inverse and b_r are loaded up front,
-    // and tile j+1 is loaded before waiting for block j, so only the short y_j
-    // read sits on the chain.
+    // Off the dependency chain: D_r, E_r and b_r are loaded up front, and tile j+1 is
+    // loaded before waiting for block j.
     const double* D = Dinv + r * TS * TS;
-    double dv[16];
+    const double* Er = Ef + r * TS * TS;
+    double dv[16], ev[16];
 #pragma unroll
-    for (int cc = 0; cc < 16; ++cc) dv[cc] = D[tx + (ty * 16 + cc) * TS];
+    for (int cc = 0; cc < 16; ++cc) {
+      dv[cc] = D[tx + (ty * 16 + cc) * TS];
+      ev[cc] = r > 0 ? Er[tx + (ty * 16 + cc) * TS] : 0.0;
+    }
     const double bb = (tid < TS && r0 + tid < n) ? b[r0 + tid] : 0.0;
     double a[16];
-    if (r > 0) {
+    if (r > 1) {
 #pragma unroll
       for (int cc = 0; cc < 16; ++cc) a[cc] = (row < n) ? C[row + (ty * 16 + cc) * ldc] : 0.0;
     }
-    int64_t ready = -1;  // highest block index known to be published
-    for (int64_t j = 0; j < r; ++j) {
+    for (int64_t j = 0; j + 1 < r; ++j) {  // tiles j <= r - 2
       double an[16];
-      if (j + 1 < r) {
+      if (j + 2 < r) {
         const int64_t c1 = (j + 1) * TS + ty * 16;
 #pragma unroll
         for (int cc = 0; cc < 16; ++cc) an[cc] = (row < n) ? C[row + (c1 + cc) * ldc] : 0.0;
       }
-      if (j > ready) {
-        __shared__ int64_t jr;
-        if (tid == 0) {
-          while (ld_acquire(flags + j) != epoch) {}
-          int64_t e = j;
-          while (e + 1 < r && ld_acquire(flags + e + 1) == epoch) ++e;
-          jr = e;
-        }
-        __syncthreads();
-        ready = jr;
-        __syncthreads();
+      while (ld_acquire(flags + j) != epoch) {
       }
       const int64_t c0 = j * TS + ty * 16;
 #pragma unroll
@@ -191,13 +189,31 @@ __global__ void __launch_bounds__(256) trsv_fwd_kernel(int64_t n, const double* 
     __syncthreads();
     if (tid < TS) part[tid] = bb - (red[0][tid] + red[1][tid] + red[2][tid] + red[3][tid]);
     __syncthreads();
-    // y_r = Dinv_r * part
+    // p_r = D_r part (still off the chain)
     double s = 0.0;
 #pragma unroll
     for (int cc = 0; cc < 16; ++cc) s = fma(dv[cc], part[ty * 16 + cc], s);
     red[ty][tx] = s;
     __syncthreads();
-    if (tid < TS && r0 + tid < n) y[r0 + tid] = red[0][tid] + red[1][tid] + red[2][tid] + red[3][tid];
+    double pr = 0.0;
+    if (tid < TS) pr = red[0][tid] + red[1][tid] + red[2][tid] + red[3][tid];
+    // the chain: y_r = p_r - E_r y_{r-1}
+    double se = 0.0;
+    if (r > 0) {
+      while (ld_acquire(flags + r - 1) != epoch) {
+      }
+      const int64_t c0 = (r - 1) * TS + ty * 16;
+      double yv[16];
+#pragma unroll
+      for (int cc = 0; cc < 16; ++cc) yv[cc] = __ldcg(y + c0 + cc);
+#pragma unroll
+      for (int cc = 0; cc < 16; ++cc) se = fma(ev[cc], yv[cc], se);
+    }
+    __syncthreads();  // red: the p_r readers are done
+    red[ty][tx] = se;
+    __syncthreads();
+    if (tid < TS && r0 + tid < n)
+      y[r0 + tid] = pr - ((red[0][tid] + red[1][tid]) + (red[2][tid] + red[3][tid]));
     // bar.sync orders the block's stores before thread 0's gpu-scope release (cumulative)
     __syncthreads();
     if (tid == 0) st_release(flags + r, epoch);
@@ -205,11 +221,13 @@ __global__ void __launch_bounds__(256) trsv_fwd_kernel(int64_t n, const double* 
 }
 
 // Backward solve C^T x = y; then I += x (and capture). Block rows claimed from the bottom.
+// x_r = DT_r (y_r - sum_{j > r+1} C_jr^T x_j) - F_r x_{r+1}, F_r = DT_r C_{r+1,r}^T
+// precomputed (DT_r = D_r^T): one 64 x 64 product on the dependency chain.
 __global__ void __launch_bounds__(256) trsv_bwd_kernel(
     int64_t n, const double* __restrict__ C, int64_t ldc, const double* __restrict__ Dinv,
-    const double* __restrict__ y, double* __restrict__ x, double* __restrict__ I,
-    double* __restrict__ Icap, unsigned long long* flags, unsigned int* counter,
-    unsigned long long epoch) {
+    const double* __restrict__ Fb, const double* __restrict__ y, double* __restrict__ x,
+    double* __restrict__ I, double* __restrict__ Icap, unsigned long long* flags,
+    unsigned int* counter, unsigned long long epoch) {
   __shared__ int64_t rblk;
   __shared__ double red[8][TS];
   __shared__ double part[TS];
@@ -226,39 +244,33 @@ __global__ void __launch_bounds__(256) trsv_bwd_kernel(
     double acc[16];
 #pragma unroll
     for (int cc = 0; cc < 16; ++cc) acc[cc] = 0.0;
-    // tiles (j, r), j = nblk-1 .. r+1; tile j-1 is prefetched before waiting for block j;
-    // the transposed diagonal inverse and y_r are loaded up front (off the chain)
+    // tiles (j, r), j = nblk-1 .. r+2; tile j-1 is prefetched before waiting for block j;
+    // DT_r, F_r and y_r are loaded up front (off the chain)
     const int64_t c0 = r0 + ty * 16;
     const double* D = Dinv + r * TS * TS;
-    double dv[16];
+    const double* Fr = Fb + r * TS * TS;
+    const bool has_next = r + 1 < nblk;
+    double dv[16], fv[16];
 #pragma unroll
-    for (int cc = 0; cc < 16; ++cc) dv[cc] = D[tx + (ty * 16 + cc) * TS];
+    for (int cc = 0; cc < 16; ++cc) {
+      dv[cc] = D[tx + (ty * 16 + cc) * TS];
+      fv[cc] = has_next ? Fr[tx + (ty * 16 + cc) * TS] : 0.0;
+    }
     const double yr = (tid < TS && r0 + tid < n) ? y[r0 + tid] : 0.0;
     double a[16];
-    if (nblk - 1 > r) {
+    if (nblk - 2 > r) {
       const int64_t rowj = (nblk - 1) * TS + tx;
 #pragma unroll
       for (int cc = 0; cc < 16; ++cc) a[cc] = (rowj < n) ? C[rowj + (c0 + cc) * ldc] : 0.0;
     }
-    int64_t ready = nblk;  // lowest block index known to be published
-    for (int64_t j = nblk - 1; j > r; --j) {
+    for (int64_t j = nblk - 1; j > r + 1; --j) {
       double an[16];
-      if (j - 1 > r) {
+      if (j - 1 > r + 1) {
         const int64_t rown = (j - 1) * TS + tx;
 #pragma unroll
         for (int cc = 0; cc < 16; ++cc) an[cc] = (rown < n) ? C[rown + (c0 + cc) * ldc] : 0.0;
       }
-      if (j < ready) {
-        __shared__ int64_t jr;
-        if (tid == 0) {
-          while (ld_acquire(flags + j) != epoch) {}
-          int64_t e = j;
-          while (e - 1 > r && ld_acquire(flags + e - 1) == epoch) --e;
-          jr = e;
-        }
-        __syncthreads();
-        ready = jr;
-        __syncthreads();
+      while (ld_acquire(flags + j) != epoch) {
       }
       const int64_t rowj = j * TS + tx;
       const double xv = (rowj < n) ? __ldcg(x + rowj) : 0.0;
@@ -281,15 +293,31 @@ __global__ void __launch_bounds__(256) trsv_bwd_kernel(
       part[tid] = yr - sumc;
     }
     __syncthreads();
-    // x_r = Dinv_r^T part with the pre-transposed block (coalesced):
-    // x[c] = sum_c' DinvT[c + c'*TS] part[c']
+    // p_r = DT_r part with the pre-transposed block (coalesced), still off the chain
     double s = 0.0;
 #pragma unroll
     for (int cc = 0; cc < 16; ++cc) s = fma(dv[cc], part[ty * 16 + cc], s);
     red[ty][tx] = s;
     __syncthreads();
+    double pr = 0.0;
+    if (tid < TS) pr = red[0][tid] + red[1][tid] + red[2][tid] + red[3][tid];
+    // the chain: x_r = p_r - F_r x_{r+1}
+    double sf = 0.0;
+    if (has_next) {
+      while (ld_acquire(flags + r + 1) != epoch) {
+      }
+      const int64_t cn = (r + 1) * TS + ty * 16;
+      double xn[16];
+#pragma unroll
+      for (int cc = 0; cc < 16; ++cc) xn[cc] = (cn + cc < n) ? __ldcg(x + cn + cc) : 0.0;
+#pragma unroll
+      for (int cc = 0; cc < 16; ++cc) sf = fma(fv[cc], xn[cc], sf);
+    }
+    __syncthreads();  // red: the p_r readers are done
+    red[ty][tx] = sf;
+    __syncthreads();
     if (tid < TS && r0 + tid < n) {
-      const double xv = red[0][tid] + red[1][tid] + red[2][tid] + red[3][tid];
+      const double xv = pr - ((red[0][tid] + red[1][tid]) + (red[2][tid] + red[3][tid]));
       x[r0 + tid] = xv;
       const double iv = I[r0 + tid] + xv;
       I[r0 + tid] = iv;
@@ -321,6 +349,28 @@ int64_t td1_plan_init(em_td1_plan* P, const double* L, int64_t ldl, const double
   P->DinvT.alloc((size_t)nblk * TS * TS, st);
   transpose_blocks_kernel<<<(unsigned)nblk, 256, 0, st>>>(P->Dinv.p, P->DinvT.p);
   EM_LAUNCHED();
+  // the chain products: Ef_r = D_r C_{r,r-1} (forward), Fb_r = D_r^T C_{r+1,r}^T (backward)
+  P->Ef.alloc((size_t)nblk * TS * TS, st);
+  P->Fb.alloc((size_t)nblk * TS * TS, st);
+  EM_CK(cudaMemsetAsync(P->Ef.p, 0, (size_t)nblk * TS * TS * sizeof(double), st));
+  EM_CK(cudaMemsetAsync(P->Fb.p, 0, (size_t)nblk * TS * TS * sizeof(double), st));
+  if (nblk > 1) {
+    std::vector<GemmArgs> pf, pb;
+    for (int64_t r = 1; r < nblk; ++r) {
+      const int64_t r0 = r * TS, bs = imin64(TS, n - r0);
+      pf.push_back(GemmArgs{bs, TS, bs, P->Dinv.p + r * TS * TS, TS, P->C.p + r0 + (r0 - TS) * n, n,
+                            P->Ef.p + r * TS * TS, TS, 1.0, 0.0, 0});
+      const int64_t q = r - 1;  // Fb_q with block q + 1 = r below it
+      pb.push_back(GemmArgs{TS, bs, TS, P->DinvT.p + q * TS * TS, TS, P->C.p + r0 + q * TS * n, n,
+                            P->Fb.p + q * TS * TS, TS, 1.0, 0.0, 0});
+    }
+    DArr<GemmArgs> df(pf.size(), st), db(pb.size(), st);
+    EM_CK(cudaMemcpyAsync(df.p, pf.data(), pf.size() * sizeof(GemmArgs), cudaMemcpyHostToDevice, st));
+    EM_CK(cudaMemcpyAsync(db.p, pb.data(), pb.size() * sizeof(GemmArgs), cudaMemcpyHostToDevice, st));
+    EM_CK(gemm_grouped(st, false, false, df.p, (int)pf.size(), 1));
+    EM_CK(gemm_grouped(st, false, true, db.p, (int)pb.size(), 1));
+    EM_CK(cudaStreamSynchronize(st));  // host argument arrays
+  }
   P->E.alloc((size_t)n * imax64(P->n_u, 1), st);
   if (P->n_u > 0) {
     td1_e_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, P->n_p, P->n_s, P->dt, P->theta,
@@ -369,14 +419,15 @@ static void td1_solve_step(em_td1_plan* P, double* I, double* Icap_col) {
   const int grid = (int)imin64(nblk, 2 * num_sms());
   {
     Stage s(st, ST_TD1_FWD);
-    trsv_fwd_kernel<<<grid, 256, 0, st>>>(n, P->C.p, n, P->Dinv.p, P->b.p, P->y.p, P->flags->p,
-                                          P->counters->p, P->epoch);
+    trsv_fwd_kernel<<<grid, 256, 0, st>>>(n, P->C.p, n, P->Dinv.p, P->Ef.p, P->b.p,
+                                                  P->y.p, P->flags->p, P->counters->p, P->epoch);
     EM_LAUNCHED();
   }
   {
     Stage s(st, ST_TD1_BWD);
-    trsv_bwd_kernel<<<grid, 256, 0, st>>>(n, P->C.p, n, P->DinvT.p, P->y.p, P->x.p, I, Icap_col,
-                                          P->flags->p + nblk, P->counters->p + 1, P->epoch);
+    trsv_bwd_kernel<<<grid, 256, 0, st>>>(n, P->C.p, n, P->DinvT.p, P->Fb.p, P->y.p,
+                                                  P->x.p, I, Icap_col, P->flags->p + nblk,
+                                                  P->counters->p + 1, P->epoch);
     EM_LAUNCHED();
   }
 }

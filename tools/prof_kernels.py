@@ -76,7 +76,7 @@ def main(which):
         out["td2_recon_TFps"] = 2 * n_obs * n * T / t / 1e12
         lib.em_td2_plan_destroy(plan)
     if which in ("td1", "all"):
-        m = 8192
+        m = int(os.environ.get("TD1_N", 8192))
         b = torch.randn(m, m, device="cuda", dtype=torch.float64, generator=g) / np.sqrt(m)
         lmat = b @ b.T + torch.eye(m, device="cuda", dtype=torch.float64)
         rmat = torch.eye(m, device="cuda", dtype=torch.float64) * 1e-3
@@ -91,7 +91,8 @@ def main(which):
         s = nat.zeros(m)
         t = timed(lambda: nat.check(lib.em_td1_run(plan, steps, nat.ptr(drive), nat.ptr(s), None, 1,
                                                    None)), reps=1)
-        out["td1_n8192_per_step_ms"] = t / steps * 1e3
+        out[f"td1_n{m}_per_step_ms"] = t / steps * 1e3
+        out[f"td1_n{m}_factor_GBps"] = 2 * 8 * m * (m + 1) / 2 / (t / steps) / 1e9
         lib.em_td1_plan_destroy(plan)
     if which == "symvsweep":
         big = torch.randn(n, n, device="cuda", dtype=torch.float64, generator=g)
