@@ -16,7 +16,8 @@
 
 namespace em {
 
-// tile configuration (em_config debug key 96): 0 / 2 = CfgT, 3 = CfgS (A/B). In the C2
+// tile configuration (em_config debug key 96): 0 = CfgT3 for transposed A, else CfgT;
+// 2 = CfgT, 3 = CfgS, 4 = CfgT3 (A/B). In the C2
 // step CfgT everywhere beats the shape rule "CfgS for long k" that the isolated probes
 // suggested (2113 -> 2103 ms: ormtr 326 -> 322, l_n product 160 -> 154)
 int64_t g_gemm_cfg = 0;
@@ -45,6 +46,7 @@ using CfgS = GCfg<128, 64, 4, 4, 2>;
 // better anywhere): every configuration plateaus at ~32 TF/s on large squares
 // (cuBLAS: 36).
 using CfgT = GCfg<64, 64, 4, 4, 4>;
+using CfgT3 = GCfg<64, 64, 4, 4, 3>;  // three CTAs per SM (up to 168 registers)
 constexpr int GBM = 128;  // m tile of both configurations (split-K / grouped bookkeeping)
 
 template <int TA, class C>
@@ -62,7 +64,7 @@ struct BTile {
 template <int TA, int TB, class C>
 constexpr int gstages() {
   constexpr int per = (ATile<TA, C>::size + BTile<TB, C>::size) * 8;
-  return C::MINB_ >= 4 ? (per * 4 * 4 <= 220 * 1024 ? 4 : 3)
+  return C::MINB_ >= 3 ? (per * 4 * C::MINB_ <= 220 * 1024 ? 4 : 3)
                        : (per * 4 * C::MINB_ <= 226 * 1024 ? 4 : 3);
 }
 
@@ -314,7 +316,7 @@ static cudaError_t launch_t(const GemmArgs& p, cudaStream_t st) {
     configured = true;
   }
   const int64_t tiles = ((p.m + C::M - 1) / C::M) * ((p.n + C::N - 1) / C::N);
-  const int sms = num_sms() * (C::MINB_ >= 4 ? 4 : 1);  // CfgT: four CTA slots per SM
+  const int sms = num_sms() * (C::MINB_ >= 3 ? C::MINB_ : 1);  // CfgT: CTA slots per SM
   // few output tiles and a long k loop: split k so every SM has work
   // pick the split count with the best wave quantisation (each slice >= 512 deep)
   int64_t splits = 1;
@@ -362,6 +364,10 @@ static cudaError_t launch_v(const GemmArgs& p, cudaStream_t st) {
   bool vec = al(p.A) && al(p.B) && (p.lda % 2 == 0) && (p.ldb % 2 == 0);
   // 16-byte chunks also need the tile starts to be even along the contiguous dim;
   // tiles start at multiples of 128 (long dims) and 16 (k), so base alignment suffices.
+  // transposed A: three CTAs per SM (more registers) measured faster (V^T Z at K = 16k:
+  // 29.6 -> 31.6 TF/s, rank-256 A^T B 28.1 -> 30.3); non-transposed A: four
+  if (g_gemm_cfg == 4 || (g_gemm_cfg == 0 && TA))
+    return vec ? launch_t<TA, TB, LOWER, 2, CfgT3>(p, st) : launch_t<TA, TB, LOWER, 1, CfgT3>(p, st);
   if (g_gemm_cfg != 3)
     return vec ? launch_t<TA, TB, LOWER, 2, CfgT>(p, st) : launch_t<TA, TB, LOWER, 1, CfgT>(p, st);
   return vec ? launch_t<TA, TB, LOWER, 2, CfgS>(p, st) : launch_t<TA, TB, LOWER, 1, CfgS>(p, st);

@@ -11,11 +11,11 @@ from tests.conftest import golden
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("cfg", [0, 2, 3])
+@pytest.mark.parametrize("cfg", [0, 2, 3, 4])
 def test_dgemm_all_transposes_vs_numpy(rng, cfg):
-    """em_config debug key 96 selects the tile configuration: 0 by k (64x64 tiles for
-    k <= 1024, else 128x64), 2 always 64x64, 3 always 128x64; (40, 70, 6000) takes
-    split-K."""
+    """em_config debug key 96 selects the tile configuration: 0 the default (64x64 tiles,
+    three CTAs per SM for a transposed A, four otherwise), 2 64x64 / four CTAs, 3 128x64,
+    4 64x64 / three CTAs; (40, 70, 6000) takes split-K."""
     from paper_2407_11993_b200 import _native as nat
     ctx = nat.context()
     lib = nat.load_library()
