@@ -144,7 +144,7 @@ int em_config(em_ctx* ctx, int key, int64_t value) {
       em::g_symv_keep_mb = value;
       return EM_OK;
     }
-    if (key == 96) {  // debug: GEMM tile configuration (0 auto, 2 64x64, 3 128x64)
+    if (key == 96) {  // debug: GEMM tiles (0 default, 2 64x64 x4, 3 128x64, 4 64x64 x3)
       em::g_gemm_cfg = value;
       return EM_OK;
     }
