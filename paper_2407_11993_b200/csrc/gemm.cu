@@ -416,6 +416,7 @@ cudaError_t gemm_lower_a(cudaStream_t st, int64_t m, int64_t n, int64_t k, doubl
   if (m <= 0 || n <= 0) return cudaSuccess;
   if (k <= 0) return scale_matrix(st, m, n, beta, C, ldc, false, 0);
   GemmArgs p{m, n, k, A, lda, B, ldb, C, ldc, alpha, beta, 0};
+  if (g_gemm_cfg == 4) return launch_lower_a<CfgT3>(p, st);
   if (g_gemm_cfg != 3) return launch_lower_a<CfgT>(p, st);
   return launch_lower_a<CfgS>(p, st);
 }
