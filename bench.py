@@ -461,6 +461,26 @@ def run_ours(args, cfg, rank, world, local_rank):
                                           + stages.get("td2_carry", (0, 0))[0]) / n_steps_timed
                                          * 1e-3)}
 
+    # the whole eigensolve against the FP64 tensor peak (north-star target: >= 0.6), on
+    # SURVEY 8(d)'s operation counts: (17/3) N^3 for the dense one-stage LAPACK sequence,
+    # and with R's band b = ny nz exploited (10/3) N^3 + 6 N^2 b
+    eig_ms = sum(stages[k][0] for k in ("potrf_R", "sygst", "potrf_L", "sytrd", "stedc",
+                                        "ormtr", "trsm_back", "finalize", "post_gemm")
+                 if k in stages) / n_steps_timed
+    if eig_ms > 0:
+        bw = cfg["grid"][1] * cfg["grid"][2]
+        fp64 = peaks.get("fp64_tflops", 37.1)
+        dense = 17.0 / 3.0 * n ** 3
+        banded = 10.0 / 3.0 * n ** 3 + 6.0 * n ** 2 * bw
+        rl["eigensolve_roofline"] = {
+            "ms_per_step": eig_ms, "bound": "tensor", "unit": "TFLOP/s", "peak": fp64,
+            "achieved_dense_count": dense / (eig_ms * 1e-3) / 1e12,
+            "frac_dense_count": dense / (eig_ms * 1e-3) / 1e12 / fp64,
+            "achieved_banded_count": banded / (eig_ms * 1e-3) / 1e12,
+            "frac_banded_count": banded / (eig_ms * 1e-3) / 1e12 / fp64,
+            "note": "one-stage tridiagonalisation: its symv (4/3 N^3 bytes) is HBM-bound, "
+                    "so the eigensolve is not tensor-bound (DESIGN.md 3, 7)"}
+
     # ---- TD1 comparator (bounded: a few hundred steps, extrapolated) and CPU baseline
     extra = {}
     if rank == 0 and not args.no_td1:
