@@ -507,14 +507,21 @@ __global__ void __launch_bounds__(256) q2_tfactor_kernel(int64_t n, const Q2Bloc
   }
 }
 
-// Explicit V (VR x b, column-major, ld VR) of a list of blocks for one wavefront.
+// Explicit V (VR x b, column-major, ld VR) of a list of blocks for one wavefront, and
+// VT = V T (the block's T folded into the update: Z -= (V T) (V^T Z), one GEMM fewer).
+// T2 holds each block's T row-major (T upper triangular).
 __global__ void __launch_bounds__(256) q2_buildv_kernel(int64_t n, const Q2Block* __restrict__ blocks,
                                                         const int64_t* __restrict__ ids,
                                                         const double* __restrict__ V2,
                                                         const int64_t* __restrict__ toff,
-                                                        double* __restrict__ Vout) {
+                                                        const double* __restrict__ T2,
+                                                        double* __restrict__ Vout,
+                                                        double* __restrict__ VTout) {
+  extern __shared__ double Vs[];  // VR x B2 (64 KB), column-major like Vout
   const Q2Block blk = blocks[ids[blockIdx.x]];
   double* V = Vout + blockIdx.x * (size_t)VR * B2;
+  double* VT = VTout + blockIdx.x * (size_t)VR * B2;
+  const double* T = T2 + ids[blockIdx.x] * (size_t)B2 * B2;
   const int64_t R0 = blk.g * B2 + 1 + blk.k * B2;
   for (int idx = threadIdx.x; idx < VR * B2; idx += blockDim.x) {
     const int r = idx % VR, t = idx / VR;  // row r of column t
@@ -524,6 +531,17 @@ __global__ void __launch_bounds__(256) q2_buildv_kernel(int64_t n, const Q2Block
     if (i >= 0 && i < B2 && R0 + r < n && s < n - 1 && blk.k < ntasks(n, s))
       val = V2[(toff[s] + blk.k) * B2 + i];
     V[idx] = val;
+    Vs[idx] = val;
+  }
+  __syncthreads();
+  // VT[r, j] = sum_{i <= j} V[r, i] T[i, j]; V[r, i] = 0 unless i <= r <= i + 63
+  for (int idx = threadIdx.x; idx < VR * B2; idx += blockDim.x) {
+    const int r = idx % VR, j = idx / VR;
+    const int i0 = r - (B2 - 1) > 0 ? r - (B2 - 1) : 0;
+    const int i1 = r < j ? r : j;
+    double acc = 0.0;
+    for (int i = i0; i <= i1; ++i) acc = fma(Vs[i * VR + r], __ldg(T + i * B2 + j), acc);
+    VT[idx] = acc;
   }
 }
 
@@ -576,8 +594,8 @@ void syev_two_stage(cudaStream_t st, int64_t n, double* A, int64_t lda, double* 
     // Q2: blocks (g, k) = reflectors of sweeps g*b .. g*b+b-1 at position k. The order
     // "groups last to first, positions ascending" is satisfied by applying wavefronts
     // w = k + 2 (G-1-g) in increasing w: blocks of one wavefront touch disjoint rows and
-    // every block they depend on sits on an earlier wavefront. Each wavefront is three
-    // grouped DMMA GEMMs over all columns of Z.
+    // every block they depend on sits on an earlier wavefront. Each wavefront is two
+    // grouped DMMA GEMMs over all columns of Z (W = V^T Z, Z -= (V T) W).
     std::vector<Q2Block> blocks;
     const int64_t ngroups = (nsw + b - 1) / b;
     for (int64_t g = ngroups - 1; g >= 0; --g) {
@@ -596,6 +614,8 @@ void syev_two_stage(cudaStream_t st, int64_t n, double* A, int64_t lda, double* 
                                  (int)smt));
       q2_tfactor_kernel<<<(unsigned)nblk, 256, smt, st>>>(n, dblk.p, V2.p, TAU2.p, dtoff.p, T2.p);
       EM_LAUNCHED();
+      EM_CK(cudaFuncSetAttribute(q2_buildv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(VR * B2 * sizeof(double))));
       // wavefront lists (chunks of at most QCH blocks)
       constexpr int QCH = 64;
       std::vector<std::vector<int64_t>> waves;
@@ -613,7 +633,7 @@ void syev_two_stage(cudaStream_t st, int64_t n, double* A, int64_t lda, double* 
       std::vector<int64_t> ids;
       std::vector<GemmArgs> args;
       std::vector<int64_t> wstart;
-      DBuf Vb((size_t)QCH * VR * B2, st), W1((size_t)QCH * B2 * n, st), W2((size_t)QCH * B2 * n, st);
+      DBuf Vb((size_t)QCH * VR * B2, st), VTb((size_t)QCH * VR * B2, st), W1((size_t)QCH * B2 * n, st);
       for (auto& wl : waves) {
         wstart.push_back((int64_t)ids.size());
         for (size_t j = 0; j < wl.size(); ++j) {
@@ -621,13 +641,11 @@ void syev_two_stage(cudaStream_t st, int64_t n, double* A, int64_t lda, double* 
           const int64_t R0 = bk.g * b + 1 + bk.k * b;
           const int64_t nrow = imin64(VR - 1, n - R0);
           double* Vj = Vb.p + j * (size_t)VR * B2;
+          double* VTj = VTb.p + j * (size_t)VR * B2;
           double* W1j = W1.p + j * (size_t)B2 * n;
-          double* W2j = W2.p + j * (size_t)B2 * n;
-          const double* Tj = T2.p + wl[j] * (size_t)B2 * B2;  // row-major T == col-major T^T
           ids.push_back(wl[j]);
           args.push_back(GemmArgs{B2, n, nrow, Vj, VR, Z + R0, ldz, W1j, B2, 1.0, 0.0, 0});
-          args.push_back(GemmArgs{B2, n, B2, Tj, B2, W1j, B2, W2j, B2, 1.0, 0.0, 0});
-          args.push_back(GemmArgs{nrow, n, B2, Vj, VR, W2j, B2, Z + R0, ldz, -1.0, 1.0, 0});
+          args.push_back(GemmArgs{nrow, n, B2, VTj, VR, W1j, B2, Z + R0, ldz, -1.0, 1.0, 0});
         }
       }
       wstart.push_back((int64_t)ids.size());
@@ -639,17 +657,17 @@ void syev_two_stage(cudaStream_t st, int64_t n, double* A, int64_t lda, double* 
       std::vector<GemmArgs> ph(args.size());
       const size_t np = ids.size();
       for (size_t i = 0; i < np; ++i)
-        for (int q = 0; q < 3; ++q) ph[q * np + i] = args[3 * i + q];
+        for (int q = 0; q < 2; ++q) ph[q * np + i] = args[2 * i + q];
       EM_CK(cudaMemcpyAsync(dargs.p, ph.data(), ph.size() * sizeof(GemmArgs),
                             cudaMemcpyHostToDevice, st));
       const int tiles_n = (int)((n + 127) / 128);
       for (size_t wi = 0; wi + 1 < wstart.size(); ++wi) {
         const int64_t o = wstart[wi], cnt = wstart[wi + 1] - wstart[wi];
-        q2_buildv_kernel<<<(unsigned)cnt, 256, 0, st>>>(n, dblk.p, dids.p + o, V2.p, dtoff.p, Vb.p);
+        q2_buildv_kernel<<<(unsigned)cnt, 256, (size_t)VR * B2 * sizeof(double), st>>>(
+            n, dblk.p, dids.p + o, V2.p, dtoff.p, T2.p, Vb.p, VTb.p);
         EM_LAUNCHED();
         EM_CK(gemm_grouped(st, true, false, dargs.p + o, (int)cnt, tiles_n));
-        EM_CK(gemm_grouped(st, true, false, dargs.p + np + o, (int)cnt, tiles_n));
-        EM_CK(gemm_grouped(st, false, false, dargs.p + 2 * np + o, (int)cnt, tiles_n));
+        EM_CK(gemm_grouped(st, false, false, dargs.p + np + o, (int)cnt, tiles_n));
       }
       EM_CK(cudaStreamSynchronize(st));  // host argument arrays / device lists lifetime
     }
