@@ -17,6 +17,7 @@ namespace em {
 extern int64_t g_two_stage_min;
 extern int g_sytrd_dbg;
 extern int g_band_off;
+extern int g_q2_mode;
 extern int g_symv_align_off;
 extern int64_t g_symv_keep_mb;
 extern int64_t g_gemm_cfg;
@@ -146,6 +147,10 @@ int em_config(em_ctx* ctx, int key, int64_t value) {
     }
     if (key == 96) {  // debug: GEMM tiles (0 default, 2 64x64 x4, 3 128x64, 4 64x64 x3)
       em::g_gemm_cfg = value;
+      return EM_OK;
+    }
+    if (key == 97) {  // debug: Q2 back-transform (0 column strips, 1 wavefront GEMMs)
+      em::g_q2_mode = (int)value;
       return EM_OK;
     }
     if (key == 98) {  // debug: sytrd switches (bit0 no TMA symv, bit1 no PDL, bit2 no graph,

@@ -545,6 +545,316 @@ __global__ void __launch_bounds__(256) q2_buildv_kernel(int64_t n, const Q2Block
   }
 }
 
+// ---- Q2 back-transform, column-strip form ----------------------------------------------
+// The columns of Z transform independently, so one CTA owns a strip of WC columns and
+// applies every block of a sweep group in order (positions ascending) with no
+// inter-CTA synchronisation. Block k of group g touches rows W0 + 1 .. W0 + 127,
+// W0 = 64 (g + k): consecutive blocks overlap by 64 rows, so the strip's rows live in
+// a ring of three 64-row halves in shared memory (two for the window, one being
+// prefetched), each half read from and written to HBM once per group instead of the
+// three passes of the grouped-GEMM form. Per block, on DMMA:
+//   W  = V^T Zwin      (64 x WC, k = 128; the parallelogram's zero k-range skipped)
+//   Zwin -= (V T) W    (128 x WC, k = 64; VT rows r only need j >= r - 64)
+// with V in compact form (64 reflectors x 64 entries) and VT = V T built per group
+// (row-major, window coordinates). Loads of the next block's V, VT and Z half are
+// issued while the current block computes (cp.async groups).
+constexpr int Q2_LDC = 3 * 64 + 4;  // Z ring, column-major [col][3 halves]: = 4 mod 16
+constexpr int Q2_LDV = 85;          // compact reflectors [t][8 + i], zero pads: LDV - 1 = 4 mod 16
+constexpr int Q2_LDT = 68;          // VT row-major [r][j]: = 4 mod 16
+int g_q2_mode = 0;                  // debug key 97: 1 = the wavefront grouped-GEMM form
+
+// VT (128 x 64 row-major, window row r = global row 64 (g + k) + r) of every block of
+// group g; T2g = the group's T factors (row-major 64 x 64, upper).
+__global__ void __launch_bounds__(256) q2_vt_kernel(int64_t n, int64_t g,
+                                                    const double* __restrict__ V2,
+                                                    const int64_t* __restrict__ toff,
+                                                    const double* __restrict__ T2g,
+                                                    double* __restrict__ VT) {
+  __shared__ double Vs[B2 * (B2 + 1)];  // [t][i]
+  const int64_t k = blockIdx.x;
+  const double* T = T2g + k * B2 * B2;
+  const int64_t W0 = B2 * (g + k);
+  for (int e = threadIdx.x; e < B2 * B2; e += blockDim.x) {
+    const int t = e >> 6, i = e & 63;
+    const int64_t s = g * B2 + t;
+    double v = 0.0;
+    if (s < n - 1 && k < ntasks(n, s) && W0 + 1 + t + i < n) v = V2[(toff[s] + k) * B2 + i];
+    Vs[t * (B2 + 1) + i] = v;
+  }
+  __syncthreads();
+  double* out = VT + k * (int64_t)VR * B2;
+  for (int e = threadIdx.x; e < VR * B2; e += blockDim.x) {
+    const int r = e >> 6, j = e & 63;
+    const int i0 = r - B2 > 0 ? r - B2 : 0;
+    const int i1 = r - 1 < j ? r - 1 : j;
+    double acc = 0.0;
+    for (int i = i0; i <= i1; ++i) acc = fma(Vs[i * (B2 + 1) + (r - 1 - i)], __ldg(T + i * B2 + j), acc);
+    out[e] = acc;
+  }
+}
+
+template <int NJ>
+struct Q2Strip {
+  static constexpr int WC = 8 * NJ;
+  static constexpr int LDW = (WC + 11) / 16 * 16 + 4;  // W row-major [j][c]: = 4 mod 16
+  static constexpr int OFF_W = WC * Q2_LDC;
+  static constexpr int OFF_V = OFF_W + B2 * LDW;
+  static constexpr int OFF_T = OFF_V + B2 * Q2_LDV;
+  static constexpr size_t SMEM = (size_t)(OFF_T + VR * Q2_LDT) * sizeof(double);
+};
+
+// rows 64 hg .. 64 hg + 63 of the strip's columns into ring slot hg % 3
+template <int NJ>
+EM_DEVINL void q2_load_half(double* Zw, const double* Z, int64_t ldz, int64_t n, int64_t ncols,
+                            int64_t c0, int64_t hg) {
+  const int slot = (int)(hg % 3);
+  for (int e = threadIdx.x; e < 64 * Q2Strip<NJ>::WC; e += blockDim.x) {
+    const int i = e & 63, c = e >> 6;
+    const int64_t row = 64 * hg + i, col = c0 + c;
+    const bool v = row < n && col < ncols;
+    cp_async8(Zw + c * Q2_LDC + slot * 64 + i, v ? Z + row + col * ldz : Z, v);
+  }
+}
+
+// W rows t = 8 W + gq of block k: W[t][c] = sum_r V[r][t] Zwin[r][c] over the 18 k-steps
+// r = 8 W + 4 s + tq (V[r][t] = v_t[r - 1 - t], zero outside [t + 1, t + 64]: the padded
+// compact row makes that a plain load). Even and odd steps accumulate separately (two
+// DMMA chains per tile); every address is a per-thread base plus an immediate.
+template <int NJ, int W>  // NJ: column fragments of this warp
+EM_DEVINL void q2_step_a(const double* zlo, const double* zhi, const double* vrow, double* wrow) {
+  double acc[2][NJ][2];
+#pragma unroll
+  for (int p = 0; p < 2; ++p)
+#pragma unroll
+    for (int jj = 0; jj < NJ; ++jj) acc[p][jj][0] = acc[p][jj][1] = 0.0;
+#pragma unroll
+  for (int s = 0; s < 18; ++s) {
+    const int r = 8 * W + 4 * s;  // + tq (in the bases)
+    const double a = vrow[4 * s];
+    const double* zc = (r < 64 ? zlo : zhi) + r;
+#pragma unroll
+    for (int jj = 0; jj < NJ; ++jj)
+      dmma884(acc[s & 1][jj][0], acc[s & 1][jj][1], a, zc[8 * jj * Q2_LDC]);
+  }
+#pragma unroll
+  for (int jj = 0; jj < NJ; ++jj) {
+    wrow[8 * jj] = acc[0][jj][0] + acc[1][jj][0];
+    wrow[8 * jj + 1] = acc[0][jj][1] + acc[1][jj][1];
+  }
+}
+
+// Zwin -= VT W for row fragments W (top half; the result goes to HBM through zg) and
+// 15 - W (bottom half; back to the ring). VT[r][j] = 0 for j < r - 64, so the bottom
+// fragment joins at step s1 = 14 - 2 W; both share the W fragments.
+template <int NJ, int LDW, int W>  // NJ: column fragments of this warp
+EM_DEVINL void q2_step_c(double* z0, double* z1, const double* arow0, const double* arow1,
+                         const double* bcol, double* zg, int64_t ldz, int64_t cl) {
+  constexpr int s1 = 14 - 2 * W;
+  double c0a[NJ][2], c1a[NJ][2];
+#pragma unroll
+  for (int jj = 0; jj < NJ; ++jj) {
+    c0a[jj][0] = z0[8 * jj * Q2_LDC];
+    c0a[jj][1] = z0[(8 * jj + 1) * Q2_LDC];
+    c1a[jj][0] = z1[8 * jj * Q2_LDC];
+    c1a[jj][1] = z1[(8 * jj + 1) * Q2_LDC];
+  }
+#pragma unroll
+  for (int s = 0; s < 16; ++s) {
+    const double x0 = -arow0[4 * s];
+    if (s < s1) {
+#pragma unroll
+      for (int jj = 0; jj < NJ; ++jj)
+        dmma884(c0a[jj][0], c0a[jj][1], x0, bcol[4 * s * LDW + 8 * jj]);
+    } else {
+      const double x1 = -arow1[4 * s];
+#pragma unroll
+      for (int jj = 0; jj < NJ; ++jj) {
+        const double b = bcol[4 * s * LDW + 8 * jj];
+        dmma884(c0a[jj][0], c0a[jj][1], x0, b);
+        dmma884(c1a[jj][0], c1a[jj][1], x1, b);
+      }
+    }
+  }
+#pragma unroll
+  for (int jj = 0; jj < NJ; ++jj) {
+    if (zg) {
+      if (8 * jj < cl) zg[8 * jj * ldz] = c0a[jj][0];
+      if (8 * jj + 1 < cl) zg[(8 * jj + 1) * ldz] = c0a[jj][1];
+    }
+    z1[8 * jj * Q2_LDC] = c1a[jj][0];
+    z1[(8 * jj + 1) * Q2_LDC] = c1a[jj][1];
+  }
+}
+
+template <int NJ>
+__global__ void __launch_bounds__(512, 1) q2_strip_kernel(int64_t n, int64_t ncols, int64_t g,
+                                                          int64_t K, const double* __restrict__ V2,
+                                                          const int64_t* __restrict__ toff,
+                                                          const double* __restrict__ VT,
+                                                          double* __restrict__ Z, int64_t ldz) {
+  using S = Q2Strip<NJ>;
+  extern __shared__ double sm[];
+  double* Zw = sm;
+  double* Ws = sm + S::OFF_W;
+  double* Vc = sm + S::OFF_V;
+  double* VTs = sm + S::OFF_T;
+  __shared__ int64_t s_toff[B2];  // task offset of each sweep of the group
+  __shared__ int64_t s_nt[B2];    // its task count (0: no such sweep)
+  // 16 warps: warp & 7 picks the row fragments, warp >> 3 the half of the column
+  // fragments (NH of them) the warp works on
+  static_assert(NJ % 2 == 0, "two column halves");
+  constexpr int NH = NJ / 2;
+  const int tid = threadIdx.x, warp = (tid >> 5) & 7, lane = tid & 31, gq = lane >> 2,
+            tq = lane & 3;
+  const int jb = 8 * NH * (tid >> 8);  // first column of the warp's half
+  const int64_t c0 = (int64_t)blockIdx.x * S::WC;
+  if (tid < B2) {
+    const int64_t s = g * B2 + tid;
+    s_toff[tid] = s < n - 1 ? toff[s] : 0;
+    s_nt[tid] = s < n - 1 ? ntasks(n, s) : 0;
+  }
+  for (int e = tid; e < B2 * Q2_LDV; e += blockDim.x) Vc[e] = 0.0;  // the pads stay zero
+  __syncthreads();
+
+  auto load_v = [&](int64_t k) {
+    if (k >= K) return;
+    const int64_t W0 = B2 * (g + k);
+    for (int e = tid; e < B2 * B2; e += blockDim.x) {
+      const int t = e >> 6, i = e & 63;
+      const bool v = k < s_nt[t] && W0 + 1 + t + i < n;
+      cp_async8(Vc + t * Q2_LDV + 8 + i, v ? V2 + (s_toff[t] + k) * B2 + i : V2, v);
+    }
+  };
+  auto load_vt = [&](int64_t k) {
+    const double* src = VT + k * (int64_t)VR * B2;
+    for (int e = tid; e < VR * B2 / 2; e += blockDim.x) {
+      const int r = e >> 5, j = (e & 31) * 2;
+      cp_async16(VTs + r * Q2_LDT + j, src + r * B2 + j, 16);
+    }
+  };
+
+  // prologue: halves g, g + 1 and V(0)
+  q2_load_half<NJ>(Zw, Z, ldz, n, ncols, c0, g);
+  q2_load_half<NJ>(Zw, Z, ldz, n, ncols, c0, g + 1);
+  load_v(0);
+  cp_async_commit();
+
+  for (int64_t k = 0; k < K; ++k) {
+    // halves g + k, g + k + 1 and V(k) landed; every warp is past block k - 1
+    cp_async_wait<0>();
+    __syncthreads();
+    if (k + 2 <= K) q2_load_half<NJ>(Zw, Z, ldz, n, ncols, c0, g + k + 2);
+    load_vt(k);
+    cp_async_commit();
+    const int hb = (int)((g + k) % 3);  // ring slot of the window's top half
+    const int base_lo = hb * 64, base_hi = ((hb + 1) % 3) * 64 - 64;
+    auto prow = [&](int r) { return (r < 64 ? base_lo : base_hi) + r; };
+
+    // W = V^T Zwin (the warp's rows t = 8 warp + gq), see q2_step_a
+    {
+      const double* zlo = Zw + (jb + gq) * Q2_LDC + base_lo + tq;
+      const double* zhi = Zw + (jb + gq) * Q2_LDC + base_hi + tq;
+      const double* vrow = Vc + (8 * warp + gq) * Q2_LDV + 8 + tq - gq - 1;
+      double* wrow = Ws + (8 * warp + gq) * S::LDW + jb + 2 * tq;
+      switch (warp) {
+        case 0: q2_step_a<NH, 0>(zlo, zhi, vrow, wrow); break;
+        case 1: q2_step_a<NH, 1>(zlo, zhi, vrow, wrow); break;
+        case 2: q2_step_a<NH, 2>(zlo, zhi, vrow, wrow); break;
+        case 3: q2_step_a<NH, 3>(zlo, zhi, vrow, wrow); break;
+        case 4: q2_step_a<NH, 4>(zlo, zhi, vrow, wrow); break;
+        case 5: q2_step_a<NH, 5>(zlo, zhi, vrow, wrow); break;
+        case 6: q2_step_a<NH, 6>(zlo, zhi, vrow, wrow); break;
+        default: q2_step_a<NH, 7>(zlo, zhi, vrow, wrow); break;
+      }
+    }
+    cp_async_wait<0>();  // VT(k) (and half k + 2)
+    __syncthreads();     // Ws complete; Vc free
+    load_v(k + 1);
+    cp_async_commit();
+
+    // Zwin -= VT W for row fragments a0 = warp (top half: written straight to HBM) and
+    // a1 = 15 - warp (bottom half: back to the ring), see q2_step_c
+    {
+      const int pr0 = base_lo + 8 * warp + gq, pr1 = base_hi + 8 * (15 - warp) + gq;
+      double* z0 = Zw + (jb + 2 * tq) * Q2_LDC + pr0;
+      double* z1 = Zw + (jb + 2 * tq) * Q2_LDC + pr1;
+      const double* arow0 = VTs + (8 * warp + gq) * Q2_LDT + tq;
+      const double* arow1 = VTs + (8 * (15 - warp) + gq) * Q2_LDT + tq;
+      const double* bcol = Ws + tq * S::LDW + jb + gq;
+      const int64_t row0 = B2 * (g + k) + 8 * warp + gq;
+      double* zg = row0 < n ? Z + row0 + (c0 + jb + 2 * tq) * ldz : nullptr;
+      const int64_t cl = ncols - c0 - jb - 2 * tq;  // columns left from this thread's first
+      switch (warp) {
+        case 0: q2_step_c<NH, S::LDW, 0>(z0, z1, arow0, arow1, bcol, zg, ldz, cl); break;
+        case 1: q2_step_c<NH, S::LDW, 1>(z0, z1, arow0, arow1, bcol, zg, ldz, cl); break;
+        case 2: q2_step_c<NH, S::LDW, 2>(z0, z1, arow0, arow1, bcol, zg, ldz, cl); break;
+        case 3: q2_step_c<NH, S::LDW, 3>(z0, z1, arow0, arow1, bcol, zg, ldz, cl); break;
+        case 4: q2_step_c<NH, S::LDW, 4>(z0, z1, arow0, arow1, bcol, zg, ldz, cl); break;
+        case 5: q2_step_c<NH, S::LDW, 5>(z0, z1, arow0, arow1, bcol, zg, ldz, cl); break;
+        case 6: q2_step_c<NH, S::LDW, 6>(z0, z1, arow0, arow1, bcol, zg, ldz, cl); break;
+        default: q2_step_c<NH, S::LDW, 7>(z0, z1, arow0, arow1, bcol, zg, ldz, cl); break;
+      }
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  {  // the last window's bottom half
+    const int64_t hg = g + K;
+    const int slot = (int)(hg % 3);
+    for (int e = tid; e < 64 * S::WC; e += blockDim.x) {
+      const int i = e & 63, c = e >> 6;
+      const int64_t row = 64 * hg + i, col = c0 + c;
+      if (row < n && col < ncols) Z[row + col * ldz] = Zw[c * Q2_LDC + slot * 64 + i];
+    }
+  }
+}
+template <int NJ>
+static void q2_strip_launch(cudaStream_t st, int64_t n, int64_t ncols, int64_t g, int64_t K,
+                            const double* V2, const int64_t* toff, const double* VT, double* Z,
+                            int64_t ldz) {
+  using S = Q2Strip<NJ>;
+  static bool attr = false;
+  if (!attr) {
+    EM_CK(cudaFuncSetAttribute(q2_strip_kernel<NJ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)S::SMEM));
+    attr = true;
+  }
+  const unsigned grid = (unsigned)((ncols + S::WC - 1) / S::WC);
+  q2_strip_kernel<NJ><<<grid, 512, S::SMEM, st>>>(n, ncols, g, K, V2, toff, VT, Z, ldz);
+  EM_LAUNCHED();
+}
+
+// Z <- Q2 Z over all sweep groups (last group first). T2 holds the blocks' T factors in
+// the order groups descending, positions ascending.
+static void q2_apply_strips(cudaStream_t st, int64_t n, int64_t ncols, int64_t ngroups,
+                            const double* V2, const int64_t* toff, const double* T2, double* Z,
+                            int64_t ldz) {
+  // strip width (columns): fewest waves of one-CTA-per-SM strips, per-block overhead
+  // counted as ~1.5 column fragments
+  const int64_t sms = num_sms();
+  int nj = 6;
+  double best = 1e300;
+  for (int c = 6; c >= 4; c -= 2) {
+    const int64_t strips = (ncols + 8 * c - 1) / (8 * c);
+    const double cost = (double)((strips + sms - 1) / sms) * (c + 1.5);
+    if (cost < best) best = cost, nj = c;
+  }
+  const int64_t kmax = ntasks(n, 0);
+  DBuf VTg((size_t)imax64(kmax, 1) * VR * B2, st);
+  int64_t off = 0;
+  for (int64_t g = ngroups - 1; g >= 0; --g) {
+    const int64_t K = ntasks(n, g * B2);
+    if (K <= 0) continue;
+    q2_vt_kernel<<<(unsigned)K, 256, 0, st>>>(n, g, V2, toff, T2 + off * B2 * B2, VTg.p);
+    EM_LAUNCHED();
+    if (nj == 6)
+      q2_strip_launch<6>(st, n, ncols, g, K, V2, toff, VTg.p, Z, ldz);
+    else
+      q2_strip_launch<4>(st, n, ncols, g, K, V2, toff, VTg.p, Z, ldz);
+    off += K;
+  }
+}
+
 // ---- driver -------------------------------------------------------------------------
 void syev_two_stage(cudaStream_t st, int64_t n, double* A, int64_t lda, double* w, double* Z,
                     int64_t ldz) {
@@ -614,6 +924,10 @@ void syev_two_stage(cudaStream_t st, int64_t n, double* A, int64_t lda, double* 
                                  (int)smt));
       q2_tfactor_kernel<<<(unsigned)nblk, 256, smt, st>>>(n, dblk.p, V2.p, TAU2.p, dtoff.p, T2.p);
       EM_LAUNCHED();
+      if (g_q2_mode == 0) {
+        q2_apply_strips(st, n, n, ngroups, V2.p, dtoff.p, T2.p, Z, ldz);
+        EM_CK(cudaStreamSynchronize(st));  // dblk lifetime
+      } else {
       EM_CK(cudaFuncSetAttribute(q2_buildv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)(VR * B2 * sizeof(double))));
       // wavefront lists (chunks of at most QCH blocks)
@@ -670,6 +984,7 @@ void syev_two_stage(cudaStream_t st, int64_t n, double* A, int64_t lda, double* 
         EM_CK(gemm_grouped(st, false, false, dargs.p + np + o, (int)cnt, tiles_n));
       }
       EM_CK(cudaStreamSynchronize(st));  // host argument arrays / device lists lifetime
+      }
     }
     // Q1 (stage-1 reflectors, vectors start b rows below their column)
     Stage sq1(st, ST_Q1);
