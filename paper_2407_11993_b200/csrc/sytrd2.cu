@@ -21,6 +21,7 @@
 //
 // Replaces the reference's cyclic Jacobi (_kernels.py:82-141) for large n.
 #include <algorithm>
+#include <queue>
 #include <vector>
 
 #include "common.cuh"
@@ -687,13 +688,11 @@ EM_DEVINL void q2_step_c(double* z0, double* z1, const double* arow0, const doub
 }
 
 template <int NJ>
-__global__ void __launch_bounds__(512, 1) q2_strip_kernel(int64_t n, int64_t ncols, int64_t g,
-                                                          int64_t K, const double* __restrict__ V2,
-                                                          const int64_t* __restrict__ toff,
-                                                          const double* __restrict__ VT,
-                                                          double* __restrict__ Z, int64_t ldz) {
+EM_DEVINL void q2_strip_body(int64_t n, int64_t ncols, int64_t g, int64_t K,
+                             const double* __restrict__ V2, const int64_t* __restrict__ toff,
+                             const double* __restrict__ VT, double* __restrict__ Z, int64_t ldz,
+                             int64_t c0, double* sm) {
   using S = Q2Strip<NJ>;
-  extern __shared__ double sm[];
   double* Zw = sm;
   double* Ws = sm + S::OFF_W;
   double* Vc = sm + S::OFF_V;
@@ -704,10 +703,12 @@ __global__ void __launch_bounds__(512, 1) q2_strip_kernel(int64_t n, int64_t nco
   // fragments (NH of them) the warp works on
   static_assert(NJ % 2 == 0, "two column halves");
   constexpr int NH = NJ / 2;
-  const int tid = threadIdx.x, warp = (tid >> 5) & 7, lane = tid & 31, gq = lane >> 2,
-            tq = lane & 3;
+  // Row roles are paired so that each scheduler (warps w, w + 4, w + 8, w + 12) gets
+  // roles r and 7 - r: step C costs 18 + 2 r k-step units for role r, so every scheduler
+  // carries the same 100 units.
+  const int tid = threadIdx.x, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
+  const int warp = ((tid >> 7) & 1) ? 7 - ((tid >> 5) & 3) : ((tid >> 5) & 3);
   const int jb = 8 * NH * (tid >> 8);  // first column of the warp's half
-  const int64_t c0 = (int64_t)blockIdx.x * S::WC;
   if (tid < B2) {
     const int64_t s = g * B2 + tid;
     s_toff[tid] = s < n - 1 ? toff[s] : 0;
@@ -808,20 +809,35 @@ __global__ void __launch_bounds__(512, 1) q2_strip_kernel(int64_t n, int64_t nco
     }
   }
 }
-template <int NJ>
-static void q2_strip_launch(cudaStream_t st, int64_t n, int64_t ncols, int64_t g, int64_t K,
-                            const double* V2, const int64_t* toff, const double* VT, double* Z,
-                            int64_t ldz) {
-  using S = Q2Strip<NJ>;
-  static bool attr = false;
-  if (!attr) {
-    EM_CK(cudaFuncSetAttribute(q2_strip_kernel<NJ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)S::SMEM));
-    attr = true;
+// Strips [0, n6) are 48 columns wide, the rest 32: CTAs are dispatched in index order,
+// so the narrow strips fill the last wave behind the wide ones.
+__global__ void __launch_bounds__(512, 1) q2_strip_kernel(int64_t n, int64_t ncols, int64_t g,
+                                                          int64_t K, const double* __restrict__ V2,
+                                                          const int64_t* __restrict__ toff,
+                                                          const double* __restrict__ VT,
+                                                          double* __restrict__ Z, int64_t ldz,
+                                                          int64_t n6) {
+  extern __shared__ double sm[];
+  const int64_t b = blockIdx.x;
+  if (b < n6)
+    q2_strip_body<6>(n, ncols, g, K, V2, toff, VT, Z, ldz, 48 * b, sm);
+  else
+    q2_strip_body<4>(n, ncols, g, K, V2, toff, VT, Z, ldz, 48 * n6 + 32 * (b - n6), sm);
+}
+
+// Makespan (in column-fragment units, ~1.5 units of per-block overhead per strip) of n6
+// wide and n4 narrow strips dispatched in order onto `sms` SMs, one CTA per SM.
+static double q2_makespan(int64_t n6, int64_t n4, int64_t sms) {
+  std::priority_queue<double, std::vector<double>, std::greater<double>> q;
+  for (int64_t i = 0; i < sms; ++i) q.push(0.0);
+  double end = 0.0;
+  for (int64_t i = 0; i < n6 + n4; ++i) {
+    const double t = q.top() + (i < n6 ? 7.5 : 5.5);
+    q.pop();
+    q.push(t);
+    end = t > end ? t : end;
   }
-  const unsigned grid = (unsigned)((ncols + S::WC - 1) / S::WC);
-  q2_strip_kernel<NJ><<<grid, 512, S::SMEM, st>>>(n, ncols, g, K, V2, toff, VT, Z, ldz);
-  EM_LAUNCHED();
+  return end;
 }
 
 // Z <- Q2 Z over all sweep groups (last group first). T2 holds the blocks' T factors in
@@ -829,16 +845,18 @@ static void q2_strip_launch(cudaStream_t st, int64_t n, int64_t ncols, int64_t g
 static void q2_apply_strips(cudaStream_t st, int64_t n, int64_t ncols, int64_t ngroups,
                             const double* V2, const int64_t* toff, const double* T2, double* Z,
                             int64_t ldz) {
-  // strip width (columns): fewest waves of one-CTA-per-SM strips, per-block overhead
-  // counted as ~1.5 column fragments
   const int64_t sms = num_sms();
-  int nj = 6;
-  double best = 1e300;
-  for (int c = 6; c >= 4; c -= 2) {
-    const int64_t strips = (ncols + 8 * c - 1) / (8 * c);
-    const double cost = (double)((strips + sms - 1) / sms) * (c + 1.5);
-    if (cost < best) best = cost, nj = c;
+  const int64_t max6 = (ncols + 47) / 48;
+  int64_t n6 = max6, n4 = 0;
+  double best = q2_makespan(max6, 0, sms);
+  const int64_t step = imax64(1, max6 / 256);
+  for (int64_t a = 0; a < max6; a += step) {
+    const int64_t b = (ncols - 48 * a + 31) / 32;
+    const double t = q2_makespan(a, b, sms);
+    if (t < best) best = t, n6 = a, n4 = b;
   }
+  EM_CK(cudaFuncSetAttribute(q2_strip_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)Q2Strip<6>::SMEM));
   const int64_t kmax = ntasks(n, 0);
   DBuf VTg((size_t)imax64(kmax, 1) * VR * B2, st);
   int64_t off = 0;
@@ -847,10 +865,9 @@ static void q2_apply_strips(cudaStream_t st, int64_t n, int64_t ncols, int64_t n
     if (K <= 0) continue;
     q2_vt_kernel<<<(unsigned)K, 256, 0, st>>>(n, g, V2, toff, T2 + off * B2 * B2, VTg.p);
     EM_LAUNCHED();
-    if (nj == 6)
-      q2_strip_launch<6>(st, n, ncols, g, K, V2, toff, VTg.p, Z, ldz);
-    else
-      q2_strip_launch<4>(st, n, ncols, g, K, V2, toff, VTg.p, Z, ldz);
+    q2_strip_kernel<<<(unsigned)(n6 + n4), 512, Q2Strip<6>::SMEM, st>>>(
+        n, ncols, g, K, V2, toff, VTg.p, Z, ldz, n6);
+    EM_LAUNCHED();
     off += K;
   }
 }

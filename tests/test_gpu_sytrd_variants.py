@@ -77,12 +77,13 @@ def test_sytrd_larger_orders(n):
 
 
 @pytest.mark.parametrize("n,lda", [(129, 129), (300, 301), (1000, 1000), (2049, 2051),
-                                   (6000, 6000)])
+                                   (6000, 6000), (9800, 9800)])
 def test_two_stage_q2_forms_agree(n, lda):
     """Two-stage reduction: the column-strip Q2 back-transform (debug key 97 = 0, the
     default) and the wavefront grouped-GEMM form (97 = 1) give the same eigenvectors up
     to rounding, and both satisfy the eigen-equation; orders with a partial last sweep
-    group and strip, and an odd leading dimension."""
+    group and strip, and an odd leading dimension; n = 9800 has more strips than SMs, so
+    the launch mixes 48- and 32-column strips."""
     from paper_2407_11993_b200 import _native as nat
     lib, ctx = nat.load_library(), nat.context()
     rng = np.random.default_rng(n)
