@@ -52,8 +52,9 @@ const char* em_last_error(const em_ctx* ctx);
 int64_t em_launch_count(const em_ctx* ctx);
 int em_synchronize(em_ctx* ctx);
 /* Tuning knobs. EM_CFG_TWO_STAGE_MIN: smallest n that uses the two-stage
- * (dense -> band -> tridiagonal) reduction in em_syev/em_sygv (default INT64_MAX:
- * one-stage Householder everywhere). */
+ * (dense -> band -> tridiagonal) reduction in em_syev/em_sygv when its extra storage
+ * (~1.6 n^2 doubles) is free on the device (default 40000; below it one-stage
+ * Householder). */
 #define EM_CFG_TWO_STAGE_MIN 1
 /* EM_CFG_BAND_OFF: 1 = always factor R densely (default 0: a banded R, lower bandwidth
  * b with 4 (b + 128) <= n, takes the banded Cholesky and banded solves). */

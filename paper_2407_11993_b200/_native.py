@@ -165,8 +165,12 @@ def stage_times() -> dict:
 EM_CFG_TWO_STAGE_MIN = 1
 
 
+TWO_STAGE_MIN_DEFAULT = 40000  # the library's default (csrc/sygv.cu g_two_stage_min)
+
+
 def set_two_stage_min(n: int) -> None:
-    """Smallest order that uses the two-stage tridiagonalisation (default: never)."""
+    """Smallest order that uses the two-stage tridiagonalisation (library default
+    TWO_STAGE_MIN_DEFAULT, and only when its extra storage fits on the device)."""
     check(load_library().em_config(context(), EM_CFG_TWO_STAGE_MIN, int(n)), "em_config")
 
 

@@ -149,6 +149,13 @@ int em_config(em_ctx* ctx, int key, int64_t value) {
       em::g_gemm_cfg = value;
       return EM_OK;
     }
+    if (key == 99) {  // debug: release the device pool's cached memory down to `value` bytes
+      EM_CK(cudaStreamSynchronize(ctx->stream));
+      cudaMemPool_t pool;
+      EM_CK(cudaDeviceGetDefaultMemPool(&pool, ctx->device));
+      EM_CK(cudaMemPoolTrimTo(pool, (size_t)value));
+      return EM_OK;
+    }
     if (key == 97) {  // debug: Q2 back-transform (0 column strips, 1 wavefront GEMMs)
       em::g_q2_mode = (int)value;
       return EM_OK;

@@ -14,16 +14,38 @@
 
 namespace em {
 
-// em_config(EM_CFG_TWO_STAGE_MIN). Off by default until the two-stage path beats the
-// one-stage one end to end; tests force it on.
-int64_t g_two_stage_min = INT64_MAX;
+// em_config(EM_CFG_TWO_STAGE_MIN): smallest order that takes the two-stage reduction.
+// Measured on one B200: one-stage wins at n = 16,384 (sytrd + ormtr 1.6 s
+// against 2.3 s), two-stage at n = 50,000 (49.3 s against 50.7 s per C3 step before the
+// lower-triangle sy2sb update). Tests force either path.
+int64_t g_two_stage_min = 40000;
+// The two-stage path keeps the stage-2 reflectors (n^2 / 2 doubles) next to the compact-WY
+// blocks of the stage-1 back-transform (~n^2 doubles): taken only when that fits.
+static bool two_stage_fits(int64_t n) {
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return false;
+  // plus what the stream-ordered pool holds reserved but unused (em_init keeps freed
+  // workspace cached between calls)
+  int dev = 0;
+  cudaMemPool_t pool;
+  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t reserved = 0, used = 0;
+    if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) ==
+            cudaSuccess &&
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess &&
+        reserved > used)
+      free_b += (size_t)(reserved - used);
+  }
+  const double need = 1.6 * (double)n * (double)n * sizeof(double) + (1ull << 30);
+  return (double)free_b >= need;
+}
 // em_config(EM_CFG_BAND_OFF): 1 forces the dense R path (tests compare both)
 int g_band_off = 0;
 
 void syev_ascending(cudaStream_t st, int64_t n, double* A, int64_t lda, double* w, double* Z,
                     int64_t ldz) {
   if (n <= 0) return;
-  if (n >= g_two_stage_min && n > 2 * kBand) {
+  if (n >= g_two_stage_min && n > 2 * kBand && two_stage_fits(n)) {
     syev_two_stage(st, n, A, lda, w, Z, ldz);
     return;
   }

@@ -206,6 +206,7 @@ static void coop_launch(const void* fn, unsigned grid, unsigned block, void** ar
 void sy2sb(cudaStream_t st, int64_t n, double* A, int64_t lda, double* tau1, double* AB,
            int64_t ldab) {
   const int b = B2;
+  constexpr int64_t SB = 2048;  // column block of the symmetric product (band above: SB - 1)
   const int sms = num_sms();
   DBuf VW((size_t)n * 2 * b, st), WV((size_t)n * 2 * b, st), VT((size_t)n * b, st);
   DBuf Gm((size_t)b * b, st), T((size_t)b * b, st), Y((size_t)b * b, st), M((size_t)b * b, st);
@@ -243,14 +244,25 @@ void sy2sb(cudaStream_t st, int64_t n, double* A, int64_t lda, double* tau1, dou
     EM_LAUNCHED();
     // X = A22 (V T);  M = T^T (V^T X);  W = X - V M / 2
     EM_CK(gemm(st, false, false, m, p, p, 1.0, V, n, T.p, p, 0.0, VT.p, n));
-    EM_CK(gemm(st, false, false, m, p, m, 1.0, A22, lda, VT.p, n, 0.0, X, n));
+    // X = A22 VT from the lower triangle plus the band of width SB above the diagonal
+    // (column blocks J: X[J:] += A22[J:, J] VT[J], X[J] += A22[J+SB:, J]^T VT[J+SB:])
+    for (int64_t j = 0; j < m; j += SB) {
+      const int64_t w = imin64(SB, m - j);
+      EM_CK(gemm(st, false, false, m - j, p, w, 1.0, A22 + j + j * lda, lda, VT.p + j, n,
+                 j == 0 ? 0.0 : 1.0, X + j, n));
+      if (j + w < m)
+        EM_CK(gemm(st, true, false, w, p, m - j - w, 1.0, A22 + (j + w) + j * lda, lda,
+                   VT.p + j + w, n, 1.0, X + j, n));
+    }
     EM_CK(gemm(st, true, false, p, p, m, 1.0, V, n, X, n, 0.0, Y.p, p));
     EM_CK(gemm(st, true, false, p, p, p, 1.0, T.p, p, Y.p, p, 0.0, M.p, p));
     EM_CK(gemm(st, false, false, m, p, p, -0.5, V, n, M.p, p, 1.0, X, n));
-    // A22 -= [V W] [W V]^T  (both triangles: A22 stays fully symmetric for the next X)
+    // A22 -= [V W] [W V]^T on the lower triangle and the band c - r < SB above it (what
+    // the next panel's blocked product reads; 1.5x fewer flops than both triangles)
     copy_matrix(st, false, m, p, X, n, WV.p, n);
     copy_matrix(st, false, m, p, V, n, WV.p + (size_t)p * n, n);
-    EM_CK(gemm(st, false, true, m, m, 2 * p, -1.0, VW.p, n, WV.p, n, 1.0, A22, lda));
+    EM_CK(gemm(st, false, true, m, m, 2 * p, -1.0, VW.p, n, WV.p, n, 1.0, A22, lda, true,
+               SB - 1));
   }
   band_extract_kernel<<<(unsigned)n, 128, 0, st>>>(n, b, A, lda, AB, ldab);
   EM_LAUNCHED();
@@ -880,7 +892,7 @@ void syev_two_stage(cudaStream_t st, int64_t n, double* A, int64_t lda, double* 
   DBuf tau1(n, st), AB((size_t)ldab * n, st);
   {
     Stage s(st, ST_SYTRD);
-    mirror_lower(st, n, A, lda);  // stage 1 works on the full symmetric matrix
+    mirror_lower(st, n, A, lda);  // stage 1 reads the lower triangle and a band above it
     Stage s1(st, ST_SY2SB);
     sy2sb(st, n, A, lda, tau1.p, AB.p, ldab);
   }

@@ -27,10 +27,17 @@ def test_lazy_vt_r_matches_eager():
     np.testing.assert_allclose(b.vt_r, a.vt_r, rtol=0, atol=1e-13 * np.abs(a.vt_r).max())
 
 
-def test_eigensolve_beyond_int32_squared():
+@pytest.mark.parametrize("two_stage", [True, False])
+def test_eigensolve_beyond_int32_squared(two_stage):
+    """Both tridiagonalisations at N = 46,400: the two-stage path (the default from
+    N = 40,000 when its storage fits) and the one-stage path."""
     import torch
     from paper_2407_11993_b200 import _native as nat
     from paper_2407_11993_b200.synth import device_plate_model
+    # the previous case's N x N tensors sit in torch's cache and the eigensolver's
+    # workspace in the library's pool (em_config debug key 99 trims it)
+    torch.cuda.empty_cache()
+    nat.check(nat.load_library().em_config(nat.context(), 99, 0))
     free = torch.cuda.mem_get_info()[0]
     m = device_plate_model(116, 100, 4, n_ports=0, n_sources=0, n_obs=1)
     L, R = m["l_i"], m["r_i"]
@@ -42,10 +49,19 @@ def test_eigensolve_beyond_int32_squared():
     tau, ln, rn = nat.empty(n), nat.empty(n), nat.empty(n)
     V = nat.empty(n, n)
     piv, which = ctypes.c_int64(-1), ctypes.c_int(-1)
-    nat.check(lib.em_sygv(ctx, n, nat.ptr(L), n, nat.ptr(R), n, nat.ptr(tau), nat.ptr(V), n,
-                          nat.ptr(ln), nat.ptr(rn), None, n, ctypes.byref(piv),
-                          ctypes.byref(which)), "em_sygv")
-    torch.cuda.synchronize()
+    nat.set_two_stage_min(0 if two_stage else 2**62)
+    try:
+        nat.profile(2)
+        nat.check(lib.em_sygv(ctx, n, nat.ptr(L), n, nat.ptr(R), n, nat.ptr(tau), nat.ptr(V),
+                              n, nat.ptr(ln), nat.ptr(rn), None, n, ctypes.byref(piv),
+                              ctypes.byref(which)), "em_sygv")
+        torch.cuda.synchronize()
+        stages = nat.stage_times()
+        nat.profile(0)
+    finally:
+        nat.set_two_stage_min(nat.TWO_STAGE_MIN_DEFAULT)
+    # the requested path ran (stage 2 of the two-stage reduction is timed as sb2st)
+    assert ("sb2st" in stages) == two_stage, sorted(stages)
     # column-major V: row j of the torch tensor is mode j
     Vt = V
     assert bool(torch.all(tau[1:] <= tau[:-1]))

@@ -199,7 +199,7 @@ def two_stage():
     from paper_2407_11993_b200 import _native as nat
     nat.set_two_stage_min(0)
     yield
-    nat.set_two_stage_min(2**62)
+    nat.set_two_stage_min(nat.TWO_STAGE_MIN_DEFAULT)
 
 
 @pytest.mark.parametrize("n", [129, 200, 257, 700, 1500])

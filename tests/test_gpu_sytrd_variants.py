@@ -97,7 +97,7 @@ def test_two_stage_q2_forms_agree(n, lda):
             out[mode] = _syev(a, lda=lda)
     finally:
         nat.check(lib.em_config(ctx, 97, 0))
-        nat.set_two_stage_min(2**62)
+        nat.set_two_stage_min(nat.TWO_STAGE_MIN_DEFAULT)
     ref = np.sort(np.linalg.eigvalsh(a))[::-1]
     scale = np.abs(ref).max()
     for w, u in out.values():
