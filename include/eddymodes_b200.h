@@ -64,8 +64,9 @@ int em_synchronize(em_ctx* ctx);
  * 126 MB L2 by every later column instead of HBM); every other tile is loaded
  * evict_first. Default 32; 0 = evict_first everywhere; < 0 = no cache hint. */
 #define EM_CFG_SYMV_L2_KEEP_MB 3
-/* Keys 95-98 are debug switches for A/B measurements and the tests (GEMM tile
- * configuration, tridiagonalisation code paths); see capi.cu. */
+/* Keys 96-99 are debug switches for A/B measurements and the tests (96 GEMM tile
+ * configuration, 97 Q2 back-transform form, 98 tridiagonalisation code paths, 99 trim
+ * the device memory pool to `value` bytes); see capi.cu. */
 int em_config(em_ctx* ctx, int key, int64_t value);
 /* Stage timers (CUDA events on the context stream). em_profile(ctx, 1) clears and
  * enables them; em_stage_times fills per-stage milliseconds / event-pair counts
