@@ -64,6 +64,11 @@ int em_synchronize(em_ctx* ctx);
  * 126 MB L2 by every later column instead of HBM); every other tile is loaded
  * evict_first. Default 32; 0 = evict_first everywhere; < 0 = no cache hint. */
 #define EM_CFG_SYMV_L2_KEEP_MB 3
+/* EM_CFG_LN_DENSE: 1 = em_sygv forms l_n = diag(V^T L V) with the N^3 product as the
+ * reference does (modal.py:79); 0 (default) = l_n = tau_n r_n, the generalized
+ * eigen-identity V^T L V = diag(tau) V^T R V (equal to ~1e-13 relative; r_n is always
+ * diag(V^T R V) from R itself). */
+#define EM_CFG_LN_DENSE 4
 /* Keys 96-99 are debug switches for A/B measurements and the tests (96 GEMM tile
  * configuration, 97 Q2 back-transform form, 98 tridiagonalisation code paths, 99 trim
  * the device memory pool to `value` bytes); see capi.cu. */

@@ -230,3 +230,50 @@ void orc_lu_solve(const double* a, const int64_t* piv, double* b, int64_t n) {
     b[i] = s / A_(i, i);
   }
 }
+
+/* run_transient's td2 loop (transient.py:293-306) over Td2Stepper.forcing
+ * (transient.py:147-155) and td2_step_kernel (_kernels.py:213-222), driven by a sample
+ * table tab ((steps+1) x (n_p+n_s), row k = [i_d(t_k) | i0(t_k)]). p_r, p_ltr: n x n_p,
+ * p_m: n x n_s row-major (= V^T R_D, V^T L_D + dt theta V^T R_D, V^T M0). Observables
+ * obs[cap][o] = (C V q)_o with cv (n_obs x n row-major) after every stride-th step;
+ * q (n) in/out; f is scratch of length n. The forcing is accumulated in the reference's
+ * order: f = 0; f -= dt (P_r i_d); f -= P_ltr di_d; f -= P_m di0 (numpy matvec sums in
+ * channel order, exact for one channel). */
+void orc_td2_run(double* q, const double* r_n, const double* c_n, double dt, const double* p_r,
+                 const double* p_ltr, const double* p_m, int64_t n, int64_t n_p, int64_t n_s,
+                 const double* tab, int64_t steps, const double* cv, int64_t n_obs,
+                 int64_t stride, double* obs, double* f) {
+  const int64_t nc = n_p + n_s;
+  int64_t cap = 0;
+  for (int64_t k = 0; k < steps; ++k) {
+    const double* t0 = tab + k * nc;
+    const double* t1 = t0 + nc;
+    for (int64_t i = 0; i < n; ++i) {
+      double fi = 0.0;
+      if (n_p) {
+        double s = 0.0;
+        for (int64_t p = 0; p < n_p; ++p) s += p_r[i * n_p + p] * t0[p];
+        fi -= dt * s;
+        s = 0.0;
+        for (int64_t p = 0; p < n_p; ++p) s += p_ltr[i * n_p + p] * (t1[p] - t0[p]);
+        fi -= s;
+      }
+      if (n_s) {
+        double s = 0.0;
+        for (int64_t j = 0; j < n_s; ++j) s += p_m[i * n_s + j] * (t1[n_p + j] - t0[n_p + j]);
+        fi -= s;
+      }
+      f[i] = fi;
+    }
+    orc_td2_step(q, r_n, c_n, dt, f, n);
+    if ((k + 1) % stride == 0) {
+      if (obs)
+        for (int64_t o = 0; o < n_obs; ++o) {
+          double s = 0.0;
+          for (int64_t i = 0; i < n; ++i) s += cv[o * n + i] * q[i];
+          obs[cap * n_obs + o] = s;
+        }
+      ++cap;
+    }
+  }
+}

@@ -72,6 +72,8 @@ def lib():
         _lib.orc_jacobi_rotations.restype = i64
         _lib.orc_td1_step.argtypes = [d, d, d, ctypes.c_double, d, d, d, d, i64]
         _lib.orc_td2_step.argtypes = [d, d, d, ctypes.c_double, d, i64]
+        _lib.orc_td2_run.argtypes = [d, d, d, ctypes.c_double, d, d, d, i64, i64, i64, d, i64,
+                                     d, i64, i64, d, d]
         _lib.orc_lu_factor.argtypes = [d, ctypes.c_void_p, i64]
         _lib.orc_lu_factor.restype = i64
         _lib.orc_lu_solve.argtypes = [d, ctypes.c_void_p, d, i64]
@@ -270,6 +272,36 @@ class Td2:
         f = np.ascontiguousarray(self.forcing(i_d, d_id, d_i0))
         lib().orc_td2_step(_p(q), _p(self._rn), _p(self._c), self.dt, _p(f), q.shape[0])
         return q
+
+
+def td2_run_table(l_n, r_n, p_r, p_l, p_m, dt, theta, tab, steps, cv=None, stride=1, q0=None):
+    """run_transient's td2 loop (transient.py:293-306) in C (orc_td2_run) for a modal
+    model given directly by l_n, r_n and the drive projections P = V^T [R_D | L_D | M0]
+    (n x n_p, n x n_p, n x n_s), as Td2Stepper.__init__ forms them (transient.py:122-145).
+    Returns (q after the last step, observables (steps // stride, n_obs) = (C V) q or None)."""
+    n = l_n.shape[0]
+    den = l_n + float(dt) * float(theta) * r_n
+    c = np.ascontiguousarray(np.sqrt(den))
+    rn = np.ascontiguousarray(r_n, dtype=float)
+    n_p, n_s = p_r.shape[1], p_m.shape[1]
+    pr = np.ascontiguousarray(p_r, dtype=float).reshape(n, n_p)
+    pltr = np.ascontiguousarray(p_l + float(dt) * float(theta) * p_r, dtype=float).reshape(n, n_p)
+    pm = np.ascontiguousarray(p_m, dtype=float).reshape(n, n_s)
+    tab = np.ascontiguousarray(tab, dtype=float)
+    q = np.zeros(n) if q0 is None else np.ascontiguousarray(q0, dtype=float).copy()
+    n_caps = steps // stride
+    obs = None
+    if cv is not None:
+        cv = np.ascontiguousarray(cv, dtype=float)
+        obs = np.zeros((n_caps, cv.shape[0]))
+    f = np.empty(n)
+    z = np.zeros(1)
+    lib().orc_td2_run(_p(q), _p(rn), _p(c), float(dt), _p(pr) if n_p else _p(z),
+                      _p(pltr) if n_p else _p(z), _p(pm) if n_s else _p(z), n, n_p, n_s,
+                      _p(tab), int(steps), _p(cv) if cv is not None else _p(z),
+                      cv.shape[0] if cv is not None else 0, int(stride),
+                      _p(obs) if obs is not None else None, _p(f))
+    return q, obs
 
 
 def run(stepper, n: int, i_d_tab: np.ndarray, i0_tab: np.ndarray, modal: Basis | None,

@@ -17,6 +17,7 @@ namespace em {
 extern int64_t g_two_stage_min;
 extern int g_sytrd_dbg;
 extern int g_band_off;
+extern int g_ln_dense;
 extern int g_q2_mode;
 extern int g_symv_align_off;
 extern int64_t g_symv_keep_mb;
@@ -139,6 +140,10 @@ int em_config(em_ctx* ctx, int key, int64_t value) {
     }
     if (key == EM_CFG_BAND_OFF) {
       em::g_band_off = value ? 1 : 0;
+      return EM_OK;
+    }
+    if (key == EM_CFG_LN_DENSE) {
+      em::g_ln_dense = value ? 1 : 0;
       return EM_OK;
     }
     if (key == EM_CFG_SYMV_L2_KEEP_MB) {

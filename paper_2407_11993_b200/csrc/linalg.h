@@ -37,6 +37,9 @@ bool csr_from_dense(cudaStream_t st, int64_t n, const double* A, int64_t lda, do
 void csr_mm(cudaStream_t st, const Csr& a, int64_t m, const double* B, int64_t ldb, double* C,
             int64_t ldc);
 void csr_to_dense(cudaStream_t st, const Csr& a, double* A, int64_t lda);
+// out[j] = V[:, j]^T A V[:, j], j < m (no product buffer)
+void csr_quadform(cudaStream_t st, const Csr& a, int64_t m, const double* V, int64_t ldv,
+                  double* out);
 void csr_spmv(cudaStream_t st, const Csr& a, double alpha, const double* x, double beta,
               double* y);
 // band.cu: banded Cholesky (128-wide block columns, kb blocks below the diagonal)

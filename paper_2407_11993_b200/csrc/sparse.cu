@@ -146,6 +146,39 @@ void csr_to_dense(cudaStream_t st, const Csr& a, double* A, int64_t lda) {
   EM_LAUNCHED();
 }
 
+// out[j] = v_j^T A v_j for the columns of V (r_n = diag(V^T R V), modal.py:80) without an
+// N x N product buffer: block j forms (A v_j)_i row by row from the CSR copy (L2-resident)
+// and reduces v_ij (A v_j)_i in a fixed order. V is read once: HBM-bound.
+__global__ void csr_quadform_kernel(int64_t n, const int64_t* __restrict__ rowptr,
+                                    const int* __restrict__ colidx, const double* __restrict__ val,
+                                    const double* __restrict__ V, int64_t ldv,
+                                    double* __restrict__ out) {
+  __shared__ double red[32];
+  const double* v = V + blockIdx.x * ldv;
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    double t = 0.0;
+    for (int64_t p = rowptr[i]; p < rowptr[i + 1]; ++p) t = fma(val[p], v[colidx[p]], t);
+    s = fma(v[i], t, s);
+  }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double t = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) out[blockIdx.x] = t;
+  }
+}
+
+void csr_quadform(cudaStream_t st, const Csr& a, int64_t m, const double* V, int64_t ldv,
+                  double* out) {
+  if (a.n <= 0 || m <= 0) return;
+  csr_quadform_kernel<<<(unsigned)m, 256, 0, st>>>(a.n, a.rowptr.p, a.colidx.p, a.val.p, V, ldv,
+                                                   out);
+  EM_LAUNCHED();
+}
+
 // C = A B using CSR when A (symmetric, n x n) has at most max_fill * n^2 nonzeros.
 // Returns false (and does nothing) when A is too dense.
 bool sym_sparse_mm(cudaStream_t st, int64_t n, const double* A, int64_t lda, int64_t m,

@@ -5,6 +5,7 @@ Run in the build container (where /root/reference exists); the resulting
 
     python tests/golden/make_golden.py kat plate_small plate_200 tubes fd   # seconds
     python tests/golden/make_golden.py c1                                # ~30 min (Jacobi at N=2000)
+    python tests/golden/make_golden.py c2                                # ~10 min (dsygvd at N=16384)
 
 The reference is copied to a writable temp dir first because its numba
 kernels use cache=True and would write into the (read-only) source tree.
@@ -172,6 +173,60 @@ def case_c1(em):
          input_sha_m0=np.array(sha(m["m0"])), **res)
 
 
+def case_c2(em):
+    """C2 (BASELINE configs[1]: N = 16,384, one port with a 5 us ramp, theta = 1 and 0.5,
+    dt = 5e-7, 10,000 steps, 32 observables). The reference's Jacobi is infeasible at this
+    N (~10 days), so the basis is the LAPACK dsygvd restatement of modal.py:46-81 (potrf +
+    sygst + syevd + trsm, then the reference's descending order, sign fix and l_n / r_n,
+    modal.py:74-80), which tests/test_oracle.py pins to the reference's Jacobi on every
+    smaller fixture. The stepping is the UNMODIFIED reference Td2Stepper
+    (transient.py:116-166 -> _kernels.td2_step_kernel) over that basis, driven by the
+    ramp sample table (run_transient's drive convention, transient.py:293-299);
+    observables y^k = (C V) q^k."""
+    import scipy.linalg as sl
+    from eddymodes.modal import ModalBasis
+    from eddymodes.transient import Td2Stepper
+    sys.path.insert(0, REPO)
+    from paper_2407_11993_b200.synth import drive_table, plate_model
+    m = plate_model(64, 64, 4, n_ports=1, n_sources=0, n_obs=32)
+    rm = _reduced(em, m["r_i"], m["l_i"], m["r_d"], m["l_d"], m["m0"], ("p0",), ())
+    lm, rmat = rm.l_i.full, rm.r_i.full
+    n = lm.shape[0]
+    t0 = time.perf_counter()
+    w, v = sl.eigh(lm, rmat, driver="gvd", lower=True)
+    order = np.argsort(-w, kind="stable")
+    w, v = w[order], np.ascontiguousarray(v[:, order])
+    idx = np.argmax(np.abs(v), axis=0)
+    signs = np.sign(v[idx, np.arange(n)])
+    signs[signs == 0] = 1.0
+    v *= signs[None, :]
+    l_n = np.einsum("ij,ij->j", v, lm @ v)
+    r_n = np.einsum("ij,ij->j", v, rmat @ v)
+    print(f"C2 dsygvd + l_n/r_n {time.perf_counter() - t0:.1f}s")
+    basis = ModalBasis(v=v, tau=w, l_n=l_n, r_n=r_n, vt_r=np.zeros((0, 0)))
+    steps, dt, keep = 10000, 5e-7, 5
+    i_d, i0 = drive_table("ramp5us", steps, dt, 1, 0)
+    cv = m["c"] @ v
+    out = dict(tau=w, l_n=l_n, r_n=r_n, v_lead=v[:, :4].copy(), keep_every=np.array(keep),
+               dt=np.array(dt), steps=np.array(steps), thetas=np.array([1.0, 0.5]),
+               input_sha_r=np.array(sha(rmat)), input_sha_l=np.array(sha(lm)),
+               input_sha_c=np.array(sha(m["c"])), input_sha_ld=np.array(sha(m["l_d"])),
+               input_sha_rd=np.array(sha(m["r_d"])))
+    for th in (1.0, 0.5):
+        st = Td2Stepper(rm, basis, dt, th)
+        q = np.zeros(n)
+        y = np.empty((steps // keep, cv.shape[0]))
+        t0 = time.perf_counter()
+        for k in range(steps):
+            st.step(q, i_d[k], i_d[k + 1] - i_d[k], i0[k + 1] - i0[k])
+            if (k + 1) % keep == 0:
+                y[(k + 1) // keep - 1] = cv @ q
+        print(f"  td2 theta={th}: {time.perf_counter() - t0:.1f}s")
+        out[f"td2_obs_theta{th}"] = y
+        out[f"q_final_theta{th}"] = q.copy()
+    save("c2", **out)
+
+
 def case_fd(em):
     """Frequency domain: the reference solve_tone on the plate_small
     and tube_small models at several tones, dft_phasor / extract_phasors KATs."""
@@ -247,6 +302,8 @@ def main(argv):
             case_tubes(em)
         elif case == "c1":
             case_c1(em)
+        elif case == "c2":
+            case_c2(em)
         elif case == "fd":
             case_fd(em)
         elif case == "cache":

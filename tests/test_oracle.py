@@ -121,3 +121,24 @@ def test_fd_solve_tone_and_dft_bitwise():
     x, dt = g["dft_x"], float(g["dft_dt"])
     for f, p in zip(g["dft_freqs"], g["dft_phasors"]):
         assert O.dft_phasor(x, dt, float(f)) == p
+
+
+def test_td2_run_table_is_the_reference_loop():
+    """orc_td2_run (the C run loop used by the C3 horizon test) reproduces the oracle's
+    Td2Stepper loop — itself bitwise equal to the reference — bit for bit."""
+    g = golden("plate_200")
+    basis = O.Basis(v=g["v"], tau=g["tau"], l_n=g["l_n"], r_n=g["r_n"], vt_r=None)
+    itab, i0tab = _tables(g)
+    steps = 300
+    for th in (0.5, 1.0, 0.0):
+        st = O.Td2(basis, g["r_d"], g["l_d"], g["m0"], float(g["dt"]), th)
+        q = np.zeros(200)
+        for k in range(steps):
+            st.step(q, itab[k], itab[k + 1] - itab[k], i0tab[k + 1] - i0tab[k])
+        tab = np.concatenate([itab, i0tab], axis=1)
+        vt = g["v"].T
+        q2, obs = O.td2_run_table(g["l_n"], g["r_n"], vt @ g["r_d"], vt @ g["l_d"],
+                                  vt @ g["m0"], float(g["dt"]), th, tab, steps,
+                                  cv=g["c"] @ g["v"], stride=7)
+        assert np.array_equal(q, q2)
+        assert obs.shape == (steps // 7, g["c"].shape[0])
