@@ -340,6 +340,24 @@ def load_peaks():
 
 
 # --------------------------------------------------------------------------- arms
+def workload_config(args, cfg, n, world):
+    """The `config` object of the JSON line (identical for both arms)."""
+    T = cfg["steps"]
+    n_rhs = (cfg["n_ports"] + cfg["n_sources"]) if cfg.get("sweep") else 1
+    return {"workload": f"{args.config}: N={n} plate {cfg['grid']}, eigensolve + "
+                        f"{T} TD2 steps x theta {list(cfg['thetas'])}"
+                        + (f" x {n_rhs} right-hand sides (excitation sweep)" if n_rhs > 1 else "")
+                        + f", {cfg['n_obs']} observables",
+            "n_rhs": n_rhs, "N": n, "T": T, "thetas": list(cfg["thetas"]),
+            "n_obs": cfg["n_obs"], "mode_steps_per_step": n * T * len(cfg["thetas"]) * n_rhs,
+            "l2": f"inputs larger than L2 (L, R {8 * n * n / 1e9:.1f} GB each)",
+            "parallelism": parallelism(args, world)}
+
+
+def parallelism(args, world):
+    return "single GPU" if world == 1 else f"replicas x{world}"
+
+
 def run_ours(args, cfg, rank, world, local_rank):
     import torch
     torch.cuda.set_device(local_rank)
@@ -398,6 +416,10 @@ def run_ours(args, cfg, rank, world, local_rank):
         fine = nat.stage_times()
         nat.profile(0)
         log(json.dumps({"fine_stage_ms": {k: [round(v[0], 3), v[1]] for k, v in fine.items()}}))
+    v_host = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        # the solved V on the host: the CPU leg times the reference's per-step V @ q on it
+        v_host = step.V.cpu().numpy()
     del step  # its V (and V^T R) buffers: the e2e arm allocates its own
     torch.cuda.empty_cache()
 
@@ -409,8 +431,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         # device-resident ones meanwhile (C3: 7 N^2 of 9 available at the eigensolve peak)
         m["l_i"] = m["r_i"] = None
         torch.cuda.empty_cache()
-        es()
-        torch.cuda.synchronize()
+        # no e2e warm-up pass: the device arm's warm-up steps already loaded every kernel
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
@@ -489,7 +510,8 @@ def run_ours(args, cfg, rank, world, local_rank):
             extra["td1_comparator"]["extrapolated_total_s"] / (t_max / args.steps))
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(m, cfg, units)
+        cpu = cpu_baseline(n, cfg, units, v_host)
+        del v_host
     if rank == 0:
         line = {
             "metric": "end-to-end transient wall time (eigensolve + steps); mode-steps/sec",
@@ -497,16 +519,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded plate generator, SURVEY.md §8(d))",
-            "config": {"workload": f"{args.config}: N={n} plate {cfg['grid']}, eigensolve + "
-                                   f"{T} TD2 steps x theta {list(cfg['thetas'])}"
-                                   + (f" x {n_rhs} right-hand sides (excitation sweep)"
-                                      if n_rhs > 1 else "")
-                                   + f", {cfg['n_obs']} observables",
-                       "n_rhs": n_rhs,
-                       "N": n, "T": T, "thetas": list(cfg["thetas"]), "n_obs": cfg["n_obs"],
-                       "mode_steps_per_step": units,
-                       "l2": f"inputs larger than L2 (L, R {8 * n * n / 1e9:.1f} GB each)",
-                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+            "config": workload_config(args, cfg, n, world),
             "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
@@ -577,41 +590,48 @@ def td1_comparator(m, cfg, steps, n_rhs=1):
     }
 
 
-def cpu_baseline(m, cfg, units):
+def cpu_baseline(n, cfg, units, v_host=None):
+    """The reference algorithm on this host's cores (oracle port), bounded samples,
+    extrapolated per component (oracle/cpu_baseline.py)."""
     from oracle import cpu_baseline as cb
-    n = m["plate"].n
-    l_i = m["l_i"].cpu().numpy()
-    r_i = m["r_i"].cpu().numpy()
-    r_d = m["r_d"].cpu().numpy().T.copy() if cfg["n_ports"] else np.zeros((n, 0))
-    l_d = m["l_d"].cpu().numpy().T.copy() if cfg["n_ports"] else np.zeros((n, 0))
     n_rhs = (cfg["n_ports"] + cfg["n_sources"]) if cfg.get("sweep") else 1
-    est = cb.estimate(l_i, r_i, r_d, l_d, m["m0"], cfg["steps"] * n_rhs, len(cfg["thetas"]),
-                      cfg["dt"])
+    est = cb.estimate(n, cfg["n_ports"], cfg["n_sources"], cfg["steps"],
+                      len(cfg["thetas"]) * n_rhs, cfg["dt"], v_full=v_host)
     return {"value": units / est["total_s"], "unit": "mode-steps/s", "cores": est["cores"],
-            "kind": "port", "sample": est["sample"], "extrapolated_total_s": est["total_s"],
-            "components_s": est["components"]}
+            "kind": "port", "sample": est["sample"], "extrapolated": True,
+            "extrapolated_total_s": est["total_s"], "components_s": est["components"],
+            "fits": est["fits"], "cpu_model": est["cpu_model"],
+            "per_step_ms": est["per_step_ms"],
+            "from_modal_gemv_ms_fit": est["from_modal_gemv_ms_fit"],
+            "from_modal_gemv_ms_full_n": est["from_modal_gemv_ms_full_n"]}
 
 
 def run_reference(args, cfg, rank, world):
-    """--impl reference: the reference algorithm on host cores (oracle port)."""
+    """--impl reference: the reference algorithm on the host cores (oracle port of its
+    numba kernels + numpy BLAS), rank 0 only. Each step is one bounded sample of the
+    workload (every eigensolve stage on small plates, the step kernel at the full N, the
+    V @ q GEMV at three orders); `value` is the full workload's mode-steps/s extrapolated
+    from the step's sample, `ms_per_step` the sample's own wall time."""
     if rank != 0:
         return
     from oracle import cpu_baseline as cb
     from paper_2407_11993_b200 import synth
     nx, ny, nz = cfg["grid"]
-    mdl = synth.plate_model(nx, ny, nz, n_ports=cfg["n_ports"], n_sources=cfg["n_sources"],
-                            n_obs=cfg["n_obs"])
-    n = mdl["r_i"].shape[0]
-    units = n * cfg["steps"] * len(cfg["thetas"])
+    n = synth.Plate(nx, ny, nz, notch=cfg.get("notch", False)).n
+    n_rhs = (cfg["n_ports"] + cfg["n_sources"]) if cfg.get("sweep") else 1
+    units = n * cfg["steps"] * len(cfg["thetas"]) * n_rhs
+
+    def sample():
+        return cb.estimate(n, cfg["n_ports"], cfg["n_sources"], cfg["steps"],
+                           len(cfg["thetas"]) * n_rhs, cfg["dt"])
     for _ in range(args.warmup):
-        cb.estimate(mdl["l_i"], mdl["r_i"], mdl["r_d"], mdl["l_d"], mdl["m0"], cfg["steps"],
-                    len(cfg["thetas"]), cfg["dt"], n_sample=256, rotations=4, sample_steps=1)
-    totals = []
+        sample()
+    totals, walls = [], []
     est = None
     for _ in range(args.steps):
-        est = cb.estimate(mdl["l_i"], mdl["r_i"], mdl["r_d"], mdl["l_d"], mdl["m0"],
-                          cfg["steps"], len(cfg["thetas"]), cfg["dt"], n_sample=768,
-                          rotations=16, sample_steps=2)
+        t0 = time.perf_counter()
+        est = sample()
+        walls.append(time.perf_counter() - t0)
         totals.append(est["total_s"])
     t = statistics.median(totals)
     value = units / t
@@ -619,16 +639,21 @@ def run_reference(args, cfg, rank, world):
         "impl": "reference",
         "metric": "end-to-end transient wall time (eigensolve + steps); mode-steps/sec",
         "value": value, "unit": "mode-steps/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "warmup": args.warmup, "ms_per_step": statistics.mean(walls) * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded plate generator, SURVEY.md §8(d))",
-        "config": {"workload": f"{args.config}: N={n}, eigensolve + {cfg['steps']} TD2 steps x "
-                               f"theta {list(cfg['thetas'])}", "N": n},
+        "config": workload_config(args, cfg, n, world),
+        "value_kind": "extrapolated: the full workload's mode-steps/s from each step's bounded "
+                      "sample (median over steps); ms_per_step is the sample's wall time",
+        "extrapolated_total_s": t,
+        "extrapolated_spread": [min(totals), max(totals)],
         "cpu_baseline": {"value": value, "unit": "mode-steps/s", "cores": est["cores"],
-                         "kind": "port", "sample": est["sample"]},
+                         "kind": "port", "sample": est["sample"], "extrapolated": True,
+                         "cpu_model": est["cpu_model"]},
         "e2e": {"value": value, "unit": "mode-steps/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "components_s": est["components"],
+        "fits": est["fits"],
     }
     print(json.dumps(line), flush=True)
 
@@ -639,8 +664,8 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=sorted(CONFIGS), default="C2")
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="C3")
+    ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--td1-steps", type=int, default=300)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-td1", action="store_true")
