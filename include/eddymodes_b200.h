@@ -149,7 +149,7 @@ int em_sygv_lh(em_ctx* ctx, int64_t n, const double* L_host, double* L, int64_t 
                int64_t ldr, double* tau, double* V, int64_t ldv, double* l_n, double* r_n,
                double* VtR, int64_t ldvtr, int flags, int64_t* pivot, int* which);
 
-/* --- modal theta-method (TD2, transient.py:258-308) ------------------------------- */
+/* --- modal theta-method (TD2, transient.py:116-166) ------------------------------- */
 
 /* Plan for the decoupled stepper. r_n, l_n: n; P_r, P_l: n x n_p; P_m: n x n_s
  * (column-major, P = V^T [R_D | L_D | M0] — see em_dgemm). Holds device copies. */
@@ -159,7 +159,7 @@ int em_td2_plan_create(em_ctx* ctx, int64_t n, int n_p, int n_s, const double* l
 void em_td2_plan_destroy(em_td2_plan* plan);
 
 /* Exact per-interval integrator for piecewise-linear drives on a uniform grid of step h
- * (exact_modal_reference / exact_first_order, transient.py:457-502): the same plan type
+ * (exact_modal_reference / exact_first_order, transient.py:315-360): the same plan type
  * and em_td2_run as the theta-method, with q^{k+1} = a q^k + c1 e0 + c2 s per mode
  * (a = exp(-h r/l)). em_td2_step / _forcing / _step_forcing reject such a plan. */
 int em_td2_plan_create_exact(em_ctx* ctx, int64_t n, int n_p, int n_s, const double* l_n,
@@ -173,7 +173,7 @@ int em_td2_set_observables(em_td2_plan* plan, int n_obs, const double* CV, int64
 
 /* Integrate T steps from modal state q (n, device, in/out) over the drive table
  * drive ((T+1) x (n_p + n_s) row-major: row k = [i_d(t_k), i0(t_k)]), exactly the
- * samples run_transient uses (transient.py:432-441).
+ * samples run_transient uses (transient.py:290-299).
  * Y (T x n_obs row-major, may be NULL): observables after every step.
  * Qcap (n x n_caps column-major, may be NULL): q after every stride-th step.
  * Blocked linear-recurrence scan over time, fused with the forcing projection
@@ -183,7 +183,7 @@ int em_td2_run(em_td2_plan* plan, int64_t T, const double* drive, double* q, dou
 
 /* Excitation sweep (BASELINE configs[4], C5): every drive channel integrated ALONE,
  * i.e. the n_c = n_p + n_s columns of the drive table as independent right-hand sides
- * (the reference superposes them into one trajectory, transient.py:289-297; by
+ * (the reference superposes them into one trajectory, transient.py:147-155; by
  * linearity the sweep's responses sum to that trajectory). Q (n x n_c column-major,
  * device, in/out): per-channel modal states. Y (n_c x n_caps x n_obs, may be NULL):
  * Y[c] = observables of channel c alone (the D term only for port channels). */
@@ -196,13 +196,13 @@ int em_td2_step(em_td2_plan* plan, double* q, const double* i_d_h, const double*
                 const double* di0_h);
 
 /* Per-mode forcing increment f (n, device) = -dt P_r i_d - P_ltr di_d - P_m di0
- * (Td2Stepper.forcing, transient.py:289-297; modal_forcing, modal.py:101-118). */
+ * (Td2Stepper.forcing, transient.py:147-155; modal_forcing, modal.py:101-118). */
 int em_td2_forcing(em_td2_plan* plan, const double* i_d_h, const double* di_d_h,
                    const double* di0_h, double* f);
-/* q += ((-dt r q + f)/c)/c with a given forcing (step_td2, transient.py:327-337). */
+/* q += ((-dt r q + f)/c)/c with a given forcing (step_td2, transient.py:185-195). */
 int em_td2_step_forcing(em_td2_plan* plan, double* q, const double* f);
 
-/* --- Cholesky theta-method (TD1, transient.py:219-255) ------------------------------ */
+/* --- Cholesky theta-method (TD1, transient.py:77-113) ------------------------------ */
 
 /* Z = L + dt*theta*R factored on device (potrf); R kept for the per-step matvec.
  * r_d, l_d: n x n_p; m0: n x n_s. *pivot reports a non-SPD stepping matrix. */
@@ -219,7 +219,7 @@ int em_td1_run(em_td1_plan* plan, int64_t T, const double* drive, double* I, dou
 int em_td1_step(em_td1_plan* plan, double* I, const double* i_d_h, const double* di_d_h,
                 const double* di0_h);
 /* Copy the lower Cholesky factor of the stepping matrix (n x n, column-major) to out
- * (device). Td1Stepper.chol (transient.py:237). */
+ * (device). Td1Stepper.chol (transient.py:95). */
 int em_td1_factor(em_td1_plan* plan, double* out, int64_t ldo);
 
 /* --- frequency domain (frequency.py) --------------------------------- */

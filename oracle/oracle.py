@@ -196,7 +196,7 @@ def drive_rhs(r_d, l_d, m0, i_d, delta_i_d, delta_i0, dt, theta) -> np.ndarray:
 # --- transient.py ---------------------------------------------------------------
 
 def tone_sampler(tones_per_channel):
-    """transient.py:363-385: per-channel sums of amp*sin(omega t + phase) via np.add.at."""
+    """transient.py:221-243: per-channel sums of amp*sin(omega t + phase) via np.add.at."""
     amps, omegas, phases, owner = [], [], [], []
     for ch, tones in enumerate(tones_per_channel):
         for (amp, freq, ph) in tones:
@@ -217,13 +217,13 @@ def tone_sampler(tones_per_channel):
 
 
 def sample_table(sample, steps: int, dt: float) -> np.ndarray:
-    """Samples at t_k = k*dt exactly as run_transient evaluates them (transient.py:432-438)."""
+    """Samples at t_k = k*dt exactly as run_transient evaluates them (transient.py:290-296)."""
     rows = [sample(0.0)] + [sample((k + 1) * dt) for k in range(steps)]
     return np.array(rows).reshape(steps + 1, -1)
 
 
 class Td1:
-    """transient.py:219-255 (Td1Stepper) over the C kernels."""
+    """transient.py:77-113 (Td1Stepper) over the C kernels."""
 
     def __init__(self, l_i, r_i, r_d, l_d, m0, dt, theta):
         self.r = np.ascontiguousarray(r_i, dtype=float)
@@ -243,7 +243,7 @@ class Td1:
 
 
 class Td2:
-    """transient.py:258-308 (Td2Stepper) over the C kernels."""
+    """transient.py:116-166 (Td2Stepper) over the C kernels."""
 
     def __init__(self, basis: Basis, r_d, l_d, m0, dt, theta):
         self.basis = basis
@@ -307,10 +307,10 @@ def td2_run_table(l_n, r_n, p_r, p_l, p_m, dt, theta, tab, steps, cv=None, strid
 def run(stepper, n: int, i_d_tab: np.ndarray, i0_tab: np.ndarray, modal: Basis | None,
         c_obs: np.ndarray | None = None, capture_stride: int = 1, capture_state: bool = True,
         max_steps: int | None = None):
-    """transient.py:390-454 (run_transient) driven by a sample table (rows t_0..t_T).
+    """transient.py:248-312 (run_transient) driven by a sample table (rows t_0..t_T).
 
     Returns (states (n_caps, N) or None, observables (n_caps, n_obs) or None).
-    td2 reconstructs internal = V q at every capture (transient.py:443)."""
+    td2 reconstructs internal = V q at every capture (transient.py:301)."""
     steps = i_d_tab.shape[0] - 1 if max_steps is None else max_steps
     n_caps = steps // capture_stride
     states = np.zeros((n_caps, n)) if capture_state else None
@@ -330,7 +330,7 @@ def run(stepper, n: int, i_d_tab: np.ndarray, i0_tab: np.ndarray, modal: Basis |
 
 
 def exact_first_order(l_n, r_n, y0, e0, slope, h):
-    """transient.py:494-502."""
+    """transient.py:352-360."""
     tau = l_n / r_n
     yp0 = (e0 - slope * tau) / r_n
     yph = (e0 + slope * h - slope * tau) / r_n
@@ -338,7 +338,7 @@ def exact_first_order(l_n, r_n, y0, e0, slope, h):
 
 
 def exact_modal_reference(basis: Basis, r_d, l_d, m0, i_d_samples, i0_samples, times):
-    """transient.py:457-491: exact per-interval integration for piecewise-linear drives."""
+    """transient.py:315-349: exact per-interval integration for piecewise-linear drives."""
     n_t = times.shape[0]
     n = basis.tau.shape[0]
     vt = basis.v.T

@@ -161,7 +161,7 @@ int em_config(em_ctx* ctx, int key, int64_t value) {
       EM_CK(cudaMemPoolTrimTo(pool, (size_t)value));
       return EM_OK;
     }
-    if (key == 97) {  // debug: Q2 back-transform (0 column strips, 1 wavefront GEMMs)
+    if (key == 97) {  // debug: Q2 back-transform (0 register-resident, 1 wavefront GEMMs, 2 strips)
       em::g_q2_mode = (int)value;
       return EM_OK;
     }

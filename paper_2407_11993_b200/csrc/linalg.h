@@ -159,4 +159,8 @@ void td1_run(em_td1_plan* P, int64_t T, const double* drive, double* I, double* 
              int64_t stride, double* Icap);
 void td1_step(em_td1_plan* P, double* I, const double* u_dev);
 
+// q2reg.cu: Z <- Q2 Z (stage-2 reflectors V2 with task offsets toff, T factors T2)
+void q2_apply_reg(cudaStream_t st, int64_t n, int64_t ncols, int64_t ngroups, const double* V2,
+                  const int64_t* toff, const double* T2, double* Z, int64_t ldz);
+
 }  // namespace em

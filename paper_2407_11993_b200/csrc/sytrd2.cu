@@ -574,7 +574,8 @@ __global__ void __launch_bounds__(256) q2_buildv_kernel(int64_t n, const Q2Block
 constexpr int Q2_LDC = 3 * 64 + 4;  // Z ring, column-major [col][3 halves]: = 4 mod 16
 constexpr int Q2_LDV = 85;          // compact reflectors [t][8 + i], zero pads: LDV - 1 = 4 mod 16
 constexpr int Q2_LDT = 68;          // VT row-major [r][j]: = 4 mod 16
-int g_q2_mode = 0;                  // debug key 97: 1 = the wavefront grouped-GEMM form
+int g_q2_mode = 0;  // debug key 97: 0 register-resident (q2reg.cu), 1 the wavefront grouped-GEMM
+                    // form, 2 the shared-memory column strips
 
 // VT (128 x 64 row-major, window row r = global row 64 (g + k) + r) of every block of
 // group g; T2g = the group's T factors (row-major 64 x 64, upper).
@@ -954,6 +955,9 @@ void syev_two_stage(cudaStream_t st, int64_t n, double* A, int64_t lda, double* 
       q2_tfactor_kernel<<<(unsigned)nblk, 256, smt, st>>>(n, dblk.p, V2.p, TAU2.p, dtoff.p, T2.p);
       EM_LAUNCHED();
       if (g_q2_mode == 0) {
+        q2_apply_reg(st, n, n, ngroups, V2.p, dtoff.p, T2.p, Z, ldz);
+        EM_CK(cudaStreamSynchronize(st));  // dblk lifetime
+      } else if (g_q2_mode == 2) {
         q2_apply_strips(st, n, n, ngroups, V2.p, dtoff.p, T2.p, Z, ldz);
         EM_CK(cudaStreamSynchronize(st));  // dblk lifetime
       } else {

@@ -1,6 +1,6 @@
 // Cholesky-factor theta-method (TD1) on B200 — the comparator of the paper.
 //
-// Reference: Td1Stepper (pkg/src/eddymodes/transient.py:219-255) factors
+// Reference: Td1Stepper (pkg/src/eddymodes/transient.py:77-113) factors
 // Z = L_i + dt*theta*R_i once (cholesky, "stepping matrix") and every step runs
 // td1_step_kernel (_kernels.py:198-210): b = -dt R I + drive_rhs (modal.py:121-131),
 // forward then backward substitution with the factor (tri_solve_vec,

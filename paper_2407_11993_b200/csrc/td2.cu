@@ -1,10 +1,10 @@
 // Modal theta-method (TD2) on B200: forcing projection + per-mode linear
 // recurrence + observable reconstruction.
 //
-// Reference: Td2Stepper (pkg/src/eddymodes/transient.py:258-308) advances every
+// Reference: Td2Stepper (pkg/src/eddymodes/transient.py:116-166) advances every
 // mode by q += ((-dt*r*q + f)/c)/c with c = sqrt(l + dt*theta*r)
 // (_kernels.py:213-222) and f = -dt*P_r i_D - P_ltr dI_D - P_m dI_0
-// (transient.py:289-297); run_transient (transient.py:390-454) reconstructs the
+// (transient.py:147-155); run_transient (transient.py:248-312) reconstructs the
 // observables from V q after every captured step.
 //
 // Here the recurrence is written q^{k+1} = (1 - eps) q^k + g^k with
@@ -76,7 +76,7 @@ __global__ void td2_coeffs_kernel(int64_t n, int n_p, int n_s, double dt, double
 }
 
 // Exact per-interval integrator for piecewise-linear drives (exact_modal_reference /
-// exact_first_order, E/transient.py:457-502) as the same recurrence
+// exact_first_order, E/transient.py:315-360) as the same recurrence
 // q^{k+1} = (1 - eps) q^k + W u^k:  with tau = l/r, a = exp(-h/tau),
 //   eps = -expm1(-h/tau),  q^{k+1} = a q^k + c1 e0 + c2 s,
 //   c1 = (1 - a)/r,  c2 = (h - (1 - a) tau)/r,
@@ -629,7 +629,7 @@ void td2_delete(em_td2_plan* p) {
 }
 em_ctx* td2_ctx(em_td2_plan* p) { return p ? p->ctx : nullptr; }
 
-// f = -dt P_r i_d - P_ltr di_d - P_m di0 (Td2Stepper.forcing, transient.py:289-297)
+// f = -dt P_r i_d - P_ltr di_d - P_m di0 (Td2Stepper.forcing, transient.py:147-155)
 __global__ void td2_forcing_kernel(int64_t n, int n_p, int n_s, double dt,
                                    const double* __restrict__ Pr, const double* __restrict__ Pltr,
                                    const double* __restrict__ Pm, const double* __restrict__ u,

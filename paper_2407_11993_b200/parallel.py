@@ -1,6 +1,6 @@
 """Mode-sharded modal stepping across GPUs (north-star (b)).
 
-After the eigensolve the modes never interact (transient.py:258-308: every
+After the eigensolve the modes never interact (transient.py:116-166: every
 mode's update uses only its own r_n, c_n and forcing row), so the TD2 stepping
 shards naturally: rank r owns a contiguous range of modes, integrates them with
 its own fused scan (em_td2_run) and produces PARTIAL observables

@@ -10,7 +10,7 @@ forcing and the observable reconstruction (em_td2_run).
 The per-step `step()` methods keep the reference's host in-place semantics
 (one device round trip per call); `run()` and run_transient are the batched
 fast path. Observables y = C I + D i_D(t_{k+1}) (the reference's
-`t_internal @ internal + t_ports @ i_d_next`, transient.py:446-447) are given
+`t_internal @ internal + t_ports @ i_d_next`, transient.py:304-305) are given
 directly as matrices; the probe geometry (assembly.field_transfer) is a front
 end outside this path.
 """
@@ -118,7 +118,7 @@ def _obs_device(observables, n: int, n_p: int):
 
 
 def _drive_projection(rm: ReducedModel, basis: ModalBasis):
-    """V^T [R_D | L_D | M0] on the device (transient.py:276-286), column-major n x n_d
+    """V^T [R_D | L_D | M0] on the device (transient.py:134-144), column-major n x n_d
     (torch (n_d, n)); a (1, n) zero block when there are no drive channels."""
     n, n_p, n_s = basis.n_modes, rm.n_ports, rm.n_sources
     nd = 2 * n_p + n_s
@@ -135,7 +135,7 @@ def _drive_projection(rm: ReducedModel, basis: ModalBasis):
 
 
 class Td2Stepper:
-    """Decoupled stepper (transient.py:258-308): per-mode scalar updates after
+    """Decoupled stepper (transient.py:116-166): per-mode scalar updates after
     projecting the drive onto the modes."""
 
     def __init__(self, rm: ReducedModel, basis: ModalBasis, dt: float, theta: float):
@@ -149,7 +149,7 @@ class Td2Stepper:
         self.theta = float(theta)
         n, n_p, n_s = basis.n_modes, rm.n_ports, rm.n_sources
         self._n, self._n_p, self._n_s = n, n_p, n_s
-        # host copies kept for API compatibility (transient.py:276-286)
+        # host copies kept for API compatibility (transient.py:134-144)
         den = basis.l_n + self.dt * self.theta * basis.r_n
         self._c = np.sqrt(den)
         self._rn = basis.r_n.copy()
@@ -185,7 +185,7 @@ class Td2Stepper:
         return nat.host_colmajor(self._proj[2 * self._n_p:], self._n, self._n_s)
 
     def forcing(self, i_d, delta_i_d, delta_i0) -> np.ndarray:
-        """-dt P_r i_D - P_ltr dI_D - P_m dI_0 (transient.py:289-297), on the device."""
+        """-dt P_r i_D - P_ltr dI_D - P_m dI_0 (transient.py:147-155), on the device."""
         f = nat.empty(self._n)
         u = [np.ascontiguousarray(np.asarray(x, dtype=float)) for x in (i_d, delta_i_d, delta_i0)]
         ptrs = [x.ctypes.data_as(ctypes.c_void_p) for x in u]
@@ -194,7 +194,7 @@ class Td2Stepper:
         return f.cpu().numpy()
 
     def step(self, modal_state: np.ndarray, i_d, delta_i_d, delta_i0) -> np.ndarray:
-        """Advance one step in place (transient.py:299-308)."""
+        """Advance one step in place (transient.py:157-166)."""
         n = self._n
         if modal_state.shape != (n,):
             raise DimensionMismatch(f"modal state must have {n} components")
@@ -267,7 +267,7 @@ class Td2Stepper:
         """Batched-excitation sweep (BASELINE configs[4]): the response to each drive
         channel (ports, then sources) ALONE, all channels integrated in one call — the
         reference would run one trajectory per channel (run_transient superposes them,
-        transient.py:289-297). Returns (observables (n_c, n_caps, n_obs) or None,
+        transient.py:147-155). Returns (observables (n_c, n_caps, n_obs) or None,
         final modal states (N, n_c))."""
         n_c = self._n_p + self._n_s
         if n_c == 0:
@@ -298,7 +298,7 @@ def _reconstruct(basis: ModalBasis, qcap, n_caps: int) -> np.ndarray:
 
 
 class Td1Stepper:
-    """Coupled stepper (transient.py:219-255): Cholesky factor of L_i + dt theta R_i."""
+    """Coupled stepper (transient.py:77-113): Cholesky factor of L_i + dt theta R_i."""
 
     def __init__(self, rm: ReducedModel, dt: float, theta: float):
         _check_theta_dt(dt, theta)
@@ -337,7 +337,7 @@ class Td1Stepper:
 
     @property
     def chol(self) -> linalg.LowerTriangular | None:
-        """The stepping-matrix factor (transient.py:237), copied from the device."""
+        """The stepping-matrix factor (transient.py:95), copied from the device."""
         if self._plan is None:
             return None
         if self._chol is None:
@@ -348,7 +348,7 @@ class Td1Stepper:
         return self._chol
 
     def step(self, state: np.ndarray, i_d, delta_i_d, delta_i0) -> np.ndarray:
-        """Advance one step in place and return the state (transient.py:244-255)."""
+        """Advance one step in place and return the state (transient.py:102-113)."""
         n = self._n
         if state.shape != (n,):
             raise DimensionMismatch(f"state must have {n} components")
@@ -397,7 +397,7 @@ def prepare_td1(rm: ReducedModel, cfg: TransientConfig) -> Td1Stepper:
 
 
 def step_td1(stepper: Td1Stepper, state, i_d, delta_i_d, delta_i0) -> np.ndarray:
-    """Functional wrapper over Td1Stepper.step (transient.py:315-320)."""
+    """Functional wrapper over Td1Stepper.step (transient.py:173-178)."""
     return stepper.step(np.asarray(state, dtype=float), np.asarray(i_d, dtype=float),
                         np.asarray(delta_i_d, dtype=float), np.asarray(delta_i0, dtype=float))
 
@@ -407,7 +407,7 @@ def prepare_td2(rm: ReducedModel, basis: ModalBasis, cfg: TransientConfig) -> Td
 
 
 def step_td2(stepper: Td2Stepper, modal_state, forcing) -> np.ndarray:
-    """Advance modal coordinates one step with a precomputed forcing (transient.py:327-337)."""
+    """Advance modal coordinates one step with a precomputed forcing (transient.py:185-195)."""
     modal_state = np.asarray(modal_state, dtype=float)
     forcing = np.asarray(forcing, dtype=float)
     if forcing.shape != modal_state.shape:
@@ -422,7 +422,7 @@ def step_td2(stepper: Td2Stepper, modal_state, forcing) -> np.ndarray:
 
 
 def _drive_channels(net, rm: ReducedModel, drives):
-    """Port/source name order and per-channel tone lists (transient.py:340-361)."""
+    """Port/source name order and per-channel tone lists (transient.py:198-219)."""
     if net is not None:
         port_names = [el.name for el in net.electrodes[:-1]] if net.n_electrodes else []
         source_names = [c.name for c in net.sources if c.port is None]
@@ -447,7 +447,7 @@ def _drive_channels(net, rm: ReducedModel, drives):
 
 def _sample_channels(tone_lists, t: np.ndarray) -> np.ndarray:
     """Per-channel multisine samples at times t, (len(t), n_ch); per channel the
-    tones are accumulated in order from 0.0 like np.add.at in transient.py:379-383."""
+    tones are accumulated in order from 0.0 like np.add.at in transient.py:237-241."""
     out = np.zeros((t.shape[0], len(tone_lists)))
     for ch, tones in enumerate(tone_lists):
         for tone in tones:
@@ -466,7 +466,7 @@ def drive_samples(net, rm: ReducedModel, drives, dt: float, n_steps: int):
 
 def run_transient(rm: ReducedModel, net, drives, cfg: TransientConfig,
                   modal: ModalBasis | None = None, observables=None) -> SimulationResult:
-    """Integrate from rest, capture every capture_stride steps (transient.py:390-454).
+    """Integrate from rest, capture every capture_stride steps (transient.py:248-312).
 
     observables: optional (C, D) with C (n_obs x N) and D (n_obs x n_ports) or None;
     captured values are C I + D i_D(t_{k+1}) for each capture."""
@@ -506,7 +506,7 @@ def run_transient(rm: ReducedModel, net, drives, cfg: TransientConfig,
 
 def exact_first_order(l_n: np.ndarray, r_n: np.ndarray, y0: np.ndarray,
                       e0: np.ndarray, slope: np.ndarray, h: float) -> np.ndarray:
-    """Closed-form step of l y' + r y = e0 + slope t (transient.py:494-502), per
+    """Closed-form step of l y' + r y = e0 + slope t (transient.py:352-360), per
     component (a small host formula, as in the reference)."""
     tau = l_n / r_n
     yp0 = (e0 - slope * tau) / r_n
@@ -517,7 +517,7 @@ def exact_first_order(l_n: np.ndarray, r_n: np.ndarray, y0: np.ndarray,
 def exact_modal_reference(basis: ModalBasis, rm: ReducedModel, i_d_samples, i0_samples,
                           times, modal_state0=None) -> np.ndarray:
     """Exact per-interval integration of every mode for piecewise-linear drives
-    (transient.py:457-491), on the device: per mode q^{k+1} = a q^k + c1 e0 + c2 s with
+    (transient.py:315-349), on the device: per mode q^{k+1} = a q^k + c1 e0 + c2 s with
     a = exp(-h r/l) is the same linear recurrence as the theta-method, so it runs as one
     blocked scan (em_td2_plan_create_exact + em_td2_run). The scan needs one factor a
     per mode, i.e. uniformly spaced sample times (ValidationError otherwise).
@@ -565,7 +565,7 @@ def exact_modal_reference(basis: ModalBasis, rm: ReducedModel, i_d_samples, i0_s
     return out
 
 
-# --- CSV export (transient.py:505-546) -----------------------------------------------
+# --- CSV export (transient.py:363-404) -----------------------------------------------
 
 def write_timeseries_csv(path, result: SimulationResult, header_lines: tuple[str, ...] = ()):
     if result.probe_fields is None:

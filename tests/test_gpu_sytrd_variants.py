@@ -77,13 +77,13 @@ def test_sytrd_larger_orders(n):
 
 
 @pytest.mark.parametrize("n,lda", [(129, 129), (300, 301), (1000, 1000), (2049, 2051),
-                                   (6000, 6000), (9800, 9800)])
+                                   (4500, 4503), (6000, 6000), (9800, 9800)])
 def test_two_stage_q2_forms_agree(n, lda):
-    """Two-stage reduction: the column-strip Q2 back-transform (debug key 97 = 0, the
-    default) and the wavefront grouped-GEMM form (97 = 1) give the same eigenvectors up
-    to rounding, and both satisfy the eigen-equation; orders with a partial last sweep
-    group and strip, and an odd leading dimension; n = 9800 has more strips than SMs, so
-    the launch mixes 48- and 32-column strips."""
+    """Two-stage reduction: the register-resident Q2 back-transform (debug key 97 = 0, the
+    default), the wavefront grouped-GEMM form (97 = 1) and the shared-memory column strips
+    (97 = 2) give the same eigenvectors up to rounding, and all satisfy the eigen-equation;
+    orders with a partial last sweep group and strip, odd leading dimensions (4500 / 4503:
+    sy2sb's blocked symmetric product with lda != n); n = 9800 has more strips than SMs."""
     from paper_2407_11993_b200 import _native as nat
     lib, ctx = nat.load_library(), nat.context()
     rng = np.random.default_rng(n)
@@ -92,7 +92,7 @@ def test_two_stage_q2_forms_agree(n, lda):
     nat.set_two_stage_min(0)
     try:
         out = {}
-        for mode in (0, 1):
+        for mode in (0, 1, 2):
             nat.check(lib.em_config(ctx, 97, mode))
             out[mode] = _syev(a, lda=lda)
     finally:
@@ -104,7 +104,8 @@ def test_two_stage_q2_forms_agree(n, lda):
         assert np.max(np.abs(w - ref)) < 1e-12 * scale * n
         assert np.max(np.abs(u.T @ u - np.eye(n))) < 1e-12 * n
         assert np.max(np.abs(a @ u - u * w)) < 1e-11 * scale * n
-    np.testing.assert_array_equal(out[0][0], out[1][0])  # Q2 does not touch the spectrum
-    # same eigenvectors (well separated random spectrum; sign fixed by the solver)
-    d = np.abs(np.abs(np.sum(out[0][1] * out[1][1], axis=0)) - 1.0)
-    assert d.max() < 1e-9
+    for mode in (1, 2):
+        np.testing.assert_array_equal(out[0][0], out[mode][0])  # Q2 does not touch the spectrum
+        # same eigenvectors (well separated random spectrum; sign fixed by the solver)
+        d = np.abs(np.abs(np.sum(out[0][1] * out[mode][1], axis=0)) - 1.0)
+        assert d.max() < 1e-9

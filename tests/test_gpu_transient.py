@@ -209,7 +209,7 @@ def test_mode_sharded_stepping_on_device():
 
 
 def test_exact_modal_integrator_on_device_matches_oracle():
-    """exact_modal_reference (transient.py:457-502) on the device (the
+    """exact_modal_reference (transient.py:315-360) on the device (the
     exponential integrator as the blocked scan) against the host restatement, over a
     ramp + tone drive, moderate dt/tau; with an initial state; non-uniform times rejected."""
     from paper_2407_11993_b200 import modal, reduction, transient
@@ -243,7 +243,7 @@ def test_excitation_sweep_matches_oracle_per_channel(theta):
     channel integrated alone as its own right-hand side. Every channel's observables
     (with the port's direct term D) against the oracle run with only that channel
     driven; the channels sum to the superposed trajectory of the UNMODIFIED reference
-    (golden td2_obs, transient.py:289-297 superposes them); final per-channel states."""
+    (golden td2_obs, transient.py:147-155 superposes them); final per-channel states."""
     from paper_2407_11993_b200 import modal, reduction, transient
     g = golden("plate_small")
     rng = np.random.default_rng(7)
