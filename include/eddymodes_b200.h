@@ -140,6 +140,17 @@ int em_sygv(em_ctx* ctx, int64_t n, const double* L, int64_t ldl, const double* 
 int em_sygv_ex(em_ctx* ctx, int64_t n, const double* L, int64_t ldl, double* R, int64_t ldr,
                double* tau, double* V, int64_t ldv, double* l_n, double* r_n, double* VtR,
                int64_t ldvtr, int flags, int64_t* pivot, int* which);
+/* One rank's share of a column-sharded generalized eigensolve (the multi-GPU layout of
+ * paper_2407_11993_b200/parallel.py): modes m_lo .. m_hi - 1 of the DESCENDING order.
+ * Outputs tau (all n), V (n x (m_hi - m_lo), ld ldv), l_n, r_n (m_hi - m_lo) and VtR
+ * (n x (m_hi - m_lo)) equal the corresponding columns / entries of em_sygv_ex's. Every
+ * rank reduces the whole pencil to tridiagonal form and solves it; only the eigenvector
+ * back-transforms, the sign fix and l_n, r_n are restricted to the rank's columns, so
+ * the ranks exchange nothing. Flags as em_sygv_ex. */
+int em_sygv_range(em_ctx* ctx, int64_t n, const double* L, int64_t ldl, double* R, int64_t ldr,
+                  int64_t m_lo, int64_t m_hi, double* tau, double* V, int64_t ldv, double* l_n,
+                  double* r_n, double* VtR, int64_t ldvtr, int flags, int64_t* pivot,
+                  int* which);
 /* em_sygv_ex with L still on the host: the library uploads L_host (n x n, leading
  * dimension n; pinned memory makes the copy asynchronous) into the device buffer L (ld
  * ldl) on a copy engine, after the work already queued on the context stream (e.g. R's

@@ -18,6 +18,7 @@ extern int64_t g_two_stage_min;
 extern int g_sytrd_dbg;
 extern int g_band_off;
 extern int g_ln_dense;
+extern int g_q2r_dbg;
 extern int g_q2_mode;
 extern int g_symv_align_off;
 extern int64_t g_symv_keep_mb;
@@ -28,7 +29,7 @@ int stages_read(double* ms, int64_t* counts, int n);
 int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const double* R,
              int64_t ldr, double* tau, double* V, int64_t ldv, double* l_n, double* r_n,
              double* VtR, int64_t ldvtr, int* which, int flags,
-             cudaEvent_t l_ready = nullptr);
+             cudaEvent_t l_ready = nullptr, int64_t m_lo = 0, int64_t m_hi = -1);
 }
 
 // full definitions live in td1.cu / td2.cu; re-declare the layout-independent API here
@@ -161,6 +162,10 @@ int em_config(em_ctx* ctx, int key, int64_t value) {
       EM_CK(cudaMemPoolTrimTo(pool, (size_t)value));
       return EM_OK;
     }
+    if (key == 95) {  // debug: register-resident Q2 switches (q2reg.cu)
+      em::g_q2r_dbg = (int)value;
+      return EM_OK;
+    }
     if (key == 97) {  // debug: Q2 back-transform (0 register-resident, 1 wavefront GEMMs, 2 strips)
       em::g_q2_mode = (int)value;
       return EM_OK;
@@ -253,6 +258,22 @@ int em_sygv_ex(em_ctx* ctx, int64_t n, const double* L, int64_t ldl, double* R, 
     int wh = -1;
     const int64_t p = em::sygv(ctx->stream, n, L, ldl, R, ldr, tau, V, ldv, l_n, r_n, VtR, ldvtr,
                                &wh, flags);
+    if (pivot) *pivot = p;
+    if (which) *which = wh;
+    return p >= 0 ? EM_ERR_NOT_PD : EM_OK;
+  });
+}
+
+int em_sygv_range(em_ctx* ctx, int64_t n, const double* L, int64_t ldl, double* R, int64_t ldr,
+                  int64_t m_lo, int64_t m_hi, double* tau, double* V, int64_t ldv, double* l_n,
+                  double* r_n, double* VtR, int64_t ldvtr, int flags, int64_t* pivot,
+                  int* which) {
+  return guarded(ctx, [&] {
+    if (flags & ~EM_SYGV_R_WORKSPACE) throw em::ArgError{"unknown em_sygv_range flags"};
+    if (m_lo < 0 || m_hi > n || m_lo > m_hi) throw em::ArgError{"em_sygv_range: bad mode range"};
+    int wh = -1;
+    const int64_t p = em::sygv(ctx->stream, n, L, ldl, R, ldr, tau, V, ldv, l_n, r_n, VtR, ldvtr,
+                               &wh, flags, nullptr, m_lo, m_hi);
     if (pivot) *pivot = p;
     if (which) *which = wh;
     return p >= 0 ? EM_ERR_NOT_PD : EM_OK;

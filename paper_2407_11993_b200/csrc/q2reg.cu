@@ -36,6 +36,9 @@
 
 namespace em {
 
+int g_q2r_dbg = 0;  // debug key 95: bit0 VT(k) waits for C(k-1); bit1 uniform strips;
+                    // bit2 synchronous Z staging loads; bit3 fences before the empty arrivals
+
 namespace {
 constexpr int QB = 64;                  // sweeps per group, reflector length
 constexpr int VP = 8 * 9 * 64;          // packed V: 8 column tiles J x 9 row tiles (R = J..J+8)
@@ -137,16 +140,31 @@ struct Q2RWarp {
   double* zst;        // this warp's staging buffer [8 cols][ZLD]
   double* Z;
   int64_t ldz, n, ncols, col, c0w;
-  int lane, gq, tq;
+  int lane, gq, tq, dbg;
 
-  // rows 64 h .. 64 h + 63 of the warp's 8 columns into the staging buffer
+  // rows 64 h .. 64 h + 63 of the warp's 8 columns into the staging buffer. L2-only
+  // copies (.cg): Z rows this SM stored earlier (the previous group's launch, or lines that
+  // straddle two halves when a column does not start 128-byte aligned) must not be served
+  // from a stale L1 line. 16-byte copies of row pairs when ldz is even, else synchronous
+  // 8-byte loads.
   EM_DEVINL void load_half(int64_t h) const {
+    if ((ldz & 1) == 0 && !(dbg & 4)) {
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const int e = q * 32 + lane, c = e >> 6, i = e & 63;
-      const int64_t row = 64 * h + i, cg = c0w + c;
-      const bool ok = row < n && cg < ncols;
-      cp_async8(zst + c * ZLD + i, ok ? Z + row + cg * ldz : Z, ok);
+      for (int q = 0; q < 8; ++q) {
+        const int e = q * 32 + lane, c = e >> 5, i = 2 * (e & 31);
+        const int64_t row = 64 * h + i, cg = c0w + c;
+        const int bytes = (cg < ncols && row < n) ? (row + 1 < n ? 16 : 8) : 0;
+        cp_async16(zst + c * ZLD + i, bytes ? Z + row + cg * ldz : Z, bytes);
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int e = q * 32 + lane, c = e >> 6, i = e & 63;
+        const int64_t row = 64 * h + i, cg = c0w + c;
+        const bool ok = row < n && cg < ncols;
+        // (8-byte cp.async exists only as .ca: synchronous L2 loads instead)
+        zst[c * ZLD + i] = ok ? __ldcg(Z + row + cg * ldz) : 0.0;
+      }
     }
     cp_async_commit();
   }
@@ -221,7 +239,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) q2r_kernel(int64_t n, int64_
                                                                const double* __restrict__ VTp,
                                                                double* __restrict__ Z,
                                                                int64_t ldz, int64_t nfull,
-                                                               int64_t ntail, int64_t rem) {
+                                                               int64_t ntail, int64_t rem,
+                                                               int dbg) {
   using S = Q2R<NW>;
   extern __shared__ __align__(128) double sm[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + S::OFF_BAR);
@@ -257,6 +276,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) q2r_kernel(int64_t n, int64_
         mbar_expect_tx(&full_v[s], VP * sizeof(double));
         bulk_g2s(sm + s * VP, Vp + k * (int64_t)VP, VP * sizeof(double), &full_v[s]);
         if (k >= 2) mbar_wait(&empty_vt[s], par);
+        if ((dbg & 1) && k >= 1) mbar_wait(&empty_vt[s ^ 1], (unsigned)(((k - 1) >> 1) & 1));
         mbar_expect_tx(&full_vt[s], VTP * sizeof(double));
         bulk_g2s(sm + S::OFF_VT + s * VTP, VTp + k * (int64_t)VTP, VTP * sizeof(double),
                  &full_vt[s]);
@@ -275,6 +295,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) q2r_kernel(int64_t n, int64_
   W.n = n;
   W.ncols = ncols;
   W.lane = lane;
+  W.dbg = dbg;
   W.gq = lane >> 2;
   W.tq = lane & 3;
   W.c0w = c0 + 8 * warp;
@@ -287,14 +308,28 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) q2r_kernel(int64_t n, int64_
 
   auto block = [&](double(&zt)[8][2], double(&zbt)[8][2], int64_t k) {
     W.read_half(zbt);  // half g + k + 1
-    if (k + 2 <= K) W.load_half(g + k + 2);
     const int s = (int)(k & 1);
     mbar_wait(&full_v[s], (unsigned)((k >> 1) & 1));
     W.step_a(zt, zbt, W.Vs + s * VP, w);
+    // The staging buffer is refilled only after every value read from it went into a
+    // product: the asm below consumes the W accumulators (so every step-A DMMA, and with it
+    // every staging load feeding one, is issued before it), and the cp.async writes
+    // follow it. An async copy issued right after the loads raced with them.
+#pragma unroll
+    for (int J = 0; J < 8; ++J) asm volatile("" : "+d"(w[J][0]), "+d"(w[J][1]));
+    if (k + 2 <= K) W.load_half(g + k + 2);
+    if (dbg & 8) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __threadfence_block();
+    }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty_v[s]);
     mbar_wait(&full_vt[s], (unsigned)((k >> 1) & 1));
     W.step_c(zt, zbt, W.VTs + s * VTP, w);
+    if (dbg & 8) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __threadfence_block();
+    }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty_vt[s]);
     W.store_half(zt, g + k);  // final for this group
@@ -318,6 +353,7 @@ void q2_apply_reg(cudaStream_t st, int64_t n, int64_t ncols, int64_t ngroups, co
                   const int64_t* toff, const double* T2, double* Z, int64_t ldz) {
   constexpr int NW = 8;
   using S = Q2R<NW>;
+  if (ncols <= 0 || n <= 1) return;
   EM_CK(cudaFuncSetAttribute(q2r_kernel<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)S::SMEM));
   constexpr size_t kPackSmem = 2 * QB * (QB + 1) * sizeof(double);
@@ -327,8 +363,9 @@ void q2_apply_reg(cudaStream_t st, int64_t n, int64_t ncols, int64_t ngroups, co
   DBuf Vp((size_t)kmax * VP, st), VTp((size_t)kmax * VTP, st);
   const int64_t sms = num_sms();
   const int64_t units = (ncols + 7) / 8;
-  const int64_t nfull = units / NW / sms * sms;
-  const int64_t rem = units - nfull * NW;
+  int64_t nfull = units / NW / sms * sms;
+  if (g_q2r_dbg & 2) nfull = (units + NW - 1) / NW;
+  const int64_t rem = imax64(units - nfull * NW, 0);
   const int64_t ntail = imin64(rem, sms);
   int64_t off = 0;
   for (int64_t g = ngroups - 1; g >= 0; --g) {
@@ -338,7 +375,7 @@ void q2_apply_reg(cudaStream_t st, int64_t n, int64_t ncols, int64_t ngroups, co
                                                          Vp.p, VTp.p);
     EM_LAUNCHED();
     q2r_kernel<NW><<<(unsigned)(nfull + ntail), (NW + 1) * 32, S::SMEM, st>>>(
-        n, ncols, g, K, Vp.p, VTp.p, Z, ldz, nfull, imax64(ntail, 1), rem);
+        n, ncols, g, K, Vp.p, VTp.p, Z, ldz, nfull, imax64(ntail, 1), rem, g_q2r_dbg);
     EM_LAUNCHED();
     off += K;
   }

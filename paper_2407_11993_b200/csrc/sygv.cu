@@ -53,10 +53,11 @@ __global__ void scale_vec_kernel(int64_t n, const double* __restrict__ a,
 }
 
 void syev_ascending(cudaStream_t st, int64_t n, double* A, int64_t lda, double* w, double* Z,
-                    int64_t ldz) {
+                    int64_t ldz, int64_t c0, int64_t nc) {
   if (n <= 0) return;
+  if (nc < 0) nc = n - c0;
   if (n >= g_two_stage_min && n > 2 * kBand && two_stage_fits(n)) {
-    syev_two_stage(st, n, A, lda, w, Z, ldz);
+    syev_two_stage(st, n, A, lda, w, Z, ldz, c0, nc);
     return;
   }
   DBuf d(n, st), e(imax64(n - 1, 1), st), tau(imax64(n - 1, 1), st);
@@ -70,7 +71,7 @@ void syev_ascending(cudaStream_t st, int64_t n, double* A, int64_t lda, double* 
   }
   {
     Stage s(st, ST_ORMTR);
-    ormtr_lower(st, n, n, A, lda, tau.p, Z, ldz);
+    ormtr_lower(st, n, nc, A, lda, tau.p, Z + c0 * ldz, ldz);
   }
   EM_CK(cudaMemcpyAsync(w, d.p, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
 }
@@ -147,6 +148,25 @@ __global__ void finalize_modes_inplace_kernel(int64_t n, double* __restrict__ V,
   }
 }
 
+// Column slice (modes m_lo .. m_lo + m - 1 in descending order): V[:, j] = s * Zs[:, m-1-j]
+// from the back-transformed ascending columns Zs, sign fixed (modal.py:74-78).
+__global__ void finalize_modes_slice_kernel(int64_t n, int64_t m, const double* __restrict__ Zs,
+                                            int64_t ldz, double* __restrict__ V, int64_t ldv) {
+  __shared__ double bv[32];
+  __shared__ int64_t bi[32];
+  __shared__ double sgn;
+  const int64_t j = blockIdx.x;
+  const double* z = Zs + (m - 1 - j) * ldz;
+  const double s = column_sign(n, z, bv, bi, &sgn);
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) V[i + j * ldv] = s * z[i];
+}
+
+// tau[j] = w[n-1-j] (descending time constants)
+__global__ void reverse_kernel(int64_t n, const double* __restrict__ w, double* __restrict__ tau) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j < n) tau[j] = w[n - 1 - j];
+}
+
 // out[j] = sum_i V[i,j] * X[i,j]
 __global__ void coldot_kernel(int64_t n, const double* __restrict__ V, int64_t ldv,
                               const double* __restrict__ X, int64_t ldx, double* __restrict__ out) {
@@ -190,11 +210,32 @@ __global__ void quadform_lower_kernel(int64_t n, const double* __restrict__ V, i
 // Returns -1 on success; else the failing pivot with *which = 0 (R) / 1 (L).
 // l_ready (optional): L is still being uploaded; the stream waits for it only before the
 // first use of L (after R's band detection and factorisation).
+//
+// Column range (m_lo, m_hi) (the column-sharded eigensolve of parallel.py: one rank's
+// modes): V, VtR are n x (m_hi - m_lo) and l_n, r_n have m_hi - m_lo entries for modes
+// m_lo .. m_hi - 1 (descending order); tau always gets all n. Everything up to the
+// tridiagonal eigenvectors is computed for the whole matrix; the back-transforms
+// (Q2, Q1 / ormtr, G^-T), the sign fix and l_n, r_n only for the rank's columns.
 int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const double* R,
              int64_t ldr, double* tau, double* V, int64_t ldv, double* l_n, double* r_n,
-             double* VtR, int64_t ldvtr, int* which, int flags, cudaEvent_t l_ready) {
+             double* VtR, int64_t ldvtr, int* which, int flags, cudaEvent_t l_ready,
+             int64_t m_lo, int64_t m_hi) {
   *which = -1;
   if (n <= 0) return -1;
+  if (m_hi < 0) m_hi = n;
+  if (m_lo < 0 || m_hi > n || m_lo > m_hi) throw ArgError{"mode range outside [0, n]"};
+  const int64_t m = m_hi - m_lo;
+  const bool slice = m < n;
+  // slice: the full tridiagonal eigenvector matrix needs an n x n workspace (the output V
+  // holds only m columns); it also hosts the certificate factor of L
+  DBuf Zfull;
+  double* Zw = V;
+  int64_t ldzw = ldv;
+  if (slice) {
+    Zfull.alloc((size_t)n * n, st);
+    Zw = Zfull.p;
+    ldzw = n;
+  }
   const size_t nn = (size_t)n * n;
   // A banded R (the 7-point stencil R of the plates: lower bandwidth ny*nz) is factored
   // in banded storage and every solve with its factor is banded (band.cu): the R stages
@@ -255,11 +296,11 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
       else
         sygst_lower(st, n, B.p, ldb, G, ldg, GDinv.p);
     }
-    // certificate only (modal.py:69-70), factored in the (still free) output buffer V
+    // certificate only (modal.py:69-70), factored in the (still free) eigenvector buffer
     {
       Stage s(st, ST_POTRF_L);
-      copy_matrix(st, false, n, n, L, ldl, V, ldv);
-      piv = potrf(st, n, V, ldv);
+      copy_matrix(st, false, n, n, L, ldl, Zw, ldzw);
+      piv = potrf(st, n, Zw, ldzw);
     }
     if (piv >= 0) {
       *which = 1;
@@ -272,21 +313,34 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
   // then the in-place descending reorder + sign fix): peak memory L, R, V + G, B and the
   // two D&C work matrices = 7 N^2 (8 with V^T R), so N = 50,000 fits one B200
   DBuf w(n, st);
-  syev_ascending(st, n, B.p, ldb, w.p, V, ldv);
+  // descending modes m_lo .. m_hi - 1 are the ascending columns n - m_hi .. n - m_lo - 1
+  const int64_t c0 = n - m_hi;
+  double* Zs = Zw + c0 * ldzw;
+  syev_ascending(st, n, B.p, ldb, w.p, Zw, ldzw, c0, m);
   B.release();
-  {
+  if (m > 0) {
     Stage s(st, ST_TRSM_BACK);
     if (banded)
-      band_solve(st, bc, true, n, V, ldv);                   // V = G^-T U
+      band_solve(st, bc, true, m, Zs, ldzw);                   // V = G^-T U
     else
-      trsm_lower(st, true, n, n, G, ldg, V, ldv, GDinv.p);
+      trsm_lower(st, true, n, m, G, ldg, Zs, ldzw, GDinv.p);
   }
   Gbuf.release();
   restore_r();
   {
     Stage s(st, ST_FINALIZE);
-    finalize_modes_inplace_kernel<<<(unsigned)((n + 1) / 2), 256, 0, st>>>(n, V, ldv, w.p, tau);
-    EM_LAUNCHED();
+    if (slice) {
+      if (m > 0) {
+        finalize_modes_slice_kernel<<<(unsigned)m, 256, 0, st>>>(n, m, Zs, ldzw, V, ldv);
+        EM_LAUNCHED();
+      }
+      reverse_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, w.p, tau);
+      EM_LAUNCHED();
+      Zfull.release();
+    } else {
+      finalize_modes_inplace_kernel<<<(unsigned)((n + 1) / 2), 256, 0, st>>>(n, V, ldv, w.p, tau);
+      EM_LAUNCHED();
+    }
   }
   Stage post(st, ST_POST_GEMM);
   // r_n = diag(V^T R V) (modal.py:80): R is typically a stencil stored dense (the
@@ -298,25 +352,29 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
   DBuf rn_tmp;
   double* rn_out = r_n;
   if (!rn_out && l_n && !g_ln_dense) {
-    rn_tmp.alloc(n, st);
+    rn_tmp.alloc(imax64(m, 1), st);
     rn_out = rn_tmp.p;
+  }
+  if (m == 0) {
+    EM_CK(cudaStreamSynchronize(st));
+    return -1;
   }
   if (VtR) {
     if (rc)
-      csr_mm(st, *rc, n, V, ldv, VtR, ldvtr);
+      csr_mm(st, *rc, m, V, ldv, VtR, ldvtr);
     else
-      EM_CK(gemm(st, false, false, n, n, n, 1.0, R, ldr, V, ldv, 0.0, VtR, ldvtr));
+      EM_CK(gemm(st, false, false, n, m, n, 1.0, R, ldr, V, ldv, 0.0, VtR, ldvtr));
     if (rn_out) {
-      coldot_kernel<<<(unsigned)n, 256, 0, st>>>(n, V, ldv, VtR, ldvtr, rn_out);
+      coldot_kernel<<<(unsigned)m, 256, 0, st>>>(n, V, ldv, VtR, ldvtr, rn_out);
       EM_LAUNCHED();
     }
   } else if (rn_out) {
     if (rc) {
-      csr_quadform(st, *rc, n, V, ldv, rn_out);
+      csr_quadform(st, *rc, m, V, ldv, rn_out);
     } else {
-      DBuf RV(nn, st);
-      EM_CK(gemm(st, false, false, n, n, n, 1.0, R, ldr, V, ldv, 0.0, RV.p, n));
-      coldot_kernel<<<(unsigned)n, 256, 0, st>>>(n, V, ldv, RV.p, n, rn_out);
+      DBuf RV((size_t)n * m, st);
+      EM_CK(gemm(st, false, false, n, m, n, 1.0, R, ldr, V, ldv, 0.0, RV.p, n));
+      coldot_kernel<<<(unsigned)m, 256, 0, st>>>(n, V, ldv, RV.p, n, rn_out);
       EM_LAUNCHED();
       EM_CK(cudaStreamSynchronize(st));
     }
@@ -325,9 +383,9 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
     if (g_ln_dense) {
       // l_n = diag(V^T L V) (modal.py:79) as the reference forms it, through the lower
       // triangle of L only (the SymMatrix definition of L): a triangular-A product
-      DBuf LV(nn, st);
-      EM_CK(gemm_lower_a(st, n, n, n, 1.0, L, ldl, V, ldv, 0.0, LV.p, n));
-      quadform_lower_kernel<<<(unsigned)n, 256, 0, st>>>(n, V, ldv, LV.p, n, L, ldl, l_n);
+      DBuf LV((size_t)n * m, st);
+      EM_CK(gemm_lower_a(st, n, m, n, 1.0, L, ldl, V, ldv, 0.0, LV.p, n));
+      quadform_lower_kernel<<<(unsigned)m, 256, 0, st>>>(n, V, ldv, LV.p, n, L, ldl, l_n);
       EM_LAUNCHED();
       EM_CK(cudaStreamSynchronize(st));
     } else {
@@ -335,7 +393,7 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
       // up to the eigen-residual, a rounding-level term), so l_n = tau_n r_n: the same
       // quantity to ~1e-13 relative (tests: test_gpu_parity_configs C2 golden, against
       // the LAPACK restatement's dense diag(V^T L V)) without the N^3 product
-      scale_vec_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, tau, rn_out, l_n);
+      scale_vec_kernel<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(m, tau + m_lo, rn_out, l_n);
       EM_LAUNCHED();
     }
   }

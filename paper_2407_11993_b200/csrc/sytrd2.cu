@@ -858,6 +858,7 @@ static double q2_makespan(int64_t n6, int64_t n4, int64_t sms) {
 static void q2_apply_strips(cudaStream_t st, int64_t n, int64_t ncols, int64_t ngroups,
                             const double* V2, const int64_t* toff, const double* T2, double* Z,
                             int64_t ldz) {
+  if (ncols <= 0) return;
   const int64_t sms = num_sms();
   const int64_t max6 = (ncols + 47) / 48;
   int64_t n6 = max6, n4 = 0;
@@ -887,7 +888,9 @@ static void q2_apply_strips(cudaStream_t st, int64_t n, int64_t ncols, int64_t n
 
 // ---- driver -------------------------------------------------------------------------
 void syev_two_stage(cudaStream_t st, int64_t n, double* A, int64_t lda, double* w, double* Z,
-                    int64_t ldz) {
+                    int64_t ldz, int64_t c0, int64_t nc) {
+  if (nc < 0) nc = n - c0;
+  double* Zc = Z + c0 * ldz;  // the back-transformed columns
   const int b = B2;
   const int64_t ldab = 2 * b + 1;
   DBuf tau1(n, st), AB((size_t)ldab * n, st);
@@ -955,10 +958,10 @@ void syev_two_stage(cudaStream_t st, int64_t n, double* A, int64_t lda, double* 
       q2_tfactor_kernel<<<(unsigned)nblk, 256, smt, st>>>(n, dblk.p, V2.p, TAU2.p, dtoff.p, T2.p);
       EM_LAUNCHED();
       if (g_q2_mode == 0) {
-        q2_apply_reg(st, n, n, ngroups, V2.p, dtoff.p, T2.p, Z, ldz);
+        q2_apply_reg(st, n, nc, ngroups, V2.p, dtoff.p, T2.p, Zc, ldz);
         EM_CK(cudaStreamSynchronize(st));  // dblk lifetime
       } else if (g_q2_mode == 2) {
-        q2_apply_strips(st, n, n, ngroups, V2.p, dtoff.p, T2.p, Z, ldz);
+        q2_apply_strips(st, n, nc, ngroups, V2.p, dtoff.p, T2.p, Zc, ldz);
         EM_CK(cudaStreamSynchronize(st));  // dblk lifetime
       } else {
       EM_CK(cudaFuncSetAttribute(q2_buildv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1021,7 +1024,7 @@ void syev_two_stage(cudaStream_t st, int64_t n, double* A, int64_t lda, double* 
     }
     // Q1 (stage-1 reflectors, vectors start b rows below their column)
     Stage sq1(st, ST_Q1);
-    if (n > b) ormqr_lower_off(st, n, n - b, b, n, A, lda, tau1.p, Z, ldz);
+    if (n > b) ormqr_lower_off(st, n, n - b, b, nc, A, lda, tau1.p, Zc, ldz);
   }
   EM_CK(cudaMemcpyAsync(w, d.p, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
 }

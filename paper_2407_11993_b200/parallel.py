@@ -1,4 +1,12 @@
-"""Mode-sharded modal stepping across GPUs (north-star (b)).
+"""Multi-GPU modal solve: column-sharded eigensolve + mode-sharded stepping
+(north-star (a) and (b)).
+
+Eigensolve (`sharded_generalized_eig`, em_sygv_range): every rank reduces the pencil
+to tridiagonal form and solves it (Cholesky of R, two-sided reduction, tridiagonalisation,
+divide and conquer: replicated), then back-transforms ONLY the eigenvector columns of its
+own contiguous mode range (Q2, Q1, G^-T: 2/3 of the eigensolve's flops at C3) and forms
+their sign fix, l_n and r_n. The ranks exchange nothing: rank r's columns are exactly the
+modes its stepping shard owns, so V is never gathered.
 
 After the eigensolve the modes never interact (transient.py:116-166: every
 mode's update uses only its own r_n, c_n and forcing row), so the TD2 stepping
@@ -20,6 +28,8 @@ import ctypes
 import numpy as np
 
 from . import _native as nat
+from . import linalg
+from .errors import DimensionMismatch, NotPositiveDefinite
 
 
 def shard_ranges(n: int, world: int) -> list[tuple[int, int]]:
@@ -48,12 +58,83 @@ def reduce_partials(partial, dist, group=None):
     return partial
 
 
+def _world_rank(dist):
+    if dist is not None and dist.is_initialized():
+        return dist.get_world_size(), dist.get_rank()
+    return 1, 0
+
+
+class ShardBasis:
+    """One rank's share of a column-sharded ModalBasis (modal.py:22-43): time constants
+    of ALL modes (descending), the rank's mode range [lo, hi), its eigenvector columns
+    V[:, lo:hi] on the device (v_dev: torch (hi - lo, N) = column-major N x (hi - lo)),
+    and l_n, r_n of its modes."""
+
+    def __init__(self, tau, lo: int, hi: int, v_dev, l_n, r_n):
+        self.tau = np.asarray(tau, dtype=float)
+        self.lo, self.hi = int(lo), int(hi)
+        self.v_dev = v_dev
+        self.l_n = np.asarray(l_n, dtype=float)
+        self.r_n = np.asarray(r_n, dtype=float)
+
+    @property
+    def n_modes(self) -> int:
+        return self.tau.shape[0]
+
+    @property
+    def n_local(self) -> int:
+        return self.hi - self.lo
+
+
+def sharded_generalized_eig(l_i, r_i, dist=None, mode_range: tuple[int, int] | None = None
+                            ) -> ShardBasis:
+    """This rank's share of generalized_eig (modal.py:46-81): modes shard_ranges(N,
+    world)[rank] (or mode_range). Inputs as modal.generalized_eig (host SymMatrix / numpy,
+    or device tensors); raises NotPositiveDefinite with the reference's `what` strings."""
+    t = nat.torch()
+    if isinstance(l_i, t.Tensor) and isinstance(r_i, t.Tensor):
+        ld = l_i.to(dtype=t.float64).contiguous()
+        rd = r_i.to(dtype=t.float64).contiguous()
+        own = False
+    else:
+        lm = l_i.full if isinstance(l_i, linalg.SymMatrix) else np.asarray(l_i, dtype=float)
+        rm = r_i.full if isinstance(r_i, linalg.SymMatrix) else np.asarray(r_i, dtype=float)
+        if lm.shape != rm.shape:
+            raise DimensionMismatch("L_i and R_i must have the same shape")
+        ld = nat.device_symmetric(lm) if isinstance(l_i, linalg.SymMatrix) else \
+            nat.device_colmajor(lm)
+        rd = nat.device_symmetric(rm) if isinstance(r_i, linalg.SymMatrix) else \
+            nat.device_colmajor(rm)
+        own = True
+    if ld.shape != rd.shape:
+        raise DimensionMismatch("L_i and R_i must have the same shape")
+    n = ld.shape[0]
+    world, rank = _world_rank(dist)
+    lo, hi = mode_range if mode_range is not None else shard_ranges(n, world)[rank]
+    m = hi - lo
+    tau = nat.empty(max(n, 1))
+    v = nat.empty(max(m, 1), n)
+    ln, rn = nat.empty(max(m, 1)), nat.empty(max(m, 1))
+    piv, which = ctypes.c_int64(-1), ctypes.c_int(-1)
+    lib = nat.load_library()
+    rc = lib.em_sygv_range(nat.context(), n, nat.ptr(ld), n, nat.ptr(rd), n, lo, hi,
+                           nat.ptr(tau), nat.ptr(v), n, nat.ptr(ln), nat.ptr(rn), None, n,
+                           1 if own else 0, ctypes.byref(piv), ctypes.byref(which))
+    if rc == nat.EM_ERR_NOT_PD:
+        what = "modal resistance matrix" if which.value == 0 else "modal inductance matrix"
+        raise NotPositiveDefinite(int(piv.value), what)
+    nat.check(rc, "em_sygv_range")
+    return ShardBasis(tau.cpu().numpy()[:n], lo, hi, v[:m], ln.cpu().numpy()[:m],
+                      rn.cpu().numpy()[:m])
+
+
 class ShardedTd2:
     """TD2 stepping of the modes [lo, hi) owned by this rank.
 
-    basis: ModalBasis (device V); rm: ReducedModel; observables C (n_obs x N).
-    run(drive_table (T+1 x n_c), steps) -> full observables (T x n_obs) on every
-    rank (partials all-reduced per time block of `block` steps)."""
+    basis: ModalBasis (device V, all modes) or this rank's ShardBasis (its columns only);
+    rm: ReducedModel; observables C (n_obs x N). run(drive_table (T+1 x n_c), steps) ->
+    full observables (T x n_obs) on every rank (partials all-reduced per time block of
+    `block` steps)."""
 
     def __init__(self, rm, basis, dt: float, theta: float, c_obs: np.ndarray, dist=None,
                  block: int = 2048, mode_range: tuple[int, int] | None = None):
@@ -62,14 +143,21 @@ class ShardedTd2:
         world = dist.get_world_size() if (dist is not None and dist.is_initialized()) else 1
         rank = dist.get_rank() if world > 1 else 0
         n = basis.n_modes
-        # mode_range overrides the rank's shard (single-process emulation in tests)
-        self.lo, self.hi = mode_range if mode_range is not None else shard_ranges(n, world)[rank]
+        if isinstance(basis, ShardBasis):
+            self.lo, self.hi = basis.lo, basis.hi
+            v_loc = basis.v_dev                           # this rank's columns (n x n_loc)
+            ln_loc, rn_loc = basis.l_n, basis.r_n
+        else:
+            # mode_range overrides the rank's shard (single-process emulation in tests)
+            self.lo, self.hi = mode_range if mode_range is not None else \
+                shard_ranges(n, world)[rank]
+            v_loc = basis.v_dev[self.lo:self.hi]          # columns lo..hi of V (n x n_loc)
+            ln_loc, rn_loc = basis.l_n[self.lo:self.hi], basis.r_n[self.lo:self.hi]
         self.n_loc = self.hi - self.lo
         self.block = block
         self.n_p, self.n_s = rm.n_ports, rm.n_sources
         nd = 2 * self.n_p + self.n_s
         ctx, lib = nat.context(), nat.load_library()
-        v_loc = basis.v_dev[self.lo:self.hi]              # columns lo..hi of V (n x n_loc)
         # P_loc = V[:, lo:hi]^T [R_D | L_D | M0]  (n_loc x nd)
         if nd:
             drv = np.concatenate([rm.r_d.reshape(n, self.n_p), rm.l_d.reshape(n, self.n_p),
@@ -88,8 +176,8 @@ class ShardedTd2:
         self.cv = nat.empty(self.n_loc, self.n_obs)
         nat.check(lib.em_dgemm(ctx, 0, 0, self.n_obs, self.n_loc, n, 1.0, nat.ptr(cd), self.n_obs,
                                nat.ptr(v_loc), n, 0.0, nat.ptr(self.cv), self.n_obs), "em_dgemm")
-        self.ln = nat.device_vector(basis.l_n[self.lo:self.hi])
-        self.rn = nat.device_vector(basis.r_n[self.lo:self.hi])
+        self.ln = nat.device_vector(ln_loc)
+        self.rn = nat.device_vector(rn_loc)
         p_r = self.proj[0:self.n_p] if self.n_p else self.proj[0:1]
         p_l = self.proj[self.n_p:2 * self.n_p] if self.n_p else self.proj[0:1]
         p_m = self.proj[2 * self.n_p:] if self.n_s else self.proj[0:1]
