@@ -384,32 +384,38 @@ class _LazyEye:
 
 
 # --------------------------------------------------------------------------- roofline
-def roofline(stages: dict, n: int, steps: int, n_theta: int, n_obs: int, peaks: dict) -> dict:
-    """Dominant stage of the step with its algorithmic work per launch."""
-    best = max(stages.items(), key=lambda kv: kv[1][0])
-    name, (ms, cnt) = best
-    per_launch_ms = ms / max(cnt, 1)
-    hbm = peaks.get("hbm_gbs", 6550.4)
+# algorithmic FP64 flop counts of the eigensolve stages at order n; the
+# two-stage pieces: sy2sb 4/3 n^3 (two-sided update), Q2 and Q1 back-transforms 2 n^3 each
+# (applying ~n^2/2 reflector entries to n columns, 4 flop per entry and column)
+def stage_flops(name, n):
+    return {"potrf_R": n ** 3 / 3, "potrf_L": n ** 3 / 3, "sygst": 2.0 * n ** 3,
+            "ormtr": 2.0 * n ** 3, "trsm_back": 1.0 * n ** 3, "sy2sb": 4.0 / 3.0 * n ** 3,
+            "q2_apply": 2.0 * n ** 3, "q1_apply": 2.0 * n ** 3}.get(name)
+
+
+def roofline(stages: dict, n: int, peaks: dict) -> dict:
+    """The dominant eigensolve stage (by time, per step) against the FP64 tensor peak, or
+    the one-stage sytrd against HBM."""
     fp64 = peaks.get("fp64_tflops", 37.1)
-    if name in ("sytrd", "sytrd_symv"):
+    hbm = peaks.get("hbm_gbs", 6550.4)
+    cands = {k: v for k, v in stages.items()
+             if stage_flops(k, n) is not None or k == "sytrd"}
+    if "q2_apply" in stages:  # two-stage: sytrd / ormtr are the sums of their pieces
+        cands.pop("sytrd", None)
+        cands.pop("ormtr", None)
+    if not cands:
+        return None
+    name, (ms, cnt) = max(cands.items(), key=lambda kv: kv[1][0])
+    if name == "sytrd":
         # lower-triangle symv over the trailing matrix per column: 8 * sum m^2/2 bytes
         byts = 8.0 * sum((n - c - 1) ** 2 / 2.0 for c in range(n))
-        if name == "sytrd_symv":
-            byts /= n
-        ach = byts / (per_launch_ms * 1e-3) / 1e9
+        ach = byts / (ms * 1e-3) / 1e9
         return dict(stage=name, bound="hbm", achieved=ach, peak=hbm, unit="GB/s",
-                    frac=ach / hbm, traffic=None, per_launch_ms=per_launch_ms, launches=cnt)
-    flops = {
-        "potrf_R": n ** 3 / 3, "potrf_L": n ** 3 / 3, "sygst": 2.0 * n ** 3,
-        "stedc": 4.0 / 3.0 * n ** 3, "ormtr": 2.0 * n ** 3, "trsm_back": 1.0 * n ** 3,
-        "post_gemm": 4.0 * n ** 3, "td2_replay": 2.0 * n_obs * n * steps,
-    }.get(name)
-    if flops is None:
-        return dict(stage=name, bound="tensor", achieved=None, peak=fp64, unit="TFLOP/s",
-                    frac=None, traffic=None, per_launch_ms=per_launch_ms, launches=cnt)
-    ach = flops / (per_launch_ms * 1e-3) / 1e12
+                    frac=ach / hbm, traffic=None, ms_per_step=ms, launches_per_step=cnt)
+    ach = stage_flops(name, n) / (ms * 1e-3) / 1e12
     return dict(stage=name, bound="tensor", achieved=ach, peak=fp64, unit="TFLOP/s",
-                frac=ach / fp64, traffic=None, per_launch_ms=per_launch_ms, launches=cnt)
+                frac=ach / fp64, traffic=None, ms_per_step=ms, launches_per_step=cnt,
+                algorithmic_flop=stage_flops(name, n))
 
 
 def symv_roofline(m, n, peaks, reps=20):
@@ -585,16 +591,22 @@ def run_ours(args, cfg, rank, world, local_rank):
     peaks = load_peaks()
     n_steps_timed = args.steps
     st_avg = {k: (v[0] / n_steps_timed, v[1] / n_steps_timed) for k, v in stages.items()}
-    # roofline of the dominant top-level stage (per launch = per step here)
-    top = {k: stages[k] for k in ("potrf_R", "sygst", "potrf_L", "sytrd", "stedc", "ormtr",
-                                  "trsm_back", "finalize", "post_gemm", "td2_local",
-                                  "td2_carry", "td2_replay") if k in stages}
-    stage_rl = roofline(top, n, T, nth, cfg["n_obs"], peaks) if top else None
-    if stage_rl and stage_rl["stage"] == "td2_replay":
-        stage_rl["achieved"] = None
-    rl = symv_roofline(m, n, peaks)
-    rl["stage"] = "sytrd"
-    rl["stage_roofline"] = stage_rl
+    # roofline of the dominant kernel: the largest eigensolve stage of the step (stage
+    # times are CUDA events on the launching stream, averaged per step)
+    rl = roofline(st_avg, n, peaks) or {}
+    q2prof = os.path.join(ROOT, "profiles", "r02", "ncu_q2r.json")
+    if rl.get("stage") == "q2_apply":
+        rl["kernel"] = ("q2r_kernel (+ q2r_pack_kernel, q2_tfactor_kernel): register-resident "
+                        "stage-2 back-transform, one launch per 64-sweep group")
+        rl["peak_source"] = "DMMA issue peak measured on this pool (profiles/r01_fp64_peaks.jsonl)"
+        if os.path.exists(q2prof):
+            pq = json.load(open(q2prof))
+            rl["traffic_per_launch"] = pq.get("dram_bytes")
+            rl["traffic_source"] = "profiles/r02/ncu_q2r.json (ncu --set full, one launch)"
+    if "sytrd" in st_avg and "q2_apply" not in st_avg:
+        # one-stage tridiagonalisation (below the two-stage threshold): its symv is the
+        # HBM-bound kernel, timed live at the full order
+        rl["symv"] = symv_roofline(m, n, peaks)
     # the modal stepping (north-star (b)): the fused replay is DMMA-bound on the observable
     # reconstruction, 2 n_obs flop per mode-step (nothing N x T reaches HBM)
     if "td2_replay" in stages:
@@ -630,8 +642,12 @@ def run_ours(args, cfg, rank, world, local_rank):
             "frac_dense_count": dense / (eig_ms * 1e-3) / 1e12 / fp64,
             "achieved_banded_count": banded / (eig_ms * 1e-3) / 1e12,
             "frac_banded_count": banded / (eig_ms * 1e-3) / 1e12 / fp64,
-            "note": "one-stage tridiagonalisation: its symv (4/3 N^3 bytes) is HBM-bound, "
-                    "so the eigensolve is not tensor-bound (DESIGN.md 3, 7)"}
+            "stages_ms": {k: round(st_avg[k][0], 1) for k in (
+                "potrf_R", "sygst", "potrf_L", "sy2sb", "sb2st", "stedc", "q2_apply",
+                "q1_apply", "sytrd", "ormtr", "trsm_back", "finalize", "post_gemm")
+                if k in st_avg},
+            "note": "dense count (17/3) N^3 is the one-stage LAPACK sequence with a dense R; "
+                    "the banded count uses R's band b = ny nz (SURVEY 8(d))"}
 
     # ---- TD1 comparator (bounded: a few hundred steps, extrapolated) and CPU baseline
     extra = {}

@@ -6,14 +6,18 @@
 // forward then backward substitution with the factor (tri_solve_vec,
 // _kernels.py:39-53), I += x.
 //
-// GPU form per step: b = E u^k - dt*R*I (CSR SpMV of the stencil R, or the lower-triangle
-// symv), then two PERSISTENT triangular-solve kernels. Block rows of 64 are claimed in
-// order from an atomic counter; a CTA streams the off-diagonal tiles of its block row as
-// soon as the producing block's flag (release/acquire, epoch-tagged) is up, reduces with
-// warp shuffles / shared memory and applies the pre-inverted 64x64 diagonal block. The
-// product with the neighbouring block's solution is folded into one precomputed 64x64
-// matrix (E_r = D_r C_{r,r-1}, F_r = D_r^T C_{r+1,r}^T), so a block's chain step is one
-// product. Each solve reads the factor once.
+// GPU form per step: one kernel forms b = E u^k - dt*R*I (CSR SpMV of the stencil R, or
+// the lower-triangle symv) and resets the solution vectors to a sentinel, then two
+// PERSISTENT triangular-solve kernels. Block rows of 64 are claimed in order from an
+// atomic counter; a CTA streams the off-diagonal tiles of its block row (the next tile is
+// in flight while the current one waits), reduces with warp shuffles / shared memory and
+// applies the pre-inverted 64x64 diagonal block. The product with the neighbouring
+// block's solution is folded into one precomputed 64x64 matrix (E_r = D_r C_{r,r-1},
+// F_r = D_r^T C_{r+1,r}^T), so a block's chain step is one product. There are no ready
+// flags: a solution entry is published by storing it over the sentinel (a NaN payload no
+// arithmetic produces; 64-bit stores are single-copy atomic), and a consumer polls the
+// entries it needs directly, so each link of the dependency chain is one L2 round trip
+// instead of flag acquire + data load + fenced release. Each solve reads the factor once.
 #include "common.cuh"
 #include "ctx.h"
 #include "gemm.h"
@@ -30,15 +34,10 @@ struct em_td1_plan {
   em::DBuf C, R, Dinv, DinvT, Ef, Fb, E, work, b, y, x;
   em::Csr Rs;          // R as CSR when it is sparse (the stencil): R I is an SpMV
   bool r_sparse = false;
-  em::DArr<unsigned long long>* flags = nullptr;
   em::DArr<unsigned int>* counters = nullptr;
-  unsigned long long epoch = 0;
   int n_obs = 0;
   em::DBuf Cobs, D;
-  ~em_td1_plan() {
-    delete flags;
-    delete counters;
-  }
+  ~em_td1_plan() { delete counters; }
 };
 
 namespace em {
@@ -83,64 +82,47 @@ __global__ void td1_e_kernel(int64_t n, int n_p, int n_s, double dt, double thet
   for (int s = 0; s < n_s; ++s) E[i + (int64_t)(2 * n_p + s) * n] = -m0[i + s * n];
 }
 
-// b = E u  (u = [i_d^k, di_d^k, di0^k] built from the drive table rows k, k+1)
-__global__ void td1_rhs_kernel(int64_t n, int n_p, int n_s, const double* __restrict__ E,
-                               const double* __restrict__ drive, int64_t k,
-                               double* __restrict__ b) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int n_c = n_p + n_s;
-  const double* d0 = drive + k * n_c;
-  const double* d1 = d0 + n_c;
-  double v = 0.0;
-  for (int p = 0; p < n_p; ++p) {
-    v = fma(E[i + p * n], d0[p], v);
-    v = fma(E[i + (int64_t)(n_p + p) * n], d1[p] - d0[p], v);
-  }
-  for (int s = 0; s < n_s; ++s) v = fma(E[i + (int64_t)(2 * n_p + s) * n], d1[n_p + s] - d0[n_p + s], v);
-  b[i] = v;
-}
+// Published solution entries replace this NaN payload (arithmetic only ever produces the
+// canonical NaN 0x7ff8000000000000).
+constexpr unsigned long long kSentinel = 0x7ff4dead00c0ffeeull;
 
-__global__ void td1_rhs_u_kernel(int64_t n, int n_u, const double* __restrict__ E,
-                                 const double* __restrict__ u, double* __restrict__ b) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  double v = 0.0;
-  for (int j = 0; j < n_u; ++j) v = fma(E[i + (int64_t)j * n], u[j], v);
-  b[i] = v;
-}
-
-EM_DEVINL unsigned long long ld_acquire(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+EM_DEVINL double ld_poll(const double* p) {
+  double v;
+  asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];\n" : "=d"(v) : "l"(p) : "memory");
   return v;
 }
-EM_DEVINL void st_release(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
+EM_DEVINL void st_pub(double* p, double v) {
+  asm volatile("st.relaxed.gpu.global.f64 [%0], %1;\n" ::"l"(p), "d"(v) : "memory");
 }
-
-// Wait until flags[j] == epoch for all j in [j0, j1]; returns once satisfied.
-EM_DEVINL void wait_flags(const unsigned long long* flags, int64_t j0, int64_t j1,
-                          unsigned long long epoch) {
-  if (threadIdx.x == 0) {
-    for (int64_t j = j0; j <= j1; ++j)
-      while (ld_acquire(flags + j) != epoch) __nanosleep(32);
+EM_DEVINL bool is_sentinel(double v) {
+  return (unsigned long long)__double_as_longlong(v) == kSentinel;
+}
+// the 16 entries p[0..15] once all are published
+EM_DEVINL void poll16(const double* p, double (&v)[16]) {
+#pragma unroll
+  for (int cc = 0; cc < 16; ++cc) v[cc] = ld_poll(p + cc);
+  while (true) {
+    bool ready = true;
+#pragma unroll
+    for (int cc = 0; cc < 16; ++cc) ready &= !is_sentinel(v[cc]);
+    if (ready) break;
+#pragma unroll
+    for (int cc = 0; cc < 16; ++cc)
+      if (is_sentinel(v[cc])) v[cc] = ld_poll(p + cc);
   }
-  __syncthreads();
 }
 
 // Forward solve C y = b, C lower (col-major, ld ldc). Block rows claimed in order.
 // y_r = D_r (b_r - sum_{j < r-1} C_rj y_j) - E_r y_{r-1} with E_r = D_r C_{r,r-1}
 // precomputed: everything but one 64 x 64 product waits only on blocks up to r-2, so the
-// dependency chain per block is: see y_{r-1}, one product, publish y_r.
+// dependency chain per block is: see y_{r-1}, one product, publish y_r. y must hold the
+// sentinel on entry (td1_pre_kernel).
 __global__ void __launch_bounds__(256) trsv_fwd_kernel(int64_t n, const double* __restrict__ C,
                                                        int64_t ldc, const double* __restrict__ Dinv,
                                                        const double* __restrict__ Ef,
                                                        const double* __restrict__ b,
                                                        double* __restrict__ y,
-                                                       unsigned long long* flags,
-                                                       unsigned int* counter,
-                                                       unsigned long long epoch) {
+                                                       unsigned int* counter) {
   __shared__ int64_t rblk;
   __shared__ double red[4][TS];
   __shared__ double part[TS];
@@ -177,11 +159,10 @@ __global__ void __launch_bounds__(256) trsv_fwd_kernel(int64_t n, const double* 
 #pragma unroll
         for (int cc = 0; cc < 16; ++cc) an[cc] = (row < n) ? C[row + (c1 + cc) * ldc] : 0.0;
       }
-      while (ld_acquire(flags + j) != epoch) {
-      }
-      const int64_t c0 = j * TS + ty * 16;
+      double yv[16];
+      poll16(y + j * TS + ty * 16, yv);
 #pragma unroll
-      for (int cc = 0; cc < 16; ++cc) acc = fma(a[cc], __ldcg(y + c0 + cc), acc);
+      for (int cc = 0; cc < 16; ++cc) acc = fma(a[cc], yv[cc], acc);
 #pragma unroll
       for (int cc = 0; cc < 16; ++cc) a[cc] = an[cc];
     }
@@ -200,34 +181,32 @@ __global__ void __launch_bounds__(256) trsv_fwd_kernel(int64_t n, const double* 
     // the chain: y_r = p_r - E_r y_{r-1}
     double se = 0.0;
     if (r > 0) {
-      while (ld_acquire(flags + r - 1) != epoch) {
-      }
-      const int64_t c0 = (r - 1) * TS + ty * 16;
       double yv[16];
-#pragma unroll
-      for (int cc = 0; cc < 16; ++cc) yv[cc] = __ldcg(y + c0 + cc);
+      poll16(y + (r - 1) * TS + ty * 16, yv);
 #pragma unroll
       for (int cc = 0; cc < 16; ++cc) se = fma(ev[cc], yv[cc], se);
     }
     __syncthreads();  // red: the p_r readers are done
     red[ty][tx] = se;
     __syncthreads();
-    if (tid < TS && r0 + tid < n)
-      y[r0 + tid] = pr - ((red[0][tid] + red[1][tid]) + (red[2][tid] + red[3][tid]));
-    // bar.sync orders the block's stores before thread 0's gpu-scope release (cumulative)
-    __syncthreads();
-    if (tid == 0) st_release(flags + r, epoch);
+    if (tid < TS) {
+      // rows past n (last block) publish 0 so the pollers of a full 16-entry group finish
+      const double v = r0 + tid < n
+                           ? pr - ((red[0][tid] + red[1][tid]) + (red[2][tid] + red[3][tid]))
+                           : 0.0;
+      st_pub(y + r0 + tid, v);
+    }
   }
 }
 
 // Backward solve C^T x = y; then I += x (and capture). Block rows claimed from the bottom.
 // x_r = DT_r (y_r - sum_{j > r+1} C_jr^T x_j) - F_r x_{r+1}, F_r = DT_r C_{r+1,r}^T
-// precomputed (DT_r = D_r^T): one 64 x 64 product on the dependency chain.
+// precomputed (DT_r = D_r^T): one 64 x 64 product on the dependency chain. x must hold the
+// sentinel on entry.
 __global__ void __launch_bounds__(256) trsv_bwd_kernel(
     int64_t n, const double* __restrict__ C, int64_t ldc, const double* __restrict__ Dinv,
     const double* __restrict__ Fb, const double* __restrict__ y, double* __restrict__ x,
-    double* __restrict__ I, double* __restrict__ Icap, unsigned long long* flags,
-    unsigned int* counter, unsigned long long epoch) {
+    double* __restrict__ I, double* __restrict__ Icap, unsigned int* counter) {
   __shared__ int64_t rblk;
   __shared__ double red[8][TS];
   __shared__ double part[TS];
@@ -270,10 +249,9 @@ __global__ void __launch_bounds__(256) trsv_bwd_kernel(
 #pragma unroll
         for (int cc = 0; cc < 16; ++cc) an[cc] = (rown < n) ? C[rown + (c0 + cc) * ldc] : 0.0;
       }
-      while (ld_acquire(flags + j) != epoch) {
-      }
       const int64_t rowj = j * TS + tx;
-      const double xv = (rowj < n) ? __ldcg(x + rowj) : 0.0;
+      double xv = ld_poll(x + rowj);  // rows past n are published as 0
+      while (is_sentinel(xv)) xv = ld_poll(x + rowj);
 #pragma unroll
       for (int cc = 0; cc < 16; ++cc) acc[cc] = fma(a[cc], xv, acc[cc]);
 #pragma unroll
@@ -304,29 +282,65 @@ __global__ void __launch_bounds__(256) trsv_bwd_kernel(
     // the chain: x_r = p_r - F_r x_{r+1}
     double sf = 0.0;
     if (has_next) {
-      while (ld_acquire(flags + r + 1) != epoch) {
-      }
-      const int64_t cn = (r + 1) * TS + ty * 16;
       double xn[16];
-#pragma unroll
-      for (int cc = 0; cc < 16; ++cc) xn[cc] = (cn + cc < n) ? __ldcg(x + cn + cc) : 0.0;
+      poll16(x + (r + 1) * TS + ty * 16, xn);
 #pragma unroll
       for (int cc = 0; cc < 16; ++cc) sf = fma(fv[cc], xn[cc], sf);
     }
     __syncthreads();  // red: the p_r readers are done
     red[ty][tx] = sf;
     __syncthreads();
-    if (tid < TS && r0 + tid < n) {
-      const double xv = pr - ((red[0][tid] + red[1][tid]) + (red[2][tid] + red[3][tid]));
-      x[r0 + tid] = xv;
-      const double iv = I[r0 + tid] + xv;
-      I[r0 + tid] = iv;
-      if (Icap) Icap[r0 + tid] = iv;
+    if (tid < TS) {
+      if (r0 + tid < n) {
+        const double xv = pr - ((red[0][tid] + red[1][tid]) + (red[2][tid] + red[3][tid]));
+        st_pub(x + r0 + tid, xv);
+        const double iv = I[r0 + tid] + xv;
+        I[r0 + tid] = iv;
+        if (Icap) Icap[r0 + tid] = iv;
+      } else {
+        st_pub(x + r0 + tid, 0.0);
+      }
     }
-    // bar.sync orders the block's stores before thread 0's gpu-scope release (cumulative)
-    __syncthreads();
-    if (tid == 0) st_release(flags + r, epoch);
   }
+}
+
+// b = E u - dt R I (u = [i_d^k, di_d^k, di0^k] from drive rows k, k+1, or u_dev when drive
+// is null); y, x <- sentinel for the step's two solves; the solves' row counters <- 0.
+__global__ void td1_pre_kernel(int64_t n, int64_t npad, int n_p, int n_s, int n_u,
+                               const double* __restrict__ E, const double* __restrict__ drive,
+                               int64_t k, const double* __restrict__ u_dev,
+                               const int64_t* __restrict__ rowptr, const int* __restrict__ colidx,
+                               const double* __restrict__ val, double dt,
+                               const double* __restrict__ I, double* __restrict__ b,
+                               double* __restrict__ y, double* __restrict__ x,
+                               unsigned int* counters) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i == 0) counters[0] = counters[1] = 0u;
+  if (i < npad) {
+    y[i] = __longlong_as_double((long long)kSentinel);
+    x[i] = __longlong_as_double((long long)kSentinel);
+  }
+  if (i >= n) return;
+  double v = 0.0;
+  if (drive) {
+    const int n_c = n_p + n_s;
+    const double* d0 = drive + k * n_c;
+    const double* d1 = d0 + n_c;
+    for (int p = 0; p < n_p; ++p) {
+      v = fma(E[i + p * n], d0[p], v);
+      v = fma(E[i + (int64_t)(n_p + p) * n], d1[p] - d0[p], v);
+    }
+    for (int s = 0; s < n_s; ++s)
+      v = fma(E[i + (int64_t)(2 * n_p + s) * n], d1[n_p + s] - d0[n_p + s], v);
+  } else {
+    for (int j = 0; j < n_u; ++j) v = fma(E[i + (int64_t)j * n], u_dev[j], v);
+  }
+  if (rowptr) {  // b -= dt R I, R's nonzeros in increasing column order
+    double s = 0.0;
+    for (int64_t p = rowptr[i]; p < rowptr[i + 1]; ++p) s += val[p] * I[colidx[p]];
+    v = fma(-dt, s, v);
+  }
+  b[i] = v;
 }
 
 int64_t td1_plan_init(em_td1_plan* P, const double* L, int64_t ldl, const double* R, int64_t ldr,
@@ -379,10 +393,8 @@ int64_t td1_plan_init(em_td1_plan* P, const double* L, int64_t ldl, const double
   }
   P->work.alloc(symv_work_size(n), st);
   P->b.alloc(n, st);
-  P->y.alloc(n, st);
-  P->x.alloc(n, st);
-  P->flags = new DArr<unsigned long long>(2 * nblk, st);
-  EM_CK(cudaMemsetAsync(P->flags->p, 0, 2 * nblk * sizeof(unsigned long long), st));
+  P->y.alloc((size_t)nblk * TS, st);  // padded to whole blocks: pollers read full groups
+  P->x.alloc((size_t)nblk * TS, st);
   P->counters = new DArr<unsigned int>(2, st);
   return -1;
 }
@@ -401,47 +413,41 @@ void td1_set_observables(em_td1_plan* P, int n_obs, const double* C, int64_t ldc
   }
 }
 
-// one step given b already holding the drive part; I in place; Icap column or null
-static void td1_solve_step(em_td1_plan* P, double* I, double* Icap_col) {
+// one step: b = E u - dt R I, forward and backward solve, I += x; Icap column or null.
+// drive (row k) or u_dev gives u.
+static void td1_solve_step(em_td1_plan* P, double* I, double* Icap_col, const double* drive,
+                           int64_t k, const double* u_dev) {
   cudaStream_t st = P->ctx->stream;
   const int64_t n = P->n;
   const int64_t nblk = (n + TS - 1) / TS;
-  // b += -dt R I
   {
     Stage s(st, ST_TD1_SYMV);
-    if (P->r_sparse)
-      csr_spmv(st, P->Rs, -P->dt, I, 1.0, P->b.p);
-    else
-      symv_lower(st, n, -P->dt, P->R.p, n, I, 1.0, P->b.p, P->work.p);
+    const bool fused_r = P->r_sparse;
+    td1_pre_kernel<<<(unsigned)((nblk * TS + 255) / 256), 256, 0, st>>>(
+        n, nblk * TS, P->n_p, P->n_s, P->n_u, P->E.p, P->n_u > 0 ? drive : nullptr, k,
+        P->n_u > 0 ? u_dev : nullptr, fused_r ? P->Rs.rowptr.p : nullptr,
+        fused_r ? P->Rs.colidx.p : nullptr, fused_r ? P->Rs.val.p : nullptr, P->dt, I, P->b.p,
+        P->y.p, P->x.p, P->counters->p);
+    EM_LAUNCHED();
+    if (!fused_r) symv_lower(st, n, -P->dt, P->R.p, n, I, 1.0, P->b.p, P->work.p);
   }
-  ++P->epoch;
-  EM_CK(cudaMemsetAsync(P->counters->p, 0, 2 * sizeof(unsigned int), st));
   const int grid = (int)imin64(nblk, 2 * num_sms());
   {
     Stage s(st, ST_TD1_FWD);
-    trsv_fwd_kernel<<<grid, 256, 0, st>>>(n, P->C.p, n, P->Dinv.p, P->Ef.p, P->b.p,
-                                                  P->y.p, P->flags->p, P->counters->p, P->epoch);
+    trsv_fwd_kernel<<<grid, 256, 0, st>>>(n, P->C.p, n, P->Dinv.p, P->Ef.p, P->b.p, P->y.p,
+                                          P->counters->p);
     EM_LAUNCHED();
   }
   {
     Stage s(st, ST_TD1_BWD);
-    trsv_bwd_kernel<<<grid, 256, 0, st>>>(n, P->C.p, n, P->DinvT.p, P->Fb.p, P->y.p,
-                                                  P->x.p, I, Icap_col, P->flags->p + nblk,
-                                                  P->counters->p + 1, P->epoch);
+    trsv_bwd_kernel<<<grid, 256, 0, st>>>(n, P->C.p, n, P->DinvT.p, P->Fb.p, P->y.p, P->x.p, I,
+                                          Icap_col, P->counters->p + 1);
     EM_LAUNCHED();
   }
 }
 
 void td1_step(em_td1_plan* P, double* I, const double* u_dev) {
-  cudaStream_t st = P->ctx->stream;
-  const int64_t n = P->n;
-  if (P->n_u > 0) {
-    td1_rhs_u_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, P->n_u, P->E.p, u_dev, P->b.p);
-    EM_LAUNCHED();
-  } else {
-    EM_CK(cudaMemsetAsync(P->b.p, 0, n * sizeof(double), st));
-  }
-  td1_solve_step(P, I, nullptr);
+  td1_solve_step(P, I, nullptr, nullptr, 0, u_dev);
 }
 
 void td1_run(em_td1_plan* P, int64_t T, const double* drive, double* I, double* Y, int64_t stride,
@@ -466,19 +472,12 @@ void td1_run(em_td1_plan* P, int64_t T, const double* drive, double* I, double* 
     chunk_start = upto;
   };
   for (int64_t k = 0; k < T; ++k) {
-    if (P->n_u > 0) {
-      td1_rhs_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, P->n_p, P->n_s, P->E.p,
-                                                                 drive, k, P->b.p);
-      EM_LAUNCHED();
-    } else {
-      EM_CK(cudaMemsetAsync(P->b.p, 0, n * sizeof(double), st));
-    }
     double* col = nullptr;
     const bool is_cap = ((k + 1) % stride) == 0;
     if (is_cap && (Icap || want_y)) {
       col = Icap ? Icap + cap * n : tmpcap.p + (cap - chunk_start) * n;
     }
-    td1_solve_step(P, I, col);
+    td1_solve_step(P, I, col, drive, k, nullptr);
     if (is_cap) {
       ++cap;
       if (!Icap && want_y && cap - chunk_start == chunk) flush(cap);

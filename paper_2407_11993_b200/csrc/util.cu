@@ -177,8 +177,15 @@ bool stages_enabled() { return g_stage_on; }
 
 int g_stage_level = 0;  // 1: top-level stages, 2: also per-call inner stages
 
+// stages recorded many times per call (per column, merge or panel): level 2 only; the
+// two-stage pieces (one event pair per eigensolve each) are top-level
+static bool inner_stage(int id) {
+  return id == ST_SYTRD_SYMV || id == ST_SYTRD_SYR2K || id == ST_STEDC_GEMM ||
+         id == ST_STEDC_SECULAR || id == ST_SY2SB_QR;
+}
+
 void stage_begin(cudaStream_t st, int id) {
-  if (!g_stage_on || (id >= ST_SYTRD_SYMV && g_stage_level < 2)) return;
+  if (!g_stage_on || (inner_stage(id) && g_stage_level < 2)) return;
   StageRec r{id, nullptr, nullptr};
   cudaEventCreate(&r.a);
   cudaEventCreate(&r.b);
