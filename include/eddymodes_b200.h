@@ -42,8 +42,16 @@ typedef struct em_td1_plan em_td1_plan;
 typedef struct em_fd_plan em_fd_plan;
 
 /* --- context --------------------------------------------------------------- */
+/* em_init keeps memory freed by the library cached in the device's default pool
+ * (stream-ordered allocator) between calls; em_trim releases it, em_finalize releases it
+ * and restores the pool's previous release threshold. */
 int em_init(int device, em_ctx** ctx);
 void em_finalize(em_ctx* ctx);
+int em_trim(em_ctx* ctx);
+/* Facts about the last call: EM_INFO_EIG_PATH = 1 one-stage (Householder sytrd), 2
+ * two-stage (band reduction + bulge chasing) tridiagonalisation in the last eigensolve. */
+#define EM_INFO_EIG_PATH 1
+int em_info(em_ctx* ctx, int key, int64_t* value);
 /* Order all work on an external CUDA stream (e.g. torch.cuda.current_stream());
  * NULL means the legacy default stream. em_init creates a private stream. */
 int em_set_stream(em_ctx* ctx, void* cuda_stream);
@@ -53,8 +61,9 @@ int64_t em_launch_count(const em_ctx* ctx);
 int em_synchronize(em_ctx* ctx);
 /* Tuning knobs. EM_CFG_TWO_STAGE_MIN: smallest n that uses the two-stage
  * (dense -> band -> tridiagonal) reduction in em_syev/em_sygv when its extra storage
- * (~1.6 n^2 doubles) is free on the device (default 40000; below it one-stage
- * Householder). */
+ * (2.5 n^2 doubles beyond the matrix and the eigenvectors at its divide-and-conquer peak,
+ * 3.5 when ldz != n) is free on the device (default 40000; below it one-stage
+ * Householder). em_info(EM_INFO_EIG_PATH) reports which path ran. */
 #define EM_CFG_TWO_STAGE_MIN 1
 /* EM_CFG_BAND_OFF: 1 = always factor R densely (default 0: a banded R, lower bandwidth
  * b with 4 (b + 128) <= n, takes the banded Cholesky and banded solves). */
@@ -152,10 +161,11 @@ int em_sygv_range(em_ctx* ctx, int64_t n, const double* L, int64_t ldl, double* 
                   double* r_n, double* VtR, int64_t ldvtr, int flags, int64_t* pivot,
                   int* which);
 /* em_sygv_ex with L still on the host: the library uploads L_host (n x n, leading
- * dimension n; pinned memory makes the copy asynchronous) into the device buffer L (ld
- * ldl) on a copy engine, after the work already queued on the context stream (e.g. R's
- * upload) and overlapped with R's band detection and Cholesky; L is first read by the
- * two-sided reduction. On return L holds the upload. */
+ * dimension n) into the device buffer L (ld ldl) on a copy engine, after the work already
+ * queued on the context stream (e.g. R's upload); L is first read by the two-sided
+ * reduction. With PINNED L_host the upload overlaps R's band detection and Cholesky;
+ * from pageable memory the copy completes before they are enqueued (no overlap). On
+ * return L holds the upload. */
 int em_sygv_lh(em_ctx* ctx, int64_t n, const double* L_host, double* L, int64_t ldl, double* R,
                int64_t ldr, double* tau, double* V, int64_t ldv, double* l_n, double* r_n,
                double* VtR, int64_t ldvtr, int flags, int64_t* pivot, int* which);

@@ -30,6 +30,8 @@ _D = ctypes.c_double
 SIGNATURES = {
     "em_init": (_I, [_I, ctypes.POINTER(_P)]),
     "em_finalize": (None, [_P]),
+    "em_trim": (_I, [_P]),
+    "em_info": (_I, [_P, _I, ctypes.POINTER(_I64)]),
     "em_set_stream": (_I, [_P, _P]),
     "em_last_error": (ctypes.c_char_p, [_P]),
     "em_launch_count": (_I64, [_P]),
@@ -174,6 +176,18 @@ def set_two_stage_min(n: int) -> None:
     """Smallest order that uses the two-stage tridiagonalisation (library default
     TWO_STAGE_MIN_DEFAULT, and only when its extra storage fits on the device)."""
     check(load_library().em_config(context(), EM_CFG_TWO_STAGE_MIN, int(n)), "em_config")
+
+
+def trim() -> None:
+    """Release the device memory the library keeps cached between calls (em_trim)."""
+    check(load_library().em_trim(context()), "em_trim")
+
+
+def last_eig_path() -> int:
+    """1 = one-stage, 2 = two-stage tridiagonalisation in the last eigensolve (em_info)."""
+    v = ctypes.c_int64(0)
+    check(load_library().em_info(context(), 1, ctypes.byref(v)), "em_info")
+    return int(v.value)
 
 
 def synchronize() -> None:

@@ -19,6 +19,7 @@ extern int g_sytrd_dbg;
 extern int g_band_off;
 extern int g_ln_dense;
 extern int g_q2r_dbg;
+extern int g_last_eig_path;
 extern int g_q2_mode;
 extern int g_symv_align_off;
 extern int64_t g_symv_keep_mb;
@@ -79,11 +80,16 @@ int em_init(int device, em_ctx** out) {
   }
   ctx->own_stream = true;
   ctx->sms = em::num_sms();
-  // keep freed pool memory cached between calls (stream-ordered allocator)
+  // keep freed pool memory cached between calls (stream-ordered allocator); the previous
+  // threshold comes back and the cache is released in em_finalize (em_trim releases it
+  // on demand)
   cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess &&
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &ctx->saved_threshold) ==
+          cudaSuccess) {
     uint64_t thr = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    ctx->pool_set =
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr) == cudaSuccess;
   }
   *out = ctx;
   return EM_OK;
@@ -92,11 +98,34 @@ int em_init(int device, em_ctx** out) {
 void em_finalize(em_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
-  if (ctx->own_stream && ctx->stream) {
-    cudaStreamSynchronize(ctx->stream);
-    cudaStreamDestroy(ctx->stream);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  cudaMemPool_t pool;
+  if (ctx->pool_set && cudaDeviceGetDefaultMemPool(&pool, ctx->device) == cudaSuccess) {
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &ctx->saved_threshold);
+    cudaMemPoolTrimTo(pool, 0);
   }
   delete ctx;
+}
+
+int em_trim(em_ctx* ctx) {
+  if (!ctx) return EM_ERR_ARG;
+  return guarded(ctx, [&] {
+    EM_CK(cudaStreamSynchronize(ctx->stream));
+    cudaMemPool_t pool;
+    EM_CK(cudaDeviceGetDefaultMemPool(&pool, ctx->device));
+    EM_CK(cudaMemPoolTrimTo(pool, 0));
+    return EM_OK;
+  });
+}
+
+int em_info(em_ctx* ctx, int key, int64_t* value) {
+  if (!ctx || !value) return EM_ERR_ARG;
+  if (key == EM_INFO_EIG_PATH) {
+    *value = em::g_last_eig_path;
+    return EM_OK;
+  }
+  return EM_ERR_ARG;
 }
 
 int em_set_stream(em_ctx* ctx, void* s) {

@@ -17,6 +17,8 @@ struct em_ctx {
   bool own_stream = false;
   std::string err;
   int sms = 148;
+  bool pool_set = false;            // em_init raised the default pool's release threshold
+  uint64_t saved_threshold = 0;     // ... from this value (restored by em_finalize)
 };
 
 namespace em {

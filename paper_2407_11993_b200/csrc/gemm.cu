@@ -17,7 +17,7 @@
 namespace em {
 
 // tile configuration (em_config debug key 96): 0 = CfgT3 for transposed A, else CfgT;
-// 2 = CfgT, 3 = CfgS, 4 = CfgT3 (A/B). In the C2
+// 2 = CfgT, 3 = CfgS, 4 = CfgT3, 5 = paired-fragment tiles (gemm_tile_pf) (A/B). In the C2
 // step CfgT everywhere beats the shape rule "CfgS for long k" that the isolated probes
 // suggested (2113 -> 2103 ms: ormtr 326 -> 322, l_n product 160 -> 154)
 int64_t g_gemm_cfg = 0;
@@ -49,21 +49,31 @@ using CfgT = GCfg<64, 64, 4, 4, 4>;
 using CfgT3 = GCfg<64, 64, 4, 4, 3>;  // three CTAs per SM (up to 168 registers)
 constexpr int GBM = 128;  // m tile of both configurations (split-K / grouped bookkeeping)
 
-template <int TA, class C>
+// Strides of the "paired fragment" tiles (PF, 16-byte operands): every thread loads the
+// fragments of two consecutive k-steps (k-contiguous tiles) or of two 8-row fragments
+// (m/n-contiguous tiles) with ONE 16-byte shared load. The k order inside a 8-deep k pair
+// is permuted to k = 8q + 2t + e (k-step 2q + e, lane t) on both operands, and the rows /
+// columns of a fragment pair are interleaved (fragment 2p + e, lane g: row 16p + 2g + e).
+// Bank-conflict free for these strides: 24 doubles for k-contiguous tiles, 66 for m/n.
+constexpr int PF_K = 24;
+
+template <int TA, class C, int PF = 0>
 struct ATile {
-  static constexpr int size = TA ? C::M * SPAD_K : GBK * C::SPM;
-  EM_DEVINL static int idx(int m, int k) { return TA ? m * SPAD_K + k : k * C::SPM + m; }
+  static constexpr int SK = PF ? PF_K : SPAD_K, SM = PF ? C::M + 2 : C::SPM;
+  static constexpr int size = TA ? C::M * SK : GBK * SM;
+  EM_DEVINL static int idx(int m, int k) { return TA ? m * SK + k : k * SM + m; }
 };
-template <int TB, class C>
+template <int TB, class C, int PF = 0>
 struct BTile {
-  static constexpr int size = TB ? GBK * C::SPN : C::N * SPAD_K;
-  EM_DEVINL static int idx(int k, int n) { return TB ? k * C::SPN + n : n * SPAD_K + k; }
+  static constexpr int SK = PF ? PF_K : SPAD_K, SN = PF ? C::N + 2 : C::SPN;
+  static constexpr int size = TB ? GBK * SN : C::N * SK;
+  EM_DEVINL static int idx(int k, int n) { return TB ? k * SN + n : n * SK + k; }
 };
 
 // Pipeline depth: 4 stages when all MINB CTAs still fit in shared memory, else 3.
-template <int TA, int TB, class C>
+template <int TA, int TB, class C, int PF = 0>
 constexpr int gstages() {
-  constexpr int per = (ATile<TA, C>::size + BTile<TB, C>::size) * 8;
+  constexpr int per = (ATile<TA, C, PF>::size + BTile<TB, C, PF>::size) * 8;
   return C::MINB_ >= 3 ? (per * 4 * C::MINB_ <= 220 * 1024 ? 4 : 3)
                        : (per * 4 * C::MINB_ <= 226 * 1024 ? 4 : 3);
 }
@@ -72,11 +82,12 @@ constexpr int gstages() {
 // TRANS == 0: X stored long-contiguous (X[l + k*ld]); TRANS == 1: k-contiguous (X[k + l*ld]).
 // AL: X is lower triangular (element (l, k) used only when k <= l; the stored upper
 // part is ignored) — VEC == 1 only.
-template <int TRANS, int VEC, int LONG, int AL = 0, int NT = GTHREADS>
+template <int TRANS, int VEC, int LONG, int AL = 0, int NT = GTHREADS, int PF = 0>
 EM_DEVINL void load_slab(double* s, const double* __restrict__ X, int64_t ld, int64_t l0,
                          int64_t k0, int64_t L, int64_t K, int tid) {
   static_assert(!AL || (VEC == 1 && TRANS == 0), "lower-A loads are 8-byte, long-contiguous");
-  constexpr int SPL = LONG + 4;
+  constexpr int SPL = PF ? LONG + 2 : LONG + 4;
+  constexpr int SKK = PF ? PF_K : SPAD_K;
   if (!TRANS) {
     // contiguous along l; smem [k][l] stride SPL
     constexpr int CH = LONG * GBK / VEC;
@@ -103,7 +114,7 @@ EM_DEVINL void load_slab(double* s, const double* __restrict__ X, int64_t ld, in
       int l = c / (GBK / VEC);
       int kk = (c % (GBK / VEC)) * VEC;
       int64_t gl = l0 + l, gk = k0 + kk;
-      double* dst = s + l * SPAD_K + kk;
+      double* dst = s + l * SKK + kk;
       if (VEC == 2) {
         int nv = (gl < L) ? (int)imin64(imax64(K - gk, 0), 2) : 0;
         const double* src = nv ? X + gk + gl * ld : X;
@@ -229,6 +240,131 @@ EM_DEVINL void gemm_tile(const GemmArgs& p, int64_t m0, int64_t n0, double* smem
   }
 }
 
+// gemm_tile with paired fragments (16-byte operands only): half the shared-memory load
+// instructions of gemm_tile for the same bytes (see PF_K above).
+template <int TA, int TB, int LOWER, class C>
+EM_DEVINL void gemm_tile_pf(const GemmArgs& p, int64_t m0, int64_t n0, double* smem) {
+  constexpr int WGM = C::WGM, WTM = C::WTM, WTN = C::WTN, GBN = C::N;
+  static_assert(WTM % 2 == 0 && WTN % 2 == 0, "fragment pairs");
+  using AT = ATile<TA, C, 1>;
+  using BT = BTile<TB, C, 1>;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp % WGM, wn = warp / WGM;
+  constexpr int ASZ = AT::size, BSZ = BT::size;
+  constexpr int GSTAGES = gstages<TA, TB, C, 1>();
+  double* As = smem;
+  double* Bs = smem + GSTAGES * ASZ;
+  double acc[WTM][WTN][2];
+#pragma unroll
+  for (int i = 0; i < WTM; ++i)
+#pragma unroll
+    for (int j = 0; j < WTN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const int64_t nk = (p.k + GBK - 1) / GBK;
+#pragma unroll
+  for (int s2 = 0; s2 < GSTAGES - 1; ++s2) {
+    if (s2 < nk) {
+      load_slab<TA, 2, C::M, 0, C::THREADS, 1>(As + s2 * ASZ, p.A, p.lda, m0, s2 * GBK, p.m, p.k, tid);
+      load_slab<!TB, 2, GBN, 0, C::THREADS, 1>(Bs + s2 * BSZ, p.B, p.ldb, n0, s2 * GBK, p.n, p.k, tid);
+    }
+    cp_async_commit();
+  }
+  const int mb = wm * 8 * WTM, nb = wn * 8 * WTN;
+  for (int64_t kt = 0; kt < nk; ++kt) {
+    cp_async_wait<GSTAGES - 2>();
+    __syncthreads();
+    {
+      const int64_t kn = kt + GSTAGES - 1;
+      const int sb = (int)(kn % GSTAGES);
+      if (kn < nk) {
+        load_slab<TA, 2, C::M, 0, C::THREADS, 1>(As + sb * ASZ, p.A, p.lda, m0, kn * GBK, p.m, p.k, tid);
+        load_slab<!TB, 2, GBN, 0, C::THREADS, 1>(Bs + sb * BSZ, p.B, p.ldb, n0, kn * GBK, p.n, p.k, tid);
+      }
+      cp_async_commit();
+    }
+    const double* as = As + (kt % GSTAGES) * ASZ;
+    const double* bs = Bs + (kt % GSTAGES) * BSZ;
+#pragma unroll
+    for (int q = 0; q < GBK / 8; ++q) {
+      double af[2][WTM], bf[2][WTN];
+      if (TA == 0) {  // [k][m]: one load = rows 16p + 2g, +1 of one k-step
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+#pragma unroll
+          for (int pp = 0; pp < WTM / 2; ++pp) {
+            const double2 v = *reinterpret_cast<const double2*>(
+                as + AT::idx(mb + 16 * pp + 2 * g, 8 * q + 2 * t + e));
+            af[e][2 * pp] = v.x;
+            af[e][2 * pp + 1] = v.y;
+          }
+      } else {  // [m][k]: one load = k-steps 2q, 2q+1 of one fragment
+#pragma unroll
+        for (int i = 0; i < WTM; ++i) {
+          const double2 v =
+              *reinterpret_cast<const double2*>(as + AT::idx(mb + 8 * i + g, 8 * q + 2 * t));
+          af[0][i] = v.x;
+          af[1][i] = v.y;
+        }
+      }
+      if (TB == 0) {  // [n][k]
+#pragma unroll
+        for (int j = 0; j < WTN; ++j) {
+          const double2 v =
+              *reinterpret_cast<const double2*>(bs + BT::idx(8 * q + 2 * t, nb + 8 * j + g));
+          bf[0][j] = v.x;
+          bf[1][j] = v.y;
+        }
+      } else {  // [k][n]: one load = columns 16p + 2g, +1 of one k-step
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+#pragma unroll
+          for (int pp = 0; pp < WTN / 2; ++pp) {
+            const double2 v = *reinterpret_cast<const double2*>(
+                bs + BT::idx(8 * q + 2 * t + e, nb + 16 * pp + 2 * g));
+            bf[e][2 * pp] = v.x;
+            bf[e][2 * pp + 1] = v.y;
+          }
+      }
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+#pragma unroll
+        for (int i = 0; i < WTM; ++i)
+#pragma unroll
+          for (int j = 0; j < WTN; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[e][i], bf[e][j]);
+    }
+  }
+  cp_async_wait<0>();
+  // epilogue (rows / columns of the interleaved fragment pairs)
+  double* __restrict__ Cr = p.C;
+  const bool has_beta = p.beta != 0.0;
+#pragma unroll
+  for (int i = 0; i < WTM; ++i) {
+    const int64_t row = m0 + mb + (TA == 0 ? 16 * (i >> 1) + 2 * g + (i & 1) : 8 * i + g);
+    double cv[WTN][2];
+    bool ok[WTN][2];
+#pragma unroll
+    for (int j = 0; j < WTN; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t col =
+            n0 + nb + (TB == 1 ? 16 * (j >> 1) + 2 * (2 * t + e) + (j & 1) : 8 * j + 2 * t + e);
+        ok[j][e] = row < p.m && col < p.n && !(LOWER && row + p.diag_off < col);
+        cv[j][e] = (has_beta && ok[j][e]) ? Cr[row + col * p.ldc] : 0.0;
+      }
+#pragma unroll
+    for (int j = 0; j < WTN; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        if (!ok[j][e]) continue;
+        const int64_t col =
+            n0 + nb + (TB == 1 ? 16 * (j >> 1) + 2 * (2 * t + e) + (j & 1) : 8 * j + 2 * t + e);
+        const double v = p.alpha * acc[i][j][e];
+        Cr[row + col * p.ldc] = has_beta ? fma(p.beta, cv[j][e], v) : v;
+      }
+  }
+}
+
 template <int TA, int TB, int LOWER, int VEC, int AL = 0, class C = CfgS>
 __global__ void __launch_bounds__(C::THREADS, C::MINB_) gemm_kernel(GemmArgs p, double* ws, int64_t kc) {
   constexpr int GBN = C::N;
@@ -259,7 +395,10 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB_) gemm_kernel(GemmArgs p, 
   const int64_t tn = (bid % per_group) / gsz;
   const int64_t m0 = tm * C::M, n0 = tn * GBN;
   if (LOWER && m0 + C::M - 1 + p.diag_off < n0) return;  // tile strictly above the diagonal
-  gemm_tile<TA, TB, LOWER, VEC, AL, C>(p, m0, n0, smem);
+  if constexpr (VEC == 3)
+    gemm_tile_pf<TA, TB, LOWER, C>(p, m0, n0, smem);
+  else
+    gemm_tile<TA, TB, LOWER, VEC, AL, C>(p, m0, n0, smem);
 }
 
 // Grouped launch: blockIdx.y selects a problem; problems carry their own sizes/pointers.
@@ -285,9 +424,10 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB_) gemm_grouped_kernel(
   }
 }
 
-template <int TA, int TB, class C = CfgS>
+template <int TA, int TB, class C = CfgS, int PF = 0>
 static size_t smem_bytes_t() {
-  return (size_t)(ATile<TA, C>::size + BTile<TB, C>::size) * gstages<TA, TB, C>() * sizeof(double);
+  return (size_t)(ATile<TA, C, PF>::size + BTile<TB, C, PF>::size) * gstages<TA, TB, C, PF>() *
+         sizeof(double);
 }
 
 // C = alpha * sum_z W_z + beta * C  (split-K reduction, fixed order)
@@ -309,7 +449,7 @@ __global__ void splitk_reduce_kernel(int64_t m, int64_t n, int splits, const dou
 template <int TA, int TB, int LOWER, int VEC, class C>
 static cudaError_t launch_t(const GemmArgs& p, cudaStream_t st) {
   auto k = gemm_kernel<TA, TB, LOWER, VEC, 0, C>;
-  size_t sm = smem_bytes_t<TA, TB, C>();
+  size_t sm = smem_bytes_t<TA, TB, C, VEC == 3 ? 1 : 0>();
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -366,6 +506,8 @@ static cudaError_t launch_v(const GemmArgs& p, cudaStream_t st) {
   // tiles start at multiples of 128 (long dims) and 16 (k), so base alignment suffices.
   // transposed A: three CTAs per SM (more registers) measured faster (V^T Z at K = 16k:
   // 29.6 -> 31.6 TF/s, rank-256 A^T B 28.1 -> 30.3); non-transposed A: four
+  if (g_gemm_cfg == 5 && vec)  // paired-fragment tiles
+    return TA ? launch_t<TA, TB, LOWER, 3, CfgT3>(p, st) : launch_t<TA, TB, LOWER, 3, CfgT>(p, st);
   if (g_gemm_cfg == 4 || (g_gemm_cfg == 0 && TA))
     return vec ? launch_t<TA, TB, LOWER, 2, CfgT3>(p, st) : launch_t<TA, TB, LOWER, 1, CfgT3>(p, st);
   if (g_gemm_cfg != 3)

@@ -19,9 +19,16 @@ namespace em {
 // against 2.3 s), two-stage at n = 50,000 (49.3 s against 50.7 s per C3 step before the
 // lower-triangle sy2sb update). Tests force either path.
 int64_t g_two_stage_min = 40000;
-// The two-stage path keeps the stage-2 reflectors (n^2 / 2 doubles) next to the compact-WY
-// blocks of the stage-1 back-transform (~n^2 doubles): taken only when that fits.
-static bool two_stage_fits(int64_t n) {
+// Extra device memory of the two-stage path beyond A and Z, phase by phase (n^2 doubles):
+// the stage-2 reflectors V2 (1/2) live from sb2st to the end; divide and conquer adds its
+// gathered Q and U (2, +1 when ldz != n); the Q2 apply the blocks' T factors (1/2); the Q1
+// apply its compact-WY V blocks (1). Taken only when the largest phase fits.
+static double two_stage_extra(int64_t ldz, int64_t n) {
+  const double stedc = 0.5 + 2.0 + (ldz != n ? 1.0 : 0.0), q2 = 0.5 + 0.5, q1 = 0.5 + 1.0;
+  return stedc > q1 ? (stedc > q2 ? stedc : q2) : (q1 > q2 ? q1 : q2);
+}
+int g_last_eig_path = 0;  // em_info(EM_INFO_EIG_PATH): 1 one-stage, 2 two-stage
+static bool two_stage_fits(int64_t n, int64_t ldz) {
   size_t free_b = 0, total_b = 0;
   if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return false;
   // plus what the stream-ordered pool holds reserved but unused (em_init keeps freed
@@ -36,7 +43,8 @@ static bool two_stage_fits(int64_t n) {
         reserved > used)
       free_b += (size_t)(reserved - used);
   }
-  const double need = 1.6 * (double)n * (double)n * sizeof(double) + (1ull << 30);
+  const double need =
+      two_stage_extra(ldz, n) * (double)n * (double)n * sizeof(double) + (1ull << 30);
   return (double)free_b >= need;
 }
 // em_config(EM_CFG_BAND_OFF): 1 forces the dense R path (tests compare both)
@@ -56,10 +64,12 @@ void syev_ascending(cudaStream_t st, int64_t n, double* A, int64_t lda, double* 
                     int64_t ldz, int64_t c0, int64_t nc) {
   if (n <= 0) return;
   if (nc < 0) nc = n - c0;
-  if (n >= g_two_stage_min && n > 2 * kBand && two_stage_fits(n)) {
+  if (n >= g_two_stage_min && n > 2 * kBand && two_stage_fits(n, ldz)) {
+    g_last_eig_path = 2;
     syev_two_stage(st, n, A, lda, w, Z, ldz, c0, nc);
     return;
   }
+  g_last_eig_path = 1;
   DBuf d(n, st), e(imax64(n - 1, 1), st), tau(imax64(n - 1, 1), st);
   {
     Stage s(st, ST_SYTRD);

@@ -343,12 +343,22 @@ __global__ void __launch_bounds__(256) sb2st_kernel(SbArgs a) {
     for (int64_t k = 0; k < K; ++k) {
       if (s > 0 && tid == 0) {
         const int need = (int)imin64(k + 3, Kp);
+        // acquire by thread 0, made CTA-wide by the barrier below; the band is read with
+        // L2-only loads (__ldcg), so no L1 invalidation is needed
         while (ld_acquire_int(a.prog + (s - 1)) < need) __nanosleep(32);
-        __threadfence();  // also invalidates this SM's L1 before the band is re-read
       }
       __syncthreads();
       const int64_t a0 = s + 1 + k * B2;
       const int L = (int)imin64(B2, n - a0);
+      // the diagonal block [a0, a0+L) is not touched by this task's off-diagonal work
+      // (columns ap .. a0-1): its loads are issued together with E's, one L2 round trip
+      for (int idx = tid; idx < B2 * B2; idx += 256) {
+        const int i = idx & (B2 - 1), j = idx >> 6;
+        double val = 0.0;
+        if (i < L && j < L)
+          val = (i >= j) ? __ldcg(AB + (i - j) + (a0 + j) * ldab) : __ldcg(AB + (j - i) + (a0 + i) * ldab);
+        D[i * SBLD + j] = val;
+      }
       double tau;
       if (k == 0) {
         // type 1: reflector from column s, rows a0 .. a0+L-1 (band offsets 1..L)
@@ -402,14 +412,6 @@ __global__ void __launch_bounds__(256) sb2st_kernel(SbArgs a) {
       }
       __syncthreads();
       // type 3 (and 1): D <- H D H on the diagonal block [a0, a0+L)
-      for (int idx = tid; idx < B2 * B2; idx += 256) {
-        const int i = idx & (B2 - 1), j = idx >> 6;
-        double val = 0.0;
-        if (i < L && j < L)
-          val = (i >= j) ? __ldcg(AB + (i - j) + (a0 + j) * ldab) : __ldcg(AB + (j - i) + (a0 + i) * ldab);
-        D[i * SBLD + j] = val;
-      }
-      __syncthreads();
       {
         double s2 = 0.0;
         for (int j = q; j < B2; j += 4) s2 = fma(D[row * SBLD + j], vn[j], s2);
@@ -441,7 +443,8 @@ __global__ void __launch_bounds__(256) sb2st_kernel(SbArgs a) {
         a.TAU2[t] = tau;
         tau_prev_s = tau;
       }
-      __threadfence();
+      // bar.sync orders every thread's band stores before thread 0's gpu-scope release
+      // (cumulativity), as in the TD1 solves
       __syncthreads();
       if (tid == 0) st_release_int(a.prog + s, (int)(k + 1));
     }

@@ -11,9 +11,10 @@
 // PERSISTENT triangular-solve kernels. Block rows of 64 are claimed in order from an
 // atomic counter; a CTA streams the off-diagonal tiles of its block row (the next tile is
 // in flight while the current one waits), reduces with warp shuffles / shared memory and
-// applies the pre-inverted 64x64 diagonal block. The product with the neighbouring
-// block's solution is folded into one precomputed 64x64 matrix (E_r = D_r C_{r,r-1},
-// F_r = D_r^T C_{r+1,r}^T), so a block's chain step is one product. There are no ready
+// applies the pre-inverted 64x64 diagonal block. The products with the two neighbouring
+// blocks' solutions are folded into precomputed 64x64 matrices (E_r = D_r C_{r,r-1},
+// E2_r = D_r C_{r,r-2}; F_r, F2_r for the backward solve), so a block's own reduction
+// finishes two chain steps ahead and its chain step is one product. There are no ready
 // flags: a solution entry is published by storing it over the sentinel (a NaN payload no
 // arithmetic produces; 64-bit stores are single-copy atomic), and a consumer polls the
 // entries it needs directly, so each link of the dependency chain is one L2 round trip
@@ -31,7 +32,7 @@ struct em_td1_plan {
   int64_t n = 0;
   int n_p = 0, n_s = 0, n_u = 0;
   double dt = 0, theta = 0;
-  em::DBuf C, R, Dinv, DinvT, Ef, Fb, E, work, b, y, x;
+  em::DBuf C, R, Dinv, DinvT, Ef, Fb, Ef2, Fb2, E, work, b, y, x;
   em::Csr Rs;          // R as CSR when it is sparse (the stencil): R I is an SpMV
   bool r_sparse = false;
   em::DArr<unsigned int>* counters = nullptr;
@@ -112,21 +113,26 @@ EM_DEVINL void poll16(const double* p, double (&v)[16]) {
   }
 }
 
-// Forward solve C y = b, C lower (col-major, ld ldc). Block rows claimed in order.
-// y_r = D_r (b_r - sum_{j < r-1} C_rj y_j) - E_r y_{r-1} with E_r = D_r C_{r,r-1}
-// precomputed: everything but one 64 x 64 product waits only on blocks up to r-2, so the
-// dependency chain per block is: see y_{r-1}, one product, publish y_r. y must hold the
+// Forward solve C y = b, C lower (col-major, ld ldc; its upper triangle holds the
+// mirror C^T, so a block row of C is read as a block column). Block rows claimed in order.
+// y_r = D_r (b_r - sum_{j < r-2} C_rj y_j) - E2_r y_{r-2} - E_r y_{r-1} with
+// E_r = D_r C_{r,r-1}, E2_r = D_r C_{r,r-2} precomputed: the tile stream and the D_r
+// product wait only on blocks up to r-3, so they finish two steps ahead of the chain,
+// whose step per block is: see y_{r-1}, one product, publish y_r. y must hold the
 // sentinel on entry (td1_pre_kernel).
 __global__ void __launch_bounds__(256) trsv_fwd_kernel(int64_t n, const double* __restrict__ C,
-                                                       int64_t ldc, const double* __restrict__ Dinv,
-                                                       const double* __restrict__ Ef,
-                                                       const double* __restrict__ b,
-                                                       double* __restrict__ y,
-                                                       unsigned int* counter) {
+                                                          int64_t ldc,
+                                                          const double* __restrict__ Dinv,
+                                                          const double* __restrict__ Ef,
+                                                          const double* __restrict__ Ef2,
+                                                          const double* __restrict__ b,
+                                                          double* __restrict__ y,
+                                                          unsigned int* counter) {
   __shared__ int64_t rblk;
   __shared__ double red[4][TS];
+  __shared__ double red8[8][16];
   __shared__ double part[TS];
-  const int tid = threadIdx.x, tx = tid & 63, ty = tid >> 6;
+  const int tid = threadIdx.x, tx = tid & 63, ty = tid >> 6, lane = tid & 31, warp = tid >> 5;
   const int64_t nblk = (n + TS - 1) / TS;
   while (true) {
     __syncthreads();
@@ -134,52 +140,74 @@ __global__ void __launch_bounds__(256) trsv_fwd_kernel(int64_t n, const double* 
     __syncthreads();
     const int64_t r = rblk;
     if (r >= nblk) break;
-    const int64_t r0 = r * TS, row = r0 + tx;
-    double acc = 0.0;
-    // Off the dependency chain: D_r, E_r and b_r are loaded up front, and tile j+1 is
-    // loaded before waiting for block j.
-    const double* D = Dinv + r * TS * TS;
-    const double* Er = Ef + r * TS * TS;
-    double dv[16], ev[16];
-#pragma unroll
-    for (int cc = 0; cc < 16; ++cc) {
-      dv[cc] = D[tx + (ty * 16 + cc) * TS];
-      ev[cc] = r > 0 ? Er[tx + (ty * 16 + cc) * TS] : 0.0;
-    }
+    const int64_t r0 = r * TS;
     const double bb = (tid < TS && r0 + tid < n) ? b[r0 + tid] : 0.0;
+    // tiles j <= r - 3, read from the mirrored upper triangle (Cm[j0 + b, r0 + a] =
+    // C[r0 + a, j0 + b]): thread (tx, ty) holds C_rj[ty*16 + cc][tx] for the 16 rows
+    // cc, coalesced along tx, and needs the single entry y_j[tx]; tile j+1 is loaded
+    // before waiting for block j
+    double acc[16];
+#pragma unroll
+    for (int cc = 0; cc < 16; ++cc) acc[cc] = 0.0;
+    const int64_t c0 = r0 + ty * 16;
     double a[16];
-    if (r > 1) {
+    if (r > 2) {
 #pragma unroll
-      for (int cc = 0; cc < 16; ++cc) a[cc] = (row < n) ? C[row + (ty * 16 + cc) * ldc] : 0.0;
+      for (int cc = 0; cc < 16; ++cc) a[cc] = (c0 + cc < n) ? C[tx + (c0 + cc) * ldc] : 0.0;
     }
-    for (int64_t j = 0; j + 1 < r; ++j) {  // tiles j <= r - 2
+    for (int64_t j = 0; j + 2 < r; ++j) {
       double an[16];
-      if (j + 2 < r) {
-        const int64_t c1 = (j + 1) * TS + ty * 16;
+      if (j + 3 < r) {
+        const int64_t rn = (j + 1) * TS + tx;
 #pragma unroll
-        for (int cc = 0; cc < 16; ++cc) an[cc] = (row < n) ? C[row + (c1 + cc) * ldc] : 0.0;
+        for (int cc = 0; cc < 16; ++cc) an[cc] = (c0 + cc < n) ? C[rn + (c0 + cc) * ldc] : 0.0;
       }
-      double yv[16];
-      poll16(y + j * TS + ty * 16, yv);
+      double yv = ld_poll(y + j * TS + tx);
+      while (is_sentinel(yv)) yv = ld_poll(y + j * TS + tx);
 #pragma unroll
-      for (int cc = 0; cc < 16; ++cc) acc = fma(a[cc], yv[cc], acc);
+      for (int cc = 0; cc < 16; ++cc) acc[cc] = fma(a[cc], yv, acc[cc]);
 #pragma unroll
       for (int cc = 0; cc < 16; ++cc) a[cc] = an[cc];
     }
-    red[ty][tx] = acc;
+    // reduce acc[cc] over the 64 columns (tx): warp shuffle, then the two warps per ty
+#pragma unroll
+    for (int cc = 0; cc < 16; ++cc) acc[cc] = warp_sum(acc[cc]);
+    if (lane == 0) {
+#pragma unroll
+      for (int cc = 0; cc < 16; ++cc) red8[warp][cc] = acc[cc];
+    }
     __syncthreads();
-    if (tid < TS) part[tid] = bb - (red[0][tid] + red[1][tid] + red[2][tid] + red[3][tid]);
+    if (tid < TS) {
+      const int gq = tid >> 4, cc = tid & 15;  // row tid = gq*16 + cc (warps 2gq, 2gq+1)
+      part[tid] = bb - (red8[2 * gq][cc] + red8[2 * gq + 1][cc]);
+    }
     __syncthreads();
-    // p_r = D_r part (still off the chain)
+    // p_r = D_r part (off the chain)
+    const double* D = Dinv + r * TS * TS;
     double s = 0.0;
 #pragma unroll
-    for (int cc = 0; cc < 16; ++cc) s = fma(dv[cc], part[ty * 16 + cc], s);
+    for (int cc = 0; cc < 16; ++cc) s = fma(D[tx + (ty * 16 + cc) * TS], part[ty * 16 + cc], s);
     red[ty][tx] = s;
     __syncthreads();
     double pr = 0.0;
     if (tid < TS) pr = red[0][tid] + red[1][tid] + red[2][tid] + red[3][tid];
-    // the chain: y_r = p_r - E_r y_{r-1}
+    // the chain operands (loaded while y_{r-2}, y_{r-1} are still on their way)
+    const double* Er = Ef + r * TS * TS;
+    const double* Er2 = Ef2 + r * TS * TS;
+    double ev[16], e2v[16];
+#pragma unroll
+    for (int cc = 0; cc < 16; ++cc) {
+      ev[cc] = r > 0 ? Er[tx + (ty * 16 + cc) * TS] : 0.0;
+      e2v[cc] = r > 1 ? Er2[tx + (ty * 16 + cc) * TS] : 0.0;
+    }
+    // E2_r y_{r-2} (one step ahead of the chain), then the chain: E_r y_{r-1}
     double se = 0.0;
+    if (r > 1) {
+      double yv[16];
+      poll16(y + (r - 2) * TS + ty * 16, yv);
+#pragma unroll
+      for (int cc = 0; cc < 16; ++cc) se = fma(e2v[cc], yv[cc], se);
+    }
     if (r > 0) {
       double yv[16];
       poll16(y + (r - 1) * TS + ty * 16, yv);
@@ -200,13 +228,14 @@ __global__ void __launch_bounds__(256) trsv_fwd_kernel(int64_t n, const double* 
 }
 
 // Backward solve C^T x = y; then I += x (and capture). Block rows claimed from the bottom.
-// x_r = DT_r (y_r - sum_{j > r+1} C_jr^T x_j) - F_r x_{r+1}, F_r = DT_r C_{r+1,r}^T
-// precomputed (DT_r = D_r^T): one 64 x 64 product on the dependency chain. x must hold the
-// sentinel on entry.
+// x_r = DT_r (y_r - sum_{j > r+2} C_jr^T x_j) - F2_r x_{r+2} - F_r x_{r+1},
+// F_r = DT_r C_{r+1,r}^T, F2_r = DT_r C_{r+2,r}^T precomputed (DT_r = D_r^T): one 64 x 64
+// product on the dependency chain. x must hold the sentinel on entry.
 __global__ void __launch_bounds__(256) trsv_bwd_kernel(
     int64_t n, const double* __restrict__ C, int64_t ldc, const double* __restrict__ Dinv,
-    const double* __restrict__ Fb, const double* __restrict__ y, double* __restrict__ x,
-    double* __restrict__ I, double* __restrict__ Icap, unsigned int* counter) {
+    const double* __restrict__ Fb, const double* __restrict__ Fb2, const double* __restrict__ y,
+    double* __restrict__ x, double* __restrict__ I, double* __restrict__ Icap,
+    unsigned int* counter) {
   __shared__ int64_t rblk;
   __shared__ double red[8][TS];
   __shared__ double part[TS];
@@ -223,28 +252,18 @@ __global__ void __launch_bounds__(256) trsv_bwd_kernel(
     double acc[16];
 #pragma unroll
     for (int cc = 0; cc < 16; ++cc) acc[cc] = 0.0;
-    // tiles (j, r), j = nblk-1 .. r+2; tile j-1 is prefetched before waiting for block j;
-    // DT_r, F_r and y_r are loaded up front (off the chain)
+    // tiles (j, r), j = nblk-1 .. r+3; tile j-1 is prefetched before waiting for block j
     const int64_t c0 = r0 + ty * 16;
-    const double* D = Dinv + r * TS * TS;
-    const double* Fr = Fb + r * TS * TS;
-    const bool has_next = r + 1 < nblk;
-    double dv[16], fv[16];
-#pragma unroll
-    for (int cc = 0; cc < 16; ++cc) {
-      dv[cc] = D[tx + (ty * 16 + cc) * TS];
-      fv[cc] = has_next ? Fr[tx + (ty * 16 + cc) * TS] : 0.0;
-    }
     const double yr = (tid < TS && r0 + tid < n) ? y[r0 + tid] : 0.0;
     double a[16];
-    if (nblk - 2 > r) {
+    if (nblk - 3 > r) {
       const int64_t rowj = (nblk - 1) * TS + tx;
 #pragma unroll
       for (int cc = 0; cc < 16; ++cc) a[cc] = (rowj < n) ? C[rowj + (c0 + cc) * ldc] : 0.0;
     }
-    for (int64_t j = nblk - 1; j > r + 1; --j) {
+    for (int64_t j = nblk - 1; j > r + 2; --j) {
       double an[16];
-      if (j - 1 > r + 1) {
+      if (j - 1 > r + 2) {
         const int64_t rown = (j - 1) * TS + tx;
 #pragma unroll
         for (int cc = 0; cc < 16; ++cc) an[cc] = (rown < n) ? C[rown + (c0 + cc) * ldc] : 0.0;
@@ -257,6 +276,7 @@ __global__ void __launch_bounds__(256) trsv_bwd_kernel(
 #pragma unroll
       for (int cc = 0; cc < 16; ++cc) a[cc] = an[cc];
     }
+    const bool has_next = r + 1 < nblk, has_next2 = r + 2 < nblk;
     // reduce acc[cc] over the 64 rows (tx): warp shuffle, then the two warps per ty
 #pragma unroll
     for (int cc = 0; cc < 16; ++cc) acc[cc] = warp_sum(acc[cc]);
@@ -271,21 +291,36 @@ __global__ void __launch_bounds__(256) trsv_bwd_kernel(
       part[tid] = yr - sumc;
     }
     __syncthreads();
-    // p_r = DT_r part with the pre-transposed block (coalesced), still off the chain
+    // p_r = DT_r part with the pre-transposed block (coalesced), off the chain
+    const double* D = Dinv + r * TS * TS;
     double s = 0.0;
 #pragma unroll
-    for (int cc = 0; cc < 16; ++cc) s = fma(dv[cc], part[ty * 16 + cc], s);
+    for (int cc = 0; cc < 16; ++cc) s = fma(D[tx + (ty * 16 + cc) * TS], part[ty * 16 + cc], s);
     red[ty][tx] = s;
     __syncthreads();
     double pr = 0.0;
     if (tid < TS) pr = red[0][tid] + red[1][tid] + red[2][tid] + red[3][tid];
-    // the chain: x_r = p_r - F_r x_{r+1}
-    double sf = 0.0;
-    if (has_next) {
-      double xn[16];
-      poll16(x + (r + 1) * TS + ty * 16, xn);
+    const double* Fr = Fb + r * TS * TS;
+    const double* Fr2 = Fb2 + r * TS * TS;
+    double fv[16], f2v[16];
 #pragma unroll
-      for (int cc = 0; cc < 16; ++cc) sf = fma(fv[cc], xn[cc], sf);
+    for (int cc = 0; cc < 16; ++cc) {
+      fv[cc] = has_next ? Fr[tx + (ty * 16 + cc) * TS] : 0.0;
+      f2v[cc] = has_next2 ? Fr2[tx + (ty * 16 + cc) * TS] : 0.0;
+    }
+    // F2_r x_{r+2}, then the chain: F_r x_{r+1}
+    double sf = 0.0;
+    if (has_next2) {
+      double xv2[16];
+      poll16(x + (r + 2) * TS + ty * 16, xv2);
+#pragma unroll
+      for (int cc = 0; cc < 16; ++cc) sf = fma(f2v[cc], xv2[cc], sf);
+    }
+    if (has_next) {
+      double xv2[16];
+      poll16(x + (r + 1) * TS + ty * 16, xv2);
+#pragma unroll
+      for (int cc = 0; cc < 16; ++cc) sf = fma(fv[cc], xv2[cc], sf);
     }
     __syncthreads();  // red: the p_r readers are done
     red[ty][tx] = sf;
@@ -354,6 +389,9 @@ int64_t td1_plan_init(em_td1_plan* P, const double* L, int64_t ldl, const double
   EM_LAUNCHED();
   const int64_t piv = potrf(st, n, P->C.p, n);
   if (piv >= 0) return piv;
+  // the forward solve reads block rows of C as block columns of C^T: keep the mirror in
+  // the (zeroed) upper triangle
+  mirror_lower(st, n, P->C.p, n);
   // the stencil R: keep only its CSR (7 nonzeros per row) for the per-step R I
   P->r_sparse = csr_from_dense(st, n, P->R.p, n, 0.02, P->Rs);
   if (P->r_sparse) P->R.release();
@@ -364,10 +402,13 @@ int64_t td1_plan_init(em_td1_plan* P, const double* L, int64_t ldl, const double
   transpose_blocks_kernel<<<(unsigned)nblk, 256, 0, st>>>(P->Dinv.p, P->DinvT.p);
   EM_LAUNCHED();
   // the chain products: Ef_r = D_r C_{r,r-1} (forward), Fb_r = D_r^T C_{r+1,r}^T (backward)
+  // and E2_r = D_r C_{r,r-2}, F2_r = D_r^T C_{r+2,r}^T (one step further)
   P->Ef.alloc((size_t)nblk * TS * TS, st);
   P->Fb.alloc((size_t)nblk * TS * TS, st);
-  EM_CK(cudaMemsetAsync(P->Ef.p, 0, (size_t)nblk * TS * TS * sizeof(double), st));
-  EM_CK(cudaMemsetAsync(P->Fb.p, 0, (size_t)nblk * TS * TS * sizeof(double), st));
+  P->Ef2.alloc((size_t)nblk * TS * TS, st);
+  P->Fb2.alloc((size_t)nblk * TS * TS, st);
+  for (DBuf* m : {&P->Ef, &P->Fb, &P->Ef2, &P->Fb2})
+    EM_CK(cudaMemsetAsync(m->p, 0, (size_t)nblk * TS * TS * sizeof(double), st));
   if (nblk > 1) {
     std::vector<GemmArgs> pf, pb;
     for (int64_t r = 1; r < nblk; ++r) {
@@ -377,6 +418,15 @@ int64_t td1_plan_init(em_td1_plan* P, const double* L, int64_t ldl, const double
       const int64_t q = r - 1;  // Fb_q with block q + 1 = r below it
       pb.push_back(GemmArgs{TS, bs, TS, P->DinvT.p + q * TS * TS, TS, P->C.p + r0 + q * TS * n, n,
                             P->Fb.p + q * TS * TS, TS, 1.0, 0.0, 0});
+      if (r >= 2) {
+        pf.push_back(GemmArgs{bs, TS, bs, P->Dinv.p + r * TS * TS, TS,
+                              P->C.p + r0 + (r0 - 2 * TS) * n, n, P->Ef2.p + r * TS * TS, TS, 1.0,
+                              0.0, 0});
+        const int64_t q2 = r - 2;  // Fb2_q2 with block q2 + 2 = r below it
+        pb.push_back(GemmArgs{TS, bs, TS, P->DinvT.p + q2 * TS * TS, TS,
+                              P->C.p + r0 + q2 * TS * n, n, P->Fb2.p + q2 * TS * TS, TS, 1.0,
+                              0.0, 0});
+      }
     }
     DArr<GemmArgs> df(pf.size(), st), db(pb.size(), st);
     EM_CK(cudaMemcpyAsync(df.p, pf.data(), pf.size() * sizeof(GemmArgs), cudaMemcpyHostToDevice, st));
@@ -434,14 +484,14 @@ static void td1_solve_step(em_td1_plan* P, double* I, double* Icap_col, const do
   const int grid = (int)imin64(nblk, 2 * num_sms());
   {
     Stage s(st, ST_TD1_FWD);
-    trsv_fwd_kernel<<<grid, 256, 0, st>>>(n, P->C.p, n, P->Dinv.p, P->Ef.p, P->b.p, P->y.p,
-                                          P->counters->p);
+    trsv_fwd_kernel<<<grid, 256, 0, st>>>(n, P->C.p, n, P->Dinv.p, P->Ef.p, P->Ef2.p, P->b.p,
+                                          P->y.p, P->counters->p);
     EM_LAUNCHED();
   }
   {
     Stage s(st, ST_TD1_BWD);
-    trsv_bwd_kernel<<<grid, 256, 0, st>>>(n, P->C.p, n, P->DinvT.p, P->Fb.p, P->y.p, P->x.p, I,
-                                          Icap_col, P->counters->p + 1);
+    trsv_bwd_kernel<<<grid, 256, 0, st>>>(n, P->C.p, n, P->DinvT.p, P->Fb.p, P->Fb2.p, P->y.p,
+                                          P->x.p, I, Icap_col, P->counters->p + 1);
     EM_LAUNCHED();
   }
 }
@@ -518,6 +568,7 @@ void td1_delete(em_td1_plan* p) {
 em_ctx* td1_ctx(em_td1_plan* p) { return p ? p->ctx : nullptr; }
 void td1_copy_factor(em_td1_plan* P, double* out, int64_t ldo) {
   copy_matrix(P->ctx->stream, false, P->n, P->n, P->C.p, P->n, out, ldo);
+  zero_upper(P->ctx->stream, P->n, out, ldo);  // the plan keeps C^T there
   EM_CK(cudaStreamSynchronize(P->ctx->stream));
 }
 

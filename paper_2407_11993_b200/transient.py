@@ -134,11 +134,45 @@ def _drive_projection(rm: ReducedModel, basis: ModalBasis):
     return proj
 
 
+def select_modes(basis: ModalBasis, tau_min: float | None = None, count: int | None = None
+                 ) -> np.ndarray:
+    """Mode indices for selective integration ("(iv) in a selective
+    manner"): the modes with tau >= tau_min and/or the `count` slowest
+    (tau is descending, so these are leading indices). Pass to Td2Stepper(modes=...)."""
+    idx = np.arange(basis.n_modes)
+    if tau_min is not None:
+        idx = idx[basis.tau[idx] >= tau_min]
+    if count is not None:
+        idx = idx[:max(int(count), 0)]
+    return idx
+
+
+def _mode_selection(n: int, modes) -> np.ndarray | None:
+    """None (all modes) or sorted unique int64 indices from indices / a boolean mask."""
+    if modes is None:
+        return None
+    sel = np.asarray(modes)
+    if sel.dtype == bool:
+        if sel.shape != (n,):
+            raise DimensionMismatch(f"mode mask needs {n} entries, got {sel.shape}")
+        sel = np.flatnonzero(sel)
+    sel = np.unique(sel.astype(np.int64))
+    if sel.size and (sel[0] < 0 or sel[-1] >= n):
+        raise ValidationError("mode index out of range")
+    return None if sel.size == n else sel
+
+
 class Td2Stepper:
     """Decoupled stepper (transient.py:116-166): per-mode scalar updates after
-    projecting the drive onto the modes."""
+    projecting the drive onto the modes.
 
-    def __init__(self, rm: ReducedModel, basis: ModalBasis, dt: float, theta: float):
+    modes (optional): integrate only these modes (indices or a boolean mask; see
+    select_modes) — the selective integration of PAPER.md:299. The others stay at their
+    state (rest for run()); observables and reconstructed currents are the truncated
+    modal sums."""
+
+    def __init__(self, rm: ReducedModel, basis: ModalBasis, dt: float, theta: float,
+                 modes=None):
         _check_theta_dt(dt, theta)
         if basis.n_modes != rm.n_internal:
             raise DimensionMismatch("modal basis does not match the reduced model")
@@ -147,21 +181,30 @@ class Td2Stepper:
         self.basis = basis
         self.dt = float(dt)
         self.theta = float(theta)
-        n, n_p, n_s = basis.n_modes, rm.n_ports, rm.n_sources
+        n_full, n_p, n_s = basis.n_modes, rm.n_ports, rm.n_sources
+        sel = _mode_selection(n_full, modes)
+        self._sel = sel
+        self._sel_dev = None if sel is None else nat.torch().from_numpy(sel).to("cuda")
+        n = n_full if sel is None else int(sel.size)
+        self._n_full = n_full
         self._n, self._n_p, self._n_s = n, n_p, n_s
+        l_n = basis.l_n if sel is None else basis.l_n[sel]
+        r_n = basis.r_n if sel is None else basis.r_n[sel]
         # host copies kept for API compatibility (transient.py:134-144)
-        den = basis.l_n + self.dt * self.theta * basis.r_n
+        den = l_n + self.dt * self.theta * r_n
         self._c = np.sqrt(den)
-        self._rn = basis.r_n.copy()
+        self._rn = r_n.copy()
         ctx = nat.context()
         lib = nat.load_library()
         proj = _drive_projection(rm, basis)
+        if sel is not None:
+            proj = proj.index_select(1, self._sel_dev).contiguous()
         self._proj = proj
         p_r = proj[0:n_p] if n_p else proj[0:1]
         p_l = proj[n_p:2 * n_p] if n_p else proj[0:1]
         p_m = proj[2 * n_p:] if n_s else proj[0:1]
-        self._ln_dev = nat.device_vector(basis.l_n)
-        self._rn_dev = nat.device_vector(basis.r_n)
+        self._ln_dev = nat.device_vector(l_n)
+        self._rn_dev = nat.device_vector(r_n)
         plan = ctypes.c_void_p()
         nat.check(lib.em_td2_plan_create(ctx, n, n_p, n_s, nat.ptr(self._ln_dev),
                                          nat.ptr(self._rn_dev), nat.ptr(p_r), nat.ptr(p_l),
@@ -185,35 +228,48 @@ class Td2Stepper:
         return nat.host_colmajor(self._proj[2 * self._n_p:], self._n, self._n_s)
 
     def forcing(self, i_d, delta_i_d, delta_i0) -> np.ndarray:
-        """-dt P_r i_D - P_ltr dI_D - P_m dI_0 (transient.py:147-155), on the device."""
+        """-dt P_r i_D - P_ltr dI_D - P_m dI_0 (transient.py:147-155), on the device
+        (zero for modes outside a selection)."""
         f = nat.empty(self._n)
         u = [np.ascontiguousarray(np.asarray(x, dtype=float)) for x in (i_d, delta_i_d, delta_i0)]
         ptrs = [x.ctypes.data_as(ctypes.c_void_p) for x in u]
         nat.check(nat.load_library().em_td2_forcing(self._plan, *ptrs, nat.ptr(f)),
                   "em_td2_forcing")
-        return f.cpu().numpy()
+        if self._sel is None:
+            return f.cpu().numpy()
+        out = np.zeros(self._n_full)
+        out[self._sel] = f.cpu().numpy()
+        return out
 
     def step(self, modal_state: np.ndarray, i_d, delta_i_d, delta_i0) -> np.ndarray:
-        """Advance one step in place (transient.py:157-166)."""
-        n = self._n
+        """Advance one step in place (transient.py:157-166); with a selection only the
+        selected modes move."""
+        n = self._n_full
         if modal_state.shape != (n,):
             raise DimensionMismatch(f"modal state must have {n} components")
-        if n == 0:
+        if n == 0 or self._n == 0:
             return modal_state
-        q = nat.device_vector(modal_state)
+        sub = modal_state if self._sel is None else modal_state[self._sel]
+        q = nat.device_vector(sub)
         u = [np.ascontiguousarray(np.asarray(x, dtype=float)) for x in (i_d, delta_i_d, delta_i0)]
         ptrs = [x.ctypes.data_as(ctypes.c_void_p) for x in u]
         nat.check(nat.load_library().em_td2_step(self._plan, nat.ptr(q), *ptrs), "em_td2_step")
-        modal_state[:] = q.cpu().numpy()
+        if self._sel is None:
+            modal_state[:] = q.cpu().numpy()
+        else:
+            modal_state[self._sel] = q.cpu().numpy()
         return modal_state
 
     def set_observables(self, observables):
-        n_obs, cdev, ddev = _obs_device(observables, self._n, self._n_p)
+        nf = self._n_full
+        n_obs, cdev, ddev = _obs_device(observables, nf, self._n_p)
         ctx = nat.context()
-        cv = nat.empty(self._n, n_obs)  # C V column-major n_obs x n
-        nat.check(nat.load_library().em_dgemm(ctx, 0, 0, n_obs, self._n, self._n, 1.0,
+        cv = nat.empty(nf, n_obs)  # C V column-major n_obs x n
+        nat.check(nat.load_library().em_dgemm(ctx, 0, 0, n_obs, nf, nf, 1.0,
                                                nat.ptr(cdev), n_obs, nat.ptr(self.basis.v_dev),
-                                               self._n, 0.0, nat.ptr(cv), n_obs), "em_dgemm")
+                                               nf, 0.0, nat.ptr(cv), n_obs), "em_dgemm")
+        if self._sel is not None:
+            cv = cv.index_select(0, self._sel_dev).contiguous()  # the selected modes' columns
         nat.check(nat.load_library().em_td2_set_observables(
             self._plan, n_obs, nat.ptr(cv), n_obs, nat.ptr(ddev), n_obs), "em_td2_set_observables")
         self._n_obs = n_obs
@@ -240,13 +296,20 @@ class Td2Stepper:
         if observables is not None:
             self.set_observables(observables)
         drive = nat.device_vector(table.reshape(-1)) if table.size else nat.zeros(1)
-        q = nat.device_vector(np.zeros(self._n) if modal_state0 is None else modal_state0)
+        q0 = np.zeros(self._n_full) if modal_state0 is None else \
+            np.asarray(modal_state0, dtype=float)
+        q = nat.device_vector(q0 if self._sel is None else q0[self._sel])
         y, qcap = self.run_device(drive, steps, q, capture_stride, capture_state,
                                   observables is not None)
         states = None
         if qcap is not None:
-            states = _reconstruct(self.basis, qcap, qcap.shape[0])
-        return states, (y.cpu().numpy() if y is not None else None), q.cpu().numpy()
+            states = _reconstruct(self.basis, qcap, qcap.shape[0], self._sel_dev)
+        q_out = q.cpu().numpy()
+        if self._sel is not None:
+            full = q0.copy()
+            full[self._sel] = q_out
+            q_out = full
+        return states, (y.cpu().numpy() if y is not None else None), q_out
 
     def run_sweep_device(self, drive_dev, steps: int, q_dev, capture_stride: int = 1,
                          want_obs: bool = True):
@@ -285,15 +348,18 @@ class Td2Stepper:
             nat.host_colmajor(q, self._n, n_c)
 
 
-def _reconstruct(basis: ModalBasis, qcap, n_caps: int) -> np.ndarray:
-    """internal states I = V Q for captured modal states (n_caps x N host)."""
+def _reconstruct(basis: ModalBasis, qcap, n_caps: int, sel_dev=None) -> np.ndarray:
+    """internal states I = V Q for captured modal states (n_caps x N host); sel_dev:
+    the modes Q holds (V's columns sel)."""
     n = basis.n_modes
     if n_caps == 0:
         return np.zeros((0, n))
+    v = basis.v_dev if sel_dev is None else basis.v_dev.index_select(0, sel_dev).contiguous()
+    m = v.shape[0]
     ctx = nat.context()
     out = nat.empty(n_caps, n)
-    nat.check(nat.load_library().em_dgemm(ctx, 0, 0, n, n_caps, n, 1.0, nat.ptr(basis.v_dev), n,
-                                           nat.ptr(qcap), n, 0.0, nat.ptr(out), n), "em_dgemm")
+    nat.check(nat.load_library().em_dgemm(ctx, 0, 0, n, n_caps, m, 1.0, nat.ptr(v), n,
+                                           nat.ptr(qcap), m, 0.0, nat.ptr(out), n), "em_dgemm")
     return out.cpu().numpy()
 
 
@@ -412,12 +478,16 @@ def step_td2(stepper: Td2Stepper, modal_state, forcing) -> np.ndarray:
     forcing = np.asarray(forcing, dtype=float)
     if forcing.shape != modal_state.shape:
         raise DimensionMismatch("forcing and state sizes differ")
-    if modal_state.shape[0]:
-        q = nat.device_vector(modal_state)
-        f = nat.device_vector(forcing)
+    sel = stepper._sel
+    if modal_state.shape[0] and stepper._n:
+        q = nat.device_vector(modal_state if sel is None else modal_state[sel])
+        f = nat.device_vector(forcing if sel is None else forcing[sel])
         nat.check(nat.load_library().em_td2_step_forcing(stepper._plan, nat.ptr(q), nat.ptr(f)),
                   "em_td2_step_forcing")
-        modal_state[:] = q.cpu().numpy()
+        if sel is None:
+            modal_state[:] = q.cpu().numpy()
+        else:
+            modal_state[sel] = q.cpu().numpy()
     return modal_state
 
 
@@ -465,11 +535,13 @@ def drive_samples(net, rm: ReducedModel, drives, dt: float, n_steps: int):
 
 
 def run_transient(rm: ReducedModel, net, drives, cfg: TransientConfig,
-                  modal: ModalBasis | None = None, observables=None) -> SimulationResult:
+                  modal: ModalBasis | None = None, observables=None,
+                  modes=None) -> SimulationResult:
     """Integrate from rest, capture every capture_stride steps (transient.py:248-312).
 
     observables: optional (C, D) with C (n_obs x N) and D (n_obs x n_ports) or None;
-    captured values are C I + D i_D(t_{k+1}) for each capture."""
+    captured values are C I + D i_D(t_{k+1}) for each capture. modes (td2 only): the
+    selective integration of PAPER.md:299 (see select_modes)."""
     if isinstance(drives, DriveSignal):
         drives = (drives,)
     if cfg.method == "td2" and modal is None:
@@ -487,7 +559,7 @@ def run_transient(rm: ReducedModel, net, drives, cfg: TransientConfig,
     if cfg.method == "td1":
         stepper = Td1Stepper(rm, cfg.dt, cfg.theta)
     else:
-        stepper = Td2Stepper(rm, modal, cfg.dt, cfg.theta)
+        stepper = Td2Stepper(rm, modal, cfg.dt, cfg.theta, modes=modes)
     nat.synchronize()
     setup_time = time.perf_counter() - setup0
 

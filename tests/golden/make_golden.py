@@ -3,7 +3,7 @@
 Run in the build container (where /root/reference exists); the resulting
 .npz files are committed and are all the GPU box ever sees:
 
-    python tests/golden/make_golden.py kat plate_small plate_200 tubes fd   # seconds
+    python tests/golden/make_golden.py kat plate_small plate_200 tubes fd reduction  # seconds
     python tests/golden/make_golden.py c1                                # ~30 min (Jacobi at N=2000)
     python tests/golden/make_golden.py c2                                # ~10 min (dsygvd at N=16384)
 
@@ -227,6 +227,38 @@ def case_c2(em):
     save("c2", **out)
 
 
+def case_reduction(em):
+    """The reference's external-model reduction (reduction.py:60-99 integer kernel,
+    21-57 lift, 143-183 project_external) on seeded integer incidence matrices: exact
+    integer K (pinned bitwise) and the projected model."""
+    from eddymodes.reduction import integer_kernel, lift_matrix, project_external
+    rng = np.random.default_rng(20240807)
+    out = {}
+    for t in range(12):
+        r = int(rng.integers(1, 5))
+        c = int(rng.integers(r + 1, 30))
+        e = rng.integers(-3, 4, size=(r, c))
+        if t % 3 == 0:
+            e[:, int(rng.integers(0, c))] = 0
+        if t % 4 == 1 and r > 1:
+            e[-1] = 2 * e[0] - e[1 % r]  # dependent row: a rank-deficient E
+        out[f"ik_e_{t}"] = e
+        out[f"ik_k_{t}"] = integer_kernel(e)
+    n_x = 48
+    a = rng.standard_normal((n_x, n_x))
+    r_x = a @ a.T / n_x + np.eye(n_x)
+    b = rng.standard_normal((n_x, n_x))
+    l_x = b @ b.T / n_x + 0.5 * np.eye(n_x)
+    e = np.zeros((2, n_x), dtype=np.int64)
+    e[0, :5] = [1, -1, 2, 0, 1]
+    e[1, 3:9] = [1, 1, 0, -2, 1, 1]
+    rm = project_external(r_x, l_x, e, port_names=("a", "b"))
+    out.update(px_r_x=r_x, px_l_x=l_x, px_e=e, px_r_i=rm.r_i.full, px_l_i=rm.l_i.full,
+               px_r_d=rm.r_d, px_l_d=rm.l_d, px_lift=rm.lift, px_k=rm.k,
+               lift_e=e, lift_m=lift_matrix(e))
+    save("reduction", **out)
+
+
 def case_fd(em):
     """Frequency domain: the reference solve_tone on the plate_small
     and tube_small models at several tones, dft_phasor / extract_phasors KATs."""
@@ -304,6 +336,8 @@ def main(argv):
             case_c1(em)
         elif case == "c2":
             case_c2(em)
+        elif case == "reduction":
+            case_reduction(em)
         elif case == "fd":
             case_fd(em)
         elif case == "cache":

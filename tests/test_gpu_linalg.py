@@ -11,11 +11,12 @@ from tests.conftest import golden
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("cfg", [0, 2, 3, 4])
+@pytest.mark.parametrize("cfg", [0, 2, 3, 4, 5])
 def test_dgemm_all_transposes_vs_numpy(rng, cfg):
     """em_config debug key 96 selects the tile configuration: 0 the default (64x64 tiles,
     three CTAs per SM for a transposed A, four otherwise), 2 64x64 / four CTAs, 3 128x64,
-    4 64x64 / three CTAs; (40, 70, 6000) takes split-K."""
+    4 64x64 / three CTAs, 5 the paired-fragment tiles (16-byte operands: the even leading
+    dimensions below); (40, 70, 6000) takes split-K."""
     from paper_2407_11993_b200 import _native as nat
     ctx = nat.context()
     lib = nat.load_library()
@@ -28,7 +29,7 @@ def test_dgemm_all_transposes_vs_numpy(rng, cfg):
 
 def _dgemm_cases(rng, nat, ctx, lib):
     for (m, n, k) in ((1, 1, 1), (37, 129, 300), (257, 131, 17), (300, 300, 300),
-                      (130, 200, 1100), (40, 70, 6000)):
+                      (130, 200, 1100), (40, 70, 6000), (256, 192, 64), (200, 330, 146)):
         for ta in (0, 1):
             for tb in (0, 1):
                 a = rng.standard_normal((k, m) if ta else (m, k))

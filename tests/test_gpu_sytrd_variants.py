@@ -109,3 +109,24 @@ def test_two_stage_q2_forms_agree(n, lda):
         # same eigenvectors (well separated random spectrum; sign fixed by the solver)
         d = np.abs(np.abs(np.sum(out[0][1] * out[mode][1], axis=0)) - 1.0)
         assert d.max() < 1e-9
+
+
+def test_eig_path_reported_and_pool_trim():
+    """em_info(EM_INFO_EIG_PATH) says which tridiagonalisation ran; em_trim releases the
+    library's cached pool memory (ADVICE: the path may depend on free memory, so it is
+    observable, and the cache is releasable)."""
+    from paper_2407_11993_b200 import _native as nat
+    rng = np.random.default_rng(3)
+    b = rng.standard_normal((300, 300))
+    a = b + b.T
+    _syev(a)
+    assert nat.last_eig_path() == 1
+    nat.set_two_stage_min(0)
+    try:
+        w2, _ = _syev(a)
+        assert nat.last_eig_path() == 2
+    finally:
+        nat.set_two_stage_min(nat.TWO_STAGE_MIN_DEFAULT)
+    nat.trim()
+    w1, _ = _syev(a)
+    assert np.max(np.abs(w1 - w2)) < 1e-11 * np.abs(w1).max()

@@ -362,3 +362,46 @@ def test_c2_full_size_td1_equals_td2(theta):
     lib.em_td1_plan_destroy(plan1)
     assert rel_l2(y2.cpu().numpy(), y1.cpu().numpy()) < 1e-8
     assert rel_l2(icap2, icap1.cpu().numpy()) < 1e-8
+
+
+def test_selective_mode_integration():
+    """SURVEY 8(f)4 / PAPER.md:299 "(iv) in a selective manner": a subset of modes
+    integrated alone. All modes = the full run (same arithmetic); a subset = the oracle's
+    run restricted to those modes; the truncation error falls as slow modes are added."""
+    from paper_2407_11993_b200 import modal, transient
+    g = golden("plate_200")
+    rm = _plate_rm(g)
+    basis = modal.generalized_eig(rm.l_i, rm.r_i)
+    dt, steps = float(g["dt"]), int(g["steps"])
+    i_d, i0 = transient.drive_samples(None, rm, _plate_drives(), dt, steps)
+    obs = (g["c"], None)
+    full = transient.Td2Stepper(rm, basis, dt, 0.5)
+    s_full, y_full, q_full = full.run(i_d, i0, observables=obs)
+    every = transient.Td2Stepper(rm, basis, dt, 0.5, modes=np.ones(200, dtype=bool))
+    _, y_all, _ = every.run(i_d, i0, capture_state=False, observables=obs)
+    np.testing.assert_array_equal(y_all, y_full)
+    sel = transient.select_modes(basis, count=40)
+    assert np.array_equal(sel, np.arange(40))
+    part = transient.Td2Stepper(rm, basis, dt, 0.5, modes=sel)
+    s_sel, y_sel, q_sel = part.run(i_d, i0, observables=obs)
+    # the truncated modal sum, by the oracle's loop over the same modes
+    from oracle import oracle as O
+    vt = basis.v.T
+    tab = np.concatenate([i_d, i0], axis=1)
+    _, y_ref = O.td2_run_table(basis.l_n[sel], basis.r_n[sel], (vt @ g["r_d"])[sel],
+                               (vt @ g["l_d"])[sel], (vt @ g["m0"])[sel], dt, 0.5, tab, steps,
+                               cv=(g["c"] @ basis.v)[:, sel])
+    assert rel_l2(y_sel, y_ref) < 1e-12
+    assert np.array_equal(q_sel[40:], np.zeros(160)) and rel_l2(q_sel[:40], q_full[:40]) < 1e-12
+    assert rel_l2(s_sel, q_sel[:40] @ basis.v[:, :40].T) < 1e-12
+    errs = [rel_l2(transient.Td2Stepper(rm, basis, dt, 0.5, modes=transient.select_modes(
+        basis, count=c)).run(i_d, i0, capture_state=False, observables=obs)[1], y_full)
+        for c in (10, 50, 150, 200)]
+    assert errs[-1] < 1e-14 and errs[0] > errs[1] > errs[2] > errs[3]
+    # by time constant, and the per-step API moves only the selected modes
+    slow = transient.select_modes(basis, tau_min=float(basis.tau[9]))
+    assert np.array_equal(slow, np.arange(10))
+    st = transient.Td2Stepper(rm, basis, dt, 0.5, modes=slow)
+    q = np.zeros(200)
+    st.step(q, np.ones(1), np.ones(1), np.ones(1))
+    assert np.any(q[:10]) and not np.any(q[10:])
