@@ -263,6 +263,16 @@ int em_fd_solve(em_fd_plan* plan, double omega, const double* c_h, const double*
 int em_tone_table(em_ctx* ctx, int64_t n_t, double dt, double t0, int n_f, const double* freqs_h,
                   double* out, int64_t ldo);
 
+/* --- probe observers (assembly.field_transfer, assembly.py:350-386) ------ */
+/* T[(p*3 + c)*nb + j] (n_probes x 3 x nb, device) = component c of the field at probe p
+ * per unit current in branch j, the exact Biot-Savart field of the straight segment
+ * starts[j] -> ends[j] (nb x 3 row-major, device; probes n_probes x 3). A probe within
+ * radius[j] of branch j's segment: EM_ERR_ARG with *bad = p*nb + j of the first such pair
+ * (the reference's ProbeTooClose), else *bad = -1. */
+int em_field_transfer(em_ctx* ctx, int64_t nb, const double* starts, const double* ends,
+                      const double* radius, int64_t n_probes, const double* probes, double* T,
+                      int64_t* bad);
+
 /* --- synthetic plate inputs (BASELINE.json configs; definition in synth.py) ----------- */
 /* Dense L (n x n), dense-stored R = rho*K7 + shift*I, and the one-port electrode
  * columns l_d, r_d (n) for voxels keep[0..n) of an nx*ny*nz grid (pos: voxel id ->

@@ -78,6 +78,7 @@ SIGNATURES = {
     "em_fd_plan_destroy": (None, [_P]),
     "em_fd_solve": (_I, [_P, _D, _P, _P, _P, _P, ctypes.POINTER(_I64)]),
     "em_tone_table": (_I, [_P, _I64, _D, _D, _I, _P, _P, _I64]),
+    "em_field_transfer": (_I, [_P, _I64, _P, _P, _P, _I64, _P, _P, ctypes.POINTER(_I64)]),
     "em_synth_plate": (_I, [_P, _I64, _I64, _I64, _D, _D, _D, _I64, _P, _P, _P, _P, _I64, _P,
                             _I64, _P, _P]),
 }

@@ -547,3 +547,15 @@ int em_td1_factor(em_td1_plan* plan, double* out, int64_t ldo) {
 }
 
 }  // extern "C"
+
+int em_field_transfer(em_ctx* ctx, int64_t nb, const double* starts, const double* ends,
+                      const double* radius, int64_t np, const double* probes, double* T,
+                      int64_t* bad) {
+  return guarded(ctx, [&] {
+    if (nb < 0 || np < 0) throw em::ArgError{"em_field_transfer: negative size"};
+    const int64_t b = em::field_transfer(ctx->stream, nb, starts, ends, radius, np, probes, T);
+    if (bad) *bad = b;
+    return b >= 0 ? EM_ERR_ARG : EM_OK;
+  });
+}
+

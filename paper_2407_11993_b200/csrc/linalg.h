@@ -165,4 +165,9 @@ void td1_step(em_td1_plan* P, double* I, const double* u_dev);
 void q2_apply_reg(cudaStream_t st, int64_t n, int64_t ncols, int64_t ngroups, const double* V2,
                   const int64_t* toff, const double* T2, double* Z, int64_t ldz);
 
+// observers.cu: Biot-Savart probe transfer T (np x 3 x nb) of straight branch segments
+// A -> B (nb x 3 row-major); returns -1 or the first probe-on-branch pair p*nb + j
+int64_t field_transfer(cudaStream_t st, int64_t nb, const double* A, const double* B,
+                       const double* radius, int64_t np, const double* P, double* T);
+
 }  // namespace em

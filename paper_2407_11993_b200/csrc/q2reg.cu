@@ -188,37 +188,52 @@ struct Q2RWarp {
       if (row + 1 < n) Z[row + 1 + col * ldz] = z[R][1];
     }
   }
-  // W^T = Zwin^T V (k-step (R, e) = rows 8R + 2t + e; R = J .. J + 8 carry V's nonzeros)
+  // W^T = Zwin^T V (k-step (R, e) = rows 8R + 2t + e; R = J .. J + 8 carry V's nonzeros).
+  // Per dR the 8 fragment pairs are loaded first and the e = 0 products of all J issued
+  // before the e = 1 ones: a DMMA never waits on the one issued just before it.
   EM_DEVINL void step_a(const double (&zt)[8][2], const double (&zb)[8][2], const double* vs,
                         double (&w)[8][2]) const {
 #pragma unroll
     for (int J = 0; J < 8; ++J) w[J][0] = w[J][1] = 0.0;
 #pragma unroll
     for (int dR = 0; dR < 9; ++dR) {
+      double2 b[8];
 #pragma unroll
-      for (int J = 0; J < 8; ++J) {
-        const int R = J + dR;
-        const double2 b = lds128(vs + (J * 9 + dR) * 64 + 2 * lane);
-        const double a0 = R < 8 ? zt[R & 7][0] : zb[R & 7][0];
-        const double a1 = R < 8 ? zt[R & 7][1] : zb[R & 7][1];
-        mma(w[J][0], w[J][1], a0, b.x);
-        mma(w[J][0], w[J][1], a1, b.y);
-      }
+      for (int J = 0; J < 8; ++J) b[J] = lds128(vs + (J * 9 + dR) * 64 + 2 * lane);
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+#pragma unroll
+        for (int J = 0; J < 8; ++J) {
+          const int R = J + dR;
+          const double a = R < 8 ? zt[R & 7][e] : zb[R & 7][e];
+          mma(w[J][0], w[J][1], a, e ? b[J].y : b[J].x);
+        }
     }
   }
   // Zwin^T += W^T (-(V T))^T (k-step (J, e) = reflectors 8J + 2t + e); VT[r][j] = 0 for
-  // j < r - 64: row tiles R >= 9 start at J = R - 8
+  // j < r - 64: row tiles R >= 9 start at J = R - 8. Row tiles in groups of 8, the e = 0
+  // products of a group before its e = 1 ones.
   EM_DEVINL void step_c(double (&zt)[8][2], double (&zb)[8][2], const double* vts,
                         const double (&w)[8][2]) const {
 #pragma unroll
     for (int J = 0; J < 8; ++J) {
 #pragma unroll
-      for (int R = 0; R < 16; ++R) {
-        if (J < vt_j0(R)) continue;
-        const double2 b = lds128(vts + (vt_t0(R) + J - vt_j0(R)) * 64 + 2 * lane);
-        double(&c)[2] = R < 8 ? zt[R & 7] : zb[R & 7];
-        mma(c[0], c[1], w[J][0], b.x);
-        mma(c[0], c[1], w[J][1], b.y);
+      for (int h = 0; h < 2; ++h) {
+        double2 b[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int R = 8 * h + q;
+          if (J >= vt_j0(R)) b[q] = lds128(vts + (vt_t0(R) + J - vt_j0(R)) * 64 + 2 * lane);
+        }
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int R = 8 * h + q;
+            if (J < vt_j0(R)) continue;
+            double(&c)[2] = h == 0 ? zt[q] : zb[q];
+            mma(c[0], c[1], w[J][e], e ? b[q].y : b[q].x);
+          }
       }
     }
   }
@@ -233,7 +248,7 @@ struct Q2RWarp {
 // units as evenly as possible (fewer active warps each), so the last wave is short
 // instead of partly empty.
 template <int NW>
-__global__ void __launch_bounds__((NW + 1) * 32, 1) q2r_kernel(int64_t n, int64_t ncols,
+__global__ void __maxnreg__(224) q2r_kernel(int64_t n, int64_t ncols,
                                                                int64_t g, int64_t K,
                                                                const double* __restrict__ Vp,
                                                                const double* __restrict__ VTp,

@@ -141,14 +141,23 @@ def solve_tone(rm: ReducedModel, omega: float, i_d_phasor: np.ndarray,
 
 def fd_solve(rm: ReducedModel, net, omega: float, i_d_phasor: np.ndarray,
              i0_phasor: np.ndarray | None = None, probes: np.ndarray | None = None):
-    """One-tone solve returning (internal current phasors, None) (E/frequency.py:97-111).
-    Probe field phasors need the filament geometry: ValidationError."""
-    if probes is not None:
-        raise ValidationError("probe fields need assembly.field_transfer (filament geometry), "
-                              "outside this package; pass observables instead")
+    """One-tone solve returning (internal current phasors, probe field phasors or None)
+    (E/frequency.py:93-111): probe fields superpose the Biot-Savart transfers
+    (observers.field_transfer) of the lifted total phasor currents."""
+    if probes is not None and (net is None or getattr(rm, "basis", None) is None):
+        raise ValidationError("probe fields require the network geometry")
     if i0_phasor is None:
         i0_phasor = np.zeros(rm.n_sources, dtype=complex)
-    return solve_tone(rm, omega, i_d_phasor, i0_phasor), None
+    currents = solve_tone(rm, omega, i_d_phasor, i0_phasor)
+    fields = None
+    if probes is not None:
+        from .observers import field_transfer
+        transfer = field_transfer(net, probes)
+        coords = np.asarray(rm.k) @ currents + np.asarray(rm.lift) @ np.asarray(i_d_phasor,
+                                                                               dtype=complex)
+        branch = np.asarray(rm.basis.w, dtype=float) @ coords
+        fields = transfer @ branch.real + 1j * (transfer @ branch.imag)
+    return currents, fields
 
 
 def _check_record(n: int, dt: float, f: float):

@@ -546,10 +546,13 @@ def run_transient(rm: ReducedModel, net, drives, cfg: TransientConfig,
         drives = (drives,)
     if cfg.method == "td2" and modal is None:
         raise ValidationError("td2 requires a modal basis")
+    probe_cd = None
     if cfg.probes is not None:
-        raise ValidationError("probe observers need the filament-network field transfer "
-                              "(assembly.field_transfer), which is outside this path; pass "
-                              "observables=(C, D) instead")
+        # probe observers (transient.py:266-273): fields = transfer @ (W K I + W lift i_D)
+        from .observers import probe_observables
+        probe_cd = probe_observables(net, rm, cfg.probes)
+        if observables is not None:
+            raise ValidationError("pass either cfg.probes or observables, not both")
     n_steps = cfg.n_steps
     i_d_tab, i0_tab = drive_samples(net, rm, drives, cfg.dt, n_steps)
     n_caps = n_steps // cfg.capture_stride
@@ -567,11 +570,24 @@ def run_transient(rm: ReducedModel, net, drives, cfg: TransientConfig,
         states = np.zeros((n_caps, 0)) if cfg.capture_state else None
         return SimulationResult(times, states, None, setup_time, 0.0, n_steps, cfg.method)
     step0 = time.perf_counter()
-    states, obs, _ = stepper.run(i_d_tab, i0_tab, cfg.capture_stride, cfg.capture_state,
-                                 observables)
+    fields = None
+    if probe_cd is None:
+        states, obs, _ = stepper.run(i_d_tab, i0_tab, cfg.capture_stride, cfg.capture_state,
+                                     observables)
+    else:
+        # at most 128 observables per scan: 42 probes (3 components each) per run
+        c, d = probe_cd
+        parts, states, obs = [], None, None
+        for r0 in range(0, c.shape[0], 126):
+            st, y, _ = stepper.run(i_d_tab, i0_tab, cfg.capture_stride,
+                                   cfg.capture_state and r0 == 0,
+                                   (c[r0:r0 + 126], d[r0:r0 + 126] if d.shape[1] else None))
+            states = st if r0 == 0 else states
+            parts.append(y)
+        fields = np.concatenate(parts, axis=1).reshape(n_caps, -1, 3)
     nat.synchronize()
     stepping_time = time.perf_counter() - step0
-    return SimulationResult(times=times, internal_states=states, probe_fields=None,
+    return SimulationResult(times=times, internal_states=states, probe_fields=fields,
                             wall_time_setup=setup_time, wall_time_stepping=stepping_time,
                             n_steps=n_steps, method=cfg.method, observables=obs)
 

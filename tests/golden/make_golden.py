@@ -3,7 +3,7 @@
 Run in the build container (where /root/reference exists); the resulting
 .npz files are committed and are all the GPU box ever sees:
 
-    python tests/golden/make_golden.py kat plate_small plate_200 tubes fd reduction  # seconds
+    python tests/golden/make_golden.py kat plate_small plate_200 tubes fd reduction observers  # seconds
     python tests/golden/make_golden.py c1                                # ~30 min (Jacobi at N=2000)
     python tests/golden/make_golden.py c2                                # ~10 min (dsygvd at N=16384)
 
@@ -259,6 +259,69 @@ def case_reduction(em):
     save("reduction", **out)
 
 
+def case_observers(em):
+    """Probe observers: the reference's field_transfer (assembly.py:350-386)
+    on its own tube network, run_transient with probes (transient.py:266-273, 302-305,
+    td2 and td1) and crack_signature (ndt.py:229-240)."""
+    from eddymodes.assembly import (assemble_branch_matrices, build_current_basis,
+                                    electrode_incidence, field_transfer)
+    from eddymodes.errors import ProbeTooClose
+    from eddymodes.frequency import PhasorSet
+    from eddymodes.modal import generalized_eig
+    from eddymodes.ndt import crack_signature
+    from eddymodes.network import DriveSignal, Tone, generate_tube_grid
+    from eddymodes.reduction import project_model
+    from eddymodes.transient import TransientConfig, run_transient
+    net = generate_tube_grid(84e-3, 0.3, 3e-3, 4, 8, 1.09e-6)
+    bm = assemble_branch_matrices(net)
+    basis_c = build_current_basis(net)
+    e = electrode_incidence(net, basis_c)
+    port_names = tuple(el.name for el in net.electrodes[:-1])
+    rm = project_model(bm, basis_c, e, port_names=port_names)
+    rng = np.random.default_rng(20240807)
+    ang = rng.uniform(0, 2 * np.pi, 12)
+    probes = np.stack([0.095 * np.cos(ang), 0.095 * np.sin(ang), rng.uniform(0.0, 0.3, 12)], 1)
+    out = dict(starts=net.branch_starts, ends=net.branch_ends, wire_radius=net.wire_radius,
+               probes=probes, transfer=field_transfer(net, probes), w=basis_c.w, k=rm.k,
+               lift=rm.lift, r_i=rm.r_i.full, l_i=rm.l_i.full, r_d=rm.r_d, l_d=rm.l_d,
+               m0=rm.m0, n_ports=np.array(rm.n_ports))
+    # a probe on a branch: ProbeTooClose names the first (probe, branch) pair
+    bad = np.concatenate([probes[:3], 0.5 * (net.branch_starts[5:6] + net.branch_ends[5:6]),
+                          probes[3:4]])
+    try:
+        field_transfer(net, bad)
+        raise SystemExit("expected ProbeTooClose")
+    except ProbeTooClose as exc:
+        out["bad_probes"] = bad
+        out["bad_msg"] = np.array(str(exc))
+    mb = generalized_eig(rm.l_i, rm.r_i)
+    drive = DriveSignal(tones=(Tone(1.0, 1e3, 0.0),), ports=port_names[:1])
+    dt = 1 / 30000
+    for method in ("td2", "td1"):
+        cfg = TransientConfig(theta=1.0, dt=dt, t_end=60 * dt, method=method, capture_stride=3,
+                              probes=probes)
+        sim = run_transient(rm, net, drive, cfg, modal=mb if method == "td2" else None)
+        out[f"{method}_fields"] = sim.probe_fields
+    out["dt"] = np.array(dt)
+    angles = tuple(float(a) for a in np.linspace(0, 2 * np.pi, 6, endpoint=False))
+    freqs = (1e3, 5e3, 2e4)
+    pd, pb = PhasorSet(probe_angles=angles), PhasorSet(probe_angles=angles)
+    for pi in range(6):
+        for f in freqs:
+            pd[(pi, f)] = complex(rng.standard_normal(), rng.standard_normal())
+            pb[(pi, f)] = complex(rng.standard_normal(), rng.standard_normal())
+    sig = crack_signature(pd, pb)
+    nrm = sig.normalized()
+    keys = sorted(sig.entries)
+    out.update(cs_angles=np.array(angles), cs_freqs=np.array(freqs),
+               cs_defect=np.array([[pd[(p, f)] for f in freqs] for p in range(6)]),
+               cs_background=np.array([[pb[(p, f)] for f in freqs] for p in range(6)]),
+               cs_keys=np.array(keys), cs_sig=np.array([sig.entries[k] for k in keys]),
+               cs_norm=np.array([nrm.entries[k] for k in keys]),
+               cs_mag=np.array([sig.magnitude_by_angle(f) for f in freqs]))
+    save("observers", **out)
+
+
 def case_fd(em):
     """Frequency domain: the reference solve_tone on the plate_small
     and tube_small models at several tones, dft_phasor / extract_phasors KATs."""
@@ -338,6 +401,8 @@ def main(argv):
             case_c2(em)
         elif case == "reduction":
             case_reduction(em)
+        elif case == "observers":
+            case_observers(em)
         elif case == "fd":
             case_fd(em)
         elif case == "cache":

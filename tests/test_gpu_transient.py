@@ -393,7 +393,8 @@ def test_selective_mode_integration():
                                cv=(g["c"] @ basis.v)[:, sel])
     assert rel_l2(y_sel, y_ref) < 1e-12
     assert np.array_equal(q_sel[40:], np.zeros(160)) and rel_l2(q_sel[:40], q_full[:40]) < 1e-12
-    assert rel_l2(s_sel, q_sel[:40] @ basis.v[:, :40].T) < 1e-12
+    # the last capture (replay pass) against the carried final state: two arithmetic paths
+    assert rel_l2(s_sel[-1], basis.v[:, :40] @ q_sel[:40]) < 1e-8
     errs = [rel_l2(transient.Td2Stepper(rm, basis, dt, 0.5, modes=transient.select_modes(
         basis, count=c)).run(i_d, i0, capture_state=False, observables=obs)[1], y_full)
         for c in (10, 50, 150, 200)]
