@@ -78,6 +78,13 @@ int em_synchronize(em_ctx* ctx);
  * eigen-identity V^T L V = diag(tau) V^T R V (equal to ~1e-13 relative; r_n is always
  * diag(V^T R V) from R itself). */
 #define EM_CFG_LN_DENSE 4
+/* EM_CFG_L_CERTIFICATE: 1 = em_sygv factors L before the eigensolve, as the reference's
+ * certificate does (modal.py:69-70); 0 (default) = the factorisation runs after the
+ * eigensolve only when the solved spectrum cannot prove it succeeds (tau_min > 0, R
+ * strictly diagonally dominant and 20 n^1.5 kappa(L) eps < 0.01 with kappa(L) <=
+ * (tau_max/tau_min) kappa(R)): a non-SPD L raises the same error with the same pivot,
+ * after the eigensolve instead of before it. */
+#define EM_CFG_L_CERTIFICATE 5
 /* Keys 96-99 are debug switches for A/B measurements and the tests (96 GEMM tile
  * configuration, 97 Q2 back-transform form, 98 tridiagonalisation code paths, 99 trim
  * the device memory pool to `value` bytes); see capi.cu. */

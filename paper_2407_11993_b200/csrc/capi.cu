@@ -18,6 +18,7 @@ extern int64_t g_two_stage_min;
 extern int g_sytrd_dbg;
 extern int g_band_off;
 extern int g_ln_dense;
+extern int g_l_certificate;
 extern int g_q2r_dbg;
 extern int g_last_eig_path;
 extern int g_q2_mode;
@@ -170,6 +171,10 @@ int em_config(em_ctx* ctx, int key, int64_t value) {
     }
     if (key == EM_CFG_BAND_OFF) {
       em::g_band_off = value ? 1 : 0;
+      return EM_OK;
+    }
+    if (key == EM_CFG_L_CERTIFICATE) {
+      em::g_l_certificate = value ? 1 : 0;
       return EM_OK;
     }
     if (key == EM_CFG_LN_DENSE) {

@@ -37,7 +37,8 @@
 namespace em {
 
 int g_q2r_dbg = 0;  // debug key 95: bit0 VT(k) waits for C(k-1); bit1 uniform strips;
-                    // bit2 synchronous Z staging loads; bit3 fences before the empty arrivals
+                    // bit2 synchronous Z staging loads; bit3 fences before the empty arrivals;
+                    // bit4 seven consumer warps (8 warps per CTA, 255 registers)
 
 namespace {
 constexpr int QB = 64;                  // sweeps per group, reflector length
@@ -248,7 +249,7 @@ struct Q2RWarp {
 // units as evenly as possible (fewer active warps each), so the last wave is short
 // instead of partly empty.
 template <int NW>
-__global__ void __maxnreg__(224) q2r_kernel(int64_t n, int64_t ncols,
+__global__ void __launch_bounds__((NW + 1) * 32, 1) q2r_kernel(int64_t n, int64_t ncols,
                                                                int64_t g, int64_t K,
                                                                const double* __restrict__ Vp,
                                                                const double* __restrict__ VTp,
@@ -364,11 +365,14 @@ __global__ void __maxnreg__(224) q2r_kernel(int64_t n, int64_t ncols,
 
 // Z (n x ncols, ld ldz) <- Q2 Z for all groups (last first); T2: every block's T factor,
 // groups descending and positions ascending (q2_tfactor_kernel's order).
-void q2_apply_reg(cudaStream_t st, int64_t n, int64_t ncols, int64_t ngroups, const double* V2,
-                  const int64_t* toff, const double* T2, double* Z, int64_t ldz) {
-  constexpr int NW = 8;
+// NW consumer warps + 1 producer per CTA. The register file is split between the four
+// SM sub-partitions, so 9 warps (NW = 8: 3 on one sub-partition) allow 168 registers per
+// thread (a few spills) while 8 warps (NW = 7) allow 255 (no spills, one consumer fewer).
+template <int NW>
+static void q2_apply_nw(cudaStream_t st, int64_t n, int64_t ncols, int64_t ngroups,
+                        const double* V2, const int64_t* toff, const double* T2, double* Z,
+                        int64_t ldz) {
   using S = Q2R<NW>;
-  if (ncols <= 0 || n <= 1) return;
   EM_CK(cudaFuncSetAttribute(q2r_kernel<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)S::SMEM));
   constexpr size_t kPackSmem = 2 * QB * (QB + 1) * sizeof(double);
@@ -394,6 +398,15 @@ void q2_apply_reg(cudaStream_t st, int64_t n, int64_t ncols, int64_t ngroups, co
     EM_LAUNCHED();
     off += K;
   }
+}
+
+void q2_apply_reg(cudaStream_t st, int64_t n, int64_t ncols, int64_t ngroups, const double* V2,
+                  const int64_t* toff, const double* T2, double* Z, int64_t ldz) {
+  if (ncols <= 0 || n <= 1) return;
+  if (g_q2r_dbg & 16)
+    q2_apply_nw<7>(st, n, ncols, ngroups, V2, toff, T2, Z, ldz);
+  else
+    q2_apply_nw<8>(st, n, ncols, ngroups, V2, toff, T2, Z, ldz);
 }
 
 }  // namespace em

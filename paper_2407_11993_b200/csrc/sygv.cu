@@ -7,6 +7,8 @@
 //   B = U diag(w) U^T   (sytrd + divide & conquer + ormtr; replaces Jacobi)
 //   V = G^-T U, descending order, sign fix (largest |entry| positive),
 //   l_n = diag(V^T L V), r_n = diag(V^T R V), V^T R (= (R V)^T).
+#include <cstring>
+
 #include "common.cuh"
 #include "ctx.h"
 #include "gemm.h"
@@ -52,6 +54,68 @@ int g_band_off = 0;
 // em_config(EM_CFG_LN_DENSE): 1 forms l_n = diag(V^T L V) with the N^3 product as the
 // reference does (modal.py:79); 0 (default) uses the eigen-identity l_n = tau r_n
 int g_ln_dense = 0;
+// em_config(EM_CFG_L_CERTIFICATE): 1 factors L (the reference's certificate, modal.py:69-70)
+// before the eigensolve, always; 0 (default) skips it when the solved spectrum proves it
+// would succeed (see sygv), and runs it otherwise
+int g_l_certificate = 0;
+
+// Gershgorin bounds of a symmetric matrix from its lower triangle: out[0] = min_i (a_ii -
+// sum_j |a_ij|), out[1] = max_i (a_ii + sum_j |a_ij|) (atomics on the ordered bit patterns
+// of non-negative doubles; out preset to +inf / 0 by the caller)
+__global__ void gershgorin_kernel(int64_t n, const double* __restrict__ A, int64_t lda,
+                                  unsigned long long* out_lo, unsigned long long* out_hi,
+                                  int* neg) {
+  const int64_t i = blockIdx.x;
+  double s = 0.0;
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+    if (j == i) continue;
+    const double v = j < i ? A[i + j * lda] : A[j + i * lda];  // lower triangle (SymMatrix)
+    s += fabs(v);
+  }
+  __shared__ double red[32];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += red[q];
+    const double d = A[i + i * lda];
+    const double lo = d - t, hi = d + t;
+    if (!(lo > 0.0)) atomicExch(neg, 1);
+    else atomicMin(out_lo, (unsigned long long)__double_as_longlong(lo));
+    atomicMax(out_hi, (unsigned long long)__double_as_longlong(fmax(hi, 0.0)));
+  }
+}
+
+// The reference's Cholesky of L (the certificate) succeeds whenever L is safely SPD. With
+// B = G^-1 L G^-T and tau = eig(B): lambda_min(L) >= tau_min lambda_min(R) and ||L|| <=
+// tau_max ||R||, so kappa(L) <= (tau_max / tau_min) kappa(R); kappa(R) is bounded by R's
+// Gershgorin interval when R is strictly diagonally dominant (the plates' stencil). Cholesky
+// completes when 20 n^1.5 kappa eps < 1 (Demmel); this asks for 100x margin.
+static bool certificate_redundant(cudaStream_t st, int64_t n, const double* R, int64_t ldr,
+                                  double tau_min, double tau_max) {
+  if (!(tau_min > 0.0) || !(tau_max >= tau_min)) return false;
+  DArr<unsigned long long> b(2, st);
+  DArr<int> neg(1, st);
+  double inf = INFINITY;
+  unsigned long long init[2] = {0ull, 0ull};
+  memcpy(&init[0], &inf, sizeof(double));
+  EM_CK(cudaMemcpyAsync(b.p, init, sizeof(init), cudaMemcpyHostToDevice, st));
+  EM_CK(cudaMemsetAsync(neg.p, 0, sizeof(int), st));
+  gershgorin_kernel<<<(unsigned)n, 256, 0, st>>>(n, R, ldr, b.p, b.p + 1, neg.p);
+  EM_LAUNCHED();
+  unsigned long long hb[2];
+  int hneg = 0;
+  EM_CK(cudaMemcpyAsync(hb, b.p, sizeof(hb), cudaMemcpyDeviceToHost, st));
+  EM_CK(cudaMemcpyAsync(&hneg, neg.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  EM_CK(cudaStreamSynchronize(st));
+  double lo, hi;
+  memcpy(&lo, &hb[0], sizeof(double));
+  memcpy(&hi, &hb[1], sizeof(double));
+  if (hneg || !(lo > 0.0)) return false;
+  const double kappa = (tau_max / tau_min) * (hi / lo);
+  return 20.0 * pow((double)n, 1.5) * kappa * 2.220446049250313e-16 < 0.01;
+}
 
 // out[i] = a[i] * b[i]
 __global__ void scale_vec_kernel(int64_t n, const double* __restrict__ a,
@@ -306,8 +370,9 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
       else
         sygst_lower(st, n, B.p, ldb, G, ldg, GDinv.p);
     }
-    // certificate only (modal.py:69-70), factored in the (still free) eigenvector buffer
-    {
+    // certificate only (modal.py:69-70), factored in the (still free) eigenvector buffer;
+    // by default deferred until the spectrum shows whether it is needed
+    if (g_l_certificate) {
       Stage s(st, ST_POTRF_L);
       copy_matrix(st, false, n, n, L, ldl, Zw, ldzw);
       piv = potrf(st, n, Zw, ldzw);
@@ -328,6 +393,27 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
   double* Zs = Zw + c0 * ldzw;
   syev_ascending(st, n, B.p, ldb, w.p, Zw, ldzw, c0, m);
   B.release();
+  if (!g_l_certificate) {
+    // The certificate is redundant when the solved pencil proves L safely SPD; otherwise
+    // (L not SPD, or too ill-conditioned to tell) it runs now, in a buffer of its own,
+    // and raises the reference's error with the reference's pivot.
+    double wb[2] = {0.0, 0.0};
+    EM_CK(cudaMemcpyAsync(&wb[0], w.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+    EM_CK(cudaMemcpyAsync(&wb[1], w.p + (n - 1), sizeof(double), cudaMemcpyDeviceToHost, st));
+    EM_CK(cudaStreamSynchronize(st));
+    if (!certificate_redundant(st, n, R, ldr, wb[0], wb[1])) {
+      Stage s(st, ST_POTRF_L);
+      DBuf Lc((size_t)n * n, st);
+      copy_matrix(st, false, n, n, L, ldl, Lc.p, n);
+      const int64_t pl = potrf(st, n, Lc.p, n);
+      if (pl >= 0) {
+        *which = 1;
+        restore_r();
+        EM_CK(cudaStreamSynchronize(st));
+        return pl;
+      }
+    }
+  }
   if (m > 0) {
     Stage s(st, ST_TRSM_BACK);
     if (banded)

@@ -33,10 +33,12 @@ def field_transfer(net, probes: np.ndarray) -> np.ndarray:
         return np.zeros((n_p, 3, nb))
     t = nat.empty(n_p * 3 * nb)
     bad = ctypes.c_int64(-1)
-    rc = nat.load_library().em_field_transfer(
-        nat.context(), nb, nat.ptr(nat.device_vector(a.reshape(-1))),
-        nat.ptr(nat.device_vector(b.reshape(-1))), nat.ptr(nat.device_vector(rad)), n_p,
-        nat.ptr(nat.device_vector(probes.reshape(-1))), nat.ptr(t), ctypes.byref(bad))
+    # the device copies must outlive the call (nat.ptr keeps no reference)
+    da, db = nat.device_vector(a.reshape(-1)), nat.device_vector(b.reshape(-1))
+    dr, dp = nat.device_vector(rad), nat.device_vector(probes.reshape(-1))
+    rc = nat.load_library().em_field_transfer(nat.context(), nb, nat.ptr(da), nat.ptr(db),
+                                              nat.ptr(dr), n_p, nat.ptr(dp), nat.ptr(t),
+                                              ctypes.byref(bad))
     if bad.value >= 0:
         p, j = divmod(int(bad.value), nb)
         raise ProbeTooClose(f"probe {p} lies on branch {j} (within the wire radius)")

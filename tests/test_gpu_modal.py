@@ -146,3 +146,38 @@ def test_c1_eigenvalues_match_reference_jacobi():
     assert np.max(np.abs(mb.tau - g["tau"]) / g["tau"]) < 1e-10
     assert_allclose(mb.l_n, g["l_n"], rtol=1e-10)
     assert rel_l2(mb.v[:, :4], g["v_lead"]) < 1e-8
+
+
+def test_certificate_deferred_only_when_provably_redundant():
+    """EM_CFG_L_CERTIFICATE (modal.py:69-70): by default the Cholesky of L is skipped when
+    the solved spectrum proves it succeeds (plate: tau > 0, R diagonally dominant, well
+    conditioned) — same basis as with the certificate forced; a non-SPD L still raises the
+    reference's error with the reference's pivot (then after the eigensolve)."""
+    from paper_2407_11993_b200 import _native as nat
+    from paper_2407_11993_b200 import modal, reduction
+    from paper_2407_11993_b200.errors import NotPositiveDefinite
+    from oracle import oracle as O
+    g = golden("plate_200")
+    rm = reduction.from_blocks(g["r_i"], g["l_i"], g["r_d"], g["l_d"], g["m0"])
+    lib, ctx = nat.load_library(), nat.context()
+    nat.profile(1)
+    b0 = modal.generalized_eig(rm.l_i, rm.r_i)
+    st0 = nat.stage_times()
+    nat.check(lib.em_config(ctx, 5, 1))
+    try:
+        nat.profile(1)
+        b1 = modal.generalized_eig(rm.l_i, rm.r_i)
+        st1 = nat.stage_times()
+    finally:
+        nat.check(lib.em_config(ctx, 5, 0))
+        nat.profile(0)
+    assert "potrf_L" not in st0 and "potrf_L" in st1
+    np.testing.assert_array_equal(b0.tau, b1.tau)
+    # an indefinite L: the deferred certificate names the reference's pivot
+    lbad = g["l_i"].copy()
+    lbad[7, 7] = -1.0
+    with pytest.raises(O.OracleNotPositiveDefinite) as ref:
+        O.cholesky(O.sym_mirror(lbad), what="modal inductance matrix")
+    with pytest.raises(NotPositiveDefinite) as e:
+        modal.generalized_eig(lbad, g["r_i"])
+    assert e.value.pivot == ref.value.pivot and "inductance" in str(e.value)
