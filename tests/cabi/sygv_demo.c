@@ -85,8 +85,38 @@ int main(void) {
     q += ((-dt * rn[0] * q + f) / c) / c;
     err = fmax(err, fabs(q - y[k]) / (fabs(q) + 1e-300));
   }
-  printf("n %lld tau0 %.17g taulast %.17g res %.3e td2_relerr %.3e launches %lld\n",
-         (long long)n, tau[0], tau[n - 1], res, err, (long long)em_launch_count(ctx));
+  /* the two "ranks" of a column-sharded solve (em_sygv_range): modes [0, h) and [h, n)
+   * must equal the corresponding columns of the full solve */
+  const int64_t h = 17;
+  double *dL = NULL, *dR = NULL, *dtau = NULL, *dV = NULL, *dln = NULL, *drn = NULL;
+  cudaMalloc((void**)&dL, n * n * 8);
+  cudaMalloc((void**)&dR, n * n * 8);
+  cudaMalloc((void**)&dtau, n * 8);
+  cudaMalloc((void**)&dV, n * n * 8);
+  cudaMalloc((void**)&dln, n * 8);
+  cudaMalloc((void**)&drn, n * 8);
+  cudaMemcpy(dL, L, n * n * 8, cudaMemcpyHostToDevice);
+  cudaMemcpy(dR, R, n * n * 8, cudaMemcpyHostToDevice);
+  double shard_err = 0.0, *Vs = malloc(n * n * 8), *lns = malloc(n * 8);
+  for (int r = 0; r < 2; ++r) {
+    const int64_t lo = r ? h : 0, hi = r ? n : h;
+    CK(em_sygv_range(ctx, n, dL, n, dR, n, lo, hi, dtau, dV, n, dln, drn, NULL, n, 0, &piv,
+                     &which));
+    cudaMemcpy(Vs, dV, n * (hi - lo) * 8, cudaMemcpyDeviceToHost);
+    cudaMemcpy(lns, dln, (hi - lo) * 8, cudaMemcpyDeviceToHost);
+    for (int64_t j = lo; j < hi; ++j) {
+      shard_err = fmax(shard_err, fabs(lns[j - lo] - ln[j]) / ln[j]);
+      for (int64_t i = 0; i < n; ++i)
+        shard_err = fmax(shard_err, fabs(Vs[i + (j - lo) * n] - V[i + j * n]));
+    }
+  }
+  int64_t path = 0;
+  CK(em_info(ctx, EM_INFO_EIG_PATH, &path));
+  CK(em_trim(ctx));
+  printf("n %lld tau0 %.17g taulast %.17g res %.3e td2_relerr %.3e launches %lld "
+         "shard_err %.3e path %lld\n",
+         (long long)n, tau[0], tau[n - 1], res, err, (long long)em_launch_count(ctx), shard_err,
+         (long long)path);
   em_td2_plan_destroy(plan);
   em_finalize(ctx);
   return 0;

@@ -45,3 +45,6 @@ def test_c_caller_runs(tmp_path):
     assert float(vals["res"]) < 1e-12
     assert float(vals["td2_relerr"]) < 1e-12
     assert int(vals["launches"]) > 0
+    # em_sygv_range: both column shards equal the full solve's columns (em_info: one-stage)
+    assert float(vals["shard_err"]) < 1e-12
+    assert int(vals["path"]) == 1

@@ -395,10 +395,11 @@ def test_selective_mode_integration():
     assert np.array_equal(q_sel[40:], np.zeros(160)) and rel_l2(q_sel[:40], q_full[:40]) < 1e-12
     # the last capture (replay pass) against the carried final state: two arithmetic paths
     assert rel_l2(s_sel[-1], basis.v[:, :40] @ q_sel[:40]) < 1e-8
-    errs = [rel_l2(transient.Td2Stepper(rm, basis, dt, 0.5, modes=transient.select_modes(
-        basis, count=c)).run(i_d, i0, capture_state=False, observables=obs)[1], y_full)
-        for c in (10, 50, 150, 200)]
-    assert errs[-1] < 1e-14 and errs[0] > errs[1] > errs[2] > errs[3]
+    # linearity: a selection and its complement superpose to the full run
+    rest = np.setdiff1d(np.arange(200), sel)
+    _, y_rest, _ = transient.Td2Stepper(rm, basis, dt, 0.5, modes=rest).run(
+        i_d, i0, capture_state=False, observables=obs)
+    assert rel_l2(y_sel + y_rest, y_full) < 1e-12
     # by time constant, and the per-step API moves only the selected modes
     slow = transient.select_modes(basis, tau_min=float(basis.tau[9]))
     assert np.array_equal(slow, np.arange(10))
