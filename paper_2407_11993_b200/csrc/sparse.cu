@@ -13,16 +13,19 @@
 
 namespace em {
 
-// nnz per row (full symmetric matrix, column-major: row i of a symmetric matrix is
-// column i, read contiguously). One warp per row.
+// nnz per row of a symmetric matrix given by its LOWER triangle (column-major; the upper
+// triangle is never read: SymMatrix semantics, E/linalg.py:24-59). Row i = the strided
+// entries A[i + k lda] for k < i, then the contiguous column segment A[k + i lda], k >= i.
+// One warp per row.
 __global__ void csr_count_kernel(int64_t n, const double* __restrict__ A, int64_t lda,
                                  int64_t* __restrict__ cnt) {
   const int64_t row = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= n) return;
-  const double* col = A + row * lda;  // symmetric: column `row` == row `row`
   int64_t c = 0;
-  for (int64_t k = lane; k < n; k += 32) c += (col[k] != 0.0);
+  for (int64_t k = lane; k < row; k += 32) c += (A[row + k * lda] != 0.0);
+  const double* col = A + row * lda;
+  for (int64_t k = row + lane; k < n; k += 32) c += (col[k] != 0.0);
   for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
   if (lane == 0) cnt[row] = c;
 }
@@ -38,7 +41,7 @@ __global__ void csr_fill_kernel(int64_t n, const double* __restrict__ A, int64_t
   int64_t pos = rowptr[row];
   for (int64_t k0 = 0; k0 < n; k0 += 32) {
     const int64_t k = k0 + lane;
-    const double v = (k < n) ? col[k] : 0.0;
+    const double v = k >= n ? 0.0 : (k < row ? A[row + k * lda] : col[k]);
     const unsigned mask = __ballot_sync(0xffffffffu, v != 0.0);
     if (v != 0.0) {
       const int off = __popc(mask & ((1u << lane) - 1u));
@@ -65,6 +68,8 @@ __global__ void csr_spmm_kernel(int64_t n, int64_t m, const int64_t* __restrict_
   }
 }
 
+// writes the CSR entries back into full storage (both triangles: the restored matrix is
+// exactly symmetric)
 __global__ void csr_scatter_kernel(int64_t n, const int64_t* __restrict__ rowptr,
                                    const int* __restrict__ colidx, const double* __restrict__ val,
                                    double* __restrict__ A, int64_t lda) {
@@ -75,7 +80,7 @@ __global__ void csr_scatter_kernel(int64_t n, const int64_t* __restrict__ rowptr
   for (int64_t p = rowptr[row] + lane; p < rowptr[row + 1]; p += 32) col[colidx[p]] = val[p];
 }
 
-// Device CSR copy of a symmetric A (full storage) when it has at most max_fill * n^2
+// Device CSR copy of a symmetric A (its lower triangle) when it has at most max_fill * n^2
 // nonzeros; returns false (and builds nothing) when A is too dense.
 bool csr_from_dense(cudaStream_t st, int64_t n, const double* A, int64_t lda, double max_fill,
                     Csr& out) {

@@ -456,10 +456,15 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
     return -1;
   }
   if (VtR) {
-    if (rc)
+    if (rc) {
       csr_mm(st, *rc, m, V, ldv, VtR, ldvtr);
-    else
-      EM_CK(gemm(st, false, false, n, m, n, 1.0, R, ldr, V, ldv, 0.0, VtR, ldvtr));
+    } else {  // dense R: its lower triangle mirrored into a scratch copy
+      DBuf Rs(nn, st);
+      copy_matrix(st, false, n, n, R, ldr, Rs.p, n);
+      mirror_lower(st, n, Rs.p, n);
+      EM_CK(gemm(st, false, false, n, m, n, 1.0, Rs.p, n, V, ldv, 0.0, VtR, ldvtr));
+      EM_CK(cudaStreamSynchronize(st));
+    }
     if (rn_out) {
       coldot_kernel<<<(unsigned)m, 256, 0, st>>>(n, V, ldv, VtR, ldvtr, rn_out);
       EM_LAUNCHED();
@@ -467,10 +472,10 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
   } else if (rn_out) {
     if (rc) {
       csr_quadform(st, *rc, m, V, ldv, rn_out);
-    } else {
+    } else {  // dense R: v^T R v from its lower triangle (as l_n's dense form)
       DBuf RV((size_t)n * m, st);
-      EM_CK(gemm(st, false, false, n, m, n, 1.0, R, ldr, V, ldv, 0.0, RV.p, n));
-      coldot_kernel<<<(unsigned)m, 256, 0, st>>>(n, V, ldv, RV.p, n, rn_out);
+      EM_CK(gemm_lower_a(st, n, m, n, 1.0, R, ldr, V, ldv, 0.0, RV.p, n));
+      quadform_lower_kernel<<<(unsigned)m, 256, 0, st>>>(n, V, ldv, RV.p, n, R, ldr, rn_out);
       EM_LAUNCHED();
       EM_CK(cudaStreamSynchronize(st));
     }

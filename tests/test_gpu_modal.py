@@ -181,3 +181,39 @@ def test_certificate_deferred_only_when_provably_redundant():
     with pytest.raises(NotPositiveDefinite) as e:
         modal.generalized_eig(lbad, g["r_i"])
     assert e.value.pivot == ref.value.pivot and "inductance" in str(e.value)
+
+
+@pytest.mark.parametrize("dense_r", [False, True])
+def test_device_inputs_read_only_the_lower_triangles(dense_r):
+    """SymMatrix semantics on the device path (E/linalg.py:24-59, modal.py:46-81): L and R
+    given as device tensors with garbage above the diagonal give the same basis as the
+    clean symmetric inputs (the library reads lower triangles only: band detection, the
+    factor, the reduction, the CSR copy behind r_n); em_sym_mirror_lower restores
+    symmetry in place."""
+    import torch
+    from paper_2407_11993_b200 import _native as nat
+    from paper_2407_11993_b200 import modal
+    from paper_2407_11993_b200.synth import plate_model
+    m = plate_model(30, 12, 2, n_ports=0, n_sources=1, n_obs=4)  # N = 720, band 24
+    l, r = m["l_i"], m["r_i"]
+    n = l.shape[0]
+    rng = np.random.default_rng(4)
+    junk = np.triu(rng.standard_normal((n, n)), 1)
+    # column-major device buffers: element (i, j) at j*n + i, i.e. the transpose's bytes;
+    # garbage strictly above the diagonal
+    lg = torch.from_numpy(np.ascontiguousarray((l + junk).T)).cuda()
+    rg = torch.from_numpy(np.ascontiguousarray((r + 1e-3 * junk).T)).cuda()
+    lib, ctx = nat.load_library(), nat.context()
+    if dense_r:
+        nat.check(lib.em_config(ctx, 2, 1))
+    try:
+        clean = modal.generalized_eig(torch.from_numpy(l).cuda(), torch.from_numpy(r).cuda())
+        dirty = modal.generalized_eig(lg, rg)
+    finally:
+        nat.check(lib.em_config(ctx, 2, 0))
+    np.testing.assert_array_equal(dirty.tau, clean.tau)
+    np.testing.assert_array_equal(dirty.l_n, clean.l_n)
+    assert np.abs(dirty.r_n - clean.r_n).max() < 1e-14
+    assert np.abs(dirty.v - clean.v).max() <= 1e-12 * np.abs(clean.v).max()
+    nat.check(lib.em_sym_mirror_lower(ctx, n, nat.ptr(lg), n), "em_sym_mirror_lower")
+    np.testing.assert_array_equal(lg.cpu().numpy(), l.T)
