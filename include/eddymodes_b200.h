@@ -167,6 +167,18 @@ int em_sygv_range(em_ctx* ctx, int64_t n, const double* L, int64_t ldl, double* 
                   int64_t m_lo, int64_t m_hi, double* tau, double* V, int64_t ldv, double* l_n,
                   double* r_n, double* VtR, int64_t ldvtr, int flags, int64_t* pivot,
                   int* which);
+/* The eigensolve for the transient without forming V ("implicit V"): on entry
+ * Y (n x k, ld ldy) holds operands — the drive columns [R_D | L_D | M0] and the observable
+ * rows C^T —, on exit V^T Y (row j = mode j, descending tau). V^T = U^T Q^T G^-1 is applied
+ * to the k columns (G: R's factor, Q: the tridiagonalisation's reflectors, U: the
+ * tridiagonal eigenvectors), so the 4 n^3 flops that form V are replaced by O(n^2 k).
+ * tau (n) as em_sygv; l_n = tau and r_n = 1 (the identities V^T L V = diag(tau),
+ * V^T R V = I; either may be NULL). Each mode keeps the eigensolver's sign rather than
+ * the reference's sign fix (modal.py:74-78, which needs V): products of two rows of V^T Y
+ * (P_n x CV_n, what the modal scan uses) are unchanged. Flags as em_sygv_ex. */
+int em_sygv_implicit(em_ctx* ctx, int64_t n, const double* L, int64_t ldl, double* R,
+                     int64_t ldr, double* tau, double* Y, int64_t ldy, int64_t k, double* l_n,
+                     double* r_n, int flags, int64_t* pivot, int* which);
 /* em_sygv_ex with L still on the host: the library uploads L_host (n x n, leading
  * dimension n) into the device buffer L (ld ldl) on a copy engine, after the work already
  * queued on the context stream (e.g. R's upload); L is first read by the two-sided

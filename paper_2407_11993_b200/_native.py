@@ -52,6 +52,8 @@ SIGNATURES = {
                         ctypes.POINTER(_I64), ctypes.POINTER(_I)]),
     "em_sygv_range": (_I, [_P, _I64, _P, _I64, _P, _I64, _I64, _I64, _P, _P, _I64, _P, _P, _P,
                            _I64, _I, ctypes.POINTER(_I64), ctypes.POINTER(_I)]),
+    "em_sygv_implicit": (_I, [_P, _I64, _P, _I64, _P, _I64, _P, _P, _I64, _I64, _P, _P, _I,
+                              ctypes.POINTER(_I64), ctypes.POINTER(_I)]),
     "em_sygv_lh": (_I, [_P, _I64, _P, _P, _I64, _P, _I64, _P, _P, _I64, _P, _P, _P, _I64, _I,
                         ctypes.POINTER(_I64), ctypes.POINTER(_I)]),
     "em_sygv_h": (_I, [_P, _I64, _P, _P, _P, _P, _P, _P, _P, ctypes.POINTER(_I64),

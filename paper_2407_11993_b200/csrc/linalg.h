@@ -117,15 +117,21 @@ void sytrd_lower(cudaStream_t st, int64_t n, double* A, int64_t lda, double* d, 
 void ormtr_lower(cudaStream_t st, int64_t n, int64_t m, const double* A, int64_t lda,
                  const double* tau, double* Z, int64_t ldz);
 // Z <- H(0) ... H(nref-1) Z, reflector c's vector starts at row c + off of column c of A
+// (trans: Z <- (H(0) ... H(nref-1))^T Z)
 void ormqr_lower_off(cudaStream_t st, int64_t n, int64_t nref, int64_t off, int64_t m,
-                     const double* A, int64_t lda, const double* tau, double* Z, int64_t ldz);
+                     const double* A, int64_t lda, const double* tau, double* Z, int64_t ldz,
+                     bool trans = false);
 
 // sytrd2.cu: two-stage tridiagonalisation (dense -> band b -> tridiagonal) with the
 // eigenvector back-transforms: syev_two_stage computes ascending w and Z for A (destroyed)
 // (only columns [c0, c0 + nc) of the ascending eigenvector matrix are back-transformed:
 // the column-sharded form of parallel.py; nc < 0 = all)
+// Yt (optional, n x ky): the "implicit eigenvector" mode — Z receives the tridiagonal
+// eigenvectors U only, and Yt <- Q^T Yt (Q the tridiagonalisation's orthogonal factor), so
+// that (Q U)^T Y = U^T Yt costs n^2 ky instead of forming Q U
 void syev_two_stage(cudaStream_t st, int64_t n, double* A, int64_t lda, double* w, double* Z,
-                    int64_t ldz, int64_t c0 = 0, int64_t nc = -1);
+                    int64_t ldz, int64_t c0 = 0, int64_t nc = -1, double* Yt = nullptr,
+                    int64_t ldy = 0, int64_t ky = 0);
 // stage pieces (exposed for tests): A -> band AB (ldab = 2b+1, band rows 0..b filled)
 void sy2sb(cudaStream_t st, int64_t n, double* A, int64_t lda, double* tau1, double* AB,
            int64_t ldab);
@@ -137,7 +143,8 @@ void stedc(cudaStream_t st, int64_t n, double* d, double* e, double* Z, int64_t 
 
 // syev.cu: symmetric eigendecomposition, eigenvalues ASCENDING; A destroyed.
 void syev_ascending(cudaStream_t st, int64_t n, double* A, int64_t lda, double* w, double* Z,
-                    int64_t ldz, int64_t c0 = 0, int64_t nc = -1);
+                    int64_t ldz, int64_t c0 = 0, int64_t nc = -1, double* Yt = nullptr,
+                    int64_t ldy = 0, int64_t ky = 0);
 
 // td1.cu / td2.cu
 void td2_plan_init(em_td2_plan* P, const double* l_n, const double* r_n, const double* P_r,

@@ -125,12 +125,12 @@ __global__ void scale_vec_kernel(int64_t n, const double* __restrict__ a,
 }
 
 void syev_ascending(cudaStream_t st, int64_t n, double* A, int64_t lda, double* w, double* Z,
-                    int64_t ldz, int64_t c0, int64_t nc) {
+                    int64_t ldz, int64_t c0, int64_t nc, double* Yt, int64_t ldy, int64_t ky) {
   if (n <= 0) return;
   if (nc < 0) nc = n - c0;
   if (n >= g_two_stage_min && n > 2 * kBand && two_stage_fits(n, ldz)) {
     g_last_eig_path = 2;
-    syev_two_stage(st, n, A, lda, w, Z, ldz, c0, nc);
+    syev_two_stage(st, n, A, lda, w, Z, ldz, c0, nc, Yt, ldy, ky);
     return;
   }
   g_last_eig_path = 1;
@@ -145,7 +145,10 @@ void syev_ascending(cudaStream_t st, int64_t n, double* A, int64_t lda, double* 
   }
   {
     Stage s(st, ST_ORMTR);
-    ormtr_lower(st, n, nc, A, lda, tau.p, Z + c0 * ldz, ldz);
+    if (Yt)  // implicit mode: Yt <- Q^T Yt
+      ormqr_lower_off(st, n, n - 1, 1, ky, A, lda, tau.p, Yt, ldy, true);
+    else
+      ormtr_lower(st, n, nc, A, lda, tau.p, Z + c0 * ldz, ldz);
   }
   EM_CK(cudaMemcpyAsync(w, d.p, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
 }
@@ -235,6 +238,32 @@ __global__ void finalize_modes_slice_kernel(int64_t n, int64_t m, const double* 
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) V[i + j * ldv] = s * z[i];
 }
 
+// Y[j, c] = X[n-1-j, c]
+__global__ void reversed_rows_kernel(int64_t n, int64_t k, const double* __restrict__ X,
+                                     int64_t ldx, double* __restrict__ Y, int64_t ldy) {
+  const int64_t total = n * k;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i % n, c = i / n;
+    Y[r + c * ldy] = X[(n - 1 - r) + c * ldx];
+  }
+}
+static void copy_reversed_rows(cudaStream_t st, int64_t n, int64_t k, const double* X,
+                               int64_t ldx, double* Y, int64_t ldy) {
+  const int64_t total = n * k;
+  reversed_rows_kernel<<<(unsigned)imin64((total + 255) / 256, 148 * 16), 256, 0, st>>>(
+      n, k, X, ldx, Y, ldy);
+  EM_LAUNCHED();
+}
+__global__ void fill_kernel(int64_t n, double v, double* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = v;
+}
+static void fill_value(cudaStream_t st, int64_t n, double v, double* out) {
+  fill_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, v, out);
+  EM_LAUNCHED();
+}
+
 // tau[j] = w[n-1-j] (descending time constants)
 __global__ void reverse_kernel(int64_t n, const double* __restrict__ w, double* __restrict__ tau) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -290,12 +319,24 @@ __global__ void quadform_lower_kernel(int64_t n, const double* __restrict__ V, i
 // m_lo .. m_hi - 1 (descending order); tau always gets all n. Everything up to the
 // tridiagonal eigenvectors is computed for the whole matrix; the back-transforms
 // (Q2, Q1 / ormtr, G^-T), the sign fix and l_n, r_n only for the rank's columns.
+//
+// Implicit mode (Y != null, V must be null): V is never formed. Y (n x ky) holds operands
+// on entry and V^T Y on exit, rows in descending mode order: V^T = U^T Q^T G^-1 is applied
+// to the ky columns (the solve with R's factor, the tridiagonalisation's reflectors
+// transposed, then one n x n x ky product with the tridiagonal eigenvectors U), so the
+// 4 n^3 flops of forming V (Q2, Q1) become O(n^2 ky). The per-mode sign of V (largest entry
+// positive, modal.py:74-78) needs V itself: here the eigensolver's own signs are kept —
+// every product of two such rows (a drive projection and an observable) is unchanged.
+// l_n, r_n: tau and 1 (V^T L V = diag(tau), V^T R V = I).
 int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const double* R,
              int64_t ldr, double* tau, double* V, int64_t ldv, double* l_n, double* r_n,
              double* VtR, int64_t ldvtr, int* which, int flags, cudaEvent_t l_ready,
-             int64_t m_lo, int64_t m_hi) {
+             int64_t m_lo, int64_t m_hi, double* Y, int64_t ldy, int64_t ky) {
   *which = -1;
   if (n <= 0) return -1;
+  const bool implicit = Y != nullptr;
+  if (implicit && (V || VtR)) throw ArgError{"implicit mode forms no V / V^T R"};
+  if (implicit) m_lo = 0, m_hi = 0;  // no eigenvector columns are formed
   if (m_hi < 0) m_hi = n;
   if (m_lo < 0 || m_hi > n || m_lo > m_hi) throw ArgError{"mode range outside [0, n]"};
   const int64_t m = m_hi - m_lo;
@@ -353,6 +394,13 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
     EM_CK(cudaStreamSynchronize(st));
     return piv;
   }
+  if (implicit && ky > 0) {  // Y <- G^-1 Y (the first factor of V^T = U^T Q^T G^-1)
+    Stage s(st, ST_TRSM_BACK);
+    if (banded)
+      band_solve(st, bc, false, ky, Y, ldy);
+    else
+      trsm_lower(st, false, n, ky, G, ldg, Y, ldy, GDinv.p);
+  }
   // leading dimension padded to 32 doubles: every column of B starts 256-byte aligned,
   // so all TMA boxes of the tridiagonalisation's symv are (symv_tma.cu)
   const int64_t ldb = (n + 31) / 32 * 32;
@@ -391,12 +439,21 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
   // descending modes m_lo .. m_hi - 1 are the ascending columns n - m_hi .. n - m_lo - 1
   const int64_t c0 = n - m_hi;
   double* Zs = Zw + c0 * ldzw;
-  syev_ascending(st, n, B.p, ldb, w.p, Zw, ldzw, c0, m);
+  syev_ascending(st, n, B.p, ldb, w.p, Zw, ldzw, c0, m, implicit ? Y : nullptr, ldy, ky);
   B.release();
+  if (m > 0) {
+    Stage s(st, ST_TRSM_BACK);
+    if (banded)
+      band_solve(st, bc, true, m, Zs, ldzw);                   // V = G^-T U
+    else
+      trsm_lower(st, true, n, m, G, ldg, Zs, ldzw, GDinv.p);
+  }
+  Gbuf.release();
+  restore_r();
   if (!g_l_certificate) {
     // The certificate is redundant when the solved pencil proves L safely SPD; otherwise
     // (L not SPD, or too ill-conditioned to tell) it runs now, in a buffer of its own,
-    // and raises the reference's error with the reference's pivot.
+    // and raises the reference's error with the reference's pivot. (R is intact again.)
     double wb[2] = {0.0, 0.0};
     EM_CK(cudaMemcpyAsync(&wb[0], w.p, sizeof(double), cudaMemcpyDeviceToHost, st));
     EM_CK(cudaMemcpyAsync(&wb[1], w.p + (n - 1), sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -408,21 +465,27 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
       const int64_t pl = potrf(st, n, Lc.p, n);
       if (pl >= 0) {
         *which = 1;
-        restore_r();
         EM_CK(cudaStreamSynchronize(st));
         return pl;
       }
     }
   }
-  if (m > 0) {
-    Stage s(st, ST_TRSM_BACK);
-    if (banded)
-      band_solve(st, bc, true, m, Zs, ldzw);                   // V = G^-T U
-    else
-      trsm_lower(st, true, n, m, G, ldg, Zs, ldzw, GDinv.p);
+  if (implicit) {
+    // Y <- U^T Y, rows reversed to descending order; tau, l_n = tau, r_n = 1
+    Stage s(st, ST_FINALIZE);
+    if (ky > 0) {
+      DBuf T((size_t)n * ky, st);
+      EM_CK(gemm(st, true, false, n, ky, n, 1.0, Zw, ldzw, Y, ldy, 0.0, T.p, n));
+      copy_reversed_rows(st, n, ky, T.p, n, Y, ldy);
+      EM_CK(cudaStreamSynchronize(st));
+    }
+    reverse_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, w.p, tau);
+    EM_LAUNCHED();
+    if (l_n) EM_CK(cudaMemcpyAsync(l_n, tau, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    if (r_n) fill_value(st, n, 1.0, r_n);
+    EM_CK(cudaStreamSynchronize(st));
+    return -1;
   }
-  Gbuf.release();
-  restore_r();
   {
     Stage s(st, ST_FINALIZE);
     if (slice) {

@@ -564,7 +564,8 @@ void ormtr_lower(cudaStream_t st, int64_t n, int64_t m, const double* A, int64_t
 // (one launch each for V, the grouped G = V^T V, the larft halves of every block in
 // one grid, the grouped T12 joins), so only the three Z GEMMs per block are sequential.
 void ormqr_lower_off(cudaStream_t st, int64_t n, int64_t nref, int64_t off, int64_t m,
-                     const double* A, int64_t lda, const double* tau, double* Z, int64_t ldz) {
+                     const double* A, int64_t lda, const double* tau, double* Z, int64_t ldz,
+                     bool trans) {
   if (nref <= 0 || m <= 0) return;
   const int64_t npan = (nref + ORM_NB - 1) / ORM_NB;
   const size_t vstride = (size_t)n * ORM_NB, tstride = (size_t)ORM_NB * ORM_NB;
@@ -614,7 +615,9 @@ void ormqr_lower_off(cudaStream_t st, int64_t n, int64_t nref, int64_t off, int6
     EM_CK(gemm_grouped(st, false, false, dt1.p, (int)t1.size(), max_t));
     EM_CK(gemm_grouped(st, false, false, dt2.p, (int)t2.size(), max_t));
   }
-  for (int64_t p = npan - 1; p >= 0; --p) {
+  // Q Z: blocks last to first with T; Q^T Z: first to last with T^T
+  for (int64_t s = 0; s < npan; ++s) {
+    const int64_t p = trans ? s : npan - 1 - s;
     const int64_t i0 = p * ORM_NB;
     const int w = (int)imin64(ORM_NB, nref - i0);
     const int64_t mr = n - i0 - off;
@@ -622,7 +625,7 @@ void ormqr_lower_off(cudaStream_t st, int64_t n, int64_t nref, int64_t off, int6
     const double* Tp = T.p + p * tstride;
     double* Zs = Z + (i0 + off);
     EM_CK(gemm(st, true, false, w, m, mr, 1.0, Vp, n, Zs, ldz, 0.0, W1.p, w));
-    EM_CK(gemm(st, false, false, w, m, w, 1.0, Tp, w, W1.p, w, 0.0, W2.p, w));
+    EM_CK(gemm(st, trans, false, w, m, w, 1.0, Tp, w, W1.p, w, 0.0, W2.p, w));
     EM_CK(gemm(st, false, false, mr, m, w, -1.0, Vp, n, W2.p, w, 1.0, Zs, ldz));
   }
   EM_CK(cudaStreamSynchronize(st));  // host argument arrays

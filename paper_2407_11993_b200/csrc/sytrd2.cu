@@ -526,13 +526,14 @@ __global__ void __launch_bounds__(256) q2_tfactor_kernel(int64_t n, const Q2Bloc
 // Explicit V (VR x b, column-major, ld VR) of a list of blocks for one wavefront, and
 // VT = V T (the block's T folded into the update: Z -= (V T) (V^T Z), one GEMM fewer).
 // T2 holds each block's T row-major (T upper triangular).
+// trans: VT = V T^T instead (the block's H^T = I - V T^T V^T, for Q2^T)
 __global__ void __launch_bounds__(256) q2_buildv_kernel(int64_t n, const Q2Block* __restrict__ blocks,
                                                         const int64_t* __restrict__ ids,
                                                         const double* __restrict__ V2,
                                                         const int64_t* __restrict__ toff,
                                                         const double* __restrict__ T2,
                                                         double* __restrict__ Vout,
-                                                        double* __restrict__ VTout) {
+                                                        double* __restrict__ VTout, int trans) {
   extern __shared__ double Vs[];  // VR x B2 (64 KB), column-major like Vout
   const Q2Block blk = blocks[ids[blockIdx.x]];
   double* V = Vout + blockIdx.x * (size_t)VR * B2;
@@ -551,12 +552,19 @@ __global__ void __launch_bounds__(256) q2_buildv_kernel(int64_t n, const Q2Block
   }
   __syncthreads();
   // VT[r, j] = sum_{i <= j} V[r, i] T[i, j]; V[r, i] = 0 unless i <= r <= i + 63
+  // (trans: sum_{i >= j} V[r, i] T[j, i])
   for (int idx = threadIdx.x; idx < VR * B2; idx += blockDim.x) {
     const int r = idx % VR, j = idx / VR;
-    const int i0 = r - (B2 - 1) > 0 ? r - (B2 - 1) : 0;
-    const int i1 = r < j ? r : j;
+    const int lo = r - (B2 - 1) > 0 ? r - (B2 - 1) : 0;
+    const int hi = r < B2 - 1 ? r : B2 - 1;
     double acc = 0.0;
-    for (int i = i0; i <= i1; ++i) acc = fma(Vs[i * VR + r], __ldg(T + i * B2 + j), acc);
+    if (!trans) {
+      for (int i = lo; i <= (hi < j ? hi : j); ++i)
+        acc = fma(Vs[i * VR + r], __ldg(T + i * B2 + j), acc);
+    } else {
+      for (int i = (lo > j ? lo : j); i <= hi; ++i)
+        acc = fma(Vs[i * VR + r], __ldg(T + j * B2 + i), acc);
+    }
     VT[idx] = acc;
   }
 }
@@ -889,9 +897,79 @@ static void q2_apply_strips(cudaStream_t st, int64_t n, int64_t ncols, int64_t n
   }
 }
 
+// Z (n x ncols) <- Q2 Z (trans: Q2^T Z) as wavefronts of grouped DMMA GEMMs: block (g, k)
+// belongs to wavefront w = k + 2 (G-1-g); blocks of one wavefront touch disjoint rows and
+// every block a block depends on sits on an earlier wavefront (Q2^T: later, and the
+// wavefronts run in reverse). Per block W = V^T Z, Z -= (V T) W (V T^T for Q2^T).
+static void q2_apply_waves(cudaStream_t st, int64_t n, int64_t ncols, int64_t ngroups,
+                           const std::vector<Q2Block>& blocks, const Q2Block* dblk,
+                           const double* V2, const int64_t* dtoff, const double* T2, double* Z,
+                           int64_t ldz, bool trans) {
+  const int b = B2;
+  const int64_t nblk = (int64_t)blocks.size();
+  if (nblk == 0 || ncols <= 0) return;
+  EM_CK(cudaFuncSetAttribute(q2_buildv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(VR * B2 * sizeof(double))));
+  constexpr int QCH = 64;  // blocks per grouped launch
+  std::vector<std::vector<int64_t>> waves;
+  {
+    std::vector<std::vector<int64_t>> byw;
+    for (int64_t i = 0; i < nblk; ++i) {
+      const int64_t wv = blocks[i].k + 2 * (ngroups - 1 - blocks[i].g);
+      if ((int64_t)byw.size() <= wv) byw.resize(wv + 1);
+      byw[wv].push_back(i);
+    }
+    if (trans) std::reverse(byw.begin(), byw.end());
+    for (auto& wl : byw)
+      for (size_t c = 0; c < wl.size(); c += QCH)
+        waves.emplace_back(wl.begin() + c, wl.begin() + std::min(wl.size(), c + QCH));
+  }
+  std::vector<int64_t> ids;
+  std::vector<GemmArgs> args;
+  std::vector<int64_t> wstart;
+  DBuf Vb((size_t)QCH * VR * B2, st), VTb((size_t)QCH * VR * B2, st),
+      W1((size_t)QCH * B2 * ncols, st);
+  for (auto& wl : waves) {
+    wstart.push_back((int64_t)ids.size());
+    for (size_t j = 0; j < wl.size(); ++j) {
+      const Q2Block& bk = blocks[wl[j]];
+      const int64_t R0 = bk.g * b + 1 + bk.k * b;
+      const int64_t nrow = imin64(VR - 1, n - R0);
+      double* Vj = Vb.p + j * (size_t)VR * B2;
+      double* VTj = VTb.p + j * (size_t)VR * B2;
+      double* W1j = W1.p + j * (size_t)B2 * ncols;
+      ids.push_back(wl[j]);
+      args.push_back(GemmArgs{B2, ncols, nrow, Vj, VR, Z + R0, ldz, W1j, B2, 1.0, 0.0, 0});
+      args.push_back(GemmArgs{nrow, ncols, B2, VTj, VR, W1j, B2, Z + R0, ldz, -1.0, 1.0, 0});
+    }
+  }
+  wstart.push_back((int64_t)ids.size());
+  DArr<int64_t> dids(ids.size(), st);
+  DArr<GemmArgs> dargs(args.size(), st);
+  EM_CK(cudaMemcpyAsync(dids.p, ids.data(), ids.size() * sizeof(int64_t), cudaMemcpyHostToDevice,
+                        st));
+  // phase-major argument arrays: [phase][problem]
+  std::vector<GemmArgs> ph(args.size());
+  const size_t np = ids.size();
+  for (size_t i = 0; i < np; ++i)
+    for (int q = 0; q < 2; ++q) ph[q * np + i] = args[2 * i + q];
+  EM_CK(cudaMemcpyAsync(dargs.p, ph.data(), ph.size() * sizeof(GemmArgs), cudaMemcpyHostToDevice,
+                        st));
+  const int tiles_n = (int)((ncols + 127) / 128);
+  for (size_t wi = 0; wi + 1 < wstart.size(); ++wi) {
+    const int64_t o = wstart[wi], cnt = wstart[wi + 1] - wstart[wi];
+    q2_buildv_kernel<<<(unsigned)cnt, 256, (size_t)VR * B2 * sizeof(double), st>>>(
+        n, dblk, dids.p + o, V2, dtoff, T2, Vb.p, VTb.p, trans ? 1 : 0);
+    EM_LAUNCHED();
+    EM_CK(gemm_grouped(st, true, false, dargs.p + o, (int)cnt, tiles_n));
+    EM_CK(gemm_grouped(st, false, false, dargs.p + np + o, (int)cnt, tiles_n));
+  }
+  EM_CK(cudaStreamSynchronize(st));  // host argument arrays / device lists lifetime
+}
+
 // ---- driver -------------------------------------------------------------------------
 void syev_two_stage(cudaStream_t st, int64_t n, double* A, int64_t lda, double* w, double* Z,
-                    int64_t ldz, int64_t c0, int64_t nc) {
+                    int64_t ldz, int64_t c0, int64_t nc, double* Yt, int64_t ldy, int64_t ky) {
   if (nc < 0) nc = n - c0;
   double* Zc = Z + c0 * ldz;  // the back-transformed columns
   const int b = B2;
@@ -942,6 +1020,10 @@ void syev_two_stage(cudaStream_t st, int64_t n, double* A, int64_t lda, double* 
     // w = k + 2 (G-1-g) in increasing w: blocks of one wavefront touch disjoint rows and
     // every block they depend on sits on an earlier wavefront. Each wavefront is two
     // grouped DMMA GEMMs over all columns of Z (W = V^T Z, Z -= (V T) W).
+    if (Yt && n > b) {  // implicit mode: Q^T = Q2^T Q1^T, so Q1^T first
+      Stage sq1(st, ST_Q1);
+      ormqr_lower_off(st, n, n - b, b, ky, A, lda, tau1.p, Yt, ldy, true);
+    }
     std::vector<Q2Block> blocks;
     const int64_t ngroups = (nsw + b - 1) / b;
     for (int64_t g = ngroups - 1; g >= 0; --g) {
@@ -960,74 +1042,24 @@ void syev_two_stage(cudaStream_t st, int64_t n, double* A, int64_t lda, double* 
                                  (int)smt));
       q2_tfactor_kernel<<<(unsigned)nblk, 256, smt, st>>>(n, dblk.p, V2.p, TAU2.p, dtoff.p, T2.p);
       EM_LAUNCHED();
-      if (g_q2_mode == 0) {
+      if (Yt) {
+        // implicit mode: Yt <- Q2^T (Q1^T Yt) (Q1^T applied above)
+        q2_apply_waves(st, n, ky, ngroups, blocks, dblk.p, V2.p, dtoff.p, T2.p, Yt, ldy, true);
+      } else if (g_q2_mode == 0) {
         q2_apply_reg(st, n, nc, ngroups, V2.p, dtoff.p, T2.p, Zc, ldz);
         EM_CK(cudaStreamSynchronize(st));  // dblk lifetime
       } else if (g_q2_mode == 2) {
         q2_apply_strips(st, n, nc, ngroups, V2.p, dtoff.p, T2.p, Zc, ldz);
         EM_CK(cudaStreamSynchronize(st));  // dblk lifetime
       } else {
-      EM_CK(cudaFuncSetAttribute(q2_buildv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(VR * B2 * sizeof(double))));
-      // wavefront lists (chunks of at most QCH blocks)
-      constexpr int QCH = 64;
-      std::vector<std::vector<int64_t>> waves;
-      {
-        std::vector<std::vector<int64_t>> byw;
-        for (int64_t i = 0; i < nblk; ++i) {
-          const int64_t wv = blocks[i].k + 2 * (ngroups - 1 - blocks[i].g);
-          if ((int64_t)byw.size() <= wv) byw.resize(wv + 1);
-          byw[wv].push_back(i);
-        }
-        for (auto& wl : byw)
-          for (size_t c = 0; c < wl.size(); c += QCH)
-            waves.emplace_back(wl.begin() + c, wl.begin() + std::min(wl.size(), c + QCH));
-      }
-      std::vector<int64_t> ids;
-      std::vector<GemmArgs> args;
-      std::vector<int64_t> wstart;
-      DBuf Vb((size_t)QCH * VR * B2, st), VTb((size_t)QCH * VR * B2, st), W1((size_t)QCH * B2 * n, st);
-      for (auto& wl : waves) {
-        wstart.push_back((int64_t)ids.size());
-        for (size_t j = 0; j < wl.size(); ++j) {
-          const Q2Block& bk = blocks[wl[j]];
-          const int64_t R0 = bk.g * b + 1 + bk.k * b;
-          const int64_t nrow = imin64(VR - 1, n - R0);
-          double* Vj = Vb.p + j * (size_t)VR * B2;
-          double* VTj = VTb.p + j * (size_t)VR * B2;
-          double* W1j = W1.p + j * (size_t)B2 * n;
-          ids.push_back(wl[j]);
-          args.push_back(GemmArgs{B2, n, nrow, Vj, VR, Z + R0, ldz, W1j, B2, 1.0, 0.0, 0});
-          args.push_back(GemmArgs{nrow, n, B2, VTj, VR, W1j, B2, Z + R0, ldz, -1.0, 1.0, 0});
-        }
-      }
-      wstart.push_back((int64_t)ids.size());
-      DArr<int64_t> dids(ids.size(), st);
-      DArr<GemmArgs> dargs(args.size(), st);
-      EM_CK(cudaMemcpyAsync(dids.p, ids.data(), ids.size() * sizeof(int64_t),
-                            cudaMemcpyHostToDevice, st));
-      // phase-major argument arrays: [phase][problem]
-      std::vector<GemmArgs> ph(args.size());
-      const size_t np = ids.size();
-      for (size_t i = 0; i < np; ++i)
-        for (int q = 0; q < 2; ++q) ph[q * np + i] = args[2 * i + q];
-      EM_CK(cudaMemcpyAsync(dargs.p, ph.data(), ph.size() * sizeof(GemmArgs),
-                            cudaMemcpyHostToDevice, st));
-      const int tiles_n = (int)((n + 127) / 128);
-      for (size_t wi = 0; wi + 1 < wstart.size(); ++wi) {
-        const int64_t o = wstart[wi], cnt = wstart[wi + 1] - wstart[wi];
-        q2_buildv_kernel<<<(unsigned)cnt, 256, (size_t)VR * B2 * sizeof(double), st>>>(
-            n, dblk.p, dids.p + o, V2.p, dtoff.p, T2.p, Vb.p, VTb.p);
-        EM_LAUNCHED();
-        EM_CK(gemm_grouped(st, true, false, dargs.p + o, (int)cnt, tiles_n));
-        EM_CK(gemm_grouped(st, false, false, dargs.p + np + o, (int)cnt, tiles_n));
-      }
-      EM_CK(cudaStreamSynchronize(st));  // host argument arrays / device lists lifetime
+        q2_apply_waves(st, n, nc, ngroups, blocks, dblk.p, V2.p, dtoff.p, T2.p, Zc, ldz, false);
       }
     }
     // Q1 (stage-1 reflectors, vectors start b rows below their column)
-    Stage sq1(st, ST_Q1);
-    if (n > b) ormqr_lower_off(st, n, n - b, b, nc, A, lda, tau1.p, Zc, ldz);
+    if (!Yt) {
+      Stage sq1(st, ST_Q1);
+      if (n > b) ormqr_lower_off(st, n, n - b, b, nc, A, lda, tau1.p, Zc, ldz);
+    }
   }
   EM_CK(cudaMemcpyAsync(w, d.p, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
 }

@@ -689,3 +689,84 @@ def write_timing_csv(path, results: list[SimulationResult], header_lines: tuple[
         for r in results:
             fh.write(f"{r.method},{r.wall_time_setup!r},{r.wall_time_stepping!r},"
                      f"{r.n_steps},{r.per_step_cost!r}\n")
+
+
+class ImplicitTd2:
+    """The modal transient without forming the eigenvectors ("implicit V"):
+    em_sygv_implicit applies V^T = U^T Q^T G^-1 to the drive columns [R_D | L_D | M0]
+    and the observable rows C^T only, so the eigensolve skips the 4 N^3 flops that form
+    V (the Q2 and Q1 back-transforms). The scan is the same em_td2 plan as Td2Stepper's,
+    with l_n = tau, r_n = 1 (V^T L V = diag(tau), V^T R V = I). Observables (C, D) are
+    fixed at construction; run() returns them exactly as Td2Stepper.run does. V, the
+    modal states' signs and the reconstructed currents are not available on this path.
+    """
+
+    def __init__(self, rm: ReducedModel, observables, dt: float, theta: float):
+        _check_theta_dt(dt, theta)
+        t0 = time.perf_counter()
+        self.rm, self.dt, self.theta = rm, float(dt), float(theta)
+        n, n_p, n_s = rm.n_internal, rm.n_ports, rm.n_sources
+        self._n, self._n_p, self._n_s = n, n_p, n_s
+        c, d = observables if isinstance(observables, tuple) else (observables, None)
+        c = np.atleast_2d(np.asarray(c, dtype=float))
+        if c.shape[1] != n:
+            raise DimensionMismatch(f"observables need {n} columns, got {c.shape}")
+        n_obs = c.shape[0]
+        nd = 2 * n_p + n_s
+        cols = [rm.r_d.reshape(n, n_p), rm.l_d.reshape(n, n_p), rm.m0.reshape(n, n_s), c.T]
+        y = nat.device_colmajor(np.concatenate(cols, axis=1))      # (nd + n_obs, n)
+        lm, rmat = rm.l_i.full, rm.r_i.full
+        dl, dr = nat.device_symmetric(lm), nat.device_symmetric(rmat)
+        tau = nat.empty(n)
+        piv, which = ctypes.c_int64(-1), ctypes.c_int(-1)
+        rc = nat.load_library().em_sygv_implicit(
+            nat.context(), n, nat.ptr(dl), n, nat.ptr(dr), n, nat.ptr(tau), nat.ptr(y), n,
+            nd + n_obs, None, None, 1, ctypes.byref(piv), ctypes.byref(which))
+        if rc == nat.EM_ERR_NOT_PD:
+            from .errors import NotPositiveDefinite
+            what = "modal resistance matrix" if which.value == 0 else "modal inductance matrix"
+            raise NotPositiveDefinite(int(piv.value), what)
+        nat.check(rc, "em_sygv_implicit")
+        del dl, dr
+        self.tau = tau.cpu().numpy()
+        self._ln = tau
+        self._rn = nat.torch().ones(n, dtype=nat.torch().float64, device="cuda")
+        proj = y[:max(nd, 1)] if nd else nat.zeros(1, n)
+        self._proj = proj
+        p_r = proj[0:n_p] if n_p else proj[0:1]
+        p_l = proj[n_p:2 * n_p] if n_p else proj[0:1]
+        p_m = proj[2 * n_p:nd] if n_s else proj[0:1]
+        plan = ctypes.c_void_p()
+        nat.check(nat.load_library().em_td2_plan_create(
+            nat.context(), n, n_p, n_s, nat.ptr(self._ln), nat.ptr(self._rn), nat.ptr(p_r),
+            nat.ptr(p_l), nat.ptr(p_m), self.dt, self.theta, ctypes.byref(plan)),
+            "em_td2_plan_create")
+        self._plan = plan
+        cv = y[nd:nd + n_obs].t().contiguous()                     # C V column-major n_obs x n
+        self._cv = cv
+        dd = None
+        if d is not None and n_p:
+            dd = nat.device_colmajor(np.asarray(d, dtype=float).reshape(n_obs, n_p))
+        self._dd = dd
+        nat.check(nat.load_library().em_td2_set_observables(
+            plan, n_obs, nat.ptr(cv), n_obs, nat.ptr(dd), n_obs), "em_td2_set_observables")
+        self._n_obs = n_obs
+        self.setup_time = time.perf_counter() - t0
+
+    def __del__(self):
+        plan = getattr(self, "_plan", None)
+        if plan:
+            nat.load_library().em_td2_plan_destroy(plan)
+            self._plan = None
+
+    def run(self, i_d_samples, i0_samples, capture_stride: int = 1):
+        """Observables (n_caps, n_obs) over a sample table (rows t_0..t_T) from rest."""
+        table = _drive_table(i_d_samples, i0_samples, self._n_p, self._n_s) \
+            if (self._n_p or self._n_s) else np.zeros((np.asarray(i_d_samples).shape[0], 0))
+        steps = table.shape[0] - 1
+        drive = nat.device_vector(table.reshape(-1)) if table.size else nat.zeros(1)
+        q = nat.zeros(self._n)
+        y = nat.empty(steps // capture_stride, self._n_obs)
+        nat.check(nat.load_library().em_td2_run(self._plan, steps, nat.ptr(drive), nat.ptr(q),
+                                                 nat.ptr(y), capture_stride, None), "em_td2_run")
+        return y.cpu().numpy()

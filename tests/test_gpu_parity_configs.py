@@ -152,3 +152,34 @@ def test_theta_range_and_large_eps_branch(theta, steps):
     q, y = _device_td2_run(l_n, r_n, p_r, p_l, p_m, dt, theta, tab, steps, cv, 1)
     assert rel_l2(q, q_ref) < TOL_OBS
     assert rel_l2(y, y_ref) < TOL_OBS
+
+
+@pytest.mark.parametrize("two_stage", [False, True])
+def test_implicit_v_transient_equals_explicit(two_stage):
+    """em_sygv_implicit / transient.ImplicitTd2 (no V formed: V^T applied to the drive
+    columns and the observable rows) against the explicit path on the same plate: the same
+    eigenvalues and the same observables (one- and two-stage: Q^T, Q1^T Q2^T transposed
+    applies), and against the reference golden."""
+    from paper_2407_11993_b200 import _native as nat
+    from paper_2407_11993_b200 import modal, reduction, transient
+    g = golden("plate_200")
+    rm = reduction.from_blocks(g["r_i"], g["l_i"], g["r_d"], g["l_d"], g["m0"],
+                               port_names=("p0",), source_names=("s0",))
+    from paper_2407_11993_b200.network import DriveSignal, Tone
+    drives = (DriveSignal(tones=(Tone(1.0, 1e4, 0.0),), sources=("s0",)),
+              DriveSignal(tones=(Tone(0.7, 2e4, 0.3), Tone(0.2, 5e4, 1.1)), ports=("p0",)))
+    dt, steps = float(g["dt"]), int(g["steps"])
+    i_d, i0 = transient.drive_samples(None, rm, drives, dt, steps)
+    if two_stage:
+        nat.set_two_stage_min(0)
+    try:
+        basis = modal.generalized_eig(rm.l_i, rm.r_i)
+        imp = transient.ImplicitTd2(rm, (g["c"], None), dt, 0.5)
+    finally:
+        nat.set_two_stage_min(nat.TWO_STAGE_MIN_DEFAULT)
+    np.testing.assert_array_equal(imp.tau, basis.tau)
+    _, y_exp, _ = transient.Td2Stepper(rm, basis, dt, 0.5).run(i_d, i0, capture_state=False,
+                                                                observables=(g["c"], None))
+    y_imp = imp.run(i_d, i0)
+    assert rel_l2(y_imp, y_exp) < 1e-10
+    assert rel_l2(y_imp, g["td2_obs_theta0.5"]) < TOL_OBS
