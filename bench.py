@@ -134,7 +134,7 @@ def build_inputs(cfg):
 class DeviceStep:
     """The hot path on device-resident inputs, straight through the C ABI."""
 
-    def __init__(self, m, cfg):
+    def __init__(self, m, cfg, form_v=True):
         from paper_2407_11993_b200 import _native as nat
         self.nat = nat
         self.m = m
@@ -145,8 +145,8 @@ class DeviceStep:
         self.n_p, self.n_s = n_p, n_s
         self.nd = 2 * n_p + n_s
         self.tau, self.ln, self.rn = nat.empty(n), nat.empty(n), nat.empty(n)
-        self.V = nat.empty(n, n)
-        self.VtR = nat.empty(n, n) if cfg.get("vtr", True) else None
+        self.V = nat.empty(n, n) if form_v else None
+        self.VtR = nat.empty(n, n) if form_v and cfg.get("vtr", True) else None
         cols = []
         if n_p:
             cols += [m["r_d"], m["l_d"]]
@@ -154,8 +154,8 @@ class DeviceStep:
             cols += [m["m0_dev"]]
         t = nat.torch()
         self.drv = t.cat(cols, dim=0).contiguous() if cols else nat.zeros(1, n)
-        self.P = nat.empty(max(self.nd, 1), n)
-        self.CV = nat.empty(n, cfg["n_obs"])
+        self.P = nat.empty(max(self.nd, 1), n) if form_v else None
+        self.CV = nat.empty(n, cfg["n_obs"]) if form_v else None
         self.n_rhs = (n_p + n_s) if cfg.get("sweep") else 1
         self.Y = [nat.empty(self.n_rhs, cfg["steps"], cfg["n_obs"]) for _ in cfg["thetas"]]
         self.q = nat.empty(self.n_rhs, n)
@@ -187,6 +187,57 @@ class DeviceStep:
                                              nat.ptr(p_r), nat.ptr(p_l), nat.ptr(p_m), cfg["dt"],
                                              th, ctypes.byref(plan)), "em_td2_plan_create")
             nat.check(lib.em_td2_set_observables(plan, n_obs, nat.ptr(self.CV), n_obs, None, 0),
+                      "em_td2_set_observables")
+            self.q.zero_()
+            if cfg.get("sweep"):
+                nat.check(lib.em_td2_run_sweep(plan, cfg["steps"], nat.ptr(self.m["table_dev"]),
+                                               nat.ptr(self.q), nat.ptr(self.Y[k]), 1),
+                          "em_td2_run_sweep")
+            else:
+                nat.check(lib.em_td2_run(plan, cfg["steps"], nat.ptr(self.m["table_dev"]),
+                                         nat.ptr(self.q), nat.ptr(self.Y[k]), 1, None),
+                          "em_td2_run")
+            lib.em_td2_plan_destroy(plan)
+
+
+class ImplicitDeviceStep(DeviceStep):
+    """The same step without forming V (em_sygv_implicit, SURVEY.md §7 "implicit V"):
+    V^T is applied to the drive columns and the observable rows only, the scan runs on
+    l_n = tau, r_n = 1. Reported beside the headline (which forms V like the reference)."""
+
+    def __init__(self, m, cfg):
+        super().__init__(m, cfg, form_v=False)
+        t = self.nat.torch()
+        n_obs = cfg["n_obs"]
+        # C^T as n_obs columns: c_dev is C column-major (n_obs x n) -> transpose
+        ct = self.m["c_dev"].reshape(self.n, n_obs).t().contiguous()
+        self.y0 = t.cat([self.drv[:self.nd], ct], dim=0).contiguous()
+        self.Yp = t.empty_like(self.y0)
+        self.one = t.ones(self.n, dtype=t.float64, device="cuda")
+
+    def __call__(self):
+        import ctypes
+        nat, lib, ctx = self.nat, self.nat.load_library(), self.nat.context()
+        n, cfg, nd = self.n, self.cfg, self.nd
+        n_obs = cfg["n_obs"]
+        self.Yp.copy_(self.y0)
+        piv, which = ctypes.c_int64(-1), ctypes.c_int(-1)
+        nat.check(lib.em_sygv_implicit(ctx, n, nat.ptr(self.m["l_i"]), n, nat.ptr(self.m["r_i"]),
+                                       n, nat.ptr(self.tau), nat.ptr(self.Yp), n, nd + n_obs,
+                                       None, None, 1, ctypes.byref(piv), ctypes.byref(which)),
+                  "em_sygv_implicit")
+        cv = self.Yp[nd:].t().contiguous()
+        n_p, n_s = self.n_p, self.n_s
+        P = self.Yp
+        p_r = P[0:1] if not n_p else P[0:n_p]
+        p_l = P[0:1] if not n_p else P[n_p:2 * n_p]
+        p_m = P[0:1] if not n_s else P[2 * n_p:nd]
+        for k, th in enumerate(cfg["thetas"]):
+            plan = ctypes.c_void_p()
+            nat.check(lib.em_td2_plan_create(ctx, n, n_p, n_s, nat.ptr(self.tau), nat.ptr(self.one),
+                                             nat.ptr(p_r), nat.ptr(p_l), nat.ptr(p_m), cfg["dt"],
+                                             th, ctypes.byref(plan)), "em_td2_plan_create")
+            nat.check(lib.em_td2_set_observables(plan, n_obs, nat.ptr(cv), n_obs, None, 0),
                       "em_td2_set_observables")
             self.q.zero_()
             if cfg.get("sweep"):
@@ -588,6 +639,28 @@ def run_ours(args, cfg, rank, world, local_rank):
         m["r_i"] = es.pinned[1].to("cuda", non_blocking=False)
         del es
 
+    # ---- the implicit-V variant of the same step (not the headline: the reference forms V)
+    implicit = None
+    if world == 1 and not args.no_implicit:
+        ist = ImplicitDeviceStep(m, cfg)
+        ist()  # warm-up (its transposed back-transform kernels)
+        torch.cuda.synchronize()
+        i0e, i1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        i0e.record()
+        for _ in range(args.implicit_steps):
+            ist()
+        i1e.record()
+        torch.cuda.synchronize()
+        ti = i0e.elapsed_time(i1e) / 1e3 / args.implicit_steps
+        implicit = {"value": units / ti, "unit": "mode-steps/s", "ms_per_step": ti * 1e3,
+                    "steps": args.implicit_steps, "warmup": 1,
+                    "note": "em_sygv_implicit: V^T applied to the drive columns and observable "
+                            "rows only (no V formed, no Q1/Q2 back-transform of the n x n "
+                            "eigenvectors); same eigenvalues and observables as the headline "
+                            "(tests/test_gpu_parity_configs.py)"}
+        del ist
+        torch.cuda.empty_cache()
+
     peaks = load_peaks()
     n_steps_timed = args.steps
     st_avg = {k: (v[0] / n_steps_timed, v[1] / n_steps_timed) for k, v in stages.items()}
@@ -673,6 +746,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             "roofline": rl,
             "stage_ms_per_step": {k: round(v[0], 3) for k, v in st_avg.items()},
             "cpu_baseline": cpu,
+            "implicit_v": implicit,
         }
         line.update(extra)
         print(json.dumps(line), flush=True)
@@ -817,6 +891,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-td1", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-implicit", action="store_true")
+    ap.add_argument("--implicit-steps", type=int, default=1)
     ap.add_argument("--two-stage", type=int, default=None,
                     help="smallest n for the two-stage tridiagonalisation (default: library)")
     ap.add_argument("--profile-fine", action="store_true",

@@ -712,6 +712,8 @@ class ImplicitTd2:
         if c.shape[1] != n:
             raise DimensionMismatch(f"observables need {n} columns, got {c.shape}")
         n_obs = c.shape[0]
+        if n_obs > 128:
+            raise ValidationError("at most 128 observables per run")
         nd = 2 * n_p + n_s
         cols = [rm.r_d.reshape(n, n_p), rm.l_d.reshape(n, n_p), rm.m0.reshape(n, n_s), c.T]
         y = nat.device_colmajor(np.concatenate(cols, axis=1))      # (nd + n_obs, n)
