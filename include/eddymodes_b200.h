@@ -175,10 +175,26 @@ int em_sygv_range(em_ctx* ctx, int64_t n, const double* L, int64_t ldl, double* 
  * tau (n) as em_sygv; l_n = tau and r_n = 1 (the identities V^T L V = diag(tau),
  * V^T R V = I; either may be NULL). Each mode keeps the eigensolver's sign rather than
  * the reference's sign fix (modal.py:74-78, which needs V): products of two rows of V^T Y
- * (P_n x CV_n, what the modal scan uses) are unchanged. Flags as em_sygv_ex. */
-int em_sygv_implicit(em_ctx* ctx, int64_t n, const double* L, int64_t ldl, double* R,
-                     int64_t ldr, double* tau, double* Y, int64_t ldy, int64_t k, double* l_n,
-                     double* r_n, int flags, int64_t* pivot, int* which);
+ * (P_n x CV_n, what the modal scan uses) are unchanged. Neither V nor the tridiagonal
+ * eigenvector matrix is formed: divide and conquer carries U^T Y through its merges
+ * (O(n k) memory), the stage-2 reflectors reuse the reduced matrix's storage.
+ * Flags: EM_SYGV_R_WORKSPACE as em_sygv_ex; EM_SYGV_L_WORKSPACE: L (ld a multiple of 32)
+ * is overwritten by the reduction instead of copied — one n x n buffer less, so the peak is
+ * L plus n^2 / 2 (the Q2 block factors) and n = 120,000 fits one B200. An in-place solve
+ * cannot run the reference's Cholesky certificate of L afterwards: when the solved spectrum
+ * and R's Gershgorin bounds do not already prove it redundant (see em_sygv), the call
+ * fails with EM_ERR_ARG and asks to solve without the flag. */
+#define EM_SYGV_L_WORKSPACE 2
+int em_sygv_implicit(em_ctx* ctx, int64_t n, double* L, int64_t ldl, double* R, int64_t ldr,
+                     double* tau, double* Y, int64_t ldy, int64_t k, double* l_n, double* r_n,
+                     int flags, int64_t* pivot, int* which);
+/* em_sygv_implicit with R given in LAPACK lower band storage (Rb[(i - j) + j * ldrb] =
+ * R(i, j) for 0 <= i - j <= bw, ldrb >= bw + 1): the stencil resistance matrix of a plate
+ * never exists as a dense n x n array. Flags: EM_SYGV_L_WORKSPACE. */
+int em_sygv_implicit_band(em_ctx* ctx, int64_t n, double* L, int64_t ldl, const double* Rb,
+                          int64_t ldrb, int64_t bw, double* tau, double* Y, int64_t ldy,
+                          int64_t k, double* l_n, double* r_n, int flags, int64_t* pivot,
+                          int* which);
 /* em_sygv_ex with L still on the host: the library uploads L_host (n x n, leading
  * dimension n) into the device buffer L (ld ldl) on a copy engine, after the work already
  * queued on the context stream (e.g. R's upload); L is first read by the two-sided

@@ -54,6 +54,8 @@ SIGNATURES = {
                            _I64, _I, ctypes.POINTER(_I64), ctypes.POINTER(_I)]),
     "em_sygv_implicit": (_I, [_P, _I64, _P, _I64, _P, _I64, _P, _P, _I64, _I64, _P, _P, _I,
                               ctypes.POINTER(_I64), ctypes.POINTER(_I)]),
+    "em_sygv_implicit_band": (_I, [_P, _I64, _P, _I64, _P, _I64, _I64, _P, _P, _I64, _I64, _P,
+                                   _P, _I, ctypes.POINTER(_I64), ctypes.POINTER(_I)]),
     "em_sygv_lh": (_I, [_P, _I64, _P, _P, _I64, _P, _I64, _P, _P, _I64, _P, _P, _P, _I64, _I,
                         ctypes.POINTER(_I64), ctypes.POINTER(_I)]),
     "em_sygv_h": (_I, [_P, _I64, _P, _P, _P, _P, _P, _P, _P, ctypes.POINTER(_I64),
@@ -169,6 +171,7 @@ def stage_times() -> dict:
     return {STAGES[i]: (ms[i], cnt[i]) for i in range(n) if cnt[i]}
 
 
+EM_SYGV_R_WORKSPACE, EM_SYGV_L_WORKSPACE = 1, 2
 EM_CFG_TWO_STAGE_MIN = 1
 
 

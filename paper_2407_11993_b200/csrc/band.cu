@@ -57,8 +57,10 @@ int64_t band_lower_width(cudaStream_t st, int64_t n, const double* A, int64_t ld
 }
 
 // panel j <- rows [128 j, 128 j + ldp) x cols [128 j, 128 j + 128) of A's lower triangle
+// (band >= 0: A is LAPACK lower band storage, A[(i - j) + j lda] = a_ij for i - j <= band)
 __global__ void band_extract_panels_kernel(int64_t n, const double* __restrict__ A, int64_t lda,
-                                           int64_t ldp, int64_t nblk, double* __restrict__ P) {
+                                           int64_t ldp, int64_t nblk, double* __restrict__ P,
+                                           int64_t band) {
   const int64_t per = ldp * BNB;
   const int64_t total = per * nblk;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
@@ -66,12 +68,15 @@ __global__ void band_extract_panels_kernel(int64_t n, const double* __restrict__
     const int64_t j = t / per, rem = t % per;
     const int64_t c = rem / ldp, r = rem % ldp;
     const int64_t gc = j * BNB + c, gr = j * BNB + r;
-    P[t] = (gr < n && gc < n && gr >= gc) ? A[gr + gc * lda] : 0.0;
+    if (band >= 0)
+      P[t] = (gr < n && gc < n && gr >= gc && gr - gc <= band) ? A[(gr - gc) + gc * lda] : 0.0;
+    else
+      P[t] = (gr < n && gc < n && gr >= gc) ? A[gr + gc * lda] : 0.0;
   }
 }
 
 int64_t band_potrf(cudaStream_t st, int64_t n, const double* A, int64_t lda, int64_t bw,
-                   BandChol& f) {
+                   BandChol& f, bool band_storage) {
   f.n = n;
   f.kb = (int)((bw + BNB - 1) / BNB);
   f.ldp = (int64_t)BNB * (f.kb + 1);
@@ -81,7 +86,8 @@ int64_t band_potrf(cudaStream_t st, int64_t n, const double* A, int64_t lda, int
   {
     const int64_t total = f.ldp * BNB * f.nblk;
     const int blocks = (int)imin64((total + 255) / 256, 32 * num_sms());
-    band_extract_panels_kernel<<<blocks, 256, 0, st>>>(n, A, lda, f.ldp, f.nblk, f.P.p);
+    band_extract_panels_kernel<<<blocks, 256, 0, st>>>(n, A, lda, f.ldp, f.nblk, f.P.p,
+                                                        band_storage ? bw : -1);
     EM_LAUNCHED();
   }
   DArr<int64_t> info(1, st);
@@ -116,6 +122,30 @@ int64_t band_potrf(cudaStream_t st, int64_t n, const double* A, int64_t lda, int
   EM_CK(cudaMemcpyAsync(&h, info.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   EM_CK(cudaStreamSynchronize(st));
   return h;
+}
+
+// Gershgorin interval of a symmetric matrix in lower band storage (one warp per row):
+// out[0] = min_i (a_ii - sum_j |a_ij|), out[1] = max_i (a_ii + sum_j |a_ij|); *neg = 1 if
+// some lower end is not positive (atomics on ordered bit patterns of non-negative doubles)
+__global__ void band_gershgorin_kernel(int64_t n, const double* __restrict__ B, int64_t ldb,
+                                       int64_t bw, unsigned long long* out_lo,
+                                       unsigned long long* out_hi, int* neg) {
+  const int64_t i = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (i >= n) return;
+  double s = 0.0;
+  for (int64_t q = 1 + lane; q <= bw; q += 32) {
+    if (i - q >= 0) s += fabs(B[q + (i - q) * ldb]);  // a_{i, i-q}
+    if (i + q < n) s += fabs(B[q + i * ldb]);         // a_{i+q, i}
+  }
+  s = warp_sum(s);
+  if (lane == 0) {
+    const double d = B[i * ldb];
+    const double lo = d - s, hi = d + s;
+    if (!(lo > 0.0)) atomicExch(neg, 1);
+    else atomicMin(out_lo, (unsigned long long)__double_as_longlong(lo));
+    atomicMax(out_hi, (unsigned long long)__double_as_longlong(fmax(hi, 0.0)));
+  }
 }
 
 // C (n x m) <- G^-1 C (trans = false, forward) or G^-T C (trans = true, backward)

@@ -32,7 +32,8 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
              int64_t ldr, double* tau, double* V, int64_t ldv, double* l_n, double* r_n,
              double* VtR, int64_t ldvtr, int* which, int flags,
              cudaEvent_t l_ready = nullptr, int64_t m_lo = 0, int64_t m_hi = -1,
-             double* Y = nullptr, int64_t ldy = 0, int64_t ky = 0);
+             double* Y = nullptr, int64_t ldy = 0, int64_t ky = 0, const double* Rb = nullptr,
+             int64_t ldrb = 0, int64_t rbw = -1);
 }
 
 // full definitions live in td1.cu / td2.cu; re-declare the layout-independent API here
@@ -315,17 +316,37 @@ int em_sygv_range(em_ctx* ctx, int64_t n, const double* L, int64_t ldl, double* 
   });
 }
 
-int em_sygv_implicit(em_ctx* ctx, int64_t n, const double* L, int64_t ldl, double* R,
-                     int64_t ldr, double* tau, double* Y, int64_t ldy, int64_t k, double* l_n,
-                     double* r_n, int flags, int64_t* pivot, int* which) {
+int em_sygv_implicit(em_ctx* ctx, int64_t n, double* L, int64_t ldl, double* R, int64_t ldr,
+                     double* tau, double* Y, int64_t ldy, int64_t k, double* l_n, double* r_n,
+                     int flags, int64_t* pivot, int* which) {
   return guarded(ctx, [&] {
-    if (flags & ~EM_SYGV_R_WORKSPACE) throw em::ArgError{"unknown em_sygv_implicit flags"};
+    if (flags & ~(EM_SYGV_R_WORKSPACE | EM_SYGV_L_WORKSPACE))
+      throw em::ArgError{"unknown em_sygv_implicit flags"};
     if (k < 0 || (k > 0 && (!Y || ldy < n))) throw em::ArgError{"em_sygv_implicit: bad Y"};
     int wh = -1;
     double dummy = 0.0;
     const int64_t p = em::sygv(ctx->stream, n, L, ldl, R, ldr, tau, nullptr, n, l_n, r_n,
                                nullptr, n, &wh, flags, nullptr, 0, -1, k > 0 ? Y : &dummy,
                                ldy, k);
+    if (pivot) *pivot = p;
+    if (which) *which = wh;
+    return p >= 0 ? EM_ERR_NOT_PD : EM_OK;
+  });
+}
+
+int em_sygv_implicit_band(em_ctx* ctx, int64_t n, double* L, int64_t ldl, const double* Rb,
+                          int64_t ldrb, int64_t bw, double* tau, double* Y, int64_t ldy,
+                          int64_t k, double* l_n, double* r_n, int flags, int64_t* pivot,
+                          int* which) {
+  return guarded(ctx, [&] {
+    if (flags & ~EM_SYGV_L_WORKSPACE) throw em::ArgError{"unknown em_sygv_implicit_band flags"};
+    if (!Rb || bw < 0 || ldrb < bw + 1) throw em::ArgError{"em_sygv_implicit_band: bad band"};
+    if (k < 0 || (k > 0 && (!Y || ldy < n))) throw em::ArgError{"em_sygv_implicit_band: bad Y"};
+    int wh = -1;
+    double dummy = 0.0;
+    const int64_t p = em::sygv(ctx->stream, n, L, ldl, nullptr, n, tau, nullptr, n, l_n, r_n,
+                               nullptr, n, &wh, flags, nullptr, 0, -1, k > 0 ? Y : &dummy,
+                               ldy, k, Rb, ldrb, bw);
     if (pivot) *pivot = p;
     if (which) *which = wh;
     return p >= 0 ? EM_ERR_NOT_PD : EM_OK;

@@ -54,8 +54,12 @@ struct BandChol {
   }
 };
 int64_t band_lower_width(cudaStream_t st, int64_t n, const double* A, int64_t lda);
+// (band_storage: A is LAPACK lower band storage of bandwidth bw, ld lda >= bw + 1)
 int64_t band_potrf(cudaStream_t st, int64_t n, const double* A, int64_t lda, int64_t bw,
-                   BandChol& f);
+                   BandChol& f, bool band_storage = false);
+__global__ void band_gershgorin_kernel(int64_t n, const double* __restrict__ B, int64_t ldb,
+                                       int64_t bw, unsigned long long* out_lo,
+                                       unsigned long long* out_hi, int* neg);
 void band_solve(cudaStream_t st, const BandChol& f, bool trans, int64_t m, double* C,
                 int64_t ldc);
 void band_sygst(cudaStream_t st, const BandChol& f, double* B, int64_t ldb);
@@ -126,9 +130,9 @@ void ormqr_lower_off(cudaStream_t st, int64_t n, int64_t nref, int64_t off, int6
 // eigenvector back-transforms: syev_two_stage computes ascending w and Z for A (destroyed)
 // (only columns [c0, c0 + nc) of the ascending eigenvector matrix are back-transformed:
 // the column-sharded form of parallel.py; nc < 0 = all)
-// Yt (optional, n x ky): the "implicit eigenvector" mode — Z receives the tridiagonal
-// eigenvectors U only, and Yt <- Q^T Yt (Q the tridiagonalisation's orthogonal factor), so
-// that (Q U)^T Y = U^T Yt costs n^2 ky instead of forming Q U
+// Yt (optional, n x ky): the "implicit eigenvector" mode — Yt <- (Q U)^T Yt (Q the
+// tridiagonalisation's orthogonal factor, U the tridiagonal eigenvectors), neither Q U nor
+// U formed (Z unused, may be null); A's storage is reused for the stage-2 reflectors
 void syev_two_stage(cudaStream_t st, int64_t n, double* A, int64_t lda, double* w, double* Z,
                     int64_t ldz, int64_t c0 = 0, int64_t nc = -1, double* Yt = nullptr,
                     int64_t ldy = 0, int64_t ky = 0);
@@ -140,6 +144,9 @@ constexpr int kBand = 64;
 // stedc.cu: tridiagonal eigensolver (divide and conquer). Eigenvalues ascending in d,
 // eigenvectors in Z (n x n, ld ldz). e is destroyed.
 void stedc(cudaStream_t st, int64_t n, double* d, double* e, double* Z, int64_t ldz);
+// Eigenvalues ascending in d and Y (n x k) <- U^T Y, U never formed (O(n k) memory)
+void stedc_apply(cudaStream_t st, int64_t n, double* d, double* e, double* Y, int64_t ldy,
+                 int64_t k);
 
 // syev.cu: symmetric eigendecomposition, eigenvalues ASCENDING; A destroyed.
 void syev_ascending(cudaStream_t st, int64_t n, double* A, int64_t lda, double* w, double* Z,

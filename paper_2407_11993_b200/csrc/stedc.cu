@@ -136,7 +136,9 @@ struct DcWork {
 __global__ void dc_deflate_kernel(const int64_t* __restrict__ moff, const int* __restrict__ mn1,
                                   const int* __restrict__ mn, const double* __restrict__ ebeta,
                                   const double* __restrict__ lam, const double* __restrict__ Q,
-                                  int64_t ldq, DcWork w, double* rho_out, MergeInfo* info) {
+                                  int64_t ldq, DcWork w, double* rho_out, MergeInfo* info,
+                                  const double* __restrict__ xf = nullptr,
+                                  const double* __restrict__ xl = nullptr) {
   const int64_t off = moff[blockIdx.x];
   const int n1 = mn1[blockIdx.x], n = mn[blockIdx.x];
   const double beta = ebeta[blockIdx.x];
@@ -147,7 +149,9 @@ __global__ void dc_deflate_kernel(const int64_t* __restrict__ moff, const int* _
   // z in block-local column order
   for (int j = threadIdx.x; j < n; j += blockDim.x) {
     double v;
-    if (j < n1)
+    if (xf)  // implicit form: the children's last / first eigenvector rows are X columns
+      v = j < n1 ? xl[off + j] : xf[off + j];
+    else if (j < n1)
       v = Q[(off + n1 - 1) + (off + j) * ldq];
     else
       v = Q[(off + n1) + (off + j) * ldq];
@@ -551,6 +555,251 @@ __global__ void absmax_kernel(int64_t n, const double* d, const double* e, doubl
   }
 }
 
+// ---- implicit form: U^T Y without U --------------------------------------------------
+//
+// stedc_apply keeps, per tree node, X = U_node^T [Y_node | e_first | e_last] (n x (k + 2),
+// column-major, ld n): the operand rows in the node's eigenbasis plus the node's first and
+// last eigenvector rows, which are all a merge needs (z = [last row of U_1, first row of
+// U_2]). A merge is U = [U_1 0; 0 U_2] G P U~ (deflation rotations G, permutation P,
+// Cauchy-like secular eigenvectors U~), so X_new = U~^T P^T G^T [X_1; X_2]: rotations act
+// on rows of X, and U~ (zhat_i / (d_i - lambda_j), normalised) is generated tile by tile
+// inside the product and never stored. Memory O(n k) instead of the 3 n^2 of stedc.
+
+// One CTA per leaf: the QL iteration as dc_leaf_kernel, then X = Q_leaf^T [Y | e_0 | e_last].
+__global__ void __launch_bounds__(LEAF) dc_leaf_apply_kernel(
+    const int64_t* __restrict__ loff, const int* __restrict__ lsz, const double* __restrict__ d0,
+    const double* __restrict__ e0, double* lam, const double* __restrict__ Y, int64_t ldy, int k,
+    double* __restrict__ X, int64_t ldx) {
+  __shared__ double Qs[LEAF][LEAF + 1];
+  __shared__ double ys[LEAF];
+  const int64_t off = loff[blockIdx.x];
+  const int n = lsz[blockIdx.x];
+  const int row = threadIdx.x;
+  double d[LEAF], e[LEAF], z[LEAF];
+  for (int i = 0; i < n; ++i) {
+    d[i] = d0[off + i];
+    e[i] = (i < n - 1) ? e0[off + i] : 0.0;
+    z[i] = (i == row) ? 1.0 : 0.0;
+  }
+  const double eps = 2.220446049250313e-16;
+  for (int l = 0; l < n; ++l) {
+    int iter = 0;
+    int m;
+    do {
+      for (m = l; m < n - 1; ++m) {
+        const double dd = fabs(d[m]) + fabs(d[m + 1]);
+        if (fabs(e[m]) <= eps * dd) break;
+      }
+      if (m != l) {
+        if (++iter > 60) break;
+        double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
+        double r = hypot(g, 1.0);
+        g = d[m] - d[l] + e[l] / (g + copysign(r, g));
+        double s = 1.0, c = 1.0, p = 0.0;
+        int i;
+        bool underflow = false;
+        for (i = m - 1; i >= l; --i) {
+          double f = s * e[i];
+          const double b = c * e[i];
+          r = hypot(f, g);
+          e[i + 1] = r;
+          if (r == 0.0) {
+            d[i + 1] -= p;
+            e[m] = 0.0;
+            underflow = true;
+            break;
+          }
+          s = f / r;
+          c = g / r;
+          g = d[i + 1] - p;
+          r = (d[i] - g) * s + 2.0 * c * b;
+          p = s * r;
+          d[i + 1] = g + p;
+          g = c * r - b;
+          f = z[i + 1];
+          z[i + 1] = s * z[i] + c * f;
+          z[i] = c * z[i] - s * f;
+        }
+        if (underflow && i >= l) continue;
+        d[l] -= p;
+        e[l] = g;
+        e[m] = 0.0;
+      }
+    } while (m != l);
+  }
+  for (int i = 0; i < n - 1; ++i) {
+    int kk = i;
+    double p = d[i];
+    for (int j = i + 1; j < n; ++j)
+      if (d[j] < p) {
+        kk = j;
+        p = d[j];
+      }
+    if (kk != i) {
+      d[kk] = d[i];
+      d[i] = p;
+      const double t = z[i];
+      z[i] = z[kk];
+      z[kk] = t;
+    }
+  }
+  if (row < n)
+    for (int j = 0; j < n; ++j) Qs[row][j] = z[j];
+  if (row == 0)
+    for (int j = 0; j < n; ++j) lam[off + j] = d[j];
+  __syncthreads();
+  for (int c = 0; c < k; ++c) {
+    if (row < n) ys[row] = Y[(off + row) + c * ldy];
+    __syncthreads();
+    if (row < n) {
+      double acc = 0.0;
+      for (int r = 0; r < n; ++r) acc = fma(Qs[r][row], ys[r], acc);
+      X[(off + row) + c * ldx] = acc;
+    }
+    __syncthreads();
+  }
+  if (row < n) {
+    X[(off + row) + (int64_t)k * ldx] = Qs[0][row];
+    X[(off + row) + (int64_t)(k + 1) * ldx] = Qs[n - 1][row];
+  }
+}
+
+// Per merge, one thread per X column: keep only the left child's rows of the first-row
+// column and the right child's rows of the last-row column, then the deflation rotations.
+__global__ void dc_xrot_kernel(const int64_t* __restrict__ moff, const int* __restrict__ mn1,
+                               const int* __restrict__ mn, const MergeInfo* __restrict__ info,
+                               DcWork w, double* X, int64_t ldx, int ncol) {
+  const int mi = blockIdx.y;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncol) return;
+  const int64_t off = moff[mi];
+  const int n1 = mn1[mi], n = mn[mi];
+  double* col = X + off + (int64_t)c * ldx;
+  if (c == ncol - 2)
+    for (int r = n1; r < n; ++r) col[r] = 0.0;
+  else if (c == ncol - 1)
+    for (int r = 0; r < n1; ++r) col[r] = 0.0;
+  const int nrot = info[mi].nrot;
+  for (int q = 0; q < nrot; ++q) {
+    const int a = w.rot_a[off + q], b = w.rot_b[off + q];
+    const double cs = w.rot_c[off + q], sn = w.rot_s[off + q];
+    const double x = col[a], y = col[b];
+    col[a] = cs * x + sn * y;
+    col[b] = cs * y - sn * x;
+  }
+}
+
+// 1 / ||(zhat_i / (d_i - lambda_j))_i|| per secular root j (into w.sortd), one warp each
+__global__ void dc_unorm_kernel(const int64_t* __restrict__ moff,
+                                const MergeInfo* __restrict__ info, DcWork w) {
+  const int mi = blockIdx.y;
+  const int64_t off = moff[mi];
+  const int K = info[mi].K;
+  const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (j >= K) return;
+  const double* d = w.dlam + off;
+  const double dorg = d[w.org[off + j]], mu = w.mu[off + j];
+  double ss = 0.0;
+  for (int i = lane; i < K; i += 32) {
+    const double v = w.zhat[off + i] / ((d[i] - dorg) - mu);
+    ss = fma(v, v, ss);
+  }
+  ss = warp_sum(ss);
+  if (lane == 0) w.sortd[off + j] = 1.0 / sqrt(ss);
+}
+
+// Xg rows 0..K-1 <- X rows src(i) (non-deflated, secular order), K..n-1 <- deflated rows
+__global__ void dc_xgather_kernel(const int64_t* __restrict__ moff, const int* __restrict__ mn,
+                                  const MergeInfo* __restrict__ info, DcWork w,
+                                  const double* __restrict__ X, double* __restrict__ Xg,
+                                  int64_t ldx, int ncol) {
+  const int mi = blockIdx.z;
+  const int64_t off = moff[mi];
+  const int n = mn[mi], K = info[mi].K;
+  for (int c = blockIdx.y; c < ncol; c += gridDim.y)
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+      const int s = i < K ? w.src[off + i] : w.dcol[off + (i - K)];
+      Xg[(off + i) + (int64_t)c * ldx] = X[(off + s) + (int64_t)c * ldx];
+    }
+}
+
+// Xn(j, :) = sum_i U~(i, j) Xg(i, :) for the K secular roots; U~ generated per 16 x 64 tile.
+constexpr int XA_J = 64, XA_C = 64, XA_I = 16;
+__global__ void __launch_bounds__(256) dc_xapply_kernel(const int64_t* __restrict__ moff,
+                                                        const MergeInfo* __restrict__ info,
+                                                        DcWork w, const double* __restrict__ Xg,
+                                                        double* __restrict__ Xn, int64_t ldx,
+                                                        int ncol) {
+  __shared__ double Vs[XA_I][XA_J + 2];
+  __shared__ double Xs[XA_I][XA_C + 2];
+  const int mi = blockIdx.z;
+  const int64_t off = moff[mi];
+  const int K = info[mi].K;
+  const int j0 = blockIdx.x * XA_J, c0 = blockIdx.y * XA_C;
+  if (j0 >= K || c0 >= ncol) return;
+  const int tid = threadIdx.x;
+  const int tj = tid >> 4, tc = tid & 15;
+  const double* d = w.dlam + off;
+  double acc[4][4] = {};
+  for (int i0 = 0; i0 < K; i0 += XA_I) {
+    for (int t = tid; t < XA_I * XA_J; t += 256) {
+      const int ii = t / XA_J, jj = t % XA_J;
+      const int i = i0 + ii, j = j0 + jj;
+      double v = 0.0;
+      if (i < K && j < K)
+        v = w.zhat[off + i] / ((d[i] - d[w.org[off + j]]) - w.mu[off + j]) * w.sortd[off + j];
+      Vs[ii][jj] = v;
+    }
+    for (int t = tid; t < XA_I * XA_C; t += 256) {
+      const int cc = t / XA_I, ii = t % XA_I;
+      const int i = i0 + ii, c = c0 + cc;
+      Xs[ii][cc] = (i < K && c < ncol) ? Xg[(off + i) + (int64_t)c * ldx] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int ii = 0; ii < XA_I; ++ii) {
+      double a[4], b[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        a[q] = Vs[ii][tj * 4 + q];
+        b[q] = Xs[ii][tc * 4 + q];
+      }
+#pragma unroll
+      for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[p][q] = fma(a[p], b[q], acc[p][q]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const int j = j0 + tj * 4 + p;
+    if (j >= K) continue;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int c = c0 + tc * 4 + q;
+      if (c < ncol) Xn[(off + j) + (int64_t)c * ldx] = acc[p][q];
+    }
+  }
+}
+
+// X row t <- Xn row p (new root p) or Xg row K + b (deflated entry b), in final order
+__global__ void dc_xplace_kernel(const int64_t* __restrict__ moff, const int* __restrict__ mn,
+                                 const MergeInfo* __restrict__ info, DcWork w,
+                                 const double* __restrict__ Xn, const double* __restrict__ Xg,
+                                 double* __restrict__ X, int64_t ldx, int ncol) {
+  const int mi = blockIdx.z;
+  const int64_t off = moff[mi];
+  const int n = mn[mi], K = info[mi].K;
+  for (int c = blockIdx.y; c < ncol; c += gridDim.y)
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+      const int p = w.perm[off + t];
+      X[(off + t) + (int64_t)c * ldx] = p >= 0 ? Xn[(off + p) + (int64_t)c * ldx]
+                                               : Xg[(off + K + (-1 - p)) + (int64_t)c * ldx];
+    }
+}
+
 // ---- driver -----------------------------------------------------------------------
 
 struct Node {
@@ -790,6 +1039,185 @@ void stedc(cudaStream_t st, int64_t n, double* d, double* e, double* Z, int64_t 
   }
   // result: lam_cur (scaled), Qcur
   if (Qcur != Z) copy_matrix(st, false, n, n, Qcur, n, Z, ldz);
+  EM_CK(cudaMemcpyAsync(d, lam_cur, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  scale_vec_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, d, scal.p, 0);
+  EM_LAUNCHED();
+  EM_CK(cudaStreamSynchronize(st));
+}
+
+}  // namespace em
+
+namespace em {
+
+// Eigenvalues of the symmetric tridiagonal (d, e) ascending in d, and Y (n x k) <- U^T Y
+// for its eigenvector matrix U, without forming U (the implicit form above).
+void stedc_apply(cudaStream_t st, int64_t n, double* d, double* e, double* Y, int64_t ldy,
+                 int64_t k) {
+  if (n <= 0) return;
+  std::vector<std::vector<Node>> levels;
+  levels.push_back({Node{0, n}});
+  while (true) {
+    bool split = false;
+    for (auto& nd : levels.back())
+      if (nd.n > LEAF) split = true;
+    if (!split) break;
+    std::vector<Node> nxt;
+    for (auto& nd : levels.back()) {
+      if (nd.n > LEAF) {
+        const int64_t n1 = nd.n / 2;
+        nxt.push_back({nd.off, n1});
+        nxt.push_back({nd.off + n1, nd.n - n1});
+      } else {
+        nxt.push_back(nd);
+      }
+    }
+    levels.push_back(nxt);
+  }
+  DBuf scal(1, st);
+  absmax_kernel<<<1, 1024, 0, st>>>(n, d, e, scal.p);
+  EM_LAUNCHED();
+  scale_vec_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, d, scal.p, 1);
+  EM_LAUNCHED();
+  if (n > 1) {
+    scale_vec_kernel<<<(unsigned)((n - 1 + 255) / 256), 256, 0, st>>>(n - 1, e, scal.p, 1);
+    EM_LAUNCHED();
+  }
+  std::vector<int64_t> splits;
+  for (size_t L = 0; L + 1 < levels.size(); ++L)
+    for (auto& nd : levels[L])
+      if (nd.n > LEAF) splits.push_back(nd.off + nd.n / 2);
+  std::sort(splits.begin(), splits.end());
+  const int nsplit = (int)splits.size();
+  DArr<int64_t> dsplit(imax64(nsplit, 1), st);
+  DBuf betas(imax64(nsplit, 1), st);
+  std::vector<double> hb(imax64(nsplit, 1));
+  if (nsplit) {
+    EM_CK(cudaMemcpyAsync(dsplit.p, splits.data(), nsplit * sizeof(int64_t),
+                          cudaMemcpyHostToDevice, st));
+    dc_tear_kernel<<<(nsplit + 127) / 128, 128, 0, st>>>(nsplit, dsplit.p, d, e, betas.p);
+    EM_LAUNCHED();
+    EM_CK(cudaMemcpyAsync(hb.data(), betas.p, nsplit * sizeof(double), cudaMemcpyDeviceToHost,
+                          st));
+  }
+  const int ncol = (int)k + 2;
+  const int64_t ldx = n;
+  DBuf lam(n, st), lam2(n, st), X((size_t)n * ncol, st), Xg((size_t)n * ncol, st),
+      Xn((size_t)n * ncol, st);
+  {
+    const auto& leaves = levels.back();
+    std::vector<int64_t> lo;
+    std::vector<int> ls;
+    for (auto& nd : leaves) {
+      lo.push_back(nd.off);
+      ls.push_back((int)nd.n);
+    }
+    DArr<int64_t> dlo(lo.size(), st);
+    DArr<int> dls(ls.size(), st);
+    EM_CK(cudaMemcpyAsync(dlo.p, lo.data(), lo.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    EM_CK(cudaMemcpyAsync(dls.p, ls.data(), ls.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    dc_leaf_apply_kernel<<<(unsigned)leaves.size(), LEAF, 0, st>>>(dlo.p, dls.p, d, e, lam.p, Y,
+                                                                   ldy, (int)k, X.p, ldx);
+    EM_LAUNCHED();
+    EM_CK(cudaStreamSynchronize(st));
+  }
+  DBuf wd((size_t)n * 10, st);
+  DArr<int> wi((size_t)n * 8, st);
+  DcWork w;
+  w.dlam = wd.p;
+  w.wz = wd.p + n;
+  w.dval = wd.p + 2 * n;
+  w.rot_c = wd.p + 3 * n;
+  w.rot_s = wd.p + 4 * n;
+  w.mu = wd.p + 5 * n;
+  w.zhat = wd.p + 6 * n;
+  w.lamn = wd.p + 7 * n;
+  w.sortd = wd.p + 8 * n;
+  w.sortz = wd.p + 9 * n;
+  w.src = wi.p;
+  w.pos = wi.p + n;
+  w.dcol = wi.p + 2 * n;
+  w.rot_a = wi.p + 3 * n;
+  w.rot_b = wi.p + 4 * n;
+  w.org = wi.p + 5 * n;
+  w.typ = wi.p + 6 * n;
+  w.perm = wi.p + 7 * n;
+  double* lam_cur = lam.p;
+  double* lam_nxt = lam2.p;
+  const double* xf = X.p + (int64_t)k * ldx;
+  const double* xl = X.p + (int64_t)(k + 1) * ldx;
+  for (int L = (int)levels.size() - 2; L >= 0; --L) {
+    std::vector<int64_t> mo;
+    std::vector<int> m1, mnn;
+    std::vector<double> mb;
+    for (auto& nd : levels[L]) {
+      if (nd.n <= LEAF) continue;
+      mo.push_back(nd.off);
+      m1.push_back((int)(nd.n / 2));
+      mnn.push_back((int)nd.n);
+      const int64_t s = nd.off + nd.n / 2;
+      mb.push_back(hb[std::lower_bound(splits.begin(), splits.end(), s) - splits.begin()]);
+    }
+    const int nm = (int)mo.size();
+    if (nm == 0) continue;
+    DArr<int64_t> dmo(nm, st);
+    DArr<int> dm1(nm, st), dmn(nm, st);
+    DBuf mbeta(nm, st), mrho(nm, st);
+    DArr<MergeInfo> minfo(nm, st);
+    EM_CK(cudaMemcpyAsync(dmo.p, mo.data(), nm * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    EM_CK(cudaMemcpyAsync(dm1.p, m1.data(), nm * sizeof(int), cudaMemcpyHostToDevice, st));
+    EM_CK(cudaMemcpyAsync(dmn.p, mnn.data(), nm * sizeof(int), cudaMemcpyHostToDevice, st));
+    EM_CK(cudaMemcpyAsync(mbeta.p, mb.data(), nm * sizeof(double), cudaMemcpyHostToDevice, st));
+    dc_deflate_kernel<<<nm, 128, 0, st>>>(dmo.p, dm1.p, dmn.p, mbeta.p, lam_cur, nullptr, 0, w,
+                                          mrho.p, minfo.p, xf, xl);
+    EM_LAUNCHED();
+    std::vector<MergeInfo> hi(nm);
+    EM_CK(cudaMemcpyAsync(hi.data(), minfo.p, nm * sizeof(MergeInfo), cudaMemcpyDeviceToHost, st));
+    EM_CK(cudaStreamSynchronize(st));
+    int maxn = 0, maxK = 0;
+    for (int q = 0; q < nm; ++q) {
+      maxn = std::max(maxn, mnn[q]);
+      maxK = std::max(maxK, hi[q].K);
+    }
+    dc_xrot_kernel<<<dim3((unsigned)((ncol + 127) / 128), (unsigned)nm), 128, 0, st>>>(
+        dmo.p, dm1.p, dmn.p, minfo.p, w, X.p, ldx, ncol);
+    EM_LAUNCHED();
+    const unsigned gy = (unsigned)std::min(ncol, 65535);
+    dc_xgather_kernel<<<dim3((unsigned)std::max(1, std::min((maxn + 255) / 256, 64)), gy,
+                             (unsigned)nm), 256, 0, st>>>(dmo.p, dmn.p, minfo.p, w, X.p, Xg.p,
+                                                          ldx, ncol);
+    EM_LAUNCHED();
+    if (maxK > 0) {
+      dim3 g1((unsigned)((maxK + 127) / 128), (unsigned)nm);
+      stage_begin(st, ST_STEDC_SECULAR);
+      dc_secular_kernel<<<g1, 128, 0, st>>>(dmo.p, minfo.p, mrho.p, w);
+      EM_LAUNCHED();
+      stage_end(st, ST_STEDC_SECULAR);
+      dc_zhat_kernel<<<g1, 128, 0, st>>>(dmo.p, minfo.p, w);
+      EM_LAUNCHED();
+      dc_unorm_kernel<<<dim3((unsigned)((maxK + 7) / 8), (unsigned)nm), 256, 0, st>>>(dmo.p,
+                                                                                    minfo.p, w);
+      EM_LAUNCHED();
+      Stage sg(st, ST_STEDC_GEMM);
+      dc_xapply_kernel<<<dim3((unsigned)((maxK + XA_J - 1) / XA_J),
+                              (unsigned)((ncol + XA_C - 1) / XA_C), (unsigned)nm), 256, 0, st>>>(
+          dmo.p, minfo.p, w, Xg.p, Xn.p, ldx, ncol);
+      EM_LAUNCHED();
+    }
+    dc_order_kernel<<<nm, 32, 0, st>>>(dmo.p, dmn.p, minfo.p, w, lam_nxt);
+    EM_LAUNCHED();
+    dc_xplace_kernel<<<dim3((unsigned)std::max(1, std::min((maxn + 255) / 256, 64)), gy,
+                            (unsigned)nm), 256, 0, st>>>(dmo.p, dmn.p, minfo.p, w, Xn.p, Xg.p,
+                                                         X.p, ldx, ncol);
+    EM_LAUNCHED();
+    for (auto& nd : levels[L]) {  // leaf-sized nodes carried up keep their rows of X
+      if (nd.n > LEAF) continue;
+      EM_CK(cudaMemcpyAsync(lam_nxt + nd.off, lam_cur + nd.off, nd.n * sizeof(double),
+                            cudaMemcpyDeviceToDevice, st));
+    }
+    EM_CK(cudaStreamSynchronize(st));
+    std::swap(lam_cur, lam_nxt);
+  }
+  copy_matrix(st, false, n, k, X.p, ldx, Y, ldy);
   EM_CK(cudaMemcpyAsync(d, lam_cur, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
   scale_vec_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, d, scal.p, 0);
   EM_LAUNCHED();

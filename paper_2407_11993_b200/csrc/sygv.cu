@@ -30,7 +30,7 @@ static double two_stage_extra(int64_t ldz, int64_t n) {
   return stedc > q1 ? (stedc > q2 ? stedc : q2) : (q1 > q2 ? q1 : q2);
 }
 int g_last_eig_path = 0;  // em_info(EM_INFO_EIG_PATH): 1 one-stage, 2 two-stage
-static bool two_stage_fits(int64_t n, int64_t ldz) {
+static bool two_stage_fits(int64_t n, int64_t ldz, bool implicit) {
   size_t free_b = 0, total_b = 0;
   if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return false;
   // plus what the stream-ordered pool holds reserved but unused (em_init keeps freed
@@ -45,8 +45,9 @@ static bool two_stage_fits(int64_t n, int64_t ldz) {
         reserved > used)
       free_b += (size_t)(reserved - used);
   }
-  const double need =
-      two_stage_extra(ldz, n) * (double)n * (double)n * sizeof(double) + (1ull << 30);
+  // implicit mode: the Q2 T factors (1/2); the reflectors live in A, nothing else is n^2
+  const double need = (implicit ? 0.5 : two_stage_extra(ldz, n)) * (double)n * (double)n *
+                          sizeof(double) + (1ull << 30);
   return (double)free_b >= need;
 }
 // em_config(EM_CFG_BAND_OFF): 1 forces the dense R path (tests compare both)
@@ -93,7 +94,8 @@ __global__ void gershgorin_kernel(int64_t n, const double* __restrict__ A, int64
 // Gershgorin interval when R is strictly diagonally dominant (the plates' stencil). Cholesky
 // completes when 20 n^1.5 kappa eps < 1 (Demmel); this asks for 100x margin.
 static bool certificate_redundant(cudaStream_t st, int64_t n, const double* R, int64_t ldr,
-                                  double tau_min, double tau_max) {
+                                  double tau_min, double tau_max, const double* Rb = nullptr,
+                                  int64_t ldrb = 0, int64_t rbw = 0) {
   if (!(tau_min > 0.0) || !(tau_max >= tau_min)) return false;
   DArr<unsigned long long> b(2, st);
   DArr<int> neg(1, st);
@@ -102,7 +104,11 @@ static bool certificate_redundant(cudaStream_t st, int64_t n, const double* R, i
   memcpy(&init[0], &inf, sizeof(double));
   EM_CK(cudaMemcpyAsync(b.p, init, sizeof(init), cudaMemcpyHostToDevice, st));
   EM_CK(cudaMemsetAsync(neg.p, 0, sizeof(int), st));
-  gershgorin_kernel<<<(unsigned)n, 256, 0, st>>>(n, R, ldr, b.p, b.p + 1, neg.p);
+  if (Rb)
+    band_gershgorin_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(n, Rb, ldrb, rbw, b.p,
+                                                                    b.p + 1, neg.p);
+  else
+    gershgorin_kernel<<<(unsigned)n, 256, 0, st>>>(n, R, ldr, b.p, b.p + 1, neg.p);
   EM_LAUNCHED();
   unsigned long long hb[2];
   int hneg = 0;
@@ -128,7 +134,7 @@ void syev_ascending(cudaStream_t st, int64_t n, double* A, int64_t lda, double* 
                     int64_t ldz, int64_t c0, int64_t nc, double* Yt, int64_t ldy, int64_t ky) {
   if (n <= 0) return;
   if (nc < 0) nc = n - c0;
-  if (n >= g_two_stage_min && n > 2 * kBand && two_stage_fits(n, ldz)) {
+  if (n >= g_two_stage_min && n > 2 * kBand && two_stage_fits(n, ldz, Yt != nullptr)) {
     g_last_eig_path = 2;
     syev_two_stage(st, n, A, lda, w, Z, ldz, c0, nc, Yt, ldy, ky);
     return;
@@ -139,16 +145,20 @@ void syev_ascending(cudaStream_t st, int64_t n, double* A, int64_t lda, double* 
     Stage s(st, ST_SYTRD);
     sytrd_lower(st, n, A, lda, d.p, e.p, tau.p);
   }
-  {
-    Stage s(st, ST_STEDC);
-    stedc(st, n, d.p, e.p, Z, ldz);
-  }
-  {
-    Stage s(st, ST_ORMTR);
-    if (Yt)  // implicit mode: Yt <- Q^T Yt
+  if (Yt) {  // implicit mode: Yt <- U^T Q^T Yt, U never formed
+    {
+      Stage s(st, ST_ORMTR);
       ormqr_lower_off(st, n, n - 1, 1, ky, A, lda, tau.p, Yt, ldy, true);
-    else
-      ormtr_lower(st, n, nc, A, lda, tau.p, Z + c0 * ldz, ldz);
+    }
+    Stage s(st, ST_STEDC);
+    stedc_apply(st, n, d.p, e.p, Yt, ldy, ky);
+  } else {
+    {
+      Stage s(st, ST_STEDC);
+      stedc(st, n, d.p, e.p, Z, ldz);
+    }
+    Stage s(st, ST_ORMTR);
+    ormtr_lower(st, n, nc, A, lda, tau.p, Z + c0 * ldz, ldz);
   }
   EM_CK(cudaMemcpyAsync(w, d.p, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
 }
@@ -331,7 +341,8 @@ __global__ void quadform_lower_kernel(int64_t n, const double* __restrict__ V, i
 int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const double* R,
              int64_t ldr, double* tau, double* V, int64_t ldv, double* l_n, double* r_n,
              double* VtR, int64_t ldvtr, int* which, int flags, cudaEvent_t l_ready,
-             int64_t m_lo, int64_t m_hi, double* Y, int64_t ldy, int64_t ky) {
+             int64_t m_lo, int64_t m_hi, double* Y, int64_t ldy, int64_t ky, const double* Rb,
+             int64_t ldrb, int64_t rbw) {
   *which = -1;
   if (n <= 0) return -1;
   const bool implicit = Y != nullptr;
@@ -341,12 +352,17 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
   if (m_lo < 0 || m_hi > n || m_lo > m_hi) throw ArgError{"mode range outside [0, n]"};
   const int64_t m = m_hi - m_lo;
   const bool slice = m < n;
+  // in-place L (EM_SYGV_L_WORKSPACE): L's storage becomes the reduced matrix B; R in band
+  // storage (Rb): no dense R anywhere. Together the N = 120,000 solve fits one GPU.
+  const bool l_ws = (flags & EM_SYGV_L_WORKSPACE) && ldl >= n;
+  const bool r_band = Rb != nullptr;
+  if (r_band && (rbw < 0 || ldrb < rbw + 1)) throw ArgError{"bad band storage of R"};
   // slice: the full tridiagonal eigenvector matrix needs an n x n workspace (the output V
-  // holds only m columns); it also hosts the certificate factor of L
+  // holds only m columns); implicit mode forms no eigenvector matrix at all
   DBuf Zfull;
   double* Zw = V;
   int64_t ldzw = ldv;
-  if (slice) {
+  if (slice && !implicit) {
     Zfull.alloc((size_t)n * n, st);
     Zw = Zfull.p;
     ldzw = n;
@@ -355,14 +371,14 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
   // A banded R (the 7-point stencil R of the plates: lower bandwidth ny*nz) is factored
   // in banded storage and every solve with its factor is banded (band.cu): the R stages
   // cost N b^2 + 6 N^2 b instead of 7/3 N^3, and no N x N factor buffer is needed.
-  const int64_t bw = g_band_off ? n : band_lower_width(st, n, R, ldr);
-  const bool banded = n > 2 * kTrsmBlock && (bw + kTrsmBlock) * 4 <= n;
+  const int64_t bw = r_band ? rbw : (g_band_off ? n : band_lower_width(st, n, R, ldr));
+  const bool banded = r_band || (n > 2 * kTrsmBlock && (bw + kTrsmBlock) * 4 <= n);
   BandChol bc;
   // EM_SYGV_R_WORKSPACE (dense-band R only): when R is sparse, keep a CSR copy, factor R
   // in its own storage and restore it from the copy before returning: one N x N buffer
   // less at the peak
   Csr rcsr;
-  const bool r_ws = !banded && (flags & EM_SYGV_R_WORKSPACE) &&
+  const bool r_ws = !banded && !r_band && (flags & EM_SYGV_R_WORKSPACE) &&
                     csr_from_dense(st, n, R, ldr, 0.02, rcsr);
   DBuf Gbuf;
   double* G = const_cast<double*>(R);
@@ -380,7 +396,9 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
   DBuf GDinv;
   {
     Stage s(st, ST_POTRF_R);
-    if (banded) {
+    if (r_band) {
+      piv = band_potrf(st, n, Rb, ldrb, bw, bc, true);
+    } else if (banded) {
       piv = band_potrf(st, n, R, ldr, bw, bc);
     } else {
       GDinv.alloc((size_t)((n + kTrsmBlock - 1) / kTrsmBlock) * kTrsmBlock * kTrsmBlock, st);
@@ -403,33 +421,41 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
   }
   // leading dimension padded to 32 doubles: every column of B starts 256-byte aligned,
   // so all TMA boxes of the tridiagonalisation's symv are (symv_tma.cu)
-  const int64_t ldb = (n + 31) / 32 * 32;
-  DBuf B((size_t)ldb * n, st);
+  // (in place in L's storage when allowed and L's columns are 256-byte aligned)
+  const bool b_in_l = l_ws && ldl % 32 == 0;
+  const int64_t ldb = b_in_l ? ldl : (n + 31) / 32 * 32;
+  // certificate only (modal.py:69-70): with EM_CFG_L_CERTIFICATE = 1 L is factored up
+  // front in a copy of its own (before an in-place solve destroys it)
+  if (g_l_certificate) {
+    Stage s(st, ST_POTRF_L);
+    DBuf Lc((size_t)n * n, st);
+    copy_matrix(st, false, n, n, L, ldl, Lc.p, n);
+    piv = potrf(st, n, Lc.p, n);
+    if (piv >= 0) {
+      *which = 1;
+      restore_r();
+      EM_CK(cudaStreamSynchronize(st));
+      return piv;
+    }
+  }
+  DBuf Bown;
+  double* Bp = const_cast<double*>(L);
+  if (!b_in_l) {
+    Bown.alloc((size_t)ldb * n, st);
+    Bp = Bown.p;
+  }
   {
     {
       // B = G^-1 L G^-T. The reference forms G^-1 (G^-1 L)^T with two full solves and
       // averages it with its transpose (modal.py:63-67); the two-sided recursive
       // reduction gives the same symmetric matrix to round-off with half the flops.
       Stage s(st, ST_SYGST);
-      copy_matrix(st, false, n, n, L, ldl, B.p, ldb);
-      mirror_lower(st, n, B.p, ldb);  // SymMatrix semantics: the lower triangle defines L
+      if (!b_in_l) copy_matrix(st, false, n, n, L, ldl, Bp, ldb);
+      mirror_lower(st, n, Bp, ldb);  // SymMatrix semantics: the lower triangle defines L
       if (banded)
-        band_sygst(st, bc, B.p, ldb);  // the reference's X = G^-1 L, G^-1 X^T, (B + B^T)/2
+        band_sygst(st, bc, Bp, ldb);  // the reference's X = G^-1 L, G^-1 X^T, (B + B^T)/2
       else
-        sygst_lower(st, n, B.p, ldb, G, ldg, GDinv.p);
-    }
-    // certificate only (modal.py:69-70), factored in the (still free) eigenvector buffer;
-    // by default deferred until the spectrum shows whether it is needed
-    if (g_l_certificate) {
-      Stage s(st, ST_POTRF_L);
-      copy_matrix(st, false, n, n, L, ldl, Zw, ldzw);
-      piv = potrf(st, n, Zw, ldzw);
-    }
-    if (piv >= 0) {
-      *which = 1;
-      restore_r();
-      EM_CK(cudaStreamSynchronize(st));
-      return piv;
+        sygst_lower(st, n, Bp, ldb, G, ldg, GDinv.p);
     }
   }
   // eigenvectors are formed directly in the output buffer V (D&C, ormtr, back-transform,
@@ -438,9 +464,9 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
   DBuf w(n, st);
   // descending modes m_lo .. m_hi - 1 are the ascending columns n - m_hi .. n - m_lo - 1
   const int64_t c0 = n - m_hi;
-  double* Zs = Zw + c0 * ldzw;
-  syev_ascending(st, n, B.p, ldb, w.p, Zw, ldzw, c0, m, implicit ? Y : nullptr, ldy, ky);
-  B.release();
+  double* Zs = Zw ? Zw + c0 * ldzw : nullptr;
+  syev_ascending(st, n, Bp, ldb, w.p, Zw, ldzw, c0, m, implicit ? Y : nullptr, ldy, ky);
+  Bown.release();
   if (m > 0) {
     Stage s(st, ST_TRSM_BACK);
     if (banded)
@@ -458,7 +484,10 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
     EM_CK(cudaMemcpyAsync(&wb[0], w.p, sizeof(double), cudaMemcpyDeviceToHost, st));
     EM_CK(cudaMemcpyAsync(&wb[1], w.p + (n - 1), sizeof(double), cudaMemcpyDeviceToHost, st));
     EM_CK(cudaStreamSynchronize(st));
-    if (!certificate_redundant(st, n, R, ldr, wb[0], wb[1])) {
+    if (!certificate_redundant(st, n, R, ldr, wb[0], wb[1], Rb, ldrb, rbw)) {
+      if (b_in_l)
+        throw ArgError{"the certificate of L is needed but L was solved in place "
+                       "(EM_SYGV_L_WORKSPACE): solve again without it"};
       Stage s(st, ST_POTRF_L);
       DBuf Lc((size_t)n * n, st);
       copy_matrix(st, false, n, n, L, ldl, Lc.p, n);
@@ -473,9 +502,9 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
   if (implicit) {
     // Y <- U^T Y, rows reversed to descending order; tau, l_n = tau, r_n = 1
     Stage s(st, ST_FINALIZE);
-    if (ky > 0) {
+    if (ky > 0) {  // syev_ascending left U^T Q^T G^-1 Y in Y, ascending rows
       DBuf T((size_t)n * ky, st);
-      EM_CK(gemm(st, true, false, n, ky, n, 1.0, Zw, ldzw, Y, ldy, 0.0, T.p, n));
+      copy_matrix(st, false, n, ky, Y, ldy, T.p, n);
       copy_reversed_rows(st, n, ky, T.p, n, Y, ldy);
       EM_CK(cudaStreamSynchronize(st));
     }

@@ -537,11 +537,11 @@ __global__ void __launch_bounds__(128) larft_smem_kernel(int w, int w1,
 __global__ void __launch_bounds__(128) larft_batched_kernel(int64_t nref, int nb,
                                                             const double* __restrict__ G,
                                                             const double* __restrict__ tau,
-                                                            double* T) {
+                                                            double* T, int64_t p0) {
   extern __shared__ double Ts[];
   __shared__ double gk[128];
-  const int64_t p = blockIdx.y;
-  const int64_t c0 = p * nb;
+  const int64_t p = blockIdx.y;  // block p0 + p, stored at index p
+  const int64_t c0 = (p0 + p) * nb;
   const int w = (int)imin64(nb, nref - c0);
   const int w1 = w < 128 ? w : 128;
   if (blockIdx.x == 1 && w <= w1) return;
@@ -569,66 +569,75 @@ void ormqr_lower_off(cudaStream_t st, int64_t n, int64_t nref, int64_t off, int6
   if (nref <= 0 || m <= 0) return;
   const int64_t npan = (nref + ORM_NB - 1) / ORM_NB;
   const size_t vstride = (size_t)n * ORM_NB, tstride = (size_t)ORM_NB * ORM_NB;
-  DBuf V(vstride * npan, st), G(tstride * npan, st), T(tstride * npan, st),
-      T1G(tstride * npan, st);
+  // the V blocks are built a chunk of panels at a time (about 2 GiB), so the workspace
+  // stays O(n) columns instead of the n x nref of all blocks at once (N = 120,000 fits)
+  const int64_t chunk =
+      imax64(1, imin64(npan, (int64_t)((2ull << 30) / (vstride * sizeof(double)))));
+  const int64_t nch = (npan + chunk - 1) / chunk;
+  DBuf V(vstride * chunk, st), G(tstride * chunk, st), T(tstride * chunk, st),
+      T1G(tstride * chunk, st);
   DBuf W1((size_t)ORM_NB * m, st), W2((size_t)ORM_NB * m, st);
   EM_CK(cudaFuncSetAttribute(larft_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(128 * 129 * sizeof(double))));
-  std::vector<GemmArgs> gg, t1, t2;
-  int max_g = 1, max_t = 1;
-  for (int64_t p = 0; p < npan; ++p) {
-    const int64_t i0 = p * ORM_NB;
-    const int w = (int)imin64(ORM_NB, nref - i0);
-    const int64_t mr = n - i0 - off;
-    double* Vp = V.p + p * vstride;
-    dim3 grid((unsigned)imax64(1, imin64((mr + 255) / 256, 64)), (unsigned)w);
-    build_v_kernel<<<grid, 256, 0, st>>>(n, A, lda, i0, w, off, Vp, n);
-    EM_LAUNCHED();
-    double* Gp = G.p + p * tstride;
-    gg.push_back(GemmArgs{w, w, mr, Vp, n, Vp, n, Gp, w, 1.0, 0.0, 0});
-    max_g = (int)imax64(max_g, ((w + 127) / 128) * ((w + 63) / 64));
-    const int w1 = (int)imin64(w, 128), w2 = w - w1;
-    double* Tp = T.p + p * tstride;
-    if (w2 > 0) {  // T12 = -T1 G12 T2 (larft joins of the two halves)
-      double* Xp = T1G.p + p * tstride;
-      t1.push_back(GemmArgs{w1, w2, w1, Tp, w, Gp + (int64_t)w1 * w, w, Xp, w1, 1.0, 0.0, 0});
-      t2.push_back(GemmArgs{w1, w2, w2, Xp, w1, Tp + w1 + (int64_t)w1 * w, w,
-                            Tp + (int64_t)w1 * w, w, -1.0, 0.0, 0});
-      max_t = (int)imax64(max_t, 4);
-    }
-  }
-  DArr<GemmArgs> dgg(gg.size(), st), dt1(imax64((int64_t)t1.size(), 1), st),
-      dt2(imax64((int64_t)t2.size(), 1), st);
-  EM_CK(cudaMemcpyAsync(dgg.p, gg.data(), gg.size() * sizeof(GemmArgs), cudaMemcpyHostToDevice,
-                        st));
-  EM_CK(gemm_grouped(st, true, false, dgg.p, (int)gg.size(), max_g));
   EM_CK(cudaFuncSetAttribute(larft_batched_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(128 * 129 * sizeof(double))));
-  larft_batched_kernel<<<dim3(2, (unsigned)npan), 128, (size_t)128 * 129 * sizeof(double), st>>>(
-      nref, ORM_NB, G.p, tau, T.p);
-  EM_LAUNCHED();
-  if (!t1.empty()) {
-    EM_CK(cudaMemcpyAsync(dt1.p, t1.data(), t1.size() * sizeof(GemmArgs),
-                          cudaMemcpyHostToDevice, st));
-    EM_CK(cudaMemcpyAsync(dt2.p, t2.data(), t2.size() * sizeof(GemmArgs),
-                          cudaMemcpyHostToDevice, st));
-    EM_CK(gemm_grouped(st, false, false, dt1.p, (int)t1.size(), max_t));
-    EM_CK(gemm_grouped(st, false, false, dt2.p, (int)t2.size(), max_t));
-  }
   // Q Z: blocks last to first with T; Q^T Z: first to last with T^T
-  for (int64_t s = 0; s < npan; ++s) {
-    const int64_t p = trans ? s : npan - 1 - s;
-    const int64_t i0 = p * ORM_NB;
-    const int w = (int)imin64(ORM_NB, nref - i0);
-    const int64_t mr = n - i0 - off;
-    const double* Vp = V.p + p * vstride;
-    const double* Tp = T.p + p * tstride;
-    double* Zs = Z + (i0 + off);
-    EM_CK(gemm(st, true, false, w, m, mr, 1.0, Vp, n, Zs, ldz, 0.0, W1.p, w));
-    EM_CK(gemm(st, trans, false, w, m, w, 1.0, Tp, w, W1.p, w, 0.0, W2.p, w));
-    EM_CK(gemm(st, false, false, mr, m, w, -1.0, Vp, n, W2.p, w, 1.0, Zs, ldz));
+  for (int64_t cs = 0; cs < nch; ++cs) {
+    const int64_t ci = trans ? cs : nch - 1 - cs;
+    const int64_t p0 = ci * chunk, p1 = imin64(npan, p0 + chunk), np = p1 - p0;
+    std::vector<GemmArgs> gg, t1, t2;
+    int max_g = 1, max_t = 1;
+    for (int64_t p = p0; p < p1; ++p) {
+      const int64_t i0 = p * ORM_NB;
+      const int w = (int)imin64(ORM_NB, nref - i0);
+      const int64_t mr = n - i0 - off;
+      double* Vp = V.p + (p - p0) * vstride;
+      dim3 grid((unsigned)imax64(1, imin64((mr + 255) / 256, 64)), (unsigned)w);
+      build_v_kernel<<<grid, 256, 0, st>>>(n, A, lda, i0, w, off, Vp, n);
+      EM_LAUNCHED();
+      double* Gp = G.p + (p - p0) * tstride;
+      gg.push_back(GemmArgs{w, w, mr, Vp, n, Vp, n, Gp, w, 1.0, 0.0, 0});
+      max_g = (int)imax64(max_g, ((w + 127) / 128) * ((w + 63) / 64));
+      const int w1 = (int)imin64(w, 128), w2 = w - w1;
+      double* Tp = T.p + (p - p0) * tstride;
+      if (w2 > 0) {  // T12 = -T1 G12 T2 (larft joins of the two halves)
+        double* Xp = T1G.p + (p - p0) * tstride;
+        t1.push_back(GemmArgs{w1, w2, w1, Tp, w, Gp + (int64_t)w1 * w, w, Xp, w1, 1.0, 0.0, 0});
+        t2.push_back(GemmArgs{w1, w2, w2, Xp, w1, Tp + w1 + (int64_t)w1 * w, w,
+                              Tp + (int64_t)w1 * w, w, -1.0, 0.0, 0});
+        max_t = (int)imax64(max_t, 4);
+      }
+    }
+    DArr<GemmArgs> dgg(gg.size(), st), dt1(imax64((int64_t)t1.size(), 1), st),
+        dt2(imax64((int64_t)t2.size(), 1), st);
+    EM_CK(cudaMemcpyAsync(dgg.p, gg.data(), gg.size() * sizeof(GemmArgs),
+                          cudaMemcpyHostToDevice, st));
+    EM_CK(gemm_grouped(st, true, false, dgg.p, (int)gg.size(), max_g));
+    larft_batched_kernel<<<dim3(2, (unsigned)np), 128, (size_t)128 * 129 * sizeof(double), st>>>(
+        nref, ORM_NB, G.p, tau, T.p, p0);
+    EM_LAUNCHED();
+    if (!t1.empty()) {
+      EM_CK(cudaMemcpyAsync(dt1.p, t1.data(), t1.size() * sizeof(GemmArgs),
+                            cudaMemcpyHostToDevice, st));
+      EM_CK(cudaMemcpyAsync(dt2.p, t2.data(), t2.size() * sizeof(GemmArgs),
+                            cudaMemcpyHostToDevice, st));
+      EM_CK(gemm_grouped(st, false, false, dt1.p, (int)t1.size(), max_t));
+      EM_CK(gemm_grouped(st, false, false, dt2.p, (int)t2.size(), max_t));
+    }
+    for (int64_t s = 0; s < np; ++s) {
+      const int64_t p = trans ? p0 + s : p1 - 1 - s;
+      const int64_t i0 = p * ORM_NB;
+      const int w = (int)imin64(ORM_NB, nref - i0);
+      const int64_t mr = n - i0 - off;
+      const double* Vp = V.p + (p - p0) * vstride;
+      const double* Tp = T.p + (p - p0) * tstride;
+      double* Zs = Z + (i0 + off);
+      EM_CK(gemm(st, true, false, w, m, mr, 1.0, Vp, n, Zs, ldz, 0.0, W1.p, w));
+      EM_CK(gemm(st, trans, false, w, m, w, 1.0, Tp, w, W1.p, w, 0.0, W2.p, w));
+      EM_CK(gemm(st, false, false, mr, m, w, -1.0, Vp, n, W2.p, w, 1.0, Zs, ldz));
+    }
+    EM_CK(cudaStreamSynchronize(st));  // host argument arrays, V/G/T reuse by the next chunk
   }
-  EM_CK(cudaStreamSynchronize(st));  // host argument arrays
 }
 
 }  // namespace em

@@ -971,7 +971,7 @@ static void q2_apply_waves(cudaStream_t st, int64_t n, int64_t ncols, int64_t ng
 void syev_two_stage(cudaStream_t st, int64_t n, double* A, int64_t lda, double* w, double* Z,
                     int64_t ldz, int64_t c0, int64_t nc, double* Yt, int64_t ldy, int64_t ky) {
   if (nc < 0) nc = n - c0;
-  double* Zc = Z + c0 * ldz;  // the back-transformed columns
+  double* Zc = Z ? Z + c0 * ldz : nullptr;  // the back-transformed columns
   const int b = B2;
   const int64_t ldab = 2 * b + 1;
   DBuf tau1(n, st), AB((size_t)ldab * n, st);
@@ -981,6 +981,10 @@ void syev_two_stage(cudaStream_t st, int64_t n, double* A, int64_t lda, double* 
     Stage s1(st, ST_SY2SB);
     sy2sb(st, n, A, lda, tau1.p, AB.p, ldab);
   }
+  if (Yt && n > b) {  // implicit mode: Q^T = Q2^T Q1^T, so Q1^T first; A is free after it
+    Stage sq1(st, ST_Q1);
+    ormqr_lower_off(st, n, n - b, b, ky, A, lda, tau1.p, Yt, ldy, true);
+  }
   // stage 2
   const int64_t nsw = n - 1;
   std::vector<int64_t> toff(nsw + 1, 0);
@@ -989,7 +993,16 @@ void syev_two_stage(cudaStream_t st, int64_t n, double* A, int64_t lda, double* 
   DArr<int64_t> dtoff(nsw + 1, st);
   EM_CK(cudaMemcpyAsync(dtoff.p, toff.data(), (nsw + 1) * sizeof(int64_t), cudaMemcpyHostToDevice,
                         st));
-  DBuf V2((size_t)imax64(ntask, 1) * b, st), TAU2(imax64(ntask, 1), st);
+  // the stage-2 reflectors: in implicit mode in A's storage (no longer needed once Q1^T is
+  // applied), so the N = 120,000 eigensolve holds A plus the Q2 T factors only
+  const size_t v2n = (size_t)imax64(ntask, 1) * b;
+  DBuf V2own;
+  double* V2 = A;
+  if (!(Yt && lda >= n && v2n <= (size_t)lda * n)) {
+    V2own.alloc(v2n, st);
+    V2 = V2own.p;
+  }
+  DBuf TAU2(imax64(ntask, 1), st);
   DArr<int> prog(imax64(nsw, 1), st);
   EM_CK(cudaMemsetAsync(prog.p, 0, imax64(nsw, 1) * sizeof(int), st));
   DBuf d(n, st), e(imax64(n - 1, 1), st);
@@ -1001,7 +1014,7 @@ void syev_two_stage(cudaStream_t st, int64_t n, double* A, int64_t lda, double* 
     int per_sm = 1;
     EM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sb2st_kernel, 256, smem));
     const unsigned grid = (unsigned)imax64(1, imin64(nsw, (int64_t)num_sms() * imax64(per_sm, 1)));
-    SbArgs sa{n, AB.p, ldab, V2.p, TAU2.p, dtoff.p, prog.p, nsw};
+    SbArgs sa{n, AB.p, ldab, V2, TAU2.p, dtoff.p, prog.p, nsw};
     void* args[] = {&sa};
     Stage s2(st, ST_SB2ST);
     if (nsw > 0) coop_launch((const void*)sb2st_kernel, grid, 256, args, smem, st);
@@ -1009,7 +1022,7 @@ void syev_two_stage(cudaStream_t st, int64_t n, double* A, int64_t lda, double* 
     EM_LAUNCHED();
   }
   AB.release();
-  {
+  if (!Yt) {
     Stage s(st, ST_STEDC);
     stedc(st, n, d.p, e.p, Z, ldz);
   }
@@ -1020,10 +1033,6 @@ void syev_two_stage(cudaStream_t st, int64_t n, double* A, int64_t lda, double* 
     // w = k + 2 (G-1-g) in increasing w: blocks of one wavefront touch disjoint rows and
     // every block they depend on sits on an earlier wavefront. Each wavefront is two
     // grouped DMMA GEMMs over all columns of Z (W = V^T Z, Z -= (V T) W).
-    if (Yt && n > b) {  // implicit mode: Q^T = Q2^T Q1^T, so Q1^T first
-      Stage sq1(st, ST_Q1);
-      ormqr_lower_off(st, n, n - b, b, ky, A, lda, tau1.p, Yt, ldy, true);
-    }
     std::vector<Q2Block> blocks;
     const int64_t ngroups = (nsw + b - 1) / b;
     for (int64_t g = ngroups - 1; g >= 0; --g) {
@@ -1040,19 +1049,19 @@ void syev_two_stage(cudaStream_t st, int64_t n, double* A, int64_t lda, double* 
       const size_t smt = ((size_t)VR * B2 + 2 * (size_t)B2 * (B2 + 1)) * sizeof(double);
       EM_CK(cudaFuncSetAttribute(q2_tfactor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smt));
-      q2_tfactor_kernel<<<(unsigned)nblk, 256, smt, st>>>(n, dblk.p, V2.p, TAU2.p, dtoff.p, T2.p);
+      q2_tfactor_kernel<<<(unsigned)nblk, 256, smt, st>>>(n, dblk.p, V2, TAU2.p, dtoff.p, T2.p);
       EM_LAUNCHED();
       if (Yt) {
         // implicit mode: Yt <- Q2^T (Q1^T Yt) (Q1^T applied above)
-        q2_apply_waves(st, n, ky, ngroups, blocks, dblk.p, V2.p, dtoff.p, T2.p, Yt, ldy, true);
+        q2_apply_waves(st, n, ky, ngroups, blocks, dblk.p, V2, dtoff.p, T2.p, Yt, ldy, true);
       } else if (g_q2_mode == 0) {
-        q2_apply_reg(st, n, nc, ngroups, V2.p, dtoff.p, T2.p, Zc, ldz);
+        q2_apply_reg(st, n, nc, ngroups, V2, dtoff.p, T2.p, Zc, ldz);
         EM_CK(cudaStreamSynchronize(st));  // dblk lifetime
       } else if (g_q2_mode == 2) {
-        q2_apply_strips(st, n, nc, ngroups, V2.p, dtoff.p, T2.p, Zc, ldz);
+        q2_apply_strips(st, n, nc, ngroups, V2, dtoff.p, T2.p, Zc, ldz);
         EM_CK(cudaStreamSynchronize(st));  // dblk lifetime
       } else {
-        q2_apply_waves(st, n, nc, ngroups, blocks, dblk.p, V2.p, dtoff.p, T2.p, Zc, ldz, false);
+        q2_apply_waves(st, n, nc, ngroups, blocks, dblk.p, V2, dtoff.p, T2.p, Zc, ldz, false);
       }
     }
     // Q1 (stage-1 reflectors, vectors start b rows below their column)
@@ -1060,6 +1069,10 @@ void syev_two_stage(cudaStream_t st, int64_t n, double* A, int64_t lda, double* 
       Stage sq1(st, ST_Q1);
       if (n > b) ormqr_lower_off(st, n, n - b, b, nc, A, lda, tau1.p, Zc, ldz);
     }
+  }
+  if (Yt) {  // Yt <- U^T Yt without forming U
+    Stage s(st, ST_STEDC);
+    stedc_apply(st, n, d.p, e.p, Yt, ldy, ky);
   }
   EM_CK(cudaMemcpyAsync(w, d.p, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
 }

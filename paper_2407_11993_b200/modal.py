@@ -231,3 +231,43 @@ def write_modal_csv(path, basis: ModalBasis, header_lines: tuple[str, ...] = ())
         for i in range(basis.n_modes):
             fh.write(f"{i},{float(basis.tau[i])!r},{float(basis.l_n[i])!r},"
                      f"{float(basis.r_n[i])!r}\n")
+
+
+def implicit_eig(l_i, r_i, y, *, r_band: int | None = None, l_workspace: bool = False):
+    """tau (descending) and V^T Y for the pencil L_i V = tau R_i V without forming V
+    (em_sygv_implicit / em_sygv_implicit_band; SURVEY.md §7 "implicit V"). Y is (n, k).
+    r_band: pass R_i as LAPACK lower band storage of that bandwidth (host (bw+1, n) array or
+    a dense R_i that is banded). l_workspace: L_i's device copy is reduced in place.
+
+    V's per-mode signs are the eigensolver's (the reference's sign fix needs V), so each row
+    of V^T Y is determined up to sign; products of two rows, (V^T Y)^T (V^T Y) = Y^T R^-1 Y
+    and (V^T Y)^T diag(tau) (V^T Y) = Y^T R^-1 L R^-1 Y are not."""
+    lm, rm = _host_square(l_i), _host_square(r_i)
+    n = lm.shape[0]
+    y = np.asarray(y, dtype=float).reshape(n, -1)
+    k = y.shape[1]
+    ld = nat.device_symmetric(lm)
+    dy = nat.device_colmajor(y)
+    tau = nat.empty(max(n, 1))
+    piv, which = ctypes.c_int64(-1), ctypes.c_int(-1)
+    flags = nat.EM_SYGV_L_WORKSPACE if l_workspace else 0
+    lib = nat.load_library()
+    if r_band is not None:
+        bw = int(r_band)
+        rb = np.zeros((n, bw + 1))  # column j of band storage = R[j:j+bw+1, j]
+        for q in range(bw + 1):
+            rb[:n - q, q] = np.diagonal(rm, -q)
+        drb = nat.device_colmajor(rb.T)  # column-major (bw+1) x n
+        rc = lib.em_sygv_implicit_band(nat.context(), n, nat.ptr(ld), n, nat.ptr(drb), bw + 1,
+                                       bw, nat.ptr(tau), nat.ptr(dy), n, k, None, None, flags,
+                                       ctypes.byref(piv), ctypes.byref(which))
+    else:
+        dr = nat.device_symmetric(rm)
+        rc = lib.em_sygv_implicit(nat.context(), n, nat.ptr(ld), n, nat.ptr(dr), n,
+                                  nat.ptr(tau), nat.ptr(dy), n, k, None, None, flags,
+                                  ctypes.byref(piv), ctypes.byref(which))
+    if rc == nat.EM_ERR_NOT_PD:
+        what = "modal resistance matrix" if which.value == 0 else "modal inductance matrix"
+        raise NotPositiveDefinite(int(piv.value), what)
+    nat.check(rc, "em_sygv_implicit")
+    return tau.cpu().numpy()[:n], nat.host_colmajor(dy, n, k)
