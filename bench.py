@@ -49,6 +49,11 @@ CONFIGS = {
     # workspace, no V^T R) on one B200
     "C5": dict(grid=(150, 100, 4), thetas=(0.5,), dt=2e-7, steps=100000, n_obs=64, n_ports=0,
                n_sources=64, drive="batched", vtr=False, sweep=True),
+    # configs[3]: the north-star Target plate, N = 120,000 minus a seeded 2 mm notch
+    # (L = 115 GB). On one B200 only as the implicit-V solve (L reduced in place, R in band
+    # storage) and the in-place Cholesky comparator: run_c4
+    "C4": dict(grid=(200, 150, 4), thetas=(0.5,), dt=1e-7, steps=100000, n_obs=128, n_ports=1,
+               n_sources=0, drive="trapezoid", notch=True),
 }
 
 
@@ -438,19 +443,23 @@ class _LazyEye:
 # algorithmic FP64 flop counts of the eigensolve stages at order n; the
 # two-stage pieces: sy2sb 4/3 n^3 (two-sided update), Q2 and Q1 back-transforms 2 n^3 each
 # (applying ~n^2/2 reflector entries to n columns, 4 flop per entry and column)
-def stage_flops(name, n):
+def stage_flops(name, n, k=None):
+    """k: implicit V (the back-transforms act on k skinny columns, not n)."""
+    m = n if k is None else k
     return {"potrf_R": n ** 3 / 3, "potrf_L": n ** 3 / 3, "sygst": 2.0 * n ** 3,
-            "ormtr": 2.0 * n ** 3, "trsm_back": 1.0 * n ** 3, "sy2sb": 4.0 / 3.0 * n ** 3,
-            "q2_apply": 2.0 * n ** 3, "q1_apply": 2.0 * n ** 3}.get(name)
+            "ormtr": 2.0 * n * n * m, "trsm_back": 1.0 * n * n * m, "sy2sb": 4.0 / 3.0 * n ** 3,
+            "q2_apply": 2.0 * n * n * m, "q1_apply": 2.0 * n * n * m}.get(name)
 
 
-def roofline(stages: dict, n: int, peaks: dict) -> dict:
+def roofline(stages: dict, n: int, peaks: dict, k=None) -> dict:
     """The dominant eigensolve stage (by time, per step) against the FP64 tensor peak, or
     the one-stage sytrd against HBM."""
     fp64 = peaks.get("fp64_tflops", 37.1)
     hbm = peaks.get("hbm_gbs", 6550.4)
     cands = {k: v for k, v in stages.items()
              if stage_flops(k, n) is not None or k == "sytrd"}
+    if k is not None:  # implicit V on a banded R: sygst is 6 n^2 b, not a dense product
+        cands.pop("sygst", None)
     if "q2_apply" in stages:  # two-stage: sytrd / ormtr are the sums of their pieces
         cands.pop("sytrd", None)
         cands.pop("ormtr", None)
@@ -463,10 +472,10 @@ def roofline(stages: dict, n: int, peaks: dict) -> dict:
         ach = byts / (ms * 1e-3) / 1e9
         return dict(stage=name, bound="hbm", achieved=ach, peak=hbm, unit="GB/s",
                     frac=ach / hbm, traffic=None, ms_per_step=ms, launches_per_step=cnt)
-    ach = stage_flops(name, n) / (ms * 1e-3) / 1e12
+    ach = stage_flops(name, n, k) / (ms * 1e-3) / 1e12
     return dict(stage=name, bound="tensor", achieved=ach, peak=fp64, unit="TFLOP/s",
                 frac=ach / fp64, traffic=None, ms_per_step=ms, launches_per_step=cnt,
-                algorithmic_flop=stage_flops(name, n))
+                algorithmic_flop=stage_flops(name, n, k))
 
 
 def symv_roofline(m, n, peaks, reps=20):
@@ -754,6 +763,172 @@ def run_ours(args, cfg, rank, world, local_rank):
         dist.destroy_process_group()
 
 
+def run_c4(args, cfg, rank, world, local_rank):
+    """configs[3] (N = 120,000 minus the notch, L = 115 GB) on ONE B200: the modal path as
+    the implicit-V eigensolve (em_sygv_implicit_band: L reduced in place, R in band storage,
+    V^T applied to [R_D | L_D | C^T] only) + 100,000 TD2 steps, and the Cholesky
+    comparator in place (em_td1_plan_create_band). L is regenerated on the device before
+    every step (the step consumes it) outside the timed region; each step is timed with
+    CUDA events around the solve + scan."""
+    import ctypes
+    import torch
+    from paper_2407_11993_b200 import _native as nat
+    from paper_2407_11993_b200 import synth
+    if world > 1:
+        if rank == 0:
+            print(json.dumps({"metric": "end-to-end transient wall time (eigensolve + steps); "
+                              "mode-steps/sec", "config": {"workload": "C4"},
+                              "unavailable": "C4 on >1 GPU needs the distributed eigensolve "
+                                             "(not built); C4 runs on one GPU"}), flush=True)
+        return
+    torch.cuda.set_device(local_rank)
+    lib, ctx = nat.load_library(), nat.context()
+    nx, ny, nz = cfg["grid"]
+    m = synth.device_plate_model(nx, ny, nz, n_ports=cfg["n_ports"], n_sources=cfg["n_sources"],
+                                 n_obs=cfg["n_obs"], notch=True, r_dense=False,
+                                 ldl=(synth.Plate(nx, ny, nz, notch=True).n + 31) // 32 * 32)
+    n = m["plate"].n
+    ldl = m["ldl"]
+    bw, rb = m["r_bw"], m["r_band"]
+    T, n_obs = cfg["steps"], cfg["n_obs"]
+    i_d, i0 = synth.drive_table(cfg["drive"], T, cfg["dt"], cfg["n_ports"], cfg["n_sources"],
+                                plate=m["plate"])
+    table = np.ascontiguousarray(np.concatenate([i_d, i0], axis=1))
+    table_dev = nat.device_vector(table.reshape(-1))
+    ct = nat.device_colmajor(m["c"]).reshape(n, n_obs).t().contiguous()   # C^T columns
+    y0 = torch.cat([m["r_d"], m["l_d"], ct], dim=0).contiguous()           # (2 + n_obs, n)
+    k = y0.shape[0]
+    yp = torch.empty_like(y0)
+    tau = nat.empty(n)
+    one = torch.ones(n, dtype=torch.float64, device="cuda")
+    q = nat.zeros(n)
+    Y = nat.empty(T, n_obs)
+    log(f"C4: n = {n}, band {bw}, k = {k}, L {8 * n * n / 1e9:.1f} GB")
+
+    def step(timed_events=None):
+        m["regen_l"]()
+        yp.copy_(y0)
+        torch.cuda.synchronize()
+        if timed_events:
+            timed_events[0].record()
+        piv, which = ctypes.c_int64(-1), ctypes.c_int(-1)
+        nat.check(lib.em_sygv_implicit_band(ctx, n, nat.ptr(m["l_i"]), ldl, nat.ptr(rb), bw + 1,
+                                            bw,
+                                            nat.ptr(tau), nat.ptr(yp), n, k, None, None,
+                                            nat.EM_SYGV_L_WORKSPACE, ctypes.byref(piv),
+                                            ctypes.byref(which)), "em_sygv_implicit_band")
+        cv = yp[2:].t().contiguous()
+        plan = ctypes.c_void_p()
+        nat.check(lib.em_td2_plan_create(ctx, n, 1, 0, nat.ptr(tau), nat.ptr(one),
+                                         nat.ptr(yp[0:1]), nat.ptr(yp[1:2]), nat.ptr(yp[0:1]),
+                                         cfg["dt"], cfg["thetas"][0], ctypes.byref(plan)),
+                  "em_td2_plan_create")
+        nat.check(lib.em_td2_set_observables(plan, n_obs, nat.ptr(cv), n_obs, None, 0),
+                  "em_td2_set_observables")
+        q.zero_()
+        nat.check(lib.em_td2_run(plan, T, nat.ptr(table_dev), nat.ptr(q), nat.ptr(Y), 1, None),
+                  "em_td2_run")
+        lib.em_td2_plan_destroy(plan)
+        if timed_events:
+            timed_events[1].record()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    nat.profile(True)
+    l0 = nat.launches()
+    total = 0.0
+    with ClockSampler(local_rank) as clk:
+        for _ in range(args.steps):
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            step(ev)
+            total += ev[0].elapsed_time(ev[1]) / 1e3
+    launches = nat.launches() - l0
+    stages = nat.stage_times()
+    nat.profile(False)
+    units = n * T
+    st_avg = {kk: (v[0] / args.steps, v[1] / args.steps) for kk, v in stages.items()}
+    peaks = load_peaks()
+    rl = roofline(st_avg, n, peaks, k=k) or {}
+    eig_ms = sum(st_avg[kk][0] for kk in ("potrf_R", "sygst", "sytrd", "stedc", "ormtr",
+                                          "finalize") if kk in st_avg)
+    fp64 = peaks.get("fp64_tflops", 37.1)
+    red = 4.0 / 3.0 * n ** 3  # the dense -> band reduction, the only n^3 term left
+    rl["eigensolve_roofline"] = {
+        "ms_per_step": eig_ms, "bound": "tensor", "unit": "TFLOP/s", "peak": fp64,
+        "achieved_reduction_count": red / (eig_ms * 1e-3) / 1e12,
+        "frac_reduction_count": red / (eig_ms * 1e-3) / 1e12 / fp64,
+        "note": "implicit V: (4/3) N^3 of the band reduction is the whole cubic count; the "
+                "back-transforms act on k = 2 + n_obs columns (O(N^2 k))"}
+    y_host = Y[-1].cpu().numpy()
+    del yp, q
+    # the Cholesky comparator in L's storage (bounded number of steps, extrapolated)
+    td1 = None
+    if not args.no_td1:
+        m["regen_l"]()
+        steps1 = min(args.td1_steps, T)
+        plan = ctypes.c_void_p()
+        piv = ctypes.c_int64(-1)
+        e0, e1, e2, e3 = (torch.cuda.Event(enable_timing=True) for _ in range(4))
+        e0.record()
+        nat.check(lib.em_td1_plan_create_band(ctx, n, 1, 0, nat.ptr(m["l_i"]), ldl, nat.ptr(rb),
+                                              bw + 1, bw, nat.ptr(m["r_d"]), nat.ptr(m["l_d"]),
+                                              None, cfg["dt"], cfg["thetas"][0],
+                                              nat.EM_TD1_L_WORKSPACE, ctypes.byref(plan),
+                                              ctypes.byref(piv)), "em_td1_plan_create_band")
+        e1.record()
+        c_dev = nat.device_colmajor(m["c"])
+        nat.check(lib.em_td1_set_observables(plan, n_obs, nat.ptr(c_dev), n_obs, None, 0))
+        state = nat.zeros(n)
+        y1 = nat.empty(steps1, n_obs)
+        nat.profile(True)
+        e2.record()
+        nat.check(lib.em_td1_run(plan, steps1, nat.ptr(table_dev), nat.ptr(state), nat.ptr(y1), 1,
+                                 None), "em_td1_run")
+        e3.record()
+        torch.cuda.synchronize()
+        st1 = nat.stage_times()
+        nat.profile(False)
+        lib.em_td1_plan_destroy(plan)
+        # the same theta-method in the Cholesky basis: its first steps must reproduce the
+        # modal run's observables (a full-size parity property of the C4 path)
+        ya, yb = y1.cpu().numpy(), Y[:steps1].cpu().numpy()
+        td1_vs_td2 = float(np.linalg.norm(ya - yb) / np.linalg.norm(yb))
+        setup = e0.elapsed_time(e1) / 1e3
+        per_step = e2.elapsed_time(e3) / 1e3 / steps1
+        fb = 8.0 * n * (n + 1) / 2
+        fwd, bwd = st1.get("td1_fwd", (0.0, 1)), st1.get("td1_bwd", (0.0, 1))
+        hbm = peaks.get("hbm_gbs", 6550.4)
+        td1 = {"method": "td1 (GPU Cholesky theta-method, factor in L's storage, R as CSR)",
+               "setup_s": setup, "per_step_ms": per_step * 1e3, "steps_timed": steps1,
+               "extrapolated_total_s": setup + per_step * T,
+               "trsv_fwd_GBps": fb / (fwd[0] / fwd[1] * 1e-3) / 1e9 if fwd[1] else None,
+               "trsv_bwd_GBps": fb / (bwd[0] / bwd[1] * 1e-3) / 1e9 if bwd[1] else None,
+               "hbm_peak_GBps": hbm,
+               "td1_vs_td2_observables_rel_l2": td1_vs_td2,
+               "modal_vs_cholesky_end_to_end": (setup + per_step * T) / (total / args.steps)}
+    line = {
+        "metric": "end-to-end transient wall time (eigensolve + steps); mode-steps/sec",
+        "value": units * args.steps / total, "unit": "mode-steps/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded notched plate generator, SURVEY.md §8(d))",
+        "config": {"workload": f"C4: N={n} notched plate {cfg['grid']}, implicit-V eigensolve "
+                               f"+ {T} TD2 steps x theta {list(cfg['thetas'])}, {n_obs} "
+                               "observables", "N": n, "T": T, "n_obs": n_obs,
+                   "mode_steps_per_step": units, "eigensolve": "implicit V (no V formed)",
+                   "l2": f"inputs larger than L2 (L {8 * n * n / 1e9:.1f} GB)",
+                   "parallelism": "single GPU"},
+        "e2e": None,
+        "e2e_note": "not measured at C4: the host copy of L alone is 115 GB",
+        "gpu_launches": int(launches), "clocks": clk.summary(), "roofline": rl,
+        "stage_ms_per_step": {kk: round(v[0], 3) for kk, v in st_avg.items()},
+        "cpu_baseline": None, "td1_comparator": td1,
+        "last_observables_l2": float(np.linalg.norm(y_host)),
+    }
+    print(json.dumps(line), flush=True)
+
+
 def td1_comparator(m, cfg, steps, n_rhs=1):
     """GPU Cholesky theta-method on the same inputs (bounded number of steps)."""
     import ctypes
@@ -892,6 +1067,9 @@ def main():
     ap.add_argument("--no-td1", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-implicit", action="store_true")
+    ap.add_argument("--grid", default=None,
+                    help="nx,ny,nz override (debugging a configuration's code path at a "
+                         "smaller plate; the workload string names the grid)")
     ap.add_argument("--implicit-steps", type=int, default=1)
     ap.add_argument("--two-stage", type=int, default=None,
                     help="smallest n for the two-stage tridiagonalisation (default: library)")
@@ -901,9 +1079,14 @@ def main():
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.grid:
+        cfg["grid"] = tuple(int(v) for v in args.grid.split(","))
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
+        return
+    if args.config == "C4":
+        run_c4(args, cfg, rank, world, local_rank)
         return
     run_ours(args, cfg, rank, world, local_rank)
 

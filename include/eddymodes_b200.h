@@ -180,7 +180,8 @@ int em_sygv_range(em_ctx* ctx, int64_t n, const double* L, int64_t ldl, double* 
  * (O(n k) memory), the stage-2 reflectors reuse the reduced matrix's storage.
  * Flags: EM_SYGV_R_WORKSPACE as em_sygv_ex; EM_SYGV_L_WORKSPACE: L (ld a multiple of 32)
  * is overwritten by the reduction instead of copied — one n x n buffer less, so the peak is
- * L plus n^2 / 2 (the Q2 block factors) and n = 120,000 fits one B200. An in-place solve
+ * L plus O(n (k + b)) (stage-2 reflectors in L's storage, their block factors formed per
+ * wavefront) and n = 120,000 fits one B200. An in-place solve
  * cannot run the reference's Cholesky certificate of L afterwards: when the solved spectrum
  * and R's Gershgorin bounds do not already prove it redundant (see em_sygv), the call
  * fails with EM_ERR_ARG and asks to solve without the flag. */
@@ -266,6 +267,16 @@ int em_td1_plan_create(em_ctx* ctx, int64_t n, int n_p, int n_s, const double* L
                        const double* R, int64_t ldr, const double* r_d, const double* l_d,
                        const double* m0, double dt, double theta, em_td1_plan** plan,
                        int64_t* pivot);
+/* em_td1_plan_create with R in LAPACK lower band storage (Rb[(i - j) + j ldrb] = R(i, j),
+ * 0 <= i - j <= bw): R enters the plan only as a CSR. EM_TD1_L_WORKSPACE (ldl == n): the
+ * stepping matrix is formed and factored in L's own storage (L is destroyed; the plan
+ * references it until destroyed), so the plan holds one n x n array — n = 120,000 fits
+ * one B200. */
+#define EM_TD1_L_WORKSPACE 1
+int em_td1_plan_create_band(em_ctx* ctx, int64_t n, int n_p, int n_s, double* L, int64_t ldl,
+                            const double* Rb, int64_t ldrb, int64_t bw, const double* r_d,
+                            const double* l_d, const double* m0, double dt, double theta,
+                            int flags, em_td1_plan** plan, int64_t* pivot);
 void em_td1_plan_destroy(em_td1_plan* plan);
 int em_td1_set_observables(em_td1_plan* plan, int n_obs, const double* C, int64_t ldc,
                            const double* D, int64_t ldd);

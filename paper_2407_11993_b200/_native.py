@@ -72,6 +72,8 @@ SIGNATURES = {
     "em_td2_step_forcing": (_I, [_P, _P, _P]),
     "em_td1_plan_create": (_I, [_P, _I64, _I, _I, _P, _I64, _P, _I64, _P, _P, _P, _D, _D,
                                 ctypes.POINTER(_P), ctypes.POINTER(_I64)]),
+    "em_td1_plan_create_band": (_I, [_P, _I64, _I, _I, _P, _I64, _P, _I64, _I64, _P, _P, _P, _D,
+                                     _D, _I, ctypes.POINTER(_P), ctypes.POINTER(_I64)]),
     "em_td1_plan_destroy": (None, [_P]),
     "em_td1_set_observables": (_I, [_P, _I, _P, _I64, _P, _I64]),
     "em_td1_run": (_I, [_P, _I64, _P, _P, _P, _I64, _P]),
@@ -172,6 +174,7 @@ def stage_times() -> dict:
 
 
 EM_SYGV_R_WORKSPACE, EM_SYGV_L_WORKSPACE = 1, 2
+EM_TD1_L_WORKSPACE = 1
 EM_CFG_TWO_STAGE_MIN = 1
 
 

@@ -553,6 +553,35 @@ int em_td1_plan_create(em_ctx* ctx, int64_t n, int n_p, int n_s, const double* L
   });
 }
 
+int em_td1_plan_create_band(em_ctx* ctx, int64_t n, int n_p, int n_s, double* L, int64_t ldl,
+                            const double* Rb, int64_t ldrb, int64_t bw, const double* r_d,
+                            const double* l_d, const double* m0, double dt, double theta,
+                            int flags, em_td1_plan** plan, int64_t* pivot) {
+  return guarded(ctx, [&] {
+    if (!plan || n < 0 || n_p < 0 || n_s < 0) throw em::ArgError{"bad td1 plan arguments"};
+    if (!Rb || bw < 0 || ldrb < bw + 1) throw em::ArgError{"em_td1_plan_create_band: bad band"};
+    if (flags & ~EM_TD1_L_WORKSPACE) throw em::ArgError{"unknown em_td1_plan_create_band flags"};
+    auto* P = em::td1_new(ctx, n, n_p, n_s, dt, theta);
+    int64_t piv = -1;
+    try {
+      piv = em::td1_plan_init(P, L, ldl, nullptr, 0, r_d, l_d, m0, Rb, ldrb, bw,
+                              (flags & EM_TD1_L_WORKSPACE) != 0);
+      EM_CK(cudaStreamSynchronize(ctx->stream));
+    } catch (...) {
+      em::td1_delete(P);
+      throw;
+    }
+    if (pivot) *pivot = piv;
+    if (piv >= 0) {
+      em::td1_delete(P);
+      *plan = nullptr;
+      return EM_ERR_NOT_PD;
+    }
+    *plan = P;
+    return EM_OK;
+  });
+}
+
 void em_td1_plan_destroy(em_td1_plan* plan) { em::td1_delete(plan); }
 
 int em_td1_set_observables(em_td1_plan* plan, int n_obs, const double* C, int64_t ldc,

@@ -37,6 +37,9 @@ bool csr_from_dense(cudaStream_t st, int64_t n, const double* A, int64_t lda, do
 void csr_mm(cudaStream_t st, const Csr& a, int64_t m, const double* B, int64_t ldb, double* C,
             int64_t ldc);
 void csr_to_dense(cudaStream_t st, const Csr& a, double* A, int64_t lda);
+// CSR of a symmetric matrix given in lower band storage (Rb[(i - j) + j ldrb], i - j <= bw)
+void csr_from_band(cudaStream_t st, int64_t n, const double* Rb, int64_t ldrb, int64_t bw,
+                   Csr& out);
 // out[j] = V[:, j]^T A V[:, j], j < m (no product buffer)
 void csr_quadform(cudaStream_t st, const Csr& a, int64_t m, const double* V, int64_t ldv,
                   double* out);
@@ -168,7 +171,9 @@ void td2_run_sweep(em_td2_plan* P, int64_t T, const double* drive, double* Q, do
                    int64_t stride);
 
 int64_t td1_plan_init(em_td1_plan* P, const double* L, int64_t ldl, const double* R, int64_t ldr,
-                      const double* r_d, const double* l_d, const double* m0);
+                      const double* r_d, const double* l_d, const double* m0,
+                      const double* Rb = nullptr, int64_t ldrb = 0, int64_t bw = 0,
+                      bool in_place = false);
 void td1_set_observables(em_td1_plan* P, int n_obs, const double* C, int64_t ldc,
                          const double* D, int64_t ldd);
 void td1_run(em_td1_plan* P, int64_t T, const double* drive, double* I, double* Y,

@@ -82,6 +82,49 @@ __global__ void csr_scatter_kernel(int64_t n, const int64_t* __restrict__ rowptr
 
 // Device CSR copy of a symmetric A (its lower triangle) when it has at most max_fill * n^2
 // nonzeros; returns false (and builds nothing) when A is too dense.
+// band storage -> CSR, one thread per row, columns ascending (pass 0 counts, 1 fills)
+__global__ void csr_band_kernel(int64_t n, const double* __restrict__ Rb, int64_t ldrb,
+                                int64_t bw, int pass, int64_t* __restrict__ cnt,
+                                const int64_t* __restrict__ rowptr, int* __restrict__ col,
+                                double* __restrict__ val) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int64_t c = 0, o = pass ? rowptr[i] : 0;
+  const int64_t j0 = i - bw < 0 ? 0 : i - bw, j1 = i + bw >= n ? n - 1 : i + bw;
+  for (int64_t j = j0; j <= j1; ++j) {
+    const double v = j <= i ? Rb[(i - j) + j * ldrb] : Rb[(j - i) + i * ldrb];
+    if (v == 0.0) continue;
+    if (pass) {
+      col[o + c] = (int)j;
+      val[o + c] = v;
+    }
+    ++c;
+  }
+  if (!pass) cnt[i] = c;
+}
+
+void csr_from_band(cudaStream_t st, int64_t n, const double* Rb, int64_t ldrb, int64_t bw,
+                   Csr& out) {
+  DArr<int64_t> cnt(n + 1, st);
+  const unsigned g = (unsigned)((n + 255) / 256);
+  csr_band_kernel<<<g, 256, 0, st>>>(n, Rb, ldrb, bw, 0, cnt.p, nullptr, nullptr, nullptr);
+  EM_LAUNCHED();
+  std::vector<int64_t> h(n + 1, 0);
+  EM_CK(cudaMemcpyAsync(h.data() + 1, cnt.p, n * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  EM_CK(cudaStreamSynchronize(st));
+  for (int64_t i = 0; i < n; ++i) h[i + 1] += h[i];
+  EM_CK(cudaMemcpyAsync(cnt.p, h.data(), (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  out.n = n;
+  out.nnz = h[n];
+  out.rowptr = std::move(cnt);
+  out.colidx.alloc(imax64(out.nnz, 1), st);
+  out.val.alloc(imax64(out.nnz, 1), st);
+  csr_band_kernel<<<g, 256, 0, st>>>(n, Rb, ldrb, bw, 1, nullptr, out.rowptr.p, out.colidx.p,
+                                     out.val.p);
+  EM_LAUNCHED();
+  EM_CK(cudaStreamSynchronize(st));  // host vector h lifetime
+}
+
 bool csr_from_dense(cudaStream_t st, int64_t n, const double* A, int64_t lda, double max_fill,
                     Csr& out) {
   if (n <= 0) return false;

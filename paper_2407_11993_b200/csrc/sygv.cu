@@ -45,8 +45,8 @@ static bool two_stage_fits(int64_t n, int64_t ldz, bool implicit) {
         reserved > used)
       free_b += (size_t)(reserved - used);
   }
-  // implicit mode: the Q2 T factors (1/2); the reflectors live in A, nothing else is n^2
-  const double need = (implicit ? 0.5 : two_stage_extra(ldz, n)) * (double)n * (double)n *
+  // implicit mode: the reflectors live in A, T factors per wavefront: nothing else is n^2
+  const double need = (implicit ? 0.0 : two_stage_extra(ldz, n)) * (double)n * (double)n *
                           sizeof(double) + (1ull << 30);
   return (double)free_b >= need;
 }

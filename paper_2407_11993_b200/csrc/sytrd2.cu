@@ -83,8 +83,11 @@ struct QRArgs {
   int R;          // rows per CTA
 };
 
+// GM: the panel is worked on in place in global memory (L2-resident) instead of shared
+// memory — for panels taller than the CTAs' shared memory holds (m > ~59,000 rows)
+template <bool GM>
 __global__ void __launch_bounds__(256) qr_panel_kernel(QRArgs a) {
-  extern __shared__ double S[];  // column-major [nbw][R]
+  extern __shared__ double Ssm[];  // column-major [nbw][R]
   __shared__ double red[8];
   __shared__ double bc[4];
   __shared__ double wsh[B2];
@@ -95,13 +98,17 @@ __global__ void __launch_bounds__(256) qr_panel_kernel(QRArgs a) {
   double* normpart = a.part;
   double* dotpart = a.part + G;
   double* alpha_slot = a.part + G + (size_t)G * B2;
-  for (int idx = tid; idx < nr * a.nbw; idx += blockDim.x) {
-    const int lr = idx % nr, c = idx / nr;
-    S[c * a.R + lr] = a.P[(r0 + lr) + c * a.ldp];
+  double* S = GM ? a.P + r0 : Ssm;
+  const int64_t ls = GM ? a.ldp : a.R;
+  if (!GM) {
+    for (int idx = tid; idx < nr * a.nbw; idx += blockDim.x) {
+      const int lr = idx % nr, c = idx / nr;
+      S[c * ls + lr] = a.P[(r0 + lr) + c * a.ldp];
+    }
   }
   __syncthreads();
   for (int j = 0; j < a.p; ++j) {
-    double* Sj = S + j * a.R;
+    double* Sj = S + j * ls;
     // (a) partial sum of squares below the diagonal; the owner of row j publishes alpha
     double ss = 0.0;
     for (int lr = tid; lr < nr; lr += blockDim.x) {
@@ -143,7 +150,7 @@ __global__ void __launch_bounds__(256) qr_panel_kernel(QRArgs a) {
     __syncthreads();
     // (c) partial w_c = v^T P[:, c] for c > j (v_j = 1)
     for (int c = j + 1 + warp; c < a.nbw; c += 8) {
-      const double* Sc = S + c * a.R;
+      const double* Sc = S + c * ls;
       double s = 0.0;
       for (int lr = lane; lr < nr; lr += 32) {
         const int64_t r = r0 + lr;
@@ -167,15 +174,17 @@ __global__ void __launch_bounds__(256) qr_panel_kernel(QRArgs a) {
         const int64_t r = r0 + lr;
         if (r >= j) {
           const double v = (r == j) ? 1.0 : Sj[lr];
-          S[c * a.R + lr] = fma(-tau * wsh[c], v, S[c * a.R + lr]);
+          S[c * ls + lr] = fma(-tau * wsh[c], v, S[c * ls + lr]);
         }
       }
     }
     __syncthreads();
   }
-  for (int idx = tid; idx < nr * a.nbw; idx += blockDim.x) {
-    const int lr = idx % nr, c = idx / nr;
-    a.P[(r0 + lr) + c * a.ldp] = S[c * a.R + lr];
+  if (!GM) {
+    for (int idx = tid; idx < nr * a.nbw; idx += blockDim.x) {
+      const int lr = idx % nr, c = idx / nr;
+      a.P[(r0 + lr) + c * a.ldp] = S[c * ls + lr];
+    }
   }
 }
 
@@ -213,8 +222,8 @@ void sy2sb(cudaStream_t st, int64_t n, double* A, int64_t lda, double* tau1, dou
   DBuf part((size_t)sms + (size_t)sms * b + 8, st);
   DArr<GridBar> bar(1, st);
   EM_CK(cudaMemsetAsync(bar.p, 0, sizeof(GridBar), st));
-  EM_CK(cudaFuncSetAttribute(qr_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             200 * 1024));
+  EM_CK(cudaFuncSetAttribute(qr_panel_kernel<false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   EM_CK(cudaFuncSetAttribute(larft_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(128 * 129 * sizeof(double))));
   for (int64_t k0 = 0; k0 + b < n; k0 += b) {
@@ -230,7 +239,12 @@ void sy2sb(cudaStream_t st, int64_t n, double* A, int64_t lda, double* tau1, dou
       QRArgs qa{m, b, p, P, lda, tau1 + k0, part.p, bar.p, R};
       void* args[] = {&qa};
       Stage sq(st, ST_SY2SB_QR);
-      coop_launch((const void*)qr_panel_kernel, G, 256, args, (size_t)R * b * sizeof(double), st);
+      const bool gm = (size_t)R * b * sizeof(double) > 200 * 1024;
+      if (gm)
+        coop_launch((const void*)qr_panel_kernel<true>, G, 256, args, 0, st);
+      else
+        coop_launch((const void*)qr_panel_kernel<false>, G, 256, args,
+                    (size_t)R * b * sizeof(double), st);
     }
     // V (m x p) into VW[:, 0:p]; T from G = V^T V
     double* V = VW.p;
@@ -533,12 +547,14 @@ __global__ void __launch_bounds__(256) q2_buildv_kernel(int64_t n, const Q2Block
                                                         const int64_t* __restrict__ toff,
                                                         const double* __restrict__ T2,
                                                         double* __restrict__ Vout,
-                                                        double* __restrict__ VTout, int trans) {
+                                                        double* __restrict__ VTout, int trans,
+                                                        int t_by_slot) {
   extern __shared__ double Vs[];  // VR x B2 (64 KB), column-major like Vout
   const Q2Block blk = blocks[ids[blockIdx.x]];
   double* V = Vout + blockIdx.x * (size_t)VR * B2;
   double* VT = VTout + blockIdx.x * (size_t)VR * B2;
-  const double* T = T2 + ids[blockIdx.x] * (size_t)B2 * B2;
+  // T2 indexed by block id, or (t_by_slot) a per-launch buffer indexed by launch slot
+  const double* T = T2 + (t_by_slot ? (int64_t)blockIdx.x : ids[blockIdx.x]) * (size_t)B2 * B2;
   const int64_t R0 = blk.g * B2 + 1 + blk.k * B2;
   for (int idx = threadIdx.x; idx < VR * B2; idx += blockDim.x) {
     const int r = idx % VR, t = idx / VR;  // row r of column t
@@ -901,10 +917,12 @@ static void q2_apply_strips(cudaStream_t st, int64_t n, int64_t ncols, int64_t n
 // belongs to wavefront w = k + 2 (G-1-g); blocks of one wavefront touch disjoint rows and
 // every block a block depends on sits on an earlier wavefront (Q2^T: later, and the
 // wavefronts run in reverse). Per block W = V^T Z, Z -= (V T) W (V T^T for Q2^T).
+// T2 == nullptr: the blocks' T factors are formed per wavefront (from V2, TAU2) into a
+// QCH-block buffer instead of all at once (n^2 / 2 doubles less: the N = 120,000 solve).
 static void q2_apply_waves(cudaStream_t st, int64_t n, int64_t ncols, int64_t ngroups,
                            const std::vector<Q2Block>& blocks, const Q2Block* dblk,
                            const double* V2, const int64_t* dtoff, const double* T2, double* Z,
-                           int64_t ldz, bool trans) {
+                           int64_t ldz, bool trans, const double* TAU2 = nullptr) {
   const int b = B2;
   const int64_t nblk = (int64_t)blocks.size();
   if (nblk == 0 || ncols <= 0) return;
@@ -925,10 +943,13 @@ static void q2_apply_waves(cudaStream_t st, int64_t n, int64_t ncols, int64_t ng
         waves.emplace_back(wl.begin() + c, wl.begin() + std::min(wl.size(), c + QCH));
   }
   std::vector<int64_t> ids;
+  std::vector<Q2Block> wblk;  // the blocks in launch order (per-wavefront T factors)
   std::vector<GemmArgs> args;
   std::vector<int64_t> wstart;
+  const bool t_waves = T2 == nullptr;
   DBuf Vb((size_t)QCH * VR * B2, st), VTb((size_t)QCH * VR * B2, st),
-      W1((size_t)QCH * B2 * ncols, st);
+      W1((size_t)QCH * B2 * ncols, st), Tw;
+  if (t_waves) Tw.alloc((size_t)QCH * B2 * B2, st);
   for (auto& wl : waves) {
     wstart.push_back((int64_t)ids.size());
     for (size_t j = 0; j < wl.size(); ++j) {
@@ -939,6 +960,7 @@ static void q2_apply_waves(cudaStream_t st, int64_t n, int64_t ncols, int64_t ng
       double* VTj = VTb.p + j * (size_t)VR * B2;
       double* W1j = W1.p + j * (size_t)B2 * ncols;
       ids.push_back(wl[j]);
+      wblk.push_back(bk);
       args.push_back(GemmArgs{B2, ncols, nrow, Vj, VR, Z + R0, ldz, W1j, B2, 1.0, 0.0, 0});
       args.push_back(GemmArgs{nrow, ncols, B2, VTj, VR, W1j, B2, Z + R0, ldz, -1.0, 1.0, 0});
     }
@@ -956,10 +978,23 @@ static void q2_apply_waves(cudaStream_t st, int64_t n, int64_t ncols, int64_t ng
   EM_CK(cudaMemcpyAsync(dargs.p, ph.data(), ph.size() * sizeof(GemmArgs), cudaMemcpyHostToDevice,
                         st));
   const int tiles_n = (int)((ncols + 127) / 128);
+  DArr<Q2Block> dwblk(t_waves ? wblk.size() : 1, st);
+  const size_t smt = ((size_t)VR * B2 + 2 * (size_t)B2 * (B2 + 1)) * sizeof(double);
+  if (t_waves) {
+    EM_CK(cudaMemcpyAsync(dwblk.p, wblk.data(), wblk.size() * sizeof(Q2Block),
+                          cudaMemcpyHostToDevice, st));
+    EM_CK(cudaFuncSetAttribute(q2_tfactor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smt));
+  }
   for (size_t wi = 0; wi + 1 < wstart.size(); ++wi) {
     const int64_t o = wstart[wi], cnt = wstart[wi + 1] - wstart[wi];
+    if (t_waves) {
+      q2_tfactor_kernel<<<(unsigned)cnt, 256, smt, st>>>(n, dwblk.p + o, V2, TAU2, dtoff, Tw.p);
+      EM_LAUNCHED();
+    }
     q2_buildv_kernel<<<(unsigned)cnt, 256, (size_t)VR * B2 * sizeof(double), st>>>(
-        n, dblk, dids.p + o, V2, dtoff, T2, Vb.p, VTb.p, trans ? 1 : 0);
+        n, dblk, dids.p + o, V2, dtoff, t_waves ? Tw.p : T2, Vb.p, VTb.p, trans ? 1 : 0,
+        t_waves ? 1 : 0);
     EM_LAUNCHED();
     EM_CK(gemm_grouped(st, true, false, dargs.p + o, (int)cnt, tiles_n));
     EM_CK(gemm_grouped(st, false, false, dargs.p + np + o, (int)cnt, tiles_n));
@@ -1045,15 +1080,20 @@ void syev_two_stage(cudaStream_t st, int64_t n, double* A, int64_t lda, double* 
       DArr<Q2Block> dblk(nblk, st);
       EM_CK(cudaMemcpyAsync(dblk.p, blocks.data(), nblk * sizeof(Q2Block), cudaMemcpyHostToDevice,
                             st));
-      DBuf T2((size_t)nblk * b * b, st);
-      const size_t smt = ((size_t)VR * B2 + 2 * (size_t)B2 * (B2 + 1)) * sizeof(double);
-      EM_CK(cudaFuncSetAttribute(q2_tfactor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smt));
-      q2_tfactor_kernel<<<(unsigned)nblk, 256, smt, st>>>(n, dblk.p, V2, TAU2.p, dtoff.p, T2.p);
-      EM_LAUNCHED();
+      DBuf T2;
+      if (!Yt) {
+        T2.alloc((size_t)nblk * b * b, st);
+        const size_t smt = ((size_t)VR * B2 + 2 * (size_t)B2 * (B2 + 1)) * sizeof(double);
+        EM_CK(cudaFuncSetAttribute(q2_tfactor_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smt));
+        q2_tfactor_kernel<<<(unsigned)nblk, 256, smt, st>>>(n, dblk.p, V2, TAU2.p, dtoff.p,
+                                                            T2.p);
+        EM_LAUNCHED();
+      }
       if (Yt) {
-        // implicit mode: Yt <- Q2^T (Q1^T Yt) (Q1^T applied above)
-        q2_apply_waves(st, n, ky, ngroups, blocks, dblk.p, V2, dtoff.p, T2.p, Yt, ldy, true);
+        // implicit mode: Yt <- Q2^T (Q1^T Yt) (Q1^T applied above), T factors per wavefront
+        q2_apply_waves(st, n, ky, ngroups, blocks, dblk.p, V2, dtoff.p, nullptr, Yt, ldy, true,
+                       TAU2.p);
       } else if (g_q2_mode == 0) {
         q2_apply_reg(st, n, nc, ngroups, V2, dtoff.p, T2.p, Zc, ldz);
         EM_CK(cudaStreamSynchronize(st));  // dblk lifetime

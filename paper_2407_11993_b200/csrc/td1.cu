@@ -33,6 +33,8 @@ struct em_td1_plan {
   int n_p = 0, n_s = 0, n_u = 0;
   double dt = 0, theta = 0;
   em::DBuf C, R, Dinv, DinvT, Ef, Fb, Ef2, Fb2, E, work, b, y, x;
+  double* Cp = nullptr;  // the factor: C.p, or the caller's L storage (in-place plan)
+  int64_t ldc = 0;
   em::Csr Rs;          // R as CSR when it is sparse (the stencil): R I is an SpMV
   bool r_sparse = false;
   em::DArr<unsigned int>* counters = nullptr;
@@ -378,26 +380,64 @@ __global__ void td1_pre_kernel(int64_t n, int64_t npad, int n_p, int n_s, int n_
   b[i] = v;
 }
 
+// Z += dt theta R on the lower band of Z (R in lower band storage)
+__global__ void td1_z_band_kernel(int64_t n, const double* __restrict__ Rb, int64_t ldrb,
+                                  int64_t bw, double dt_theta, double* __restrict__ Z,
+                                  int64_t ldz) {
+  for (int64_t j = blockIdx.y; j < n; j += gridDim.y)
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q <= bw && j + q < n;
+         q += (int64_t)gridDim.x * blockDim.x)
+      Z[(j + q) + j * ldz] += dt_theta * Rb[q + j * ldrb];
+}
+
+// Rb (band storage) given: Z = L + dt theta R is formed in L's own storage when in_place
+// (ldl == n; the caller's L is the factor afterwards), R enters only as its CSR.
 int64_t td1_plan_init(em_td1_plan* P, const double* L, int64_t ldl, const double* R, int64_t ldr,
-                      const double* r_d, const double* l_d, const double* m0) {
+                      const double* r_d, const double* l_d, const double* m0, const double* Rb,
+                      int64_t ldrb, int64_t bw, bool in_place) {
   cudaStream_t st = P->ctx->stream;
   const int64_t n = P->n;
-  P->C.alloc((size_t)n * n, st);
-  P->R.alloc((size_t)n * n, st);
-  dim3 grid((unsigned)imin64((n + 255) / 256, 64), (unsigned)imin64(n, 65535));
-  td1_z_kernel<<<grid, 256, 0, st>>>(n, L, ldl, R, ldr, P->dt * P->theta, P->C.p, P->R.p);
-  EM_LAUNCHED();
-  const int64_t piv = potrf(st, n, P->C.p, n);
+  if (Rb) {
+    if (in_place) {
+      if (ldl < n) throw ArgError{"in-place TD1 plan needs ldl >= n"};
+      P->Cp = const_cast<double*>(L);
+      P->ldc = ldl;
+    } else {
+      P->C.alloc((size_t)n * n, st);
+      P->Cp = P->C.p;
+      P->ldc = n;
+      copy_matrix(st, false, n, n, L, ldl, P->Cp, n);
+    }
+    dim3 grid((unsigned)((bw + 256) / 256), (unsigned)imin64(n, 65535));
+    td1_z_band_kernel<<<grid, 256, 0, st>>>(n, Rb, ldrb, bw, P->dt * P->theta, P->Cp, P->ldc);
+    EM_LAUNCHED();
+    // Z symmetric in both triangles, as the dense plan forms it (the lower one defines L)
+    mirror_lower(st, n, P->Cp, P->ldc);
+    P->r_sparse = true;
+    csr_from_band(st, n, Rb, ldrb, bw, P->Rs);
+  } else {
+    P->C.alloc((size_t)n * n, st);
+    P->Cp = P->C.p;
+    P->ldc = n;
+    P->R.alloc((size_t)n * n, st);
+    dim3 grid((unsigned)imin64((n + 255) / 256, 64), (unsigned)imin64(n, 65535));
+    td1_z_kernel<<<grid, 256, 0, st>>>(n, L, ldl, R, ldr, P->dt * P->theta, P->Cp, P->R.p);
+    EM_LAUNCHED();
+  }
+  const int64_t ldc = P->ldc;
+  const int64_t piv = potrf(st, n, P->Cp, ldc);
   if (piv >= 0) return piv;
   // the forward solve reads block rows of C as block columns of C^T: keep the mirror in
   // the (zeroed) upper triangle
-  mirror_lower(st, n, P->C.p, n);
+  mirror_lower(st, n, P->Cp, ldc);
   // the stencil R: keep only its CSR (7 nonzeros per row) for the per-step R I
-  P->r_sparse = csr_from_dense(st, n, P->R.p, n, 0.02, P->Rs);
-  if (P->r_sparse) P->R.release();
+  if (!Rb) {
+    P->r_sparse = csr_from_dense(st, n, P->R.p, n, 0.02, P->Rs);
+    if (P->r_sparse) P->R.release();
+  }
   const int64_t nblk = (n + TS - 1) / TS;
   P->Dinv.alloc((size_t)nblk * TS * TS, st);
-  trtri_blocks(st, TS, n, P->C.p, n, P->Dinv.p);
+  trtri_blocks(st, TS, n, P->Cp, ldc, P->Dinv.p);
   P->DinvT.alloc((size_t)nblk * TS * TS, st);
   transpose_blocks_kernel<<<(unsigned)nblk, 256, 0, st>>>(P->Dinv.p, P->DinvT.p);
   EM_LAUNCHED();
@@ -413,18 +453,18 @@ int64_t td1_plan_init(em_td1_plan* P, const double* L, int64_t ldl, const double
     std::vector<GemmArgs> pf, pb;
     for (int64_t r = 1; r < nblk; ++r) {
       const int64_t r0 = r * TS, bs = imin64(TS, n - r0);
-      pf.push_back(GemmArgs{bs, TS, bs, P->Dinv.p + r * TS * TS, TS, P->C.p + r0 + (r0 - TS) * n, n,
+      pf.push_back(GemmArgs{bs, TS, bs, P->Dinv.p + r * TS * TS, TS, P->Cp + r0 + (r0 - TS) * ldc, ldc,
                             P->Ef.p + r * TS * TS, TS, 1.0, 0.0, 0});
       const int64_t q = r - 1;  // Fb_q with block q + 1 = r below it
-      pb.push_back(GemmArgs{TS, bs, TS, P->DinvT.p + q * TS * TS, TS, P->C.p + r0 + q * TS * n, n,
+      pb.push_back(GemmArgs{TS, bs, TS, P->DinvT.p + q * TS * TS, TS, P->Cp + r0 + q * TS * ldc, ldc,
                             P->Fb.p + q * TS * TS, TS, 1.0, 0.0, 0});
       if (r >= 2) {
         pf.push_back(GemmArgs{bs, TS, bs, P->Dinv.p + r * TS * TS, TS,
-                              P->C.p + r0 + (r0 - 2 * TS) * n, n, P->Ef2.p + r * TS * TS, TS, 1.0,
+                              P->Cp + r0 + (r0 - 2 * TS) * ldc, ldc, P->Ef2.p + r * TS * TS, TS, 1.0,
                               0.0, 0});
         const int64_t q2 = r - 2;  // Fb2_q2 with block q2 + 2 = r below it
         pb.push_back(GemmArgs{TS, bs, TS, P->DinvT.p + q2 * TS * TS, TS,
-                              P->C.p + r0 + q2 * TS * n, n, P->Fb2.p + q2 * TS * TS, TS, 1.0,
+                              P->Cp + r0 + q2 * TS * ldc, ldc, P->Fb2.p + q2 * TS * TS, TS, 1.0,
                               0.0, 0});
       }
     }
@@ -484,13 +524,13 @@ static void td1_solve_step(em_td1_plan* P, double* I, double* Icap_col, const do
   const int grid = (int)imin64(nblk, 2 * num_sms());
   {
     Stage s(st, ST_TD1_FWD);
-    trsv_fwd_kernel<<<grid, 256, 0, st>>>(n, P->C.p, n, P->Dinv.p, P->Ef.p, P->Ef2.p, P->b.p,
+    trsv_fwd_kernel<<<grid, 256, 0, st>>>(n, P->Cp, P->ldc, P->Dinv.p, P->Ef.p, P->Ef2.p, P->b.p,
                                           P->y.p, P->counters->p);
     EM_LAUNCHED();
   }
   {
     Stage s(st, ST_TD1_BWD);
-    trsv_bwd_kernel<<<grid, 256, 0, st>>>(n, P->C.p, n, P->DinvT.p, P->Fb.p, P->Fb2.p, P->y.p,
+    trsv_bwd_kernel<<<grid, 256, 0, st>>>(n, P->Cp, P->ldc, P->DinvT.p, P->Fb.p, P->Fb2.p, P->y.p,
                                           P->x.p, I, Icap_col, P->counters->p + 1);
     EM_LAUNCHED();
   }
@@ -567,7 +607,7 @@ void td1_delete(em_td1_plan* p) {
 }
 em_ctx* td1_ctx(em_td1_plan* p) { return p ? p->ctx : nullptr; }
 void td1_copy_factor(em_td1_plan* P, double* out, int64_t ldo) {
-  copy_matrix(P->ctx->stream, false, P->n, P->n, P->C.p, P->n, out, ldo);
+  copy_matrix(P->ctx->stream, false, P->n, P->n, P->Cp, P->ldc, out, ldo);
   zero_upper(P->ctx->stream, P->n, out, ldo);  // the plan keeps C^T there
   EM_CK(cudaStreamSynchronize(P->ctx->stream));
 }

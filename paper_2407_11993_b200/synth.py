@@ -93,6 +93,30 @@ class Plate:
             r[jj[m], ii[m]] = -RHO
         return r
 
+    def resistance_band(self) -> tuple[np.ndarray, int]:
+        """R in LAPACK lower band storage, (bw + 1, N) with band[i - j, j] = R[i, j] for
+        0 <= i - j <= bw — the same stencil as resistance(), without the N x N array."""
+        n = self.n
+        pos = -np.ones(self.nx * self.ny * self.nz, dtype=np.int64)
+        pos[self.keep] = np.arange(n)
+        ix, iy, iz = np.unravel_index(self.keep, (self.nx, self.ny, self.nz))
+        pairs = []
+        for sx, sy, sz in ((1, 0, 0), (0, 1, 0), (0, 0, 1)):
+            jx, jy, jz = ix + sx, iy + sy, iz + sz
+            ok = (jx < self.nx) & (jy < self.ny) & (jz < self.nz)
+            j_all = np.ravel_multi_index((jx[ok], jy[ok], jz[ok]), (self.nx, self.ny, self.nz))
+            jj = pos[j_all]
+            ii = np.arange(n)[ok]
+            m = jj >= 0
+            pairs.append((ii[m], jj[m]))
+        bw = max([int(np.max(np.abs(jj - ii))) for ii, jj in pairs if ii.size] or [0])
+        band = np.zeros((bw + 1, n))
+        band[0, :] = RHO * 6.0 + R_SHIFT
+        for ii, jj in pairs:
+            lo, hi = np.minimum(ii, jj), np.maximum(ii, jj)
+            band[hi - lo, lo] = -RHO
+        return band, bw
+
     def inductance(self, rows: slice | None = None) -> np.ndarray:
         """Dense L (or a row block of it)."""
         x = self.centroids()
@@ -187,10 +211,13 @@ def plate_model(nx: int, ny: int, nz: int, n_ports: int = 0, n_sources: int = 1,
 
 def device_plate_model(nx: int, ny: int, nz: int, n_ports: int = 0, n_sources: int = 1,
                        n_obs: int = 16, seed: int = DEFAULT_SEED, notch: bool = False,
-                       h: float = 1e-3) -> dict:
+                       h: float = 1e-3, r_dense: bool = True, ldl: int | None = None) -> dict:
     """plate_model with the O(N^2) parts generated on the device (em_synth_plate):
     l_i, r_i (torch, (N, N) symmetric), r_d, l_d (torch (n_ports, N) = column-major
-    N x n_ports), plus host m0 (N x n_sources) and c (n_obs x N)."""
+    N x n_ports), plus host m0 (N x n_sources) and c (n_obs x N).
+    r_dense=False: no dense R; r_band (torch (N, bw + 1) = column-major lower band storage)
+    and r_bw instead (the N = 120,000 plate: L alone is 115 GB). ldl: L's leading dimension
+    (torch (N, ldl)); a multiple of 32 lets the eigensolve reduce L in place."""
     from . import _native as nat
     p = Plate(nx, ny, nz, h=h, seed=seed, notch=notch)
     n = p.n
@@ -201,18 +228,33 @@ def device_plate_model(nx: int, ny: int, nz: int, n_ports: int = 0, n_sources: i
     keep_d = t.from_numpy(p.keep.astype(np.int64)).to("cuda")
     pos_d = t.from_numpy(pos).to("cuda")
     ang_d = nat.device_vector(theta)
-    L = nat.empty(n, n)
-    R = nat.empty(n, n)
+    ldl = n if ldl is None else int(ldl)
+    L = nat.empty(n, ldl)
+    R = nat.empty(n, n) if r_dense else None
     ld = nat.zeros(max(n_ports, 1), n)
     rd = nat.zeros(max(n_ports, 1), n)
     lib = nat.load_library()
     nat.check(lib.em_synth_plate(nat.context(), nx, ny, nz, h, RHO, R_SHIFT, n, nat.ptr(keep_d),
-                                 nat.ptr(pos_d), nat.ptr(ang_d), nat.ptr(L), n, nat.ptr(R), n,
+                                 nat.ptr(pos_d), nat.ptr(ang_d), nat.ptr(L), ldl,
+                                 nat.ptr(R) if R is not None else None, n,
                                  nat.ptr(ld) if n_ports else None,
                                  nat.ptr(rd) if n_ports else None), "em_synth_plate")
     m0 = p.source_profiles(n_sources) if n_sources else np.zeros((n, 0))
     c = p.observables(n_obs)
-    return dict(plate=p, l_i=L, r_i=R, l_d=ld[:n_ports], r_d=rd[:n_ports], m0=m0, c=c)
+    out = dict(plate=p, l_i=L, r_i=R, l_d=ld[:n_ports], r_d=rd[:n_ports], m0=m0, c=c, ldl=ldl)
+
+    def regen_l():
+        """Regenerate L into out["l_i"] (after an in-place solve consumed it)."""
+        nat.check(lib.em_synth_plate(nat.context(), nx, ny, nz, h, RHO, R_SHIFT, n,
+                                     nat.ptr(keep_d), nat.ptr(pos_d), nat.ptr(ang_d),
+                                     nat.ptr(out["l_i"]), ldl, None, n, None, None),
+                  "em_synth_plate")
+    out["regen_l"] = regen_l
+    if not r_dense:
+        band, bw = p.resistance_band()
+        out["r_band"] = nat.device_colmajor(band)  # (N, bw + 1): column-major (bw + 1) x N
+        out["r_bw"] = bw
+    return out
 
 
 def drive_table(kind: str, steps: int, dt: float, n_ports: int, n_sources: int,
