@@ -85,8 +85,8 @@ int em_synchronize(em_ctx* ctx);
  * (tau_max/tau_min) kappa(R)): a non-SPD L raises the same error with the same pivot,
  * after the eigensolve instead of before it. */
 #define EM_CFG_L_CERTIFICATE 5
-/* Keys 96-99 are debug switches for A/B measurements and the tests (96 GEMM tile
- * configuration, 97 Q2 back-transform form, 98 tridiagonalisation code paths, 99 trim
+/* Keys 95-99 are debug switches for A/B measurements and the tests (95 TMA-fed GEMM: 0
+ * off, 1 auto, 2, 4, 5 force a tile configuration; 96 cp.async GEMM tile configuration, 97 Q2 back-transform form, 98 tridiagonalisation code paths, 99 trim
  * the device memory pool to `value` bytes); see capi.cu. */
 int em_config(em_ctx* ctx, int key, int64_t value);
 /* Stage timers (CUDA events on the context stream). em_profile(ctx, 1) clears and
@@ -104,6 +104,14 @@ int em_stage_times(em_ctx* ctx, double* ms, int64_t* counts, int n);
 int em_dgemm(em_ctx* ctx, int trans_a, int trans_b, int64_t m, int64_t n, int64_t k,
              double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
              double beta, double* C, int64_t ldc);
+
+/* em_dgemm computing and writing only the entries (r, c) of C with r + diag_off >= c (the
+ * triangular-output products of the Cholesky trailing updates and the syr2k-style
+ * updates of the tridiagonalisation, _kernels.py:18-36 / linalg.py:119-134 on the
+ * reference side); entries above that diagonal are left untouched. */
+int em_dgemm_lower(em_ctx* ctx, int trans_a, int trans_b, int64_t m, int64_t n, int64_t k,
+                   double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
+                   double beta, double* C, int64_t ldc, int64_t diag_off);
 
 /* y = alpha A x + beta y for symmetric A reading only its lower triangle (the dense
  * R @ state loop of td1_step_kernel, _kernels.py:203-207). HBM-bound. */

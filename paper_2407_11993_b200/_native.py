@@ -40,6 +40,8 @@ SIGNATURES = {
     "em_profile": (_I, [_P, _I]),
     "em_stage_times": (_I, [_P, _P, _P, _I]),
     "em_dgemm": (_I, [_P, _I, _I, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D, _P, _I64]),
+    "em_dgemm_lower": (_I, [_P, _I, _I, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D, _P, _I64,
+                            _I64]),
     "em_sym_mirror_lower": (_I, [_P, _I64, _P, _I64]),
     "em_sym_mm": (_I, [_P, _I64, _I64, _P, _I64, _P, _I64, _P, _I64]),
     "em_symv_lower": (_I, [_P, _I64, _D, _P, _I64, _P, _D, _P]),

@@ -25,6 +25,7 @@ extern int g_q2_mode;
 extern int g_symv_align_off;
 extern int64_t g_symv_keep_mb;
 extern int64_t g_gemm_cfg;
+extern int64_t g_gemm_tma;
 void stages_reset(bool on);
 void stages_level(int level);
 int stages_read(double* ms, int64_t* counts, int n);
@@ -187,6 +188,10 @@ int em_config(em_ctx* ctx, int key, int64_t value) {
       em::g_symv_keep_mb = value;
       return EM_OK;
     }
+    if (key == 95) {  // debug: TMA-fed GEMM (0 off, 1 auto, 2 / 4 / 5 force a tile configuration)
+      em::g_gemm_tma = value;
+      return EM_OK;
+    }
     if (key == 96) {  // debug: GEMM tiles (0 default, 2 64x64 x4, 3 128x64, 4 64x64 x3)
       em::g_gemm_cfg = value;
       return EM_OK;
@@ -228,6 +233,16 @@ int em_dgemm(em_ctx* ctx, int ta, int tb, int64_t m, int64_t n, int64_t k, doubl
              int64_t ldc) {
   return guarded(ctx, [&] {
     EM_CK(em::gemm(ctx->stream, ta != 0, tb != 0, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc));
+    return EM_OK;
+  });
+}
+
+int em_dgemm_lower(em_ctx* ctx, int ta, int tb, int64_t m, int64_t n, int64_t k, double alpha,
+                   const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
+                   double* C, int64_t ldc, int64_t diag_off) {
+  return guarded(ctx, [&] {
+    EM_CK(em::gemm(ctx->stream, ta != 0, tb != 0, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc,
+                   true, diag_off));
     return EM_OK;
   });
 }

@@ -446,6 +446,15 @@ __global__ void splitk_reduce_kernel(int64_t m, int64_t n, int splits, const dou
   }
 }
 
+void splitk_reduce(cudaStream_t st, int64_t m, int64_t n, int splits, const double* ws,
+                   double alpha, double beta, double* C, int64_t ldc, int lower, int64_t diag_off) {
+  const int64_t total = m * n;
+  const int blocks = (int)imin64((total + 255) / 256, 8 * (int64_t)num_sms());
+  splitk_reduce_kernel<<<blocks, 256, 0, st>>>(m, n, splits, ws, alpha, beta, C, ldc, lower,
+                                               diag_off);
+  count_launch();
+}
+
 template <int TA, int TB, int LOWER, int VEC, class C>
 static cudaError_t launch_t(const GemmArgs& p, cudaStream_t st) {
   auto k = gemm_kernel<TA, TB, LOWER, VEC, 0, C>;
@@ -489,11 +498,7 @@ static cudaError_t launch_t(const GemmArgs& p, cudaStream_t st) {
   dim3 grid((unsigned)tiles, 1, (unsigned)splits);
   k<<<grid, C::THREADS, sm, st>>>(p, ws, kc);
   count_launch();
-  const int64_t total = p.m * p.n;
-  const int blocks = (int)imin64((total + 255) / 256, 8 * sms);
-  splitk_reduce_kernel<<<blocks, 256, 0, st>>>(p.m, p.n, (int)splits, ws, p.alpha, p.beta, p.C,
-                                               p.ldc, LOWER, p.diag_off);
-  count_launch();
+  splitk_reduce(st, p.m, p.n, (int)splits, ws, p.alpha, p.beta, p.C, p.ldc, LOWER, p.diag_off);
   cudaFreeAsync(ws, st);
   return cudaGetLastError();
 }
@@ -523,6 +528,10 @@ cudaError_t gemm(cudaStream_t st, bool ta, bool tb, int64_t m, int64_t n, int64_
   if (k <= 0) {
     // pure scaling: C = beta*C
     return scale_matrix(st, m, n, beta, C, ldc, lower, diag_off);
+  }
+  {  // large aligned products: the TMA-fed persistent kernel (gemm_tma.cu)
+    const cudaError_t e = gemm_tma(st, ta, tb, p, lower);
+    if (e != cudaErrorNotSupported) return e;
   }
   int code = (ta ? 4 : 0) | (tb ? 2 : 0) | (lower ? 1 : 0);
   switch (code) {

@@ -33,6 +33,13 @@ cudaError_t gemm_lower_a(cudaStream_t st, int64_t m, int64_t n, int64_t k, doubl
 cudaError_t gemm_grouped(cudaStream_t st, bool ta, bool tb, const GemmArgs* d_probs, int nprob,
                          int max_tiles);
 
+// TMA-fed persistent kernel for large aligned products (gemm_tma.cu); returns
+// cudaErrorNotSupported when the product does not qualify (gemm() then takes the cp.async path).
+cudaError_t gemm_tma(cudaStream_t st, bool ta, bool tb, const GemmArgs& p, bool lower);
+// C = alpha * sum_z W_z + beta * C over `splits` m x n partials (fixed order).
+void splitk_reduce(cudaStream_t st, int64_t m, int64_t n, int splits, const double* ws,
+                   double alpha, double beta, double* C, int64_t ldc, int lower, int64_t diag_off);
+
 cudaError_t scale_matrix(cudaStream_t st, int64_t m, int64_t n, double beta, double* C, int64_t ldc,
                          bool lower, int64_t diag_off);
 

@@ -493,7 +493,8 @@ def step_td2(stepper: Td2Stepper, modal_state, forcing) -> np.ndarray:
 
 def _drive_channels(net, rm: ReducedModel, drives):
     """Port/source name order and per-channel tone lists (transient.py:198-219)."""
-    if net is not None:
+    # a geometry-only network (observers need just the segment geometry) names nothing
+    if net is not None and hasattr(net, "electrodes"):
         port_names = [el.name for el in net.electrodes[:-1]] if net.n_electrodes else []
         source_names = [c.name for c in net.sources if c.port is None]
     else:

@@ -24,6 +24,8 @@ def timed(fn, reps=5):
 
 
 ctx, lib = nat.context(), nat.load_library()
+if "GEMM_TMA" in os.environ:  # em_config debug key 95: 0 off, 1 auto, 2..5 forced TMA config
+    nat.check(lib.em_config(ctx, 95, int(os.environ["GEMM_TMA"])))
 if "GEMM_CFG" in os.environ:  # em_config debug key 96: 0 auto, 2 64x64 tiles, 3 128x64
     nat.check(lib.em_config(ctx, 96, int(os.environ["GEMM_CFG"])))
 g = torch.Generator(device="cuda").manual_seed(3)
@@ -60,8 +62,14 @@ for m, n, k, ta, tb, label in shapes:
     else:
         t_cub = timed(lambda: torch.addmm(c, aa, bb, beta=BETA, out=c))
     fl = 2.0 * m * n * k
+    # one checked product (beta = 0) against cuBLAS
+    nat.check(lib.em_dgemm(ctx, ta, tb, m, n, k, 1.0, nat.ptr(A), lda, nat.ptr(B), ldb, 0.0,
+                           nat.ptr(ct), m))
+    torch.matmul(aa, bb, out=c)
+    err = float((ct.t() - c).abs().max()) / float(c.abs().max())
     out.append({"beta": BETA, "shape": label, "m": m, "n": n, "k": k, "own_TFps": fl / t_own / 1e12,
-                "cublas_TFps": fl / t_cub / 1e12})
+                "cublas_TFps": fl / t_cub / 1e12, "rel_err_vs_cublas": err,
+                "tma": os.environ.get("GEMM_TMA", "auto")})
     del a, b, c, A, B, ct
 for o in out:
     print(json.dumps(o))
