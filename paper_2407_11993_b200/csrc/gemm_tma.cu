@@ -88,6 +88,10 @@ struct TmaGemmParams {
   int64_t tiles_m, tiles_n;
   unsigned long long* ctr;  // [0] next unit, [1] CTAs done
   int prefetch_c;           // beta != 0 and C admits a tensor map: L2-prefetch each C tile
+  int sh_a, sh_b;           // operand starts 8 bytes past a 16-byte boundary: the map's base is
+                            // the aligned address below it (TMA box starts must be 16-byte
+                            // aligned), so the tile sits one element into its box — inside
+                            // the 4 padding elements — and the fragment offsets move up by 1
 };
 
 constexpr int TGROUP = 16;  // tile rows walked per tile-column run
@@ -197,8 +201,8 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
   const int wm = warp % C::WGM, wn = warp / C::WGM;
   const int mb = wm * 8 * WTM, nb = wn * 8 * WTN;
   // fragment offsets of this lane for k-step 0 (constant over the kernel)
-  const int a_off = AT::idx(mb + g, t);
-  const int b_off = BT::idx(t, nb + g);
+  const int a_off = AT::idx(mb + g, t) + q.sh_a;
+  const int b_off = BT::idx(t, nb + g) + q.sh_b;
   constexpr int A_I = AT::idx(8, 0) - AT::idx(0, 0);   // next 8-row fragment
   constexpr int A_K = AT::idx(0, 4) - AT::idx(0, 0);   // next k-step
   constexpr int B_J = BT::idx(0, 8) - BT::idx(0, 0);
@@ -378,10 +382,12 @@ cudaError_t launch_tma(const GemmArgs& p, cudaStream_t st) {
   unsigned long long* ctrs = claim_counters();
   if (!ctrs) return cudaErrorMemoryAllocation;
   CUtensorMap mapA, mapB;
-  const bool okA = TA ? make_map(&mapA, p.A, p.k, p.m, p.lda, TPK, C::BM)
-                      : make_map(&mapA, p.A, p.m, p.k, p.lda, C::SPM, TBK);
-  const bool okB = TB ? make_map(&mapB, p.B, p.n, p.k, p.ldb, C::SPN, TBK)
-                      : make_map(&mapB, p.B, p.k, p.n, p.ldb, TPK, C::BN);
+  const int sh_a = (reinterpret_cast<uintptr_t>(p.A) & 15) ? 1 : 0;
+  const int sh_b = (reinterpret_cast<uintptr_t>(p.B) & 15) ? 1 : 0;
+  const bool okA = TA ? make_map(&mapA, p.A - sh_a, p.k + sh_a, p.m, p.lda, TPK, C::BM)
+                      : make_map(&mapA, p.A - sh_a, p.m + sh_a, p.k, p.lda, C::SPM, TBK);
+  const bool okB = TB ? make_map(&mapB, p.B - sh_b, p.n + sh_b, p.k, p.ldb, C::SPN, TBK)
+                      : make_map(&mapB, p.B - sh_b, p.k + sh_b, p.n, p.ldb, TPK, C::BN);
   if (!okA || !okB) return cudaErrorNotSupported;
   CUtensorMap mapC = mapA;  // placeholder when C is not prefetched
   const bool okC = p.beta != 0.0 && (reinterpret_cast<uintptr_t>(p.C) & 15) == 0 &&
@@ -435,6 +441,8 @@ cudaError_t launch_tma(const GemmArgs& p, cudaStream_t st) {
   q.kc = kc;
   q.splits = (int)splits;
   q.prefetch_c = (okC && !ws) ? 1 : 0;
+  q.sh_a = sh_a;
+  q.sh_b = sh_b;
   q.ctr = ctrs + 2 * (g_tma_launch_no.fetch_add(1, std::memory_order_relaxed) % NCTR);
   const int grid = (int)imin64((int64_t)slots, tiles * splits);
   kern<<<grid, C::THREADS, sm, st>>>(mapA, mapB, mapC, q);
@@ -469,13 +477,12 @@ cudaError_t launch_cfg(const GemmArgs& p, cudaStream_t st, int cfg) {
 }  // namespace
 
 // Returns cudaErrorNotSupported when the product does not qualify (the caller falls back
-// to the cp.async kernels): operands must be 16-byte aligned with even leading dimensions,
+// to the cp.async kernels): the leading dimensions must be even (TMA strides),
 // extents must fit TMA's 32-bit coordinates, and the product must be large enough to fill
 // the persistent grid.
 cudaError_t gemm_tma(cudaStream_t st, bool ta, bool tb, const GemmArgs& p, bool lower) {
   if (g_gemm_tma == 0) return cudaErrorNotSupported;
-  auto al = [](const void* x) { return (reinterpret_cast<uintptr_t>(x) & 15) == 0; };
-  if (!al(p.A) || !al(p.B) || (p.lda & 1) || (p.ldb & 1)) return cudaErrorNotSupported;
+  if ((p.lda & 1) || (p.ldb & 1)) return cudaErrorNotSupported;  // TMA strides: 16-byte units
   if (p.m > INT32_MAX || p.n > INT32_MAX || p.k > INT32_MAX) return cudaErrorNotSupported;
   if (p.lda * 8 >= (1ll << 40) || p.ldb * 8 >= (1ll << 40)) return cudaErrorNotSupported;
   if (g_gemm_tma == 1) {
@@ -491,7 +498,13 @@ cudaError_t gemm_tma(cudaStream_t st, bool ta, bool tb, const GemmArgs& p, bool 
             (long long)p.m, (long long)p.n, (long long)p.k, (long long)p.lda, (long long)p.ldb,
             (long long)p.ldc, (long long)p.diag_off, p.alpha, p.beta, (const void*)p.A,
             (const void*)p.B, (const void*)p.C);
-  const int cfg = (int)g_gemm_tma;
+  int cfg = (int)g_gemm_tma;
+  // auto: 128-column tiles unless they would pad n by more than 5% (n = 64 panels of the
+  // band reduction: half of every 128 x 128 tile would be zero work)
+  if (cfg == 1) {
+    const int64_t n128 = (p.n + 127) / 128 * 128, n64 = (p.n + 63) / 64 * 64;
+    cfg = (n128 - n64) * 20 > n128 ? 2 : 4;
+  }
   const int code = (ta ? 4 : 0) | (tb ? 2 : 0) | (lower ? 1 : 0);
   switch (code) {
     case 0: return launch_cfg<0, 0, 0>(p, st, cfg);

@@ -1010,7 +1010,14 @@ void stedc(cudaStream_t st, int64_t n, double* d, double* e, double* Z, int64_t 
                             cudaMemcpyHostToDevice, st));
       const int grid_x = std::min(max_tiles, 4 * num_sms());
       Stage sg(st, ST_STEDC_GEMM);
-      EM_CK(gemm_grouped(st, false, false, dp.p, (int)probs.size(), grid_x));
+      if (nm <= 8 && maxn >= 4096) {
+        // the few large merges at the top of the tree: one product each (TMA-fed kernel)
+        for (const GemmArgs& g : probs)
+          EM_CK(gemm(st, false, false, g.m, g.n, g.k, g.alpha, g.A, g.lda, g.B, g.ldb, g.beta,
+                     g.C, g.ldc));
+      } else {
+        EM_CK(gemm_grouped(st, false, false, dp.p, (int)probs.size(), grid_x));
+      }
       EM_CK(cudaStreamSynchronize(st));  // dp lifetime
     }
     dc_order_kernel<<<nm, 32, 0, st>>>(dmo.p, dmn.p, minfo.p, w, lam_nxt);

@@ -11,6 +11,11 @@ SHAPES = ((256, 192, 64), (300, 333, 146), (130, 64, 1100), (517, 260, 33), (128
           (1, 1, 1), (37, 129, 300), (96, 2000, 2100))
 
 
+def _off8(t):
+    import ctypes
+    return ctypes.c_void_p(t.data_ptr() + 8)
+
+
 def _lib():
     from paper_2407_11993_b200 import _native as nat
     return nat, nat.context(), nat.load_library()
@@ -97,3 +102,39 @@ def test_dgemm_tma_auto_large_and_repeatable():
         assert torch.equal(outs[0], outs[1])
         scale = float(outs[2].abs().max())
         assert float((outs[0] - outs[2]).abs().max()) <= 1e-12 * scale
+
+
+@pytest.mark.parametrize("cfg", [2, 4])
+def test_dgemm_tma_operands_on_odd_elements(cfg):
+    """Operands starting 8 bytes past a 16-byte boundary (sub-blocks at odd row offsets, as
+    the divide-and-conquer merges pass them): the tensor map starts one element lower and
+    the contiguous coordinate moves up by one."""
+    nat, ctx, lib = _lib()
+    rng = np.random.default_rng(3)
+    nat.check(lib.em_config(ctx, 95, cfg))
+    try:
+        for (m, n, k) in ((300, 333, 146), (256, 192, 64), (129, 70, 2100)):
+            for ta in (0, 1):
+                for tb in (0, 1):
+                    a = rng.standard_normal((k, m) if ta else (m, k))
+                    b = rng.standard_normal((n, k) if tb else (k, n))
+                    c0 = rng.standard_normal((m, n))
+                    # one garbage row above each operand; even leading dimensions
+                    lda = a.shape[0] + 1 + ((a.shape[0] + 1) & 1)
+                    ldb = b.shape[0] + 1 + ((b.shape[0] + 1) & 1)
+                    ap = np.full((lda, a.shape[1]), np.nan)
+                    ap[1:1 + a.shape[0]] = a
+                    ap[1 + a.shape[0]:] = 7.0
+                    bp = np.full((ldb, b.shape[1]), np.nan)
+                    bp[1:1 + b.shape[0]] = b
+                    bp[1 + b.shape[0]:] = -3.0
+                    da, db, dc = (nat.device_colmajor(ap), nat.device_colmajor(bp),
+                                  nat.device_colmajor(c0))
+                    nat.check(lib.em_dgemm(ctx, ta, tb, m, n, k, 1.0, _off8(da), lda,
+                                           _off8(db), ldb, 1.0, nat.ptr(dc), m))
+                    ref = (a.T if ta else a) @ (b.T if tb else b) + c0
+                    got = nat.host_colmajor(dc, m, n)
+                    assert np.abs(got - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max()), \
+                        (cfg, m, n, k, ta, tb)
+    finally:
+        nat.check(lib.em_config(ctx, 95, 1))
