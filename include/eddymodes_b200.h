@@ -113,6 +113,14 @@ int em_dgemm_lower(em_ctx* ctx, int trans_a, int trans_b, int64_t m, int64_t n, 
                    double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
                    double beta, double* C, int64_t ldc, int64_t diag_off);
 
+/* C (m x n) = A B for a symmetric m x m A of which only the lower triangle and the 127
+ * diagonals above it are read (those must hold the mirrored values): the product
+ * X = A22 (V T) of the blocked band reduction behind sym_eig (linalg.py:119-134), one
+ * TMA-fed kernel in which every row tile runs over the whole k range. A must be 16-byte
+ * aligned with even lda and ldb (else EM_ERR_ARG). */
+int em_dsymm_band_lower(em_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda,
+                        const double* B, int64_t ldb, double* C, int64_t ldc);
+
 /* y = alpha A x + beta y for symmetric A reading only its lower triangle (the dense
  * R @ state loop of td1_step_kernel, _kernels.py:203-207). HBM-bound. */
 int em_symv_lower(em_ctx* ctx, int64_t n, double alpha, const double* A, int64_t lda,

@@ -42,6 +42,7 @@ SIGNATURES = {
     "em_dgemm": (_I, [_P, _I, _I, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D, _P, _I64]),
     "em_dgemm_lower": (_I, [_P, _I, _I, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D, _P, _I64,
                             _I64]),
+    "em_dsymm_band_lower": (_I, [_P, _I64, _I64, _P, _I64, _P, _I64, _P, _I64]),
     "em_sym_mirror_lower": (_I, [_P, _I64, _P, _I64]),
     "em_sym_mm": (_I, [_P, _I64, _I64, _P, _I64, _P, _I64, _P, _I64]),
     "em_symv_lower": (_I, [_P, _I64, _D, _P, _I64, _P, _D, _P]),

@@ -247,6 +247,17 @@ int em_dgemm_lower(em_ctx* ctx, int ta, int tb, int64_t m, int64_t n, int64_t k,
   });
 }
 
+int em_dsymm_band_lower(em_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda,
+                        const double* B, int64_t ldb, double* C, int64_t ldc) {
+  return guarded(ctx, [&] {
+    const cudaError_t e = em::gemm_symm_lower_tma(ctx->stream, m, n, A, lda, B, ldb, C, ldc);
+    if (e == cudaErrorNotSupported)
+      throw em::ArgError{"em_dsymm_band_lower: A must be 16-byte aligned with even lda, ldb"};
+    EM_CK(e);
+    return EM_OK;
+  });
+}
+
 int em_symv_lower(em_ctx* ctx, int64_t n, double alpha, const double* A, int64_t lda,
                   const double* x, double beta, double* y) {
   return guarded(ctx, [&] {

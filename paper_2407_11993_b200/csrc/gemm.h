@@ -36,6 +36,11 @@ cudaError_t gemm_grouped(cudaStream_t st, bool ta, bool tb, const GemmArgs* d_pr
 // TMA-fed persistent kernel for large aligned products (gemm_tma.cu); returns
 // cudaErrorNotSupported when the product does not qualify (gemm() then takes the cp.async path).
 cudaError_t gemm_tma(cudaStream_t st, bool ta, bool tb, const GemmArgs& p, bool lower);
+// C (m x n) = A B for a symmetric A read from its lower triangle and the SYMM_BAND diagonals
+// above it (gemm_tma.cu); cudaErrorNotSupported when TMA cannot address the operands.
+constexpr int SYMM_BAND = 127;
+cudaError_t gemm_symm_lower_tma(cudaStream_t st, int64_t m, int64_t n, const double* A,
+                                int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc);
 // C = alpha * sum_z W_z + beta * C over `splits` m x n partials (fixed order).
 void splitk_reduce(cudaStream_t st, int64_t m, int64_t n, int splits, const double* ws,
                    double alpha, double beta, double* C, int64_t ldc, int lower, int64_t diag_off);

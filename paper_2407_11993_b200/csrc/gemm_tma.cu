@@ -112,15 +112,55 @@ EM_DEVINL bool unit_decode(const TmaGemmParams& q, int64_t u, int64_t& m0, int64
   return !(LOWER && m0 + C::BM - 1 + q.p.diag_off < n0);
 }
 
-template <int TA, int TB, int LOWER, class C>
+// One k-tile of the warp tile: fragments of a TA_/TB_-layout stage (pointers at this lane's
+// k-step-0 fragments), double-buffered in registers.
+template <int TA_, int TB_, class C>
+EM_DEVINL void ktile_mma(double (&acc)[C::TM][C::TN][2], const double* as, const double* bs) {
+  using AT = TATile<TA_, C>;
+  using BT = TBTile<TB_, C>;
+  constexpr int WTM = C::TM, WTN = C::TN;
+  constexpr int A_I = AT::idx(8, 0) - AT::idx(0, 0);   // next 8-row fragment
+  constexpr int A_K = AT::idx(0, 4) - AT::idx(0, 0);   // next k-step
+  constexpr int B_J = BT::idx(0, 8) - BT::idx(0, 0);
+  constexpr int B_K = BT::idx(4, 0) - BT::idx(0, 0);
+  double af[2][WTM], bf[2][WTN];
+#pragma unroll
+  for (int i = 0; i < WTM; ++i) af[0][i] = as[i * A_I];
+#pragma unroll
+  for (int j = 0; j < WTN; ++j) bf[0][j] = bs[j * B_J];
+#pragma unroll
+  for (int ks = 0; ks < TBK / 4; ++ks) {
+    const int cur = ks & 1, nx = cur ^ 1;
+    if (ks + 1 < TBK / 4) {
+#pragma unroll
+      for (int i = 0; i < WTM; ++i) af[nx][i] = as[i * A_I + (ks + 1) * A_K];
+#pragma unroll
+      for (int j = 0; j < WTN; ++j) bf[nx][j] = bs[j * B_J + (ks + 1) * B_K];
+    }
+#pragma unroll
+    for (int i = 0; i < WTM; ++i)
+#pragma unroll
+      for (int j = 0; j < WTN; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[cur][i], bf[cur][j]);
+  }
+}
+
+// SYMM: C = A B for a symmetric A given by its lower triangle plus the BM - 1 diagonals above
+// it (TA is ignored, A is m x m = k x k): the k-tiles of a row tile left of and on its
+// diagonal block are read as stored (A[m0.., kk..], m-contiguous boxes of mapA), those
+// below it through the transpose (A[kk.., m0..]^T, k-contiguous boxes of mapC, which no
+// beta = 0 product needs for C) — every row tile runs over the whole k range.
+template <int TA, int TB, int LOWER, class C, int SYMM = 0>
 __global__ void __launch_bounds__(C::THREADS, C::MINB)
     gemm_tma_kernel(const __grid_constant__ CUtensorMap mapA,
                     const __grid_constant__ CUtensorMap mapB,
                     const __grid_constant__ CUtensorMap mapC, const TmaGemmParams q) {
-  using AT = TATile<TA, C>;
+  using AT = TATile<SYMM ? 0 : TA, C>;
+  using ATT = TATile<1, C>;  // SYMM: the transposed reads
   using BT = TBTile<TB, C>;
-  constexpr int ASZ = AT::size, BSZ = BT::size, NST = tma_stages<TA, TB, C>();
-  constexpr unsigned STAGE_BYTES = (ASZ + BSZ) * sizeof(double);
+  constexpr int ASZ = SYMM ? (ATT::size > AT::size ? ATT::size : AT::size) : AT::size;
+  constexpr int BSZ = BT::size, NST = tma_stages<(SYMM ? 1 : TA), TB, C>();
+  constexpr unsigned STAGE_BYTES = (AT::size + BSZ) * sizeof(double);
+  constexpr unsigned STAGE_BYTES_T = (ATT::size + BSZ) * sizeof(double);
   extern __shared__ __align__(128) double smem[];
   double* As = smem;
   double* Bs = smem + NST * ASZ;
@@ -166,7 +206,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
       if (u >= total) break;
       // the epilogue's reads of C (beta != 0) are dependent round trips: fetch the tile into
       // L2 now, a whole main loop ahead
-      if (q.prefetch_c)
+      if (!SYMM && q.prefetch_c)
         asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n" ::"l"(
                          &mapC),
                      "r"((int)m0), "r"((int)n0)
@@ -177,9 +217,15 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
       for (int kt = 0; kt < nk; ++kt, ++it) {
         const int s = it % NST;
         mbar_wait(&empty[s], ((it / NST) & 1) ^ 1);
-        mbar_expect_tx(&full[s], STAGE_BYTES);
         const int kk = (int)(k0 + (int64_t)kt * TBK);
-        tma_load_2d(As + s * ASZ, &mapA, TA ? kk : (int)m0, TA ? (int)m0 : kk, &full[s], pol);
+        if (SYMM && kk >= m0 + C::BM) {
+          mbar_expect_tx(&full[s], STAGE_BYTES_T);
+          tma_load_2d(As + s * ASZ, &mapC, kk, (int)m0, &full[s], pol);
+        } else {
+          mbar_expect_tx(&full[s], STAGE_BYTES);
+          tma_load_2d(As + s * ASZ, &mapA, (SYMM || !TA) ? (int)m0 : kk,
+                      (SYMM || !TA) ? kk : (int)m0, &full[s], pol);
+        }
         tma_load_2d(Bs + s * BSZ, &mapB, TB ? (int)n0 : kk, TB ? kk : (int)n0, &full[s], pol);
       }
     }
@@ -202,11 +248,8 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
   const int mb = wm * 8 * WTM, nb = wn * 8 * WTN;
   // fragment offsets of this lane for k-step 0 (constant over the kernel)
   const int a_off = AT::idx(mb + g, t) + q.sh_a;
+  const int a_off_t = ATT::idx(mb + g, t);
   const int b_off = BT::idx(t, nb + g) + q.sh_b;
-  constexpr int A_I = AT::idx(8, 0) - AT::idx(0, 0);   // next 8-row fragment
-  constexpr int A_K = AT::idx(0, 4) - AT::idx(0, 0);   // next k-step
-  constexpr int B_J = BT::idx(0, 8) - BT::idx(0, 0);
-  constexpr int B_K = BT::idx(4, 0) - BT::idx(0, 0);
   unsigned it = 0, tq = 0;
   for (;;) {
     mbar_wait(&tq_full[tq & 1], (tq >> 1) & 1);
@@ -231,27 +274,11 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
     for (int kt = 0; kt < nk; ++kt, ++it) {
       const int s = it % NST;
       mbar_wait(&full[s], (it / NST) & 1);
-      const double* as = As + s * ASZ + a_off;
       const double* bs = Bs + s * BSZ + b_off;
-      double af[2][WTM], bf[2][WTN];
-#pragma unroll
-      for (int i = 0; i < WTM; ++i) af[0][i] = as[i * A_I];
-#pragma unroll
-      for (int j = 0; j < WTN; ++j) bf[0][j] = bs[j * B_J];
-#pragma unroll
-      for (int ks = 0; ks < TBK / 4; ++ks) {
-        const int cur = ks & 1, nx = cur ^ 1;
-        if (ks + 1 < TBK / 4) {
-#pragma unroll
-          for (int i = 0; i < WTM; ++i) af[nx][i] = as[i * A_I + (ks + 1) * A_K];
-#pragma unroll
-          for (int j = 0; j < WTN; ++j) bf[nx][j] = bs[j * B_J + (ks + 1) * B_K];
-        }
-#pragma unroll
-        for (int i = 0; i < WTM; ++i)
-#pragma unroll
-          for (int j = 0; j < WTN; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[cur][i], bf[cur][j]);
-      }
+      if (SYMM && k0 + (int64_t)kt * TBK >= m0 + C::BM)
+        ktile_mma<1, TB, C>(acc, As + s * ASZ + a_off_t, bs);
+      else
+        ktile_mma<(SYMM ? 0 : TA), TB, C>(acc, As + s * ASZ + a_off, bs);
       // Release the PREVIOUS stage: every DMMA that consumed its fragments has been issued
       // by now (they precede this k-tile's barrier wait), so its shared-memory reads are
       // done. Releasing a stage right after its own last fragment load is not safe: ptxas
@@ -371,30 +398,32 @@ unsigned long long* claim_counters() {
 }
 
 template <int TA, int TB, class C>
-constexpr size_t tma_smem_bytes() {
+constexpr size_t tma_smem_bytes() {  // (SYMM launches pass TA = 1: the larger A stage)
   return (size_t)(TATile<TA, C>::size + TBTile<TB, C>::size) * tma_stages<TA, TB, C>() *
              sizeof(double) +
          (2 * tma_stages<TA, TB, C>() + 4) * sizeof(uint64_t) + 2 * sizeof(long long);
 }
 
-template <int TA, int TB, int LOWER, class C>
+template <int TA, int TB, int LOWER, class C, int SYMM = 0>
 cudaError_t launch_tma(const GemmArgs& p, cudaStream_t st) {
   unsigned long long* ctrs = claim_counters();
   if (!ctrs) return cudaErrorMemoryAllocation;
   CUtensorMap mapA, mapB;
   const int sh_a = (reinterpret_cast<uintptr_t>(p.A) & 15) ? 1 : 0;
   const int sh_b = (reinterpret_cast<uintptr_t>(p.B) & 15) ? 1 : 0;
-  const bool okA = TA ? make_map(&mapA, p.A - sh_a, p.k + sh_a, p.m, p.lda, TPK, C::BM)
+  if (SYMM && sh_a) return cudaErrorNotSupported;
+  const bool okA = (TA && !SYMM) ? make_map(&mapA, p.A - sh_a, p.k + sh_a, p.m, p.lda, TPK, C::BM)
                       : make_map(&mapA, p.A - sh_a, p.m + sh_a, p.k, p.lda, C::SPM, TBK);
   const bool okB = TB ? make_map(&mapB, p.B - sh_b, p.n + sh_b, p.k, p.ldb, C::SPN, TBK)
                       : make_map(&mapB, p.B - sh_b, p.k + sh_b, p.n, p.ldb, TPK, C::BN);
   if (!okA || !okB) return cudaErrorNotSupported;
   CUtensorMap mapC = mapA;  // placeholder when C is not prefetched
-  const bool okC = p.beta != 0.0 && (reinterpret_cast<uintptr_t>(p.C) & 15) == 0 &&
+  if (SYMM && !make_map(&mapC, p.A, p.k, p.m, p.lda, TPK, C::BM)) return cudaErrorNotSupported;
+  const bool okC = !SYMM && p.beta != 0.0 && (reinterpret_cast<uintptr_t>(p.C) & 15) == 0 &&
                    (p.ldc & 1) == 0 && p.ldc * 8 < (1ll << 40) &&
                    make_map(&mapC, p.C, p.m, p.n, p.ldc, C::BM, C::BN);
-  auto kern = gemm_tma_kernel<TA, TB, LOWER, C>;
-  constexpr size_t sm = tma_smem_bytes<TA, TB, C>();
+  auto kern = gemm_tma_kernel<TA, TB, LOWER, C, SYMM>;
+  constexpr size_t sm = tma_smem_bytes<(SYMM ? 1 : TA), TB, C>();
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -516,6 +545,22 @@ cudaError_t gemm_tma(cudaStream_t st, bool ta, bool tb, const GemmArgs& p, bool 
     case 6: return launch_cfg<1, 1, 0>(p, st, cfg);
     default: return launch_cfg<1, 1, 1>(p, st, cfg);
   }
+}
+
+// C (m x n) = A B for a symmetric m x m A of which only the lower triangle and the 127
+// diagonals above it are read (B is m x n, column-major; the product X = A22 (V T) of the
+// band reduction, n = 64). cudaErrorNotSupported when TMA cannot address the operands.
+cudaError_t gemm_symm_lower_tma(cudaStream_t st, int64_t m, int64_t n, const double* A,
+                                int64_t lda, const double* B, int64_t ldb, double* C,
+                                int64_t ldc) {
+  if (g_gemm_tma == 0 || m <= 0 || n <= 0) return cudaErrorNotSupported;
+  if ((lda & 1) || (ldb & 1) || (reinterpret_cast<uintptr_t>(A) & 15)) return cudaErrorNotSupported;
+  if (m > INT32_MAX || n > INT32_MAX || lda * 8 >= (1ll << 40) || ldb * 8 >= (1ll << 40))
+    return cudaErrorNotSupported;
+  GemmArgs p{m, n, m, A, lda, B, ldb, C, ldc, 1.0, 0.0, 0};
+  static_assert(TC2::BM == 128 && TC3::BM == 128, "the band above the diagonal is BM - 1 wide");
+  if (n <= 64) return launch_tma<0, 0, 0, TC2, 1>(p, st);
+  return launch_tma<0, 0, 0, TC3, 1>(p, st);
 }
 
 }  // namespace em

@@ -216,6 +216,13 @@ void sy2sb(cudaStream_t st, int64_t n, double* A, int64_t lda, double* tau1, dou
            int64_t ldab) {
   const int b = B2;
   constexpr int64_t SB = 2048;  // column block of the symmetric product (band above: SB - 1)
+  // The symmetric product as ONE TMA-fed kernel (every row tile runs over the whole k
+  // range, reading left of its diagonal block as stored and below it transposed) when TMA
+  // can address A: then only SYMM_BAND diagonals above the diagonal are kept current.
+  extern int64_t g_gemm_tma;
+  const bool symm_tma = g_gemm_tma != 0 && (lda & 1) == 0 && (n & 1) == 0 &&
+                        (reinterpret_cast<uintptr_t>(A) & 15) == 0 && n >= 1024;
+  const int64_t band_up = symm_tma ? SYMM_BAND : SB - 1;
   const int sms = num_sms();
   DBuf VW((size_t)n * 2 * b, st), WV((size_t)n * 2 * b, st), VT((size_t)n * b, st);
   DBuf Gm((size_t)b * b, st), T((size_t)b * b, st), Y((size_t)b * b, st), M((size_t)b * b, st);
@@ -260,7 +267,13 @@ void sy2sb(cudaStream_t st, int64_t n, double* A, int64_t lda, double* tau1, dou
     EM_CK(gemm(st, false, false, m, p, p, 1.0, V, n, T.p, p, 0.0, VT.p, n));
     // X = A22 VT from the lower triangle plus the band of width SB above the diagonal
     // (column blocks J: X[J:] += A22[J:, J] VT[J], X[J] += A22[J+SB:, J]^T VT[J+SB:])
-    for (int64_t j = 0; j < m; j += SB) {
+    bool symm_done = false;
+    if (symm_tma) {
+      const cudaError_t e = gemm_symm_lower_tma(st, m, p, A22, lda, VT.p, n, X, n);
+      if (e != cudaSuccess) EM_CK(e);  // operands were checked above: no fallback mid-way
+      symm_done = true;
+    }
+    for (int64_t j = 0; j < m && !symm_done; j += SB) {
       const int64_t w = imin64(SB, m - j);
       EM_CK(gemm(st, false, false, m - j, p, w, 1.0, A22 + j + j * lda, lda, VT.p + j, n,
                  j == 0 ? 0.0 : 1.0, X + j, n));
@@ -276,7 +289,7 @@ void sy2sb(cudaStream_t st, int64_t n, double* A, int64_t lda, double* tau1, dou
     copy_matrix(st, false, m, p, X, n, WV.p, n);
     copy_matrix(st, false, m, p, V, n, WV.p + (size_t)p * n, n);
     EM_CK(gemm(st, false, true, m, m, 2 * p, -1.0, VW.p, n, WV.p, n, 1.0, A22, lda, true,
-               SB - 1));
+               band_up));
   }
   band_extract_kernel<<<(unsigned)n, 128, 0, st>>>(n, b, A, lda, AB, ldab);
   EM_LAUNCHED();

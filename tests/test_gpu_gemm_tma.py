@@ -138,3 +138,29 @@ def test_dgemm_tma_operands_on_odd_elements(cfg):
                         (cfg, m, n, k, ta, tb)
     finally:
         nat.check(lib.em_config(ctx, 95, 1))
+
+
+def test_dsymm_band_lower_reads_only_lower_and_band():
+    """C = A B for symmetric A from its lower triangle plus 127 diagonals above it: entries
+    further above the diagonal are poisoned with NaN and must not be read; ragged sizes,
+    the 64- and 128-column tile configurations, split-k."""
+    nat, ctx, lib = _lib()
+    rng = np.random.default_rng(9)
+    for (m, n) in ((1000, 64), (4436, 64), (2050, 33), (3000, 192), (130, 64), (6000, 64)):
+        s = rng.standard_normal((m, m))
+        a = s + s.T
+        b = rng.standard_normal((m, n))
+        r, c = np.indices((m, m))
+        ap = np.where(c - r > 127, np.nan, a)
+        lda = m + (m & 1)
+        app = np.zeros((lda, m))
+        app[:m] = ap
+        bp = np.zeros((lda, n))
+        bp[:m] = b
+        da, db = nat.device_colmajor(app), nat.device_colmajor(bp)
+        dc = nat.device_colmajor(np.full((m, n), np.nan))
+        nat.check(lib.em_dsymm_band_lower(ctx, m, n, nat.ptr(da), lda, nat.ptr(db), lda,
+                                          nat.ptr(dc), m))
+        got = nat.host_colmajor(dc, m, n)
+        ref = a @ b
+        assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max() * np.sqrt(m), (m, n)
