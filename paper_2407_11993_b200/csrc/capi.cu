@@ -203,7 +203,7 @@ int em_config(em_ctx* ctx, int key, int64_t value) {
       EM_CK(cudaMemPoolTrimTo(pool, (size_t)value));
       return EM_OK;
     }
-    if (key == 95) {  // debug: register-resident Q2 switches (q2reg.cu)
+    if (key == 94) {  // debug: register-resident Q2 switches (q2reg.cu)
       em::g_q2r_dbg = (int)value;
       return EM_OK;
     }

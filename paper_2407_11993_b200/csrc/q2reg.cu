@@ -36,7 +36,7 @@
 
 namespace em {
 
-int g_q2r_dbg = 0;  // debug key 95: bit0 VT(k) waits for C(k-1); bit1 uniform strips;
+int g_q2r_dbg = 0;  // debug key 94: bit0 VT(k) waits for C(k-1); bit1 uniform strips;
                     // bit2 synchronous Z staging loads; bit3 fences before the empty arrivals;
                     // bit4 seven consumer warps (8 warps per CTA, 255 registers)
 
@@ -44,7 +44,13 @@ namespace {
 constexpr int QB = 64;                  // sweeps per group, reflector length
 constexpr int VP = 8 * 9 * 64;          // packed V: 8 column tiles J x 9 row tiles (R = J..J+8)
 constexpr int VTP = 100 * 64;           // packed -VT: the 100 nonzero 8 x 8 tiles (R, J >= R - 8)
-constexpr int ZLD = 72;                 // staging column stride: conflict-free 16-byte reads
+constexpr int ZLD = 64;                 // staging column stride (no padding: 12 warps' buffers
+                                        // fit beside the rings); 16-byte slots XOR-swizzled
+                                        // by the column's parity for conflict-free reads
+// element (column c, row i) of a staging buffer
+__host__ __device__ __forceinline__ int zidx(int c, int i) {
+  return c * ZLD + ((((i >> 1) ^ ((c & 1) << 2)) << 1) | (i & 1));
+}
 
 __host__ __device__ __forceinline__ int64_t tasks(int64_t n, int64_t s) {
   return (n - 1 - s + QB - 1) / QB;
@@ -155,7 +161,7 @@ struct Q2RWarp {
         const int e = q * 32 + lane, c = e >> 5, i = 2 * (e & 31);
         const int64_t row = 64 * h + i, cg = c0w + c;
         const int bytes = (cg < ncols && row < n) ? (row + 1 < n ? 16 : 8) : 0;
-        cp_async16(zst + c * ZLD + i, bytes ? Z + row + cg * ldz : Z, bytes);
+        cp_async16(zst + zidx(c, i), bytes ? Z + row + cg * ldz : Z, bytes);
       }
     } else {
 #pragma unroll
@@ -164,7 +170,7 @@ struct Q2RWarp {
         const int64_t row = 64 * h + i, cg = c0w + c;
         const bool ok = row < n && cg < ncols;
         // (8-byte cp.async exists only as .ca: synchronous L2 loads instead)
-        zst[c * ZLD + i] = ok ? __ldcg(Z + row + cg * ldz) : 0.0;
+        zst[zidx(c, i)] = ok ? __ldcg(Z + row + cg * ldz) : 0.0;
       }
     }
     cp_async_commit();
@@ -174,7 +180,7 @@ struct Q2RWarp {
     __syncwarp();
 #pragma unroll
     for (int R = 0; R < 8; ++R) {
-      const double2 v = lds128(zst + gq * ZLD + 8 * R + 2 * tq);
+      const double2 v = lds128(zst + zidx(gq, 8 * R + 2 * tq));
       z[R][0] = v.x;
       z[R][1] = v.y;
     }
@@ -196,18 +202,24 @@ struct Q2RWarp {
                         double (&w)[8][2]) const {
 #pragma unroll
     for (int J = 0; J < 8; ++J) w[J][0] = w[J][1] = 0.0;
+    // fragment pairs double-buffered: the loads of dR + 1 are in flight under dR's products
+    double2 b[2][8];
+#pragma unroll
+    for (int J = 0; J < 8; ++J) b[0][J] = lds128(vs + (J * 9) * 64 + 2 * lane);
 #pragma unroll
     for (int dR = 0; dR < 9; ++dR) {
-      double2 b[8];
+      const int cur = dR & 1;
+      if (dR + 1 < 9) {
 #pragma unroll
-      for (int J = 0; J < 8; ++J) b[J] = lds128(vs + (J * 9 + dR) * 64 + 2 * lane);
+        for (int J = 0; J < 8; ++J) b[cur ^ 1][J] = lds128(vs + (J * 9 + dR + 1) * 64 + 2 * lane);
+      }
 #pragma unroll
       for (int e = 0; e < 2; ++e)
 #pragma unroll
         for (int J = 0; J < 8; ++J) {
           const int R = J + dR;
           const double a = R < 8 ? zt[R & 7][e] : zb[R & 7][e];
-          mma(w[J][0], w[J][1], a, e ? b[J].y : b[J].x);
+          mma(w[J][0], w[J][1], a, e ? b[cur][J].y : b[cur][J].x);
         }
     }
   }
@@ -216,26 +228,30 @@ struct Q2RWarp {
   // products of a group before its e = 1 ones.
   EM_DEVINL void step_c(double (&zt)[8][2], double (&zb)[8][2], const double* vts,
                         const double (&w)[8][2]) const {
+    // 16 (J, h) half-steps, fragment pairs double-buffered across them
+    double2 b[2][8];
+    auto load = [&](int step, double2(&bb)[8]) {
+      const int J = step >> 1, h = step & 1;
 #pragma unroll
-    for (int J = 0; J < 8; ++J) {
+      for (int q = 0; q < 8; ++q) {
+        const int R = 8 * h + q;
+        if (J >= vt_j0(R)) bb[q] = lds128(vts + (vt_t0(R) + J - vt_j0(R)) * 64 + 2 * lane);
+      }
+    };
+    load(0, b[0]);
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        double2 b[8];
+    for (int step = 0; step < 16; ++step) {
+      const int J = step >> 1, h = step & 1, cur = step & 1;
+      if (step + 1 < 16) load(step + 1, b[cur ^ 1]);
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           const int R = 8 * h + q;
-          if (J >= vt_j0(R)) b[q] = lds128(vts + (vt_t0(R) + J - vt_j0(R)) * 64 + 2 * lane);
+          if (J < vt_j0(R)) continue;
+          double(&c)[2] = h == 0 ? zt[q] : zb[q];
+          mma(c[0], c[1], w[J][e], e ? b[cur][q].y : b[cur][q].x);
         }
-#pragma unroll
-        for (int e = 0; e < 2; ++e)
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const int R = 8 * h + q;
-            if (J < vt_j0(R)) continue;
-            double(&c)[2] = h == 0 ? zt[q] : zb[q];
-            mma(c[0], c[1], w[J][e], e ? b[q].y : b[q].x);
-          }
-      }
     }
   }
 };
@@ -248,8 +264,22 @@ struct Q2RWarp {
 // multiple of the SM count); the ntail CTAs after them share the remaining `rem` 8-column
 // units as evenly as possible (fewer active warps each), so the last wave is short
 // instead of partly empty.
+// With NW a multiple of 4 the producer is a whole warpgroup (one active lane) that hands
+// its registers to the consumer warpgroups (setmaxnreg): the consumers run at RC registers
+// (no spills, V / VT fragments of the next step prefetched) instead of 168.
 template <int NW>
-__global__ void __launch_bounds__((NW + 1) * 32, 1) q2r_kernel(int64_t n, int64_t ncols,
+struct Q2RRegs {
+  static constexpr bool kSplit = NW % 4 == 0;
+  static constexpr int PW = kSplit ? 4 : 1;
+  static constexpr int RP = 40;
+  static constexpr int RC = kSplit ? ((65536 - 128 * RP) / (NW * 32)) / 8 * 8 > 232
+                                         ? 232
+                                         : ((65536 - 128 * RP) / (NW * 32)) / 8 * 8
+                                   : 0;
+};
+
+template <int NW>
+__global__ void __launch_bounds__((NW + Q2RRegs<NW>::PW) * 32, 1) q2r_kernel(int64_t n, int64_t ncols,
                                                                int64_t g, int64_t K,
                                                                const double* __restrict__ Vp,
                                                                const double* __restrict__ VTp,
@@ -283,8 +313,10 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) q2r_kernel(int64_t n, int64_
   }
   __syncthreads();
 
-  if (warp == NW) {  // producer
-    if (lane == 0) {
+  if (warp >= NW) {  // producer
+    if constexpr (Q2RRegs<NW>::kSplit)
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(Q2RRegs<NW>::RP));
+    if (warp == NW && lane == 0) {
       for (int64_t k = 0; k < K; ++k) {
         const int s = (int)(k & 1);
         const unsigned par = (unsigned)(((k >> 1) - 1) & 1);
@@ -300,6 +332,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) q2r_kernel(int64_t n, int64_
     }
     return;
   }
+  if constexpr (Q2RRegs<NW>::kSplit)
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(Q2RRegs<NW>::RC));
   if (warp >= nact) return;
 
   Q2RWarp<NW> W;
@@ -393,7 +427,7 @@ static void q2_apply_nw(cudaStream_t st, int64_t n, int64_t ncols, int64_t ngrou
     q2r_pack_kernel<<<(unsigned)K, 256, kPackSmem, st>>>(n, g, V2, toff, T2 + off * QB * QB,
                                                          Vp.p, VTp.p);
     EM_LAUNCHED();
-    q2r_kernel<NW><<<(unsigned)(nfull + ntail), (NW + 1) * 32, S::SMEM, st>>>(
+    q2r_kernel<NW><<<(unsigned)(nfull + ntail), (NW + Q2RRegs<NW>::PW) * 32, S::SMEM, st>>>(
         n, ncols, g, K, Vp.p, VTp.p, Z, ldz, nfull, imax64(ntail, 1), rem, g_q2r_dbg);
     EM_LAUNCHED();
     off += K;
@@ -405,8 +439,10 @@ void q2_apply_reg(cudaStream_t st, int64_t n, int64_t ncols, int64_t ngroups, co
   if (ncols <= 0 || n <= 1) return;
   if (g_q2r_dbg & 16)
     q2_apply_nw<7>(st, n, ncols, ngroups, V2, toff, T2, Z, ldz);
-  else
+  else if (g_q2r_dbg & 32)
     q2_apply_nw<8>(st, n, ncols, ngroups, V2, toff, T2, Z, ldz);
+  else
+    q2_apply_nw<12>(st, n, ncols, ngroups, V2, toff, T2, Z, ldz);
 }
 
 }  // namespace em

@@ -13,7 +13,7 @@ def main():
     mode = int(sys.argv[2]) if len(sys.argv) > 2 else 0
     dbg = int(sys.argv[3]) if len(sys.argv) > 3 else 0
     lib, ctx = nat.load_library(), nat.context()
-    nat.check(lib.em_config(ctx, 95, dbg))
+    nat.check(lib.em_config(ctx, 94, dbg))
     nat.set_two_stage_min(0)
     nat.check(lib.em_config(ctx, 97, mode))
     rng = np.random.default_rng(n)
