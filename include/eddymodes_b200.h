@@ -46,6 +46,28 @@ typedef struct em_fd_plan em_fd_plan;
  * (stream-ordered allocator) between calls; em_trim releases it, em_finalize releases it
  * and restores the pool's previous release threshold. */
 int em_init(int device, em_ctx** ctx);
+
+/* ---- multi-GPU: one process (and one context) per GPU --------------------------------
+ * The reference's distributed run is ScaLAPACK PDSYGVX over MPI ranks;
+ * here every rank calls the same em_* entry points and the library exchanges data with
+ * NCCL on the context stream (panel broadcasts and partial-product all-reduces of the
+ * band reduction, em_sygv_range with EM_SYGV_DIST). Rank 0 obtains an id
+ * (em_comm_unique_id, EM_COMM_ID_BYTES bytes), the host application hands it to the other
+ * ranks (e.g. torch.distributed broadcast), every rank calls em_comm_init_nccl.
+ * em_comm_init_callbacks installs host-supplied collectives instead (tests: several
+ * ranks on one GPU, which NCCL refuses); the library synchronises the stream, then calls
+ * them with DEVICE pointers. Collectives are issued in the same order on every rank. */
+#define EM_COMM_ID_BYTES 128
+typedef int (*em_allreduce_fn)(void* user, double* device_buf, int64_t count);
+typedef int (*em_bcast_fn)(void* user, double* device_buf, int64_t count, int root);
+int em_comm_unique_id(em_ctx* ctx, void* id);
+int em_comm_init_nccl(em_ctx* ctx, int nranks, int rank, const void* id);
+int em_comm_init_callbacks(em_ctx* ctx, int nranks, int rank, em_allreduce_fn allreduce,
+                           em_bcast_fn bcast, void* user);
+/* info[0..5] = nranks, rank, backend (0 none, 1 NCCL, 2 callbacks), all-reduces issued,
+ * broadcasts issued, bytes moved through them */
+int em_comm_info(em_ctx* ctx, int64_t* info);
+int em_comm_destroy(em_ctx* ctx);
 void em_finalize(em_ctx* ctx);
 int em_trim(em_ctx* ctx);
 /* Facts about the last call: EM_INFO_EIG_PATH = 1 one-stage (Householder sytrd), 2

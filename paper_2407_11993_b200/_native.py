@@ -42,6 +42,11 @@ SIGNATURES = {
     "em_dgemm": (_I, [_P, _I, _I, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D, _P, _I64]),
     "em_dgemm_lower": (_I, [_P, _I, _I, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D, _P, _I64,
                             _I64]),
+    "em_comm_unique_id": (_I, [_P, _P]),
+    "em_comm_init_nccl": (_I, [_P, _I, _I, _P]),
+    "em_comm_init_callbacks": (_I, [_P, _I, _I, _P, _P, _P]),
+    "em_comm_info": (_I, [_P, ctypes.POINTER(_I64)]),
+    "em_comm_destroy": (_I, [_P]),
     "em_dsymm_band_lower": (_I, [_P, _I64, _I64, _P, _I64, _P, _I64, _P, _I64]),
     "em_sym_mirror_lower": (_I, [_P, _I64, _P, _I64]),
     "em_sym_mm": (_I, [_P, _I64, _I64, _P, _I64, _P, _I64, _P, _I64]),

@@ -6,6 +6,7 @@
 #include <string>
 
 #include "common.cuh"
+#include "comm.h"
 #include "ctx.h"
 #include "gemm.h"
 #include "linalg.h"
@@ -46,6 +47,7 @@ template <typename F>
 int guarded(em_ctx* ctx, F&& f) {
   try {
     if (ctx) cudaSetDevice(ctx->device);
+    em::g_cur_ctx = ctx;  // the context whose communicator the distributed stages use
     return f();
   } catch (const em::CudaError& e) {
     if (ctx) ctx->err = std::string(cudaGetErrorString(e.code)) + " in " + e.where;
@@ -99,9 +101,56 @@ int em_init(int device, em_ctx** out) {
   return EM_OK;
 }
 
+int em_comm_unique_id(em_ctx* ctx, void* id) {
+  if (!ctx || !id) return EM_ERR_ARG;
+  return guarded(ctx, [&] {
+    em::comm_unique_id(id);
+    return EM_OK;
+  });
+}
+
+int em_comm_init_nccl(em_ctx* ctx, int nranks, int rank, const void* id) {
+  if (!ctx || !id) return EM_ERR_ARG;
+  return guarded(ctx, [&] {
+    EM_CK(cudaSetDevice(ctx->device));
+    em::comm_init_nccl(ctx, nranks, rank, id);
+    return EM_OK;
+  });
+}
+
+int em_comm_init_callbacks(em_ctx* ctx, int nranks, int rank, em_allreduce_fn allreduce,
+                           em_bcast_fn bcast, void* user) {
+  if (!ctx) return EM_ERR_ARG;
+  return guarded(ctx, [&] {
+    em::comm_init_callbacks(ctx, nranks, rank, allreduce, bcast, user);
+    return EM_OK;
+  });
+}
+
+int em_comm_info(em_ctx* ctx, int64_t* info) {
+  if (!ctx || !info) return EM_ERR_ARG;
+  const em_comm* c = ctx->comm;
+  info[0] = c ? c->nranks : 1;
+  info[1] = c ? c->rank : 0;
+  info[2] = c ? c->backend : 0;
+  info[3] = c ? c->n_allreduce : 0;
+  info[4] = c ? c->n_bcast : 0;
+  info[5] = c ? c->bytes : 0;
+  return EM_OK;
+}
+
+int em_comm_destroy(em_ctx* ctx) {
+  if (!ctx) return EM_ERR_ARG;
+  return guarded(ctx, [&] {
+    em::comm_destroy(ctx);
+    return EM_OK;
+  });
+}
+
 void em_finalize(em_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
+  em::comm_destroy(ctx);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   cudaMemPool_t pool;

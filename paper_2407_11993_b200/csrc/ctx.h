@@ -11,7 +11,9 @@
 
 #include "../../include/eddymodes_b200.h"
 
+struct em_comm;
 struct em_ctx {
+  em_comm* comm = nullptr;          // inter-GPU communicator (em_comm_init_*), else single GPU
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;

@@ -39,8 +39,19 @@ cudaError_t gemm_tma(cudaStream_t st, bool ta, bool tb, const GemmArgs& p, bool 
 // C (m x n) = A B for a symmetric A read from its lower triangle and the SYMM_BAND diagonals
 // above it (gemm_tma.cu); cudaErrorNotSupported when TMA cannot address the operands.
 constexpr int SYMM_BAND = 127;
+// Column ownership of a distributed band reduction: g ranks, this one r; 64-column blocks
+// dealt round-robin, block index = org + column / 64 (org: the operand's first column / 64).
+struct GemmOwn {
+  int g = 1, r = 0;
+  int64_t org = 0;
+};
+// own.g > 1: only the k-tiles read from owned columns are added (this rank's partial).
 cudaError_t gemm_symm_lower_tma(cudaStream_t st, int64_t m, int64_t n, const double* A,
-                                int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc);
+                                int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
+                                const GemmOwn& own = GemmOwn{});
+// The LOWER product of gemm() on the column tiles this rank owns only.
+cudaError_t gemm_lower_owned_tma(cudaStream_t st, bool ta, bool tb, const GemmArgs& p,
+                                 const GemmOwn& own);
 // C = alpha * sum_z W_z + beta * C over `splits` m x n partials (fixed order).
 void splitk_reduce(cudaStream_t st, int64_t m, int64_t n, int splits, const double* ws,
                    double alpha, double beta, double* C, int64_t ldc, int lower, int64_t diag_off);

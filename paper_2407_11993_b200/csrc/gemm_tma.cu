@@ -88,6 +88,13 @@ struct TmaGemmParams {
   int64_t tiles_m, tiles_n;
   unsigned long long* ctr;  // [0] next unit, [1] CTAs done
   int prefetch_c;           // beta != 0 and C admits a tensor map: L2-prefetch each C tile
+  // Column ownership of a distributed band reduction (own_g ranks, this one own_r; 64-column
+  // blocks dealt round-robin, block index = own_org + column / 64): a LOWER product
+  // updates only the owned column tiles (BN = 64); a SYMM product adds up only the k-tiles
+  // read from owned columns (stored reads: the k-tile's block; transposed reads: the row
+  // tile's block, BM = 64), i.e. this rank's partial of the product. own_g = 1: everything.
+  int own_g, own_r;
+  int64_t own_org;
   int sh_a, sh_b;           // operand starts 8 bytes past a 16-byte boundary: the map's base is
                             // the aligned address below it (TMA box starts must be 16-byte
                             // aligned), so the tile sits one element into its box — inside
@@ -109,7 +116,16 @@ EM_DEVINL bool unit_decode(const TmaGemmParams& q, int64_t u, int64_t& m0, int64
   const int64_t tn = (b % per_group) / gsz;
   m0 = tm * C::BM;
   n0 = tn * C::BN;
+  if (LOWER && q.own_g > 1 && (q.own_org + n0 / 64) % q.own_g != q.own_r) return false;
   return !(LOWER && m0 + C::BM - 1 + q.p.diag_off < n0);
+}
+
+// SYMM with column ownership: does this rank add k-tile kk of row tile m0?
+template <class C>
+EM_DEVINL bool ktile_owned(const TmaGemmParams& q, int64_t m0, int64_t kk) {
+  if (q.own_g <= 1) return true;
+  const int64_t col = kk >= m0 + C::BM ? m0 : kk;  // transposed reads come from columns m0..
+  return (q.own_org + col / 64) % q.own_g == q.own_r;
 }
 
 // One k-tile of the warp tile: fragments of a TA_/TB_-layout stage (pointers at this lane's
@@ -214,10 +230,12 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
       const int64_t k0 = (int64_t)z * q.kc;
       const int64_t kl = imin64(q.kc, q.p.k - k0);
       const int nk = (int)((kl + TBK - 1) / TBK);
-      for (int kt = 0; kt < nk; ++kt, ++it) {
+      for (int kt = 0; kt < nk; ++kt) {
+        const int kk = (int)(k0 + (int64_t)kt * TBK);
+        if (SYMM && !ktile_owned<C>(q, m0, kk)) continue;
         const int s = it % NST;
         mbar_wait(&empty[s], ((it / NST) & 1) ^ 1);
-        const int kk = (int)(k0 + (int64_t)kt * TBK);
+        ++it;
         if (SYMM && kk >= m0 + C::BM) {
           mbar_expect_tx(&full[s], STAGE_BYTES_T);
           tma_load_2d(As + s * ASZ, &mapC, kk, (int)m0, &full[s], pol);
@@ -271,11 +289,15 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
 #pragma unroll
       for (int j = 0; j < WTN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    for (int kt = 0; kt < nk; ++kt, ++it) {
+    int done = 0;  // k-tiles of this unit consumed so far
+    for (int kt = 0; kt < nk; ++kt) {
+      const int64_t kk = k0 + (int64_t)kt * TBK;
+      if (SYMM && !ktile_owned<C>(q, m0, kk)) continue;
       const int s = it % NST;
       mbar_wait(&full[s], (it / NST) & 1);
+      ++it;
       const double* bs = Bs + s * BSZ + b_off;
-      if (SYMM && k0 + (int64_t)kt * TBK >= m0 + C::BM)
+      if (SYMM && kk >= m0 + C::BM)
         ktile_mma<1, TB, C>(acc, As + s * ASZ + a_off_t, bs);
       else
         ktile_mma<(SYMM ? 0 : TA), TB, C>(acc, As + s * ASZ + a_off, bs);
@@ -287,10 +309,11 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
       // be overtaken by the arrive and then by the producer's next TMA write into the stage
       // (seen as wrong 16 x 64 blocks with beta != 0, tools/dbg_gemm_tma.py).
       __syncwarp();
-      if (kt > 0 && lane == 0) mbar_arrive(&empty[(it + NST - 1) % NST]);
+      if (done > 0 && lane == 0) mbar_arrive(&empty[(it + NST - 2) % NST]);
+      ++done;
     }
 
-    {
+    if (done > 0) {
       // The tile's last stage is released before the epilogue (so the producer refills the
       // whole ring under it). The barrier address carries a data dependency on every
       // accumulator, so the arrive cannot issue before the final DMMAs have delivered, i.e.
@@ -405,7 +428,10 @@ constexpr size_t tma_smem_bytes() {  // (SYMM launches pass TA = 1: the larger A
 }
 
 template <int TA, int TB, int LOWER, class C, int SYMM = 0>
-cudaError_t launch_tma(const GemmArgs& p, cudaStream_t st) {
+cudaError_t launch_tma(const GemmArgs& p, cudaStream_t st, const GemmOwn& own = GemmOwn{}) {
+  static_assert(!SYMM || C::BM == 128 || C::BM == 64, "symmetric band: BM - 1 diagonals");
+  if (own.g > 1 && ((LOWER && C::BN != 64) || (SYMM && C::BM != 64) || (!LOWER && !SYMM)))
+    return cudaErrorInvalidValue;
   unsigned long long* ctrs = claim_counters();
   if (!ctrs) return cudaErrorMemoryAllocation;
   CUtensorMap mapA, mapB;
@@ -472,6 +498,9 @@ cudaError_t launch_tma(const GemmArgs& p, cudaStream_t st) {
   q.prefetch_c = (okC && !ws) ? 1 : 0;
   q.sh_a = sh_a;
   q.sh_b = sh_b;
+  q.own_g = own.g;
+  q.own_r = own.r;
+  q.own_org = own.org;
   q.ctr = ctrs + 2 * (g_tma_launch_no.fetch_add(1, std::memory_order_relaxed) % NCTR);
   const int grid = (int)imin64((int64_t)slots, tiles * splits);
   kern<<<grid, C::THREADS, sm, st>>>(mapA, mapB, mapC, q);
@@ -490,6 +519,9 @@ cudaError_t launch_tma(const GemmArgs& p, cudaStream_t st) {
 using TC2 = TCfg<128, 64, 4, 8, 2, 4, 4, 216, 40>;
 // 128 x 128 tiles, 8 consumer warps of 32 x 64, one CTA per SM (launched at 168, then 232/40)
 using TC3 = TCfg<128, 128, 4, 8, 1, 5, 4, 232, 40>;
+// 64 x 64 tiles, 4 consumer warps of 32 x 32 and one producer warp, two CTAs per SM: the
+// row tile of a symmetric band product whose columns are owned in 64-column blocks
+using TC6 = TCfg<64, 64, 4, 4, 2, 5, 1, 0, 0>;
 // 128 x 96 tiles, 12 consumer warps of 32 x 32 and one producer warp, one CTA per SM (128)
 using TC4 = TCfg<128, 96, 4, 4, 1, 6, 1, 0, 0>;
 
@@ -552,15 +584,28 @@ cudaError_t gemm_tma(cudaStream_t st, bool ta, bool tb, const GemmArgs& p, bool 
 // band reduction, n = 64). cudaErrorNotSupported when TMA cannot address the operands.
 cudaError_t gemm_symm_lower_tma(cudaStream_t st, int64_t m, int64_t n, const double* A,
                                 int64_t lda, const double* B, int64_t ldb, double* C,
-                                int64_t ldc) {
+                                int64_t ldc, const GemmOwn& own) {
   if (g_gemm_tma == 0 || m <= 0 || n <= 0) return cudaErrorNotSupported;
   if ((lda & 1) || (ldb & 1) || (reinterpret_cast<uintptr_t>(A) & 15)) return cudaErrorNotSupported;
   if (m > INT32_MAX || n > INT32_MAX || lda * 8 >= (1ll << 40) || ldb * 8 >= (1ll << 40))
     return cudaErrorNotSupported;
   GemmArgs p{m, n, m, A, lda, B, ldb, C, ldc, 1.0, 0.0, 0};
   static_assert(TC2::BM == 128 && TC3::BM == 128, "the band above the diagonal is BM - 1 wide");
+  if (own.g > 1) return launch_tma<0, 0, 0, TC6, 1>(p, st, own);  // (64-row tiles)
   if (n <= 64) return launch_tma<0, 0, 0, TC2, 1>(p, st);
   return launch_tma<0, 0, 0, TC3, 1>(p, st);
+}
+
+// The LOWER product of gemm() restricted to the column tiles this rank owns (64-column
+// blocks, see TmaGemmParams): the trailing update of a distributed band reduction.
+cudaError_t gemm_lower_owned_tma(cudaStream_t st, bool ta, bool tb, const GemmArgs& p,
+                                 const GemmOwn& own) {
+  if ((p.lda & 1) || (p.ldb & 1)) return cudaErrorNotSupported;
+  if (p.m > INT32_MAX || p.n > INT32_MAX || p.k > INT32_MAX) return cudaErrorNotSupported;
+  if (!ta && tb) return launch_tma<0, 1, 1, TC2>(p, st, own);
+  if (!ta && !tb) return launch_tma<0, 0, 1, TC2>(p, st, own);
+  if (ta && !tb) return launch_tma<1, 0, 1, TC2>(p, st, own);
+  return launch_tma<1, 1, 1, TC2>(p, st, own);
 }
 
 }  // namespace em

@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "comm.h"
 #include "ctx.h"
 #include "gemm.h"
 #include "linalg.h"
@@ -223,6 +224,18 @@ void sy2sb(cudaStream_t st, int64_t n, double* A, int64_t lda, double* tau1, dou
   const bool symm_tma = g_gemm_tma != 0 && (lda & 1) == 0 && (n & 1) == 0 &&
                         (reinterpret_cast<uintptr_t>(A) & 15) == 0 && n >= 1024;
   const int64_t band_up = symm_tma ? SYMM_BAND : SB - 1;
+  // Distributed reduction (a communicator with G > 1 ranks on the calling context, every
+  // rank holding the same A on entry): the columns of the trailing matrix are owned in
+  // 64-column blocks dealt round-robin (global block c / 64 -> rank (c / 64) mod G). Per
+  // panel the owner of its columns factors it and broadcasts the finished columns; every
+  // rank forms V, T, V T itself, adds up the k-tiles of X = A22 (V T) that read its own
+  // columns, the partials are all-reduced, and the rank-2b update touches only owned column
+  // tiles. Each finished column block is thus valid on every rank (band extraction and the
+  // Q1 back-transform read them), everything right of the current panel only on its owner.
+  em_ctx* cctx = g_cur_ctx;
+  const int G = (symm_tma && cctx && cctx->stream == st) ? comm_size(cctx) : 1;
+  const int rk = G > 1 ? comm_rank(cctx) : 0;
+  DBuf PB(G > 1 ? (size_t)n * b + b : 0, st);  // a panel's columns (with its diagonal block) + tau
   const int sms = num_sms();
   DBuf VW((size_t)n * 2 * b, st), WV((size_t)n * 2 * b, st), VT((size_t)n * b, st);
   DBuf Gm((size_t)b * b, st), T((size_t)b * b, st), Y((size_t)b * b, st), M((size_t)b * b, st);
@@ -238,8 +251,13 @@ void sy2sb(cudaStream_t st, int64_t n, double* A, int64_t lda, double* tau1, dou
     const int p = (int)imin64(b, m);
     double* P = A + (k0 + b) + k0 * lda;
     double* A22 = A + (k0 + b) + (k0 + b) * lda;
+    const int owner = G > 1 ? (int)((k0 / b) % G) : 0;
+    GemmOwn own;
+    own.g = G;
+    own.r = rk;
+    own.org = (k0 + b) / 64;
     // panel QR
-    {
+    if (rk == owner) {
       const int64_t gmax = imax64(1, imin64(sms, (m + 15) / 16));
       const int R = (int)(((m + gmax - 1) / gmax + 7) / 8 * 8);
       const unsigned G = (unsigned)((m + R - 1) / R);
@@ -252,6 +270,20 @@ void sy2sb(cudaStream_t st, int64_t n, double* A, int64_t lda, double* tau1, dou
       else
         coop_launch((const void*)qr_panel_kernel<false>, G, 256, args,
                     (size_t)R * b * sizeof(double), st);
+    }
+    if (G > 1) {  // columns k0 .. k0 + b - 1 from their diagonal block down, and the panel's tau
+      const int64_t rows = n - k0;
+      if (rk == owner) {
+        copy_matrix(st, false, rows, b, A + k0 + k0 * lda, lda, PB.p, rows);
+        EM_CK(cudaMemcpyAsync(PB.p + rows * b, tau1 + k0, b * sizeof(double),
+                              cudaMemcpyDeviceToDevice, st));
+      }
+      comm_bcast(cctx, PB.p, rows * b + b, owner);
+      if (rk != owner) {
+        copy_matrix(st, false, rows, b, PB.p, rows, A + k0 + k0 * lda, lda);
+        EM_CK(cudaMemcpyAsync(tau1 + k0, PB.p + rows * b, b * sizeof(double),
+                              cudaMemcpyDeviceToDevice, st));
+      }
     }
     // V (m x p) into VW[:, 0:p]; T from G = V^T V
     double* V = VW.p;
@@ -269,9 +301,14 @@ void sy2sb(cudaStream_t st, int64_t n, double* A, int64_t lda, double* tau1, dou
     // (column blocks J: X[J:] += A22[J:, J] VT[J], X[J] += A22[J+SB:, J]^T VT[J+SB:])
     bool symm_done = false;
     if (symm_tma) {
-      const cudaError_t e = gemm_symm_lower_tma(st, m, p, A22, lda, VT.p, n, X, n);
+      const cudaError_t e = gemm_symm_lower_tma(st, m, p, A22, lda, VT.p, n, X, n, own);
       if (e != cudaSuccess) EM_CK(e);  // operands were checked above: no fallback mid-way
       symm_done = true;
+      if (G > 1) {  // partial products -> X (rows below m zeroed: the block is sent whole)
+        if (m < n)
+          EM_CK(cudaMemset2DAsync(X + m, n * sizeof(double), 0, (n - m) * sizeof(double), p, st));
+        comm_allreduce_sum(cctx, X, n * (int64_t)p);
+      }
     }
     for (int64_t j = 0; j < m && !symm_done; j += SB) {
       const int64_t w = imin64(SB, m - j);
@@ -288,8 +325,21 @@ void sy2sb(cudaStream_t st, int64_t n, double* A, int64_t lda, double* tau1, dou
     // the next panel's blocked product reads; 1.5x fewer flops than both triangles)
     copy_matrix(st, false, m, p, X, n, WV.p, n);
     copy_matrix(st, false, m, p, V, n, WV.p + (size_t)p * n, n);
-    EM_CK(gemm(st, false, true, m, m, 2 * p, -1.0, VW.p, n, WV.p, n, 1.0, A22, lda, true,
-               band_up));
+    if (G > 1) {
+      GemmArgs ua{m, m, 2 * p, VW.p, n, WV.p, n, A22, lda, -1.0, 1.0, band_up};
+      EM_CK(gemm_lower_owned_tma(st, false, true, ua, own));
+    } else {
+      EM_CK(gemm(st, false, true, m, m, 2 * p, -1.0, VW.p, n, WV.p, n, 1.0, A22, lda, true,
+                 band_up));
+    }
+  }
+  if (G > 1) {  // the columns right of the last panel: valid on their owner only
+    const int64_t kl = ((n - 1) / b) * b;  // = last k0 + b (or 0 when there was no panel)
+    const int owner = (int)((kl / b) % G);
+    const int64_t rows = n - kl;
+    if (rk == owner) copy_matrix(st, false, rows, rows, A + kl + kl * lda, lda, PB.p, rows);
+    comm_bcast(cctx, PB.p, rows * rows, owner);
+    if (rk != owner) copy_matrix(st, false, rows, rows, PB.p, rows, A + kl + kl * lda, lda);
   }
   band_extract_kernel<<<(unsigned)n, 128, 0, st>>>(n, b, A, lda, AB, ldab);
   EM_LAUNCHED();

@@ -32,6 +32,89 @@ from . import linalg
 from .errors import DimensionMismatch, NotPositiveDefinite
 
 
+# ---- the library's own communicator (distributed band reduction) -----------------------
+_ALLREDUCE_T = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64)
+_BCAST_T = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                            ctypes.c_int)
+_comm_keepalive: list = []
+
+
+class _DevView:
+    """Zero-copy view of `count` doubles at a device address (for torch.as_tensor)."""
+
+    def __init__(self, ptr: int, count: int):
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": "<f8",
+                                         "data": (int(ptr), False), "version": 2}
+
+
+def attach_communicator(dist, backend: str | None = None) -> dict:
+    """Give the library a communicator over the ranks of `dist` (torch.distributed), so the
+    band reduction of every eigensolve on this context is distributed (csrc/sytrd2.cu).
+
+    backend "nccl": the library's own NCCL communicator on the context stream — rank 0's
+    ncclUniqueId is handed out through torch.distributed, the data path never touches
+    torch. backend "callbacks": collectives through torch.distributed itself (gloo in the
+    tests, where several ranks share one GPU, which NCCL refuses). Default: "nccl" when
+    torch.distributed runs on NCCL, else "callbacks". Returns communicator_info()."""
+    t = nat.torch()
+    lib, ctx = nat.load_library(), nat.context()
+    world, rank = _world_rank(dist)
+    if world <= 1:
+        nat.check(lib.em_comm_destroy(ctx), "em_comm_destroy")
+        return communicator_info()
+    if backend is None:
+        backend = "nccl" if dist.get_backend() == "nccl" else "callbacks"
+    if backend == "nccl":
+        uid = ctypes.create_string_buffer(128)
+        if rank == 0:
+            nat.check(lib.em_comm_unique_id(ctx, uid), "em_comm_unique_id")
+        box = [bytes(uid.raw)]
+        dist.broadcast_object_list(box, src=0)
+        uid = ctypes.create_string_buffer(box[0], 128)
+        nat.check(lib.em_comm_init_nccl(ctx, world, rank, uid), "em_comm_init_nccl")
+    elif backend == "callbacks":
+        def _allreduce(_user, ptr, count):
+            try:
+                buf = t.as_tensor(_DevView(ptr, count), device="cuda")
+                dist.all_reduce(buf)
+                t.cuda.synchronize()
+                return 0
+            except Exception:  # noqa: BLE001 (reported through the status code)
+                return 1
+
+        def _bcast(_user, ptr, count, root):
+            try:
+                buf = t.as_tensor(_DevView(ptr, count), device="cuda")
+                dist.broadcast(buf, src=root)
+                t.cuda.synchronize()
+                return 0
+            except Exception:  # noqa: BLE001
+                return 1
+
+        cbs = (_ALLREDUCE_T(_allreduce), _BCAST_T(_bcast))
+        _comm_keepalive[:] = [cbs]
+        nat.check(lib.em_comm_init_callbacks(ctx, world, rank,
+                                             ctypes.cast(cbs[0], ctypes.c_void_p),
+                                             ctypes.cast(cbs[1], ctypes.c_void_p), None),
+                  "em_comm_init_callbacks")
+    else:
+        raise ValueError(f"unknown communicator backend {backend!r}")
+    return communicator_info()
+
+
+def detach_communicator() -> None:
+    nat.check(nat.load_library().em_comm_destroy(nat.context()), "em_comm_destroy")
+    _comm_keepalive.clear()
+
+
+def communicator_info() -> dict:
+    info = (ctypes.c_int64 * 6)()
+    nat.check(nat.load_library().em_comm_info(nat.context(), info), "em_comm_info")
+    return {"nranks": info[0], "rank": info[1],
+            "backend": ("none", "nccl", "callbacks")[info[2]], "allreduces": info[3],
+            "broadcasts": info[4], "bytes": info[5]}
+
+
 def shard_ranges(n: int, world: int) -> list[tuple[int, int]]:
     """Contiguous, balanced mode ranges [lo, hi) per rank (sizes differ by <= 1)."""
     if world < 1:
