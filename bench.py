@@ -543,9 +543,11 @@ def workload_config(args, cfg, n, world):
 
 def parallelism(args, world):
     return "single GPU" if world == 1 else (
-        f"modes sharded x{world}: eigensolve reduction + tridiagonal solve replicated, "
-        f"eigenvector back-transforms, drive/observable projections and stepping column-"
-        f"sharded, one all-reduce of partial observables per 2048-step block")
+        f"modes sharded x{world}: band reduction distributed (64-column blocks round-robin, "
+        f"panel broadcasts + all-reduced partial products over the library's NCCL "
+        f"communicator), bulge chasing + tridiagonal solve replicated, eigenvector "
+        f"back-transforms, drive/observable projections and stepping column-sharded, one "
+        f"all-reduce of partial observables per 2048-step block")
 
 
 def run_ours(args, cfg, rank, world, local_rank):
@@ -564,6 +566,11 @@ def run_ours(args, cfg, rank, world, local_rank):
         else:
             dist.init_process_group(backend)
     nat.context()
+    if world > 1:
+        # the library's own communicator: NCCL on the context stream (callbacks through
+        # torch.distributed when the ranks share a device under gloo)
+        from paper_2407_11993_b200 import parallel
+        parallel.attach_communicator(dist)
     if args.two_stage is not None:
         nat.set_two_stage_min(args.two_stage)
     if os.environ.get("EM_SYTRD_DBG"):  # A/B switch for the tridiagonalisation code paths
@@ -760,6 +767,10 @@ def run_ours(args, cfg, rank, world, local_rank):
         line.update(extra)
         print(json.dumps(line), flush=True)
     if dist:
+        from paper_2407_11993_b200 import parallel
+        if rank == 0:
+            print("communicator: " + json.dumps(parallel.communicator_info()), file=sys.stderr)
+        parallel.detach_communicator()
         dist.destroy_process_group()
 
 

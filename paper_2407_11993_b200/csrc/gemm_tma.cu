@@ -337,37 +337,55 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
     const double alpha = q.ws ? 1.0 : q.p.alpha;
     const double beta = q.ws ? 0.0 : q.p.beta;
     const bool has_beta = beta != 0.0;
-    constexpr int EB = WTN > 4 ? 1 : 2;
+    // Interior tiles (no edge, not cut by the LOWER diagonal) take a path without
+    // per-element predicates or address arithmetic, software-pipelined over the fragment
+    // rows: the C loads of row i + 1 are in flight while row i is combined and stored (the
+    // general path below spilled registers and waited on every load round trip:
+    // profiles/r02/ncu_gemm_tma.json, K = 128, beta = 1).
+    const bool interior = m0 + C::BM <= q.p.m && n0 + C::BN <= q.p.n &&
+                          (!LOWER || q.ws != nullptr || m0 + q.p.diag_off >= n0 + C::BN - 1);
+    if (interior) {
+      double* cp = Cr + (m0 + mb + g) + (n0 + nb + 2 * t) * ldc;
+      double cv[2][WTN][2];
+      if (has_beta) {
 #pragma unroll
-    for (int i2 = 0; i2 < WTM; i2 += EB) {
-      double cv[EB][WTN][2];
-      bool ok[EB][WTN][2];
+        for (int j = 0; j < WTN; ++j)
 #pragma unroll
-      for (int ii = 0; ii < EB; ++ii) {
-        const int64_t row = m0 + mb + (i2 + ii) * 8 + g;
+          for (int e = 0; e < 2; ++e) cv[0][j][e] = cp[(8 * j + e) * ldc];
+      }
+#pragma unroll
+      for (int i = 0; i < WTM; ++i) {
+        if (has_beta && i + 1 < WTM) {
+#pragma unroll
+          for (int j = 0; j < WTN; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) cv[(i + 1) & 1][j][e] = cp[8 * (i + 1) + (8 * j + e) * ldc];
+        }
 #pragma unroll
         for (int j = 0; j < WTN; ++j)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const int64_t col = n0 + nb + j * 8 + 2 * t + e;
-            ok[ii][j][e] = row < q.p.m && col < q.p.n &&
-                           !(LOWER && !q.ws && row + q.p.diag_off < col);
-            cv[ii][j][e] = (has_beta && ok[ii][j][e]) ? Cr[row + col * ldc] : 0.0;
+            const double v = alpha * acc[i][j][e];
+            cp[8 * i + (8 * j + e) * ldc] = has_beta ? fma(beta, cv[i & 1][j][e], v) : v;
           }
       }
+      continue;
+    }
 #pragma unroll
-      for (int ii = 0; ii < EB; ++ii) {
-        const int64_t row = m0 + mb + (i2 + ii) * 8 + g;
+    for (int i2 = 0; i2 < WTM; ++i2) {
+      const int64_t row = m0 + mb + i2 * 8 + g;
 #pragma unroll
-        for (int j = 0; j < WTN; ++j)
+      for (int j = 0; j < WTN; ++j)
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            if (!ok[ii][j][e]) continue;
-            const int64_t col = n0 + nb + j * 8 + 2 * t + e;
-            const double v = alpha * acc[i2 + ii][j][e];
-            Cr[row + col * ldc] = has_beta ? fma(beta, cv[ii][j][e], v) : v;
-          }
-      }
+        for (int e = 0; e < 2; ++e) {
+          const int64_t col = n0 + nb + j * 8 + 2 * t + e;
+          const bool ok = row < q.p.m && col < q.p.n &&
+                          !(LOWER && !q.ws && row + q.p.diag_off < col);
+          if (!ok) continue;
+          const double v = alpha * acc[i2][j][e];
+          double* cpe = Cr + row + col * ldc;
+          *cpe = has_beta ? fma(beta, *cpe, v) : v;
+        }
     }
   }
 }
