@@ -146,7 +146,10 @@ constexpr int kBand = 64;
 
 // stedc.cu: tridiagonal eigensolver (divide and conquer). Eigenvalues ascending in d,
 // eigenvectors in Z (n x n, ld ldz). e is destroyed.
-void stedc(cudaStream_t st, int64_t n, double* d, double* e, double* Z, int64_t ldz);
+// c0, nc: only eigenvector columns [c0, c0 + nc) are needed (nc < 0: all); the others are
+// left undefined (the root merge forms just that range)
+void stedc(cudaStream_t st, int64_t n, double* d, double* e, double* Z, int64_t ldz,
+           int64_t c0 = 0, int64_t nc = -1);
 // Eigenvalues ascending in d and Y (n x k) <- U^T Y, U never formed (O(n k) memory)
 void stedc_apply(cudaStream_t st, int64_t n, double* d, double* e, double* Y, int64_t ldy,
                  int64_t k);

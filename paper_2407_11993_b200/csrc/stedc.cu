@@ -504,12 +504,13 @@ __global__ void dc_order_kernel(const int64_t* __restrict__ moff, const int* __r
 __global__ void dc_place_kernel(const int64_t* __restrict__ moff, const int* __restrict__ mn,
                                 const MergeInfo* __restrict__ info, DcWork w,
                                 const double* __restrict__ Q, double* __restrict__ Qout,
-                                int64_t ldq) {
+                                int64_t ldq, int t0, int t1) {
   const int mi = blockIdx.z;
   const int64_t off = moff[mi];
   const int n = mn[mi];
   const int K = info[mi].K;
-  for (int t = blockIdx.y; t < n; t += gridDim.y) {
+  if (t1 > n) t1 = n;
+  for (int t = t0 + blockIdx.y; t < t1; t += gridDim.y) {
     const int p = w.perm[off + t];
     const double* src = Q + (off + ((p >= 0) ? p : K + (-1 - p))) * ldq;
     double* dst = Qout + (off + t) * ldq;
@@ -807,8 +808,17 @@ struct Node {
   int64_t n;
 };
 
-void stedc(cudaStream_t st, int64_t n, double* d, double* e, double* Z, int64_t ldz) {
+// c0, nc: the caller needs eigenvector columns [c0, c0 + nc) only (ascending order; nc < 0:
+// all). The root merge — 3/4 of the merge flops — then forms only those columns (a
+// contiguous range of the non-deflated eigenvectors, because both the secular roots and
+// the deflated values are sorted); the other columns of Z are left undefined.
+void stedc(cudaStream_t st, int64_t n, double* d, double* e, double* Z, int64_t ldz, int64_t c0,
+           int64_t nc) {
   if (n <= 0) return;
+  if (nc < 0 || c0 < 0 || c0 + nc > n) {
+    c0 = 0;
+    nc = n;
+  }
   // tree: levels[0] = root ... levels[L] = leaves
   std::vector<std::vector<Node>> levels;
   levels.push_back({Node{0, n}});
@@ -979,6 +989,25 @@ void stedc(cudaStream_t st, int64_t n, double* d, double* e, double* Z, int64_t 
       dc_gather_kernel<<<g3, 256, 0, st>>>(dmo.p, dmn.p, minfo.p, w, Qcur, Qalt, n);
       EM_LAUNCHED();
     }
+    // the final order of the merged spectrum depends on the eigenvalues only
+    dc_order_kernel<<<nm, 32, 0, st>>>(dmo.p, dmn.p, minfo.p, w, lam_nxt);
+    EM_LAUNCHED();
+    // root merge with a column range: the new eigenvectors landing in [c0, c0 + nc)
+    const bool root_range = L == 0 && nm == 1 && mnn[0] == n && nc < n;
+    int a_lo = 0, a_hi = nm == 1 ? hi[0].K : 0;
+    if (root_range) {
+      std::vector<int> hp((size_t)std::max<int64_t>(nc, 1));
+      EM_CK(cudaMemcpyAsync(hp.data(), w.perm + c0, nc * sizeof(int), cudaMemcpyDeviceToHost, st));
+      EM_CK(cudaStreamSynchronize(st));
+      a_lo = hi[0].K;
+      a_hi = 0;
+      for (int64_t t = 0; t < nc; ++t)
+        if (hp[t] >= 0) {
+          a_lo = std::min(a_lo, hp[t]);
+          a_hi = std::max(a_hi, hp[t] + 1);
+        }
+      if (a_hi < a_lo) a_lo = a_hi = 0;  // only deflated columns in the range
+    }
     // grouped GEMMs: top rows use type 1+2 columns, bottom rows type 2+3
     std::vector<GemmArgs> probs;
     int max_tiles = 1;
@@ -991,6 +1020,14 @@ void stedc(cudaStream_t st, int64_t n, double* d, double* e, double* Z, int64_t 
                    Qcur + off + off * n, n, 1.0, 0.0, 0};
       GemmArgs bot{n2, K, K - c1, Qalt + (off + n1) + (off + c1) * n, n,
                    Ub.p + (off + c1) + off * n, n, Qcur + (off + n1) + off * n, n, 1.0, 0.0, 0};
+      if (root_range) {  // columns a_lo .. a_hi - 1 of the product only
+        for (GemmArgs* g : {&top, &bot}) {
+          g->n = a_hi - a_lo;
+          g->B += (int64_t)a_lo * g->ldb;
+          g->C += (int64_t)a_lo * g->ldc;
+        }
+        if (a_hi <= a_lo) continue;
+      }
       probs.push_back(top);
       probs.push_back(bot);
       max_tiles = std::max<int>(max_tiles, (int)(((n1 + 127) / 128) * ((K + 127) / 128)));
@@ -1020,15 +1057,15 @@ void stedc(cudaStream_t st, int64_t n, double* d, double* e, double* Z, int64_t 
       }
       EM_CK(cudaStreamSynchronize(st));  // dp lifetime
     }
-    dc_order_kernel<<<nm, 32, 0, st>>>(dmo.p, dmn.p, minfo.p, w, lam_nxt);
-    EM_LAUNCHED();
     {
       dim3 g((unsigned)std::max(1, std::min((maxn + 255) / 256, 8)), (unsigned)std::min(maxn, 65535), (unsigned)nm);
       // deflated columns next to the GEMM output in Qcur, then everything placed in
       // final order into Qalt (free after the GEMM) and the roles swapped
       dc_copy_deflated_kernel<<<g, 256, 0, st>>>(dmo.p, dmn.p, minfo.p, Qalt, Qcur, n);
       EM_LAUNCHED();
-      dc_place_kernel<<<g, 256, 0, st>>>(dmo.p, dmn.p, minfo.p, w, Qcur, Qalt, n);
+      dc_place_kernel<<<g, 256, 0, st>>>(dmo.p, dmn.p, minfo.p, w, Qcur, Qalt, n,
+                                         root_range ? (int)c0 : 0,
+                                         root_range ? (int)(c0 + nc) : maxn);
       EM_LAUNCHED();
     }
     // blocks not merged at this level (leaf-sized nodes carried up) keep their data:
@@ -1045,7 +1082,7 @@ void stedc(cudaStream_t st, int64_t n, double* d, double* e, double* Z, int64_t 
     std::swap(lam_cur, lam_nxt);
   }
   // result: lam_cur (scaled), Qcur
-  if (Qcur != Z) copy_matrix(st, false, n, n, Qcur, n, Z, ldz);
+  if (Qcur != Z) copy_matrix(st, false, n, nc, Qcur + c0 * n, n, Z + c0 * ldz, ldz);
   EM_CK(cudaMemcpyAsync(d, lam_cur, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
   scale_vec_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, d, scal.p, 0);
   EM_LAUNCHED();

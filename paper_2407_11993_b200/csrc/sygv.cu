@@ -155,7 +155,7 @@ void syev_ascending(cudaStream_t st, int64_t n, double* A, int64_t lda, double* 
   } else {
     {
       Stage s(st, ST_STEDC);
-      stedc(st, n, d.p, e.p, Z, ldz);
+      stedc(st, n, d.p, e.p, Z, ldz, c0, nc);
     }
     Stage s(st, ST_ORMTR);
     ormtr_lower(st, n, nc, A, lda, tau.p, Z + c0 * ldz, ldz);

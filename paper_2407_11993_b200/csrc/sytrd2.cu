@@ -1122,7 +1122,7 @@ void syev_two_stage(cudaStream_t st, int64_t n, double* A, int64_t lda, double* 
   AB.release();
   if (!Yt) {
     Stage s(st, ST_STEDC);
-    stedc(st, n, d.p, e.p, Z, ldz);
+    stedc(st, n, d.p, e.p, Z, ldz, c0, nc);
   }
   {
     Stage s(st, ST_ORMTR);
