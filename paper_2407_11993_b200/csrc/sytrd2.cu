@@ -404,7 +404,7 @@ EM_DEVINL double smem_larfg(double* x, int L, double* v, double* red) {
   return tau;
 }
 
-__global__ void __launch_bounds__(256) sb2st_kernel(SbArgs a) {
+__global__ void __launch_bounds__(256, 2) sb2st_kernel(SbArgs a) {
   extern __shared__ double sm[];
   double* E = sm;                 // E[i*SBLD + j]: row i of block k, column j of block k-1
   double* D = E + B2 * SBLD;      // full symmetric copy of the diagonal block
@@ -429,12 +429,31 @@ __global__ void __launch_bounds__(256) sb2st_kernel(SbArgs a) {
       const int L = (int)imin64(B2, n - a0);
       // the diagonal block [a0, a0+L) is not touched by this task's off-diagonal work
       // (columns ap .. a0-1): its loads are issued together with E's, one L2 round trip
-      for (int idx = tid; idx < B2 * B2; idx += 256) {
+      // Every load of the task (16 + 16 per thread) is issued before the first value is
+      // used: one L2 round trip per task instead of one per partially unrolled batch (the
+      // loads were 40% of a task's non-waiting stall samples, profiles/r02/ncu_sb2st.json).
+      double dreg[16], ereg[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int idx = tid + 256 * u;
         const int i = idx & (B2 - 1), j = idx >> 6;
-        double val = 0.0;
-        if (i < L && j < L)
-          val = (i >= j) ? __ldcg(AB + (i - j) + (a0 + j) * ldab) : __ldcg(AB + (j - i) + (a0 + i) * ldab);
-        D[i * SBLD + j] = val;
+        const int lo = i >= j ? j : i, hi = i >= j ? i : j;  // symmetric: the lower entry
+        const double* p = AB + (hi - lo) + (a0 + lo) * ldab;
+        dreg[u] = (i < L && j < L) ? __ldcg(p) : 0.0;
+      }
+      if (k > 0) {
+        const int64_t ap = a0 - B2;
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int idx = tid + 256 * u;
+          const int i = idx & (B2 - 1), j = idx >> 6;
+          ereg[u] = (i < L) ? __ldcg(AB + (B2 + i - j) + (ap + j) * ldab) : 0.0;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int idx = tid + 256 * u;
+        D[(idx & (B2 - 1)) * SBLD + (idx >> 6)] = dreg[u];
       }
       double tau;
       if (k == 0) {
@@ -446,9 +465,10 @@ __global__ void __launch_bounds__(256) sb2st_kernel(SbArgs a) {
       } else {
         // type 2 on E = A[a0.., ap..] (element (i, j) at band offset 64 + i - j)
         const int64_t ap = a0 - B2;
-        for (int idx = tid; idx < B2 * B2; idx += 256) {
-          const int i = idx & (B2 - 1), j = idx >> 6;
-          E[i * SBLD + j] = (i < L) ? __ldcg(AB + (B2 + i - j) + (ap + j) * ldab) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int idx = tid + 256 * u;
+          E[(idx & (B2 - 1)) * SBLD + (idx >> 6)] = ereg[u];
         }
         __syncthreads();
         const double tp = tau_prev_s;
