@@ -157,14 +157,20 @@ __global__ void __launch_bounds__(256) trsv_fwd_kernel(int64_t n, const double* 
 #pragma unroll
       for (int cc = 0; cc < 16; ++cc) a[cc] = (c0 + cc < n) ? C[tx + (c0 + cc) * ldc] : 0.0;
     }
+    // the solution entry of the NEXT tile is requested together with that tile's data
+    // (blocks far behind the chain are published long ago: their poll is a plain L2 load
+    // whose latency used to be exposed once per tile — 64% of the stall samples at
+    // N = 40,000, profiles/r02/ncu_trsv_fwd_40k.json); a sentinel is re-polled when due
+    double ynext = r > 2 ? ld_poll(y + tx) : 0.0;
     for (int64_t j = 0; j + 2 < r; ++j) {
       double an[16];
+      double yv = ynext;
       if (j + 3 < r) {
         const int64_t rn = (j + 1) * TS + tx;
 #pragma unroll
         for (int cc = 0; cc < 16; ++cc) an[cc] = (c0 + cc < n) ? C[rn + (c0 + cc) * ldc] : 0.0;
+        ynext = ld_poll(y + rn);
       }
-      double yv = ld_poll(y + j * TS + tx);
       while (is_sentinel(yv)) yv = ld_poll(y + j * TS + tx);
 #pragma unroll
       for (int cc = 0; cc < 16; ++cc) acc[cc] = fma(a[cc], yv, acc[cc]);
@@ -263,15 +269,18 @@ __global__ void __launch_bounds__(256) trsv_bwd_kernel(
 #pragma unroll
       for (int cc = 0; cc < 16; ++cc) a[cc] = (rowj < n) ? C[rowj + (c0 + cc) * ldc] : 0.0;
     }
+    // (the next tile's solution entry travels with its data, as in the forward solve)
+    double xnext = nblk - 3 > r ? ld_poll(x + (nblk - 1) * TS + tx) : 0.0;
     for (int64_t j = nblk - 1; j > r + 2; --j) {
       double an[16];
+      double xv = xnext;  // rows past n are published as 0
       if (j - 1 > r + 2) {
         const int64_t rown = (j - 1) * TS + tx;
 #pragma unroll
         for (int cc = 0; cc < 16; ++cc) an[cc] = (rown < n) ? C[rown + (c0 + cc) * ldc] : 0.0;
+        xnext = ld_poll(x + rown);
       }
       const int64_t rowj = j * TS + tx;
-      double xv = ld_poll(x + rowj);  // rows past n are published as 0
       while (is_sentinel(xv)) xv = ld_poll(x + rowj);
 #pragma unroll
       for (int cc = 0; cc < 16; ++cc) acc[cc] = fma(a[cc], xv, acc[cc]);
