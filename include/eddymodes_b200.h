@@ -107,8 +107,8 @@ int em_synchronize(em_ctx* ctx);
  * (tau_max/tau_min) kappa(R)): a non-SPD L raises the same error with the same pivot,
  * after the eigensolve instead of before it. */
 #define EM_CFG_L_CERTIFICATE 5
-/* Keys 94-99 are debug switches for A/B measurements and the tests (94 Q2 kernel
- * switches; 95 TMA-fed GEMM: 0 off, 1 auto, 2 / 4 / 5 force a tile configuration; 96
+/* Keys 93-99 are debug switches for A/B measurements and the tests (93 TD1 solves: 0
+ * register tiles, 1 TMA-staged tiles; 94 Q2 kernel switches; 95 TMA-fed GEMM: 0 off, 1 auto, 2 / 4 / 5 force a tile configuration; 96
  * cp.async GEMM tile configuration; 97 Q2 back-transform form; 98 tridiagonalisation code
  * paths; 99 trim the device memory pool to `value` bytes); see capi.cu. */
 int em_config(em_ctx* ctx, int key, int64_t value);

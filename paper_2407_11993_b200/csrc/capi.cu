@@ -27,6 +27,7 @@ extern int g_symv_align_off;
 extern int64_t g_symv_keep_mb;
 extern int64_t g_gemm_cfg;
 extern int64_t g_gemm_tma;
+extern int64_t g_td1_staged;
 void stages_reset(bool on);
 void stages_level(int level);
 int stages_read(double* ms, int64_t* counts, int n);
@@ -250,6 +251,10 @@ int em_config(em_ctx* ctx, int key, int64_t value) {
       cudaMemPool_t pool;
       EM_CK(cudaDeviceGetDefaultMemPool(&pool, ctx->device));
       EM_CK(cudaMemPoolTrimTo(pool, (size_t)value));
+      return EM_OK;
+    }
+    if (key == 93) {  // debug: TD1 solves (0 register tiles, 1 TMA-staged tiles)
+      em::g_td1_staged = value;
       return EM_OK;
     }
     if (key == 94) {  // debug: register-resident Q2 switches (q2reg.cu)

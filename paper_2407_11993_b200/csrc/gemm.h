@@ -52,6 +52,10 @@ cudaError_t gemm_symm_lower_tma(cudaStream_t st, int64_t m, int64_t n, const dou
 // The LOWER product of gemm() on the column tiles this rank owns only.
 cudaError_t gemm_lower_owned_tma(cudaStream_t st, bool ta, bool tb, const GemmArgs& p,
                                  const GemmOwn& own);
+// 2-D TMA tensor map (a CUtensorMap at `map`) over a column-major operand; false when TMA
+// cannot address it (base not 16-byte aligned, odd leading dimension, extents past int32).
+bool tma_map_2d(void* map, const double* base, int64_t inner, int64_t outer, int64_t ld,
+                int box_inner, int box_outer);
 // C = alpha * sum_z W_z + beta * C over `splits` m x n partials (fixed order).
 void splitk_reduce(cudaStream_t st, int64_t m, int64_t n, int splits, const double* ws,
                    double alpha, double beta, double* C, int64_t ldc, int lower, int64_t diag_off);

@@ -597,6 +597,16 @@ cudaError_t gemm_tma(cudaStream_t st, bool ta, bool tb, const GemmArgs& p, bool 
   }
 }
 
+// 2-D tensor map over a column-major operand (shared with td1.cu): `map` points at a
+// CUtensorMap; inner = contiguous extent, outer = columns of stride ld doubles.
+bool tma_map_2d(void* map, const double* base, int64_t inner, int64_t outer, int64_t ld,
+                int box_inner, int box_outer) {
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || (ld & 1) || inner <= 0 || outer <= 0 ||
+      inner > INT32_MAX || outer > INT32_MAX || ld * 8 >= (1ll << 40))
+    return false;
+  return make_map(static_cast<CUtensorMap*>(map), base, inner, outer, ld, box_inner, box_outer);
+}
+
 // C (m x n) = A B for a symmetric m x m A of which only the lower triangle and the 127
 // diagonals above it are read (B is m x n, column-major; the product X = A22 (V T) of the
 // band reduction, n = 64). cudaErrorNotSupported when TMA cannot address the operands.

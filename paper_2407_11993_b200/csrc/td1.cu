@@ -24,6 +24,7 @@
 #include "gemm.h"
 #include "linalg.h"
 #include "plans.h"
+#include "symv_tma.cuh"
 
 #include <vector>
 
@@ -38,6 +39,8 @@ struct em_td1_plan {
   em::Csr Rs;          // R as CSR when it is sparse (the stencil): R I is an SpMV
   bool r_sparse = false;
   em::DArr<unsigned int>* counters = nullptr;
+  alignas(64) unsigned char cmap[128] = {};  // CUtensorMap over the factor (TMA-staged solves)
+  bool tma_ok = false;
   int n_obs = 0;
   em::DBuf Cobs, D;
   ~em_td1_plan() { delete counters; }
@@ -46,6 +49,7 @@ struct em_td1_plan {
 namespace em {
 
 constexpr int TS = 64;  // triangular-solve block
+int64_t g_td1_staged = 1;  // em_config debug key 93: 0 = register-tile solves, 1 = TMA-staged
 
 __global__ void td1_z_kernel(int64_t n, const double* __restrict__ L, int64_t ldl,
                              const double* __restrict__ R, int64_t ldr, double dt_theta,
@@ -115,6 +119,129 @@ EM_DEVINL void poll16(const double* p, double (&v)[16]) {
   }
 }
 
+// ---- TMA-staged tile stream (STG = 1) -----------------------------------------------------
+// The factor tiles of a block row do not depend on the solution, only their USE does: a
+// producer warp streams the row's 64 x 64 tiles with cp.async.bulk.tensor into a ring of
+// TD1_NST shared-memory stages (192 KB in flight per SM, against two register tiles = 64 KB
+// in the register form, whose 214 registers allow one CTA per SM), the 8 consumer warps
+// wait on a stage, take their solution entry and accumulate from shared memory. The
+// producer also claims the block rows (in order) and hands them to the consumers through a
+// two-slot queue; consumer-wide barriers are the named barrier 1 (256 threads).
+constexpr int TD1_NST = 6;
+constexpr int TD1_TILE = TS * TS;  // doubles
+constexpr size_t TD1_SMEM = (size_t)TD1_NST * TD1_TILE * sizeof(double) + 128;
+
+struct Td1Ring {
+  double* tiles;
+  uint64_t* full;      // [TD1_NST]
+  uint64_t* empty;     // [TD1_NST]
+  uint64_t* tq_full;   // [2]
+  uint64_t* tq_empty;  // [2]
+  long long* tq_val;   // [2]
+};
+
+template <int STG>
+EM_DEVINL void csync() {
+  if constexpr (STG)
+    asm volatile("bar.sync 1, 256;\n" ::: "memory");
+  else
+    __syncthreads();
+}
+
+EM_DEVINL Td1Ring td1_ring_init(double* dyn, uint64_t* bars) {
+  Td1Ring R{dyn, bars, bars + TD1_NST, bars + 2 * TD1_NST, bars + 2 * TD1_NST + 2,
+            reinterpret_cast<long long*>(bars + 2 * TD1_NST + 4)};
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < TD1_NST; ++s) {
+      mbar_init(&R.full[s], 1);
+      mbar_init(&R.empty[s], 8);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&R.tq_full[s], 1);
+      mbar_init(&R.tq_empty[s], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  return R;
+}
+
+// Producer (one lane): claims block rows from `counter` (forward: ascending, backward:
+// descending) and streams tiles (j, r) of each row — forward j = 0 .. r-3, backward
+// j = nblk-1 .. r+3 — as boxes {64 rows at 64 j, 64 columns at 64 r} of the factor.
+template <int BWD>
+EM_DEVINL void td1_producer(const CUtensorMap* map, const Td1Ring& R, int64_t nblk,
+                            unsigned int* counter) {
+  const uint64_t pol = pol_evict_first();
+  unsigned it = 0, tq = 0;
+  for (;;) {
+    const int64_t c = (int64_t)atomicAdd(counter, 1u);
+    const int64_t r = BWD ? nblk - 1 - c : c;
+    const bool done = BWD ? r < 0 : r >= nblk;
+    mbar_wait(&R.tq_empty[tq & 1], ((tq >> 1) & 1) ^ 1);
+    R.tq_val[tq & 1] = done ? -1ll : (long long)r;
+    mbar_arrive(&R.tq_full[tq & 1]);
+    ++tq;
+    if (done) return;
+    const int64_t j0 = BWD ? nblk - 1 : 0, cnt = BWD ? nblk - 3 - r : r - 2;
+    for (int64_t q = 0; q < cnt; ++q, ++it) {
+      const int64_t j = BWD ? j0 - q : j0 + q;
+      const int s = it % TD1_NST;
+      mbar_wait(&R.empty[s], ((it / TD1_NST) & 1) ^ 1);
+      mbar_expect_tx(&R.full[s], TD1_TILE * sizeof(double));
+      tma_load_2d(R.tiles + s * TD1_TILE, map, (int)(j * TS), (int)(r * TS), &R.full[s], pol);
+    }
+  }
+}
+
+// Consumers: next block row from the queue (-1: none left).
+EM_DEVINL int64_t td1_next_row(const Td1Ring& R, unsigned& tq, int lane) {
+  mbar_wait(&R.tq_full[tq & 1], (tq >> 1) & 1);
+  const long long r = R.tq_val[tq & 1];
+  __syncwarp();
+  if (lane == 0) mbar_arrive(&R.tq_empty[tq & 1]);
+  ++tq;
+  return (int64_t)r;
+}
+
+// Consumers: acc[cc] += tile[ty*16 + cc][tx] * v for the cnt tiles of a row; the solution
+// entry of tile q is sol[(BWD ? j0 - q : j0 + q) * TS + tx], polled past the sentinel.
+// A stage is released one tile late (after the next stage's wait: every FMA that read it
+// has issued, so its shared-memory loads are done — see gemm_tma.cu), the row's last stage
+// behind a data dependency on the accumulators.
+template <int BWD>
+EM_DEVINL void td1_stream(const Td1Ring& R, unsigned& it, int64_t j0, int64_t cnt,
+                          const double* sol, int tx, int ty, int lane, double (&acc)[16]) {
+  if (cnt <= 0) return;
+  double vnext = ld_poll(sol + j0 * TS + tx);
+  for (int64_t q = 0; q < cnt; ++q) {
+    const int64_t j = BWD ? j0 - q : j0 + q;
+    const int s = it % TD1_NST;
+    mbar_wait(&R.full[s], (it / TD1_NST) & 1);
+    ++it;
+    double v = vnext;
+    if (q + 1 < cnt) vnext = ld_poll(sol + (BWD ? j - 1 : j + 1) * TS + tx);
+    const double* t = R.tiles + s * TD1_TILE + (ty * 16) * TS + tx;
+    double a[16];
+#pragma unroll
+    for (int cc = 0; cc < 16; ++cc) a[cc] = t[cc * TS];
+    while (is_sentinel(v)) v = ld_poll(sol + j * TS + tx);
+#pragma unroll
+    for (int cc = 0; cc < 16; ++cc) acc[cc] = fma(a[cc], v, acc[cc]);
+    __syncwarp();
+    if (q > 0 && lane == 0) mbar_arrive(&R.empty[(it + TD1_NST - 2) % TD1_NST]);
+  }
+  double dep = 0.0;
+#pragma unroll
+  for (int cc = 0; cc < 16; ++cc) dep += acc[cc];
+  const unsigned never = __double2hiint(dep) == 0x7ff00001 ? 8u : 0u;
+  __syncwarp();
+  if (lane == 0)
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(
+                     smem_u32(&R.empty[(it + TD1_NST - 1) % TD1_NST]) + never)
+                 : "memory");
+}
+
 // Forward solve C y = b, C lower (col-major, ld ldc; its upper triangle holds the
 // mirror C^T, so a block row of C is read as a block column). Block rows claimed in order.
 // y_r = D_r (b_r - sum_{j < r-2} C_rj y_j) - E2_r y_{r-2} - E_r y_{r-1} with
@@ -122,26 +249,42 @@ EM_DEVINL void poll16(const double* p, double (&v)[16]) {
 // product wait only on blocks up to r-3, so they finish two steps ahead of the chain,
 // whose step per block is: see y_{r-1}, one product, publish y_r. y must hold the
 // sentinel on entry (td1_pre_kernel).
-__global__ void __launch_bounds__(256) trsv_fwd_kernel(int64_t n, const double* __restrict__ C,
-                                                          int64_t ldc,
-                                                          const double* __restrict__ Dinv,
-                                                          const double* __restrict__ Ef,
-                                                          const double* __restrict__ Ef2,
-                                                          const double* __restrict__ b,
-                                                          double* __restrict__ y,
-                                                          unsigned int* counter) {
+template <int STG>
+__global__ void __launch_bounds__(STG ? 288 : 256) trsv_fwd_kernel(
+    const __grid_constant__ CUtensorMap cmap, int64_t n, const double* __restrict__ C,
+    int64_t ldc, const double* __restrict__ Dinv, const double* __restrict__ Ef,
+    const double* __restrict__ Ef2, const double* __restrict__ b, double* __restrict__ y,
+    unsigned int* counter) {
+  extern __shared__ __align__(128) double dyn[];
+  __shared__ uint64_t bars[2 * TD1_NST + 6];
   __shared__ int64_t rblk;
   __shared__ double red[4][TS];
   __shared__ double red8[8][16];
   __shared__ double part[TS];
-  const int tid = threadIdx.x, tx = tid & 63, ty = tid >> 6, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, tx = tid & 63, ty = (tid >> 6) & 3, lane = tid & 31, warp = tid >> 5;
   const int64_t nblk = (n + TS - 1) / TS;
+  Td1Ring R{};
+  unsigned it = 0, tq = 0;
+  if constexpr (STG) {
+    R = td1_ring_init(dyn, bars);
+    if (warp == 8) {
+      if (lane == 0) td1_producer<0>(&cmap, R, nblk, counter);
+      return;
+    }
+  }
   while (true) {
-    __syncthreads();
-    if (tid == 0) rblk = atomicAdd(counter, 1u);
-    __syncthreads();
-    const int64_t r = rblk;
-    if (r >= nblk) break;
+    int64_t r;
+    if constexpr (STG) {
+      csync<STG>();  // the previous row's readers of the reduction buffers are done
+      r = td1_next_row(R, tq, lane);
+      if (r < 0) break;
+    } else {
+      __syncthreads();
+      if (tid == 0) rblk = atomicAdd(counter, 1u);
+      __syncthreads();
+      r = rblk;
+      if (r >= nblk) break;
+    }
     const int64_t r0 = r * TS;
     const double bb = (tid < TS && r0 + tid < n) ? b[r0 + tid] : 0.0;
     // tiles j <= r - 3, read from the mirrored upper triangle (Cm[j0 + b, r0 + a] =
@@ -151,31 +294,35 @@ __global__ void __launch_bounds__(256) trsv_fwd_kernel(int64_t n, const double* 
     double acc[16];
 #pragma unroll
     for (int cc = 0; cc < 16; ++cc) acc[cc] = 0.0;
-    const int64_t c0 = r0 + ty * 16;
-    double a[16];
-    if (r > 2) {
-#pragma unroll
-      for (int cc = 0; cc < 16; ++cc) a[cc] = (c0 + cc < n) ? C[tx + (c0 + cc) * ldc] : 0.0;
-    }
-    // the solution entry of the NEXT tile is requested together with that tile's data
-    // (blocks far behind the chain are published long ago: their poll is a plain L2 load
-    // whose latency used to be exposed once per tile — 64% of the stall samples at
-    // N = 40,000, profiles/r02/ncu_trsv_fwd_40k.json); a sentinel is re-polled when due
-    double ynext = r > 2 ? ld_poll(y + tx) : 0.0;
-    for (int64_t j = 0; j + 2 < r; ++j) {
-      double an[16];
-      double yv = ynext;
-      if (j + 3 < r) {
-        const int64_t rn = (j + 1) * TS + tx;
-#pragma unroll
-        for (int cc = 0; cc < 16; ++cc) an[cc] = (c0 + cc < n) ? C[rn + (c0 + cc) * ldc] : 0.0;
-        ynext = ld_poll(y + rn);
+    if constexpr (STG) {
+      td1_stream<0>(R, it, 0, r - 2, y, tx, ty, lane, acc);
+    } else {
+      const int64_t c0 = r0 + ty * 16;
+      double a[16];
+      if (r > 2) {
+  #pragma unroll
+        for (int cc = 0; cc < 16; ++cc) a[cc] = (c0 + cc < n) ? C[tx + (c0 + cc) * ldc] : 0.0;
       }
-      while (is_sentinel(yv)) yv = ld_poll(y + j * TS + tx);
-#pragma unroll
-      for (int cc = 0; cc < 16; ++cc) acc[cc] = fma(a[cc], yv, acc[cc]);
-#pragma unroll
-      for (int cc = 0; cc < 16; ++cc) a[cc] = an[cc];
+      // the solution entry of the NEXT tile is requested together with that tile's data
+      // (blocks far behind the chain are published long ago: their poll is a plain L2 load
+      // whose latency used to be exposed once per tile — 64% of the stall samples at
+      // N = 40,000, profiles/r02/ncu_trsv_fwd_40k.json); a sentinel is re-polled when due
+      double ynext = r > 2 ? ld_poll(y + tx) : 0.0;
+      for (int64_t j = 0; j + 2 < r; ++j) {
+        double an[16];
+        double yv = ynext;
+        if (j + 3 < r) {
+          const int64_t rn = (j + 1) * TS + tx;
+  #pragma unroll
+          for (int cc = 0; cc < 16; ++cc) an[cc] = (c0 + cc < n) ? C[rn + (c0 + cc) * ldc] : 0.0;
+          ynext = ld_poll(y + rn);
+        }
+        while (is_sentinel(yv)) yv = ld_poll(y + j * TS + tx);
+  #pragma unroll
+        for (int cc = 0; cc < 16; ++cc) acc[cc] = fma(a[cc], yv, acc[cc]);
+  #pragma unroll
+        for (int cc = 0; cc < 16; ++cc) a[cc] = an[cc];
+      }
     }
     // reduce acc[cc] over the 64 columns (tx): warp shuffle, then the two warps per ty
 #pragma unroll
@@ -184,19 +331,19 @@ __global__ void __launch_bounds__(256) trsv_fwd_kernel(int64_t n, const double* 
 #pragma unroll
       for (int cc = 0; cc < 16; ++cc) red8[warp][cc] = acc[cc];
     }
-    __syncthreads();
+    csync<STG>();
     if (tid < TS) {
       const int gq = tid >> 4, cc = tid & 15;  // row tid = gq*16 + cc (warps 2gq, 2gq+1)
       part[tid] = bb - (red8[2 * gq][cc] + red8[2 * gq + 1][cc]);
     }
-    __syncthreads();
+    csync<STG>();
     // p_r = D_r part (off the chain)
     const double* D = Dinv + r * TS * TS;
     double s = 0.0;
 #pragma unroll
     for (int cc = 0; cc < 16; ++cc) s = fma(D[tx + (ty * 16 + cc) * TS], part[ty * 16 + cc], s);
     red[ty][tx] = s;
-    __syncthreads();
+    csync<STG>();
     double pr = 0.0;
     if (tid < TS) pr = red[0][tid] + red[1][tid] + red[2][tid] + red[3][tid];
     // the chain operands (loaded while y_{r-2}, y_{r-1} are still on their way)
@@ -222,9 +369,9 @@ __global__ void __launch_bounds__(256) trsv_fwd_kernel(int64_t n, const double* 
 #pragma unroll
       for (int cc = 0; cc < 16; ++cc) se = fma(ev[cc], yv[cc], se);
     }
-    __syncthreads();  // red: the p_r readers are done
+    csync<STG>();  // red: the p_r readers are done
     red[ty][tx] = se;
-    __syncthreads();
+    csync<STG>();
     if (tid < TS) {
       // rows past n (last block) publish 0 so the pollers of a full 16-entry group finish
       const double v = r0 + tid < n
@@ -239,23 +386,42 @@ __global__ void __launch_bounds__(256) trsv_fwd_kernel(int64_t n, const double* 
 // x_r = DT_r (y_r - sum_{j > r+2} C_jr^T x_j) - F2_r x_{r+2} - F_r x_{r+1},
 // F_r = DT_r C_{r+1,r}^T, F2_r = DT_r C_{r+2,r}^T precomputed (DT_r = D_r^T): one 64 x 64
 // product on the dependency chain. x must hold the sentinel on entry.
-__global__ void __launch_bounds__(256) trsv_bwd_kernel(
-    int64_t n, const double* __restrict__ C, int64_t ldc, const double* __restrict__ Dinv,
-    const double* __restrict__ Fb, const double* __restrict__ Fb2, const double* __restrict__ y,
-    double* __restrict__ x, double* __restrict__ I, double* __restrict__ Icap,
-    unsigned int* counter) {
+template <int STG>
+__global__ void __launch_bounds__(STG ? 288 : 256) trsv_bwd_kernel(
+    const __grid_constant__ CUtensorMap cmap, int64_t n, const double* __restrict__ C,
+    int64_t ldc, const double* __restrict__ Dinv, const double* __restrict__ Fb,
+    const double* __restrict__ Fb2, const double* __restrict__ y, double* __restrict__ x,
+    double* __restrict__ I, double* __restrict__ Icap, unsigned int* counter) {
+  extern __shared__ __align__(128) double dyn[];
+  __shared__ uint64_t bars[2 * TD1_NST + 6];
   __shared__ int64_t rblk;
   __shared__ double red[8][TS];
   __shared__ double part[TS];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int tx = tid & 63, ty = tid >> 6;
+  const int tx = tid & 63, ty = (tid >> 6) & 3;
   const int64_t nblk = (n + TS - 1) / TS;
+  Td1Ring R{};
+  unsigned it = 0, tq = 0;
+  if constexpr (STG) {
+    R = td1_ring_init(dyn, bars);
+    if (warp == 8) {
+      if (lane == 0) td1_producer<1>(&cmap, R, nblk, counter);
+      return;
+    }
+  }
   while (true) {
-    __syncthreads();
-    if (tid == 0) rblk = nblk - 1 - (int64_t)atomicAdd(counter, 1u);
-    __syncthreads();
-    const int64_t r = rblk;
-    if (r < 0) break;
+    int64_t r;
+    if constexpr (STG) {
+      csync<STG>();  // the previous row's readers of the reduction buffers are done
+      r = td1_next_row(R, tq, lane);
+      if (r < 0) break;
+    } else {
+      __syncthreads();
+      if (tid == 0) rblk = nblk - 1 - (int64_t)atomicAdd(counter, 1u);
+      __syncthreads();
+      r = rblk;
+      if (r < 0) break;
+    }
     const int64_t r0 = r * TS;
     double acc[16];
 #pragma unroll
@@ -263,29 +429,33 @@ __global__ void __launch_bounds__(256) trsv_bwd_kernel(
     // tiles (j, r), j = nblk-1 .. r+3; tile j-1 is prefetched before waiting for block j
     const int64_t c0 = r0 + ty * 16;
     const double yr = (tid < TS && r0 + tid < n) ? y[r0 + tid] : 0.0;
-    double a[16];
-    if (nblk - 3 > r) {
-      const int64_t rowj = (nblk - 1) * TS + tx;
-#pragma unroll
-      for (int cc = 0; cc < 16; ++cc) a[cc] = (rowj < n) ? C[rowj + (c0 + cc) * ldc] : 0.0;
-    }
-    // (the next tile's solution entry travels with its data, as in the forward solve)
-    double xnext = nblk - 3 > r ? ld_poll(x + (nblk - 1) * TS + tx) : 0.0;
-    for (int64_t j = nblk - 1; j > r + 2; --j) {
-      double an[16];
-      double xv = xnext;  // rows past n are published as 0
-      if (j - 1 > r + 2) {
-        const int64_t rown = (j - 1) * TS + tx;
-#pragma unroll
-        for (int cc = 0; cc < 16; ++cc) an[cc] = (rown < n) ? C[rown + (c0 + cc) * ldc] : 0.0;
-        xnext = ld_poll(x + rown);
+    if constexpr (STG) {
+      td1_stream<1>(R, it, nblk - 1, nblk - 3 - r, x, tx, ty, lane, acc);
+    } else {
+      double a[16];
+      if (nblk - 3 > r) {
+        const int64_t rowj = (nblk - 1) * TS + tx;
+  #pragma unroll
+        for (int cc = 0; cc < 16; ++cc) a[cc] = (rowj < n) ? C[rowj + (c0 + cc) * ldc] : 0.0;
       }
-      const int64_t rowj = j * TS + tx;
-      while (is_sentinel(xv)) xv = ld_poll(x + rowj);
-#pragma unroll
-      for (int cc = 0; cc < 16; ++cc) acc[cc] = fma(a[cc], xv, acc[cc]);
-#pragma unroll
-      for (int cc = 0; cc < 16; ++cc) a[cc] = an[cc];
+      // (the next tile's solution entry travels with its data, as in the forward solve)
+      double xnext = nblk - 3 > r ? ld_poll(x + (nblk - 1) * TS + tx) : 0.0;
+      for (int64_t j = nblk - 1; j > r + 2; --j) {
+        double an[16];
+        double xv = xnext;  // rows past n are published as 0
+        if (j - 1 > r + 2) {
+          const int64_t rown = (j - 1) * TS + tx;
+  #pragma unroll
+          for (int cc = 0; cc < 16; ++cc) an[cc] = (rown < n) ? C[rown + (c0 + cc) * ldc] : 0.0;
+          xnext = ld_poll(x + rown);
+        }
+        const int64_t rowj = j * TS + tx;
+        while (is_sentinel(xv)) xv = ld_poll(x + rowj);
+  #pragma unroll
+        for (int cc = 0; cc < 16; ++cc) acc[cc] = fma(a[cc], xv, acc[cc]);
+  #pragma unroll
+        for (int cc = 0; cc < 16; ++cc) a[cc] = an[cc];
+      }
     }
     const bool has_next = r + 1 < nblk, has_next2 = r + 2 < nblk;
     // reduce acc[cc] over the 64 rows (tx): warp shuffle, then the two warps per ty
@@ -295,20 +465,20 @@ __global__ void __launch_bounds__(256) trsv_bwd_kernel(
 #pragma unroll
       for (int cc = 0; cc < 16; ++cc) red[warp][cc] = acc[cc];
     }
-    __syncthreads();
+    csync<STG>();
     if (tid < TS) {
       const int g = tid >> 4, cc = tid & 15;  // column tid = g*16 + cc belongs to ty = g (warps 2g, 2g+1)
       const double sumc = red[2 * g][cc] + red[2 * g + 1][cc];
       part[tid] = yr - sumc;
     }
-    __syncthreads();
+    csync<STG>();
     // p_r = DT_r part with the pre-transposed block (coalesced), off the chain
     const double* D = Dinv + r * TS * TS;
     double s = 0.0;
 #pragma unroll
     for (int cc = 0; cc < 16; ++cc) s = fma(D[tx + (ty * 16 + cc) * TS], part[ty * 16 + cc], s);
     red[ty][tx] = s;
-    __syncthreads();
+    csync<STG>();
     double pr = 0.0;
     if (tid < TS) pr = red[0][tid] + red[1][tid] + red[2][tid] + red[3][tid];
     const double* Fr = Fb + r * TS * TS;
@@ -333,9 +503,9 @@ __global__ void __launch_bounds__(256) trsv_bwd_kernel(
 #pragma unroll
       for (int cc = 0; cc < 16; ++cc) sf = fma(fv[cc], xv2[cc], sf);
     }
-    __syncthreads();  // red: the p_r readers are done
+    csync<STG>();  // red: the p_r readers are done
     red[ty][tx] = sf;
-    __syncthreads();
+    csync<STG>();
     if (tid < TS) {
       if (r0 + tid < n) {
         const double xv = pr - ((red[0][tid] + red[1][tid]) + (red[2][tid] + red[3][tid]));
@@ -495,6 +665,8 @@ int64_t td1_plan_init(em_td1_plan* P, const double* L, int64_t ldl, const double
   P->y.alloc((size_t)nblk * TS, st);  // padded to whole blocks: pollers read full groups
   P->x.alloc((size_t)nblk * TS, st);
   P->counters = new DArr<unsigned int>(2, st);
+  // tiles of the factor (with its mirror in the upper triangle) as TMA boxes of 64 x 64
+  P->tma_ok = tma_map_2d(P->cmap, P->Cp, n, n, P->ldc, TS, TS);
   return -1;
 }
 
@@ -531,16 +703,40 @@ static void td1_solve_step(em_td1_plan* P, double* I, double* Icap_col, const do
     if (!fused_r) symv_lower(st, n, -P->dt, P->R.p, n, I, 1.0, P->b.p, P->work.p);
   }
   const int grid = (int)imin64(nblk, 2 * num_sms());
+  const CUtensorMap& cmap = *reinterpret_cast<const CUtensorMap*>(P->cmap);
+  const bool staged = P->tma_ok && g_td1_staged != 0;
+  if (staged) {
+    static bool configured = false;
+    if (!configured) {
+      EM_CK(cudaFuncSetAttribute(trsv_fwd_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)TD1_SMEM));
+      EM_CK(cudaFuncSetAttribute(trsv_bwd_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)TD1_SMEM));
+      configured = true;
+    }
+  }
+  const int grid_s = (int)imin64(nblk, (int64_t)num_sms());
   {
     Stage s(st, ST_TD1_FWD);
-    trsv_fwd_kernel<<<grid, 256, 0, st>>>(n, P->Cp, P->ldc, P->Dinv.p, P->Ef.p, P->Ef2.p, P->b.p,
-                                          P->y.p, P->counters->p);
+    if (staged)
+      trsv_fwd_kernel<1><<<grid_s, 288, TD1_SMEM, st>>>(cmap, n, P->Cp, P->ldc, P->Dinv.p,
+                                                        P->Ef.p, P->Ef2.p, P->b.p, P->y.p,
+                                                        P->counters->p);
+    else
+      trsv_fwd_kernel<0><<<grid, 256, 0, st>>>(cmap, n, P->Cp, P->ldc, P->Dinv.p, P->Ef.p,
+                                               P->Ef2.p, P->b.p, P->y.p, P->counters->p);
     EM_LAUNCHED();
   }
   {
     Stage s(st, ST_TD1_BWD);
-    trsv_bwd_kernel<<<grid, 256, 0, st>>>(n, P->Cp, P->ldc, P->DinvT.p, P->Fb.p, P->Fb2.p, P->y.p,
-                                          P->x.p, I, Icap_col, P->counters->p + 1);
+    if (staged)
+      trsv_bwd_kernel<1><<<grid_s, 288, TD1_SMEM, st>>>(cmap, n, P->Cp, P->ldc, P->DinvT.p,
+                                                        P->Fb.p, P->Fb2.p, P->y.p, P->x.p, I,
+                                                        Icap_col, P->counters->p + 1);
+    else
+      trsv_bwd_kernel<0><<<grid, 256, 0, st>>>(cmap, n, P->Cp, P->ldc, P->DinvT.p, P->Fb.p,
+                                               P->Fb2.p, P->y.p, P->x.p, I, Icap_col,
+                                               P->counters->p + 1);
     EM_LAUNCHED();
   }
 }
