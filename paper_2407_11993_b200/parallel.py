@@ -115,6 +115,33 @@ def communicator_info() -> dict:
             "broadcasts": info[4], "bytes": info[5]}
 
 
+BAND_BLOCK = 64  # columns per ownership block of the distributed band reduction (= its band)
+
+
+def band_block_owner(col: int, world: int) -> int:
+    """Rank owning global column `col` of the trailing matrix in the distributed band
+    reduction (csrc/sytrd2.cu): 64-column blocks dealt round-robin."""
+    if world < 1 or col < 0:
+        raise ValueError("world size must be >= 1 and the column non-negative")
+    return (col // BAND_BLOCK) % world
+
+
+def band_reduction_collectives(n: int, world: int) -> dict:
+    """Collectives the distributed band reduction of an order-n matrix issues per eigensolve
+    (what communicator_info() counts): one broadcast per 64-column panel (its finished
+    columns from the diagonal block down, plus tau) and one for the columns right of the
+    last panel; one all-reduce of the n x 64 partial symmetric product per panel."""
+    if world <= 1 or n <= BAND_BLOCK:
+        return {"broadcasts": 0, "allreduces": 0, "bytes": 0}
+    panels = (n - 1) // BAND_BLOCK
+    last = panels * BAND_BLOCK                      # first column right of the last panel
+    bcast = sum((n - k * BAND_BLOCK) * BAND_BLOCK + BAND_BLOCK for k in range(panels))
+    bcast += (n - last) ** 2
+    widths = [min(BAND_BLOCK, n - (k + 1) * BAND_BLOCK) for k in range(panels)]
+    allred = sum(n * w for w in widths)
+    return {"broadcasts": panels + 1, "allreduces": panels, "bytes": 8 * (bcast + allred)}
+
+
 def shard_ranges(n: int, world: int) -> list[tuple[int, int]]:
     """Contiguous, balanced mode ranges [lo, hi) per rank (sizes differ by <= 1)."""
     if world < 1:

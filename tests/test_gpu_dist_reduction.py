@@ -68,10 +68,13 @@ def test_distributed_band_reduction_equals_single_rank(tmp_path, world, n):
         nat.set_two_stage_min(nat.TWO_STAGE_MIN_DEFAULT)
     ref = np.sort(np.linalg.eigvalsh(a))[::-1]
     scale = np.abs(ref).max()
-    panels = (n - 1) // 64
+    from paper_2407_11993_b200 import parallel
+    want = parallel.band_reduction_collectives(n, world)
     for r in res:
         # one broadcast per panel + the last columns, one all-reduce per panel
-        assert int(r["broadcasts"]) == panels + 1 and int(r["allreduces"]) == panels
+        assert int(r["broadcasts"]) == want["broadcasts"]
+        assert int(r["allreduces"]) == want["allreduces"]
+        assert int(r["bytes"]) == want["bytes"]
         assert np.max(np.abs(r["w"] - ref)) < 1e-12 * scale * n
         assert np.max(np.abs(r["w"] - w1)) < 1e-12 * scale * n
         u = r["u"]

@@ -144,3 +144,27 @@ def test_sharded_sweep_sums_to_the_reference_run(tmp_path):
     g = golden("plate_small")
     assert y.shape[0] == 2
     assert rel_l2(y.sum(axis=0), g["td2_obs_theta0.5"]) < 1e-12
+
+
+def test_band_reduction_partition_host_logic():
+    """The distributed band reduction's partition (csrc/sytrd2.cu) as the host sees it:
+    64-column blocks dealt round-robin, and the collective counts / bytes communicator_info()
+    reports per eigensolve (the GPU tests compare the library's counters with these)."""
+    from paper_2407_11993_b200 import parallel
+    assert [parallel.band_block_owner(c, 3) for c in (0, 63, 64, 127, 128, 191, 192)] == \
+        [0, 0, 1, 1, 2, 2, 0]
+    # every rank owns the same number of blocks up to one (balance of the shrinking matrix)
+    for world in (2, 3, 8):
+        for n in (1346, 1536, 50000):
+            blocks = [parallel.band_block_owner(c, world) for c in range(0, n, 64)]
+            counts = [blocks.count(r) for r in range(world)]
+            assert max(counts) - min(counts) <= 1
+    c = parallel.band_reduction_collectives(1536, 2)
+    assert c["broadcasts"] == 24 and c["allreduces"] == 23
+    assert parallel.band_reduction_collectives(1536, 1) == {"broadcasts": 0, "allreduces": 0,
+                                                            "bytes": 0}
+    # C3: 781 panels, ~10 GB of broadcasts + ~20 GB of all-reduced partials
+    c3 = parallel.band_reduction_collectives(50000, 8)
+    assert c3["allreduces"] == 781 and 29e9 < c3["bytes"] < 31e9
+    with pytest.raises(ValueError):
+        parallel.band_block_owner(5, 0)
