@@ -425,17 +425,24 @@ bool make_map(CUtensorMap* m, const double* base, int64_t inner, int64_t outer, 
 // claim counters: a ring, so that products in flight on different streams do not share one
 constexpr int NCTR = 64;
 std::atomic<unsigned> g_tma_launch_no{0};
-unsigned long long* claim_counters() {
-  static unsigned long long* d = nullptr;
-  if (!d) {
-    if (cudaMalloc(reinterpret_cast<void**>(&d), NCTR * 2 * sizeof(unsigned long long)) !=
+constexpr int kMaxDev = 64;
+int cur_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev >= 0 && dev < kMaxDev ? dev : 0;
+}
+unsigned long long* claim_counters() {  // one ring per device
+  static unsigned long long* d[kMaxDev] = {};
+  const int dev = cur_device();
+  if (!d[dev]) {
+    if (cudaMalloc(reinterpret_cast<void**>(&d[dev]), NCTR * 2 * sizeof(unsigned long long)) !=
         cudaSuccess) {
       cudaGetLastError();
       return nullptr;
     }
-    cudaMemset(d, 0, NCTR * 2 * sizeof(unsigned long long));
+    cudaMemset(d[dev], 0, NCTR * 2 * sizeof(unsigned long long));
   }
-  return d;
+  return d[dev];
 }
 
 template <int TA, int TB, class C>
@@ -468,10 +475,10 @@ cudaError_t launch_tma(const GemmArgs& p, cudaStream_t st, const GemmOwn& own = 
                    make_map(&mapC, p.C, p.m, p.n, p.ldc, C::BM, C::BN);
   auto kern = gemm_tma_kernel<TA, TB, LOWER, C, SYMM>;
   constexpr size_t sm = tma_smem_bytes<(SYMM ? 1 : TA), TB, C>();
-  static bool configured = false;
-  if (!configured) {
+  static bool configured[kMaxDev] = {};  // the attribute is per device
+  if (!configured[cur_device()]) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    configured = true;
+    configured[cur_device()] = true;
   }
   TmaGemmParams q;
   q.p = p;

@@ -38,7 +38,8 @@ namespace em {
 
 int g_q2r_dbg = 0;  // debug key 94: bit0 VT(k) waits for C(k-1); bit1 uniform strips;
                     // bit2 synchronous Z staging loads; bit3 fences before the empty arrivals;
-                    // bit4 seven consumer warps (8 warps per CTA, 255 registers)
+                    // bit4 seven consumer warps (8 warps per CTA, 255 registers); bit5 eight
+                    // consumer warps instead of the default twelve
 
 namespace {
 constexpr int QB = 64;                  // sweeps per group, reflector length

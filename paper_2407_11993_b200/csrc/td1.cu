@@ -706,13 +706,14 @@ static void td1_solve_step(em_td1_plan* P, double* I, double* Icap_col, const do
   const CUtensorMap& cmap = *reinterpret_cast<const CUtensorMap*>(P->cmap);
   const bool staged = P->tma_ok && g_td1_staged != 0;
   if (staged) {
-    static bool configured = false;
-    if (!configured) {
+    static bool configured[64] = {};  // the attribute is per device
+    const int dev = P->ctx->device >= 0 && P->ctx->device < 64 ? P->ctx->device : 0;
+    if (!configured[dev]) {
       EM_CK(cudaFuncSetAttribute(trsv_fwd_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)TD1_SMEM));
       EM_CK(cudaFuncSetAttribute(trsv_bwd_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)TD1_SMEM));
-      configured = true;
+      configured[dev] = true;
     }
   }
   const int grid_s = (int)imin64(nblk, (int64_t)num_sms());
