@@ -164,3 +164,32 @@ def test_dsymm_band_lower_reads_only_lower_and_band():
         got = nat.host_colmajor(dc, m, n)
         ref = a @ b
         assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max() * np.sqrt(m), (m, n)
+
+
+@pytest.mark.parametrize("cfg", [2, 4])
+def test_dgemm_tma_accumulate_many_tiles_per_cta_repeated(cfg):
+    """beta != 0 with several tiles per CTA, repeated: the configuration in which a ring
+    stage released right behind its last fragment load was overwritten by the next TMA box
+    while other warps' epilogue traffic delayed the load (wrong 16 x 64 blocks in ~40% of
+    the runs before the stage release moved behind the consuming DMMAs)."""
+    import torch
+    nat, ctx, lib = _lib()
+    rng = np.random.default_rng(0)
+    m = n = 4436
+    k = 128
+    a = rng.standard_normal((m, k))
+    b = rng.standard_normal((n, k))
+    c0 = rng.standard_normal((m, n))
+    ref = c0 - a @ b.T
+    A = torch.from_numpy(a.T.copy()).cuda()
+    B = torch.from_numpy(b.T.copy()).cuda()
+    nat.check(lib.em_config(ctx, 95, cfg))
+    try:
+        for _ in range(8):
+            C = torch.from_numpy(c0.T.copy()).cuda()
+            nat.check(lib.em_dgemm(ctx, 0, 1, m, n, k, -1.0, nat.ptr(A), m, nat.ptr(B), n, 1.0,
+                                   nat.ptr(C), m))
+            got = C.t().cpu().numpy()
+            assert np.abs(got - ref).max() <= 1e-11
+    finally:
+        nat.check(lib.em_config(ctx, 95, 1))
