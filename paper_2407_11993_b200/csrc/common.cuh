@@ -53,6 +53,15 @@ __host__ __device__ __forceinline__ int64_t imax64(int64_t a, int64_t b) { retur
 EM_DEVINL void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 EM_DEVINL void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 
+// 0 for every double an arithmetic instruction can produce (results are never signalling
+// NaNs: high word 0x7ff00001 has the quiet bit clear), but data-dependent on x: OR-ing it
+// over a set of accumulators and adding the result to an address makes the instruction
+// using that address wait for all of them (used to order mbarrier releases and async
+// copies behind the DMMAs that consumed a shared-memory stage).
+EM_DEVINL unsigned never_set(double x) {
+  return __double2hiint(x) == 0x7ff00001 ? 8u : 0u;
+}
+
 EM_DEVINL double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -317,14 +317,13 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
       // The tile's last stage is released before the epilogue (so the producer refills the
       // whole ring under it). The barrier address carries a data dependency on every
       // accumulator, so the arrive cannot issue before the final DMMAs have delivered, i.e.
-      // before their fragment loads are done (the added term is always zero: no sum of
-      // doubles has the signalling-NaN high word 0x7ff00001).
-      double dep = 0.0;
+      // before their fragment loads are done (the added term is always zero: never_set in
+      // common.cuh).
+      unsigned never = 0u;
 #pragma unroll
       for (int i = 0; i < WTM; ++i)
 #pragma unroll
-        for (int j = 0; j < WTN; ++j) dep += acc[i][j][0];
-      const unsigned never = __double2hiint(dep) == 0x7ff00001 ? 8u : 0u;
+        for (int j = 0; j < WTN; ++j) never |= never_set(acc[i][j][0]);
       __syncwarp();
       if (lane == 0)
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(

@@ -361,6 +361,15 @@ __global__ void __launch_bounds__((NW + Q2RRegs<NW>::PW) * 32, 1) q2r_kernel(int
     W.read_half(zbt);  // half g + k + 1
     const int s = (int)(k & 1);
     mbar_wait(&full_v[s], (unsigned)((k >> 1) & 1));
+    // Stage releases come one phase late, behind the NEXT barrier wait: every DMMA that
+    // read the stage precedes that wait in program order, and a DMMA issues only once its
+    // fragment loads have delivered, so the stage's shared-memory reads are done. (Released
+    // right after its last use, ptxas schedules the arrive directly behind the last LDS,
+    // ahead of the consuming DMMAs, and a load delayed behind other warps' global traffic
+    // can be overtaken by the producer's next bulk copy: seen in gemm_tma.cu. A release
+    // made data-dependent on the accumulators is safe too but stalls the warp: +4%.)
+    __syncwarp();
+    if (k > 0 && lane == 0) mbar_arrive(&empty_vt[s ^ 1]);  // VT(k-1): step C of block k-1
     W.step_a(zt, zbt, W.Vs + s * VP, w);
     // The staging buffer is refilled only after every value read from it went into a
     // product: the asm below consumes the W accumulators (so every step-A DMMA, and with it
@@ -373,16 +382,10 @@ __global__ void __launch_bounds__((NW + Q2RRegs<NW>::PW) * 32, 1) q2r_kernel(int
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       __threadfence_block();
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty_v[s]);
     mbar_wait(&full_vt[s], (unsigned)((k >> 1) & 1));
-    W.step_c(zt, zbt, W.VTs + s * VTP, w);
-    if (dbg & 8) {
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      __threadfence_block();
-    }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty_vt[s]);
+    if (lane == 0) mbar_arrive(&empty_v[s]);  // V(k): step A above
+    W.step_c(zt, zbt, W.VTs + s * VTP, w);
     W.store_half(zt, g + k);  // final for this group
   };
   int64_t k = 0;

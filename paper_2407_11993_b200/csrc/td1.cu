@@ -231,10 +231,9 @@ EM_DEVINL void td1_stream(const Td1Ring& R, unsigned& it, int64_t j0, int64_t cn
     __syncwarp();
     if (q > 0 && lane == 0) mbar_arrive(&R.empty[(it + TD1_NST - 2) % TD1_NST]);
   }
-  double dep = 0.0;
+  unsigned never = 0u;
 #pragma unroll
-  for (int cc = 0; cc < 16; ++cc) dep += acc[cc];
-  const unsigned never = __double2hiint(dep) == 0x7ff00001 ? 8u : 0u;
+  for (int cc = 0; cc < 16; ++cc) never |= never_set(acc[cc]);
   __syncwarp();
   if (lane == 0)
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(
