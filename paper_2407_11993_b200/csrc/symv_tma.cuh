@@ -222,8 +222,16 @@ EM_DEVINL double symv_tma_loop(const CUtensorMap* map, const TmaRing& R, uint32_
         col[cc] = cs;
       }
     }
+    // this warp is done with the stage; the release is data-dependent on the column sums
+    // (into which every value loaded from the stage went), so it cannot be scheduled ahead
+    // of the loads' completion (never_set, common.cuh; the hazard is described in gemm_tma.cu)
+    const unsigned never =
+        never_set(col[0]) | never_set(col[1]) | never_set(col[2]) | never_set(col[3]);
     __syncwarp();
-    if (lane == 0) mbar_arrive(&R.empty[s]);  // this warp is done with the stage
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&R.empty[s]) +
+                                                                      never)
+                   : "memory");
     {  // column sums over the 32 lanes: 4 values, 6 shuffles
       const bool h16 = lane & 16, h8 = lane & 8;
       const double a0 = h16 ? col[2] : col[0], a1 = h16 ? col[3] : col[1];
