@@ -39,7 +39,7 @@ namespace em {
 int g_q2r_dbg = 0;  // debug key 94: bit0 VT(k) waits for C(k-1); bit1 uniform strips;
                     // bit2 synchronous Z staging loads; bit3 fences before the empty arrivals;
                     // bit4 seven consumer warps (8 warps per CTA, 255 registers); bit5 eight
-                    // consumer warps instead of the default twelve
+                    // consumer warps instead of twelve; bit6 twelve even for few columns
 
 namespace {
 constexpr int QB = 64;                  // sweeps per group, reflector length
@@ -441,9 +441,13 @@ static void q2_apply_nw(cudaStream_t st, int64_t n, int64_t ncols, int64_t ngrou
 void q2_apply_reg(cudaStream_t st, int64_t n, int64_t ncols, int64_t ngroups, const double* V2,
                   const int64_t* toff, const double* T2, double* Z, int64_t ldz) {
   if (ncols <= 0 || n <= 1) return;
+  // 12 consumer warps per CTA run the tensor pipe fuller (C3: 11.05 s against 11.31 s with
+  // 8), but with fewer than two full waves of 96-column strips the short last wave costs
+  // more than that (n = 16,384: 505 ms against 450 ms): 8 warps there
+  const bool few = (ncols + 7) / 8 < 2 * 12 * (int64_t)num_sms();
   if (g_q2r_dbg & 16)
     q2_apply_nw<7>(st, n, ncols, ngroups, V2, toff, T2, Z, ldz);
-  else if (g_q2r_dbg & 32)
+  else if ((g_q2r_dbg & 32) || (few && !(g_q2r_dbg & 64)))
     q2_apply_nw<8>(st, n, ncols, ngroups, V2, toff, T2, Z, ldz);
   else
     q2_apply_nw<12>(st, n, ncols, ngroups, V2, toff, T2, Z, ldz);
