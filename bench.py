@@ -690,8 +690,13 @@ def run_ours(args, cfg, rank, world, local_rank):
         rl["peak_source"] = "DMMA issue peak measured on this pool (profiles/r01_fp64_peaks.jsonl)"
         if os.path.exists(q2prof):
             pq = json.load(open(q2prof))
-            rl["traffic_per_launch"] = pq.get("dram_bytes")
-            rl["traffic_source"] = "profiles/r02/ncu_q2r.json (ncu --set full, one launch)"
+            # measured at n = 16,384 (one group of 101 blocks), not at this workload's n: the
+            # contract's `traffic` (per launch of THIS run) stays null
+            rl["traffic_ncu"] = {"n": pq.get("n"), "dram_bytes_per_launch": pq.get("dram_bytes"),
+                                 "algorithmic_bytes_per_launch": pq.get("algorithmic_bytes"),
+                                 "dmma_pipe_active_pct": pq.get("dmma_pipe_active_pct"),
+                                 "source": "profiles/r02/ncu_q2r.json (ncu --set full, one "
+                                           "launch of tools/q2_probe.py 16384)"}
     if "sytrd" in st_avg and "q2_apply" not in st_avg:
         # one-stage tridiagonalisation (below the two-stage threshold): its symv is the
         # HBM-bound kernel, timed live at the full order
