@@ -17,9 +17,11 @@
 namespace em {
 
 // em_config(EM_CFG_TWO_STAGE_MIN): smallest order that takes the two-stage reduction.
-// Measured on one B200: one-stage wins at n = 16,384 (sytrd + ormtr 1.6 s
-// against 2.3 s), two-stage at n = 50,000 (49.3 s against 50.7 s per C3 step before the
-// lower-triangle sy2sb update). Tests force either path.
+// Measured on one B200: one-stage still wins at n = 16,384 (sytrd + ormtr
+// 1.58 s against 1.85 s for sy2sb + sb2st + Q2 + Q1 at the end of round 2), two-stage
+// clearly at n = 50,000 (the C3 step: 31 s against 50.7 s one-stage in round 1; the
+// crossover now lies near n = 22,000 by the n^3 / n^2 scaling of the stages). Tests force
+// either path.
 int64_t g_two_stage_min = 40000;
 // Extra device memory of the two-stage path beyond A and Z, phase by phase (n^2 doubles):
 // the stage-2 reflectors V2 (1/2) live from sb2st to the end; divide and conquer adds its
