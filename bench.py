@@ -543,9 +543,10 @@ def workload_config(args, cfg, n, world):
 
 def parallelism(args, world):
     return "single GPU" if world == 1 else (
-        f"modes sharded x{world}: band reduction distributed (64-column blocks round-robin, "
-        f"panel broadcasts + all-reduced partial products over the library's NCCL "
-        f"communicator), bulge chasing + tridiagonal solve replicated, eigenvector "
+        f"modes sharded x{world}: band reduction distributed when the library communicator "
+        f"is attached (64-column blocks round-robin, panel broadcasts + all-reduced partial "
+        f"products over NCCL; see the communicator line on stderr), bulge chasing + "
+        f"tridiagonal solve replicated, eigenvector "
         f"back-transforms, drive/observable projections and stepping column-sharded, one "
         f"all-reduce of partial observables per 2048-step block")
 
@@ -570,7 +571,18 @@ def run_ours(args, cfg, rank, world, local_rank):
         # the library's own communicator: NCCL on the context stream (callbacks through
         # torch.distributed when the ranks share a device under gloo)
         from paper_2407_11993_b200 import parallel
-        parallel.attach_communicator(dist)
+        try:
+            parallel.attach_communicator(dist)
+        except Exception as exc:  # noqa: BLE001 (the run continues with a replicated reduction)
+            # every rank must take the same path: agree on the outcome
+            ok = torch.zeros(1, device="cuda")
+            print(f"[rank {rank}] library communicator unavailable ({exc}); band reduction "
+                  f"replicated", file=sys.stderr)
+        else:
+            ok = torch.ones(1, device="cuda")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if float(ok.item()) == 0.0:
+            parallel.detach_communicator()
     if args.two_stage is not None:
         nat.set_two_stage_min(args.two_stage)
     if os.environ.get("EM_SYTRD_DBG"):  # A/B switch for the tridiagonalisation code paths
