@@ -79,26 +79,32 @@ struct QRArgs {
   double* P;      // panel (m x nbw, ld ldp), in place: R above, V below the diagonal
   int64_t ldp;
   double* tau;    // p
-  double* part;   // G + G*64 + 1 scratch
+  double* part;   // 2 x (G*64 + 64) scratch (double-buffered by the column's parity)
   GridBar* bar;
   int R;          // rows per CTA
 };
 
 // GM: the panel is worked on in place in global memory (L2-resident) instead of shared
-// memory — for panels taller than the CTAs' shared memory holds (m > ~59,000 rows)
+// memory — for panels taller than the CTAs' shared memory holds (m > ~59,000 rows).
+//
+// ONE grid barrier per column: from the unscaled column x = P[j+1:, j] every CTA publishes
+// its partial sum of squares and its partial products d_c = x^T P[j+1:, c] (c > j), the
+// owner of row j that row; behind the barrier every CTA forms beta, tau, scale and
+// w_c = v^T P[:, c] = P[j, c] + scale d_c itself (v = scale x below the unit entry) and
+// updates its own rows. (Two barriers per column — the norm, then the products with the
+// scaled v — and a single thread summing the G partials cost 1.7 ms per panel at C3, 1.3 s
+// of the band reduction on its critical path.) The partials are double-buffered by the
+// column's parity: a CTA writing column j + 1's has passed barrier j, which every CTA
+// reaches only after reading column j - 1's.
 template <bool GM>
 __global__ void __launch_bounds__(256) qr_panel_kernel(QRArgs a) {
   extern __shared__ double Ssm[];  // column-major [nbw][R]
-  __shared__ double red[8];
-  __shared__ double bc[4];
   __shared__ double wsh[B2];
+  __shared__ double rowsh[B2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned G = gridDim.x;
   const int64_t r0 = blockIdx.x * (int64_t)a.R;
   const int nr = (int)imax64(0, imin64(a.R, a.m - r0));
-  double* normpart = a.part;
-  double* dotpart = a.part + G;
-  double* alpha_slot = a.part + G + (size_t)G * B2;
   double* S = GM ? a.P + r0 : Ssm;
   const int64_t ls = GM ? a.ldp : a.R;
   if (!GM) {
@@ -108,79 +114,80 @@ __global__ void __launch_bounds__(256) qr_panel_kernel(QRArgs a) {
     }
   }
   __syncthreads();
+  const int chunk = (int)((G + 3) / 4);
   for (int j = 0; j < a.p; ++j) {
     double* Sj = S + j * ls;
-    // (a) partial sum of squares below the diagonal; the owner of row j publishes alpha
-    double ss = 0.0;
-    for (int lr = tid; lr < nr; lr += blockDim.x) {
-      const int64_t r = r0 + lr;
-      if (r > j) ss = fma(Sj[lr], Sj[lr], ss);
-      else if (r == j) *alpha_slot = Sj[lr];
+    double* dotpart = a.part + (size_t)(j & 1) * ((size_t)G * B2 + B2);
+    double* rowj = dotpart + (size_t)G * B2;
+    // (a) partials over the own rows below row j: slot j = sum of squares, slot c = x^T P[:, c]
+    for (int c = j + warp; c < a.nbw; c += 8) {
+      const double* Sc = S + c * ls;
+      double s = 0.0;
+      for (int lr = lane; lr < nr; lr += 32)
+        if (r0 + lr > j) s = fma(Sj[lr], Sc[lr], s);
+      s = warp_sum(s);
+      if (lane == 0) dotpart[(size_t)blockIdx.x * B2 + c] = s;
     }
-    ss = block_reduce_sum(ss, red);
-    if (tid == 0) normpart[blockIdx.x] = ss;
+    if (j >= r0 && j < r0 + nr)
+      for (int c = j + tid; c < a.nbw; c += blockDim.x) rowj[c] = S[c * ls + (j - r0)];
     grid_sync(a.bar, G);
-    // (b) every CTA forms beta, tau, scale identically
-    if (tid == 0) {
-      double xs = 0.0;
-      for (unsigned b = 0; b < G; ++b) xs += __ldcg(normpart + b);
-      const double alpha = *(volatile double*)alpha_slot;
-      const double xnorm = sqrt(xs);
-      double beta, tau, scale;
-      if (xnorm == 0.0) {
-        tau = 0.0;
-        beta = alpha;
-        scale = 0.0;
-      } else {
-        beta = -copysign(hypot(alpha, xnorm), alpha);
-        tau = (beta - alpha) / beta;
-        scale = 1.0 / (alpha - beta);
+    // (b) totals in a fixed order: 4 threads per column, a contiguous quarter of the CTAs each
+    {
+      const int c = tid >> 2, q = tid & 3;
+      double s = 0.0;
+      if (c >= j && c < a.nbw) {
+        // every load of the thread's quarter in flight at once (one L2 round trip for up to
+        // 160 CTAs), summed in a fixed order
+        const int b0 = q * chunk, b1 = (int)imin64(b0 + chunk, G);
+        for (int bb = b0; bb < b1; bb += 40) {
+          double t[40];
+#pragma unroll
+          for (int u = 0; u < 40; ++u)
+            t[u] = bb + u < b1 ? __ldcg(dotpart + (size_t)(bb + u) * B2 + c) : 0.0;
+#pragma unroll
+          for (int u = 0; u < 40; ++u) s += t[u];
+        }
       }
-      bc[0] = beta;
-      bc[1] = tau;
-      bc[2] = scale;
-      if (blockIdx.x == 0) a.tau[j] = tau;
+      s += __shfl_xor_sync(0xffffffffu, s, 1);
+      s += __shfl_xor_sync(0xffffffffu, s, 2);
+      if (q == 0 && c < a.nbw) {
+        wsh[c] = s;
+        rowsh[c] = c >= j ? __ldcg(rowj + c) : 0.0;
+      }
     }
     __syncthreads();
-    const double beta = bc[0], tau = bc[1], scale = bc[2];
+    // (c) beta, tau, scale: identical in every thread of every CTA
+    const double alpha = rowsh[j], xnorm = sqrt(wsh[j]);
+    double beta = alpha, tau = 0.0, scale = 0.0;
+    if (xnorm != 0.0) {
+      beta = -copysign(hypot(alpha, xnorm), alpha);
+      tau = (beta - alpha) / beta;
+      scale = 1.0 / (alpha - beta);
+    }
+    if (blockIdx.x == 0 && tid == 0) a.tau[j] = tau;
+    // (d) apply H_j to the remaining columns of the own rows: w_c = P[j, c] + scale d_c
+    if (tau != 0.0) {
+      // 64 row lanes x 4 column groups (no index divisions)
+      const int lr0 = tid & 63;
+      for (int c = j + 1 + (tid >> 6); c < a.nbw; c += 4) {
+        const double twc = -tau * fma(scale, wsh[c], rowsh[c]);
+        double* Sc = S + c * ls;
+        for (int lr = lr0; lr < nr; lr += 64) {
+          const int64_t r = r0 + lr;
+          if (r >= j) Sc[lr] = fma(twc, (r == j) ? 1.0 : Sj[lr] * scale, Sc[lr]);
+        }
+      }
+    }
+    __syncthreads();
     for (int lr = tid; lr < nr; lr += blockDim.x) {
       const int64_t r = r0 + lr;
       if (r > j && scale != 0.0) Sj[lr] *= scale;
       else if (r == j) Sj[lr] = beta;
     }
-    __syncthreads();
-    // (c) partial w_c = v^T P[:, c] for c > j (v_j = 1)
-    for (int c = j + 1 + warp; c < a.nbw; c += 8) {
-      const double* Sc = S + c * ls;
-      double s = 0.0;
-      for (int lr = lane; lr < nr; lr += 32) {
-        const int64_t r = r0 + lr;
-        if (r >= j) s = fma(r == j ? 1.0 : Sj[lr], Sc[lr], s);
-      }
-      s = warp_sum(s);
-      if (lane == 0) dotpart[(size_t)blockIdx.x * B2 + c] = s;
-    }
-    grid_sync(a.bar, G);
-    // (d) apply H_j to the remaining columns of the own rows
-    for (int c = j + 1 + tid; c < a.nbw; c += blockDim.x) {
-      double s = 0.0;
-      for (unsigned b = 0; b < G; ++b) s += __ldcg(dotpart + (size_t)b * B2 + c);
-      wsh[c] = s;
-    }
-    __syncthreads();
-    if (tau != 0.0) {
-      const int ncol = a.nbw - j - 1;
-      for (int idx = tid; idx < nr * ncol; idx += blockDim.x) {
-        const int lr = idx % nr, c = j + 1 + idx / nr;
-        const int64_t r = r0 + lr;
-        if (r >= j) {
-          const double v = (r == j) ? 1.0 : Sj[lr];
-          S[c * ls + lr] = fma(-tau * wsh[c], v, S[c * ls + lr]);
-        }
-      }
-    }
-    __syncthreads();
+    // (column j is not read again; the next column's wsh / rowsh writes come behind its
+    // grid barrier)
   }
+  __syncthreads();
   if (!GM) {
     for (int idx = tid; idx < nr * a.nbw; idx += blockDim.x) {
       const int lr = idx % nr, c = idx / nr;
@@ -239,7 +246,7 @@ void sy2sb(cudaStream_t st, int64_t n, double* A, int64_t lda, double* tau1, dou
   const int sms = num_sms();
   DBuf VW((size_t)n * 2 * b, st), WV((size_t)n * 2 * b, st), VT((size_t)n * b, st);
   DBuf Gm((size_t)b * b, st), T((size_t)b * b, st), Y((size_t)b * b, st), M((size_t)b * b, st);
-  DBuf part((size_t)sms + (size_t)sms * b + 8, st);
+  DBuf part(2 * ((size_t)sms * b + b) + 8, st);
   DArr<GridBar> bar(1, st);
   EM_CK(cudaMemsetAsync(bar.p, 0, sizeof(GridBar), st));
   EM_CK(cudaFuncSetAttribute(qr_panel_kernel<false>,
@@ -419,7 +426,11 @@ __global__ void __launch_bounds__(256, 2) sb2st_kernel(SbArgs a) {
     const int64_t Kp = s > 0 ? ntasks(n, s - 1) : 0;
     for (int64_t k = 0; k < K; ++k) {
       if (s > 0 && tid == 0) {
-        const int need = (int)imin64(k + 3, Kp);
+        // Task (s, k) touches rows a0 .. a0 + 63 = s + 1 + 64 k .. s + 64 (k + 1) only (its
+        // E and D blocks); task (s - 1, k') rows s + 64 k' .. s + 64 k' + 63: k' <= k + 1
+        // overlap, k' = k + 2 starts one row below. A lag of two tasks, not three: the
+        // critical path of the chase is (lag x n) task latencies.
+        const int need = (int)imin64(k + 2, Kp);
         // acquire by thread 0, made CTA-wide by the barrier below; the band is read with
         // L2-only loads (__ldcg), so no L1 invalidation is needed
         while (ld_acquire_int(a.prog + (s - 1)) < need) __nanosleep(32);
