@@ -190,7 +190,11 @@ int em_sygv(em_ctx* ctx, int64_t n, const double* L, int64_t ldl, const double* 
  * the stencil resistance matrix), R's own storage holds its Cholesky factor during the
  * solve and is restored from a device CSR copy before return (its contents are
  * transient garbage meanwhile; -0.0 entries come back as +0.0). Saves one n x n buffer:
- * 6 n^2 doubles at the memory peak with VtR = NULL, so n = 60,000 fits one B200. */
+ * 6 n^2 doubles at the memory peak with VtR = NULL, so n = 60,000 fits one B200.
+ * A BANDED sparse R (the plates' stencil) is factored in band storage of its own; then
+ * R's storage (ldr a multiple of 32, 256-byte aligned) holds the reduced matrix
+ * B = G^-1 L G^-T instead, and is restored the same way: at n = 60,000 the two-stage
+ * tridiagonalisation (2.5 n^2 of workspace) fits beside L, R and V. */
 #define EM_SYGV_R_WORKSPACE 1
 int em_sygv_ex(em_ctx* ctx, int64_t n, const double* L, int64_t ldl, double* R, int64_t ldr,
                double* tau, double* V, int64_t ldv, double* l_n, double* r_n, double* VtR,

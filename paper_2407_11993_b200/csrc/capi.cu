@@ -16,6 +16,7 @@ struct em_td1_plan;
 
 namespace em {
 extern int64_t g_two_stage_min;
+extern int g_qr_gm;
 extern int g_sytrd_dbg;
 extern int g_band_off;
 extern int g_ln_dense;
@@ -251,6 +252,10 @@ int em_config(em_ctx* ctx, int key, int64_t value) {
       cudaMemPool_t pool;
       EM_CK(cudaDeviceGetDefaultMemPool(&pool, ctx->device));
       EM_CK(cudaMemPoolTrimTo(pool, (size_t)value));
+      return EM_OK;
+    }
+    if (key == 92) {  // debug: the band reduction's panel QR in global memory (tall-panel form)
+      em::g_qr_gm = value ? 1 : 0;
       return EM_OK;
     }
     if (key == 93) {  // debug: TD1 solves (0 register tiles, 1 TMA-staged tiles)

@@ -391,8 +391,19 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
     G = Gbuf.p;
     ldg = n;
   }
+  // A BANDED R's factor lives in band storage of its own, so with EM_SYGV_R_WORKSPACE the
+  // dense R (sparse: a stencil) is free during the eigensolve: its storage holds the
+  // reduced matrix B (when its columns are 256-byte aligned, as B's must be) and is
+  // restored from the CSR copy once the back-transform is done. One N x N buffer less at
+  // the peak: the N = 60,000 pencil then runs the two-stage tridiagonalisation on one GPU.
+  const bool l_ws_ok = (flags & EM_SYGV_L_WORKSPACE) && ldl >= n && ldl % 32 == 0;
+  const bool rb_ws = banded && !r_band && !l_ws_ok && (flags & EM_SYGV_R_WORKSPACE) &&
+                     ldr >= n && ldr % 32 == 0 &&
+                     (reinterpret_cast<uintptr_t>(R) & 255) == 0 &&
+                     csr_from_dense(st, n, R, ldr, 0.02, rcsr);
   auto restore_r = [&] {
     if (r_ws) csr_to_dense(st, rcsr, G, ldg);
+    if (rb_ws) csr_to_dense(st, rcsr, const_cast<double*>(R), ldr);
   };
   int64_t piv;
   DBuf GDinv;
@@ -425,7 +436,7 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
   // so all TMA boxes of the tridiagonalisation's symv are (symv_tma.cu)
   // (in place in L's storage when allowed and L's columns are 256-byte aligned)
   const bool b_in_l = l_ws && ldl % 32 == 0;
-  const int64_t ldb = b_in_l ? ldl : (n + 31) / 32 * 32;
+  const int64_t ldb = b_in_l ? ldl : rb_ws ? ldr : (n + 31) / 32 * 32;
   // certificate only (modal.py:69-70): with EM_CFG_L_CERTIFICATE = 1 L is factored up
   // front in a copy of its own (before an in-place solve destroys it)
   if (g_l_certificate) {
@@ -442,7 +453,9 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
   }
   DBuf Bown;
   double* Bp = const_cast<double*>(L);
-  if (!b_in_l) {
+  if (rb_ws) {
+    Bp = const_cast<double*>(R);
+  } else if (!b_in_l) {
     Bown.alloc((size_t)ldb * n, st);
     Bp = Bown.p;
   }
@@ -537,7 +550,7 @@ int64_t sygv(cudaStream_t st, int64_t n, const double* L, int64_t ldl, const dou
   // reference's SymMatrix), so through a CSR copy, fused with the column dots (no N x N
   // product); V^T R = (R V)^T only when asked for.
   Csr rq;
-  const Csr* rc = r_ws ? &rcsr : nullptr;
+  const Csr* rc = (r_ws || rb_ws) ? &rcsr : nullptr;
   if (!rc && (r_n || l_n) && csr_from_dense(st, n, R, ldr, 0.02, rq)) rc = &rq;
   DBuf rn_tmp;
   double* rn_out = r_n;

@@ -214,6 +214,8 @@ __global__ void __launch_bounds__(128) larft_smem_kernel(int w, int w1,
 __global__ void build_v_kernel(int64_t n, const double* A, int64_t lda, int64_t i0, int w,
                                int64_t off, double* V, int64_t ldv);
 
+int g_qr_gm = 0;  // em_config debug key 92: 1 = the panel QR always in its global-memory form
+
 static void coop_launch(const void* fn, unsigned grid, unsigned block, void** args, size_t smem,
                         cudaStream_t st) {
   EM_CK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(block), args, smem, st));
@@ -271,7 +273,7 @@ void sy2sb(cudaStream_t st, int64_t n, double* A, int64_t lda, double* tau1, dou
       QRArgs qa{m, b, p, P, lda, tau1 + k0, part.p, bar.p, R};
       void* args[] = {&qa};
       Stage sq(st, ST_SY2SB_QR);
-      const bool gm = (size_t)R * b * sizeof(double) > 200 * 1024;
+      const bool gm = g_qr_gm || (size_t)R * b * sizeof(double) > 200 * 1024;
       if (gm)
         coop_launch((const void*)qr_panel_kernel<true>, G, 256, args, 0, st);
       else

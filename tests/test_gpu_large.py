@@ -159,6 +159,35 @@ def test_banded_r_path_matches_dense_path(grid):
     assert np.all(err[sep] < 1e-7 * np.abs(v0).max())
 
 
+@pytest.mark.parametrize("two_stage", [False, True])
+def test_banded_r_workspace_holds_reduced_matrix_and_is_restored(two_stage):
+    """EM_SYGV_R_WORKSPACE with a BANDED stencil R (factor in band storage of its own): R's
+    dense storage holds the reduced matrix during the eigensolve (N = 2,048: columns
+    256-byte aligned) and comes back bit for bit from the CSR copy; tau, l_n, r_n, V are
+    identical to the default mode, on the one-stage and the two-stage tridiagonalisation."""
+    import torch
+    from paper_2407_11993_b200 import _native as nat
+    from paper_2407_11993_b200.synth import device_plate_model
+    m = device_plate_model(32, 16, 4, n_ports=0, n_sources=0, n_obs=1)
+    L, R = m["l_i"], m["r_i"]
+    n = L.shape[0]
+    assert n % 32 == 0
+    R0 = R.clone()
+    if two_stage:
+        nat.set_two_stage_min(0)
+    try:
+        rc0, _, _, o0 = _sygv_dev(L, R, n, flags=0)
+        rc1, _, _, o1 = _sygv_dev(L, R, n, flags=nat.EM_SYGV_R_WORKSPACE)
+    finally:
+        nat.set_two_stage_min(nat.TWO_STAGE_MIN_DEFAULT)
+    nat.check(rc0)
+    nat.check(rc1)
+    torch.cuda.synchronize()
+    assert torch.equal(R, R0)
+    for a, b in zip(o0, o1):
+        assert np.array_equal(a, b)
+
+
 def test_banded_r_not_pd_reports_the_dense_pivot():
     """A banded R that is not positive definite: same failing pivot (the reference's
     first failing Crout column, cholesky_kernel _kernels.py:18-36) on both paths."""

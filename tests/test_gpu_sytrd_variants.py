@@ -111,6 +111,34 @@ def test_two_stage_q2_forms_agree(n, lda):
         assert d.max() < 1e-9
 
 
+@pytest.mark.parametrize("n", [130, 1000, 3001])
+def test_panel_qr_global_memory_form(n):
+    """The band reduction's panel QR (one grid barrier per column) in its global-memory
+    form (debug key 92: the form panels taller than the CTAs' shared memory take, N > ~59,000)
+    runs the same arithmetic in the same order as the shared-memory form: identical
+    eigenvalues and eigenvectors, bit for bit, and both match LAPACK. Orders with a last
+    panel shorter than 64 rows (130, 3001)."""
+    from paper_2407_11993_b200 import _native as nat
+    lib, ctx = nat.load_library(), nat.context()
+    rng = np.random.default_rng(7 * n)
+    b = rng.standard_normal((n, n))
+    a = b + b.T
+    nat.set_two_stage_min(0)
+    try:
+        w0, u0 = _syev(a)
+        nat.check(lib.em_config(ctx, 92, 1))
+        w1, u1 = _syev(a)
+    finally:
+        nat.check(lib.em_config(ctx, 92, 0))
+        nat.set_two_stage_min(nat.TWO_STAGE_MIN_DEFAULT)
+    ref = np.sort(np.linalg.eigvalsh(a))[::-1]
+    scale = np.abs(ref).max()
+    assert np.max(np.abs(w0 - ref)) < 1e-12 * scale * n
+    assert np.max(np.abs(a @ u0 - u0 * w0)) < 1e-11 * scale * n
+    np.testing.assert_array_equal(w0, w1)
+    np.testing.assert_array_equal(u0, u1)
+
+
 def test_eig_path_reported_and_pool_trim():
     """em_info(EM_INFO_EIG_PATH) says which tridiagonalisation ran; em_trim releases the
     library's cached pool memory (ADVICE: the path may depend on free memory, so it is
