@@ -381,51 +381,55 @@ __host__ __device__ __forceinline__ int64_t ntasks(int64_t n, int64_t s) {
 
 constexpr int SBLD = B2 + 1;
 
-// dlarfg on x[0..L) in shared memory: returns tau, writes v (v[0] = 1) and beta via x[0]
-EM_DEVINL double smem_larfg(double* x, int L, double* v, double* red) {
-  double ss = 0.0;
-  for (int i = 1 + threadIdx.x; i < L; i += blockDim.x) ss = fma(x[i], x[i], ss);
-  ss = block_reduce_sum(ss, red);
-  __shared__ double bcs[3];
-  if (threadIdx.x == 0) {
-    const double alpha = x[0];
-    const double xnorm = sqrt(ss);
-    if (xnorm == 0.0) {
-      bcs[0] = alpha;
-      bcs[1] = 0.0;
-      bcs[2] = 0.0;
-    } else {
-      const double beta = -copysign(hypot(alpha, xnorm), alpha);
-      bcs[0] = beta;
-      bcs[1] = (beta - alpha) / beta;
-      bcs[2] = 1.0 / (alpha - beta);
-    }
+// dlarfg on x[0..L) (L <= 64) in shared memory, every thread computing the scalars itself:
+// returns tau, sets beta, writes v (v[0] = 1, zero from L on). x is left untouched. One
+// barrier inside (the two warp sums of squares) and one at the end (v visible). beta =
+// -sign(alpha) sqrt(alpha^2 + |x[1:]|^2) from the sum of squares directly.
+EM_DEVINL double larfg64(const double* x, int L, double* v, double* red, double& beta) {
+  const int tid = threadIdx.x;
+  if (tid < B2) {
+    const double xv = (tid >= 1 && tid < L) ? x[tid] : 0.0;
+    const double ss = warp_sum(xv * xv);
+    if ((tid & 31) == 0) red[tid >> 5] = ss;
   }
   __syncthreads();
-  const double scale = bcs[2];
-  for (int i = threadIdx.x; i < L; i += blockDim.x) v[i] = (i == 0) ? 1.0 : x[i] * scale;
-  for (int i = threadIdx.x; i < B2; i += blockDim.x)
-    if (i >= L) v[i] = 0.0;
-  __syncthreads();
-  if (threadIdx.x == 0) x[0] = bcs[0];
-  const double tau = bcs[1];
+  const double ss = red[0] + red[1];
+  const double alpha = x[0];
+  double tau = 0.0, scale = 0.0;
+  beta = alpha;
+  if (ss != 0.0) {
+    beta = -copysign(sqrt(fma(alpha, alpha, ss)), alpha);
+    tau = (beta - alpha) / beta;
+    scale = 1.0 / (alpha - beta);
+  }
+  if (tid < B2) v[tid] = tid == 0 ? 1.0 : (tid < L ? x[tid] * scale : 0.0);
   __syncthreads();
   return tau;
 }
 
+// One task = one 64 x 64 off-diagonal block E (right application of the sweep's previous
+// reflector, new reflector from its first column, left application) and the diagonal block
+// D (two-sided). Thread (i = tid & 63, jg = tid >> 6) owns the elements (i, jg + 4 u),
+// u < 16, of both blocks IN REGISTERS from the loads to the final stores (band storage:
+// element (i, j) sits at base + j (ldab - 1), one add per element); shared memory holds the
+// copies the matrix-vector products read. The scalars (beta, tau, the rank-2 coefficient)
+// are computed redundantly by every thread or warp instead of by one thread behind two
+// barriers: 9 barriers per task instead of 17 (the chase is bound by the task latency: a
+// sweep follows its predecessor by two tasks).
 __global__ void __launch_bounds__(256, 2) sb2st_kernel(SbArgs a) {
   extern __shared__ double sm[];
   double* E = sm;                 // E[i*SBLD + j]: row i of block k, column j of block k-1
   double* D = E + B2 * SBLD;      // full symmetric copy of the diagonal block
-  __shared__ double v[B2], vn[B2], w[B2], xcol[B2], red[8];
-  __shared__ double tau_prev_s, alpha_s;
+  __shared__ double v[B2], vn[B2], w[B2], w2[B2], xcol[B2], red[2];
   const int tid = threadIdx.x;
   const int q = tid & 3, row = tid >> 2;  // 4 threads per row (or column) in the matvecs
-  const int64_t n = a.n, ldab = a.ldab;
+  const int ti = tid & (B2 - 1), jg = tid >> 6;  // owner of elements (ti, jg + 4 u)
+  const int64_t n = a.n, ldab = a.ldab, st1 = a.ldab - 1;
   double* AB = a.AB;
   for (int64_t s = blockIdx.x; s < a.nsweeps; s += gridDim.x) {
     const int64_t K = ntasks(n, s);
     const int64_t Kp = s > 0 ? ntasks(n, s - 1) : 0;
+    double tp = 0.0;  // tau of the sweep's previous reflector
     for (int64_t k = 0; k < K; ++k) {
       if (s > 0 && tid == 0) {
         // Task (s, k) touches rows a0 .. a0 + 63 = s + 1 + 64 k .. s + 64 (k + 1) only (its
@@ -439,52 +443,44 @@ __global__ void __launch_bounds__(256, 2) sb2st_kernel(SbArgs a) {
       }
       __syncthreads();
       const int64_t a0 = s + 1 + k * B2;
+      const int64_t ap = a0 - B2;
       const int L = (int)imin64(B2, n - a0);
-      // the diagonal block [a0, a0+L) is not touched by this task's off-diagonal work
-      // (columns ap .. a0-1): its loads are issued together with E's, one L2 round trip
-      // Every load of the task (16 + 16 per thread) is issued before the first value is
-      // used: one L2 round trip per task instead of one per partially unrolled batch (the
-      // loads were 40% of a task's non-waiting stall samples, profiles/r02/ncu_sb2st.json).
+      // Every load of the task is issued before the first value is used: one L2 round trip
+      // per task (the loads were 40% of a task's non-waiting stall samples,
+      // profiles/r02/ncu_sb2st.json). D from its lower triangle only (mirrored into shared
+      // memory); the diagonal block [a0, a0+L) is not touched by the off-diagonal work.
+      double* dbase = AB + ti + a0 * ldab;       // (ti, j) at dbase + j (ldab - 1), j <= ti
+      double* ebase = AB + (B2 + ti) + ap * ldab;  // (ti, j) at ebase + j (ldab - 1)
       double dreg[16], ereg[16];
 #pragma unroll
       for (int u = 0; u < 16; ++u) {
-        const int idx = tid + 256 * u;
-        const int i = idx & (B2 - 1), j = idx >> 6;
-        const int lo = i >= j ? j : i, hi = i >= j ? i : j;  // symmetric: the lower entry
-        const double* p = AB + (hi - lo) + (a0 + lo) * ldab;
-        dreg[u] = (i < L && j < L) ? __ldcg(p) : 0.0;
+        const int j = jg + 4 * u;
+        dreg[u] = (j <= ti && ti < L) ? __ldcg(dbase + j * st1) : 0.0;
       }
       if (k > 0) {
-        const int64_t ap = a0 - B2;
 #pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          const int idx = tid + 256 * u;
-          const int i = idx & (B2 - 1), j = idx >> 6;
-          ereg[u] = (i < L) ? __ldcg(AB + (B2 + i - j) + (ap + j) * ldab) : 0.0;
-        }
+        for (int u = 0; u < 16; ++u) ereg[u] = ti < L ? __ldcg(ebase + (jg + 4 * u) * st1) : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < 16; ++u) {
-        const int idx = tid + 256 * u;
-        D[(idx & (B2 - 1)) * SBLD + (idx >> 6)] = dreg[u];
+        const int j = jg + 4 * u;
+        if (j <= ti) {
+          D[ti * SBLD + j] = dreg[u];
+          D[j * SBLD + ti] = dreg[u];
+        }
       }
-      double tau;
+      double tau, beta;
       if (k == 0) {
         // type 1: reflector from column s, rows a0 .. a0+L-1 (band offsets 1..L)
         if (tid < B2) xcol[tid] = (tid < L) ? __ldcg(AB + (1 + tid) + s * ldab) : 0.0;
         __syncthreads();
-        tau = smem_larfg(xcol, L, vn, red);
-        if (tid < L) AB[(1 + tid) + s * ldab] = (tid == 0) ? xcol[0] : 0.0;
+        tau = larfg64(xcol, L, vn, red, beta);
+        if (tid < L) AB[(1 + tid) + s * ldab] = (tid == 0) ? beta : 0.0;
       } else {
         // type 2 on E = A[a0.., ap..] (element (i, j) at band offset 64 + i - j)
-        const int64_t ap = a0 - B2;
 #pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          const int idx = tid + 256 * u;
-          E[(idx & (B2 - 1)) * SBLD + (idx >> 6)] = ereg[u];
-        }
+        for (int u = 0; u < 16; ++u) E[ti * SBLD + jg + 4 * u] = ereg[u];
         __syncthreads();
-        const double tp = tau_prev_s;
         {  // w = E v (right application of the previous reflector)
           double s2 = 0.0;
           for (int j = q; j < B2; j += 4) s2 = fma(E[row * SBLD + j], v[j], s2);
@@ -493,14 +489,18 @@ __global__ void __launch_bounds__(256, 2) sb2st_kernel(SbArgs a) {
           if (q == 0) w[row] = s2;
         }
         __syncthreads();
-        for (int idx = tid; idx < B2 * B2; idx += 256) {
-          const int i = idx >> 6, j = idx & (B2 - 1);
-          E[i * SBLD + j] = fma(-tp * w[i], v[j], E[i * SBLD + j]);
+        {  // E -= tp w v^T in the owner's registers and the shared copy; its first column
+          const double twi = -tp * w[ti];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            const int j = jg + 4 * u;
+            ereg[u] = fma(twi, v[j], ereg[u]);
+            E[ti * SBLD + j] = ereg[u];
+          }
+          if (jg == 0) xcol[ti] = ereg[0];  // (rows from L on are zero)
         }
         __syncthreads();
-        if (tid < B2) xcol[tid] = (tid < L) ? E[tid * SBLD] : 0.0;
-        __syncthreads();
-        tau = smem_larfg(xcol, L, vn, red);
+        tau = larfg64(xcol, L, vn, red, beta);
         {  // u_j = sum_i vn_i E_ij, j >= 1 (left application of the new reflector)
           const int j = row;
           double s2 = 0.0;
@@ -511,37 +511,43 @@ __global__ void __launch_bounds__(256, 2) sb2st_kernel(SbArgs a) {
           if (q == 0) w[j] = s2;
         }
         __syncthreads();
-        for (int idx = tid; idx < B2 * B2; idx += 256) {
-          const int i = idx & (B2 - 1), j = idx >> 6;
-          if (i < L) {
-            const double val = (j == 0) ? ((i == 0) ? xcol[0] : 0.0)
-                                        : fma(-tau * vn[i], w[j], E[i * SBLD + j]);
-            AB[(B2 + i - j) + (ap + j) * ldab] = val;
+        if (ti < L) {
+          const double tvi = -tau * vn[ti];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            const int j = jg + 4 * u;
+            const double val = (j == 0) ? ((ti == 0) ? beta : 0.0) : fma(tvi, w[j], ereg[u]);
+            ebase[j * st1] = val;
           }
         }
       }
-      __syncthreads();
-      // type 3 (and 1): D <- H D H on the diagonal block [a0, a0+L)
+      // type 3 (and 1): D <- H D H on the diagonal block [a0, a0+L) (w2: the E stores above
+      // may still be reading w)
       {
         double s2 = 0.0;
         for (int j = q; j < B2; j += 4) s2 = fma(D[row * SBLD + j], vn[j], s2);
         s2 += __shfl_xor_sync(0xffffffffu, s2, 1);
         s2 += __shfl_xor_sync(0xffffffffu, s2, 2);
-        if (q == 0) w[row] = tau * s2;
+        if (q == 0) w2[row] = tau * s2;
       }
       __syncthreads();
-      if (tid < 32) {
-        double t2 = fma(w[tid], vn[tid], w[tid + 32] * vn[tid + 32]);
+      {
+        // alpha = -tau/2 (w2 . vn), by every warp; w' = w2 + alpha vn formed where needed
+        const int lane = tid & 31;
+        double t2 = fma(w2[lane], vn[lane], w2[lane + 32] * vn[lane + 32]);
         t2 = warp_sum(t2);
-        if (tid == 0) alpha_s = -0.5 * tau * t2;
-      }
-      __syncthreads();
-      if (tid < B2) w[tid] = fma(alpha_s, vn[tid], w[tid]);
-      __syncthreads();
-      for (int idx = tid; idx < B2 * B2; idx += 256) {
-        const int i = idx & (B2 - 1), j = idx >> 6;
-        if (i < L && j <= i)
-          AB[(i - j) + (a0 + j) * ldab] = D[i * SBLD + j] - vn[i] * w[j] - w[i] * vn[j];
+        const double alpha = -0.5 * tau * t2;
+        if (ti < L) {
+          const double vi = vn[ti], wi = fma(alpha, vi, w2[ti]);
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            const int j = jg + 4 * u;
+            if (j <= ti) {
+              const double vj = vn[j], wj = fma(alpha, vj, w2[j]);
+              dbase[j * st1] = dreg[u] - vi * wj - wi * vj;
+            }
+          }
+        }
       }
       // record the reflector; it becomes the "previous" one for the next task
       const int64_t t = a.toff[s] + k;
@@ -549,10 +555,8 @@ __global__ void __launch_bounds__(256, 2) sb2st_kernel(SbArgs a) {
         a.V2[t * B2 + tid] = vn[tid];
         v[tid] = vn[tid];
       }
-      if (tid == 0) {
-        a.TAU2[t] = tau;
-        tau_prev_s = tau;
-      }
+      if (tid == 0) a.TAU2[t] = tau;
+      tp = tau;
       // bar.sync orders every thread's band stores before thread 0's gpu-scope release
       // (cumulativity), as in the TD1 solves
       __syncthreads();
