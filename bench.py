@@ -702,13 +702,22 @@ def run_ours(args, cfg, rank, world, local_rank):
         rl["peak_source"] = "DMMA issue peak measured on this pool (profiles/r01_fp64_peaks.jsonl)"
         if os.path.exists(q2prof):
             pq = json.load(open(q2prof))
-            # measured at n = 16,384 (one group of 101 blocks), not at this workload's n: the
-            # contract's `traffic` (per launch of THIS run) stays null
+            # measured at n = 16,384 (one group of 101 blocks), not at this workload's n
             rl["traffic_ncu"] = {"n": pq.get("n"), "dram_bytes_per_launch": pq.get("dram_bytes"),
                                  "algorithmic_bytes_per_launch": pq.get("algorithmic_bytes"),
                                  "dmma_pipe_active_pct": pq.get("dmma_pipe_active_pct"),
                                  "source": "profiles/r02/ncu_q2r.json (ncu --set full, one "
                                            "launch of tools/q2_probe.py 16384)"}
+        q2c3 = os.path.join(ROOT, "profiles", "r02", "ncu_q2r_c3.json")
+        if n == 50000 and os.path.exists(q2c3):
+            # one launch of THIS workload under ncu --set full (the middle sweep group):
+            # DRAM bytes of that launch beside its algorithmic bytes (its Z rows once in,
+            # once out); the stage's other 781 launches differ only in their row count
+            pc = json.load(open(q2c3))
+            rl["traffic"] = pc.get("dram_bytes")
+            rl["traffic_launch"] = {k: pc.get(k) for k in (
+                "launch_index", "group", "blocks", "duration_ms", "algorithmic_bytes",
+                "useful_flop", "useful_TFps", "dmma_pipe_active_pct", "source_report")}
     if "sytrd" in st_avg and "q2_apply" not in st_avg:
         # one-stage tridiagonalisation (below the two-stage threshold): its symv is the
         # HBM-bound kernel, timed live at the full order
