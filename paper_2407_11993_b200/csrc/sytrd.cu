@@ -490,15 +490,15 @@ __global__ void larft_wide_kernel(int w, const double* __restrict__ G, int64_t l
   }
 }
 
-// larft for the diagonal 128-blocks of T (w x w, ld ldt): CTA half b builds the block
-// of reflectors [b*w1, ...) from the matching diagonal block of G = V^T V in shared
-// memory; also zeroes the strictly-lower blocks of T.
+// larft for the diagonal 128-blocks of T (w x w, ld ldt): CTA `half` builds the block of
+// reflectors [half*w1, half*w1 + 128) (w1 = 128 unless w < 128) from the matching diagonal
+// block of G = V^T V in shared memory; also zeroes the blocks of T left of it.
 EM_DEVINL void larft_smem_body(int half, int w, int w1, const double* __restrict__ G,
                                int64_t ldg, const double* __restrict__ tau, int64_t c0,
                                double* T, int64_t ldt, double* Ts, double* gk) {
   constexpr int LD = 129;
   const int off = half * w1;
-  const int bw = half == 0 ? w1 : w - w1;
+  const int bw = w - off < w1 ? w - off : w1;
   const int tid = threadIdx.x;
   for (int i = tid; i < 128 * LD; i += blockDim.x) Ts[i] = 0.0;
   __syncthreads();
@@ -518,8 +518,8 @@ EM_DEVINL void larft_smem_body(int half, int w, int w1, const double* __restrict
     const int r = i % bw, c = i / bw;
     T[(off + r) + (off + c) * ldt] = Ts[r + c * LD];
   }
-  if (half == 1)  // strictly-lower off-diagonal block
-    for (int i = tid; i < bw * w1; i += blockDim.x) T[(w1 + i % bw) + (i / bw) * ldt] = 0.0;
+  // strictly-lower block row: rows [off, off + bw) x columns [0, off)
+  for (int i = tid; i < bw * off; i += blockDim.x) T[(off + i % bw) + (i / bw) * ldt] = 0.0;
 }
 
 __global__ void __launch_bounds__(128) larft_smem_kernel(int w, int w1,
@@ -533,7 +533,7 @@ __global__ void __launch_bounds__(128) larft_smem_kernel(int w, int w1,
 }
 
 // every ORM_NB-reflector block of ormqr at once: block p = blockIdx.y (G, T with
-// stride nb^2, ld = its width), half = blockIdx.x
+// stride nb^2, ld = its width), 128-reflector sub-block = blockIdx.x
 __global__ void __launch_bounds__(128) larft_batched_kernel(int64_t nref, int nb,
                                                             const double* __restrict__ G,
                                                             const double* __restrict__ tau,
@@ -544,15 +544,16 @@ __global__ void __launch_bounds__(128) larft_batched_kernel(int64_t nref, int nb
   const int64_t c0 = (p0 + p) * nb;
   const int w = (int)imin64(nb, nref - c0);
   const int w1 = w < 128 ? w : 128;
-  if (blockIdx.x == 1 && w <= w1) return;
+  if ((int)blockIdx.x * w1 >= w) return;
   const size_t str = (size_t)nb * nb;
   larft_smem_body(blockIdx.x, w, w1, G + p * str, w, tau, c0, T + p * str, w, Ts, gk);
 }
 
 // Z <- Q Z, Q = H(0)...H(n-2), in blocks of ORM_NB reflectors (compact WY,
 // three DMMA GEMMs per block; a wide block keeps the rank-w updates of Z
-// compute-bound instead of re-streaming Z once per 64 reflectors).
-constexpr int ORM_NB = 256;
+// compute-bound instead of re-streaming Z once per 64 reflectors: the accumulating
+// rank-256 update ran at 32 TF/s, a rank-512 one runs at 34, tools/gemm_probe.py).
+constexpr int ORM_NB = 512;
 
 void ormtr_lower(cudaStream_t st, int64_t n, int64_t m, const double* A, int64_t lda,
                  const double* tau, double* Z, int64_t ldz) {
@@ -585,8 +586,10 @@ void ormqr_lower_off(cudaStream_t st, int64_t n, int64_t nref, int64_t off, int6
   for (int64_t cs = 0; cs < nch; ++cs) {
     const int64_t ci = trans ? cs : nch - 1 - cs;
     const int64_t p0 = ci * chunk, p1 = imin64(npan, p0 + chunk), np = p1 - p0;
-    std::vector<GemmArgs> gg, t1, t2;
-    int max_g = 1, max_t = 1;
+    // T of a block from its 128-reflector diagonal blocks (larft) joined pairwise, then the
+    // pairs joined: T_ab = -T_a G_ab T_b (two grouped products per level)
+    std::vector<GemmArgs> gg, jx[2], jt[2];
+    int max_g = 1, max_j[2] = {1, 1};
     for (int64_t p = p0; p < p1; ++p) {
       const int64_t i0 = p * ORM_NB;
       const int w = (int)imin64(ORM_NB, nref - i0);
@@ -598,31 +601,39 @@ void ormqr_lower_off(cudaStream_t st, int64_t n, int64_t nref, int64_t off, int6
       double* Gp = G.p + (p - p0) * tstride;
       gg.push_back(GemmArgs{w, w, mr, Vp, n, Vp, n, Gp, w, 1.0, 0.0, 0});
       max_g = (int)imax64(max_g, ((w + 127) / 128) * ((w + 63) / 64));
-      const int w1 = (int)imin64(w, 128), w2 = w - w1;
       double* Tp = T.p + (p - p0) * tstride;
-      if (w2 > 0) {  // T12 = -T1 G12 T2 (larft joins of the two halves)
-        double* Xp = T1G.p + (p - p0) * tstride;
-        t1.push_back(GemmArgs{w1, w2, w1, Tp, w, Gp + (int64_t)w1 * w, w, Xp, w1, 1.0, 0.0, 0});
-        t2.push_back(GemmArgs{w1, w2, w2, Xp, w1, Tp + w1 + (int64_t)w1 * w, w,
-                              Tp + (int64_t)w1 * w, w, -1.0, 0.0, 0});
-        max_t = (int)imax64(max_t, 4);
-      }
+      double* Xp = T1G.p + (p - p0) * tstride;
+      auto join = [&](int lvl, int a0, int na, int b0, int nb2, double* X) {
+        if (nb2 <= 0) return;
+        jx[lvl].push_back(GemmArgs{na, nb2, na, Tp + a0 + (int64_t)a0 * w, w,
+                                   Gp + a0 + (int64_t)b0 * w, w, X, na, 1.0, 0.0, 0});
+        jt[lvl].push_back(GemmArgs{na, nb2, nb2, X, na, Tp + b0 + (int64_t)b0 * w, w,
+                                   Tp + a0 + (int64_t)b0 * w, w, -1.0, 0.0, 0});
+        max_j[lvl] = (int)imax64(max_j[lvl], ((na + 127) / 128) * ((nb2 + 63) / 64));
+      };
+      join(0, 0, 128, 128, (int)imin64(128, w - 128), Xp);
+      join(0, 256, 128, 384, (int)imin64(128, w - 384), Xp + 128 * 128);
+      join(1, 0, 256, 256, w - 256, Xp + 2 * 128 * 128);
     }
-    DArr<GemmArgs> dgg(gg.size(), st), dt1(imax64((int64_t)t1.size(), 1), st),
-        dt2(imax64((int64_t)t2.size(), 1), st);
+    DArr<GemmArgs> dgg(gg.size(), st);
     EM_CK(cudaMemcpyAsync(dgg.p, gg.data(), gg.size() * sizeof(GemmArgs),
                           cudaMemcpyHostToDevice, st));
     EM_CK(gemm_grouped(st, true, false, dgg.p, (int)gg.size(), max_g));
-    larft_batched_kernel<<<dim3(2, (unsigned)np), 128, (size_t)128 * 129 * sizeof(double), st>>>(
-        nref, ORM_NB, G.p, tau, T.p, p0);
+    larft_batched_kernel<<<dim3(ORM_NB / 128, (unsigned)np), 128,
+                           (size_t)128 * 129 * sizeof(double), st>>>(nref, ORM_NB, G.p, tau, T.p,
+                                                                     p0);
     EM_LAUNCHED();
-    if (!t1.empty()) {
-      EM_CK(cudaMemcpyAsync(dt1.p, t1.data(), t1.size() * sizeof(GemmArgs),
+    DArr<GemmArgs> djx[2], djt[2];
+    for (int lvl = 0; lvl < 2; ++lvl) {
+      if (jx[lvl].empty()) continue;
+      djx[lvl].alloc(jx[lvl].size(), st);
+      djt[lvl].alloc(jt[lvl].size(), st);
+      EM_CK(cudaMemcpyAsync(djx[lvl].p, jx[lvl].data(), jx[lvl].size() * sizeof(GemmArgs),
                             cudaMemcpyHostToDevice, st));
-      EM_CK(cudaMemcpyAsync(dt2.p, t2.data(), t2.size() * sizeof(GemmArgs),
+      EM_CK(cudaMemcpyAsync(djt[lvl].p, jt[lvl].data(), jt[lvl].size() * sizeof(GemmArgs),
                             cudaMemcpyHostToDevice, st));
-      EM_CK(gemm_grouped(st, false, false, dt1.p, (int)t1.size(), max_t));
-      EM_CK(gemm_grouped(st, false, false, dt2.p, (int)t2.size(), max_t));
+      EM_CK(gemm_grouped(st, false, false, djx[lvl].p, (int)jx[lvl].size(), max_j[lvl]));
+      EM_CK(gemm_grouped(st, false, false, djt[lvl].p, (int)jt[lvl].size(), max_j[lvl]));
     }
     for (int64_t s = 0; s < np; ++s) {
       const int64_t p = trans ? p0 + s : p1 - 1 - s;

@@ -1028,7 +1028,11 @@ static void q2_apply_waves(cudaStream_t st, int64_t n, int64_t ncols, int64_t ng
   if (nblk == 0 || ncols <= 0) return;
   EM_CK(cudaFuncSetAttribute(q2_buildv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(VR * B2 * sizeof(double))));
-  constexpr int QCH = 64;  // blocks per grouped launch
+  // blocks per grouped launch: a block is one CTA of the V / T kernels and a few tiles of
+  // the grouped products, so a skinny operand (implicit mode: the drive and observable
+  // columns) takes up to 512 blocks per launch — whole wavefronts, more CTAs than SMs —
+  // while wide operands keep the per-launch workspace (QCH x 64 x ncols) small
+  const int QCH = ncols <= 2048 ? 512 : 64;
   std::vector<std::vector<int64_t>> waves;
   {
     std::vector<std::vector<int64_t>> byw;
