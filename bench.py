@@ -700,6 +700,8 @@ def run_ours(args, cfg, rank, world, local_rank):
         rl["kernel"] = ("q2r_kernel (+ q2r_pack_kernel, q2_tfactor_kernel): register-resident "
                         "stage-2 back-transform, one launch per 64-sweep group")
         rl["peak_source"] = "DMMA issue peak measured on this pool (profiles/r01_fp64_peaks.jsonl)"
+        # the stage is one q2r_kernel launch per 64-sweep group (the stage timer counts 1)
+        rl["launches_per_step"] = float((n - 1 + 63) // 64)
         if os.path.exists(q2prof):
             pq = json.load(open(q2prof))
             # measured at n = 16,384 (one group of 101 blocks), not at this workload's n

@@ -84,7 +84,7 @@ int em_synchronize(em_ctx* ctx);
 /* Tuning knobs. EM_CFG_TWO_STAGE_MIN: smallest n that uses the two-stage
  * (dense -> band -> tridiagonal) reduction in em_syev/em_sygv when its extra storage
  * (2.5 n^2 doubles beyond the matrix and the eigenvectors at its divide-and-conquer peak,
- * 3.5 when ldz != n) is free on the device (default 20000; below it one-stage
+ * 3.5 when ldz != n) is free on the device (default 16000; below it one-stage
  * Householder). em_info(EM_INFO_EIG_PATH) reports which path ran. */
 #define EM_CFG_TWO_STAGE_MIN 1
 /* EM_CFG_BAND_OFF: 1 = always factor R densely (default 0: a banded R, lower bandwidth

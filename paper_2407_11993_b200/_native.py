@@ -186,7 +186,7 @@ EM_TD1_L_WORKSPACE = 1
 EM_CFG_TWO_STAGE_MIN = 1
 
 
-TWO_STAGE_MIN_DEFAULT = 20000  # the library's default (csrc/sygv.cu g_two_stage_min)
+TWO_STAGE_MIN_DEFAULT = 16000  # the library's default (csrc/sygv.cu g_two_stage_min)
 
 
 def set_two_stage_min(n: int) -> None:

@@ -17,13 +17,13 @@
 namespace em {
 
 // em_config(EM_CFG_TWO_STAGE_MIN): smallest order that takes the two-stage reduction.
-// Measured on one B200 (em_syev, eigenvectors formed, profiles/r02/crossover.json): the two
-// paths tie at n = 16,384 (1.76 s two-stage, 1.82 s one-stage; the C2 pass 1.82 / 1.83 s),
-// two-stage wins from there on: n = 24,576 4.53 s against 5.53 s, n = 32,768 9.34 s against
-// 12.5 s, the C3 step 29.4 s against 50.7 s. (Before the band reduction's panel QR took one
-// grid barrier per column and the bulge chase a lag of two tasks, the crossover lay near
-// n = 22,000 and the default was 40,000.) Tests force either path.
-int64_t g_two_stage_min = 20000;
+// Measured on one B200 (em_syev, eigenvectors formed, profiles/r02/crossover.json): at
+// n = 16,384 the two-stage path is ahead by ~8% (the C2 pass 1.69 s against 1.83 s
+// one-stage), n = 24,576 4.53 s against 5.53 s, n = 32,768 9.34 s against 12.5 s, the C3
+// step 29.0 s against 50.7 s. (Before the band reduction's panel QR took one grid barrier
+// per column and the bulge chase was reworked, the crossover lay near n = 22,000 and the
+// default was 40,000.) Tests force either path.
+int64_t g_two_stage_min = 16000;
 // Extra device memory of the two-stage path beyond A and Z, phase by phase (n^2 doubles):
 // the stage-2 reflectors V2 (1/2) live from sb2st to the end; divide and conquer adds its
 // gathered Q and U (2, +1 when ldz != n); the Q2 apply the blocks' T factors (1/2); the Q1
